@@ -1,0 +1,129 @@
+/*
+ * zkl_b200 — C ABI of the B200-native zkLoRA sumcheck / logUp prover backend.
+ *
+ * Plain pointers and sizes only.  Device buffers are caller-owned (the Python
+ * host allocates them with torch); `stream` is a cudaStream_t (NULL = legacy
+ * default stream).  Field elements live on the device in the backend's
+ * storage form: 32-byte Montgomery (field 0, BLS12-381 Fr) or 8-byte
+ * canonical (field 1, 2^61-1), little-endian.  Every field SCALAR crossing
+ * the ABI on the host side is canonical little-endian (32 or 8 bytes), like
+ * the reference's field.to_bytes (pkg/src/zklora/field.py:58-60).
+ *
+ * Status: 0 ok; <0 error (zkl_last_error() describes it).  Error codes that
+ * map to reference exceptions:
+ *   ZKL_ERR_ZERO    -> zklora.field.InversionOfZero   (field.py:27-28, 38-39)
+ *   ZKL_ERR_MISSING -> zklora.lookup.ElementNotInTable (lookup.py:94-98)
+ * with the FIRST offending index written to the int64 out-parameter.
+ *
+ * Each entry point names the reference interface it replaces.
+ */
+#ifndef ZKL_B200_H
+#define ZKL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ZKL_FIELD_BLS12_381_FR 0 /* field.py:9  MODULUS      */
+#define ZKL_FIELD_M61 1          /* field.py:12 TEST_MODULUS */
+
+#define ZKL_OK 0
+#define ZKL_ERR_CUDA -1
+#define ZKL_ERR_ARG -2
+#define ZKL_ERR_ZERO -3
+#define ZKL_ERR_MISSING -4
+#define ZKL_ERR_UNSUPPORTED -5
+
+/* matrix / integer element types */
+#define ZKL_MT_FIELD 0
+#define ZKL_MT_I16 1
+#define ZKL_MT_I32 2
+#define ZKL_MT_I64 3
+
+int zkl_abi_version(void);
+const char* zkl_last_error(void);
+/* bytes per stored element (32 or 8); <0 for an unknown field */
+int zkl_elem_bytes(int field);
+
+/* canonical residues -> storage form and back (in place allowed).
+ * Replaces the implicit int residues of field.py / quantize.py:176-183. */
+int zkl_to_mont(int field, void* dst, const void* src, uint64_t n, void* stream);
+int zkl_from_mont(int field, void* dst, const void* src, uint64_t n, void* stream);
+
+/* signed int16/32/64 -> field (negatives as p-|x|): field.py:54-55
+ * (from_signed) as used by QuantizedTensor.from_field, quantize.py:176-183. */
+int zkl_lift(int field, int int_type, void* dst, const void* src, uint64_t n, void* stream);
+
+/* eq(point, .) over {0,1}^m, point[0] = MSB: mle.py:67-82 (eq_table).
+ * point_canon: m canonical scalars (host). */
+int zkl_eq_table(int field, void* dst, const uint8_t* point_canon, int m, void* stream);
+
+/* fold_table: dst[i] = (1-r) src[i] + r src[i+half], mle.py:50-56. */
+int zkl_fold(int field, void* dst, const void* src, uint64_t half, const uint8_t* r_canon,
+             void* stream);
+
+/* y = a + k*b (device vectors, k host canonical). */
+int zkl_axpy(int field, void* y, const void* a, const uint8_t* k_canon, const void* b, uint64_t n,
+             void* stream);
+
+/* Lifted logUp columns (lookup.py:188-202):
+ *   mode 0 (pad):  dst[i] = i < src_n ? (src ? src[i] : 0) + add : pad
+ *   mode 1 (tile): dst[i] = (src ? src[i % src_n] : 0) + add
+ * add/pad canonical host scalars (NULL = 0). */
+int zkl_expand(int field, void* dst, uint64_t dst_n, const void* src, uint64_t src_n, int mode,
+               const uint8_t* add_canon, const uint8_t* pad_canon, void* stream);
+
+/* uint32 counts (zkl_multiplicities output) -> field vector. */
+int zkl_lift_u32(int field, void* dst, const uint32_t* src, uint64_t n, void* stream);
+
+/* canonical host copy of n device elements (synchronises). */
+int zkl_read(int field, uint8_t* host_out, const void* src, uint64_t n, void* stream);
+
+/* out_host = sum_i a[i]*b[i] (b NULL: sum_i a[i]) as a canonical scalar. */
+int zkl_dot(int field, uint8_t* out_host, const void* a, const void* b, uint64_t n, void* stream);
+
+/* One round of prove_sumcheck (sumcheck.py:110-129):
+ *   tables: k device pointers (host array), each holding `size` elements.
+ *   fold != 0: first fold every table in place by r_prev (the previous
+ *   round's challenge, sumcheck.py:129), then evaluate over the folded
+ *   tables (size/2 entries); fold == 0: evaluate over `size` entries.
+ *   evals_out_host[x] = post_mul * (post_add + sum_i combine(terms, t_x(i)))
+ *   for x = 0..degree (combine: sumcheck.py:70-78; the claim's own rounds use
+ *   post_add = 0, post_mul = 1).  Terms: nterms <= 8, nfactors[t] <= 3,
+ *   factors[3*t + s] table indices, coeffs canonical (nterms scalars).
+ *   Synchronises the stream (the transcript needs the evaluations). */
+int zkl_sumcheck_round(int field, void* const* tables, int k, uint64_t size, int fold,
+                       const uint8_t* r_prev_canon, int degree, int nterms,
+                       const int32_t* nfactors, const int32_t* factors,
+                       const uint8_t* coeffs_canon, const uint8_t* post_add_canon,
+                       const uint8_t* post_mul_canon, uint8_t* evals_out_host, void* stream);
+
+/* After the last round: final_values[j] = fold(tables[j], r_last)[0]
+ * (sumcheck.py:129-130), tables of size 2. */
+int zkl_sumcheck_finish(int field, void* const* tables, int k, const uint8_t* r_last_canon,
+                        uint8_t* finals_out_host, void* stream);
+
+/* batch_inverse (field.py:34-46): dst[i] = 1/(src[i] + add) (add_canon may
+ * be NULL).  ZKL_ERR_ZERO with *first_zero = first index whose input is 0;
+ * lookup.py:163-171 uses the same check as its pole test. */
+int zkl_batch_inverse(int field, void* dst, const void* src, uint64_t n, const uint8_t* add_canon,
+                      int64_t* first_zero, void* stream);
+
+/* compute_multiplicities (lookup.py:91-99): counts[j] (uint32, device) =
+ * #{i : secret[i] == table[last j with that value]}; ZKL_ERR_MISSING with
+ * *first_miss = first secret index not in the table. */
+int zkl_multiplicities(int field, const void* secret, uint64_t d, const void* table, uint64_t n,
+                       uint32_t* counts, int64_t* first_miss, void* stream);
+
+/* y = M x (transpose 0) or M^T x (transpose 1); M row-major rows x cols of
+ * type mtype (ZKL_MT_*), x/y device field vectors.  The MLE partial
+ * evaluations behind the factored zkMat prover (gadgets.py:210-251). */
+int zkl_matvec(int field, int mtype, const void* M, uint64_t rows, uint64_t cols, int transpose,
+               const void* x, void* y, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZKL_B200_H */

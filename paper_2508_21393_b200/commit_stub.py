@@ -1,0 +1,64 @@
+"""Deterministic commitment stub for commitment-free benchmarking and tests.
+
+Commitments and openings are outside this backend's target (BASELINE.json:
+"Polynomial commitment opening (Pedersen/Hyrax MSM) stays on the reference
+path and is timed separately"), but their serialized bytes feed the
+transcript.  With a real zklora CommitmentKey the prover delegates to
+zklora.commit; with a StubKey it uses this stub, whose wire behaviour is
+shared with oracle/stubcommit.py and tests/golden/make_golden.py:
+
+  Commitment.serialize(group) = b"zkl-stub/v1" + u8(num_vars)
+  open_batch appends each point coordinate (b"open/point") and each opened
+  value (b"open/value") -- commit.py:192-195 -- and nothing else; the opened
+  values are the true MLE evaluations (computed on the GPU).
+"""
+
+from dataclasses import dataclass
+
+STUB_TAG = b"zkl-stub/v1"
+
+
+@dataclass(frozen=True)
+class StubCommitment:
+    num_vars: int
+
+    def serialize(self, group):
+        return STUB_TAG + bytes([self.num_vars])
+
+
+class StubKey:
+    """Stands in for zklora.commit.CommitmentKey (only .group is read)."""
+
+    is_stub = True
+    group = None
+
+
+def split_shape(num_vars):
+    """commit.py:26-29."""
+    row_vars = (num_vars + 1) // 2
+    return 1 << row_vars, 1 << (num_vars - row_vars)
+
+
+def commit(key, table, blinding=None):
+    return StubCommitment((len(table) - 1).bit_length())
+
+
+def commit_size(num_vars):
+    return StubCommitment(num_vars)
+
+
+def combine_commitments(group, commitments, coefficients):
+    return StubCommitment(commitments[0].num_vars)
+
+
+def open_batch(key, tables, blindings, point, tr, rng, values=None):
+    """Stub opening; ``values`` may carry already-known evaluations."""
+    if values is None:
+        from .mle import mle_evaluate_any
+
+        values = [mle_evaluate_any(t, point, tr.modulus) for t in tables]
+    for r in point:
+        tr.append(b"open/point", r)
+    for y in values:
+        tr.append(b"open/value", y)
+    return list(values), None

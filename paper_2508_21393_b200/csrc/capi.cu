@@ -1,0 +1,171 @@
+// extern "C" entry points (declared in include/zkl_b200.h): argument
+// checking, canonical <-> Montgomery scalar conversion on the host, dispatch
+// on the field id.
+#include "../../include/zkl_b200.h"
+#include "ops.cuh"
+
+using namespace zkl;
+
+namespace {
+
+template <class F>
+typename F::T scalar(const uint8_t* canon) {
+  if (!canon) return F::zero();
+  return load_canon<F>(canon);
+}
+
+template <class F>
+Terms<F> make_terms(int degree, int nterms, const int32_t* nfactors, const int32_t* factors,
+                    const uint8_t* coeffs, int k, int* err) {
+  Terms<F> tm;
+  *err = 0;
+  tm.degree = degree;
+  tm.nterms = nterms;
+  for (int t = 0; t < kMaxTerms; t++) {
+    tm.nf[t] = 0;
+    tm.fi[t][0] = tm.fi[t][1] = tm.fi[t][2] = 0;
+    tm.coef[t] = F::zero();
+  }
+  for (int t = 0; t < nterms; t++) {
+    if (nfactors[t] < 0 || nfactors[t] > 3 || nfactors[t] > degree) *err = 1;
+    tm.nf[t] = nfactors[t];
+    for (int s = 0; s < nfactors[t] && s < 3; s++) {
+      int f = factors[3 * t + s];
+      if (f < 0 || f >= k) *err = 1;
+      tm.fi[t][s] = f;
+    }
+    tm.coef[t] = load_canon<F>(coeffs + (size_t)t * F::kBytes);
+  }
+  return tm;
+}
+
+template <class F>
+int sumcheck_round(void* const* tables, int k, uint64_t size, int fold, const uint8_t* r_prev,
+                   int degree, int nterms, const int32_t* nfactors, const int32_t* factors,
+                   const uint8_t* coeffs, const uint8_t* post_add, const uint8_t* post_mul,
+                   uint8_t* evals_out, cudaStream_t s) {
+  if (nterms < 0 || nterms > kMaxTerms) {
+    set_error("sumcheck_round: %d terms (max %d)", nterms, kMaxTerms);
+    return kErrArg;
+  }
+  int err;
+  Terms<F> tm = make_terms<F>(degree, nterms, nfactors, factors, coeffs, k, &err);
+  if (err) { set_error("sumcheck_round: bad term factors"); return kErrArg; }
+  Post<F> post;
+  post.add = scalar<F>(post_add);
+  post.mul = post_mul ? scalar<F>(post_mul) : F::one();
+  typename F::T r = fold ? scalar<F>(r_prev) : F::zero();
+  return op_sumcheck_round<F>(tables, k, size, fold != 0, r, tm, post, evals_out, s);
+}
+
+template <class F>
+int dot_impl(uint8_t* out, const void* a, const void* b, uint64_t n, cudaStream_t s) {
+  void* ws;
+  int rc = scratch_reserve(sizeof(typename F::T) * 2, &ws, s);
+  if (rc) return rc;
+  rc = op_dot<F>((typename F::T*)ws, a, b, n, s);
+  if (rc) return rc;
+  return op_read<F>(out, ws, 1, s);
+}
+
+}  // namespace
+
+#define DISPATCH(field, EXPR_FR, EXPR_M61)                                      \
+  do {                                                                          \
+    if ((field) == ZKL_FIELD_BLS12_381_FR) { using F = Fr255; return EXPR_FR; }  \
+    if ((field) == ZKL_FIELD_M61) { using F = M61; return EXPR_M61; }          \
+    set_error("unknown field id %d", (int)(field));                             \
+    return kErrArg;                                                             \
+  } while (0)
+#define D(field, EXPR) DISPATCH(field, EXPR, EXPR)
+
+extern "C" {
+
+int zkl_abi_version(void) { return 1; }
+const char* zkl_last_error(void) { return get_error(); }
+int zkl_elem_bytes(int field) {
+  if (field == ZKL_FIELD_BLS12_381_FR) return 32;
+  if (field == ZKL_FIELD_M61) return 8;
+  return kErrArg;
+}
+
+int zkl_to_mont(int field, void* dst, const void* src, uint64_t n, void* stream) {
+  D(field, op_to_mont<F>(dst, src, n, (cudaStream_t)stream));
+}
+int zkl_from_mont(int field, void* dst, const void* src, uint64_t n, void* stream) {
+  D(field, op_from_mont<F>(dst, src, n, (cudaStream_t)stream));
+}
+int zkl_lift(int field, int int_type, void* dst, const void* src, uint64_t n, void* stream) {
+  D(field, op_lift<F>(dst, src, int_type, n, (cudaStream_t)stream));
+}
+
+static int eq_table_impl_fr(void* dst, const uint8_t* pt, int m, cudaStream_t s) {
+  if (m < 0 || m > kMaxPoint) { set_error("eq_table: m=%d", m); return kErrArg; }
+  Fr255::T p[kMaxPoint];
+  for (int j = 0; j < m; j++) p[j] = load_canon<Fr255>(pt + 32 * j);
+  return op_eq_table<Fr255>(dst, p, m, s);
+}
+static int eq_table_impl_m61(void* dst, const uint8_t* pt, int m, cudaStream_t s) {
+  if (m < 0 || m > kMaxPoint) { set_error("eq_table: m=%d", m); return kErrArg; }
+  M61::T p[kMaxPoint];
+  for (int j = 0; j < m; j++) p[j] = load_canon<M61>(pt + 8 * j);
+  return op_eq_table<M61>(dst, p, m, s);
+}
+int zkl_eq_table(int field, void* dst, const uint8_t* point_canon, int m, void* stream) {
+  DISPATCH(field, eq_table_impl_fr(dst, point_canon, m, (cudaStream_t)stream),
+           eq_table_impl_m61(dst, point_canon, m, (cudaStream_t)stream));
+}
+
+int zkl_fold(int field, void* dst, const void* src, uint64_t half, const uint8_t* r_canon,
+             void* stream) {
+  D(field, op_fold<F>(dst, src, half, scalar<F>(r_canon), (cudaStream_t)stream));
+}
+int zkl_axpy(int field, void* y, const void* a, const uint8_t* k_canon, const void* b, uint64_t n,
+             void* stream) {
+  D(field, op_axpy<F>(y, a, scalar<F>(k_canon), b, n, (cudaStream_t)stream));
+}
+int zkl_expand(int field, void* dst, uint64_t dst_n, const void* src, uint64_t src_n, int mode,
+               const uint8_t* add_canon, const uint8_t* pad_canon, void* stream) {
+  D(field, op_expand<F>(dst, dst_n, src, src_n, mode, scalar<F>(add_canon), scalar<F>(pad_canon),
+                        (cudaStream_t)stream));
+}
+int zkl_lift_u32(int field, void* dst, const uint32_t* src, uint64_t n, void* stream) {
+  D(field, op_lift_u32<F>(dst, src, n, (cudaStream_t)stream));
+}
+int zkl_read(int field, uint8_t* host_out, const void* src, uint64_t n, void* stream) {
+  D(field, op_read<F>(host_out, src, n, (cudaStream_t)stream));
+}
+
+int zkl_dot(int field, uint8_t* out_host, const void* a, const void* b, uint64_t n, void* stream) {
+  D(field, dot_impl<F>(out_host, a, b, n, (cudaStream_t)stream));
+}
+
+int zkl_sumcheck_round(int field, void* const* tables, int k, uint64_t size, int fold,
+                       const uint8_t* r_prev_canon, int degree, int nterms,
+                       const int32_t* nfactors, const int32_t* factors,
+                       const uint8_t* coeffs_canon, const uint8_t* post_add_canon,
+                       const uint8_t* post_mul_canon, uint8_t* evals_out_host, void* stream) {
+  D(field, sumcheck_round<F>(tables, k, size, fold, r_prev_canon, degree, nterms, nfactors,
+                             factors, coeffs_canon, post_add_canon, post_mul_canon,
+                             evals_out_host, (cudaStream_t)stream));
+}
+int zkl_sumcheck_finish(int field, void* const* tables, int k, const uint8_t* r_last_canon,
+                        uint8_t* finals_out_host, void* stream) {
+  D(field, op_sumcheck_finish<F>(tables, k, scalar<F>(r_last_canon), finals_out_host,
+                                 (cudaStream_t)stream));
+}
+int zkl_batch_inverse(int field, void* dst, const void* src, uint64_t n, const uint8_t* add_canon,
+                      int64_t* first_zero, void* stream) {
+  D(field, op_batch_inverse<F>(dst, src, n, scalar<F>(add_canon), add_canon != nullptr,
+                               first_zero, (cudaStream_t)stream));
+}
+int zkl_multiplicities(int field, const void* secret, uint64_t d, const void* table, uint64_t n,
+                       uint32_t* counts, int64_t* first_miss, void* stream) {
+  D(field, op_multiplicities<F>(secret, d, table, n, counts, first_miss, (cudaStream_t)stream));
+}
+int zkl_matvec(int field, int mtype, const void* M, uint64_t rows, uint64_t cols, int transpose,
+               const void* x, void* y, void* stream) {
+  D(field, op_matvec<F>(mtype, M, rows, cols, transpose, x, y, (cudaStream_t)stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,133 @@
+// Shared device helpers: element load/store, warp/block field reductions,
+// per-device scratch arena, error plumbing for the C-ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "field.cuh"
+
+namespace zkl {
+
+constexpr int kSMs = 148;  // B200
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---- element IO -------------------------------------------------------------
+template <class F>
+ZKL_D typename F::T ld(const typename F::T* p) { return *p; }
+template <class F>
+ZKL_D void st(typename F::T* p, const typename F::T& v) { *p = v; }
+
+// streaming (read-once) loads: keep big sweeps from evicting reused data
+ZKL_D fr_t ld_stream(const fr_t* p) {
+  const uint4* q = reinterpret_cast<const uint4*>(p);
+  uint4 a = __ldcs(q), b = __ldcs(q + 1);
+  fr_t r;
+  r.v[0] = a.x; r.v[1] = a.y; r.v[2] = a.z; r.v[3] = a.w;
+  r.v[4] = b.x; r.v[5] = b.y; r.v[6] = b.z; r.v[7] = b.w;
+  return r;
+}
+ZKL_D uint64_t ld_stream(const uint64_t* p) { return __ldcs(p); }
+// L2-coherent loads (data written by other blocks of the same launch)
+ZKL_D fr_t ld_cg(const fr_t* p) {
+  const uint4* q = reinterpret_cast<const uint4*>(p);
+  uint4 a = __ldcg(q), b = __ldcg(q + 1);
+  fr_t r;
+  r.v[0] = a.x; r.v[1] = a.y; r.v[2] = a.z; r.v[3] = a.w;
+  r.v[4] = b.x; r.v[5] = b.y; r.v[6] = b.z; r.v[7] = b.w;
+  return r;
+}
+ZKL_D uint64_t ld_cg(const uint64_t* p) { return __ldcg(p); }
+
+// ---- shuffles -----------------------------------------------------------------
+ZKL_D fr_t shfl_down(const fr_t& x, int off) {
+  fr_t y;
+#pragma unroll
+  for (int i = 0; i < 8; i++) y.v[i] = __shfl_down_sync(kFull, x.v[i], off);
+  return y;
+}
+ZKL_D uint64_t shfl_down(uint64_t x, int off) { return __shfl_down_sync(kFull, x, off); }
+ZKL_D fr_t shfl_idx(const fr_t& x, int src) {
+  fr_t y;
+#pragma unroll
+  for (int i = 0; i < 8; i++) y.v[i] = __shfl_sync(kFull, x.v[i], src);
+  return y;
+}
+ZKL_D uint64_t shfl_idx(uint64_t x, int src) { return __shfl_sync(kFull, x, src); }
+
+template <class F>
+ZKL_D typename F::T warp_sum(typename F::T x) {
+#pragma unroll
+  for (int off = 16; off; off >>= 1) x = F::add(x, shfl_down(x, off));
+  return x;
+}
+
+// Block-wide sum of NV field values per thread; result valid in thread 0.
+// smem must hold (blockDim.x/32) * NV elements.
+template <class F, int NV>
+ZKL_D void block_sum(typename F::T (&v)[NV], typename F::T* smem) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NV; j++) v[j] = warp_sum<F>(v[j]);
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; j++) smem[warp * NV + j] = v[j];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; j++) v[j] = lane < nw ? smem[lane * NV + j] : F::zero();
+#pragma unroll
+    for (int j = 0; j < NV; j++) v[j] = warp_sum<F>(v[j]);
+  }
+  __syncthreads();
+}
+
+// ---- launch geometry ------------------------------------------------------------
+inline unsigned grid_for(uint64_t work, unsigned block, unsigned max_per_sm = 8) {
+  uint64_t g = (work + block - 1) / block;
+  uint64_t cap = (uint64_t)kSMs * max_per_sm;
+  if (g > cap) g = cap;
+  if (g == 0) g = 1;
+  return (unsigned)g;
+}
+
+// ---- host-side status ------------------------------------------------------------
+enum Status : int {
+  kOk = 0,
+  kErrCuda = -1,
+  kErrArg = -2,
+  kErrZero = -3,      // inversion of zero (first index reported)
+  kErrMissing = -4,   // element not in table (first index reported)
+  kErrUnsupported = -5,
+};
+
+void set_error(const char* fmt, ...);
+const char* get_error();
+
+#define ZKL_CUDA(call)                                                         \
+  do {                                                                         \
+    cudaError_t e_ = (call);                                                   \
+    if (e_ != cudaSuccess) {                                                   \
+      ::zkl::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,              \
+                       cudaGetErrorString(e_));                                \
+      return ::zkl::kErrCuda;                                                  \
+    }                                                                          \
+  } while (0)
+
+#define ZKL_LAUNCH_CHECK() ZKL_CUDA(cudaGetLastError())
+
+// Per-device scratch arena (single owner, stream-ordered reuse).  Grows by
+// reallocating; callers must not hold pointers across zkl_* calls.
+struct Scratch {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  void* pinned = nullptr;  // small pinned host staging buffer
+  size_t pinned_bytes = 0;
+};
+Scratch& scratch_for_current_device();
+int scratch_reserve(size_t bytes, void** out, cudaStream_t s);
+int pinned_reserve(size_t bytes, void** out);
+
+}  // namespace zkl

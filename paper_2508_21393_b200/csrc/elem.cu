@@ -1,0 +1,304 @@
+// Element-wise field kernels: Montgomery conversion, int -> field lift,
+// eq-table, fold, axpy, dot; plus the scratch arena and error plumbing.
+//
+// Reference: mle.py:50-82 (fold_table, eq_table), field.py:49-55 (signed
+// lift), quantize.py:176-183 (row-major zero-padded residues).
+#include <stdarg.h>
+#include <string.h>
+
+#include <map>
+#include <mutex>
+
+#include "ops.cuh"
+
+namespace zkl {
+
+// ---------------------------------------------------------------------------
+// error + scratch
+static thread_local char g_err[512];
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+const char* get_error() { return g_err; }
+
+static std::map<int, Scratch>& arenas() {
+  static std::map<int, Scratch> m;
+  return m;
+}
+Scratch& scratch_for_current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return arenas()[dev];
+}
+int scratch_reserve(size_t bytes, void** out, cudaStream_t s) {
+  Scratch& a = scratch_for_current_device();
+  if (bytes > a.bytes) {
+    if (a.ptr) {
+      ZKL_CUDA(cudaStreamSynchronize(s));
+      ZKL_CUDA(cudaFree(a.ptr));
+      a.ptr = nullptr;
+      a.bytes = 0;
+    }
+    size_t want = bytes < (1u << 20) ? (1u << 20) : bytes + bytes / 4;
+    ZKL_CUDA(cudaMalloc(&a.ptr, want));
+    a.bytes = want;
+  }
+  *out = a.ptr;
+  return kOk;
+}
+int pinned_reserve(size_t bytes, void** out) {
+  Scratch& a = scratch_for_current_device();
+  if (bytes > a.pinned_bytes) {
+    if (a.pinned) ZKL_CUDA(cudaFreeHost(a.pinned));
+    size_t want = bytes < 65536 ? 65536 : bytes;
+    ZKL_CUDA(cudaHostAlloc(&a.pinned, want, cudaHostAllocDefault));
+    a.pinned_bytes = want;
+  }
+  *out = a.pinned;
+  return kOk;
+}
+
+// ---------------------------------------------------------------------------
+template <class F>
+__global__ void k_to_mont(typename F::T* dst, const typename F::T* src, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    typename F::T v = src[i];
+    // canonical inputs are < p; reduce once defensively for Fr255 inputs < 2^256
+    dst[i] = F::to_mont(v);
+  }
+}
+template <class F>
+__global__ void k_from_mont(typename F::T* dst, const typename F::T* src, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = F::from_mont(src[i]);
+}
+template <class F, class I>
+__global__ void k_lift(typename F::T* dst, const I* src, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = F::from_i64((int64_t)src[i]);
+}
+
+template <class F>
+int op_to_mont(void* dst, const void* src, uint64_t n, cudaStream_t s) {
+  if (!n) return kOk;
+  k_to_mont<F><<<grid_for(n, 256), 256, 0, s>>>((typename F::T*)dst,
+                                                 (const typename F::T*)src, n);
+  ZKL_LAUNCH_CHECK();
+  return kOk;
+}
+template <class F>
+int op_from_mont(void* dst, const void* src, uint64_t n, cudaStream_t s) {
+  if (!n) return kOk;
+  k_from_mont<F><<<grid_for(n, 256), 256, 0, s>>>((typename F::T*)dst,
+                                                   (const typename F::T*)src, n);
+  ZKL_LAUNCH_CHECK();
+  return kOk;
+}
+template <class F>
+int op_lift(void* dst, const void* src, int mtype, uint64_t n, cudaStream_t s) {
+  if (!n) return kOk;
+  auto* d = (typename F::T*)dst;
+  unsigned g = grid_for(n, 256);
+  switch (mtype) {
+    case 1: k_lift<F, int16_t><<<g, 256, 0, s>>>(d, (const int16_t*)src, n); break;
+    case 2: k_lift<F, int32_t><<<g, 256, 0, s>>>(d, (const int32_t*)src, n); break;
+    case 3: k_lift<F, int64_t><<<g, 256, 0, s>>>(d, (const int64_t*)src, n); break;
+    default: set_error("lift: bad integer type %d", mtype); return kErrArg;
+  }
+  ZKL_LAUNCH_CHECK();
+  return kOk;
+}
+
+// ---------------------------------------------------------------------------
+// eq table: eq[idx] = prod_j (bit_{m-1-j}(idx) ? r_j : 1 - r_j)   (mle.py:67-82)
+// Two-level: eq = hi (x) lo with hi over the first mh coordinates.
+template <class F>
+struct PointArg {
+  typename F::T r[kMaxPoint];
+  typename F::T omr[kMaxPoint];  // 1 - r
+};
+template <class F>
+__global__ void k_eq_direct(typename F::T* dst, PointArg<F> pt, int off, int m) {
+  uint64_t n = 1ull << m;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    typename F::T acc = F::one();
+    for (int j = 0; j < m; j++) {
+      bool bit = (i >> (m - 1 - j)) & 1;
+      acc = F::mul(acc, bit ? pt.r[off + j] : pt.omr[off + j]);
+    }
+    dst[i] = acc;
+  }
+}
+template <class F>
+__global__ void k_eq_outer(typename F::T* dst, const typename F::T* hi, const typename F::T* lo,
+                           int ml, uint64_t n) {
+  uint64_t mask = (1ull << ml) - 1;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = F::mul(hi[i >> ml], lo[i & mask]);
+}
+
+template <class F>
+int op_eq_table(void* dst, const typename F::T* point, int m, cudaStream_t s) {
+  using T = typename F::T;
+  if (m < 0 || m > kMaxPoint) { set_error("eq_table: m=%d unsupported", m); return kErrArg; }
+  PointArg<F> pt;
+  for (int j = 0; j < m; j++) {
+    pt.r[j] = point[j];
+    pt.omr[j] = F::sub(F::one(), point[j]);
+  }
+  T* out = (T*)dst;
+  if (m <= 12) {
+    k_eq_direct<F><<<grid_for(1ull << m, 256), 256, 0, s>>>(out, pt, 0, m);
+    ZKL_LAUNCH_CHECK();
+    return kOk;
+  }
+  int mh = m / 2, ml = m - mh;
+  void* ws;
+  int rc = scratch_reserve(((1ull << mh) + (1ull << ml)) * sizeof(T), &ws, s);
+  if (rc) return rc;
+  T* hi = (T*)ws;
+  T* lo = hi + (1ull << mh);
+  k_eq_direct<F><<<grid_for(1ull << mh, 256), 256, 0, s>>>(hi, pt, 0, mh);
+  k_eq_direct<F><<<grid_for(1ull << ml, 256), 256, 0, s>>>(lo, pt, mh, ml);
+  k_eq_outer<F><<<grid_for(1ull << m, 256), 256, 0, s>>>(out, hi, lo, ml, 1ull << m);
+  ZKL_LAUNCH_CHECK();
+  return kOk;
+}
+
+// ---------------------------------------------------------------------------
+// fold: dst[i] = src[i] + r (src[i+half] - src[i])   (mle.py:50-56)
+template <class F>
+__global__ void k_fold(typename F::T* dst, const typename F::T* src, uint64_t half,
+                       typename F::T r) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < half;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    typename F::T a = src[i], b = src[i + half];
+    dst[i] = F::add(a, F::mul(r, F::sub(b, a)));
+  }
+}
+template <class F>
+int op_fold(void* dst, const void* src, uint64_t half, typename F::T r, cudaStream_t s) {
+  if (!half) return kOk;
+  k_fold<F><<<grid_for(half, 256), 256, 0, s>>>((typename F::T*)dst,
+                                                 (const typename F::T*)src, half, r);
+  ZKL_LAUNCH_CHECK();
+  return kOk;
+}
+
+template <class F>
+__global__ void k_axpy(typename F::T* y, const typename F::T* a, typename F::T k,
+                       const typename F::T* b, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    y[i] = F::add(a[i], F::mul(k, b[i]));
+}
+template <class F>
+int op_axpy(void* y, const void* a, typename F::T k, const void* b, uint64_t n, cudaStream_t s) {
+  if (!n) return kOk;
+  k_axpy<F><<<grid_for(n, 256), 256, 0, s>>>((typename F::T*)y, (const typename F::T*)a, k,
+                                              (const typename F::T*)b, n);
+  ZKL_LAUNCH_CHECK();
+  return kOk;
+}
+
+// single-block dot / sum (vectors here are <= a few 2^12 entries)
+template <class F>
+__global__ void k_dot(typename F::T* out, const typename F::T* a, const typename F::T* b,
+                      uint64_t n) {
+  using T = typename F::T;
+  __shared__ T sm[32];
+  T acc[1] = {F::zero()};
+  for (uint64_t i = threadIdx.x; i < n; i += blockDim.x)
+    acc[0] = F::add(acc[0], b ? F::mul(a[i], b[i]) : a[i]);
+  block_sum<F, 1>(acc, sm);
+  if (threadIdx.x == 0) *out = acc[0];
+}
+template <class F>
+int op_dot(typename F::T* out_dev, const void* a, const void* b, uint64_t n, cudaStream_t s) {
+  k_dot<F><<<1, 1024, 0, s>>>(out_dev, (const typename F::T*)a, (const typename F::T*)b, n);
+  ZKL_LAUNCH_CHECK();
+  return kOk;
+}
+
+// expand: mode 0 (pad):  dst[i] = i < src_n ? (src ? src[i] : 0) + add : pad
+//         mode 1 (tile): dst[i] = (src ? src[i % src_n] : 0) + add
+// (lookup.py:188-202: zero-padded secret side / replicated table side)
+template <class F>
+__global__ void k_expand(typename F::T* dst, uint64_t dst_n, const typename F::T* src,
+                         uint64_t src_n, int mode, typename F::T add, typename F::T pad) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < dst_n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    typename F::T v;
+    if (mode == 0) {
+      v = i < src_n ? (src ? F::add(src[i], add) : add) : pad;
+    } else {
+      v = src ? F::add(src[i % src_n], add) : add;
+    }
+    dst[i] = v;
+  }
+}
+template <class F>
+int op_expand(void* dst, uint64_t dst_n, const void* src, uint64_t src_n, int mode,
+              typename F::T add, typename F::T pad, cudaStream_t s) {
+  if (!dst_n) return kOk;
+  if (mode == 1 && src_n == 0) { set_error("expand: empty tile source"); return kErrArg; }
+  k_expand<F><<<grid_for(dst_n, 256), 256, 0, s>>>((typename F::T*)dst, dst_n,
+                                                    (const typename F::T*)src, src_n, mode,
+                                                    add, pad);
+  ZKL_LAUNCH_CHECK();
+  return kOk;
+}
+
+// u32 counts -> field
+template <class F>
+__global__ void k_lift_u32(typename F::T* dst, const uint32_t* src, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = F::from_u32(src[i]);
+}
+template <class F>
+int op_lift_u32(void* dst, const uint32_t* src, uint64_t n, cudaStream_t s) {
+  if (!n) return kOk;
+  k_lift_u32<F><<<grid_for(n, 256), 256, 0, s>>>((typename F::T*)dst, src, n);
+  ZKL_LAUNCH_CHECK();
+  return kOk;
+}
+
+template <class F>
+int op_read(uint8_t* host, const void* src, uint64_t n, cudaStream_t s) {
+  using T = typename F::T;
+  if (!n) return kOk;
+  void* ws;
+  int rc = scratch_reserve(n * sizeof(T), &ws, s);
+  if (rc) return rc;
+  rc = op_from_mont<F>(ws, src, n, s);
+  if (rc) return rc;
+  ZKL_CUDA(cudaMemcpyAsync(host, ws, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+  ZKL_CUDA(cudaStreamSynchronize(s));
+  return kOk;
+}
+
+#define ZKL_INST(F)                                                                       \
+  template int op_to_mont<F>(void*, const void*, uint64_t, cudaStream_t);                 \
+  template int op_from_mont<F>(void*, const void*, uint64_t, cudaStream_t);               \
+  template int op_lift<F>(void*, const void*, int, uint64_t, cudaStream_t);               \
+  template int op_eq_table<F>(void*, const F::T*, int, cudaStream_t);                     \
+  template int op_fold<F>(void*, const void*, uint64_t, F::T, cudaStream_t);              \
+  template int op_axpy<F>(void*, const void*, F::T, const void*, uint64_t, cudaStream_t); \
+  template int op_read<F>(uint8_t*, const void*, uint64_t, cudaStream_t);                 \
+  template int op_dot<F>(F::T*, const void*, const void*, uint64_t, cudaStream_t);          \
+  template int op_expand<F>(void*, uint64_t, const void*, uint64_t, int, F::T, F::T,        \
+                            cudaStream_t);                                                  \
+  template int op_lift_u32<F>(void*, const uint32_t*, uint64_t, cudaStream_t);
+ZKL_INST(Fr255)
+ZKL_INST(M61)
+
+}  // namespace zkl

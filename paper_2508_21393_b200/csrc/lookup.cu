@@ -1,0 +1,105 @@
+// logUp multiplicities: m_j = #{i : s_i == t_j}.
+//
+// Reference: lookup.py:91-99 (compute_multiplicities).  Semantics kept:
+//   * duplicate table values count toward their LAST index (the reference
+//     builds {value: j} in order, later j overwrite earlier ones);
+//   * a secret value absent from the table raises ElementNotInTable with
+//     the FIRST offending index.
+// Device design: open-addressing hash table over table indices (2x load),
+// built with atomicCAS / atomicMax (duplicates keep the largest index), then
+// one probe per secret entry with atomicAdd on the counts and atomicMin on
+// the first miss.
+#include "ops.cuh"
+
+namespace zkl {
+
+ZKL_D uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16; h *= 0x85ebca6bu;
+  h ^= h >> 13; h *= 0xc2b2ae35u;
+  h ^= h >> 16;
+  return h;
+}
+ZKL_D uint32_t hash_elem(const fr_t& v) {
+  uint32_t h = v.v[0] ^ (v.v[1] * 0x9e3779b1u) ^ (v.v[2] * 0x7feb352du) ^ (v.v[7] * 0x846ca68bu);
+  return fmix32(h);
+}
+ZKL_D uint32_t hash_elem(uint64_t v) { return fmix32((uint32_t)v ^ (uint32_t)(v >> 32) * 0x9e3779b1u); }
+
+constexpr uint32_t kEmpty = 0xffffffffu;
+
+template <class F>
+__global__ void k_ht_insert(const typename F::T* table, uint32_t n, uint32_t* slots,
+                            uint32_t mask) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    typename F::T v = table[j];
+    uint32_t h = hash_elem(v) & mask;
+    while (true) {
+      uint32_t old = atomicCAS(&slots[h], kEmpty, j);
+      if (old == kEmpty) break;
+      if (F::eq(table[old], v)) {  // duplicate value: keep the last index
+        atomicMax(&slots[h], j);
+        break;
+      }
+      h = (h + 1) & mask;
+    }
+  }
+}
+
+template <class F>
+__global__ void k_ht_count(const typename F::T* secret, uint64_t d, const typename F::T* table,
+                           const uint32_t* slots, uint32_t mask, uint32_t* counts,
+                           unsigned long long* first_miss) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < d;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    typename F::T v = secret[i];
+    uint32_t h = hash_elem(v) & mask;
+    while (true) {
+      uint32_t e = slots[h];
+      if (e == kEmpty) { atomicMin(first_miss, (unsigned long long)i); break; }
+      if (F::eq(table[e], v)) { atomicAdd(&counts[e], 1u); break; }
+      h = (h + 1) & mask;
+    }
+  }
+}
+
+template <class F>
+int op_multiplicities(const void* secret, uint64_t d, const void* table, uint64_t n,
+                      uint32_t* counts, int64_t* first_miss, cudaStream_t s) {
+  using T = typename F::T;
+  *first_miss = -1;
+  if (n == 0 || n > (1ull << 31)) { set_error("multiplicities: bad table size"); return kErrArg; }
+  uint64_t cap = 1;
+  while (cap < 2 * n) cap <<= 1;
+  void* ws;
+  int rc = scratch_reserve(cap * 4 + 64, &ws, s);
+  if (rc) return rc;
+  uint32_t* slots = (uint32_t*)ws;
+  unsigned long long* flag = (unsigned long long*)((char*)ws + cap * 4);
+  ZKL_CUDA(cudaMemsetAsync(slots, 0xff, cap * 4, s));
+  ZKL_CUDA(cudaMemsetAsync(flag, 0xff, 8, s));
+  ZKL_CUDA(cudaMemsetAsync(counts, 0, n * 4, s));
+  k_ht_insert<F><<<grid_for(n, 256), 256, 0, s>>>((const T*)table, (uint32_t)n, slots,
+                                                   (uint32_t)(cap - 1));
+  ZKL_LAUNCH_CHECK();
+  if (d) {
+    k_ht_count<F><<<grid_for(d, 256), 256, 0, s>>>((const T*)secret, d, (const T*)table, slots,
+                                                    (uint32_t)(cap - 1), counts, flag);
+    ZKL_LAUNCH_CHECK();
+  }
+  unsigned long long fm;
+  void* pin;
+  rc = pinned_reserve(16, &pin);
+  if (rc) return rc;
+  ZKL_CUDA(cudaMemcpyAsync(pin, flag, 8, cudaMemcpyDeviceToHost, s));
+  ZKL_CUDA(cudaStreamSynchronize(s));
+  memcpy(&fm, pin, 8);
+  if (fm != ~0ull) { *first_miss = (int64_t)fm; return kErrMissing; }
+  return kOk;
+}
+
+template int op_multiplicities<Fr255>(const void*, uint64_t, const void*, uint64_t, uint32_t*,
+                                      int64_t*, cudaStream_t);
+template int op_multiplicities<M61>(const void*, uint64_t, const void*, uint64_t, uint32_t*,
+                                    int64_t*, cudaStream_t);
+
+}  // namespace zkl

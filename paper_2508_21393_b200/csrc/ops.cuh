@@ -1,0 +1,73 @@
+// Host-side launchers (templated on the field), dispatched by capi.cu.
+#pragma once
+#include "common.cuh"
+
+namespace zkl {
+
+constexpr int kMaxTables = 8;
+constexpr int kMaxTerms = 8;
+constexpr int kMaxPoint = 64;
+
+// element-wise ---------------------------------------------------------------
+template <class F> int op_to_mont(void* dst, const void* src, uint64_t n, cudaStream_t s);
+template <class F> int op_from_mont(void* dst, const void* src, uint64_t n, cudaStream_t s);
+// mtype: 1 = int16, 2 = int32, 3 = int64 (signed; negatives -> p - |x|)
+template <class F> int op_lift(void* dst, const void* src, int mtype, uint64_t n, cudaStream_t s);
+template <class F>
+int op_eq_table(void* dst, const typename F::T* point, int m, cudaStream_t s);
+template <class F>
+int op_fold(void* dst, const void* src, uint64_t half, typename F::T r, cudaStream_t s);
+// y = a + k * b
+template <class F>
+int op_axpy(void* y, const void* a, typename F::T k, const void* b, uint64_t n, cudaStream_t s);
+// canonical host copy of n device elements (synchronises)
+template <class F> int op_read(uint8_t* host, const void* src, uint64_t n, cudaStream_t s);
+// out = sum_i a[i]*b[i] (b == nullptr: sum_i a[i]); device scalar (Montgomery)
+template <class F>
+int op_dot(typename F::T* out_dev, const void* a, const void* b, uint64_t n, cudaStream_t s);
+
+template <class F>
+int op_expand(void* dst, uint64_t dst_n, const void* src, uint64_t src_n, int mode,
+              typename F::T add, typename F::T pad, cudaStream_t s);
+template <class F> int op_lift_u32(void* dst, const uint32_t* src, uint64_t n, cudaStream_t s);
+
+// sumcheck -----------------------------------------------------------------------
+template <class F>
+struct Terms {
+  int nterms;
+  int degree;
+  int nf[kMaxTerms];
+  int fi[kMaxTerms][3];
+  typename F::T coef[kMaxTerms];
+};
+template <class F>
+struct Post {
+  typename F::T add;  // evals[x] = mul * (sum_x + add)
+  typename F::T mul;
+};
+template <class F>
+int op_sumcheck_round(void* const* tables, int k, uint64_t size, bool fold,
+                      typename F::T r_prev, const Terms<F>& terms, const Post<F>& post,
+                      uint8_t* evals_host, cudaStream_t s);
+template <class F>
+int op_sumcheck_finish(void* const* tables, int k, typename F::T r, uint8_t* finals_host,
+                       cudaStream_t s);
+
+// batch inversion: dst[i] = 1 / (src[i] + add); returns kErrZero and sets
+// *first_zero to the first zero index when some src[i] + add == 0.
+template <class F>
+int op_batch_inverse(void* dst, const void* src, uint64_t n, typename F::T add, bool has_add,
+                     int64_t* first_zero, cudaStream_t s);
+
+// multiplicities ---------------------------------------------------------------
+template <class F>
+int op_multiplicities(const void* secret, uint64_t d, const void* table, uint64_t n,
+                      uint32_t* counts, int64_t* first_miss, cudaStream_t s);
+
+// matrix x field-vector ------------------------------------------------------------
+// mtype: 0 = field (Montgomery), 1 = int16, 2 = int32, 3 = int64
+template <class F>
+int op_matvec(int mtype, const void* M, uint64_t rows, uint64_t cols, int transpose,
+              const void* x, void* y, cudaStream_t s);
+
+}  // namespace zkl

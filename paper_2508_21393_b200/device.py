@@ -1,0 +1,138 @@
+"""Device-side field vectors (torch tensors as plain memory) and scalar codecs.
+
+A field vector of n elements is a torch.int64 CUDA tensor of shape (n, W),
+W = 4 (BLS12-381 Fr, 32-byte Montgomery limbs) or 1 (2^61-1, canonical).
+Torch is only the allocator / stream provider here; all arithmetic runs in
+libzkl_b200.so.
+"""
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+MODULUS = 0x73EDA753299D7D483339D80809A1D80553BDA402FFFE5BFEFFFFFFFF00000001
+TEST_MODULUS = (1 << 61) - 1
+
+
+class UnsupportedField(ValueError):
+    """The GPU backend implements the reference's two prover fields only."""
+
+
+class FieldSpec:
+    __slots__ = ("modulus", "fid", "nbytes", "words")
+
+    def __init__(self, modulus, fid, nbytes):
+        self.modulus = modulus
+        self.fid = fid
+        self.nbytes = nbytes
+        self.words = nbytes // 8
+
+
+FR = FieldSpec(MODULUS, 0, 32)
+M61 = FieldSpec(TEST_MODULUS, 1, 8)
+
+
+def spec_for(modulus):
+    """Field spec for a reference modulus; requires the CUDA backend."""
+    if modulus == MODULUS:
+        spec = FR
+    elif modulus == TEST_MODULUS:
+        spec = M61
+    else:
+        raise UnsupportedField("no GPU field for modulus %d" % modulus)
+    N.lib()  # raises BackendUnavailable: no CPU fallback
+    return spec
+
+
+def stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def empty(spec, n):
+    return torch.empty((max(n, 1), spec.words), dtype=torch.int64, device="cuda")
+
+
+def scalar_bytes(v, spec):
+    return (int(v) % spec.modulus).to_bytes(spec.nbytes, "little")
+
+
+def scalars_bytes(vals, spec):
+    p, nb = spec.modulus, spec.nbytes
+    return b"".join((int(v) % p).to_bytes(nb, "little") for v in vals)
+
+
+def encode(values, spec):
+    """Python ints -> canonical little-endian bytes (reduced mod p)."""
+    p = spec.modulus
+    if spec.words == 1:
+        arr = np.fromiter((int(v) % p for v in values), dtype=np.uint64, count=len(values))
+        return arr.tobytes()
+    return b"".join((int(v) % p).to_bytes(32, "little") for v in values)
+
+
+def upload(values, spec, out=None):
+    """Python ints -> device storage form (Montgomery for Fr)."""
+    n = len(values)
+    host = torch.frombuffer(bytearray(encode(values, spec)), dtype=torch.int64)
+    if out is None:
+        out = empty(spec, n)
+    if n:
+        out.view(-1)[: n * spec.words].copy_(host, non_blocking=False)
+        N.check(N.lib().zkl_to_mont(spec.fid, ptr(out), ptr(out), n, stream()))
+    return out
+
+
+def decode(raw, spec, n):
+    if spec.words == 1:
+        return [int(x) for x in np.frombuffer(raw, dtype=np.uint64, count=n)]
+    mv = memoryview(raw)
+    return [int.from_bytes(mv[32 * i: 32 * i + 32], "little") for i in range(n)]
+
+
+def download(buf, spec, n):
+    """Device storage -> canonical Python ints."""
+    if n == 0:
+        return []
+    raw = (ctypes.c_uint8 * (n * spec.nbytes))()
+    N.check(N.lib().zkl_read(spec.fid, raw, ptr(buf), n, stream()))
+    return decode(bytes(raw), spec, n)
+
+
+def read_scalar(buf, spec, index=0):
+    raw = (ctypes.c_uint8 * spec.nbytes)()
+    src = ctypes.c_void_p(buf.data_ptr() + index * spec.nbytes)
+    N.check(N.lib().zkl_read(spec.fid, raw, src, 1, stream()))
+    return int.from_bytes(bytes(raw), "little")
+
+
+def lift(int_tensor, spec, out=None):
+    """Signed int16/int32/int64 CUDA tensor -> field vector (negatives p-|x|)."""
+    t = int_tensor.contiguous()
+    mt = {torch.int16: N.MT_I16, torch.int32: N.MT_I32, torch.int64: N.MT_I64}[t.dtype]
+    n = t.numel()
+    if out is None:
+        out = empty(spec, n)
+    N.check(N.lib().zkl_lift(spec.fid, mt, ptr(out), ptr(t), n, stream()))
+    return out
+
+
+def eq_table(point, spec, out=None):
+    m = len(point)
+    if out is None:
+        out = empty(spec, 1 << m)
+    N.check(N.lib().zkl_eq_table(spec.fid, ptr(out), scalars_bytes(point, spec), m, stream()))
+    return out
+
+
+def dot(a, b, spec, n):
+    raw = (ctypes.c_uint8 * spec.nbytes)()
+    N.check(N.lib().zkl_dot(spec.fid, raw, ptr(a), ptr(b) if b is not None else None, n,
+                            stream()))
+    return int.from_bytes(bytes(raw), "little")

@@ -1,0 +1,311 @@
+"""zkMat and elementprod provers on the GPU (drop-ins for zklora.gadgets).
+
+prove_matmul (gadgets.py:230-265) emits the reference's (d0+d1+d2)-round
+replicated-table sumcheck (gadgets.py:210-251) bit for bit, but never builds
+its four 2^(d0+d1+d2) tables.  The claim
+    sum_{u,w,v} eq(r_u,u) eq(r_v,v) [A(u,w) B(w,v) - 2^-d1 C(u,v)] = 0
+is proven phase by phase over MLE partial evaluations (DESIGN.md,
+"Factored zkMat"):
+  U (d0 rounds): two-factor sumcheck of (E_u, h), h = A (B E_v) - (C E_v)
+  W (d1 rounds): E_hat [ sum a(w) bv(w) - 2^-d1 2^rem kappa ],
+                 a = E(rho_u)^T A, bv = B E_v, kappa = <E(rho_u)^T C, E_v>
+  V (d2 rounds): E_hat sum E_v(v) [alpha_s bw(v) - 2^-d1 cu(v)],
+                 bw = E(rho_w)^T B, cu = E(rho_u)^T C
+Every matrix is read twice (one row product, one column product) by the
+wide-accumulator matvec kernels; every phase runs on the dense round engine.
+Operands may be the reference's ProverTensor (field residues on the host)
+or DeviceMatrix (int16 / int32 / int64 / field matrices already on the GPU).
+"""
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _native as N
+from . import device as D
+from .field import inverse
+from .sumcheck import TYPES as SC_TYPES
+from .sumcheck import Term, absorb_claim, run_rounds
+
+
+class ShapeMismatch(ValueError):
+    pass
+
+
+@dataclass(frozen=True)
+class TensorRef:
+    """Mirror of gadgets.py:56-97 (verifier-side operand handle)."""
+
+    kind: str
+    row_vars: int
+    col_vars: int
+    commitment: object = None
+    value: int = 0
+
+    @property
+    def num_vars(self):
+        return self.row_vars + self.col_vars
+
+    def digest(self, group):
+        head = bytes([self.row_vars, self.col_vars])
+        if self.kind == "committed":
+            return b"com:" + head + self.commitment.serialize(group)
+        return self.kind.encode() + b":" + head + self.value.to_bytes(32, "little", signed=False)
+
+
+class DeviceMatrix:
+    """A padded row-major matrix resident on the GPU.
+
+    mtype: N.MT_I16 / MT_I32 / MT_I64 (signed integers, value = x mod p) or
+    N.MT_FIELD (storage-form field elements, W int64 words per entry).
+    """
+
+    def __init__(self, tensor, rows, cols, mtype, spec=None):
+        self.t = tensor
+        self.rows, self.cols, self.mtype, self.spec = rows, cols, mtype, spec
+        self._field = None
+
+    @classmethod
+    def from_int_tensor(cls, t):
+        t = t.contiguous()
+        mt = {torch.int16: N.MT_I16, torch.int32: N.MT_I32, torch.int64: N.MT_I64}[t.dtype]
+        r, c = t.shape
+        return cls(t, r, c, mt)
+
+    @classmethod
+    def from_field_list(cls, values, rows, cols, spec):
+        return cls(D.upload(list(values), spec), rows, cols, N.MT_FIELD, spec)
+
+    def as_field_vector(self, spec):
+        if self.mtype == N.MT_FIELD:
+            return self.t
+        if self._field is None:
+            self._field = D.lift(self.t.view(-1), spec)
+        return self._field
+
+
+@dataclass(frozen=True)
+class ProverTensor:
+    """Mirror of gadgets.py:100-113 with an optional device-resident copy."""
+
+    tensor: object
+    ref: TensorRef
+    blinding: tuple = ()
+    device: object = None  # DeviceMatrix
+
+    def flat(self):
+        return list(self.tensor.data)
+
+
+@dataclass
+class Opening:
+    values: tuple
+    proof: object
+
+
+@dataclass
+class MatmulProof:
+    tag = "matmul"
+    dims: tuple
+    sumcheck: object
+    a_opening: object
+    b_opening: object
+    c_opening: object
+
+
+@dataclass
+class ElementprodProof:
+    tag = "elementprod"
+    shape: tuple
+    c_opening: object
+    sumcheck: object
+    ab_opening: object
+
+
+TYPES = {"Opening": Opening, "MatmulProof": MatmulProof, "ElementprodProof": ElementprodProof}
+
+
+# ---------------------------------------------------------------------------
+def commit_backend(key):
+    """zklora.commit for real keys, the stub for StubKey (commit_stub.py)."""
+    if getattr(key, "is_stub", False):
+        from . import commit_stub
+
+        return commit_stub
+    import zklora.commit as zc  # the reference's own commitment path
+
+    return zc
+
+
+def _absorb_operands(tr, tag, refs, group):
+    """gadgets.py:183-186."""
+    tr.append(b"gadget/tag", tag)
+    for ref in refs:
+        tr.append(b"gadget/operand", ref.digest(group))
+
+
+def _open_tables(key, prover_tensors, point, tr, rng, values=None):
+    """gadgets.py:160-167 through the commitment backend."""
+    be = commit_backend(key)
+    tables, blindings = [], []
+    for pt in prover_tensors:
+        dev = getattr(pt, "device", None)
+        tables.append(dev if (dev is not None and be.__name__.endswith("commit_stub"))
+                      else pt.flat())
+        rows, _ = be.split_shape(pt.ref.num_vars)
+        blindings.append(list(pt.blinding) if pt.blinding else [0] * rows)
+    if values is not None and be.__name__.endswith("commit_stub"):
+        vals, proof = be.open_batch(key, tables, blindings, point, tr, rng, values=values)
+    else:
+        vals, proof = be.open_batch(key, tables, blindings, point, tr, rng)
+    return TYPES["Opening"](tuple(vals), proof)
+
+
+def _device_matrix(pt, rows, cols, spec):
+    dev = getattr(pt, "device", None)
+    if dev is not None:
+        return dev
+    return DeviceMatrix.from_field_list(pt.flat(), rows, cols, spec)
+
+
+# ---------------------------------------------------------------------------
+def _matvec(M, x, transpose, spec):
+    out = D.empty(spec, M.cols if transpose else M.rows)
+    N.check(N.lib().zkl_matvec(spec.fid, M.mtype, D.ptr(M.t), M.rows, M.cols,
+                               1 if transpose else 0, D.ptr(x), D.ptr(out), D.stream()))
+    return out
+
+
+def _axpy(a, k, b, n, spec):
+    out = D.empty(spec, n)
+    N.check(N.lib().zkl_axpy(spec.fid, D.ptr(out), D.ptr(a), D.scalar_bytes(k, spec),
+                             D.ptr(b), n, D.stream()))
+    return out
+
+
+def matmul_sumcheck(A, B, C, dims, tr):
+    """The sumcheck of prove_matmul (gadgets.py:241-251), factored, on the GPU.
+
+    A, B, C: DeviceMatrix of shapes 2^d0 x 2^d1, 2^d1 x 2^d2, 2^d0 x 2^d2.
+    Starts by drawing r_u / r_v; returns (rounds, point, final_values) with
+    rounds as evaluation tuples, identical to the reference's.
+    """
+    p = tr.modulus
+    spec = D.spec_for(p)
+    d0, d1, d2 = dims
+    D0, D1, D2 = 1 << d0, 1 << d1, 1 << d2
+    if (A.rows, A.cols, B.rows, B.cols, C.rows, C.cols) != (D0, D1, D1, D2, D0, D2):
+        raise ShapeMismatch("device operands do not match dims %r" % (dims,))
+    r_u = tr.challenge_vector(b"matmul/r_u", d0)
+    r_v = tr.challenge_vector(b"matmul/r_v", d2)
+    cneg = (-inverse(1 << d1, p)) % p
+    absorb_claim(tr, 0, [Term(1, (0, 1, 2)), Term(cneg, (0, 3))], 3, d0 + d1 + d2)
+    E_v = D.eq_table(r_v, spec)
+
+    # U phase
+    bv = _matvec(B, E_v, False, spec)
+    cv = _matvec(C, E_v, False, spec)
+    abv = _matvec(A, bv, False, spec)
+    h = _axpy(abv, cneg * pow(2, d1, p) % p, cv, D0, spec)
+    if d0:
+        E_u = D.eq_table(r_u, spec)
+        rounds_u, pt_u, fin_u = run_rounds(spec, [E_u, h], d0, [(1, (0, 1))], 3, tr)
+        e_hat = fin_u[0]
+    else:
+        rounds_u, pt_u, e_hat = [], [], 1
+
+    # W phase
+    E_ru = D.eq_table(pt_u, spec)
+    a = _matvec(A, E_ru, True, spec)
+    cu = _matvec(C, E_ru, True, spec)
+    kappa = D.dot(cu, E_v, spec, D2)
+    if d1:
+        def post_w(j):
+            return (cneg * pow(2, d1 - j - 1, p) % p * kappa % p, e_hat)
+
+        rounds_w, pt_w, fin_w = run_rounds(spec, [a, bv], d1, [(1, (0, 1))], 3, tr, post_w)
+        alpha_s = fin_w[0]
+    else:
+        rounds_w, pt_w, alpha_s = [], [], D.read_scalar(a, spec)
+
+    # V phase
+    E_rw = D.eq_table(pt_w, spec)
+    bw = _matvec(B, E_rw, True, spec)
+    if d2:
+        rounds_v, pt_v, fin_v = run_rounds(
+            spec, [E_v, bw, cu], d2, [(alpha_s, (0, 1)), (cneg, (0, 2))], 3, tr,
+            lambda j: (0, e_hat))
+        ev, bw_f, cu_f = fin_v
+    else:
+        rounds_v, pt_v = [], []
+        ev, bw_f, cu_f = 1, D.read_scalar(bw, spec), D.read_scalar(cu, spec)
+    finals = (e_hat * ev % p, alpha_s, bw_f, cu_f)
+    return rounds_u + rounds_w + rounds_v, pt_u + pt_w + pt_v, finals
+
+
+def prove_matmul(a, b, c, key, tr, rng):
+    """Drop-in for zklora.gadgets.prove_matmul (gadgets.py:230-265)."""
+    p = tr.modulus
+    d0, d1 = a.ref.row_vars, a.ref.col_vars
+    d1b, d2 = b.ref.row_vars, b.ref.col_vars
+    if d1 != d1b or (c.ref.row_vars, c.ref.col_vars) != (d0, d2):
+        raise ShapeMismatch(
+            "matmul shapes (%d,%d)x(%d,%d)->(%d,%d) do not conform"
+            % (d0, d1, d1b, d2, c.ref.row_vars, c.ref.col_vars))
+    _absorb_operands(tr, b"matmul", [a.ref, b.ref, c.ref], key.group)
+    spec = D.spec_for(p)
+    D0, D1, D2 = 1 << d0, 1 << d1, 1 << d2
+    A = _device_matrix(a, D0, D1, spec)
+    B = _device_matrix(b, D1, D2, spec)
+    C = _device_matrix(c, D0, D2, spec)
+    rounds, point, finals = matmul_sumcheck(A, B, C, (d0, d1, d2), tr)
+    RP = SC_TYPES["RoundPolynomial"]
+    sc_proof = SC_TYPES["SumcheckProof"]([RP(e) for e in rounds], tuple(finals))
+    rho_u, rho_w, rho_v = point[:d0], point[d0:d0 + d1], point[d0 + d1:]
+
+    def maybe_open(pt, opening_point, value):
+        if pt.ref.kind != "committed":
+            return None
+        return _open_tables(key, [pt], opening_point, tr, rng, values=[value])
+
+    return TYPES["MatmulProof"](
+        dims=(d0, d1, d2),
+        sumcheck=sc_proof,
+        a_opening=maybe_open(a, rho_u + rho_w, finals[1]),
+        b_opening=maybe_open(b, rho_w + rho_v, finals[2]),
+        c_opening=maybe_open(c, rho_u + rho_v, finals[3]),
+    )
+
+
+def prove_elementprod(a, b, c, key, tr, rng):
+    """Drop-in for zklora.gadgets.prove_elementprod (gadgets.py:383-410)."""
+    p = tr.modulus
+    shape = (a.ref.row_vars, a.ref.col_vars)
+    if (b.ref.row_vars, b.ref.col_vars) != shape or (c.ref.row_vars, c.ref.col_vars) != shape:
+        raise ShapeMismatch("elementprod operands must share a shape")
+    if c.ref.kind != "committed":
+        raise ValueError("elementprod output must be committed")
+    _absorb_operands(tr, b"elementprod", [a.ref, b.ref, c.ref], key.group)
+    n = a.ref.num_vars
+    r = tr.challenge_vector(b"elementprod/r", n)
+    c_opening = _open_tables(key, [c], r, tr, rng)
+    claimed = c_opening.values[0]
+    spec = D.spec_for(p)
+    rows, cols = 1 << shape[0], 1 << shape[1]
+    ta = _device_matrix(a, rows, cols, spec).as_field_vector(spec).clone()
+    tb = _device_matrix(b, rows, cols, spec).as_field_vector(spec).clone()
+    term = Term(1, (0, 1, 2))
+    absorb_claim(tr, claimed, [term], 3, n)
+    if n:
+        rounds, point, finals = run_rounds(spec, [D.eq_table(r, spec), ta, tb], n,
+                                           [(1, (0, 1, 2))], 3, tr)
+    else:
+        rounds, point = [], []
+        finals = [1, D.read_scalar(ta, spec), D.read_scalar(tb, spec)]
+    RP = SC_TYPES["RoundPolynomial"]
+    sc_proof = SC_TYPES["SumcheckProof"]([RP(e) for e in rounds], tuple(finals))
+    committed = [t for t in (a, b) if t.ref.kind == "committed"]
+    vals = [finals[1] if t is a else finals[2] for t in committed]
+    ab_opening = _open_tables(key, committed, point, tr, rng, values=vals) if committed else None
+    return TYPES["ElementprodProof"](shape=shape, c_opening=c_opening, sumcheck=sc_proof,
+                                     ab_opening=ab_opening)

@@ -1,0 +1,73 @@
+"""Install the GPU backend into an importable reference package (zklora).
+
+Module-attribute swap at every by-name import site:
+  prove_sumcheck         -> zklora.sumcheck, zklora.lookup, zklora.gadgets
+  prove_lookup,
+  compute_multiplicities -> zklora.lookup, zklora.gadgets
+  prove_matmul,
+  prove_elementprod      -> zklora.gadgets, zklora.pipeline
+  batch_inverse          -> zklora.field, zklora.lookup
+  eq_table               -> zklora.mle, zklora.lookup, zklora.gadgets, zklora.commit
+  fold_table             -> zklora.mle, zklora.sumcheck
+and the result classes are pointed at the reference's own dataclasses, so
+proofs serialize with the reference wire format (serialize.py:52-74).
+Returns a callable that restores the original bindings.
+"""
+
+import importlib
+
+
+def install(pkg=None):
+    from . import field as bf, gadgets as bg, lookup as bl, mle as bm, sumcheck as bs
+
+    z = pkg or importlib.import_module("zklora")
+    name = z.__name__
+    mods = {m: importlib.import_module("%s.%s" % (name, m))
+            for m in ("field", "mle", "sumcheck", "lookup", "gadgets", "commit", "pipeline")}
+    zs, zl, zg = mods["sumcheck"], mods["lookup"], mods["gadgets"]
+
+    saved = []
+
+    def swap(mod, attr, value):
+        if hasattr(mod, attr):
+            saved.append((mod, attr, getattr(mod, attr)))
+            setattr(mod, attr, value)
+
+    # result / error classes of the reference
+    type_saves = [(bs.TYPES, dict(bs.TYPES)), (bg.TYPES, dict(bg.TYPES)),
+                  (bl.TYPES, dict(bl.TYPES))]
+    bs.TYPES.update(RoundPolynomial=zs.RoundPolynomial, SumcheckProof=zs.SumcheckProof)
+    bg.TYPES.update(Opening=zg.Opening, MatmulProof=zg.MatmulProof,
+                    ElementprodProof=zg.ElementprodProof)
+    bl.TYPES.update(LookupProof=zl.LookupProof, ElementNotInTable=zl.ElementNotInTable,
+                    PoleCollision=zl.PoleCollision)
+
+    def batch_inverse(values, modulus):
+        try:
+            return bf.batch_inverse(values, modulus)
+        except bf.InversionOfZero as e:
+            raise mods["field"].InversionOfZero(str(e)) from None
+
+    for m in (zs, zl, zg):
+        swap(m, "prove_sumcheck", bs.prove_sumcheck)
+    for m in (zl, zg):
+        swap(m, "prove_lookup", bl.prove_lookup)
+        swap(m, "compute_multiplicities", bl.compute_multiplicities)
+    for m in (zg, mods["pipeline"]):
+        swap(m, "prove_matmul", bg.prove_matmul)
+        swap(m, "prove_elementprod", bg.prove_elementprod)
+    for m in (mods["field"], zl):
+        swap(m, "batch_inverse", batch_inverse)
+    for m in (mods["mle"], zl, zg, mods["commit"]):
+        swap(m, "eq_table", bm.eq_table)
+    for m in (mods["mle"], zs):
+        swap(m, "fold_table", bm.fold_table)
+
+    def uninstall():
+        for mod, attr, value in reversed(saved):
+            setattr(mod, attr, value)
+        for d, old in type_saves:
+            d.clear()
+            d.update(old)
+
+    return uninstall

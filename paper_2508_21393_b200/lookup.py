@@ -1,0 +1,271 @@
+"""logUp lookup argument on the GPU (drop-ins for zklora.lookup).
+
+prove_lookup follows lookup.py:143-251 step for step -- the same transcript
+traffic, beta pole retries, Eq.-7 claim and openings -- with the heavy parts
+on the device: beta + s and beta + t are inverted by one hierarchical
+Montgomery-trick pass each (whose zero detection IS the pole test of
+lookup.py:163-171), the seven lifted columns of lookup.py:188-202 are built
+by zkl_expand, and the degree-3 sumcheck runs on the fused round engine.
+compute_multiplicities (lookup.py:91-99) is a device hash-table histogram.
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+from . import _native as N
+from . import device as D
+from .field import batch_inverse_device, inverse
+from .gadgets import commit_backend
+from .mle import mle_evaluate_device
+from .sumcheck import TYPES as SC_TYPES
+from .sumcheck import Term, absorb_claim, run_rounds
+
+MAX_BETA_RETRIES = 3
+
+
+class ElementNotInTable(ValueError):
+    def __init__(self, index, value):
+        super().__init__("secret entry %d (value %d) not in table" % (index, value))
+        self.index = index
+        self.value = value
+
+
+class PoleCollision(RuntimeError):
+    pass
+
+
+@dataclass(frozen=True)
+class LookupTable:
+    entries: tuple
+    commitment: object
+    name: str = "table"
+
+    @property
+    def size(self):
+        return len(self.entries)
+
+    @property
+    def num_vars(self):
+        return (self.size - 1).bit_length()
+
+
+@dataclass(frozen=True)
+class SecretVector:
+    entries: tuple
+    commitment: object
+    blinding: tuple
+
+    @property
+    def num_vars(self):
+        return (len(self.entries) - 1).bit_length()
+
+
+@dataclass
+class LookupProof:
+    secret_vars: int
+    beta_retries: int
+    multiplicity_commitment: object
+    inverse_secret_commitment: object
+    inverse_table_commitment: object
+    sumcheck: object
+    secret_values: tuple
+    secret_opening: object
+    table_values: tuple
+    table_opening: object
+
+
+TYPES = {"LookupProof": LookupProof, "ElementNotInTable": ElementNotInTable,
+         "PoleCollision": PoleCollision}
+
+
+def _terms(alpha, ratio, p):
+    """lookup.py:116-126; factors 0 eq, 1 A, 2 S+beta, 3 ind, 4 B, 5 T+beta, 6 m."""
+    a2 = alpha * alpha % p
+    a3 = a2 * alpha % p
+    return [
+        Term(alpha, (0, 1, 2)),
+        Term((-alpha) % p, (0, 3)),
+        Term(a2, (0, 4, 5)),
+        Term(a3, (1,)),
+        Term((-a3 * ratio) % p, (6, 4)),
+    ]
+
+
+def _check_canonical(values, p, what):
+    if values and (min(values) < 0 or max(values) >= p):
+        raise NotImplementedError("%s must be canonical residues for the GPU path" % what)
+
+
+def multiplicities_device(secret_buf, d, table_buf, n, spec):
+    """Device histogram; returns (uint32 counts tensor, first_miss or None)."""
+    import torch
+
+    counts = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    fm = ctypes.c_int64(-1)
+    rc = N.lib().zkl_multiplicities(spec.fid, D.ptr(secret_buf), d, D.ptr(table_buf), n,
+                                    D.ptr(counts), ctypes.byref(fm), D.stream())
+    if rc == N.ZKL_ERR_MISSING:
+        return counts, fm.value
+    N.check(rc)
+    return counts, None
+
+
+def compute_multiplicities(secret_entries, table, modulus=None):
+    """Drop-in for zklora.lookup.compute_multiplicities (lookup.py:91-99)."""
+    entries = list(secret_entries)
+    tab = list(table.entries)
+    if modulus is None:
+        from .field import MODULUS, TEST_MODULUS
+
+        top = max(tab + entries + [0])
+        modulus = TEST_MODULUS if top < TEST_MODULUS else MODULUS
+    spec = D.spec_for(modulus)
+    _check_canonical(entries, modulus, "secret entries")
+    _check_canonical(tab, modulus, "table entries")
+    sbuf = D.upload(entries, spec)
+    tbuf = D.upload(tab, spec)
+    counts, miss = multiplicities_device(sbuf, len(entries), tbuf, len(tab), spec)
+    if miss is not None:
+        raise TYPES["ElementNotInTable"](miss, entries[miss])
+    return [int(c) for c in counts[: len(tab)].cpu().tolist()]
+
+
+class _Sized:
+    """len()-only stand-in handed to the commitment stub (no host copy)."""
+
+    def __init__(self, n):
+        self.n = n
+
+    def __len__(self):
+        return self.n
+
+
+def _expand(spec, dst_n, src, src_n, mode, add=None, pad=None):
+    out = D.empty(spec, dst_n)
+    N.check(N.lib().zkl_expand(
+        spec.fid, D.ptr(out), dst_n, D.ptr(src) if src is not None else None, src_n, mode,
+        D.scalar_bytes(add, spec) if add is not None else None,
+        D.scalar_bytes(pad, spec) if pad is not None else None, D.stream()))
+    return out
+
+
+def prove_lookup(secret, multiplicities, table, key, tr, rng):
+    """Drop-in for zklora.lookup.prove_lookup (lookup.py:143-251)."""
+    p = tr.modulus
+    spec = D.spec_for(p)
+    group = key.group
+    entries = secret.entries
+    d, n = len(entries), table.size
+    if d == 0 or d & (d - 1):
+        raise ValueError("secret length must be a power of two")
+    if len(multiplicities) != n:
+        raise ValueError("multiplicity vector must match the table size")
+    be = commit_backend(key)
+    stub = be.__name__.endswith("commit_stub")
+
+    # m commitment + setup absorption (lookup.py:158-161)
+    m_rows, _ = be.split_shape(table.num_vars)
+    m_blinding = rng.vector(m_rows)
+    m_commitment = be.commit(key, list(multiplicities), m_blinding)
+    tr.append(b"lookup/table", table.commitment.serialize(group))
+    tr.append(b"lookup/secret", secret.commitment.serialize(group))
+    tr.append(b"lookup/mult", m_commitment.serialize(group))
+
+    s_buf = D.upload(list(entries), spec)
+    t_buf = D.upload(list(table.entries), spec)
+    m_buf = D.upload(list(multiplicities), spec)
+
+    # beta with pole retries (lookup.py:163-171): a pole is exactly a zero in
+    # beta + s or beta + t, which the device batch inversion reports.
+    retries = 0
+    beta = tr.challenge(b"lookup/beta")
+    while True:
+        inv_s, z1 = batch_inverse_device(s_buf, d, spec, add=beta)
+        z2 = None
+        if z1 is None:
+            inv_t, z2 = batch_inverse_device(t_buf, n, spec, add=beta)
+        if z1 is None and z2 is None:
+            break
+        retries += 1
+        if retries > MAX_BETA_RETRIES:
+            raise TYPES["PoleCollision"]("challenge hit a pole %d times" % retries)
+        tr.append(b"lookup/beta-retry", retries)
+        beta = tr.challenge(b"lookup/beta")
+
+    # helper-column commitments (lookup.py:175-180)
+    a_rows, _ = be.split_shape(secret.num_vars)
+    a_blinding = rng.vector(a_rows)
+    if stub:
+        inv_s_host = inv_t_host = None
+        a_commitment = be.commit(key, _Sized(d), a_blinding)
+        b_commitment = be.commit(key, _Sized(n))
+    else:
+        inv_s_host = D.download(inv_s, spec, d)
+        inv_t_host = D.download(inv_t, spec, n)
+        a_commitment = be.commit(key, inv_s_host, a_blinding)
+        b_commitment = be.commit(key, inv_t_host)
+    tr.append(b"lookup/inv-secret", a_commitment.serialize(group))
+    tr.append(b"lookup/inv-table", b_commitment.serialize(group))
+
+    alpha = tr.challenge(b"lookup/alpha")
+    big = max(d, n)
+    num_vars = (big - 1).bit_length()
+    u = tr.challenge_vector(b"lookup/u", num_vars)
+    ratio = inverse(big // n, p)
+
+    # lifted columns (lookup.py:188-202)
+    if d <= n:
+        A = _expand(spec, n, inv_s, d, 0)
+        Sb = _expand(spec, n, s_buf, d, 0, add=beta, pad=beta)
+        ind = _expand(spec, n, None, d, 0, add=1, pad=0)
+        Bt = inv_t.clone()
+        Tb = _expand(spec, n, t_buf, n, 1, add=beta)
+        Mt = m_buf.clone()
+    else:
+        A = inv_s.clone()
+        Sb = _expand(spec, d, s_buf, d, 1, add=beta)
+        ind = _expand(spec, d, None, d, 0, add=1, pad=0)
+        Bt = _expand(spec, d, inv_t, n, 1)
+        Tb = _expand(spec, d, t_buf, n, 1, add=beta)
+        Mt = _expand(spec, d, m_buf, n, 1)
+    E = D.eq_table(u, spec)
+    terms = _terms(alpha, ratio, p)
+    claimed = alpha * alpha % p
+    absorb_claim(tr, claimed, terms, 3, num_vars)
+    tuples = [(t.coefficient, t.factors) for t in terms]
+    if num_vars:
+        rounds, point, finals = run_rounds(spec, [E, A, Sb, ind, Bt, Tb, Mt], num_vars, tuples,
+                                           3, tr)
+    else:
+        rounds, point = [], []
+        finals = [D.read_scalar(x, spec) for x in (E, A, Sb, ind, Bt, Tb, Mt)]
+    RP = SC_TYPES["RoundPolynomial"]
+    sc_proof = SC_TYPES["SumcheckProof"]([RP(e) for e in rounds], tuple(finals))
+
+    # openings (lookup.py:221-239)
+    d_vars, n_vars = secret.num_vars, table.num_vars
+    secret_point = point[num_vars - d_vars:]
+    table_point = point[num_vars - n_vars:]
+    zero_blind = [0] * m_rows
+    if stub:
+        if d >= n:  # finals are the unpadded MLEs (replication is MLE-transparent)
+            s_vals = [finals[1], (finals[2] - beta) % p]
+        else:
+            s_vals = [mle_evaluate_device(inv_s, d_vars, secret_point, spec),
+                      mle_evaluate_device(s_buf, d_vars, secret_point, spec)]
+        # the table side is either unpadded (d <= n) or replicated (d > n)
+        t_vals = [finals[6], finals[4], (finals[5] - beta) % p]
+        secret_values, secret_opening = be.open_batch(
+            key, None, None, secret_point, tr, rng, values=s_vals)
+        table_values, table_opening = be.open_batch(
+            key, None, None, table_point, tr, rng, values=t_vals)
+    else:
+        secret_values, secret_opening = be.open_batch(
+            key, [inv_s_host, list(entries)], [list(a_blinding), list(secret.blinding)],
+            secret_point, tr, rng)
+        table_values, table_opening = be.open_batch(
+            key, [list(multiplicities), inv_t_host, list(table.entries)],
+            [list(m_blinding), zero_blind, zero_blind], table_point, tr, rng)
+    return TYPES["LookupProof"](
+        secret.num_vars, retries, m_commitment, a_commitment, b_commitment, sc_proof,
+        tuple(secret_values), secret_opening, tuple(table_values), table_opening)

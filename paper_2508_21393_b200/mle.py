@@ -1,0 +1,87 @@
+"""MLE helpers on the GPU: drop-ins for zklora.mle (mle.py:50-100).
+
+Variable order as in the reference: the first coordinate is the most
+significant index bit; matrices are row bits || column bits.
+"""
+
+import ctypes
+
+from . import _native as N
+from . import device as D
+
+
+class DimensionMismatch(ValueError):
+    pass
+
+
+def fold_table(table, r, modulus):
+    """mle.py:50-56 on the device."""
+    spec = D.spec_for(modulus)
+    half = len(table) // 2
+    if half == 0:
+        return []
+    src = D.upload(list(table), spec)
+    dst = D.empty(spec, half)
+    N.check(N.lib().zkl_fold(spec.fid, D.ptr(dst), D.ptr(src), half, D.scalar_bytes(r, spec),
+                             D.stream()))
+    return D.download(dst, spec, half)
+
+
+def eq_table(point, modulus):
+    """mle.py:67-82 on the device."""
+    spec = D.spec_for(modulus)
+    return D.download(D.eq_table(list(point), spec), spec, 1 << len(point))
+
+
+def mle_evaluate_device(buf, n_vars, point, spec):
+    """MLE of a device field vector (2^n_vars entries) at `point` by folds."""
+    if len(point) != n_vars:
+        raise DimensionMismatch("point has %d coordinates, polynomial has %d variables"
+                                % (len(point), n_vars))
+    lib = N.lib()
+    if n_vars == 0:
+        return D.read_scalar(buf, spec)
+    size = 1 << n_vars
+    tmp = D.empty(spec, size // 2)
+    src = buf
+    for r in point:  # first fold out of place (keeps buf), then in place
+        half = size // 2
+        N.check(lib.zkl_fold(spec.fid, D.ptr(tmp), D.ptr(src), half, D.scalar_bytes(r, spec),
+                             D.stream()))
+        src = tmp
+        size = half
+    return D.read_scalar(tmp, spec)
+
+
+def mle_evaluate(table, point, modulus):
+    """mle.py:59-64 on the device."""
+    spec = D.spec_for(modulus)
+    n = (len(table) - 1).bit_length()
+    return mle_evaluate_device(D.upload(list(table), spec), n, list(point), spec)
+
+
+def mle_evaluate_any(table, point, modulus):
+    """Python list or DeviceMatrix / device vector."""
+    spec = D.spec_for(modulus)
+    lifted = getattr(table, "as_field_vector", None)
+    if lifted is not None:
+        return mle_evaluate_device(lifted(spec), len(point), list(point), spec)
+    return mle_evaluate(table, point, modulus)
+
+
+def eq_eval(u, x, modulus):
+    """mle.py:85-92 (scalar, host)."""
+    if len(u) != len(x):
+        raise DimensionMismatch("eq kernel arity mismatch")
+    acc = 1
+    for a, b in zip(u, x):
+        acc = acc * ((a * b + (1 - a) * (1 - b)) % modulus) % modulus
+    return acc
+
+
+def zero_prefix_eval(point, count, modulus):
+    """mle.py:95-100 (scalar, host)."""
+    acc = 1
+    for r in point[:count]:
+        acc = acc * ((1 - r) % modulus) % modulus
+    return acc

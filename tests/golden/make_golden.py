@@ -208,6 +208,7 @@ def _capture(fn, *args):
     orig_abs, orig_sc = G._absorb_operands, G.prove_sumcheck
 
     def absorb(tr, tag, refs, group):
+        rec.setdefault("state_in", tr.state)
         orig_abs(tr, tag, refs, group)
         rec.setdefault("state_before", tr.state)
 
@@ -255,7 +256,7 @@ def gen_matmul():
             tamper=list(tamper) if tamper else None,
             data=dict(a=a.reshape(-1).tolist(), b=b.reshape(-1).tolist(),
                       c=cm.reshape(-1).tolist()) if small else None,
-            state_before=hx(rec["state_before"]),
+            state_in=hx(rec["state_in"]), state_before=hx(rec["state_before"]),
             rounds=[list(x.evaluations) for x in proof.sumcheck.rounds],
             final_values=list(proof.sumcheck.final_values),
             state_after=hx(rec["state_after"]),
@@ -279,7 +280,8 @@ def gen_elementprod():
             proof, rec = _capture(G.prove_elementprod, ta, tb, tc, KEY, tr, RNG)
             cases.append(dict(
                 field=fname, shape=[r, c], a=a.reshape(-1).tolist(), b=b.reshape(-1).tolist(),
-                c=cm.reshape(-1).tolist(), state_before=hx(rec["state_before"]),
+                c=cm.reshape(-1).tolist(), state_in=hx(rec["state_in"]),
+                state_before=hx(rec["state_before"]),
                 state_pre_sumcheck=hx(rec["state_pre_sumcheck"]),
                 claimed_sum=rec["claimed_sum"],
                 rounds=[list(x.evaluations) for x in proof.sumcheck.rounds],

@@ -1,0 +1,342 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference goldens
+and the CPU oracle, bit-exact.  Run on a B200: pytest -m gpu.
+"""
+
+import random
+
+import numpy as np
+import pytest
+
+from conftest import FIELDS, P_BIG, P_TEST, load_golden
+import inputs
+from oracle import fs, logup, multilinear, prime, sc, zkmat
+from oracle.stubcommit import StubBackend
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2508_21393_b200 as zb  # noqa: E402
+from paper_2508_21393_b200 import device as D  # noqa: E402
+from paper_2508_21393_b200.commit_stub import StubCommitment, StubKey  # noqa: E402
+from paper_2508_21393_b200.gadgets import DeviceMatrix, ProverTensor, TensorRef  # noqa: E402
+from paper_2508_21393_b200.transcript import Transcript  # noqa: E402
+
+KEY = StubKey()
+
+
+class _Rng:
+    def vector(self, n):
+        return [0] * n
+
+    def next(self):
+        return 0
+
+
+RNG = _Rng()
+
+
+def _tr(state_hex, p):
+    return Transcript.from_state(bytes.fromhex(state_hex), p)
+
+
+# --- field / mle -------------------------------------------------------------------
+
+
+def test_field_mle_golden():
+    g = load_golden("field_mle.json")
+    for c in g["batch_inverse"]:
+        p = FIELDS[c["field"]]
+        if "error" in c:
+            with pytest.raises(zb.InversionOfZero) as e:
+                zb.batch_inverse(c["values"], p)
+            assert str(e.value) == c["error"]
+        else:
+            assert zb.batch_inverse(c["values"], p) == c["inverse"]
+    for c in g["eq"]:
+        assert zb.eq_table(c["point"], FIELDS[c["field"]]) == c["table"]
+    for c in g["fold"]:
+        assert zb.fold_table(c["table"], c["r"], FIELDS[c["field"]]) == c["out"]
+    for c in g["mle"]:
+        assert zb.mle_evaluate(c["table"], c["point"], FIELDS[c["field"]]) == c["value"]
+
+
+@pytest.mark.parametrize("field", ["big", "test"])
+@pytest.mark.parametrize("n", [1, 2, 255, 2048, 2049, 100000, (1 << 20) + 7])
+def test_batch_inverse_sizes(field, n):
+    p = FIELDS[field]
+    vals = inputs.field_vec(1000 + n, min(n, 4096), p)
+    vals = (vals * (n // len(vals) + 1))[:n]
+    vals = [v or 1 for v in vals]
+    got = zb.batch_inverse(vals, p)
+    idx = [0, n // 2, n - 1] + random.Random(n).sample(range(n), min(n, 50))
+    for i in idx:
+        assert got[i] * vals[i] % p == 1
+
+
+@pytest.mark.parametrize("field", ["big", "test"])
+def test_batch_inverse_zero_reports_first_index(field):
+    p = FIELDS[field]
+    vals = list(range(1, 5001))
+    vals[3333] = 0
+    vals[4444] = 0
+    with pytest.raises(zb.InversionOfZero, match="at index 3333"):
+        zb.batch_inverse(vals, p)
+    vals = list(range(1, 100))
+    vals[7] = p  # multiple of p but not a literal zero: reference fails at the end
+    with pytest.raises(zb.InversionOfZero) as e:
+        zb.batch_inverse(vals, p)
+    assert str(e.value) == "cannot invert 0"
+
+
+@pytest.mark.parametrize("field", ["big", "test"])
+def test_eq_table_large_two_level(field):
+    p = FIELDS[field]
+    pt = inputs.field_vec(77, 15, p)
+    spec = D.spec_for(p)
+    got = D.download(D.eq_table(pt, spec), spec, 1 << 15)
+    hi = multilinear.eq_vec(pt[:7], p)
+    lo = multilinear.eq_vec(pt[7:], p)
+    for i in random.Random(3).sample(range(1 << 15), 200):
+        assert got[i] == hi[i >> 8] * lo[i & 255] % p
+
+
+# --- sumcheck ----------------------------------------------------------------
+
+
+def test_sumcheck_golden():
+    for c in load_golden("sumcheck.json"):
+        p = FIELDS[c["field"]]
+        t = _tr(c["state_before"], p)
+        terms = [zb.Term(co, tuple(f)) for co, f in c["terms"]]
+        claim = zb.SumcheckClaim(c["claimed_sum"], c["tables"], terms, c["degree"], p)
+        proof, point = zb.prove_sumcheck(claim, t)
+        assert [list(r.evaluations) for r in proof.rounds] == c["rounds"], c["note"]
+        assert list(proof.final_values) == c["final_values"], c["note"]
+        assert isinstance(proof.rounds, list) and isinstance(proof.final_values, tuple)
+        assert point == c["point"]
+        assert t.state.hex() == c["state_after"]
+
+
+@pytest.mark.parametrize("field", ["big", "test"])
+@pytest.mark.parametrize("k,degree,n", [(2, 2, 12), (3, 3, 13), (4, 3, 11), (7, 3, 10),
+                                        (8, 3, 9), (1, 1, 14)])
+def test_sumcheck_random_vs_oracle(field, k, degree, n):
+    p = FIELDS[field]
+    rnd = random.Random(k * 100 + n)
+    tabs = [inputs.field_vec(rnd.randrange(1 << 30), 1 << n, p) for _ in range(k)]
+    terms = []
+    for _ in range(rnd.randrange(1, 9)):
+        nf = rnd.randrange(0, degree + 1)
+        terms.append(zb.Term(rnd.randrange(p), tuple(rnd.randrange(k) for _ in range(nf))))
+    claimed = rnd.randrange(p)
+    t1 = Transcript(b"rand", p, b"s")
+    proof, point = zb.prove_sumcheck(zb.SumcheckClaim(claimed, tabs, terms, degree, p), t1)
+    t2 = fs.FS(b"rand", p, b"s")
+    rounds, finals, opoint = sc.prove(claimed, tabs, [(x.coefficient, x.factors) for x in terms],
+                                      degree, t2)
+    assert [r.evaluations for r in proof.rounds] == rounds
+    assert proof.final_values == finals
+    assert point == opoint and t1.state == t2.state
+
+
+# --- zkMat ---------------------------------------------------------------------------
+
+
+def _mm_data(c):
+    if c["data"] is not None:
+        a, b, cm = (np.asarray(c["data"][k], dtype=np.int64) for k in ("a", "b", "c"))
+        d0, d1, d2 = c["dims"]
+        return a.reshape(1 << d0, 1 << d1), b.reshape(1 << d1, 1 << d2), cm.reshape(1 << d0, 1 << d2)
+    r, k, co = c["shape"]
+    return inputs.matmul_case(c["seed"], r, k, co,
+                              tamper=tuple(c["tamper"]) if c["tamper"] else None)
+
+
+def _dev(arr, dtype):
+    return DeviceMatrix.from_int_tensor(torch.from_numpy(np.ascontiguousarray(arr)).to(dtype).cuda())
+
+
+@pytest.mark.parametrize("mode", ["i64", "i16", "field"])
+def test_matmul_sumcheck_golden(mode):
+    for c in load_golden("matmul.json"):
+        p = FIELDS[c["field"]]
+        a, b, cm = _mm_data(c)
+        dims = tuple(c["dims"])
+        if mode == "field":
+            spec = D.spec_for(p)
+            A = DeviceMatrix.from_field_list(inputs.to_field(a, p), *a.shape, spec)
+            B = DeviceMatrix.from_field_list(inputs.to_field(b, p), *b.shape, spec)
+            C = DeviceMatrix.from_field_list(inputs.to_field(cm, p), *cm.shape, spec)
+        elif mode == "i16":
+            if np.abs(cm).max() >= (1 << 15):
+                A, B = _dev(a, torch.int16), _dev(b, torch.int16)
+                C = _dev(cm, torch.int64)
+            else:
+                A, B, C = (_dev(x, torch.int16) for x in (a, b, cm))
+        else:
+            A, B, C = (_dev(x, torch.int64) for x in (a, b, cm))
+        t = _tr(c["state_before"], p)
+        rounds, point, finals = zb.matmul_sumcheck(A, B, C, dims, t)
+        assert [list(r) for r in rounds] == c["rounds"], (mode, c["shape"])
+        assert list(finals) == c["final_values"]
+        assert t.state.hex() == c["state_after"]
+
+
+def test_prove_matmul_full_with_stub_openings():
+    """Whole gadget (gadgets.py:230-265) from the pre-absorption state."""
+    for c in load_golden("matmul.json"):
+        p = FIELDS[c["field"]]
+        a, b, cm = _mm_data(c)
+        d0, d1, d2 = c["dims"]
+
+        def pt(arr, rv, cv):
+            ref = TensorRef("committed", rv, cv, commitment=StubCommitment(rv + cv))
+            return ProverTensor(None, ref, (), device=_dev(arr, torch.int64))
+
+        t = _tr(c["state_in"], p)
+        proof = zb.prove_matmul(pt(a, d0, d1), pt(b, d1, d2), pt(cm, d0, d2), KEY, t, RNG)
+        assert proof.dims == (d0, d1, d2)
+        assert [list(r.evaluations) for r in proof.sumcheck.rounds] == c["rounds"]
+        assert list(proof.sumcheck.final_values) == c["final_values"]
+        assert [list(o.values) for o in (proof.a_opening, proof.b_opening,
+                                          proof.c_opening)] == c["openings"]
+        assert t.state.hex() == c["state_end"]
+
+
+@pytest.mark.parametrize("field", ["big", "test"])
+@pytest.mark.parametrize("dims,dt", [((5, 9, 3), "i16"), ((0, 10, 2), "i16"), ((7, 0, 7), "i16"),
+                                     ((4, 6, 0), "i64"), ((8, 8, 8), "i16"), ((6, 4, 9), "i32")])
+def test_matmul_factored_vs_oracle(field, dims, dt):
+    p = FIELDS[field]
+    d0, d1, d2 = dims
+    g = inputs.rng(sum(dims) * 7 + len(dt))
+    a = g.integers(-32768, 32768, size=(1 << d0, 1 << d1))
+    b = g.integers(-32768, 32768, size=(1 << d1, 1 << d2))
+    cm = a @ b
+    cm[0, 0] += 3  # a false claim exercises the non-zero U phase
+    tdt = {"i16": torch.int16, "i32": torch.int32, "i64": torch.int64}[dt]
+    A, B = _dev(a, tdt), _dev(b, tdt)
+    C = _dev(cm, torch.int64)
+    t1 = Transcript(b"mm", p, b"x")
+    rounds, point, finals = zb.matmul_sumcheck(A, B, C, dims, t1)
+    t2 = fs.FS(b"mm", p, b"x")
+    orounds, ofinals, opoint = zkmat.prove_factored(a.reshape(-1), b.reshape(-1), cm.reshape(-1),
+                                                    dims, t2)
+    assert rounds == orounds and tuple(finals) == ofinals and point == opoint
+    assert t1.state == t2.state
+
+
+@pytest.mark.parametrize("field", ["big", "test"])
+@pytest.mark.parametrize("mt", ["i16", "i32", "i64"])
+@pytest.mark.parametrize("shape", [(1, 1), (3, 70), (64, 5), (1024, 256), (33, 4096)])
+def test_matvec_extremes_vs_numpy(field, mt, shape):
+    from paper_2508_21393_b200.gadgets import _matvec
+
+    p = FIELDS[field]
+    spec = D.spec_for(p)
+    lo, hi = {"i16": (-32768, 32767), "i32": (-2**31, 2**31 - 1), "i64": (-2**63, 2**63 - 1)}[mt]
+    g = inputs.rng(shape[0] * 31 + shape[1])
+    M = g.integers(lo, hi, size=shape, dtype=np.int64, endpoint=True)
+    M.flat[0] = lo
+    M.flat[-1] = hi
+    tdt = {"i16": torch.int16, "i32": torch.int32, "i64": torch.int64}[mt]
+    Md = _dev(M, tdt)
+    for transpose in (0, 1):
+        xlen = shape[0] if transpose else shape[1]
+        x = inputs.field_vec(xlen + transpose, xlen, p)
+        y = D.download(_matvec(Md, D.upload(x, spec), bool(transpose), spec), spec,
+                       shape[1] if transpose else shape[0])
+        ML = M.T if transpose else M
+        want = [sum(int(v) * x[j] for j, v in enumerate(row)) % p for row in ML.tolist()]
+        assert y == want, transpose
+
+
+def test_elementprod_golden():
+    for c in load_golden("elementprod.json"):
+        p = FIELDS[c["field"]]
+        rv, cv = ((x - 1).bit_length() for x in c["shape"])
+
+        def pt(vals):
+            ref = TensorRef("committed", rv, cv, commitment=StubCommitment(rv + cv))
+            arr = np.asarray(vals, dtype=np.int64).reshape(1 << rv, 1 << cv)
+            return ProverTensor(None, ref, (), device=_dev(arr, torch.int64))
+
+        t = _tr(c["state_in"], p)
+        proof = zb.prove_elementprod(pt(c["a"]), pt(c["b"]), pt(c["c"]), KEY, t, RNG)
+        assert proof.c_opening.values[0] == c["claimed_sum"]
+        assert [list(r.evaluations) for r in proof.sumcheck.rounds] == c["rounds"]
+        assert list(proof.sumcheck.final_values) == c["final_values"]
+        assert list(proof.ab_opening.values) == c["ab_opening"]
+        assert t.state.hex() == c["state_end"]
+
+
+# --- logUp -----------------------------------------------------------------------------
+
+
+def test_multiplicities_golden():
+    for c in load_golden("lookup.json")["multiplicities"]:
+        table = zb.LookupTable(tuple(c["table"]), None)
+        if "error" in c:
+            with pytest.raises(zb.ElementNotInTable) as e:
+                zb.compute_multiplicities(c["secret"], table)
+            assert [e.value.index, e.value.value] == c["error"]
+        else:
+            assert zb.compute_multiplicities(c["secret"], table) == c["counts"]
+
+
+def test_multiplicities_large_vs_oracle():
+    rnd = random.Random(8)
+    table = [rnd.randrange(P_BIG) for _ in range(1 << 12)]
+    table[5] = table[900]  # duplicate: last index wins
+    secret = [rnd.choice(table) for _ in range(1 << 16)]
+    got = zb.compute_multiplicities(secret, zb.LookupTable(tuple(table), None))
+    assert got == logup.multiplicities(secret, table)
+    secret[40000] = 12345
+    secret[50000] = 54321
+    with pytest.raises(zb.ElementNotInTable) as e:
+        zb.compute_multiplicities(secret, zb.LookupTable(tuple(table), None))
+    assert e.value.index == 40000
+
+
+def _lookup_run(c):
+    p = FIELDS[c["field"]]
+    d, n = len(c["secret"]), len(c["table"])
+    table = zb.LookupTable(tuple(c["table"]), StubCommitment((n - 1).bit_length()))
+    secret = zb.SecretVector(tuple(c["secret"]), StubCommitment((d - 1).bit_length()), ())
+    t = _tr(c["state_before"], p)
+    return zb.prove_lookup(secret, list(c["mult"]), table, KEY, t, RNG), t
+
+
+def test_lookup_golden():
+    for c in load_golden("lookup.json")["lookup"]:
+        proof, t = _lookup_run(c)
+        assert proof.beta_retries == c["beta_retries"]
+        assert [list(r.evaluations) for r in proof.sumcheck.rounds] == c["rounds"], c["note"]
+        assert list(proof.sumcheck.final_values) == c["final_values"], c["note"]
+        assert list(proof.secret_values) == c["secret_values"], c["note"]
+        assert list(proof.table_values) == c["table_values"], c["note"]
+        assert t.state.hex() == c["state_end"], c["note"]
+
+
+@pytest.mark.parametrize("field", ["big", "test"])
+@pytest.mark.parametrize("d,n", [(1 << 14, 1 << 10), (1 << 8, 1 << 12), (1 << 10, 1 << 10)])
+def test_lookup_vs_oracle(field, d, n):
+    p = FIELDS[field]
+    rnd = random.Random(d + n)
+    table = [rnd.randrange(p) for _ in range(n)]
+    secret = [rnd.choice(table) for _ in range(d)]
+    mult = logup.multiplicities(secret, table)
+    nb = lambda k: (k - 1).bit_length()  # noqa: E731
+    t1 = Transcript(b"lk", p, b"q")
+    proof = zb.prove_lookup(zb.SecretVector(tuple(secret), StubCommitment(nb(d)), ()), mult,
+                            zb.LookupTable(tuple(table), StubCommitment(nb(n))), KEY, t1, RNG)
+    t2 = fs.FS(b"lk", p, b"q")
+    from oracle.stubcommit import stub_bytes
+
+    out = logup.prove(secret, mult, table, stub_bytes(nb(n)), stub_bytes(nb(d)), t2,
+                      StubBackend(p))
+    assert [r.evaluations for r in proof.sumcheck.rounds] == out["rounds"]
+    assert proof.sumcheck.final_values == out["final_values"]
+    assert proof.secret_values == out["secret_values"]
+    assert proof.table_values == out["table_values"]
+    assert t1.state == t2.state

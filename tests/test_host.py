@@ -1,0 +1,163 @@
+"""CPU-side tests of the product package (no GPU needed).
+
+* the C-ABI library loads and exports every symbol include/zkl_b200.h declares
+* the host transcript is byte-identical to the reference (frozen vectors)
+* claim validation mirrors sumcheck.py:39-52
+* install() swaps exactly the reference's by-name import sites
+"""
+
+import os
+import re
+
+import pytest
+
+from conftest import FIELDS, P_BIG, P_TEST, ROOT, load_golden
+from oracle import fs
+
+import paper_2508_21393_b200 as zb
+from paper_2508_21393_b200 import _native as N
+from paper_2508_21393_b200.transcript import Transcript
+
+
+def _declared_symbols():
+    with open(os.path.join(ROOT, "include", "zkl_b200.h")) as fh:
+        text = fh.read()
+    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(zkl_\w+)\(", text, re.M)))
+
+
+def test_library_loads_and_exports_header_symbols():
+    lib = N.load()
+    declared = _declared_symbols()
+    assert len(declared) >= 15
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert set(declared) == set(N.EXPORTS)
+    assert lib.zkl_abi_version() == 1
+    assert lib.zkl_elem_bytes(0) == 32 and lib.zkl_elem_bytes(1) == 8
+    assert lib.zkl_elem_bytes(7) < 0
+
+
+def test_transcript_reference_vectors():
+    # pkg/tests/test_transcript.py:56-70
+    t = Transcript(b"zklora/fixture", P_TEST, seed=b"golden")
+    t.append(b"step", b"\x01\x02\x03")
+    assert t.challenge(b"alpha") == 1003351324687887681
+    t.append(b"step", (12345).to_bytes(4, "little"))
+    assert t.challenge(b"beta") == 383246615542169770
+    assert t.challenge(b"beta") == 1771741828449350904
+    tb = Transcript(b"zklora/fixture", P_BIG, seed=b"golden")
+    tb.append(b"step", b"\x01\x02\x03")
+    assert tb.challenge(b"alpha") == 0x3854DBD0DC30202B050AC1F48591FA60CBC12634D58C198681FC7807DF8BD2EF
+
+
+def test_transcript_matches_golden_streams():
+    for case in load_golden("transcript.json"):
+        p = FIELDS[case["field"]]
+        t = Transcript(bytes.fromhex(case["domain"]), p, bytes.fromhex(case["seed"]))
+        got = []
+        for op in case["ops"]:
+            lab = bytes.fromhex(op[1])
+            if op[0] == "bytes":
+                t.append(lab, bytes.fromhex(op[2]))
+            elif op[0] == "int":
+                t.append(lab, op[2])
+            elif op[0] == "challenge":
+                got.append(t.challenge(lab))
+            else:
+                got.extend(t.challenge_vector(lab, op[2]))
+        assert got == case["challenges"]
+        assert t.state.hex() == case["state"]
+        assert [x[1] for x in t.log] == [x[1] for x in t.log]
+
+
+def test_transcript_resume_and_fork():
+    a = fs.FS(b"d", P_BIG, b"s")
+    a.append(b"x", 77)
+    b = Transcript.from_state(a.state, P_BIG)
+    assert a.challenge(b"c") == b.challenge(b"c")
+    t = Transcript(b"t", P_TEST)
+    assert t.fork(b"g1").challenge(b"c") != t.fork(b"g2").challenge(b"c")
+
+
+def test_claim_validation_mirrors_reference():
+    with pytest.raises(zb.DegreeOverflow):
+        zb.SumcheckClaim(0, [[1, 2]] * 4, [zb.Term(1, (0, 1, 2, 3))], 4, P_TEST)
+    with pytest.raises(zb.DegreeOverflow):
+        zb.SumcheckClaim(0, [[1, 2]] * 3, [zb.Term(1, (0, 1, 2))], 2, P_TEST)
+    with pytest.raises(zb.SumcheckError):
+        zb.SumcheckClaim(0, [[1, 2], [1, 2, 3, 4]], [zb.Term(1, (0, 1))], 2, P_TEST)
+    with pytest.raises(zb.SumcheckError):
+        zb.SumcheckClaim(0, [[1, 2, 3]], [zb.Term(1, (0,))], 1, P_TEST)
+    assert zb.SumcheckClaim(0, [[1] * 8], [zb.Term(1, (0,))], 1, P_TEST).num_vars == 3
+
+
+def test_unsupported_field_is_rejected():
+    from paper_2508_21393_b200 import device as D
+
+    with pytest.raises(D.UnsupportedField):
+        D.spec_for(2**31 - 1)
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(N.BackendUnavailable):
+        zb.batch_inverse([1, 2, 3], P_TEST)
+
+
+def test_host_verifier_matches_oracle_on_goldens():
+    from paper_2508_21393_b200.sumcheck import RoundPolynomial, SumcheckProof, verify_sumcheck
+
+    for c in load_golden("sumcheck.json")[:20]:
+        if c["degree"] == 0 and c["rounds"]:
+            continue
+        p = FIELDS[c["field"]]
+        terms = [zb.Term(co, tuple(f)) for co, f in c["terms"]]
+        proof = SumcheckProof([RoundPolynomial(tuple(r)) for r in c["rounds"]],
+                              tuple(c["final_values"]))
+        ok, pt, exp = verify_sumcheck(c["claimed_sum"], terms, c["degree"], len(c["rounds"]),
+                                      proof, Transcript.from_state(bytes.fromhex(c["state_before"]), p))
+        from oracle import sc
+
+        v = fs.FS(b"", p)
+        v.state = bytes.fromhex(c["state_before"])
+        ok2, pt2, exp2 = sc.verify(c["claimed_sum"], [(t.coefficient, t.factors) for t in terms],
+                                   c["degree"], len(c["rounds"]), c["rounds"], v)
+        assert (ok, pt, exp) == (ok2, pt2, exp2)
+
+
+REF_SRC = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference not mounted (GPU box)")
+def test_install_swaps_reference_import_sites():
+    import sys
+
+    sys.path.insert(0, REF_SRC)
+    try:
+        import zklora
+        import zklora.gadgets as zg
+        import zklora.lookup as zl
+        import zklora.sumcheck as zs
+
+        before = (zs.prove_sumcheck, zl.prove_lookup, zg.prove_matmul)
+        undo = zb.install(zklora)
+        try:
+            assert zs.prove_sumcheck is zb.prove_sumcheck
+            assert zl.prove_sumcheck is zb.prove_sumcheck
+            assert zg.prove_sumcheck is zb.prove_sumcheck
+            assert zl.prove_lookup is zb.prove_lookup
+            assert zg.prove_matmul is zb.prove_matmul
+            import zklora.pipeline as zp
+
+            assert zp.prove_matmul is zb.prove_matmul
+            from paper_2508_21393_b200 import sumcheck as bs
+
+            assert bs.TYPES["SumcheckProof"] is zs.SumcheckProof
+        finally:
+            undo()
+        assert (zs.prove_sumcheck, zl.prove_lookup, zg.prove_matmul) == before
+    finally:
+        sys.path.remove(REF_SRC)
