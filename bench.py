@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Benchmark: zkLoRA sumcheck prover throughput on B200 (BASELINE.json).
+
+Workload (BASELINE.json configs[1], "cfg2"): one LLaMA-2-7B-shaped LoRA
+projection, forward + backward, proven by the 8 zkMat sumchecks
+  Y1 = X W, Hw = X A_L, Y2 = H B_L, dX1 = dY W^T, Gw = dY B_L^T,
+  dX2 = G A_L^T, dA = X^T G, dB = H^T dY
+with X 2048x4096, W 4096x4096, A_L 4096x16, B_L 16x4096, dY 2048x4096
+(seeded synthetic int16 fixed point at scale 2^12: X ~ N(0,1), W, A_L,
+B_L ~ N(0, 0.02), dY ~ N(0, sigma=1e-2); H = round(X A_L / 2^12),
+G = round(dY B_L^T / 2^12); wide products exact int64).  232 rounds.
+One step = all 8 sumchecks (Fiat-Shamir transcript included), each in the
+reference's replicated-claim form (gadgets.py:241-251), bit-identical.
+
+metric: field-elem/s = sum over claims of k * 2^n (k = 4 tables,
+n = d0+d1+d2, the reference claim's size) / step time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+for _p in (ROOT, os.path.join(ROOT, "tests", "golden")):
+    if _p not in sys.path:
+        sys.path.insert(0, _p)
+
+import numpy as np  # noqa: E402
+
+METRIC = "sumcheck prover field-elem/s"
+BASELINE_METRIC = "sumcheck prover field-elem/s & LoRA-block proof s at 1/2/4/8 B200 vs CPU ref"
+UNIT = "field-elem/s"
+P_BIG = 0x73EDA753299D7D483339D80809A1D80553BDA402FFFE5BFEFFFFFFFF00000001
+WORKLOAD = "cfg2: LoRA projection LLaMA-2-7B shape fwd+bwd, 8 zkMat sumchecks (232 rounds)"
+CPU_SAMPLE = "reference-algorithm dense zkMat sumcheck (gadgets.py:241-251, sumcheck.py:98-130) " \
+             "on the (6,7,6) corner block X[:64,:128] W[:128,:64] of the cfg2 X.W claim"
+
+
+def round_half_away(a):
+    return np.sign(a) * np.floor(np.abs(a) + 0.5)
+
+
+def q16(a, scale=4096.0):
+    return np.clip(round_half_away(a * scale), -32768, 32767).astype(np.int16)
+
+
+def cfg2_host(seed):
+    g = np.random.Generator(np.random.PCG64(seed))
+    X = q16(g.standard_normal((2048, 4096)))
+    W = q16(g.normal(0.0, 0.02, (4096, 4096)))
+    AL = q16(g.normal(0.0, 0.02, (4096, 16)))
+    BL = q16(g.normal(0.0, 0.02, (16, 4096)))
+    dY = q16(g.normal(0.0, 1e-2, (2048, 4096)))
+    return X, W, AL, BL, dY
+
+
+def cfg2_claims(seed, device):
+    """Device-resident claims [(name, A, B, C, dims)] + host copies for e2e."""
+    import torch
+
+    X, W, AL, BL, dY = (torch.from_numpy(a).to(device) for a in cfg2_host(seed))
+
+    def exact(a, b):  # exact int64 product (|partial sums| < 2^53)
+        return torch.matmul(a.double(), b.double()).round().long()
+
+    def narrow(w):
+        return torch.clamp(torch.round(w.double() / 4096.0), -32768, 32767).short()
+
+    H = narrow(exact(X, AL))
+    G = narrow(exact(dY, BL.t()))
+    mats = [
+        ("Y1=X.W", X, W), ("Hw=X.A", X, AL), ("Y2=H.B", H, BL), ("dX1=dY.Wt", dY, W.t()),
+        ("Gw=dY.Bt", dY, BL.t()), ("dX2=G.At", G, AL.t()), ("dA=Xt.G", X.t(), G),
+        ("dB=Ht.dY", H.t(), dY),
+    ]
+    claims = []
+    for name, a, b in mats:
+        a = a.contiguous()
+        b = b.contiguous()
+        c = exact(a, b).contiguous()
+        dims = tuple((s - 1).bit_length() for s in (a.shape[0], a.shape[1], b.shape[1]))
+        claims.append((name, a, b, c, dims))
+    torch.cuda.synchronize()
+    return claims
+
+
+def elems_of(claims):
+    return sum(4 * (1 << sum(c[4])) for c in claims)
+
+
+def rounds_of(claims):
+    return sum(sum(c[4]) for c in claims)
+
+
+class MatvecTimer:
+    """CUDA-event brackets around every zkl_matvec launch on its stream."""
+
+    def __init__(self):
+        self.rec = []
+
+    def __call__(self, stream, nbytes):
+        import torch
+
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        self.rec.append((a, b, nbytes))
+        return b
+
+    def stats(self):
+        ms = [a.elapsed_time(b) for a, b, _ in self.rec]
+        by = [n for _, _, n in self.rec]
+        return ms, by
+
+
+def prove_step(claims, step_seed, DeviceMatrix, matmul_sumcheck, Transcript):
+    tr = Transcript(b"zklora-b200/bench", P_BIG, b"cfg2/%d" % step_seed)
+    finals = []
+    for name, a, b, c, dims in claims:
+        tr.append(b"gadget/tag", b"matmul")
+        tr.append(b"bench/claim", name.encode())
+        A = DeviceMatrix.from_int_tensor(a)
+        B = DeviceMatrix.from_int_tensor(b)
+        C = DeviceMatrix.from_int_tensor(c)
+        _, _, f = matmul_sumcheck(A, B, C, dims, tr)
+        finals.append(f)
+    return finals, tr.state
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.tmp = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.tmp, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        self.proc.wait()
+        self.tmp.flush()
+        with open(self.tmp.name) as fh:
+            rows = [r.strip().split(", ") for r in fh if r.strip()]
+        os.unlink(self.tmp.name)
+        sm, mx, reasons = [], 0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx = max(mx, float(r[1]))
+                for nm, v in zip(names, r[3:7]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_reference_sample(seed=0):
+    """The reference algorithm (oracle port) on a bounded sample; returns
+    (elements, seconds)."""
+    from oracle import fs, zkmat
+
+    X, W = cfg2_host(seed)[:2]
+    a = X[:64, :128].astype(np.int64)
+    b = W[:128, :64].astype(np.int64)
+    c = a @ b
+    p = P_BIG
+    A = [int(v) % p for v in a.reshape(-1)]
+    B = [int(v) % p for v in b.reshape(-1)]
+    C = [int(v) % p for v in c.reshape(-1)]
+    t0 = time.perf_counter()
+    zkmat.prove_dense(A, B, C, (6, 7, 6), fs.FS(b"cpu", p, b"sample"))
+    return 4 * (1 << 19), time.perf_counter() - t0
+
+
+def _pool_sample(i):
+    return cpu_reference_sample(i)
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm on all host cores."""
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    cores = os.cpu_count() or 1
+    with mp.Pool(cores) as pool:
+        for _ in range(args.warmup):
+            pool.map(_pool_sample, range(cores))
+        t0 = time.perf_counter()
+        elems = 0
+        for s in range(args.steps):
+            res = pool.map(_pool_sample, [1000 * s + i for i in range(cores)])
+            elems += sum(e for e, _ in res)
+        dt = time.perf_counter() - t0
+    value = elems / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u256-mod-p",
+        "data": "synthetic", "config": {"workload": WORKLOAD, "field": "BLS12-381 Fr"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": CPU_SAMPLE + " x %d processes per step" % cores},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2508_21393_b200 as zb
+    from paper_2508_21393_b200 import _native as N
+    from paper_2508_21393_b200 import gadgets as G
+    from paper_2508_21393_b200.gadgets import DeviceMatrix
+
+    lib = N.lib()
+    claims = cfg2_claims(1234 + rank, "cuda")
+    elems = elems_of(claims)
+    nrounds = rounds_of(claims)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for s in range(args.warmup):
+        prove_step(claims, s, DeviceMatrix, zb.matmul_sumcheck, zb.Transcript)
+
+    # ---- device-resident timing (value) ----
+    timer = MatvecTimer()
+    G.MATVEC_HOOK = timer
+    clocks = ClockSampler(local)
+    launches0 = lib.zkl_launch_count()
+    step_ms = []
+    barrier()
+    for s in range(args.steps):
+        flush.zero_()  # inputs (> 300 MB) exceed L2 anyway; flush between steps too
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        prove_step(claims, 100 + s, DeviceMatrix, zb.matmul_sumcheck, zb.Transcript)
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+    barrier()
+    launches = (lib.zkl_launch_count() - launches0) // args.steps
+    G.MATVEC_HOOK = None
+    clk = clocks.stop()
+    local_ms = sum(step_ms)
+    t = torch.tensor([local_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = elems * world / (total_ms / 1000.0 / args.steps)
+
+    # ---- dominant kernel roofline (zkl_matvec family, CUDA events) ----
+    mv_ms, mv_bytes = timer.stats()
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    avg_ms = sum(mv_ms) / max(len(mv_ms), 1)
+    avg_bytes = sum(mv_bytes) / max(len(mv_bytes), 1)
+    achieved = avg_bytes / (avg_ms / 1000.0) / 1e9 if avg_ms else 0.0
+    matvec_ms_per_step = sum(mv_ms) / args.steps
+
+    # ---- end-to-end through the public API from pinned host buffers ----
+    host = [(n, a.cpu().pin_memory(), b.cpu().pin_memory(), c.cpu().pin_memory(), d)
+            for n, a, b, c, d in claims]
+    dev_bufs = [(torch.empty_like(a, device="cuda"), torch.empty_like(b, device="cuda"),
+                 torch.empty_like(c, device="cuda")) for _, a, b, c, _ in host]
+    h2d = sum(a.numel() * a.element_size() + b.numel() * b.element_size()
+              + c.numel() * c.element_size() for _, a, b, c, _ in host)
+    d2h = sum(sum(d) * 4 * 32 + 4 * 32 for *_, d in host)  # round evals + finals
+    e2e_ms = []
+    barrier()
+    for s in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step_claims = []
+        for (n, a, b, c, d), (da, db, dc) in zip(host, dev_bufs):
+            da.copy_(a, non_blocking=True)
+            db.copy_(b, non_blocking=True)
+            dc.copy_(c, non_blocking=True)
+            step_claims.append((n, da, db, dc, d))
+        prove_step(step_claims, 200 + s, DeviceMatrix, zb.matmul_sumcheck, zb.Transcript)
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    barrier()
+    t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_value = elems * world / (float(t.item()) / 1000.0 / args.steps)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- parity: one full-size claim against the CPU oracle (outside timing) ----
+    parity = None
+    if not args.no_check:
+        from oracle import fs, zkmat
+
+        name, a, b, c, dims = claims[0]
+        tr1 = zb.Transcript(b"check", P_BIG, b"x")
+        r1 = zb.matmul_sumcheck(DeviceMatrix.from_int_tensor(a), DeviceMatrix.from_int_tensor(b),
+                                DeviceMatrix.from_int_tensor(c), dims, tr1)
+        tr2 = fs.FS(b"check", P_BIG, b"x")
+        r2 = zkmat.prove_factored(a.cpu().numpy().astype(np.int64).reshape(-1),
+                                  b.cpu().numpy().astype(np.int64).reshape(-1),
+                                  c.cpu().numpy().reshape(-1), dims, tr2)
+        ok = (r1[0] == r2[0] and tuple(r1[2]) == r2[1] and tr1.state == tr2.state)
+        parity = {"claim": name, "dims": list(dims), "bit_exact_vs_oracle": bool(ok)}
+
+    cpu = None
+    if not args.no_cpu:
+        el, sec = cpu_reference_sample(0)
+        cpu = {"value": el / sec, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": CPU_SAMPLE + " (%.1f s)" % sec}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u256-mod-p (BLS12-381 Fr)",
+        "data": "synthetic (seeded PCG64, int16 fixed point at 2^12)",
+        "config": {"workload": WORKLOAD, "field": "BLS12-381 Fr", "claims": len(claims),
+                   "rounds_per_step": nrounds, "field_elems_per_step": elems,
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "256 MB flush between steps; inputs > 300 MB"},
+        "baseline_metric": BASELINE_METRIC,
+        "proof_seconds_per_step": ms_per_step / 1000.0,
+        "roofline": {"kernel": "zkl_matvec (wide-accumulator int x Fr MLE partial evaluation)",
+                     "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None,
+                     "launches_per_step": len(mv_ms) // args.steps,
+                     "gpu_ms_per_step": matvec_ms_per_step,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "parity": parity,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

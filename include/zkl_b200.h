@@ -44,6 +44,8 @@ extern "C" {
 
 int zkl_abi_version(void);
 const char* zkl_last_error(void);
+/* number of CUDA kernels this library has launched in this process */
+uint64_t zkl_launch_count(void);
 /* bytes per stored element (32 or 8); <0 for an unknown field */
 int zkl_elem_bytes(int field);
 

@@ -23,7 +23,7 @@ EXPORTS = (
     "zkl_abi_version", "zkl_last_error", "zkl_elem_bytes", "zkl_to_mont", "zkl_from_mont",
     "zkl_lift", "zkl_eq_table", "zkl_fold", "zkl_axpy", "zkl_read", "zkl_dot",
     "zkl_sumcheck_round", "zkl_sumcheck_finish", "zkl_batch_inverse", "zkl_multiplicities",
-    "zkl_matvec", "zkl_expand", "zkl_lift_u32",
+    "zkl_matvec", "zkl_expand", "zkl_lift_u32", "zkl_launch_count",
 )
 
 
@@ -44,6 +44,7 @@ _vp, _u64, _i32, _i64p, _u8p = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, \
 
 _SIGS = {
     "zkl_abi_version": ([], ctypes.c_int),
+    "zkl_launch_count": ([], ctypes.c_uint64),
     "zkl_last_error": ([], ctypes.c_char_p),
     "zkl_elem_bytes": ([_i32], ctypes.c_int),
     "zkl_to_mont": ([_i32, _vp, _vp, _u64, _vp], ctypes.c_int),

@@ -82,6 +82,7 @@ int dot_impl(uint8_t* out, const void* a, const void* b, uint64_t n, cudaStream_
 extern "C" {
 
 int zkl_abi_version(void) { return 1; }
+uint64_t zkl_launch_count(void) { return g_launches; }
 const char* zkl_last_error(void) { return get_error(); }
 int zkl_elem_bytes(int field) {
   if (field == ZKL_FIELD_BLS12_381_FR) return 32;

@@ -116,7 +116,14 @@ const char* get_error();
     }                                                                          \
   } while (0)
 
-#define ZKL_LAUNCH_CHECK() ZKL_CUDA(cudaGetLastError())
+// every kernel launch is followed by exactly one ZKL_LAUNCH_CHECK, which also
+// counts it (zkl_launch_count, used by bench.py's gpu_launches)
+extern unsigned long long g_launches;
+#define ZKL_LAUNCH_CHECK()          \
+  do {                              \
+    ++::zkl::g_launches;            \
+    ZKL_CUDA(cudaGetLastError());   \
+  } while (0)
 
 // Per-device scratch arena (single owner, stream-ordered reuse).  Grows by
 // reallocating; callers must not hold pointers across zkl_* calls.

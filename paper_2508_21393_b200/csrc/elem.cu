@@ -15,6 +15,7 @@ namespace zkl {
 
 // ---------------------------------------------------------------------------
 // error + scratch
+unsigned long long g_launches = 0;
 static thread_local char g_err[512];
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -167,7 +168,9 @@ int op_eq_table(void* dst, const typename F::T* point, int m, cudaStream_t s) {
   T* hi = (T*)ws;
   T* lo = hi + (1ull << mh);
   k_eq_direct<F><<<grid_for(1ull << mh, 256), 256, 0, s>>>(hi, pt, 0, mh);
+  ZKL_LAUNCH_CHECK();
   k_eq_direct<F><<<grid_for(1ull << ml, 256), 256, 0, s>>>(lo, pt, mh, ml);
+  ZKL_LAUNCH_CHECK();
   k_eq_outer<F><<<grid_for(1ull << m, 256), 256, 0, s>>>(out, hi, lo, ml, 1ull << m);
   ZKL_LAUNCH_CHECK();
   return kOk;

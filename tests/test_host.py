@@ -22,7 +22,7 @@ from paper_2508_21393_b200.transcript import Transcript
 def _declared_symbols():
     with open(os.path.join(ROOT, "include", "zkl_b200.h")) as fh:
         text = fh.read()
-    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(zkl_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^(?:int|uint64_t|const char\*)\s+(zkl_\w+)\(", text, re.M)))
 
 
 def test_library_loads_and_exports_header_symbols():
