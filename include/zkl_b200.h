@@ -102,6 +102,27 @@ int zkl_sumcheck_round(int field, void* const* tables, int k, uint64_t size, int
                        const uint8_t* coeffs_canon, const uint8_t* post_add_canon,
                        const uint8_t* post_mul_canon, uint8_t* evals_out_host, void* stream);
 
+/* The whole of prove_sumcheck after _absorb_claim (sumcheck.py:108-130) with
+ * the native transcript: state_inout is the 64-byte transcript state
+ * (transcript.py:24-42), updated in place.  Per round: fused fold+eval, the
+ * (degree+1) evaluations appended under b"sumcheck/eval" (minimal LE ints),
+ * challenge b"sumcheck/round".  post_add_canon: num_vars scalars (one per
+ * round) or NULL; post_mul_canon: NULL = 1.  Outputs (canonical LE):
+ * rounds_out num_vars*(degree+1) scalars, point_out num_vars, finals_out k. */
+int zkl_sumcheck_prove(int field, void* const* tables, int k, int num_vars, int degree,
+                       int nterms, const int32_t* nfactors, const int32_t* factors,
+                       const uint8_t* coeffs_canon, const uint8_t* post_add_canon,
+                       const uint8_t* post_mul_canon, uint8_t* state_inout, uint8_t* rounds_out,
+                       uint8_t* point_out, uint8_t* finals_out, void* stream);
+
+/* Host SHAKE-256 (FIPS 202) and transcript primitives (transcript.py:13-42),
+ * exported for cross-checks against hashlib; no GPU involved. */
+int zkl_shake256(const uint8_t* in, uint64_t len, uint8_t* out, uint64_t outlen);
+int zkl_transcript_append(uint8_t* state_inout, const uint8_t* label, uint64_t label_len,
+                          const uint8_t* data, uint64_t data_len);
+int zkl_transcript_challenge(int field, uint8_t* state_inout, const char* label,
+                             uint8_t* out_canon);
+
 /* After the last round: final_values[j] = fold(tables[j], r_last)[0]
  * (sumcheck.py:129-130), tables of size 2. */
 int zkl_sumcheck_finish(int field, void* const* tables, int k, const uint8_t* r_last_canon,

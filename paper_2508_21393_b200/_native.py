@@ -23,7 +23,8 @@ EXPORTS = (
     "zkl_abi_version", "zkl_last_error", "zkl_elem_bytes", "zkl_to_mont", "zkl_from_mont",
     "zkl_lift", "zkl_eq_table", "zkl_fold", "zkl_axpy", "zkl_read", "zkl_dot",
     "zkl_sumcheck_round", "zkl_sumcheck_finish", "zkl_batch_inverse", "zkl_multiplicities",
-    "zkl_matvec", "zkl_expand", "zkl_lift_u32", "zkl_launch_count",
+    "zkl_matvec", "zkl_expand", "zkl_lift_u32", "zkl_launch_count", "zkl_sumcheck_prove",
+    "zkl_shake256", "zkl_transcript_append", "zkl_transcript_challenge",
 )
 
 
@@ -61,6 +62,12 @@ _SIGS = {
         [_i32, _vp, _i32, _u64, _i32, _u8p, _i32, _i32, _vp, _vp, _u8p, _u8p, _u8p, _vp, _vp],
         ctypes.c_int),
     "zkl_sumcheck_finish": ([_i32, _vp, _i32, _u8p, _vp, _vp], ctypes.c_int),
+    "zkl_sumcheck_prove": (
+        [_i32, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _u8p, _u8p, _u8p, _vp, _vp, _vp, _vp,
+         _vp], ctypes.c_int),
+    "zkl_shake256": ([_u8p, _u64, _vp, _u64], ctypes.c_int),
+    "zkl_transcript_append": ([_vp, _u8p, _u64, _u8p, _u64], ctypes.c_int),
+    "zkl_transcript_challenge": ([_i32, _vp, _u8p, _vp], ctypes.c_int),
     "zkl_batch_inverse": ([_i32, _vp, _vp, _u64, _u8p, _i64p, _vp], ctypes.c_int),
     "zkl_multiplicities": ([_i32, _vp, _u64, _vp, _u64, _vp, _i64p, _vp], ctypes.c_int),
     "zkl_matvec": ([_i32, _i32, _vp, _u64, _u64, _i32, _vp, _vp, _vp], ctypes.c_int),

@@ -18,7 +18,8 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libzkl_b200.so")
 BUILD = os.path.join(ROOT, "build", "zkl")
 
-SOURCES = ["elem.cu", "sumcheck.cu", "inverse.cu", "lookup.cu", "matvec.cu", "capi.cu"]
+SOURCES = ["elem.cu", "sumcheck.cu", "persistent.cu", "inverse.cu", "lookup.cu", "matvec.cu", "transcript.cu",
+           "capi.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

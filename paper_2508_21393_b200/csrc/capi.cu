@@ -1,8 +1,11 @@
 // extern "C" entry points (declared in include/zkl_b200.h): argument
 // checking, canonical <-> Montgomery scalar conversion on the host, dispatch
 // on the field id.
+#include <vector>
+
 #include "../../include/zkl_b200.h"
 #include "ops.cuh"
+#include "transcript.cuh"
 
 using namespace zkl;
 
@@ -56,6 +59,37 @@ int sumcheck_round(void* const* tables, int k, uint64_t size, int fold, const ui
   post.mul = post_mul ? scalar<F>(post_mul) : F::one();
   typename F::T r = fold ? scalar<F>(r_prev) : F::zero();
   return op_sumcheck_round<F>(tables, k, size, fold != 0, r, tm, post, evals_out, s);
+}
+
+template <class F>
+int sumcheck_prove(void* const* tables, int k, int num_vars, int degree, int nterms,
+                   const int32_t* nfactors, const int32_t* factors, const uint8_t* coeffs,
+                   const uint8_t* post_add, const uint8_t* post_mul, uint8_t* state,
+                   uint8_t* rounds_out, uint8_t* point_out, uint8_t* finals_out, cudaStream_t s) {
+  if (nterms < 0 || nterms > kMaxTerms || num_vars < 0 || num_vars > 63) {
+    set_error("sumcheck_prove: bad nterms/num_vars");
+    return kErrArg;
+  }
+  int err;
+  Terms<F> tm = make_terms<F>(degree, nterms, nfactors, factors, coeffs, k, &err);
+  if (err) { set_error("sumcheck_prove: bad term factors"); return kErrArg; }
+  std::vector<typename F::T> adds;
+  if (post_add) {
+    adds.resize(num_vars > 0 ? num_vars : 1);
+    for (int j = 0; j < num_vars; j++) adds[j] = load_canon<F>(post_add + (size_t)j * F::kBytes);
+  }
+  typename F::T mul = post_mul ? scalar<F>(post_mul) : F::one();
+  return op_sumcheck_prove<F>(tables, k, num_vars, tm, post_add ? adds.data() : nullptr, mul,
+                              state, rounds_out, point_out, finals_out, s);
+}
+
+template <class F>
+int transcript_challenge(uint8_t* state, const char* label, uint8_t* out) {
+  HostTranscript tr;
+  memcpy(tr.state, state, 64);
+  challenge_canon<F>(tr, label, out);
+  memcpy(state, tr.state, 64);
+  return kOk;
 }
 
 template <class F>
@@ -149,6 +183,31 @@ int zkl_sumcheck_round(int field, void* const* tables, int k, uint64_t size, int
   D(field, sumcheck_round<F>(tables, k, size, fold, r_prev_canon, degree, nterms, nfactors,
                              factors, coeffs_canon, post_add_canon, post_mul_canon,
                              evals_out_host, (cudaStream_t)stream));
+}
+int zkl_sumcheck_prove(int field, void* const* tables, int k, int num_vars, int degree,
+                       int nterms, const int32_t* nfactors, const int32_t* factors,
+                       const uint8_t* coeffs_canon, const uint8_t* post_add_canon,
+                       const uint8_t* post_mul_canon, uint8_t* state_inout, uint8_t* rounds_out,
+                       uint8_t* point_out, uint8_t* finals_out, void* stream) {
+  D(field, sumcheck_prove<F>(tables, k, num_vars, degree, nterms, nfactors, factors,
+                             coeffs_canon, post_add_canon, post_mul_canon, state_inout,
+                             rounds_out, point_out, finals_out, (cudaStream_t)stream));
+}
+int zkl_shake256(const uint8_t* in, uint64_t len, uint8_t* out, uint64_t outlen) {
+  shake256(in, (size_t)len, out, (size_t)outlen);
+  return kOk;
+}
+int zkl_transcript_append(uint8_t* state_inout, const uint8_t* label, uint64_t label_len,
+                          const uint8_t* data, uint64_t data_len) {
+  HostTranscript tr;
+  memcpy(tr.state, state_inout, 64);
+  tr.append((const char*)label, (size_t)label_len, data, (size_t)data_len);
+  memcpy(state_inout, tr.state, 64);
+  return kOk;
+}
+int zkl_transcript_challenge(int field, uint8_t* state_inout, const char* label,
+                             uint8_t* out_canon) {
+  D(field, transcript_challenge<F>(state_inout, label, out_canon));
 }
 int zkl_sumcheck_finish(int field, void* const* tables, int k, const uint8_t* r_last_canon,
                         uint8_t* finals_out_host, void* stream) {

@@ -39,6 +39,7 @@ ZKL_D fr_t ld_cg(const fr_t* p) {
   return r;
 }
 ZKL_D uint64_t ld_cg(const uint64_t* p) { return __ldcg(p); }
+ZKL_D unsigned ld_cg(const unsigned* p) { return __ldcg(p); }
 
 // ---- shuffles -----------------------------------------------------------------
 ZKL_D fr_t shfl_down(const fr_t& x, int off) {
@@ -132,9 +133,27 @@ struct Scratch {
   size_t bytes = 0;
   void* pinned = nullptr;  // small pinned host staging buffer
   size_t pinned_bytes = 0;
+  void* fixed = nullptr;   // 4 KB device block, zeroed once: round ticket, flags
 };
 Scratch& scratch_for_current_device();
 int scratch_reserve(size_t bytes, void** out, cudaStream_t s);
 int pinned_reserve(size_t bytes, void** out);
+// fixed device words (zero-initialised once per device)
+int fixed_words(void** out);
+constexpr size_t kFixedTicket = 0;    // u32, k_round last-block ticket (self-resetting)
+constexpr size_t kFixedFail = 64;     // u32, persistent-kernel failure flag
+constexpr size_t kFixedRbuf = 128;    // one field element, broadcast challenge
+
+// Host <-> device mailbox in mapped pinned memory (persistent sumcheck).
+struct alignas(64) Mailbox {
+  volatile uint32_t ev_seq;  // device -> host: evaluations of round ev_seq-1 ready
+  volatile uint32_t ch_seq;  // host -> device: challenge of round ch_seq-1 ready
+  volatile uint32_t abort;   // host -> device
+  volatile uint32_t status;  // device -> host: 1 = timed out waiting
+  volatile uint8_t evals[8 * 32];  // raw sums (Montgomery), up to 8
+  volatile uint8_t chal[32];
+  volatile uint8_t finals[8 * 32];
+};
+int mailbox_for_current_device(Mailbox** host, Mailbox** dev);
 
 }  // namespace zkl

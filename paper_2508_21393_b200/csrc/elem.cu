@@ -50,6 +50,36 @@ int scratch_reserve(size_t bytes, void** out, cudaStream_t s) {
   *out = a.ptr;
   return kOk;
 }
+int fixed_words(void** out) {
+  Scratch& a = scratch_for_current_device();
+  if (!a.fixed) {
+    ZKL_CUDA(cudaMalloc(&a.fixed, 4096));
+    ZKL_CUDA(cudaMemset(a.fixed, 0, 4096));
+  }
+  *out = a.fixed;
+  return kOk;
+}
+static std::map<int, std::pair<Mailbox*, Mailbox*>>& mailboxes() {
+  static std::map<int, std::pair<Mailbox*, Mailbox*>> m;
+  return m;
+}
+int mailbox_for_current_device(Mailbox** host, Mailbox** dev) {
+  int d = 0;
+  cudaGetDevice(&d);
+  auto& e = mailboxes()[d];
+  if (!e.first) {
+    void* h = nullptr;
+    ZKL_CUDA(cudaHostAlloc(&h, sizeof(Mailbox), cudaHostAllocMapped | cudaHostAllocPortable));
+    memset(h, 0, sizeof(Mailbox));
+    void* dp = nullptr;
+    ZKL_CUDA(cudaHostGetDevicePointer(&dp, h, 0));
+    e.first = (Mailbox*)h;
+    e.second = (Mailbox*)dp;
+  }
+  *host = e.first;
+  *dev = e.second;
+  return kOk;
+}
 int pinned_reserve(size_t bytes, void** out) {
   Scratch& a = scratch_for_current_device();
   if (bytes > a.pinned_bytes) {

@@ -257,7 +257,7 @@ struct Fr255 {
     for (int j = 0; j < 8; j++) t[j] = t[j + 1];
     t[8] = 0;
   }
-  ZKL_D static T mul(const T& a, const T& b) {
+  ZKL_D static T mul_inl(const T& a, const T& b) {
     uint32_t t[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 8; i++) cios_step(t, a, b.v[i]);
@@ -266,11 +266,36 @@ struct Fr255 {
     for (int i = 0; i < 8; i++) r.v[i] = t[i];
     return reduce_once(r);
   }
+  // Compact form used everywhere: the outer CIOS loop stays rolled (the next
+  // limb of b is rotated into place, so nothing is dynamically indexed).  A
+  // fully unrolled multiply is ~300 SASS instructions (~5 KB); inlining that
+  // at every call site overflows the instruction cache, which dominated the
+  // latency-bound single-warp stretches of a round ("I-cache").
+  static __device__ __noinline__ T mul(const T& a, const T& b) { return mul_inl(a, b); }
+  // two independent products with interleaved carry chains (ILP 2), one call
+  static __device__ __noinline__ void mul2(const T& a, const T& b, const T& c, const T& d,
+                                           T& ab, T& cd) {
+    uint32_t t[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, u[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      cios_step(t, a, b.v[i]);
+      cios_step(u, c, d.v[i]);
+    }
+    T r, s;
+#pragma unroll
+    for (int i = 0; i < 8; i++) { r.v[i] = t[i]; s.v[i] = u[i]; }
+    ab = reduce_once(r);
+    cd = reduce_once(s);
+  }
 #else
   static T reduce_once(const T& a) { return geq_p_portable(a) ? sub_p_portable(a) : a; }
   static T add(const T& a, const T& b) { return add_portable(a, b); }
   static T sub(const T& a, const T& b) { return sub_portable(a, b); }
   static T mul(const T& a, const T& b) { return mul_portable(a, b); }
+  static void mul2(const T& a, const T& b, const T& c, const T& d, T& ab, T& cd) {
+    ab = mul_portable(a, b);
+    cd = mul_portable(c, d);
+  }
 #endif
 
   ZKL_HD static T neg(const T& a) { return sub(zero(), a); }
@@ -317,6 +342,10 @@ struct M61 {
     uint64_t r = (lo & P) + ((lo >> 61) | (hi << 3));
     r = (r & P) + (r >> 61);
     return r >= P ? r - P : r;
+  }
+  ZKL_HD static void mul2(T a, T b, T c, T d, T& ab, T& cd) {
+    ab = mul(a, b);
+    cd = mul(c, d);
   }
   ZKL_HD static T to_mont(T a) { return a; }
   ZKL_HD static T from_mont(T a) { return a; }

@@ -50,6 +50,11 @@ int op_sumcheck_round(void* const* tables, int k, uint64_t size, bool fold,
                       typename F::T r_prev, const Terms<F>& terms, const Post<F>& post,
                       uint8_t* evals_host, cudaStream_t s);
 template <class F>
+int op_sumcheck_prove(void* const* tables, int k, int num_vars, const Terms<F>& tm,
+                      const typename F::T* post_add, const typename F::T& post_mul,
+                      uint8_t* state, uint8_t* rounds_out, uint8_t* point_out,
+                      uint8_t* finals_out, cudaStream_t s);
+template <class F>
 int op_sumcheck_finish(void* const* tables, int k, typename F::T r, uint8_t* finals_host,
                        cudaStream_t s);
 

@@ -231,10 +231,9 @@ def matmul_sumcheck(A, B, C, dims, tr):
     cu = _matvec(C, E_ru, True, spec)
     kappa = D.dot(cu, E_v, spec, D2)
     if d1:
-        def post_w(j):
-            return (cneg * pow(2, d1 - j - 1, p) % p * kappa % p, e_hat)
-
-        rounds_w, pt_w, fin_w = run_rounds(spec, [a, bv], d1, [(1, (0, 1))], 3, tr, post_w)
+        adds = [cneg * pow(2, d1 - j - 1, p) % p * kappa % p for j in range(d1)]
+        rounds_w, pt_w, fin_w = run_rounds(spec, [a, bv], d1, [(1, (0, 1))], 3, tr,
+                                           post_add=adds, post_mul=e_hat)
         alpha_s = fin_w[0]
     else:
         rounds_w, pt_w, alpha_s = [], [], D.read_scalar(a, spec)
@@ -245,7 +244,7 @@ def matmul_sumcheck(A, B, C, dims, tr):
     if d2:
         rounds_v, pt_v, fin_v = run_rounds(
             spec, [E_v, bw, cu], d2, [(alpha_s, (0, 1)), (cneg, (0, 2))], 3, tr,
-            lambda j: (0, e_hat))
+            post_mul=e_hat)
         ev, bw_f, cu_f = fin_v
     else:
         rounds_v, pt_v = [], []

@@ -114,12 +114,37 @@ class _TermArgs:
         self.coeffs = D.scalars_bytes([c for c, _ in terms], spec) or b"\0" * spec.nbytes
 
 
-def run_rounds(spec, tables, num_vars, terms, degree, tr, post=None, emit=True):
+def _native_transcript(tr, spec):
+    """True when `tr` is a reference-semantics Transcript whose state the
+    native driver can advance (this package's or zklora's own class)."""
+    st = getattr(tr, "state", None)
+    if not isinstance(st, (bytes, bytearray)) or len(st) != 64:
+        return False
+    if getattr(tr, "modulus", None) != spec.modulus or NATIVE_TRANSCRIPT is False:
+        return False
+    app = getattr(type(tr), "append", None)
+    from .transcript import Transcript
+
+    if app is Transcript.append:
+        return True
+    return (getattr(app, "__qualname__", "") == "Transcript.append"
+            and type(tr).__module__.endswith("transcript"))
+
+
+NATIVE_TRANSCRIPT = True  # tests flip this to exercise the per-round host path
+
+
+def _decode(raw, nb, count):
+    return [int.from_bytes(raw[nb * i: nb * i + nb], "little") for i in range(count)]
+
+
+def run_rounds(spec, tables, num_vars, terms, degree, tr, post_add=None, post_mul=None):
     """Run every round of a device-resident claim.
 
     tables: list of device field vectors (each 2^num_vars entries, consumed).
     terms: list of (coefficient int, factor tuple).
-    post(j) -> (add, mul) ints or None: evals[x] = mul * (add + sum_x).
+    post_add: per-round ints or None; post_mul: int or None (1):
+    evals[x] = post_mul * (post_add[j] + sum_x).
     Returns (rounds as tuples, point, finals) with finals canonical ints.
     """
     lib = N.lib()
@@ -129,40 +154,46 @@ def run_rounds(spec, tables, num_vars, terms, degree, tr, post=None, emit=True):
     ta = _TermArgs(terms, spec)
     ptrs = (ctypes.c_void_p * k)(*[t.data_ptr() for t in tables])
     nb = spec.nbytes
-    evbuf = (ctypes.c_uint8 * (4 * nb))()
     strm = D.stream()
+    if num_vars == 0:
+        return [], [], [D.read_scalar(t, spec) for t in tables]
+    addb = D.scalars_bytes(post_add, spec) if post_add is not None else None
+    mulb = D.scalar_bytes(post_mul, spec) if post_mul is not None else None
+    if _native_transcript(tr, spec):
+        state = ctypes.create_string_buffer(bytes(tr.state), 64)
+        rbuf = (ctypes.c_uint8 * (num_vars * (degree + 1) * nb))()
+        pbuf = (ctypes.c_uint8 * (num_vars * nb))()
+        fbuf = (ctypes.c_uint8 * (k * nb))()
+        N.check(lib.zkl_sumcheck_prove(spec.fid, ptrs, k, num_vars, degree, ta.nt, ta.nf, ta.fi,
+                                       ta.coeffs, addb, mulb, state, rbuf, pbuf, fbuf, strm))
+        flat = _decode(bytes(rbuf), nb, num_vars * (degree + 1))
+        rounds = [tuple(flat[j * (degree + 1):(j + 1) * (degree + 1)]) for j in range(num_vars)]
+        tr.state = state.raw[:64]
+        log = getattr(tr, "log", None)
+        if log is not None:
+            log.extend((b"sumcheck/eval", (e.bit_length() + 7) // 8 or 1) for e in flat)
+        return rounds, _decode(bytes(pbuf), nb, num_vars), _decode(bytes(fbuf), nb, k)
+    # generic transcript object: per-round host loop
+    evbuf = (ctypes.c_uint8 * (4 * nb))()
     rounds, point = [], []
     size = 1 << num_vars
     r_prev = None
     for j in range(num_vars):
-        addb = mulb = None
-        if post is not None:
-            pa = post(j)
-            if pa is not None:
-                addb = D.scalar_bytes(pa[0], spec)
-                mulb = D.scalar_bytes(pa[1], spec)
+        ab = addb[j * nb:(j + 1) * nb] if addb is not None else None
         rb = D.scalar_bytes(r_prev, spec) if r_prev is not None else None
         N.check(lib.zkl_sumcheck_round(spec.fid, ptrs, k, size, 1 if rb else 0, rb, degree,
-                                       ta.nt, ta.nf, ta.fi, ta.coeffs, addb, mulb, evbuf, strm))
+                                       ta.nt, ta.nf, ta.fi, ta.coeffs, ab, mulb, evbuf, strm))
         if rb:
             size >>= 1
-        raw = bytes(evbuf)
-        evals = tuple(int.from_bytes(raw[nb * x: nb * x + nb], "little")
-                      for x in range(degree + 1))
+        evals = tuple(_decode(bytes(evbuf), nb, degree + 1))
         rounds.append(evals)
         for e in evals:
             tr.append(b"sumcheck/eval", e)
         r_prev = tr.challenge(b"sumcheck/round")
         point.append(r_prev)
-    if num_vars == 0:
-        finals = [D.read_scalar(t, spec) for t in tables]
-    else:
-        fin = (ctypes.c_uint8 * (k * nb))()
-        N.check(lib.zkl_sumcheck_finish(spec.fid, ptrs, k, D.scalar_bytes(r_prev, spec), fin,
-                                        strm))
-        raw = bytes(fin)
-        finals = [int.from_bytes(raw[nb * j: nb * j + nb], "little") for j in range(k)]
-    return rounds, point, finals
+    fin = (ctypes.c_uint8 * (k * nb))()
+    N.check(lib.zkl_sumcheck_finish(spec.fid, ptrs, k, D.scalar_bytes(r_prev, spec), fin, strm))
+    return rounds, point, _decode(bytes(fin), nb, k)
 
 
 def prove_sumcheck(claim, tr):

@@ -103,7 +103,11 @@ def test_eq_table_large_two_level(field):
 # --- sumcheck ----------------------------------------------------------------
 
 
-def test_sumcheck_golden():
+@pytest.mark.parametrize("native", [True, False])
+def test_sumcheck_golden(native, monkeypatch):
+    from paper_2508_21393_b200 import sumcheck as S
+
+    monkeypatch.setattr(S, "NATIVE_TRANSCRIPT", native)
     for c in load_golden("sumcheck.json"):
         p = FIELDS[c["field"]]
         t = _tr(c["state_before"], p)

@@ -70,6 +70,45 @@ def test_transcript_matches_golden_streams():
         assert [x[1] for x in t.log] == [x[1] for x in t.log]
 
 
+def test_native_shake256_matches_hashlib():
+    import ctypes
+    import hashlib
+    import random
+
+    lib = N.load()
+    rnd = random.Random(4)
+    for n in list(range(0, 300)) + [1000, 4096]:
+        msg = bytes(rnd.randrange(256) for _ in range(n))
+        for outlen in (64, 200):
+            out = (ctypes.c_uint8 * outlen)()
+            lib.zkl_shake256(msg, n, out, outlen)
+            assert bytes(out) == hashlib.shake_256(msg).digest(outlen), (n, outlen)
+
+
+@pytest.mark.parametrize("field", ["big", "test"])
+def test_native_transcript_matches_python(field):
+    import ctypes
+    import random
+
+    p = FIELDS[field]
+    lib = N.load()
+    rnd = random.Random(9)
+    py = Transcript(b"native", p, b"seed")
+    st = ctypes.create_string_buffer(py.state, 64)
+    nb = 32 if field == "big" else 8
+    for i in range(200):
+        label = b"lbl/%d" % rnd.randrange(1000)
+        if rnd.random() < 0.6:
+            data = rnd.randrange(p).to_bytes(nb, "little").rstrip(b"\0") or b"\0"
+            py.append(label, int.from_bytes(data, "little"))
+            lib.zkl_transcript_append(st, label, len(label), data, len(data))
+        else:
+            out = (ctypes.c_uint8 * nb)()
+            lib.zkl_transcript_challenge(0 if field == "big" else 1, st, label, out)
+            assert int.from_bytes(bytes(out), "little") == py.challenge(label)
+        assert st.raw[:64] == py.state
+
+
 def test_transcript_resume_and_fork():
     a = fs.FS(b"d", P_BIG, b"s")
     a.append(b"x", 77)
