@@ -157,14 +157,25 @@ struct PointArg {
 template <class F>
 __global__ void k_eq_direct(typename F::T* dst, PointArg<F> pt, int off, int m) {
   uint64_t n = 1ull << m;
+  // two interleaved product chains (first / second half of the coordinates)
+  // halve the dependent-multiply latency of this latency-bound kernel
+  const int mh = m / 2;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    typename F::T acc = F::one();
-    for (int j = 0; j < m; j++) {
-      bool bit = (i >> (m - 1 - j)) & 1;
-      acc = F::mul(acc, bit ? pt.r[off + j] : pt.omr[off + j]);
+    typename F::T a = F::one(), b = F::one();
+    int j = 0;
+    for (; j < mh; j++) {
+      const int k = mh + j;
+      const bool ba = (i >> (m - 1 - j)) & 1, bb = (i >> (m - 1 - k)) & 1;
+      F::mul2(a, ba ? pt.r[off + j] : pt.omr[off + j], b, bb ? pt.r[off + k] : pt.omr[off + k],
+              a, b);
     }
-    dst[i] = acc;
+    if (2 * mh < m) {  // odd m: last coordinate
+      const int k = m - 1;
+      const bool bb = (i >> (m - 1 - k)) & 1;
+      b = F::mul(b, bb ? pt.r[off + k] : pt.omr[off + k]);
+    }
+    dst[i] = F::mul(a, b);
   }
 }
 template <class F>

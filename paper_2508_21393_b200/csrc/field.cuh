@@ -271,27 +271,38 @@ struct Fr255 {
   // fully unrolled multiply is ~300 SASS instructions (~5 KB); inlining that
   // at every call site overflows the instruction cache, which dominated the
   // latency-bound single-warp stretches of a round ("I-cache").
-  static __device__ __noinline__ T mul(const T& a, const T& b) { return mul_inl(a, b); }
+  // Arguments and results travel BY VALUE: with references the ABI spills
+  // them (and any kernel-parameter struct they point into) to local memory.
+  static __device__ __noinline__ T mul(T a, T b) { return mul_inl(a, b); }
+  struct Pair {
+    T x, y;
+  };
   // two independent products with interleaved carry chains (ILP 2), one call
-  static __device__ __noinline__ void mul2(const T& a, const T& b, const T& c, const T& d,
-                                           T& ab, T& cd) {
+  static __device__ __noinline__ Pair mul2_call(T a, T b, T c, T d) {
     uint32_t t[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, u[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 8; i++) {
       cios_step(t, a, b.v[i]);
       cios_step(u, c, d.v[i]);
     }
-    T r, s;
+    Pair p;
 #pragma unroll
-    for (int i = 0; i < 8; i++) { r.v[i] = t[i]; s.v[i] = u[i]; }
-    ab = reduce_once(r);
-    cd = reduce_once(s);
+    for (int i = 0; i < 8; i++) { p.x.v[i] = t[i]; p.y.v[i] = u[i]; }
+    p.x = reduce_once(p.x);
+    p.y = reduce_once(p.y);
+    return p;
+  }
+  ZKL_D static void mul2(const T& a, const T& b, const T& c, const T& d, T& ab, T& cd) {
+    Pair p = mul2_call(a, b, c, d);
+    ab = p.x;
+    cd = p.y;
   }
 #else
   static T reduce_once(const T& a) { return geq_p_portable(a) ? sub_p_portable(a) : a; }
   static T add(const T& a, const T& b) { return add_portable(a, b); }
   static T sub(const T& a, const T& b) { return sub_portable(a, b); }
   static T mul(const T& a, const T& b) { return mul_portable(a, b); }
+  static T mul_inl(const T& a, const T& b) { return mul_portable(a, b); }
   static void mul2(const T& a, const T& b, const T& c, const T& d, T& ab, T& cd) {
     ab = mul_portable(a, b);
     cd = mul_portable(c, d);

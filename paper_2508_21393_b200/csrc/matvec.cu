@@ -127,161 +127,236 @@ ZKL_D fr_t reduce_wide(const Wide<W>& a) {
 }
 
 // ---------------------------------------------------------------------------
-// accumulation policies
-struct AccI16 {  // Fr255, int16 entries, offset 2^15
-  using M = int16_t;
-  Wide<10> a;
-  ZKL_D void init() {
+// accumulation policies.  Signed integer entries use sign-magnitude: the
+// shared x chunk is staged twice, as x and p - x, and every entry s picks
+// (|s|, s < 0 ? p - x : x), so the wide accumulator only ever adds.
+template <class F, class MT>
+struct Mac;
+
+template <>
+struct Mac<Fr255, int16_t> {
+  using Acc = Wide<10>;
+  static constexpr bool kSigned = true;
+  ZKL_D static void init(Acc& a) {
 #pragma unroll
     for (int i = 0; i < 10; i++) a.w[i] = 0;
   }
-  ZKL_D void mac(int16_t s, const fr_t& x) { mac10(a, (uint32_t)((int32_t)s + 32768), x); }
-  ZKL_D fr_t done() const { return reduce_wide<10>(a); }
-  ZKL_D static fr_t offset() { return Fr255::from_u32(1u << 15); }
+  ZKL_D static void mac(Acc& a, int16_t s, const fr_t* xp, const fr_t* xn) {
+    const bool neg = s < 0;
+    mac10(a, (uint32_t)(neg ? -(int32_t)s : (int32_t)s), neg ? *xn : *xp);
+  }
+  ZKL_D static fr_t done(const Acc& a) { return reduce_wide<10>(a); }
 };
-struct AccI32 {  // Fr255, int32 entries, offset 2^31
-  using M = int32_t;
-  Wide<10> a;
-  ZKL_D void init() {
+template <>
+struct Mac<Fr255, int32_t> {
+  using Acc = Wide<10>;
+  static constexpr bool kSigned = true;
+  ZKL_D static void init(Acc& a) {
 #pragma unroll
     for (int i = 0; i < 10; i++) a.w[i] = 0;
   }
-  ZKL_D void mac(int32_t s, const fr_t& x) { mac10(a, (uint32_t)s ^ 0x80000000u, x); }
-  ZKL_D fr_t done() const { return reduce_wide<10>(a); }
-  ZKL_D static fr_t offset() { return Fr255::from_u32(1u << 31); }
+  ZKL_D static void mac(Acc& a, int32_t s, const fr_t* xp, const fr_t* xn) {
+    const bool neg = s < 0;
+    mac10(a, neg ? (uint32_t)(-(int64_t)s) : (uint32_t)s, neg ? *xn : *xp);
+  }
+  ZKL_D static fr_t done(const Acc& a) { return reduce_wide<10>(a); }
 };
-struct AccI64 {  // Fr255, int64 entries, offset 2^63
-  using M = int64_t;
-  Wide<12> a;
-  ZKL_D void init() {
+template <>
+struct Mac<Fr255, int64_t> {
+  using Acc = Wide<12>;
+  static constexpr bool kSigned = true;
+  ZKL_D static void init(Acc& a) {
 #pragma unroll
     for (int i = 0; i < 12; i++) a.w[i] = 0;
   }
-  ZKL_D void mac(int64_t s, const fr_t& x) {
-    uint64_t u = (uint64_t)s ^ 0x8000000000000000ull;
+  ZKL_D static void mac(Acc& a, int64_t s, const fr_t* xp, const fr_t* xn) {
+    const bool neg = s < 0;
+    const uint64_t u = neg ? (uint64_t)(-(s + 1)) + 1u : (uint64_t)s;
+    const fr_t& x = neg ? *xn : *xp;
     mac12<0>(a, (uint32_t)u, x);
-    mac12<1>(a, (uint32_t)(u >> 32), x);
+    if (u >> 32) mac12<1>(a, (uint32_t)(u >> 32), x);
   }
-  ZKL_D fr_t done() const { return reduce_wide<12>(a); }
-  ZKL_D static fr_t offset() {
-    return Fr255::mul(Fr255::from_u32(1u << 31), Fr255::from_i64(1ll << 32));
+  ZKL_D static fr_t done(const Acc& a) { return reduce_wide<12>(a); }
+};
+template <class F, class MT>
+struct Mac {  // generic: field arithmetic per entry (M61 ints, field-valued matrices)
+  using T = typename F::T;
+  using Acc = T;
+  static constexpr bool kSigned = false;
+  ZKL_D static void init(Acc& a) { a = F::zero(); }
+  template <class V>
+  ZKL_D static T lift(const V& s) { return F::from_i64((int64_t)s); }
+  ZKL_D static T lift(const T& s) { return s; }
+  ZKL_D static void mac(Acc& a, const MT& s, const T* xp, const T*) {
+    a = F::add(a, F::mul(lift(s), *xp));
   }
-};
-template <class F, class I>
-struct AccField {  // generic: acc += lift(s) * x in the field
-  using M = I;
-  typename F::T a;
-  ZKL_D void init() { a = F::zero(); }
-  ZKL_D void mac(I s, const typename F::T& x) { a = F::add(a, F::mul(F::from_i64((int64_t)s), x)); }
-  ZKL_D typename F::T done() const { return a; }
-  ZKL_D static typename F::T offset() { return F::zero(); }
-};
-template <class F>
-struct AccElem {  // field-valued matrix
-  using M = typename F::T;
-  typename F::T a;
-  ZKL_D void init() { a = F::zero(); }
-  ZKL_D void mac(const typename F::T& s, const typename F::T& x) { a = F::add(a, F::mul(s, x)); }
-  ZKL_D typename F::T done() const { return a; }
-  ZKL_D static typename F::T offset() { return F::zero(); }
+  ZKL_D static T done(const Acc& a) { return a; }
 };
 
-// ---------------------------------------------------------------------------
-// y[r] = sum_c M[r, c] x[c] - off * S,  S = sum_c x[c];  one warp per row
-template <class F, class ACC>
-__global__ void __launch_bounds__(256)
-    k_rowmv(const typename ACC::M* M, uint64_t rows, uint64_t cols, const typename F::T* x,
-            const typename F::T* S, typename F::T* y) {
-  using T = typename F::T;
-  const int lane = threadIdx.x & 31;
-  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  const T corr = F::mul(*S, ACC::offset());
-  for (uint64_t r = warp; r < rows; r += nwarps) {
-    ACC acc;
-    acc.init();
-    const typename ACC::M* row = M + r * cols;
-    for (uint64_t c = lane; c < cols; c += 32) acc.mac(row[c], x[c]);
-    T f = warp_sum<F>(acc.done());
-    if (lane == 0) y[r] = F::sub(f, corr);
-  }
+// vector loads of VEC consecutive entries (16-byte aligned)
+template <class MT, int VEC>
+ZKL_D void load_vec(const MT* p, MT (&v)[VEC]) {
+  static_assert((sizeof(MT) * VEC) % 16 == 0, "vector width");
+  const uint4* q = reinterpret_cast<const uint4*>(p);
+  uint4* d = reinterpret_cast<uint4*>(v);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(MT) * VEC / 16); i++) d[i] = __ldcs(q + i);
 }
 
-// column products: partial[by][c] = sum_{r in chunk by} x[r] M[r, c]
-template <class F, class ACC>
+// stage x[lo, hi) (and p - x for signed entries) into shared memory
+template <class F, bool SIGNED>
+ZKL_D void stage_x(const typename F::T* x, uint64_t lo, uint64_t hi, typename F::T* xp,
+                   typename F::T* xn) {
+  for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const typename F::T v = x[i];
+    xp[i - lo] = v;
+    if (SIGNED) xn[i - lo] = F::neg(v);
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// row products: part[chunk][r] = sum_{c in chunk} M[r, c] x[c]; thread per row,
+// VEC entries of the row per vector load, x broadcast from shared memory.
+template <class F, class MT, int VEC>
 __global__ void __launch_bounds__(256)
-    k_colmv_part(const typename ACC::M* M, uint64_t rows, uint64_t cols, const typename F::T* x,
-                 int cw, uint64_t rch, typename F::T* part) {
+    k_mv_rows(const MT* M, uint64_t rows, uint64_t cols, const typename F::T* x, uint64_t cch,
+              typename F::T* part) {
   using T = typename F::T;
-  __shared__ T sm[256];
+  using P = Mac<F, MT>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* xp = reinterpret_cast<T*>(smem_raw);
+  T* xn = xp + cch;
+  const uint64_t c0 = blockIdx.y * cch;
+  const uint64_t c1 = c0 + cch < cols ? c0 + cch : cols;
+  stage_x<F, P::kSigned>(x, c0, c1, xp, xn);
+  const uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  typename P::Acc acc;
+  P::init(acc);
+  const MT* row = M + r * cols;
+  uint64_t c = c0;
+  for (; c + VEC <= c1; c += VEC) {
+    MT v[VEC];
+    if constexpr (VEC == 1)
+      v[0] = row[c];
+    else
+      load_vec<MT, VEC>(row + c, v);
+#pragma unroll
+    for (int k = 0; k < VEC; k++) P::mac(acc, v[k], xp + (c - c0) + k, xn + (c - c0) + k);
+  }
+  for (; c < c1; c++) P::mac(acc, row[c], xp + (c - c0), xn + (c - c0));
+  part[blockIdx.y * rows + r] = P::done(acc);
+}
+
+// column products: part[chunk][c] = sum_{r in chunk} x[r] M[r, c]; threads
+// over columns (coalesced rows of M), x[r] broadcast from shared memory; for
+// narrow matrices several row groups share a block and reduce in shared memory.
+template <class F, class MT>
+__global__ void __launch_bounds__(256)
+    k_mv_cols(const MT* M, uint64_t rows, uint64_t cols, const typename F::T* x, int cw,
+              uint64_t rch, typename F::T* part) {
+  using T = typename F::T;
+  using P = Mac<F, MT>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* xp = reinterpret_cast<T*>(smem_raw);
+  T* xn = xp + rch;                               // only staged for signed entries
+  T* red = xp + (P::kSigned ? 2 : 1) * rch;       // 256 entries
+  const uint64_t r0 = blockIdx.y * rch;
+  const uint64_t r1 = r0 + rch < rows ? r0 + rch : rows;
+  stage_x<F, P::kSigned>(x, r0, r1, xp, xn);
   const int tc = threadIdx.x % cw, rg = threadIdx.x / cw, ngrp = blockDim.x / cw;
   const uint64_t c = blockIdx.x * (uint64_t)cw + tc;
-  const uint64_t r0 = blockIdx.y * rch;
-  uint64_t r1 = r0 + rch;
-  if (r1 > rows) r1 = rows;
-  ACC acc;
-  acc.init();
+  typename P::Acc acc;
+  P::init(acc);
   if (c < cols)
-    for (uint64_t r = r0 + rg; r < r1; r += ngrp) acc.mac(M[r * cols + c], x[r]);
-  sm[threadIdx.x] = acc.done();
+    for (uint64_t r = r0 + rg; r < r1; r += ngrp) P::mac(acc, M[r * cols + c], xp + (r - r0), xn + (r - r0));
+  if (ngrp == 1) {
+    if (c < cols) part[blockIdx.y * cols + c] = P::done(acc);
+    return;
+  }
+  red[threadIdx.x] = P::done(acc);
   __syncthreads();
   if (rg == 0 && c < cols) {
-    T v = sm[tc];
-    for (int g = 1; g < ngrp; g++) v = F::add(v, sm[g * cw + tc]);
+    T v = red[tc];
+    for (int g = 1; g < ngrp; g++) v = F::add(v, red[g * cw + tc]);
     part[blockIdx.y * cols + c] = v;
   }
 }
 
-template <class F, class ACC>
-__global__ void k_colmv_sum(const typename F::T* part, uint64_t nchunks, uint64_t cols,
-                            const typename F::T* S, typename F::T* y) {
+// y[i] = sum_b part[b][i]; one warp per output
+template <class F>
+__global__ void __launch_bounds__(256)
+    k_mv_reduce(const typename F::T* part, uint64_t nchunks, uint64_t n, typename F::T* y) {
   using T = typename F::T;
-  const T corr = F::mul(*S, ACC::offset());
-  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < cols;
-       c += (uint64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = w; i < n; i += nw) {
     T v = F::zero();
-    for (uint64_t b = 0; b < nchunks; b++) v = F::add(v, part[b * cols + c]);
-    y[c] = F::sub(v, corr);
+    for (uint64_t b = lane; b < nchunks; b += 32) v = F::add(v, part[b * n + i]);
+    v = warp_sum<F>(v);
+    if (lane == 0) y[i] = v;
   }
 }
 
-template <class F, class ACC>
+template <class F, class MT>
 static int matvec_impl(const void* Mv, uint64_t rows, uint64_t cols, int transpose,
                        const void* xv, void* yv, cudaStream_t s) {
   using T = typename F::T;
-  const auto* M = (const typename ACC::M*)Mv;
+  const MT* M = (const MT*)Mv;
   const T* x = (const T*)xv;
   T* y = (T*)yv;
-  uint64_t xlen = transpose ? rows : cols;
-  // scratch: S (1) + partials
-  int cw = 1;
-  while (cw < 256 && (uint64_t)cw < cols) cw <<= 1;
-  uint64_t col_blocks = (cols + cw - 1) / cw;
-  uint64_t ngrp = 256 / cw;
-  uint64_t want_rb = (4ull * kSMs + col_blocks - 1) / col_blocks;
-  uint64_t max_rb = (rows + ngrp - 1) / ngrp;
-  uint64_t rb = want_rb < max_rb ? want_rb : max_rb;
-  if (rb < 1) rb = 1;
-  if (rb > 65535) rb = 65535;
-  uint64_t rch = (rows + rb - 1) / rb;
-  rb = (rows + rch - 1) / rch;
-  size_t need = sizeof(T) * (1 + (transpose ? rb * cols : 0)) + 64;
+  constexpr int kWant = 4 * kSMs;  // blocks to aim for
+  constexpr size_t kSmemCap = 40 * 1024;
+  const size_t per_x = sizeof(T) * (Mac<F, MT>::kSigned ? 2 : 1);
+  uint64_t nchunks, nout = transpose ? cols : rows;
   void* ws;
-  int rc = scratch_reserve(need, &ws, s);
-  if (rc) return rc;
-  T* S = (T*)ws;
-  T* part = S + 1;
-  rc = op_dot<F>(S, x, nullptr, xlen, s);
-  if (rc) return rc;
+  int rc;
   if (!transpose) {
-    unsigned grid = grid_for(rows * 32, 256, 8);
-    k_rowmv<F, ACC><<<grid, 256, 0, s>>>(M, rows, cols, x, S, y);
-  } else {
-    dim3 g((unsigned)col_blocks, (unsigned)rb);
-    k_colmv_part<F, ACC><<<g, 256, 0, s>>>(M, rows, cols, x, cw, rch, part);
+    constexpr int VEC = (sizeof(MT) >= 16) ? 1 : (int)(16 / sizeof(MT));
+    const bool aligned = ((uintptr_t)M % 16 == 0) && (cols % VEC == 0);
+    const uint64_t rb = (rows + 255) / 256;
+    uint64_t cs = (kWant + rb - 1) / rb;
+    const uint64_t max_cs = (cols + 63) / 64;
+    if (cs > max_cs) cs = max_cs;
+    if (cs < 1) cs = 1;
+    uint64_t cch = (cols + cs - 1) / cs;
+    const uint64_t cap = kSmemCap / per_x;
+    if (cch > cap) cch = cap;
+    cch = (cch + 7) / 8 * 8;
+    nchunks = (cols + cch - 1) / cch;
+    rc = scratch_reserve(nchunks * rows * sizeof(T), &ws, s);
+    if (rc) return rc;
+    const size_t smem = cch * per_x;
+    dim3 g((unsigned)rb, (unsigned)nchunks);
+    if (aligned && VEC > 1)
+      k_mv_rows<F, MT, VEC><<<g, 256, smem, s>>>(M, rows, cols, x, cch, (T*)ws);
+    else
+      k_mv_rows<F, MT, 1><<<g, 256, smem, s>>>(M, rows, cols, x, cch, (T*)ws);
     ZKL_LAUNCH_CHECK();
-    k_colmv_sum<F, ACC><<<grid_for(cols, 256), 256, 0, s>>>(part, rb, cols, S, y);
+  } else {
+    int cw = 1;
+    while (cw < 256 && (uint64_t)cw < cols) cw <<= 1;
+    const uint64_t cb = (cols + cw - 1) / cw;
+    const uint64_t ngrp = 256 / cw;
+    uint64_t rs = (kWant + cb - 1) / cb;
+    const uint64_t max_rs = (rows + ngrp * 4 - 1) / (ngrp * 4);
+    if (rs > max_rs) rs = max_rs;
+    if (rs < 1) rs = 1;
+    uint64_t rch = (rows + rs - 1) / rs;
+    const uint64_t cap = (kSmemCap - 256 * sizeof(T)) / per_x;
+    if (rch > cap) rch = cap;
+    nchunks = (rows + rch - 1) / rch;
+    if (nchunks > 65535) { set_error("matvec: too many row chunks"); return kErrArg; }
+    rc = scratch_reserve(nchunks * cols * sizeof(T), &ws, s);
+    if (rc) return rc;
+    const size_t smem = rch * per_x + 256 * sizeof(T);
+    dim3 g((unsigned)cb, (unsigned)nchunks);
+    k_mv_cols<F, MT><<<g, 256, smem, s>>>(M, rows, cols, x, cw, rch, (T*)ws);
+    ZKL_LAUNCH_CHECK();
   }
+  k_mv_reduce<F><<<grid_for(nout * 32, 256, 8), 256, 0, s>>>((const T*)ws, nchunks, nout, y);
   ZKL_LAUNCH_CHECK();
   return kOk;
 }
@@ -290,20 +365,11 @@ template <class F>
 int op_matvec(int mtype, const void* M, uint64_t rows, uint64_t cols, int transpose,
               const void* x, void* y, cudaStream_t s) {
   if (!rows || !cols) { set_error("matvec: empty matrix"); return kErrArg; }
-  if constexpr (F::kId == Fr255::kId) {
-    switch (mtype) {
-      case 0: return matvec_impl<F, AccElem<F>>(M, rows, cols, transpose, x, y, s);
-      case 1: return matvec_impl<F, AccI16>(M, rows, cols, transpose, x, y, s);
-      case 2: return matvec_impl<F, AccI32>(M, rows, cols, transpose, x, y, s);
-      case 3: return matvec_impl<F, AccI64>(M, rows, cols, transpose, x, y, s);
-    }
-  } else {
-    switch (mtype) {
-      case 0: return matvec_impl<F, AccElem<F>>(M, rows, cols, transpose, x, y, s);
-      case 1: return matvec_impl<F, AccField<F, int16_t>>(M, rows, cols, transpose, x, y, s);
-      case 2: return matvec_impl<F, AccField<F, int32_t>>(M, rows, cols, transpose, x, y, s);
-      case 3: return matvec_impl<F, AccField<F, int64_t>>(M, rows, cols, transpose, x, y, s);
-    }
+  switch (mtype) {
+    case 0: return matvec_impl<F, typename F::T>(M, rows, cols, transpose, x, y, s);
+    case 1: return matvec_impl<F, int16_t>(M, rows, cols, transpose, x, y, s);
+    case 2: return matvec_impl<F, int32_t>(M, rows, cols, transpose, x, y, s);
+    case 3: return matvec_impl<F, int64_t>(M, rows, cols, transpose, x, y, s);
   }
   set_error("matvec: bad matrix type %d", mtype);
   return kErrArg;

@@ -410,6 +410,31 @@ int op_sumcheck_prove(void* const* tables, int k, int num_vars, const Terms<F>& 
     return kErrArg;
   }
   if (num_vars == 0) return kOk;
+  // ZKL_NO_PERSISTENT=1: one launch per round (needed under profilers that
+  // serialise launches, e.g. ncu, which would starve the mailbox handshake)
+  static const bool no_persistent =
+      getenv("ZKL_NO_PERSISTENT") != nullptr ||
+      (getenv("CUDA_LAUNCH_BLOCKING") && getenv("CUDA_LAUNCH_BLOCKING")[0] == '1');
+  if (no_persistent) {
+    HostTranscript tr;
+    memcpy(tr.state, state, 64);
+    uint64_t size = 1ull << num_vars;
+    T r_prev = F::zero();
+    for (int j = 0; j < num_vars; j++) {
+      Post<F> post;
+      post.add = post_add ? post_add[j] : F::zero();
+      post.mul = post_mul;
+      uint8_t* rj = rounds_out + (size_t)j * (tm.degree + 1) * nb;
+      int rc = op_sumcheck_round<F>(tables, k, size, j > 0, r_prev, tm, post, rj, s);
+      if (rc) return rc;
+      if (j > 0) size >>= 1;
+      for (int x = 0; x <= tm.degree; x++) tr.append_elem("sumcheck/eval", rj + x * nb, nb);
+      challenge_canon<F>(tr, "sumcheck/round", point_out + (size_t)j * nb);
+      r_prev = load_canon<F>(point_out + (size_t)j * nb);
+    }
+    memcpy(state, tr.state, 64);
+    return op_sumcheck_finish<F>(tables, k, r_prev, finals_out, s);
+  }
   Mailbox* mb_host;
   Mailbox* mb_dev;
   int rc = mailbox_for_current_device(&mb_host, &mb_dev);
