@@ -410,10 +410,12 @@ int op_sumcheck_prove(void* const* tables, int k, int num_vars, const Terms<F>& 
     return kErrArg;
   }
   if (num_vars == 0) return kOk;
-  // ZKL_NO_PERSISTENT=1: one launch per round (needed under profilers that
-  // serialise launches, e.g. ncu, which would starve the mailbox handshake)
+  // ZKL_NO_PERSISTENT=1: one launch per round.  Also chosen automatically
+  // under tools that inject into the process and serialise / replay kernels
+  // (ncu, compute-sanitizer set CUDA_INJECTION64_PATH): a replayed kernel
+  // would spin on a mailbox the host never answers.
   static const bool no_persistent =
-      getenv("ZKL_NO_PERSISTENT") != nullptr ||
+      getenv("ZKL_NO_PERSISTENT") != nullptr || getenv("CUDA_INJECTION64_PATH") != nullptr ||
       (getenv("CUDA_LAUNCH_BLOCKING") && getenv("CUDA_LAUNCH_BLOCKING")[0] == '1');
   if (no_persistent) {
     HostTranscript tr;
