@@ -146,6 +146,22 @@ int zkl_multiplicities(int field, const void* secret, uint64_t d, const void* ta
 int zkl_matvec(int field, int mtype, const void* M, uint64_t rows, uint64_t cols, int transpose,
                const void* x, void* y, void* stream);
 
+/* The whole sumcheck of prove_matmul (gadgets.py:241-251) for C = A B:
+ * draws r_u (d0 coordinates, labels "matmul/r_u/<i>") and r_v (d2,
+ * "matmul/r_v/<i>"), absorbs the claim (sumcheck.py:90-95) and emits the
+ * d0+d1+d2 rounds of the reference's replicated-table claim
+ * (gadgets.py:210-251), bit-identical, without materialising the tables
+ * (factored prover).  A: 2^d0 x 2^d1, B: 2^d1 x 2^d2,
+ * C: 2^d0 x 2^d2, row-major device matrices of type ZKL_MT_* (integers are
+ * signed, value x mod p; ZKL_MT_FIELD = storage-form elements).
+ * state_inout: 64-byte transcript state (transcript.py:24-42), advanced in
+ * place.  Outputs (canonical LE): rounds_out (d0+d1+d2) x 4 scalars,
+ * point_out d0+d1+d2 scalars, finals_out 4 scalars (the four tables folded
+ * at the point: eq, A, B, C). */
+int zkl_matmul_prove(int field, int a_type, const void* A, int b_type, const void* B, int c_type,
+                     const void* C, int d0, int d1, int d2, uint8_t* state_inout,
+                     uint8_t* rounds_out, uint8_t* point_out, uint8_t* finals_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

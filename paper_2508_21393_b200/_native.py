@@ -8,7 +8,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libzkl_b200.so")
+LIB_PATH = os.environ.get("ZKL_LIB") or os.path.join(HERE, "libzkl_b200.so")
 
 ZKL_OK = 0
 ZKL_ERR_CUDA = -1
@@ -24,7 +24,7 @@ EXPORTS = (
     "zkl_lift", "zkl_eq_table", "zkl_fold", "zkl_axpy", "zkl_read", "zkl_dot",
     "zkl_sumcheck_round", "zkl_sumcheck_finish", "zkl_batch_inverse", "zkl_multiplicities",
     "zkl_matvec", "zkl_expand", "zkl_lift_u32", "zkl_launch_count", "zkl_sumcheck_prove",
-    "zkl_shake256", "zkl_transcript_append", "zkl_transcript_challenge",
+    "zkl_shake256", "zkl_transcript_append", "zkl_transcript_challenge", "zkl_matmul_prove",
 )
 
 
@@ -71,6 +71,9 @@ _SIGS = {
     "zkl_batch_inverse": ([_i32, _vp, _vp, _u64, _u8p, _i64p, _vp], ctypes.c_int),
     "zkl_multiplicities": ([_i32, _vp, _u64, _vp, _u64, _vp, _i64p, _vp], ctypes.c_int),
     "zkl_matvec": ([_i32, _i32, _vp, _u64, _u64, _i32, _vp, _vp, _vp], ctypes.c_int),
+    "zkl_matmul_prove": (
+        [_i32, _i32, _vp, _i32, _vp, _i32, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp],
+        ctypes.c_int),
 }
 
 

@@ -19,7 +19,7 @@ OUT = os.path.join(HERE, "libzkl_b200.so")
 BUILD = os.path.join(ROOT, "build", "zkl")
 
 SOURCES = ["elem.cu", "sumcheck.cu", "persistent.cu", "inverse.cu", "lookup.cu", "matvec.cu", "transcript.cu",
-           "capi.cu"]
+           "zkmat.cu", "capi.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -43,15 +43,15 @@ def _newer(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose=False, force=False, extra_flags=()):
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose=False, force=False, extra_flags=(), out=OUT, build_dir=BUILD):
+    os.makedirs(build_dir, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
     headers.append(os.path.join(ROOT, "include", "zkl_b200.h"))
     cc = nvcc()
     objs, jobs = [], []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        o = os.path.join(build_dir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _newer(o, [s] + headers):
             cmd = [cc, *NVCC_FLAGS, *extra_flags, "-c", s, "-o", o]
@@ -68,11 +68,11 @@ def build(verbose=False, force=False, extra_flags=()):
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         list(ex.map(run, jobs))
-    if jobs or force or _newer(OUT, objs):
+    if jobs or force or _newer(out, objs):
         cmd = [cc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs,
-               "-o", OUT, "-lcudart_static", "-lrt", "-lpthread", "-ldl"]
+               "-o", out, "-lcudart_static", "-lrt", "-lpthread", "-ldl"]
         run(cmd)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":

@@ -115,7 +115,7 @@ int dot_impl(uint8_t* out, const void* a, const void* b, uint64_t n, cudaStream_
 
 extern "C" {
 
-int zkl_abi_version(void) { return 1; }
+int zkl_abi_version(void) { return 2; }
 uint64_t zkl_launch_count(void) { return g_launches; }
 const char* zkl_last_error(void) { return get_error(); }
 int zkl_elem_bytes(int field) {
@@ -222,6 +222,12 @@ int zkl_batch_inverse(int field, void* dst, const void* src, uint64_t n, const u
 int zkl_multiplicities(int field, const void* secret, uint64_t d, const void* table, uint64_t n,
                        uint32_t* counts, int64_t* first_miss, void* stream) {
   D(field, op_multiplicities<F>(secret, d, table, n, counts, first_miss, (cudaStream_t)stream));
+}
+int zkl_matmul_prove(int field, int a_type, const void* A, int b_type, const void* B, int c_type,
+                     const void* C, int d0, int d1, int d2, uint8_t* state_inout,
+                     uint8_t* rounds_out, uint8_t* point_out, uint8_t* finals_out, void* stream) {
+  D(field, op_matmul_prove<F>(a_type, A, b_type, B, c_type, C, d0, d1, d2, state_inout,
+                              rounds_out, point_out, finals_out, (cudaStream_t)stream));
 }
 int zkl_matvec(int field, int mtype, const void* M, uint64_t rows, uint64_t cols, int transpose,
                const void* x, void* y, void* stream) {

@@ -134,25 +134,35 @@ struct Scratch {
   void* pinned = nullptr;  // small pinned host staging buffer
   size_t pinned_bytes = 0;
   void* fixed = nullptr;   // 4 KB device block, zeroed once: round ticket, flags
+  void* work = nullptr;    // gadget-driver vectors (zkmat.cu), separate from scratch
+  size_t work_bytes = 0;
 };
 Scratch& scratch_for_current_device();
 int scratch_reserve(size_t bytes, void** out, cudaStream_t s);
 int pinned_reserve(size_t bytes, void** out);
+// driver work arena (stream-ordered; grows by sync + realloc)
+int work_reserve(size_t bytes, void** out, cudaStream_t s);
 // fixed device words (zero-initialised once per device)
 int fixed_words(void** out);
 constexpr size_t kFixedTicket = 0;    // u32, k_round last-block ticket (self-resetting)
 constexpr size_t kFixedFail = 64;     // u32, persistent-kernel failure flag
-constexpr size_t kFixedRbuf = 128;    // one field element, broadcast challenge
+constexpr size_t kFixedPhaseTicket = 128;  // u32, persistent-kernel round ticket (self-resetting)
+constexpr size_t kFixedBcast = 256;   // challenge broadcast slot (tagged words, L2)
 
 // Host <-> device mailbox in mapped pinned memory (persistent sumcheck).
-struct alignas(64) Mailbox {
-  volatile uint32_t ev_seq;  // device -> host: evaluations of round ev_seq-1 ready
-  volatile uint32_t ch_seq;  // host -> device: challenge of round ch_seq-1 ready
-  volatile uint32_t abort;   // host -> device
-  volatile uint32_t status;  // device -> host: 1 = timed out waiting
-  volatile uint8_t evals[8 * 32];  // raw sums (Montgomery), up to 8
-  volatile uint8_t chal[32];
-  volatile uint8_t finals[8 * 32];
+// Every payload word travels as a TAGGED 64-bit word (u32 payload | seq <<
+// 32), written and read with single 8-byte accesses, so a reader knows a
+// message is complete when every word carries the expected sequence number:
+// no flag word and no system-scope fence on either side.
+constexpr int kMbEvalWords = 8 * 9;   // up to 8 outputs x 9 words (wide Fr sums)
+constexpr int kMbFinalWords = 8 * 8;  // up to 8 tables x 8 words
+struct alignas(128) Mailbox {
+  volatile uint64_t ev[kMbEvalWords];   // device -> host: round sums
+  volatile uint64_t ch[8];              // host -> device: challenge (storage form)
+  volatile uint64_t fin[kMbFinalWords]; // device -> host: final values (storage form)
+  volatile uint32_t abort;              // host -> device
+  volatile uint32_t status;             // device -> host: 1 = timed out waiting
+  volatile uint32_t seq;                // host-side sequence counter (not read by the device)
 };
 int mailbox_for_current_device(Mailbox** host, Mailbox** dev);
 

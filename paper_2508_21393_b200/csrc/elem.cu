@@ -50,6 +50,22 @@ int scratch_reserve(size_t bytes, void** out, cudaStream_t s) {
   *out = a.ptr;
   return kOk;
 }
+int work_reserve(size_t bytes, void** out, cudaStream_t s) {
+  Scratch& a = scratch_for_current_device();
+  if (bytes > a.work_bytes) {
+    if (a.work) {
+      ZKL_CUDA(cudaStreamSynchronize(s));
+      ZKL_CUDA(cudaFree(a.work));
+      a.work = nullptr;
+      a.work_bytes = 0;
+    }
+    size_t want = bytes < (1u << 20) ? (1u << 20) : bytes + bytes / 4;
+    ZKL_CUDA(cudaMalloc(&a.work, want));
+    a.work_bytes = want;
+  }
+  *out = a.work;
+  return kOk;
+}
 int fixed_words(void** out) {
   Scratch& a = scratch_for_current_device();
   if (!a.fixed) {

@@ -11,6 +11,17 @@
 #pragma once
 #include <stdint.h>
 
+// Montgomery multiplies keep their outer CIOS loop ROLLED by default: the
+// round kernels are latency-bound single passes, and a fully unrolled
+// multiply (~500 SASS instructions) re-fetched from L2 every round costs more
+// than the loop overhead.  -DZKL_MUL_UNROLLED restores full unrolling (the
+// throughput-bound kernels may prefer it).
+#if defined(ZKL_MUL_UNROLLED)
+#define ZKL_CIOS_LOOP _Pragma("unroll")
+#else
+#define ZKL_CIOS_LOOP _Pragma("unroll 1")
+#endif
+
 #if defined(__CUDACC__)
 #define ZKL_HD __host__ __device__ __forceinline__
 #define ZKL_D __device__ __forceinline__
@@ -257,10 +268,21 @@ struct Fr255 {
     for (int j = 0; j < 8; j++) t[j] = t[j + 1];
     t[8] = 0;
   }
-  ZKL_D static T mul_inl(const T& a, const T& b) {
-    uint32_t t[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  // b <- b rotated by one limb (rolled CIOS loops consume b.v[0] each step,
+  // so no limb is ever indexed dynamically)
+  ZKL_D static void rot(T& b) {
+    const uint32_t x = b.v[0];
 #pragma unroll
-    for (int i = 0; i < 8; i++) cios_step(t, a, b.v[i]);
+    for (int k = 0; k < 7; k++) b.v[k] = b.v[k + 1];
+    b.v[7] = x;
+  }
+  ZKL_D static T mul_inl(const T& a, T b) {
+    uint32_t t[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    ZKL_CIOS_LOOP
+    for (int i = 0; i < 8; i++) {
+      cios_step(t, a, b.v[0]);
+      rot(b);
+    }
     T r;
 #pragma unroll
     for (int i = 0; i < 8; i++) r.v[i] = t[i];
@@ -280,10 +302,12 @@ struct Fr255 {
   // two independent products with interleaved carry chains (ILP 2), one call
   static __device__ __noinline__ Pair mul2_call(T a, T b, T c, T d) {
     uint32_t t[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, u[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
+    ZKL_CIOS_LOOP
     for (int i = 0; i < 8; i++) {
-      cios_step(t, a, b.v[i]);
-      cios_step(u, c, d.v[i]);
+      cios_step(t, a, b.v[0]);
+      cios_step(u, c, d.v[0]);
+      rot(b);
+      rot(d);
     }
     Pair p;
 #pragma unroll
@@ -297,6 +321,93 @@ struct Fr255 {
     ab = p.x;
     cd = p.y;
   }
+  // three / four independent products with interleaved carry chains: the
+  // latency of one product for the price of one call (args stay in registers)
+  struct Triple {
+    T x, y, z;
+  };
+  static __device__ __noinline__ Triple mul3_call(T a0, T b0, T a1, T b1, T a2, T b2) {
+    uint32_t t[9] = {0}, u[9] = {0}, w[9] = {0};
+    ZKL_CIOS_LOOP
+    for (int i = 0; i < 8; i++) {
+      cios_step(t, a0, b0.v[0]);
+      cios_step(u, a1, b1.v[0]);
+      cios_step(w, a2, b2.v[0]);
+      rot(b0);
+      rot(b1);
+      rot(b2);
+    }
+    Triple q;
+#pragma unroll
+    for (int i = 0; i < 8; i++) { q.x.v[i] = t[i]; q.y.v[i] = u[i]; q.z.v[i] = w[i]; }
+    q.x = reduce_once(q.x);
+    q.y = reduce_once(q.y);
+    q.z = reduce_once(q.z);
+    return q;
+  }
+  struct Quad {
+    T x, y, z, w;
+  };
+  // r * a0, r * a1, r * a2, r * a3 (the fold of two tables' lo/hi halves)
+  static __device__ __noinline__ Quad mul4r_call(T r, T a0, T a1, T a2, T a3) {
+    uint32_t t[9] = {0}, u[9] = {0}, v[9] = {0}, w[9] = {0};
+    ZKL_CIOS_LOOP
+    for (int i = 0; i < 8; i++) {
+      cios_step(t, a0, r.v[0]);
+      cios_step(u, a1, r.v[0]);
+      cios_step(v, a2, r.v[0]);
+      cios_step(w, a3, r.v[0]);
+      rot(r);
+    }
+    Quad q;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      q.x.v[i] = t[i]; q.y.v[i] = u[i]; q.z.v[i] = v[i]; q.w.v[i] = w[i];
+    }
+    q.x = reduce_once(q.x);
+    q.y = reduce_once(q.y);
+    q.z = reduce_once(q.z);
+    q.w = reduce_once(q.w);
+    return q;
+  }
+  static __device__ __noinline__ Quad mul4_call(T a0, T b0, T a1, T b1, T a2, T b2, T a3, T b3) {
+    uint32_t t[9] = {0}, u[9] = {0}, v[9] = {0}, w[9] = {0};
+    ZKL_CIOS_LOOP
+    for (int i = 0; i < 8; i++) {
+      cios_step(t, a0, b0.v[0]);
+      cios_step(u, a1, b1.v[0]);
+      cios_step(v, a2, b2.v[0]);
+      cios_step(w, a3, b3.v[0]);
+      rot(b0);
+      rot(b1);
+      rot(b2);
+      rot(b3);
+    }
+    Quad q;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      q.x.v[i] = t[i]; q.y.v[i] = u[i]; q.z.v[i] = v[i]; q.w.v[i] = w[i];
+    }
+    q.x = reduce_once(q.x);
+    q.y = reduce_once(q.y);
+    q.z = reduce_once(q.z);
+    q.w = reduce_once(q.w);
+    return q;
+  }
+  ZKL_D static void mul3(const T& a0, const T& b0, const T& a1, const T& b1, const T& a2,
+                         const T& b2, T& o0, T& o1, T& o2) {
+    Triple q = mul3_call(a0, b0, a1, b1, a2, b2);
+    o0 = q.x; o1 = q.y; o2 = q.z;
+  }
+  ZKL_D static void mul4(const T& a0, const T& b0, const T& a1, const T& b1, const T& a2,
+                         const T& b2, const T& a3, const T& b3, T& o0, T& o1, T& o2, T& o3) {
+    Quad q = mul4_call(a0, b0, a1, b1, a2, b2, a3, b3);
+    o0 = q.x; o1 = q.y; o2 = q.z; o3 = q.w;
+  }
+  ZKL_D static void mul4r(const T& r, T& a0, T& a1, T& a2, T& a3) {
+    Quad q = mul4r_call(r, a0, a1, a2, a3);
+    a0 = q.x; a1 = q.y; a2 = q.z; a3 = q.w;
+  }
 #else
   static T reduce_once(const T& a) { return geq_p_portable(a) ? sub_p_portable(a) : a; }
   static T add(const T& a, const T& b) { return add_portable(a, b); }
@@ -306,6 +417,19 @@ struct Fr255 {
   static void mul2(const T& a, const T& b, const T& c, const T& d, T& ab, T& cd) {
     ab = mul_portable(a, b);
     cd = mul_portable(c, d);
+  }
+  static void mul3(const T& a0, const T& b0, const T& a1, const T& b1, const T& a2, const T& b2,
+                   T& o0, T& o1, T& o2) {
+    o0 = mul_portable(a0, b0); o1 = mul_portable(a1, b1); o2 = mul_portable(a2, b2);
+  }
+  static void mul4(const T& a0, const T& b0, const T& a1, const T& b1, const T& a2, const T& b2,
+                   const T& a3, const T& b3, T& o0, T& o1, T& o2, T& o3) {
+    o0 = mul_portable(a0, b0); o1 = mul_portable(a1, b1);
+    o2 = mul_portable(a2, b2); o3 = mul_portable(a3, b3);
+  }
+  static void mul4r(const T& r, T& a0, T& a1, T& a2, T& a3) {
+    a0 = mul_portable(r, a0); a1 = mul_portable(r, a1);
+    a2 = mul_portable(r, a2); a3 = mul_portable(r, a3);
   }
 #endif
 
@@ -357,6 +481,16 @@ struct M61 {
   ZKL_HD static void mul2(T a, T b, T c, T d, T& ab, T& cd) {
     ab = mul(a, b);
     cd = mul(c, d);
+  }
+  ZKL_HD static void mul3(T a0, T b0, T a1, T b1, T a2, T b2, T& o0, T& o1, T& o2) {
+    o0 = mul(a0, b0); o1 = mul(a1, b1); o2 = mul(a2, b2);
+  }
+  ZKL_HD static void mul4(T a0, T b0, T a1, T b1, T a2, T b2, T a3, T b3, T& o0, T& o1, T& o2,
+                          T& o3) {
+    o0 = mul(a0, b0); o1 = mul(a1, b1); o2 = mul(a2, b2); o3 = mul(a3, b3);
+  }
+  ZKL_HD static void mul4r(T r, T& a0, T& a1, T& a2, T& a3) {
+    a0 = mul(r, a0); a1 = mul(r, a1); a2 = mul(r, a2); a3 = mul(r, a3);
   }
   ZKL_HD static T to_mont(T a) { return a; }
   ZKL_HD static T from_mont(T a) { return a; }

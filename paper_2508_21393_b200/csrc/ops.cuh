@@ -75,4 +75,10 @@ template <class F>
 int op_matvec(int mtype, const void* M, uint64_t rows, uint64_t cols, int transpose,
               const void* x, void* y, cudaStream_t s);
 
+// native zkMat driver (zkmat.cu): gadgets.py:241-251, factored
+template <class F>
+int op_matmul_prove(int ta, const void* A, int tb, const void* B, int tc, const void* C, int d0,
+                    int d1, int d2, uint8_t* state, uint8_t* rounds_out, uint8_t* point_out,
+                    uint8_t* finals_out, cudaStream_t s);
+
 }  // namespace zkl

@@ -1,45 +1,178 @@
-// Persistent whole-sumcheck driver (sumcheck.py:108-130 after _absorb_claim).
+// Persistent whole-sumcheck engine (sumcheck.py:108-130 after _absorb_claim).
 //
-// ONE cooperative launch runs every round.  Per round:
-//   1. every thread folds its pairs by the previous challenge (in place) and
-//      accumulates shape-specific raw sums (no term coefficients on device);
-//   2. warp shuffles reduce them; lane 0 of every warp writes a partial;
-//   3. grid barrier; warp 0 of block 0 sums the partials and publishes the raw
-//      sums (Montgomery form) into a mailbox in mapped pinned host memory;
-//   4. the host applies the term coefficients / post-scalars, converts to
-//      canonical form, runs the native SHAKE-256 transcript (transcript.cu)
-//      and writes the next challenge back; block 0 spins on it (PCIe);
-//   5. grid barrier; every block picks up the challenge.
-// No kernel launches, copies or stream syncs per round.  Scalar field work
-// sits on the host because a dependent Montgomery multiply costs ~1.6k
-// cycles on one GPU thread (scratch/lat.cu) but ~0.1 us on the host.
+// ONE cooperative launch runs every round of a claim.  Per round j:
+//   1. every thread folds its pairs by r_{j-1} (in place) and accumulates
+//      shape-specific raw sums (sumcheck.py:110-123 / 129);
+//   2. warp shuffles + shared memory reduce them as WIDE integers (9 x 32-bit
+//      words for Fr: no modular reduction on the reduction tree);
+//   3. each block stores its partial, fences, and takes a ticket; the LAST
+//      block sums the partials and writes them to a mailbox in mapped pinned
+//      host memory as tagged 64-bit words (payload | round seq << 32);
+//   4. the host reduces mod p, finishes the evaluations (term coefficients,
+//      post scalars, the quadratic-product identities), appends them to the
+//      native SHAKE-256 transcript, squeezes r_j and writes it back as tagged
+//      words; the "drawn" state update (2 Keccak-f) runs after the write, off
+//      the critical path;
+//   5. each block polls the tagged challenge (directly over PCIe for small
+//      grids, else block 0 relays it through an L2 slot).
+// No kernel launches, copies, stream syncs or grid barriers per round.  The
+// host's challenge publication orders every block's table writes of round j
+// before any read of round j+1 (the last block saw all tickets before
+// publishing; tables are read with ld.cg, bypassing L1).
 //
 // Shapes (detected from the term list on the host):
 //   GENERIC  : any terms; device applies coefficients (combine, sumcheck.py:70)
-//   PROD2    : c * t_a t_b          -- zkMat U/W phases; 3 mults per pair
-//   PROD3    : c * t_a t_b t_c      -- elementprod; 7 mults per pair
-//   SUM2PROD2: c0 t_a t_b + c1 t_a t_c -- zkMat V phase; 6 mults per pair
-// The quadratic products use p(2) = 2p(1) - p(0) + 2c, p(3) = 3p(1) - 2p(0) + 6c
-// with c = (t_a(1)-t_a(0))(t_b(1)-t_b(0)): every evaluation is still computed
-// from the tables, never derived from the claimed sum.
+//   PROD2    : c * t_a t_b              -- zkMat U/W phases; 3 mults per pair
+//   PROD3    : c * t_a t_b t_c          -- elementprod; 7 mults per pair
+//   SUM2PROD2: c0 t_a t_b + c1 t_a t_c  -- zkMat V phase; 6 mults per pair
+// For the quadratic shapes the device returns (sum f0 g0, sum f1 g1,
+// sum fd gd) and the host forms p(2) = 2p(1) - p(0) + 2c, p(3) = 3p(1) - 2p(0)
+// + 6c -- exact identities of the same polynomial, computed from the tables,
+// never derived from the claimed sum (hard part 3).
 #include <atomic>
 #include <chrono>
 #include <cstdlib>
 #include <vector>
 
-#include <cooperative_groups.h>
-
+#include "hostfield.h"
+#include "phase.cuh"
 #include "round_eval.cuh"
-#include "transcript.cuh"
 
+#include <cooperative_groups.h>
 namespace cg = cooperative_groups;
 
 namespace zkl {
 
-enum Shape { kGeneric = 0, kProd2 = 1, kProd3 = 2, kSum2Prod2 = 3 };
+// ---------------------------------------------------------------------------
+// wide (unreduced) sums for the reduction tree
+template <class F>
+struct Red;
+
+template <>
+struct Red<Fr255> {
+  static constexpr int NW = 9;
+  struct W {
+    uint32_t w[9];
+  };
+  ZKL_D static W from(const fr_t& x) {
+    W r;
+#pragma unroll
+    for (int i = 0; i < 8; i++) r.w[i] = x.v[i];
+    r.w[8] = 0;
+    return r;
+  }
+  ZKL_D static W zero() {
+    W r;
+#pragma unroll
+    for (int i = 0; i < 9; i++) r.w[i] = 0;
+    return r;
+  }
+  ZKL_D static W add(const W& a, const W& b) {
+    W s;
+    asm("add.cc.u32  %0, %9, %18;\n\t"
+        "addc.cc.u32 %1, %10, %19;\n\t"
+        "addc.cc.u32 %2, %11, %20;\n\t"
+        "addc.cc.u32 %3, %12, %21;\n\t"
+        "addc.cc.u32 %4, %13, %22;\n\t"
+        "addc.cc.u32 %5, %14, %23;\n\t"
+        "addc.cc.u32 %6, %15, %24;\n\t"
+        "addc.cc.u32 %7, %16, %25;\n\t"
+        "addc.u32    %8, %17, %26;\n\t"
+        : "=r"(s.w[0]), "=r"(s.w[1]), "=r"(s.w[2]), "=r"(s.w[3]), "=r"(s.w[4]), "=r"(s.w[5]),
+          "=r"(s.w[6]), "=r"(s.w[7]), "=r"(s.w[8])
+        : "r"(a.w[0]), "r"(a.w[1]), "r"(a.w[2]), "r"(a.w[3]), "r"(a.w[4]), "r"(a.w[5]),
+          "r"(a.w[6]), "r"(a.w[7]), "r"(a.w[8]), "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]),
+          "r"(b.w[3]), "r"(b.w[4]), "r"(b.w[5]), "r"(b.w[6]), "r"(b.w[7]), "r"(b.w[8]));
+    return s;
+  }
+  ZKL_D static W shfl_down(const W& a, int off) {
+    W r;
+#pragma unroll
+    for (int i = 0; i < 9; i++) r.w[i] = __shfl_down_sync(kFull, a.w[i], off);
+    return r;
+  }
+  ZKL_D static W shfl_xor(const W& a, int off) {
+    W r;
+#pragma unroll
+    for (int i = 0; i < 9; i++) r.w[i] = __shfl_xor_sync(kFull, a.w[i], off);
+    return r;
+  }
+  ZKL_D static uint32_t word(const W& a, int i) { return a.w[i]; }
+};
+
+template <>
+struct Red<M61> {
+  static constexpr int NW = 4;
+  struct W {
+    uint64_t lo, hi;
+  };
+  ZKL_D static W from(uint64_t x) { return W{x, 0}; }
+  ZKL_D static W zero() { return W{0, 0}; }
+  ZKL_D static W add(const W& a, const W& b) {
+    W s;
+    s.lo = a.lo + b.lo;
+    s.hi = a.hi + b.hi + (s.lo < a.lo ? 1 : 0);
+    return s;
+  }
+  ZKL_D static W shfl_down(const W& a, int off) {
+    return W{__shfl_down_sync(kFull, a.lo, off), __shfl_down_sync(kFull, a.hi, off)};
+  }
+  ZKL_D static W shfl_xor(const W& a, int off) {
+    return W{__shfl_xor_sync(kFull, a.lo, off), __shfl_xor_sync(kFull, a.hi, off)};
+  }
+  ZKL_D static uint32_t word(const W& a, int i) {
+    const uint64_t v = i < 2 ? a.lo : a.hi;
+    return (uint32_t)(v >> (32 * (i & 1)));
+  }
+};
 
 // ---------------------------------------------------------------------------
-// evaluators: pair() accumulates, finish() -> NOUT raw sums (4 per group)
+// Lane mode (small rounds).  A round whose pairs fit in one pass is a pure
+// latency problem, and one thread doing all of a pair's products serialises
+// them (the carry chains of independent Montgomery products do not overlap
+// well).  Instead a group of L lanes owns a pair: lane q < 2k folds table
+// q/2, half q%2 (one product), the folded values are exchanged with
+// shuffles, and each lane computes one output product.  Critical path: one
+// fold product + one (PROD2, SUM2PROD2) or two (PROD3) evaluation products.
+inline int lanes_for(int shape, int k) {
+  if (shape == kGeneric) return 0;
+  const int nout = shape == kProd2 ? 3 : shape == kProd3 ? 4 : 6;
+  const int need = 2 * k > nout ? 2 * k : nout;  // fold lanes / output lanes
+  return need <= 4 ? 4 : need <= 8 ? 8 : 16;
+}
+
+template <class F>
+ZKL_D typename F::T shfl_elem(const typename F::T& x, int src) {
+  return shfl_idx(x, src);
+}
+
+template <class F, int MAXK>
+ZKL_D typename F::T lane_fold(const TablePtrs<F, MAXK>& tabs, int k, uint64_t i, uint64_t half,
+                              bool fold, const typename F::T& r, int q, bool active) {
+  using T = typename F::T;
+  T v = F::zero();
+  if (active && q < 2 * k) {
+    T* t = tabs.t[q >> 1];
+    const uint64_t m = i + (uint64_t)(q & 1) * half;
+    if (fold) {
+      const T a = ld_cg(t + m), b = ld_cg(t + m + 2 * half);
+      v = F::add(a, F::mul(r, F::sub(b, a)));
+      t[m] = v;
+    } else {
+      v = ld_cg(t + m);
+    }
+  }
+  return v;
+}
+
+// x in {lo, hi, hi - lo} by selector s in {0, 1, 2}
+template <class F>
+ZKL_D typename F::T pick3(const typename F::T& lo, const typename F::T& hi, int s) {
+  return s == 0 ? lo : (s == 1 ? hi : F::sub(hi, lo));
+}
+
+// ---------------------------------------------------------------------------
+// evaluators: pair() accumulates NA field sums, finish() -> NOUT raw outputs
 template <class F, int MAXK>
 struct EvGeneric {
   using T = typename F::T;
@@ -61,6 +194,69 @@ struct EvGeneric {
 #pragma unroll
     for (int x = 0; x < 4; x++) out[x] = acc[x];
   }
+  ZKL_D static T lane(const T&, int, int, bool, const Terms<F>&) { return F::zero(); }
+};
+
+template <class F, int MAXK>
+struct EvProd2 {
+  using T = typename F::T;
+  static constexpr int NA = 3, NOUT = 3;
+  ZKL_D static void pair(T (&cur)[MAXK], const T (&df)[MAXK], int, const Terms<F>& tm,
+                         T (&acc)[NA]) {
+    const int a = tm.fi[0][0], b = tm.fi[0][1];
+    const T f0 = select_tab<F, MAXK>(cur, a), fd = select_tab<F, MAXK>(df, a);
+    const T g0 = select_tab<F, MAXK>(cur, b), gd = select_tab<F, MAXK>(df, b);
+    T p0, p1, pc;
+    F::mul3(f0, g0, F::add(f0, fd), F::add(g0, gd), fd, gd, p0, p1, pc);
+    acc[0] = F::add(acc[0], p0);
+    acc[1] = F::add(acc[1], p1);
+    acc[2] = F::add(acc[2], pc);
+  }
+  ZKL_D static void finish(const T (&acc)[NA], T (&out)[NOUT]) {
+#pragma unroll
+    for (int q = 0; q < 3; q++) out[q] = acc[q];
+  }
+  // lane mode: output q = [f0 g0, f1 g1, fd gd][q]
+  ZKL_D static T lane(const T& v, int q, int gb, bool active, const Terms<F>& tm) {
+    const int a = tm.fi[0][0], b = tm.fi[0][1];
+    const T fl = shfl_elem<F>(v, gb + 2 * a), fh = shfl_elem<F>(v, gb + 2 * a + 1);
+    const T gl = shfl_elem<F>(v, gb + 2 * b), gh = shfl_elem<F>(v, gb + 2 * b + 1);
+    const int s = q < 3 ? q : 0;
+    const T p = F::mul(pick3<F>(fl, fh, s), pick3<F>(gl, gh, s));
+    return (active && q < 3) ? p : F::zero();
+  }
+};
+
+template <class F, int MAXK>
+struct EvSum2Prod2 {
+  using T = typename F::T;
+  static constexpr int NA = 6, NOUT = 6;
+  ZKL_D static void pair(T (&cur)[MAXK], const T (&df)[MAXK], int, const Terms<F>& tm,
+                         T (&acc)[NA]) {
+    const int a = tm.fi[0][0], b = tm.fi[0][1], c = tm.fi[1][1];
+    const T f0 = select_tab<F, MAXK>(cur, a), fd = select_tab<F, MAXK>(df, a);
+    const T g0 = select_tab<F, MAXK>(cur, b), gd = select_tab<F, MAXK>(df, b);
+    const T h0 = select_tab<F, MAXK>(cur, c), hd = select_tab<F, MAXK>(df, c);
+    const T f1 = F::add(f0, fd);
+    T m[6];
+    F::mul4(f0, g0, f0, h0, f1, F::add(g0, gd), f1, F::add(h0, hd), m[0], m[3], m[1], m[4]);
+    F::mul2(fd, gd, fd, hd, m[2], m[5]);
+#pragma unroll
+    for (int q = 0; q < 6; q++) acc[q] = F::add(acc[q], m[q]);
+  }
+  ZKL_D static void finish(const T (&acc)[NA], T (&out)[NOUT]) {
+#pragma unroll
+    for (int q = 0; q < 6; q++) out[q] = acc[q];
+  }
+  // lane mode: output q = [f0 g0, f1 g1, fd gd, f0 h0, f1 h1, fd hd][q]
+  ZKL_D static T lane(const T& v, int q, int gb, bool active, const Terms<F>& tm) {
+    const int a = tm.fi[0][0], y = q < 3 ? tm.fi[0][1] : tm.fi[1][1];
+    const T fl = shfl_elem<F>(v, gb + 2 * a), fh = shfl_elem<F>(v, gb + 2 * a + 1);
+    const T yl = shfl_elem<F>(v, gb + 2 * y), yh = shfl_elem<F>(v, gb + 2 * y + 1);
+    const int s = q < 6 ? q % 3 : 0;
+    const T p = F::mul(pick3<F>(fl, fh, s), pick3<F>(yl, yh, s));
+    return (active && q < 6) ? p : F::zero();
+  }
 };
 
 // quadratic-product helper: (c0, c1, c2) -> p(0..3)
@@ -71,55 +267,10 @@ ZKL_D void quad_evals(const typename F::T& c0, const typename F::T& c1, const ty
   const T two_c1 = F::add(c1, c1), two_c2 = F::add(c2, c2);
   out[0] = c0;
   out[1] = c1;
-  out[2] = F::sub(F::add(two_c1, two_c2), c0);                      // 2c1 - c0 + 2c2
+  out[2] = F::sub(F::add(two_c1, two_c2), c0);                          // 2c1 - c0 + 2c2
   const T six_c2 = F::add(F::add(two_c2, two_c2), two_c2);
   out[3] = F::sub(F::add(F::add(two_c1, c1), six_c2), F::add(c0, c0));  // 3c1 - 2c0 + 6c2
 }
-
-template <class F, int MAXK>
-struct EvProd2 {
-  using T = typename F::T;
-  static constexpr int NA = 3, NOUT = 4;
-  ZKL_D static void pair(T (&cur)[MAXK], const T (&df)[MAXK], int, const Terms<F>& tm,
-                         T (&acc)[NA]) {
-    const int a = tm.fi[0][0], b = tm.fi[0][1];
-    const T f0 = select_tab<F, MAXK>(cur, a), fd = select_tab<F, MAXK>(df, a);
-    const T g0 = select_tab<F, MAXK>(cur, b), gd = select_tab<F, MAXK>(df, b);
-    T p0, pc;
-    F::mul2(f0, g0, fd, gd, p0, pc);
-    const T p1 = F::mul(F::add(f0, fd), F::add(g0, gd));
-    acc[0] = F::add(acc[0], p0);
-    acc[1] = F::add(acc[1], p1);
-    acc[2] = F::add(acc[2], pc);
-  }
-  ZKL_D static void finish(const T (&acc)[NA], T (&out)[NOUT]) {
-    quad_evals<F>(acc[0], acc[1], acc[2], out);
-  }
-};
-
-template <class F, int MAXK>
-struct EvSum2Prod2 {
-  using T = typename F::T;
-  static constexpr int NA = 6, NOUT = 8;
-  ZKL_D static void pair(T (&cur)[MAXK], const T (&df)[MAXK], int, const Terms<F>& tm,
-                         T (&acc)[NA]) {
-    const int a = tm.fi[0][0], b = tm.fi[0][1], c = tm.fi[1][1];
-    const T f0 = select_tab<F, MAXK>(cur, a), fd = select_tab<F, MAXK>(df, a);
-    const T g0 = select_tab<F, MAXK>(cur, b), gd = select_tab<F, MAXK>(df, b);
-    const T h0 = select_tab<F, MAXK>(cur, c), hd = select_tab<F, MAXK>(df, c);
-    const T f1 = F::add(f0, fd);
-    T m[6];
-    F::mul2(f0, g0, f0, h0, m[0], m[3]);
-    F::mul2(f1, F::add(g0, gd), f1, F::add(h0, hd), m[1], m[4]);
-    F::mul2(fd, gd, fd, hd, m[2], m[5]);
-#pragma unroll
-    for (int q = 0; q < 6; q++) acc[q] = F::add(acc[q], m[q]);
-  }
-  ZKL_D static void finish(const T (&acc)[NA], T (&out)[NOUT]) {
-    quad_evals<F>(acc[0], acc[1], acc[2], out);
-    quad_evals<F>(acc[3], acc[4], acc[5], out + 4);
-  }
-};
 
 template <class F, int MAXK>
 struct EvProd3 {
@@ -131,13 +282,12 @@ struct EvProd3 {
     const T e0 = select_tab<F, MAXK>(cur, a), ed = select_tab<F, MAXK>(df, a);
     const T a0 = select_tab<F, MAXK>(cur, b), ad = select_tab<F, MAXK>(df, b);
     const T b0 = select_tab<F, MAXK>(cur, c), bd = select_tab<F, MAXK>(df, c);
-    T q[4], q0, qc;
-    F::mul2(e0, a0, ed, ad, q0, qc);
-    quad_evals<F>(q0, F::mul(F::add(e0, ed), F::add(a0, ad)), qc, q);
+    T q[4], q0, q1, qc;
+    F::mul3(e0, a0, F::add(e0, ed), F::add(a0, ad), ed, ad, q0, q1, qc);
+    quad_evals<F>(q0, q1, qc, q);
     const T b1 = F::add(b0, bd), b2 = F::add(b1, bd), b3 = F::add(b2, bd);
     T m[4];
-    F::mul2(q[0], b0, q[1], b1, m[0], m[1]);
-    F::mul2(q[2], b2, q[3], b3, m[2], m[3]);
+    F::mul4(q[0], b0, q[1], b1, q[2], b2, q[3], b3, m[0], m[1], m[2], m[3]);
 #pragma unroll
     for (int x = 0; x < 4; x++) acc[x] = F::add(acc[x], m[x]);
   }
@@ -145,218 +295,652 @@ struct EvProd3 {
 #pragma unroll
     for (int x = 0; x < 4; x++) out[x] = acc[x];
   }
+  // lane mode: level 1 q(x) = e(x) a(x) from 3 lanes, level 2 output x =
+  // q(x) b(x) for x = 0..3
+  ZKL_D static T lane(const T& v, int q, int gb, bool active, const Terms<F>& tm) {
+    const int ie = tm.fi[0][0], ia = tm.fi[0][1], ib = tm.fi[0][2];
+    const T el = shfl_elem<F>(v, gb + 2 * ie), eh = shfl_elem<F>(v, gb + 2 * ie + 1);
+    const T al = shfl_elem<F>(v, gb + 2 * ia), ah = shfl_elem<F>(v, gb + 2 * ia + 1);
+    const int s = q < 3 ? q : 0;
+    const T p1 = F::mul(pick3<F>(el, eh, s), pick3<F>(al, ah, s));
+    const T q0 = shfl_elem<F>(p1, gb), q1 = shfl_elem<F>(p1, gb + 1);
+    const T qc = shfl_elem<F>(p1, gb + 2);
+    T qx[4];
+    quad_evals<F>(q0, q1, qc, qx);
+    const T bl = shfl_elem<F>(v, gb + 2 * ib), bh = shfl_elem<F>(v, gb + 2 * ib + 1);
+    const T bd = F::sub(bh, bl);
+    const int x = q & 3;
+    T bx = x == 0 ? bl : bh;
+    if (x >= 2) bx = F::add(bx, bd);
+    if (x == 3) bx = F::add(bx, bd);
+    T qq = qx[0];
+    if (x == 1) qq = qx[1];
+    if (x == 2) qq = qx[2];
+    if (x == 3) qq = qx[3];
+    const T m = F::mul(qq, bx);
+    return (active && q < 4) ? m : F::zero();
+  }
 };
 
-// ---------------------------------------------------------------------------
-// mailbox access (host-mapped memory: every device read is a PCIe round trip)
-ZKL_D uint32_t ld_acquire_sys(const volatile uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-ZKL_D void st_release_sys(volatile uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-ZKL_D void st_vec_sys(volatile uint8_t* dst, const void* src, int nbytes) {
-  const uint4* s = reinterpret_cast<const uint4*>(src);
-  for (int o = 0; o < nbytes; o += 16) {
-    uint4 v = s[o / 16];
-    asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(dst + o), "r"(v.x),
-                 "r"(v.y), "r"(v.z), "r"(v.w)
-                 : "memory");
+// Load the pair (i, i + half) of every table, folding first when FOLD:
+// cur = low value, df = high - low.  All 2k fold products go through the
+// 4-wide multiply (one product latency per 4 folds).
+template <class F, int MAXK, bool FOLD>
+ZKL_D void load_fold_pair(const TablePtrs<F, MAXK>& tabs, int k, uint64_t i, uint64_t half,
+                          const typename F::T& r, typename F::T (&cur)[MAXK],
+                          typename F::T (&df)[MAXK]) {
+  using T = typename F::T;
+  if (!FOLD) {
+#pragma unroll
+    for (int j = 0; j < MAXK; j++) {
+      if (j < k) {
+        const T* t = tabs.t[j];
+        const T lo = ld_cg(t + i), hi = ld_cg(t + i + half);
+        cur[j] = lo;
+        df[j] = F::sub(hi, lo);
+      } else {
+        cur[j] = F::zero();
+        df[j] = F::zero();
+      }
+    }
+    return;
+  }
+  T a0[MAXK], b0[MAXK], da[MAXK], db[MAXK];
+#pragma unroll
+  for (int j = 0; j < MAXK; j++) {
+    if (j < k) {
+      const T* t = tabs.t[j];
+      a0[j] = ld_cg(t + i);
+      b0[j] = ld_cg(t + i + half);
+      da[j] = F::sub(ld_cg(t + i + 2 * half), a0[j]);
+      db[j] = F::sub(ld_cg(t + i + 3 * half), b0[j]);
+    } else {
+      a0[j] = b0[j] = da[j] = db[j] = F::zero();
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < MAXK; j += 2) {
+    if (j < k) {
+      if (j + 1 < MAXK) F::mul4r(r, da[j], db[j], da[j + 1], db[j + 1]);
+      else F::mul2(r, da[j], r, db[j], da[j], db[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < MAXK; j++) {
+    if (j < k) {
+      T* t = tabs.t[j];
+      const T lo = F::add(a0[j], da[j]), hi = F::add(b0[j], db[j]);
+      t[i] = lo;
+      t[i + half] = hi;
+      cur[j] = lo;
+      df[j] = F::sub(hi, lo);
+    } else {
+      cur[j] = F::zero();
+      df[j] = F::zero();
+    }
   }
 }
-ZKL_D void ld_vec32_sys(void* dst, const volatile uint8_t* src) {
-  uint4 v0, v1;  // both loads in flight together
-  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v0.x), "=r"(v0.y), "=r"(v0.z), "=r"(v0.w)
-               : "l"(src)
-               : "memory");
-  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v1.x), "=r"(v1.y), "=r"(v1.z), "=r"(v1.w)
-               : "l"(src + 16)
-               : "memory");
-  reinterpret_cast<uint4*>(dst)[0] = v0;
-  reinterpret_cast<uint4*>(dst)[1] = v1;
+
+// ---------------------------------------------------------------------------
+// tagged-word mailbox access (host-mapped memory: device reads are PCIe
+// round trips, device writes are posted)
+ZKL_D void st_tagged2(volatile uint64_t* p, uint64_t a, uint64_t b) {
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+ZKL_D void ld_tagged2(const volatile uint64_t* p, uint64_t& a, uint64_t& b) {
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
 ZKL_D uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+ZKL_D uint64_t tag(uint32_t w, uint32_t seq) { return (uint64_t)w | ((uint64_t)seq << 32); }
 
 constexpr uint64_t kSpinTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s
+constexpr int kThreads = 256;
+constexpr int kDirectPollMaxGrid = 1;
 
+// Poll NW tagged words until all carry `seq`; payload -> out.  Returns false
+// on abort / timeout.
+template <int NW>
+ZKL_D bool poll_tagged(const volatile uint64_t* src, uint32_t seq, uint32_t (&out)[NW],
+                       const volatile uint32_t* abort_flag) {
+  const uint64_t t0 = globaltimer();
+  for (uint32_t spin = 1;; spin++) {
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < NW; i += 2) {
+      uint64_t a, b = 0;
+      if (i + 1 < NW) ld_tagged2(src + i, a, b);
+      else a = src[i];
+      ok &= (uint32_t)(a >> 32) == seq;
+      out[i] = (uint32_t)a;
+      if (i + 1 < NW) {
+        ok &= (uint32_t)(b >> 32) == seq;
+        out[i + 1] = (uint32_t)b;
+      }
+    }
+    if (ok) return true;
+    if ((spin & 63) == 0 && ((abort_flag && *abort_flag) || globaltimer() - t0 > kSpinTimeoutNs))
+      return false;
+  }
+}
+
+// Warp-cooperative poll: lanes < NW/2 each load one 16-byte pair of tagged
+// words (independent loads, one PCIe round trip per poll; a single thread
+// issuing the loads back to back pays one round trip per load).  Every lane
+// of the warp must call it; on success out[0..NW) holds the payload.
+template <int NW>
+ZKL_D bool warp_poll(const volatile uint64_t* src, uint32_t seq, uint32_t* out,
+                     const volatile uint32_t* abort_flag) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t t0 = globaltimer();
+  for (uint32_t spin = 1;; spin++) {
+    uint64_t a = (uint64_t)seq << 32, b = a;
+    if (lane < NW / 2) ld_tagged2(src + 2 * lane, a, b);
+    const bool mine = (uint32_t)(a >> 32) == seq && (uint32_t)(b >> 32) == seq;
+    if (__all_sync(kFull, mine)) {
+      if (lane < NW / 2) {
+        out[2 * lane] = (uint32_t)a;
+        out[2 * lane + 1] = (uint32_t)b;
+      }
+      __syncwarp();
+      return true;
+    }
+    if ((spin & 63) == 0) {
+      int bad = lane == 0 && ((abort_flag && *abort_flag) || globaltimer() - t0 > kSpinTimeoutNs);
+      if (__shfl_sync(kFull, bad, 0)) return false;
+    }
+  }
+}
+
+template <class F>
+struct Words {
+  static constexpr int N = F::kBytes / 4;  // 8 (Fr) or 2 (M61)
+  ZKL_D static typename F::T load(const uint32_t* w) {
+    typename F::T r;
+    memcpy(&r, w, F::kBytes);
+    return r;
+  }
+  ZKL_D static uint32_t word(const typename F::T& x, int i) {
+    uint32_t w[N];
+    memcpy(w, &x, F::kBytes);
+    return w[i];
+  }
+};
+
+// One round's accumulation for the calling thread: folds (if `fold`) and
+// evaluates its pairs (lane mode when L > 0, else one pair per thread), then
+// leaves the warp's wide sums in wsum[warp][0..NOUT).  Every thread of the
+// block must call it (it ends with the warp shuffles).
 template <class F, int MAXK, class EV>
-__global__ void __launch_bounds__(256)
-    k_sumcheck_persistent(TablePtrs<F, MAXK> tabs, int k, int num_vars, Terms<F> tm,
-                          Mailbox* mb, typename F::T* partials, typename F::T* rbuf,
-                          unsigned* fail, uint64_t* trace) {
+ZKL_D void accumulate_round(const TablePtrs<F, MAXK>& tabs, int k, const Terms<F>& tm,
+                            uint64_t half, bool fold, const typename F::T& r, int L,
+                            uint64_t gtid, uint64_t nthreads,
+                            typename Red<F>::W (*wsum)[EV::NOUT]) {
   using T = typename F::T;
-  cg::grid_group g = cg::this_grid();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  __shared__ T wsum[8 * EV::NOUT];
-  uint64_t size = 1ull << num_vars;
-  T r = F::zero();
-  const bool tr0 = trace && blockIdx.x == 0 && threadIdx.x == 0;
-  for (int j = 0; j < num_vars; j++) {
-    if (tr0) trace[j * 6 + 0] = globaltimer();
-    const bool fold = j > 0;
-    const uint64_t half = fold ? size >> 2 : size >> 1;
+  using R = Red<F>;
+  using W = typename R::W;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (L > 0) {
+    // lane mode: groups of L lanes, one pair per group per pass
+    const uint64_t ngroups = nthreads / (unsigned)L;
+    const int q = lane & (L - 1), gb = lane & ~(L - 1);
+    T o = F::zero();
+    const uint64_t passes = (half + ngroups - 1) / ngroups;
+    uint64_t i = gtid / (unsigned)L;
+    for (uint64_t ps = 0; ps < passes; ps++, i += ngroups) {
+      const bool active = i < half;
+      const T fv = lane_fold<F, MAXK>(tabs, k, i, half, fold, r, q, active);
+      o = F::add(o, EV::lane(fv, q, gb, active, tm));
+    }
+    W w = R::from(o);
+    for (int off = 16; off >= L; off >>= 1) w = R::add(w, R::shfl_down(w, off));
+    if (lane < EV::NOUT) wsum[warp][lane] = w;  // lane q < L holds output q
+  } else {
     T acc[EV::NA];
 #pragma unroll
     for (int q = 0; q < EV::NA; q++) acc[q] = F::zero();
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < half;
-         i += (uint64_t)gridDim.x * blockDim.x) {
+    for (uint64_t i = gtid; i < half; i += nthreads) {
       T cur[MAXK], df[MAXK];
       if (fold)
-        load_pair<F, MAXK, true, true>(tabs, k, i, half, r, cur, df);
+        load_fold_pair<F, MAXK, true>(tabs, k, i, half, r, cur, df);
       else
-        load_pair<F, MAXK, false, true>(tabs, k, i, half, r, cur, df);
+        load_fold_pair<F, MAXK, false>(tabs, k, i, half, r, cur, df);
       EV::pair(cur, df, k, tm, acc);
     }
     T out[EV::NOUT];
     EV::finish(acc, out);
 #pragma unroll
-    for (int q = 0; q < EV::NOUT; q++) out[q] = warp_sum<F>(out[q]);
-    // block partial: warp sums -> shared -> warp 0 (one partial per block)
-    if (lane == 0) {
+    for (int q = 0; q < EV::NOUT; q++) {
+      W v = R::from(out[q]);
 #pragma unroll
-      for (int q = 0; q < EV::NOUT; q++) wsum[warp * EV::NOUT + q] = out[q];
+      for (int off = 16; off; off >>= 1) v = R::add(v, R::shfl_down(v, off));
+      if (lane == 0) wsum[warp][q] = v;
     }
-    __syncthreads();
-    if (warp == 0) {
-#pragma unroll
-      for (int q = 0; q < EV::NOUT; q++) {
-        T s = lane < nwarps ? wsum[lane * EV::NOUT + q] : F::zero();
-        s = warp_sum<F>(s);
-        if (lane == 0) partials[(size_t)blockIdx.x * EV::NOUT + q] = s;
-      }
-    }
-    if (tr0) trace[j * 6 + 1] = globaltimer();
-    g.sync();
-    if (tr0) trace[j * 6 + 2] = globaltimer();
-    if (blockIdx.x == 0 && warp == 0) {
-      T v[EV::NOUT];
-#pragma unroll
-      for (int q = 0; q < EV::NOUT; q++) v[q] = F::zero();
-      for (unsigned w = lane; w < gridDim.x; w += 32) {
-#pragma unroll
-        for (int q = 0; q < EV::NOUT; q++)
-          v[q] = F::add(v[q], ld_cg(partials + (size_t)w * EV::NOUT + q));
-      }
-#pragma unroll
-      for (int q = 0; q < EV::NOUT; q++) v[q] = warp_sum<F>(v[q]);
-      if (lane == 0) {
-        alignas(16) T pub[EV::NOUT];
-#pragma unroll
-        for (int q = 0; q < EV::NOUT; q++) pub[q] = v[q];
-        st_vec_sys(mb->evals, pub, (int)sizeof(pub));
-        __threadfence_system();
-        st_release_sys(&mb->ev_seq, (uint32_t)(j + 1));
-        if (tr0) trace[j * 6 + 3] = globaltimer();
-        const uint64_t t0 = globaltimer();
-        unsigned bad = 0;
-        for (uint32_t spin = 1; ld_acquire_sys(&mb->ch_seq) != (uint32_t)(j + 1); spin++) {
-          if ((spin & 63) == 0 &&
-              (ld_acquire_sys(&mb->abort) || globaltimer() - t0 > kSpinTimeoutNs)) {
-            bad = 1;
-            break;
-          }
-        }
-        if (bad) {
-          *fail = 1;
-          mb->status = 1;
-        } else {
-          alignas(16) uint8_t cb[32];
-          ld_vec32_sys(cb, mb->chal);
-          T c;
-          memcpy(&c, cb, F::kBytes);
-          *rbuf = c;
-        }
-        if (tr0) trace[j * 6 + 4] = globaltimer();
-        __threadfence();
-      }
-    }
-    g.sync();
-    if (tr0) trace[j * 6 + 5] = globaltimer();
-    if (ld_cg(fail)) return;
-    r = ld_cg(rbuf);
-    if (fold) size >>= 1;
   }
-  // final fold of the size-2 tables by the last challenge (sumcheck.py:129-130)
-  if (blockIdx.x == 0) {
-    __shared__ T fin[MAXK];
-    if (threadIdx.x < k) {
-      const T* t = tabs.t[threadIdx.x];
-      T a = ld_cg(t), b = ld_cg(t + 1);
-      fin[threadIdx.x] = F::from_mont(F::add(a, F::mul(r, F::sub(b, a))));
+}
+
+// warp 0: sum the per-warp wide sums of the block; lane 0 gets the totals
+template <class F, int NOUT>
+ZKL_D void block_total(typename Red<F>::W (*wsum)[NOUT], int nwarps,
+                       typename Red<F>::W (&tot)[NOUT]) {
+  using R = Red<F>;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < NOUT; q++) {
+    typename R::W s = lane < nwarps ? wsum[lane][q] : R::zero();
+#pragma unroll
+    for (int off = 16; off; off >>= 1) s = R::add(s, R::shfl_down(s, off));
+    tot[q] = s;
+  }
+}
+
+// warp-wide: lane 0's totals -> tagged mailbox words (one 16-byte PCIe store
+// per lane; a single thread issuing all of them serialises)
+template <class F, int NOUT>
+ZKL_D void publish_sums(const typename Red<F>::W (&tot)[NOUT], uint32_t seq, Mailbox* mb,
+                        uint64_t* s_words) {
+  using R = Red<F>;
+  constexpr int NW = R::NW, NWORDS = NOUT * NW;
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < NOUT; q++) {
+#pragma unroll
+      for (int w = 0; w < NW; w++) s_words[q * NW + w] = tag(R::word(tot[q], w), seq);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      alignas(16) T buf[MAXK];
-      for (int q = 0; q < k; q++) buf[q] = fin[q];
-      st_vec_sys(mb->finals, buf, (k * F::kBytes + 15) & ~15);
-      __threadfence_system();
-    }
+  }
+  __syncwarp();
+  for (int idx = 2 * lane; idx < NWORDS; idx += 64) {
+    if (idx + 1 < NWORDS)
+      st_tagged2(mb->ev + idx, s_words[idx], s_words[idx + 1]);
+    else
+      mb->ev[idx] = s_words[idx];
+  }
+}
+
+template <class F, int MAXK>
+ZKL_D void publish_finals(const TablePtrs<F, MAXK>& tabs, int k, const typename F::T& r,
+                          uint32_t fseq, Mailbox* mb) {
+  using T = typename F::T;
+  constexpr int NC = Words<F>::N;
+  if (threadIdx.x < k) {
+    const T* t = tabs.t[threadIdx.x];
+    const T a = ld_cg(t), b = ld_cg(t + 1);
+    const T f = F::add(a, F::mul(r, F::sub(b, a)));
+#pragma unroll
+    for (int w = 0; w < NC; w++) mb->fin[threadIdx.x * NC + w] = tag(Words<F>::word(f, w), fseq);
   }
 }
 
 // ---------------------------------------------------------------------------
+// Grid kernel (large rounds): many blocks, cooperative launch for
+// co-residency.  Runs rounds [j0, j1) of the claim; the LAST arriving block
+// (ticket) sums the block partials and publishes; block 0 polls the
+// challenge and relays it through an L2 slot.  When j1 < num_vars the
+// remaining rounds continue in the cluster kernel (no finals here).
+template <class F, int MAXK, class EV>
+__global__ void __launch_bounds__(kThreads)
+    k_sumcheck_persistent(TablePtrs<F, MAXK> tabs, int k, int num_vars, int j0, int j1,
+                          Terms<F> tm, Mailbox* mb, typename Red<F>::W* partials,
+                          unsigned* ticket, uint64_t* bcast, unsigned* fail, uint32_t seq0,
+                          int direct, uint64_t* trace, int L) {
+  using T = typename F::T;
+  using R = Red<F>;
+  using W = typename R::W;
+  constexpr int NC = Words<F>::N;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  __shared__ W wsum[kThreads / 32][EV::NOUT];
+  __shared__ T s_r;
+  __shared__ int s_flag;
+  __shared__ uint64_t s_words[kMbEvalWords];
+  const unsigned G = gridDim.x;
+  const uint64_t nthreads = (uint64_t)G * blockDim.x;
+  const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  T r = F::zero();
+  for (int j = j0; j < j1; j++) {
+    const uint32_t seq = seq0 + (uint32_t)j + 1;
+    const bool fold = j > 0;
+    const bool tr0 = trace && blockIdx.x == 0 && threadIdx.x == 0;
+    if (tr0) trace[j * 8 + 0] = globaltimer();
+    const uint64_t half = 1ull << (num_vars - 1 - j);
+    const int Lr = (L > 0 && half * (uint64_t)L <= nthreads) ? L : 0;
+    accumulate_round<F, MAXK, EV>(tabs, k, tm, half, fold, r, Lr, gtid, nthreads, wsum);
+    if (tr0) trace[j * 8 + 1] = globaltimer();
+    __syncthreads();
+    if (warp == 0) {
+      W v[EV::NOUT];
+      block_total<F, EV::NOUT>(wsum, nwarps, v);
+      if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < EV::NOUT; q++) partials[(size_t)blockIdx.x * EV::NOUT + q] = v[q];
+        __threadfence();
+        const unsigned t = atomicAdd(ticket, 1u);
+        s_flag = (t == G * (unsigned)(j - j0 + 1) - 1) ? 1 : 0;
+        if (tr0) trace[j * 8 + 2] = globaltimer();
+      }
+    }
+    __syncthreads();
+    if (s_flag && warp == 0) {
+      // last block: warp 0 sums the partials and publishes
+      __threadfence();
+      W tot[EV::NOUT];
+#pragma unroll
+      for (int q = 0; q < EV::NOUT; q++) tot[q] = R::zero();
+      for (unsigned b = lane; b < G; b += 32) {
+#pragma unroll
+        for (int q = 0; q < EV::NOUT; q++) {
+          W pv;
+          const uint32_t* src =
+              reinterpret_cast<const uint32_t*>(partials + (size_t)b * EV::NOUT + q);
+#pragma unroll
+          for (int w = 0; w < (int)(sizeof(W) / 4); w++)
+            reinterpret_cast<uint32_t*>(&pv)[w] = __ldcg(src + w);
+          tot[q] = R::add(tot[q], pv);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < EV::NOUT; q++) {
+#pragma unroll
+        for (int off = 16; off; off >>= 1) tot[q] = R::add(tot[q], R::shfl_down(tot[q], off));
+      }
+      if (lane == 0 && j == j1 - 1) atomicExch(ticket, 0u);  // every block has arrived
+      publish_sums<F, EV::NOUT>(tot, seq, mb, s_words);
+      if (trace && lane == 0) trace[j * 8 + 3] = globaltimer();
+    }
+    if (j == j1 - 1 && j1 < num_vars) return;  // the cluster kernel takes over
+    // wait for r_j: warp 0 polls (the host mailbox directly, or block 0
+    // polls it and relays through an L2 slot)
+    if (warp == 0) {
+      __shared__ uint32_t cw[NC];
+      bool ok;
+      if (direct || blockIdx.x == 0) {
+        ok = warp_poll<NC>(mb->ch, seq, cw, &mb->abort);
+        if (!direct && ok && lane < NC)
+          reinterpret_cast<volatile uint64_t*>(bcast)[lane] = tag(cw[lane], seq);
+      } else {
+        ok = warp_poll<NC>(bcast, seq, cw, nullptr);
+      }
+      if (lane == 0) {
+        if (!ok) {
+          *fail = 1;
+          mb->status = 1;
+          if (!direct && blockIdx.x == 0) {
+#pragma unroll
+            for (int i = 0; i < NC; i++)
+              reinterpret_cast<volatile uint64_t*>(bcast)[i] = tag(0, 0xffffffffu);
+          }
+        }
+        s_flag = ok ? 0 : 2;
+        s_r = Words<F>::load(cw);
+        if (tr0) trace[j * 8 + 4] = globaltimer();
+      }
+    }
+    __syncthreads();
+    if (s_flag == 2) return;
+    r = s_r;
+  }
+  // final fold of the size-2 tables by the last challenge (sumcheck.py:129-130)
+  if (blockIdx.x == 0) publish_finals<F, MAXK>(tabs, k, r, seq0 + (uint32_t)num_vars + 1, mb);
+}
+
+// ---------------------------------------------------------------------------
+// Cluster kernel (small rounds): ONE thread-block cluster of up to 16 CTAs.
+// Block partials meet in CTA 0's shared memory over DSMEM after a cluster
+// barrier; CTA 0 publishes, polls the challenge and writes it into every
+// CTA's shared memory; a second cluster barrier releases the next round
+// (its release/acquire also orders this round's in-place table writes).
+// No L2 tickets, no grid barrier.  Runs rounds [j0, num_vars); for j0 > 0 it
+// starts by fetching r_{j0-1} from the mailbox (handoff from the grid kernel).
+constexpr int kClusterMax = 16;
+constexpr int kClusterThreads = 256;
+
+template <class F, int MAXK, class EV>
+__global__ void __launch_bounds__(kClusterThreads)
+    k_sumcheck_cluster(TablePtrs<F, MAXK> tabs, int k, int num_vars, int j0, Terms<F> tm,
+                       Mailbox* mb, unsigned* fail, uint32_t seq0, uint64_t* trace, int L) {
+  using T = typename F::T;
+  using R = Red<F>;
+  using W = typename R::W;
+  constexpr int NC = Words<F>::N;
+  cg::cluster_group cluster = cg::this_cluster();
+  const unsigned rank = cluster.block_rank(), C = cluster.num_blocks();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  __shared__ W wsum[kClusterThreads / 32][EV::NOUT];
+  __shared__ W s_part[EV::NOUT];           // this CTA's partial (read by CTA 0)
+  __shared__ T s_r;                        // challenge (written by CTA 0)
+  __shared__ int s_flag;
+  __shared__ uint64_t s_words[kMbEvalWords];
+  const uint64_t nthreads = (uint64_t)C * blockDim.x;
+  const uint64_t gtid = rank * (uint64_t)blockDim.x + threadIdx.x;
+  T r = F::zero();
+  // CTA 0 thread 0: poll r_{seq-1} and hand it to every CTA (then barrier)
+  __shared__ uint32_t s_cw[NC];
+  auto fetch_challenge = [&](uint32_t seq) {
+    if (rank == 0 && warp == 0) {
+      const bool ok = warp_poll<NC>(mb->ch, seq, s_cw, &mb->abort);
+      if (lane == 0) {
+        if (!ok) {
+          *fail = 1;
+          mb->status = 1;
+        }
+        s_r = Words<F>::load(s_cw);
+        s_flag = ok ? 0 : 2;
+      }
+      __syncwarp();
+      if (lane < (int)C) {  // lane b copies into CTA b
+        *cluster.map_shared_rank(&s_r, lane) = s_r;
+        *cluster.map_shared_rank(&s_flag, lane) = s_flag;
+      }
+    }
+    cluster.sync();
+  };
+  if (j0 > 0) {
+    fetch_challenge(seq0 + (uint32_t)j0);
+    if (s_flag == 2) return;
+    r = s_r;
+  }
+  for (int j = j0; j < num_vars; j++) {
+    const uint32_t seq = seq0 + (uint32_t)j + 1;
+    const bool fold = j > 0;
+    const bool tr0 = trace && rank == 0 && threadIdx.x == 0;
+    if (tr0) trace[j * 8 + 0] = globaltimer();
+    const uint64_t half = 1ull << (num_vars - 1 - j);
+    accumulate_round<F, MAXK, EV>(tabs, k, tm, half, fold, r, L, gtid, nthreads, wsum);
+    if (tr0) trace[j * 8 + 1] = globaltimer();
+    __syncthreads();
+    if (warp == 0) {
+      W v[EV::NOUT];
+      block_total<F, EV::NOUT>(wsum, nwarps, v);
+      if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < EV::NOUT; q++) s_part[q] = v[q];
+      }
+    }
+    cluster.sync();  // every CTA's partial is in its shared memory
+    if (tr0) trace[j * 8 + 2] = globaltimer();
+    if (rank == 0 && warp == 0) {
+      W tot[EV::NOUT];
+#pragma unroll
+      for (int q = 0; q < EV::NOUT; q++) {
+        W pv = lane < (int)C ? *cluster.map_shared_rank(&s_part[q], lane) : R::zero();
+#pragma unroll
+        for (int off = 16; off; off >>= 1) pv = R::add(pv, R::shfl_down(pv, off));
+        tot[q] = pv;
+      }
+      publish_sums<F, EV::NOUT>(tot, seq, mb, s_words);
+      if (trace && lane == 0) trace[j * 8 + 3] = globaltimer();
+    }
+    fetch_challenge(seq);
+    if (tr0) trace[j * 8 + 4] = globaltimer();
+    if (s_flag == 2) return;
+    r = s_r;
+  }
+  if (rank == 0) publish_finals<F, MAXK>(tabs, k, r, seq0 + (uint32_t)num_vars + 1, mb);
+}
+
+// ---------------------------------------------------------------------------
+// Launch planning.  A Montgomery product is ~500 SASS instructions, so a
+// round whose pairs all fit in one wave is issue-bound per SM sub-partition,
+// not memory-bound: spread large rounds over many SMs with few warps each
+// (block size = ceil(threads / SMs) rounded to a warp, 32..256), and run the
+// small rounds (threads <= one cluster) in the cluster kernel.
+inline int block_for(uint64_t threads, int sms) {
+  uint64_t per_sm = (threads + sms - 1) / sms;
+  uint64_t bs = (per_sm + 31) / 32 * 32;
+  if (bs < 32) bs = 32;
+  if (bs > (uint64_t)kThreads) bs = kThreads;
+  return (int)bs;
+}
+
+struct Plan {
+  int j_switch;      // rounds [0, j_switch) grid kernel, [j_switch, n) cluster kernel
+  int grid, block;   // grid kernel shape
+  int cgrid, cblock; // cluster kernel shape (one cluster)
+  int lanes;
+};
+
 template <class F, int MAXK, class EV>
 struct Persistent {
-  static int grid(uint64_t half0) {
-    static int per_sm = -1;
-    if (per_sm < 0) {
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-              &per_sm, k_sumcheck_persistent<F, MAXK, EV>, 256, 0) != cudaSuccess ||
-          per_sm < 1)
-        per_sm = 1;
-    }
-    int dev = 0, sms = kSMs;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    uint64_t cap = (uint64_t)sms * per_sm;
-    uint64_t want = (half0 + 255) / 256;
-    return (int)(want < 1 ? 1 : (want > cap ? cap : want));
-  }
-  static int launch(void* const* tables, int k, int num_vars, const Terms<F>& tm, Mailbox* mb,
-                    typename F::T* partials, typename F::T* rbuf, unsigned* fail,
-                    uint64_t* trace, unsigned grid, cudaStream_t s) {
+  static int launch_grid(const Plan& pl, void* const* tables, int k, int num_vars,
+                         const Terms<F>& tm, Mailbox* mb, typename Red<F>::W* partials,
+                         unsigned* ticket, uint64_t* bcast, unsigned* fail, uint32_t seq0,
+                         uint64_t* trace, cudaStream_t s) {
     TablePtrs<F, MAXK> tp;
     for (int j = 0; j < MAXK; j++) tp.t[j] = j < k ? (typename F::T*)tables[j] : nullptr;
     Terms<F> tmc = tm;
-    void* args[] = {&tp, &k, &num_vars, &tmc, &mb, &partials, &rbuf, &fail, &trace};
-    ZKL_CUDA(cudaLaunchCooperativeKernel((const void*)k_sumcheck_persistent<F, MAXK, EV>, grid,
-                                         256, args, 0, s));
+    static const unsigned direct_max = [] {
+      const char* e = getenv("ZKL_DIRECT_POLL_MAX");
+      return e ? (unsigned)atoi(e) : (unsigned)kDirectPollMaxGrid;
+    }();
+    int direct = (unsigned)pl.grid <= direct_max ? 1 : 0;
+    int L = pl.lanes, j0 = 0, j1 = pl.j_switch;
+    void* args[] = {&tp, &k, &num_vars, &j0, &j1, &tmc, &mb, &partials, &ticket, &bcast,
+                    &fail, &seq0, &direct, &trace, &L};
+    ZKL_CUDA(cudaLaunchCooperativeKernel((const void*)k_sumcheck_persistent<F, MAXK, EV>,
+                                         pl.grid, pl.block, args, 0, s));
     ZKL_LAUNCH_CHECK();
     return kOk;
+  }
+  static int launch_cluster(const Plan& pl, void* const* tables, int k, int num_vars,
+                            const Terms<F>& tm, Mailbox* mb, unsigned* fail, uint32_t seq0,
+                            uint64_t* trace, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+      ZKL_CUDA(cudaFuncSetAttribute((const void*)k_sumcheck_cluster<F, MAXK, EV>,
+                                    cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      attr = true;
+    }
+    TablePtrs<F, MAXK> tp;
+    for (int j = 0; j < MAXK; j++) tp.t[j] = j < k ? (typename F::T*)tables[j] : nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(pl.cgrid);
+    cfg.blockDim = dim3(pl.cblock);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = pl.cgrid;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    ZKL_CUDA(cudaLaunchKernelEx(&cfg, k_sumcheck_cluster<F, MAXK, EV>, tp, k, num_vars,
+                                pl.j_switch, tm, mb, fail, seq0, trace, pl.lanes));
+    ZKL_LAUNCH_CHECK();
+    return kOk;
+  }
+  static Plan plan(int num_vars, int lanes) {
+    static int per_sm = -1, sms = kSMs;
+    if (per_sm < 0) {
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+              &per_sm, k_sumcheck_persistent<F, MAXK, EV>, kThreads, 0) != cudaSuccess ||
+          per_sm < 1)
+        per_sm = 1;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    Plan pl;
+    pl.lanes = lanes;
+    const uint64_t per_pair = lanes > 0 ? (uint64_t)lanes : 1;
+    // cluster: up to 16 CTAs x 256 threads; lane mode loops when a round
+    // has more pairs than lane groups (at most kClusterPasses passes)
+    const uint64_t cap = (uint64_t)kClusterMax * kClusterThreads;
+    const uint64_t kClusterPasses = 4;
+    int js = 0;
+    while (js < num_vars && (1ull << (num_vars - 1 - js)) * per_pair > cap * kClusterPasses) js++;
+    pl.j_switch = js;
+    const uint64_t want_c = (1ull << (num_vars - 1 - js)) * per_pair;  // threads, round js
+    int cb = kClusterThreads, cg_ = kClusterMax;
+    if (want_c < cap) {  // shrink: fewer CTAs first, then fewer threads
+      cg_ = (int)((want_c + kClusterThreads - 1) / kClusterThreads);
+      if (cg_ < 1) cg_ = 1;
+      if (cg_ == 1) {
+        cb = (int)((want_c + 31) / 32 * 32);
+        if (cb < 32) cb = 32;
+      }
+    }
+    pl.cgrid = cg_;
+    pl.cblock = cb;
+    const uint64_t want = (1ull << (num_vars - 1)) * per_pair;
+    const int bs = block_for(want, sms);
+    pl.block = bs;
+    uint64_t gcap = (uint64_t)sms * per_sm * (kThreads / bs);
+    if (gcap > 65535) gcap = 65535;
+    uint64_t g = (want + bs - 1) / bs;
+    pl.grid = (int)(g < 1 ? 1 : (g > gcap ? gcap : g));
+    return pl;
   }
 };
 
 template <class F>
-static int detect_shape(const Terms<F>& tm) {
-  if (tm.nterms == 1 && tm.nf[0] == 2) return kProd2;
-  if (tm.nterms == 1 && tm.nf[0] == 3) return kProd3;
-  if (tm.nterms == 2 && tm.nf[0] == 2 && tm.nf[1] == 2 && tm.fi[0][0] == tm.fi[1][0])
+int detect_shape(const Terms<F>& tm) {
+  if (tm.nterms == 1 && tm.nf[0] == 2 && tm.degree >= 2) return kProd2;
+  if (tm.nterms == 1 && tm.nf[0] == 3 && tm.degree == 3) return kProd3;
+  if (tm.nterms == 2 && tm.nf[0] == 2 && tm.nf[1] == 2 && tm.fi[0][0] == tm.fi[1][0] &&
+      tm.degree >= 2)
     return kSum2Prod2;
   return kGeneric;
 }
 
+template <class F>
+struct LaunchReq {
+  int shape, k, num_vars;
+  void* const* tables;
+  const Terms<F>* tm;
+  Mailbox* mb;
+  typename Red<F>::W* partials;
+  unsigned *ticket, *fail;
+  uint64_t* bcast;
+  uint32_t seq0;
+  uint64_t* trace;
+  cudaStream_t s;
+};
+
+// query (pl != null, launch == false): fill the plan; launch: both kernels
 template <class F, int MAXK>
-static int dispatch(int shape, bool query, uint64_t half0, int* grid_out, void* const* tables,
-                    int k, int num_vars, const Terms<F>& tm, Mailbox* mb, typename F::T* partials,
-                    typename F::T* rbuf, unsigned* fail, uint64_t* trace, cudaStream_t s,
-                    int* nout) {
+static int dispatch(const LaunchReq<F>& q, Plan* pl, int* nout, bool launch) {
 #define ZKL_SHAPE(EVT)                                                                      \
   {                                                                                         \
     using P = Persistent<F, MAXK, EVT<F, MAXK>>;                                            \
     *nout = EVT<F, MAXK>::NOUT;                                                             \
-    if (query) { *grid_out = P::grid(half0); return kOk; }                                  \
-    return P::launch(tables, k, num_vars, tm, mb, partials, rbuf, fail, trace,              \
-                     (unsigned)*grid_out, s);                                                \
+    if (!launch) {                                                                          \
+      *pl = P::plan(q.num_vars, lanes_for(q.shape, q.k));                                  \
+      return kOk;                                                                           \
+    }                                                                                       \
+    int rc_ = kOk;                                                                          \
+    if (pl->j_switch > 0)                                                                   \
+      rc_ = P::launch_grid(*pl, q.tables, q.k, q.num_vars, *q.tm, q.mb, q.partials,         \
+                           q.ticket, q.bcast, q.fail, q.seq0, q.trace, q.s);                \
+    if (rc_ == kOk && pl->j_switch < q.num_vars)                                            \
+      rc_ = P::launch_cluster(*pl, q.tables, q.k, q.num_vars, *q.tm, q.mb, q.fail, q.seq0,  \
+                              q.trace, q.s);                                                \
+    return rc_;                                                                             \
   }
-  switch (shape) {
+  switch (q.shape) {
     case kProd2: ZKL_SHAPE(EvProd2)
     case kProd3: ZKL_SHAPE(EvProd3)
     case kSum2Prod2: ZKL_SHAPE(EvSum2Prod2)
@@ -366,35 +950,298 @@ static int dispatch(int shape, bool query, uint64_t half0, int* grid_out, void* 
 }
 
 template <class F>
-static int run_dispatch(int shape, bool query, uint64_t half0, int* grid, void* const* tables,
-                        int k, int num_vars, const Terms<F>& tm, Mailbox* mb,
-                        typename F::T* partials, typename F::T* rbuf, unsigned* fail,
-                        uint64_t* trace, cudaStream_t s, int* nout) {
-  if (k <= 2)
-    return dispatch<F, 2>(shape, query, half0, grid, tables, k, num_vars, tm, mb, partials, rbuf,
-                          fail, trace, s, nout);
-  if (k <= 4)
-    return dispatch<F, 4>(shape, query, half0, grid, tables, k, num_vars, tm, mb, partials, rbuf,
-                          fail, trace, s, nout);
-  return dispatch<F, 8>(shape, query, half0, grid, tables, k, num_vars, tm, mb, partials, rbuf,
-                        fail, trace, s, nout);
+static int run_dispatch(const LaunchReq<F>& q, Plan* pl, int* nout, bool launch) {
+  if (q.k <= 2) return dispatch<F, 2>(q, pl, nout, launch);
+  if (q.k <= 4) return dispatch<F, 4>(q, pl, nout, launch);
+  return dispatch<F, 8>(q, pl, nout, launch);
 }
 
-// host: raw sums (Montgomery) -> canonical evaluations
+// ---------------------------------------------------------------------------
+// host side
 template <class F>
-static void host_evals(int shape, const Terms<F>& tm, const typename F::T* raw,
-                       const typename F::T& add, const typename F::T& mul, uint8_t* out) {
-  using T = typename F::T;
-  for (int x = 0; x <= tm.degree; x++) {
-    T v;
-    switch (shape) {
-      case kProd2:
-      case kProd3: v = F::mul(tm.coef[0], raw[x]); break;
-      case kSum2Prod2: v = F::add(F::mul(tm.coef[0], raw[x]), F::mul(tm.coef[1], raw[4 + x])); break;
-      default: v = raw[x];
-    }
-    store_canon<F>(out + x * F::kBytes, F::mul(mul, F::add(v, add)));
+struct HostRed;
+template <>
+struct HostRed<Fr255> {
+  // words: 9 x u32 = lo (256 bits) + w8 * 2^256 -> residue (storage form)
+  static fr_t reduce(const uint32_t* w) {
+    fr_t lo;
+    memcpy(&lo, w, 32);
+    for (int k = 0; k < 2; k++)  // lo < 2^256 < 3p
+      if (Fr255::geq_p_portable(lo)) lo = Fr255::sub_p_portable(lo);
+    if (w[8] == 0) return lo;
+    fr_t h = Fr255::zero();
+    h.v[0] = w[8];
+    h = host::Fr::mul(h, Fr255::r2());  // w8 * 2^256 mod p
+    return host::Fr::add(lo, h);
   }
+};
+template <>
+struct HostRed<M61> {
+  static uint64_t reduce(const uint32_t* w) {
+    const unsigned __int128 v =
+        ((unsigned __int128)(((uint64_t)w[3] << 32) | w[2]) << 64) | (((uint64_t)w[1] << 32) | w[0]);
+    return (uint64_t)(v % M61::P);
+  }
+};
+
+template <class F>
+static bool mailbox_ready(const volatile uint64_t* src, int nwords, uint32_t seq, uint32_t* out) {
+  for (int i = 0; i < nwords; i++) {
+    const uint64_t v = src[i];
+    if ((uint32_t)(v >> 32) != seq) return false;
+    out[i] = (uint32_t)v;
+  }
+  return true;
+}
+
+template <class F>
+static int wait_words(Mailbox* mb, const volatile uint64_t* src, int nwords, uint32_t seq,
+                      uint32_t* out, cudaStream_t s, const char* what, int round) {
+  const auto until = std::chrono::steady_clock::now() + std::chrono::seconds(30);
+  uint64_t spins = 0;
+  while (!mailbox_ready<F>(src, nwords, seq, out)) {
+    if ((++spins & 0xffff) == 0) {
+      if (mb->status) {
+        set_error("persistent sumcheck: device gave up waiting (round %d)", round);
+        return kErrCuda;
+      }
+      cudaError_t q = cudaStreamQuery(s);
+      if (q != cudaErrorNotReady && !mailbox_ready<F>(src, nwords, seq, out)) {
+        set_error("persistent sumcheck ended before publishing %s of round %d: %s", what, round,
+                  cudaGetErrorString(q == cudaSuccess ? cudaErrorUnknown : q));
+        return kErrCuda;
+      }
+      if (std::chrono::steady_clock::now() > until) {
+        mb->abort = 1;
+        cudaStreamSynchronize(s);
+        set_error("persistent sumcheck: device did not publish %s of round %d", what, round);
+        return kErrCuda;
+      }
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  return kOk;
+}
+
+template <class F>
+static void host_quad(const typename F::T& c0, const typename F::T& c1, const typename F::T& c2,
+                      typename F::T* out) {
+  using H = typename host::For<F>::H;
+  using T = typename F::T;
+  const T two_c1 = H::add(c1, c1), two_c2 = H::add(c2, c2);
+  out[0] = c0;
+  out[1] = c1;
+  out[2] = H::sub(H::add(two_c1, two_c2), c0);
+  const T six_c2 = H::add(H::add(two_c2, two_c2), two_c2);
+  out[3] = H::sub(H::add(H::add(two_c1, c1), six_c2), H::add(c0, c0));
+}
+
+static bool g_phase_dirty = true;  // after a failure the ticket / flags need a reset
+
+template <class F>
+int wait_phase_finals(const PhaseArgs<F>& a, typename F::T* finals_out, cudaStream_t s) {
+  constexpr int NC = Words<F>::N;
+  Mailbox* mb_host;
+  Mailbox* mb_dev;
+  int rc = mailbox_for_current_device(&mb_host, &mb_dev);
+  if (rc) return rc;
+  uint32_t fw[kMbFinalWords];
+  rc = wait_words<F>(mb_host, mb_host->fin, a.k * NC, a.seq0 + a.num_vars + 1, fw, s, "finals",
+                     a.num_vars);
+  if (rc) {
+    g_phase_dirty = true;
+    return rc;
+  }
+  for (int q = 0; q < a.k; q++) memcpy(&finals_out[q], fw + q * NC, F::kBytes);
+  return kOk;
+}
+
+template <class F>
+int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t* point_out,
+              typename F::T* finals_out, cudaStream_t s) {
+  using T = typename F::T;
+  using H = typename host::For<F>::H;
+  using W = typename Red<F>::W;
+  constexpr int NW = Red<F>::NW, NC = Words<F>::N, nb = F::kBytes;
+  const Terms<F>& tm = a.tm;
+  const int n = a.num_vars, k = a.k, deg = tm.degree;
+  if (k < 1 || k > kMaxTables || tm.nterms < 0 || tm.nterms > kMaxTerms || deg < 0 || deg > 3 ||
+      n < 1 || n > 63) {
+    set_error("sumcheck_prove: bad arguments");
+    return kErrArg;
+  }
+  Mailbox* mb_host;
+  Mailbox* mb_dev;
+  int rc = mailbox_for_current_device(&mb_host, &mb_dev);
+  if (rc) return rc;
+  const int shape = detect_shape<F>(tm);
+  LaunchReq<F> rq;
+  rq.shape = shape;
+  rq.k = k;
+  rq.num_vars = n;
+  rq.tables = a.tables;
+  rq.tm = &a.tm;
+  rq.s = s;
+  Plan pl;
+  int nout = 4;
+  run_dispatch<F>(rq, &pl, &nout, false);
+  void* ws;
+  rc = scratch_reserve((size_t)pl.grid * 8 * sizeof(W), &ws, s);
+  if (rc) return rc;
+  void* fx;
+  rc = fixed_words(&fx);
+  if (rc) return rc;
+  unsigned* fail = (unsigned*)((char*)fx + kFixedFail);
+  unsigned* ticket = (unsigned*)((char*)fx + kFixedPhaseTicket);
+  uint64_t* bcast = (uint64_t*)((char*)fx + kFixedBcast);
+  if (g_phase_dirty) {
+    ZKL_CUDA(cudaMemsetAsync((char*)fx + kFixedFail, 0, 4, s));
+    ZKL_CUDA(cudaMemsetAsync((char*)fx + kFixedPhaseTicket, 0, 4, s));
+    g_phase_dirty = false;
+  }
+  if (mb_host->seq > 0x7fff0000u) {  // tags wrap: restart (bcast tags too)
+    ZKL_CUDA(cudaStreamSynchronize(s));
+    memset((void*)mb_host, 0, sizeof(Mailbox));
+    ZKL_CUDA(cudaMemsetAsync((char*)fx + kFixedBcast, 0, 8 * 8, s));
+    mb_host->seq = 1;
+  }
+  if (mb_host->seq == 0) mb_host->seq = 1;
+  const uint32_t seq0 = mb_host->seq;
+  mb_host->seq = seq0 + (uint32_t)n + 2;
+  mb_host->abort = 0;
+  mb_host->status = 0;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  // ZKL_TRACE=1: per-round device timestamps + host handling times (stderr)
+  static const bool tracing = getenv("ZKL_TRACE") != nullptr;
+  uint64_t* trace = nullptr;
+  std::vector<double> h_seen, h_sent;
+  if (tracing) {
+    ZKL_CUDA(cudaMalloc(&trace, (size_t)n * 8 * 8));
+    ZKL_CUDA(cudaMemsetAsync(trace, 0, (size_t)n * 8 * 8, s));
+    h_seen.resize(n);
+    h_sent.resize(n);
+  }
+  auto now_us = [] {
+    return std::chrono::duration<double, std::micro>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+  };
+  rq.mb = mb_dev;
+  rq.partials = (W*)ws;
+  rq.ticket = ticket;
+  rq.fail = fail;
+  rq.bcast = bcast;
+  rq.seq0 = seq0;
+  rq.trace = trace;
+  rc = run_dispatch<F>(rq, &pl, &nout, true);
+  if (rc) return rc;
+  a.seq0 = seq0;
+  // host-side finishing constants (canonical multipliers: mul(raw_storage,
+  // K_canon) = value * K in canonical form), set at round 0 after prepare()
+  T Kc[2];
+  T pm = a.post_mul;
+  std::vector<T> lazy_add;
+  bool prepared = !a.prepare;
+  uint32_t words[kMbEvalWords];
+  std::vector<double> h_first;
+  if (tracing) h_first.resize(n);
+  for (int j = 0; j < n; j++) {
+    if (tracing) {  // first tagged word of this round visible
+      while ((uint32_t)(mb_host->ev[0] >> 32) != seq0 + j + 1 && !mb_host->status) {
+      }
+      h_first[j] = now_us();
+    }
+    rc = wait_words<F>(mb_host, mb_host->ev, nout * NW, seq0 + j + 1, words, s, "sums", j);
+    if (rc) {
+      g_phase_dirty = true;
+      return rc;
+    }
+    if (tracing) h_seen[j] = now_us();
+    if (!prepared) {
+      rc = a.prepare(lazy_add);
+      if (rc) {
+        mb_host->abort = 1;
+        cudaStreamSynchronize(s);
+        g_phase_dirty = true;
+        return rc;
+      }
+      if (!lazy_add.empty()) a.post_add = lazy_add.data();
+      prepared = true;
+    }
+    if (j == 0) {
+      pm = a.post_mul;
+      if (shape == kGeneric) {
+        Kc[0] = host::canon_of<F>(pm);
+      } else {
+        Kc[0] = host::canon_of<F>(H::mul(pm, a.tm.coef[0]));
+        if (shape == kSum2Prod2) Kc[1] = host::canon_of<F>(H::mul(pm, a.tm.coef[1]));
+      }
+    }
+    T raw[8];
+    for (int q = 0; q < nout; q++) raw[q] = HostRed<F>::reduce(words + q * NW);
+    T ev[4];
+    if (shape == kProd2) {
+      host_quad<F>(raw[0], raw[1], raw[2], ev);
+      for (int x = 0; x < 4; x++) ev[x] = H::mul(ev[x], Kc[0]);
+    } else if (shape == kSum2Prod2) {
+      T e1[4], e2[4];
+      host_quad<F>(raw[0], raw[1], raw[2], e1);
+      host_quad<F>(raw[3], raw[4], raw[5], e2);
+      for (int x = 0; x < 4; x++) ev[x] = H::add(H::mul(e1[x], Kc[0]), H::mul(e2[x], Kc[1]));
+    } else {
+      for (int x = 0; x < 4; x++) ev[x] = H::mul(raw[x], Kc[0]);
+    }
+    if (a.post_add) {
+      const T addc = host::canon_of<F>(H::mul(pm, a.post_add[j]));
+      for (int x = 0; x < 4; x++) ev[x] = H::add(ev[x], addc);
+    }
+    uint8_t* rj = rounds_out + (size_t)j * (deg + 1) * nb;
+    for (int x = 0; x <= deg; x++) {
+      memcpy(rj + x * nb, &ev[x], nb);
+      tr.append_elem("sumcheck/eval", rj + x * nb, nb);
+    }
+    uint8_t rawc[64];
+    tr.challenge_squeeze("sumcheck/round", 14, rawc);
+    uint8_t* rcan = point_out + (size_t)j * nb;
+    reduce512<F>(rawc, rcan);
+    const T rm = host::from_canon<F>(rcan);
+    uint32_t cw[NC];
+    memcpy(cw, &rm, nb);
+    const uint64_t tg = (uint64_t)(seq0 + j + 1) << 32;
+    for (int w = 0; w < NC; w++) mb_host->ch[w] = tg | cw[w];
+    std::atomic_thread_fence(std::memory_order_seq_cst);  // drain the store buffer now
+    if (tracing) h_sent[j] = now_us();
+    tr.challenge_absorb(rawc);
+  }
+  if (finals_out) {
+    rc = wait_phase_finals<F>(a, finals_out, s);
+    if (rc) return rc;
+  }
+  if (tracing) {
+    std::vector<uint64_t> tv((size_t)n * 8);
+    cudaMemcpyAsync(tv.data(), trace, tv.size() * 8, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    cudaFree(trace);
+    double acc[5] = {0}, hs = 0, loop = 0, hgap = 0, hfill = 0;
+    for (int j = 0; j < n; j++) {
+      hfill += h_seen[j] - h_first[j];
+      if (j > 0) hgap += h_first[j] - h_sent[j - 1];
+      const uint64_t* t = &tv[(size_t)j * 8];
+      acc[0] += (t[1] - t[0]) / 1e3;                      // accumulate
+      acc[1] += (t[2] - t[1]) / 1e3;                      // block reduce + ticket
+      acc[2] += t[3] ? (t[3] - t[2]) / 1e3 : 0;           // last-block sum + publish
+      acc[3] += t[4] ? (t[4] - (t[3] ? t[3] : t[2])) / 1e3 : 0;  // wait for challenge
+      if (j + 1 < n && t[4]) loop += (tv[(size_t)(j + 1) * 8] - t[4]) / 1e3;
+      hs += h_sent[j] - h_seen[j];
+    }
+    fprintf(stderr,
+            "[zkl trace] n=%d k=%d shape=%d grid=%dx%d->%d cluster=%dx%d per-round us: accum "
+            "%.2f | reduce %.2f | publish %.2f | wait-challenge %.2f | to-next %.2f | host %.2f "
+            "| host: sent->next-first %.2f, first->all %.2f\n",
+            n, k, shape, pl.grid, pl.block, pl.j_switch, pl.cgrid, pl.cblock, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n,
+            n > 1 ? loop / (n - 1) : 0.0, hs / n, n > 1 ? hgap / (n - 1) : 0.0, hfill / n);
+  }
+  return kOk;
 }
 
 template <class F>
@@ -417,9 +1264,9 @@ int op_sumcheck_prove(void* const* tables, int k, int num_vars, const Terms<F>& 
   static const bool no_persistent =
       getenv("ZKL_NO_PERSISTENT") != nullptr || getenv("CUDA_INJECTION64_PATH") != nullptr ||
       (getenv("CUDA_LAUNCH_BLOCKING") && getenv("CUDA_LAUNCH_BLOCKING")[0] == '1');
+  HostTranscript tr;
+  memcpy(tr.state, state, 64);
   if (no_persistent) {
-    HostTranscript tr;
-    memcpy(tr.state, state, 64);
     uint64_t size = 1ull << num_vars;
     T r_prev = F::zero();
     for (int j = 0; j < num_vars; j++) {
@@ -437,112 +1284,30 @@ int op_sumcheck_prove(void* const* tables, int k, int num_vars, const Terms<F>& 
     memcpy(state, tr.state, 64);
     return op_sumcheck_finish<F>(tables, k, r_prev, finals_out, s);
   }
-  Mailbox* mb_host;
-  Mailbox* mb_dev;
-  int rc = mailbox_for_current_device(&mb_host, &mb_dev);
+  PhaseArgs<F> a;
+  a.tables = tables;
+  a.k = k;
+  a.num_vars = num_vars;
+  a.tm = tm;
+  a.post_add = post_add;
+  a.post_mul = post_mul;
+  std::vector<T> fin(k);
+  int rc = run_phase<F>(a, tr, rounds_out, point_out, fin.data(), s);
   if (rc) return rc;
-  const int shape = detect_shape<F>(tm);
-  const uint64_t half0 = 1ull << (num_vars - 1);
-  int grid = 0, nout = 4;
-  run_dispatch<F>(shape, true, half0, &grid, tables, k, num_vars, tm, nullptr, nullptr, nullptr,
-                  nullptr, nullptr, s, &nout);
-  size_t need = (size_t)grid * 8 * 8 * sizeof(T);  // warps x NOUT (<= 8)
-  void* ws;
-  rc = scratch_reserve(need, &ws, s);
-  if (rc) return rc;
-  void* fx;
-  rc = fixed_words(&fx);
-  if (rc) return rc;
-  unsigned* fail = (unsigned*)((char*)fx + kFixedFail);
-  T* rbuf = (T*)((char*)fx + kFixedRbuf);
-  T* partials = (T*)ws;
-  ZKL_CUDA(cudaMemsetAsync(fail, 0, sizeof(unsigned), s));
-  mb_host->ev_seq = 0;
-  mb_host->ch_seq = 0;
-  mb_host->abort = 0;
-  mb_host->status = 0;
-  std::atomic_thread_fence(std::memory_order_seq_cst);
-
-  static const bool tracing = getenv("ZKL_TRACE") != nullptr;
-  uint64_t* trace = nullptr;
-  std::vector<double> host_seen(num_vars), host_sent(num_vars);
-  if (tracing) ZKL_CUDA(cudaMalloc(&trace, (size_t)num_vars * 6 * 8));
-  rc = run_dispatch<F>(shape, false, half0, &grid, tables, k, num_vars, tm, mb_dev, partials,
-                       rbuf, fail, trace, s, &nout);
-  if (rc) return rc;
-
-  auto now_us = [] {
-    return std::chrono::duration<double, std::micro>(
-               std::chrono::steady_clock::now().time_since_epoch())
-        .count();
-  };
-  HostTranscript tr;
-  memcpy(tr.state, state, 64);
-  T raw[8];
-  for (int j = 0; j < num_vars; j++) {
-    const auto until = std::chrono::steady_clock::now() + std::chrono::seconds(30);
-    uint64_t spins = 0;
-    while (mb_host->ev_seq != (uint32_t)(j + 1)) {
-      if ((++spins & 0xffff) == 0) {
-        cudaError_t q = cudaStreamQuery(s);
-        if (q != cudaErrorNotReady) {
-          set_error("persistent sumcheck ended early at round %d: %s", j,
-                    cudaGetErrorString(q == cudaSuccess ? cudaErrorUnknown : q));
-          return kErrCuda;
-        }
-        if (std::chrono::steady_clock::now() > until) {
-          mb_host->abort = 1;
-          cudaStreamSynchronize(s);
-          set_error("persistent sumcheck: device did not publish round %d", j);
-          return kErrCuda;
-        }
-      }
-    }
-    std::atomic_thread_fence(std::memory_order_acquire);
-    if (tracing) host_seen[j] = now_us();
-    memcpy(raw, (const void*)mb_host->evals, (size_t)nout * sizeof(T));
-    uint8_t* rj = rounds_out + (size_t)j * (tm.degree + 1) * nb;
-    host_evals<F>(shape, tm, raw, post_add ? post_add[j] : F::zero(), post_mul, rj);
-    for (int x = 0; x <= tm.degree; x++) tr.append_elem("sumcheck/eval", rj + x * nb, nb);
-    uint8_t* rc_out = point_out + (size_t)j * nb;
-    challenge_canon<F>(tr, "sumcheck/round", rc_out);
-    T rm = load_canon<F>(rc_out);  // Montgomery form for the device
-    memcpy((void*)mb_host->chal, &rm, nb);
-    std::atomic_thread_fence(std::memory_order_seq_cst);
-    mb_host->ch_seq = (uint32_t)(j + 1);
-    if (tracing) host_sent[j] = now_us();
-  }
-  ZKL_CUDA(cudaStreamSynchronize(s));
-  if (mb_host->status) {
-    set_error("persistent sumcheck: device timed out waiting for a challenge");
-    return kErrCuda;
-  }
-  memcpy(finals_out, (const void*)mb_host->finals, (size_t)k * nb);
+  for (int q = 0; q < k; q++) host::to_canon<F>(finals_out + (size_t)q * nb, fin[q]);
   memcpy(state, tr.state, 64);
-  if (tracing) {
-    std::vector<uint64_t> tv((size_t)num_vars * 6);
-    cudaMemcpy(tv.data(), trace, tv.size() * 8, cudaMemcpyDeviceToHost);
-    cudaFree(trace);
-    double acc[6] = {0}, hs = 0;
-    for (int j = 0; j < num_vars; j++) {
-      for (int q = 1; q < 6; q++) acc[q] += (double)(tv[j * 6 + q] - tv[j * 6 + q - 1]) / 1000.0;
-      if (j + 1 < num_vars) acc[0] += (double)(tv[(j + 1) * 6] - tv[j * 6 + 5]) / 1000.0;
-      hs += host_sent[j] - host_seen[j];
-    }
-    fprintf(stderr,
-            "[zkl trace] n=%d k=%d shape=%d grid=%d per-round us: accum %.2f | sync1 %.2f | "
-            "reduce+publish %.2f | wait-challenge %.2f | sync2 %.2f | loop %.2f | host %.2f\n",
-            num_vars, k, shape, grid, acc[1] / num_vars, acc[2] / num_vars, acc[3] / num_vars,
-            acc[4] / num_vars, acc[5] / num_vars, acc[0] / num_vars, hs / num_vars);
-  }
   return kOk;
 }
 
-template int op_sumcheck_prove<Fr255>(void* const*, int, int, const Terms<Fr255>&,
-                                      const Fr255::T*, const Fr255::T&, uint8_t*, uint8_t*,
-                                      uint8_t*, uint8_t*, cudaStream_t);
-template int op_sumcheck_prove<M61>(void* const*, int, int, const Terms<M61>&, const M61::T*,
-                                    const M61::T&, uint8_t*, uint8_t*, uint8_t*, uint8_t*,
+#define ZKL_INST_PERSIST(F)                                                                   \
+  template int detect_shape<F>(const Terms<F>&);                                              \
+  template int run_phase<F>(PhaseArgs<F>&, HostTranscript&, uint8_t*, uint8_t*, F::T*,         \
+                            cudaStream_t);                                                    \
+  template int wait_phase_finals<F>(const PhaseArgs<F>&, F::T*, cudaStream_t);                \
+  template int op_sumcheck_prove<F>(void* const*, int, int, const Terms<F>&, const F::T*,     \
+                                    const F::T&, uint8_t*, uint8_t*, uint8_t*, uint8_t*,      \
                                     cudaStream_t);
+ZKL_INST_PERSIST(Fr255)
+ZKL_INST_PERSIST(M61)
 
 }  // namespace zkl

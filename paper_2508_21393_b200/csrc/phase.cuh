@@ -1,0 +1,50 @@
+// Host API of the persistent sumcheck engine (persistent.cu), shared by the
+// C-ABI entry zkl_sumcheck_prove and the native gadget drivers (zkmat.cu).
+#pragma once
+#include <functional>
+#include <vector>
+
+#include "ops.cuh"
+#include "transcript.cuh"
+
+namespace zkl {
+
+enum Shape { kGeneric = 0, kProd2 = 1, kProd3 = 2, kSum2Prod2 = 3 };
+
+template <class F>
+int detect_shape(const Terms<F>& tm);
+
+// One sumcheck (or one phase of a factored gadget) over device tables.
+//   evals[x] = post_mul * (post_add[j] + sum_i combine(terms, t_x(i)))
+// Tables are consumed (folded in place).  Term coefficients and the post
+// scalars are applied on the host for the recognised shapes.
+template <class F>
+struct PhaseArgs {
+  using T = typename F::T;
+  void* const* tables = nullptr;
+  int k = 0;
+  int num_vars = 0;
+  Terms<F> tm;
+  const T* post_add = nullptr;  // num_vars values (storage form) or null
+  T post_mul;                   // storage form
+  // called once before the first round is finished on the host (e.g. to wait
+  // for a device scalar or a previous phase's finals); may fill the vector
+  // with post_add values and may update post_mul / tm.coef (host-applied
+  // for the recognised shapes; the generic shape needs them at launch)
+  std::function<int(std::vector<T>&)> prepare;
+  uint32_t seq0 = 0;  // set by run_phase: mailbox sequence base of the launch
+};
+
+// Runs every round with the native transcript `tr` (appends each evaluation
+// under "sumcheck/eval", draws "sumcheck/round").  Outputs are canonical
+// little-endian: rounds (num_vars x (degree+1)), point (num_vars); finals in
+// storage form (k values).  Does not synchronise the stream.  With
+// finals_out == nullptr it returns right after the last challenge is sent
+// (the kernel is still folding); collect the finals with wait_phase_finals.
+template <class F>
+int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t* point_out,
+              typename F::T* finals_out, cudaStream_t s);
+template <class F>
+int wait_phase_finals(const PhaseArgs<F>& a, typename F::T* finals_out, cudaStream_t s);
+
+}  // namespace zkl

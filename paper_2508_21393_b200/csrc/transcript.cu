@@ -1,9 +1,10 @@
 // Host SHAKE-256 / Keccak-f[1600] (FIPS 202) and the transcript operations.
 #include "transcript.cuh"
+#include "hostfield.h"
 
 namespace zkl {
 
-static const uint64_t kRC[24] = {
+static const uint64_t RC[24] = {
     0x0000000000000001ull, 0x0000000000008082ull, 0x800000000000808Aull, 0x8000000080008000ull,
     0x000000000000808Bull, 0x0000000080000001ull, 0x8000000080008081ull, 0x8000000000008009ull,
     0x000000000000008Aull, 0x0000000000000088ull, 0x0000000080008009ull, 0x000000008000000Aull,
@@ -11,45 +12,55 @@ static const uint64_t kRC[24] = {
     0x8000000000008002ull, 0x8000000000000080ull, 0x000000000000800Aull, 0x800000008000000Aull,
     0x8000000080008081ull, 0x8000000000008080ull, 0x0000000080000001ull, 0x8000000080008008ull};
 
-// rho offsets indexed by lane x + 5y
-static const int kRho[25] = {0,  1,  62, 28, 27, 36, 44, 6,  55, 20, 3,  10, 43,
-                             25, 39, 41, 45, 15, 21, 8,  18, 2,  61, 56, 14};
-
-static inline uint64_t rotl(uint64_t v, int s) { return s ? (v << s) | (v >> (64 - s)) : v; }
-
-// pi destination of lane i = x + 5y is y + 5 * ((2x + 3y) % 5)
-static constexpr int pi_dst(int i) { return (i / 5) + 5 * ((2 * (i % 5) + 3 * (i / 5)) % 5); }
-
-template <int I>
-static inline void rho_pi(const uint64_t* a, uint64_t* b) {
-  b[pi_dst(I)] = rotl(a[I], kRho[I]);
-  if constexpr (I + 1 < 25) rho_pi<I + 1>(a, b);
-}
-
-void keccak_f1600(uint64_t a[25]) {
-  uint64_t b[25];
-  for (int round = 0; round < 24; round++) {
-    const uint64_t c0 = a[0] ^ a[5] ^ a[10] ^ a[15] ^ a[20];
-    const uint64_t c1 = a[1] ^ a[6] ^ a[11] ^ a[16] ^ a[21];
-    const uint64_t c2 = a[2] ^ a[7] ^ a[12] ^ a[17] ^ a[22];
-    const uint64_t c3 = a[3] ^ a[8] ^ a[13] ^ a[18] ^ a[23];
-    const uint64_t c4 = a[4] ^ a[9] ^ a[14] ^ a[19] ^ a[24];
-    const uint64_t d0 = c4 ^ rotl(c1, 1), d1 = c0 ^ rotl(c2, 1), d2 = c1 ^ rotl(c3, 1),
-                   d3 = c2 ^ rotl(c4, 1), d4 = c3 ^ rotl(c0, 1);
-    for (int y = 0; y < 25; y += 5) {
-      a[y] ^= d0; a[y + 1] ^= d1; a[y + 2] ^= d2; a[y + 3] ^= d3; a[y + 4] ^= d4;
-    }
-    rho_pi<0>(a, b);
-    for (int y = 0; y < 25; y += 5) {
-      const uint64_t b0 = b[y], b1 = b[y + 1], b2 = b[y + 2], b3 = b[y + 3], b4 = b[y + 4];
-      a[y] = b0 ^ (~b1 & b2);
-      a[y + 1] = b1 ^ (~b2 & b3);
-      a[y + 2] = b2 ^ (~b3 & b4);
-      a[y + 3] = b3 ^ (~b4 & b0);
-      a[y + 4] = b4 ^ (~b0 & b1);
-    }
-    a[0] ^= kRC[round];
+#define ROL(a, n) (((a) << (n)) | ((a) >> (64 - (n))))
+// Keccak-f[1600], 25 lanes in registers, theta/rho/pi fused per lane
+// (b[y, 2x+3y] = rot(a[x,y] ^ d[x], rho[x,y])), then chi + iota.  ~1.3x the
+// speed of the table-driven loop; the transcript is on every round's
+// critical path (7 permutations per degree-3 round).
+void keccak_f1600(uint64_t s[25]) {
+  uint64_t a00=s[0],a01=s[1],a02=s[2],a03=s[3],a04=s[4],a05=s[5],a06=s[6],a07=s[7],a08=s[8],a09=s[9],
+           a10=s[10],a11=s[11],a12=s[12],a13=s[13],a14=s[14],a15=s[15],a16=s[16],a17=s[17],a18=s[18],a19=s[19],
+           a20=s[20],a21=s[21],a22=s[22],a23=s[23],a24=s[24];
+  for (int r = 0; r < 24; r++) {
+    uint64_t c0=a00^a05^a10^a15^a20, c1=a01^a06^a11^a16^a21, c2=a02^a07^a12^a17^a22,
+             c3=a03^a08^a13^a18^a23, c4=a04^a09^a14^a19^a24;
+    uint64_t d0=c4^ROL(c1,1), d1=c0^ROL(c2,1), d2=c1^ROL(c3,1), d3=c2^ROL(c4,1), d4=c3^ROL(c0,1);
+    // theta + rho + pi: b[y, 2x+3y] = rot(a[x,y]^d[x], r[x,y]); lane index i = x + 5y
+    uint64_t b00=a00^d0;
+    uint64_t b10=ROL(a01^d1,1);   // (1,0)->(0,2): idx 10
+    uint64_t b20=ROL(a02^d2,62);  // (2,0)->(0,4): 20
+    uint64_t b05=ROL(a03^d3,28);  // (3,0)->(0,1): 5
+    uint64_t b15=ROL(a04^d4,27);  // (4,0)->(0,3): 15
+    uint64_t b16=ROL(a05^d0,36);  // (0,1)->(1,3): 16
+    uint64_t b01=ROL(a06^d1,44);  // (1,1)->(1,0): 1
+    uint64_t b11=ROL(a07^d2,6);   // (2,1)->(1,2): 11
+    uint64_t b21=ROL(a08^d3,55);  // (3,1)->(1,4): 21
+    uint64_t b06=ROL(a09^d4,20);  // (4,1)->(1,1): 6
+    uint64_t b07=ROL(a10^d0,3);   // (0,2)->(2,1): 7
+    uint64_t b17=ROL(a11^d1,10);  // (1,2)->(2,3): 17
+    uint64_t b02=ROL(a12^d2,43);  // (2,2)->(2,0): 2
+    uint64_t b12=ROL(a13^d3,25);  // (3,2)->(2,2): 12
+    uint64_t b22=ROL(a14^d4,39);  // (4,2)->(2,4): 22
+    uint64_t b23=ROL(a15^d0,41);  // (0,3)->(3,4): 23
+    uint64_t b08=ROL(a16^d1,45);  // (1,3)->(3,1): 8
+    uint64_t b18=ROL(a17^d2,15);  // (2,3)->(3,3): 18
+    uint64_t b03=ROL(a18^d3,21);  // (3,3)->(3,0): 3
+    uint64_t b13=ROL(a19^d4,8);   // (4,3)->(3,2): 13
+    uint64_t b14=ROL(a20^d0,18);  // (0,4)->(4,2): 14
+    uint64_t b24=ROL(a21^d1,2);   // (1,4)->(4,4): 24
+    uint64_t b09=ROL(a22^d2,61);  // (2,4)->(4,1): 9
+    uint64_t b19=ROL(a23^d3,56);  // (3,4)->(4,3): 19
+    uint64_t b04=ROL(a24^d4,14);  // (4,4)->(4,0): 4
+    a00=b00^(~b01&b02); a01=b01^(~b02&b03); a02=b02^(~b03&b04); a03=b03^(~b04&b00); a04=b04^(~b00&b01);
+    a05=b05^(~b06&b07); a06=b06^(~b07&b08); a07=b07^(~b08&b09); a08=b08^(~b09&b05); a09=b09^(~b05&b06);
+    a10=b10^(~b11&b12); a11=b11^(~b12&b13); a12=b12^(~b13&b14); a13=b13^(~b14&b10); a14=b14^(~b10&b11);
+    a15=b15^(~b16&b17); a16=b16^(~b17&b18); a17=b17^(~b18&b19); a18=b18^(~b19&b15); a19=b19^(~b15&b16);
+    a20=b20^(~b21&b22); a21=b21^(~b22&b23); a22=b22^(~b23&b24); a23=b23^(~b24&b20); a24=b24^(~b20&b21);
+    a00^=RC[r];
   }
+  s[0]=a00;s[1]=a01;s[2]=a02;s[3]=a03;s[4]=a04;s[5]=a05;s[6]=a06;s[7]=a07;s[8]=a08;s[9]=a09;
+  s[10]=a10;s[11]=a11;s[12]=a12;s[13]=a13;s[14]=a14;s[15]=a15;s[16]=a16;s[17]=a17;s[18]=a18;s[19]=a19;
+  s[20]=a20;s[21]=a21;s[22]=a22;s[23]=a23;s[24]=a24;
 }
 
 void shake256(const uint8_t* in, size_t len, uint8_t* out, size_t outlen) {
@@ -98,6 +109,11 @@ void HostTranscript::append_elem(const char* label, const uint8_t* canon, int nb
 }
 
 void HostTranscript::challenge_raw(const char* label, size_t llen, uint8_t raw[64]) {
+  challenge_squeeze(label, llen, raw);
+  challenge_absorb(raw);
+}
+
+void HostTranscript::challenge_squeeze(const char* label, size_t llen, uint8_t raw[64]) {
   // raw = H(state || record("challenge", label))
   uint8_t buf[64 + 2 + 9 + 8 + 256];
   uint8_t* w = buf;
@@ -108,7 +124,6 @@ void HostTranscript::challenge_raw(const char* label, size_t llen, uint8_t raw[6
   w += 8;
   memcpy(w, label, llen); w += llen;
   shake256(buf, (size_t)(w - buf), raw, 64);
-  append("drawn", 5, raw, 64);
 }
 
 void reduce512_fr(const uint8_t raw[64], uint8_t out[32]) {
@@ -120,8 +135,8 @@ void reduce512_fr(const uint8_t raw[64], uint8_t out[32]) {
     if (Fr255::geq_p_portable(hi)) hi = Fr255::sub_p_portable(hi);
   }
   // hi * 2^256 mod p = mont_mul(hi, R^2)
-  fr_t h = Fr255::mul_portable(hi, Fr255::r2());
-  fr_t r = Fr255::add_portable(lo, h);
+  fr_t h = host::Fr::mul(hi, Fr255::r2());
+  fr_t r = host::Fr::add(lo, h);
   memcpy(out, &r, 32);
 }
 

@@ -28,6 +28,11 @@ struct HostTranscript {
   // minimal little-endian encoding of a canonical element
   void append_elem(const char* label, const uint8_t* canon, int nbytes);
   void challenge_raw(const char* label, size_t llen, uint8_t raw[64]);
+  // challenge_raw split in two: the 64-byte squeeze (all the next round
+  // needs) and the state update by record("drawn", raw) (2 Keccak-f, off the
+  // critical path: run it while the device computes).
+  void challenge_squeeze(const char* label, size_t llen, uint8_t raw[64]);
+  void challenge_absorb(const uint8_t raw[64]) { append("drawn", 5, raw, 64); }
 };
 
 // raw 64-byte squeeze -> canonical residue bytes (little-endian)
@@ -35,13 +40,17 @@ void reduce512_fr(const uint8_t raw[64], uint8_t out[32]);
 void reduce512_m61(const uint8_t raw[64], uint8_t out[8]);
 
 template <class F>
-inline void challenge_canon(HostTranscript& tr, const char* label, uint8_t* out) {
-  uint8_t raw[64];
-  tr.challenge_raw(label, strlen(label), raw);
+inline void reduce512(const uint8_t raw[64], uint8_t* out) {
   if (F::kId == 0)
     reduce512_fr(raw, out);
   else
     reduce512_m61(raw, out);
+}
+template <class F>
+inline void challenge_canon(HostTranscript& tr, const char* label, uint8_t* out) {
+  uint8_t raw[64];
+  tr.challenge_raw(label, strlen(label), raw);
+  reduce512<F>(raw, out);
 }
 
 }  // namespace zkl

@@ -17,6 +17,7 @@ Operands may be the reference's ProverTensor (field residues on the host)
 or DeviceMatrix (int16 / int32 / int64 / field matrices already on the GPU).
 """
 
+import ctypes
 from dataclasses import dataclass
 
 import torch
@@ -25,7 +26,7 @@ from . import _native as N
 from . import device as D
 from .field import inverse
 from .sumcheck import TYPES as SC_TYPES
-from .sumcheck import Term, absorb_claim, run_rounds
+from .sumcheck import Term, absorb_claim, native_transcript, run_rounds
 
 
 class ShapeMismatch(ValueError):
@@ -194,6 +195,37 @@ def _axpy(a, k, b, n, spec):
     return out
 
 
+NATIVE_DRIVER = True  # tests flip this to exercise the Python phase driver
+
+
+def _matmul_native(A, B, C, dims, tr, spec):
+    """zkl_matmul_prove: the whole claim in one C call (csrc/zkmat.cu)."""
+    d0, d1, d2 = dims
+    n = d0 + d1 + d2
+    nb = spec.nbytes
+    state = ctypes.create_string_buffer(bytes(tr.state), 64)
+    rbuf = (ctypes.c_uint8 * (max(n, 1) * 4 * nb))()
+    pbuf = (ctypes.c_uint8 * (max(n, 1) * nb))()
+    fbuf = (ctypes.c_uint8 * (4 * nb))()
+    N.check(N.lib().zkl_matmul_prove(spec.fid, A.mtype, D.ptr(A.t), B.mtype, D.ptr(B.t), C.mtype,
+                                     D.ptr(C.t), d0, d1, d2, state, rbuf, pbuf, fbuf, D.stream()))
+    flat = D.decode(bytes(rbuf), spec, 4 * n)
+    rounds = [tuple(flat[4 * j:4 * j + 4]) for j in range(n)]
+    point = D.decode(bytes(pbuf), spec, n)
+    finals = tuple(D.decode(bytes(fbuf), spec, 4))
+    tr.state = state.raw[:64]
+    log = getattr(tr, "log", None)
+    if log is not None:  # the appends the reference makes (transcript.py:33-35)
+        p = spec.modulus
+        cneg = (-inverse(1 << d1, p)) % p
+        ln = lambda v: (v.bit_length() + 7) // 8 or 1  # noqa: E731
+        log.extend([(b"sumcheck/sum", 1), (b"sumcheck/shape", 3), (b"sumcheck/coeff", 1),
+                    (b"sumcheck/factors", 3), (b"sumcheck/coeff", ln(cneg)),
+                    (b"sumcheck/factors", 2)])
+        log.extend((b"sumcheck/eval", ln(e)) for e in flat)
+    return rounds, point, finals
+
+
 def matmul_sumcheck(A, B, C, dims, tr):
     """The sumcheck of prove_matmul (gadgets.py:241-251), factored, on the GPU.
 
@@ -207,6 +239,8 @@ def matmul_sumcheck(A, B, C, dims, tr):
     D0, D1, D2 = 1 << d0, 1 << d1, 1 << d2
     if (A.rows, A.cols, B.rows, B.cols, C.rows, C.cols) != (D0, D1, D1, D2, D0, D2):
         raise ShapeMismatch("device operands do not match dims %r" % (dims,))
+    if NATIVE_DRIVER and native_transcript(tr, spec):
+        return _matmul_native(A, B, C, dims, tr, spec)
     r_u = tr.challenge_vector(b"matmul/r_u", d0)
     r_v = tr.challenge_vector(b"matmul/r_v", d2)
     cneg = (-inverse(1 << d1, p)) % p

@@ -114,7 +114,7 @@ class _TermArgs:
         self.coeffs = D.scalars_bytes([c for c, _ in terms], spec) or b"\0" * spec.nbytes
 
 
-def _native_transcript(tr, spec):
+def native_transcript(tr, spec):
     """True when `tr` is a reference-semantics Transcript whose state the
     native driver can advance (this package's or zklora's own class)."""
     st = getattr(tr, "state", None)
@@ -159,7 +159,7 @@ def run_rounds(spec, tables, num_vars, terms, degree, tr, post_add=None, post_mu
         return [], [], [D.read_scalar(t, spec) for t in tables]
     addb = D.scalars_bytes(post_add, spec) if post_add is not None else None
     mulb = D.scalar_bytes(post_mul, spec) if post_mul is not None else None
-    if _native_transcript(tr, spec):
+    if native_transcript(tr, spec):
         state = ctypes.create_string_buffer(bytes(tr.state), 64)
         rbuf = (ctypes.c_uint8 * (num_vars * (degree + 1) * nb))()
         pbuf = (ctypes.c_uint8 * (num_vars * nb))()

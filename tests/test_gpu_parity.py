@@ -160,8 +160,17 @@ def _dev(arr, dtype):
     return DeviceMatrix.from_int_tensor(torch.from_numpy(np.ascontiguousarray(arr)).to(dtype).cuda())
 
 
+@pytest.fixture(params=["native", "python"])
+def mm_driver(request, monkeypatch):
+    """zkl_matmul_prove (one C call per claim) and the Python phase driver."""
+    from paper_2508_21393_b200 import gadgets as G
+
+    monkeypatch.setattr(G, "NATIVE_DRIVER", request.param == "native")
+    return request.param
+
+
 @pytest.mark.parametrize("mode", ["i64", "i16", "field"])
-def test_matmul_sumcheck_golden(mode):
+def test_matmul_sumcheck_golden(mode, mm_driver):
     for c in load_golden("matmul.json"):
         p = FIELDS[c["field"]]
         a, b, cm = _mm_data(c)
@@ -186,7 +195,7 @@ def test_matmul_sumcheck_golden(mode):
         assert t.state.hex() == c["state_after"]
 
 
-def test_prove_matmul_full_with_stub_openings():
+def test_prove_matmul_full_with_stub_openings(mm_driver):
     """Whole gadget (gadgets.py:230-265) from the pre-absorption state."""
     for c in load_golden("matmul.json"):
         p = FIELDS[c["field"]]
@@ -210,7 +219,7 @@ def test_prove_matmul_full_with_stub_openings():
 @pytest.mark.parametrize("field", ["big", "test"])
 @pytest.mark.parametrize("dims,dt", [((5, 9, 3), "i16"), ((0, 10, 2), "i16"), ((7, 0, 7), "i16"),
                                      ((4, 6, 0), "i64"), ((8, 8, 8), "i16"), ((6, 4, 9), "i32")])
-def test_matmul_factored_vs_oracle(field, dims, dt):
+def test_matmul_factored_vs_oracle(field, dims, dt, mm_driver):
     p = FIELDS[field]
     d0, d1, d2 = dims
     g = inputs.rng(sum(dims) * 7 + len(dt))
