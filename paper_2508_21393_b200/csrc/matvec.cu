@@ -13,6 +13,8 @@
 // loop.  Signed entries use offset binary: sum (s + o) x - o * sum x, so the
 // inner loop is unsigned; the wide sum is reduced mod p once per output.
 // Other combinations (M61, field-valued matrices) multiply-add in the field.
+#include <cstdlib>
+
 #include "ops.cuh"
 
 namespace zkl {
@@ -300,6 +302,318 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ===========================================================================
+// Fast path (Fr255 x int16 / int64): per-limb 64-bit accumulators fed by
+// mad.wide.u32 -- no carry chains in the inner loop.
+//
+// x (Montgomery form, 8 x 32-bit limbs x_l) is shared by all outputs.  Every
+// signed entry s is made unsigned by offset binary, u = s + OFF, so
+//   sum_c s_c x_c = sum_c u_c x_c - OFF * sum_c x_c,
+// where OFF * sum x is ONE per-chunk constant K (x is shared).  Limb products
+// u_k x_l (u_k < 2^16, x_l < 2^32) are accumulated in u64 without carries:
+//   int16 (1 chunk):  e[l]   += u x_l                      (weight 2^(32 l))
+//   int64 (4 chunks of 16 bits, u = s + 2^63):
+//                     e[l]   += u0 x_l,  e[l+1] += u2 x_l  (weight 2^(32 l))
+//                     o[l]   += u1 x_l,  o[l+1] += u3 x_l  (weight 2^(32 l + 16))
+// Each accumulator takes < 2^49 per entry, so chunks of <= 2^15 entries
+// never overflow.  The epilogue folds the accumulators into a wide integer,
+// reduces it mod p once and subtracts K.  Cost per int16 entry: 8 mad.wide
+// (vs ~20 carry-chained mad.lo/hi.cc in the wide-accumulator kernels above).
+template <int CH>
+struct LimbAcc {
+  static constexpr int NE = CH == 1 ? 8 : 9;
+  uint64_t e[NE];
+  uint64_t o[CH == 1 ? 1 : 9];
+  ZKL_D void zero() {
+#pragma unroll
+    for (int i = 0; i < NE; i++) e[i] = 0;
+#pragma unroll
+    for (int i = 0; i < (CH == 1 ? 1 : 9); i++) o[i] = 0;
+  }
+};
+
+ZKL_D uint64_t madw(uint32_t a, uint32_t b, uint64_t c) {
+  uint64_t r;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(c));
+  return r;
+}
+
+ZKL_D void mac_u16(LimbAcc<1>& a, uint32_t u, const fr_t& x) {
+#pragma unroll
+  for (int l = 0; l < 8; l++) a.e[l] = madw(u, x.v[l], a.e[l]);
+}
+ZKL_D void mac_u64(LimbAcc<4>& a, uint64_t u, const fr_t& x) {
+  const uint32_t u0 = (uint32_t)u & 0xffffu, u1 = (uint32_t)(u >> 16) & 0xffffu;
+  const uint32_t u2 = (uint32_t)(u >> 32) & 0xffffu, u3 = (uint32_t)(u >> 48);
+#pragma unroll
+  for (int l = 0; l < 8; l++) {
+    a.e[l] = madw(u0, x.v[l], a.e[l]);
+    a.e[l + 1] = madw(u2, x.v[l], a.e[l + 1]);
+    a.o[l] = madw(u1, x.v[l], a.o[l]);
+    a.o[l + 1] = madw(u3, x.v[l], a.o[l + 1]);
+  }
+}
+
+// wide integer sum_m e[m] 2^(32m) + o[m] 2^(32m+16) -> value mod p (storage)
+template <int CH>
+ZKL_D fr_t limb_reduce(const LimbAcc<CH>& a) {
+  // 14 x 32-bit words are enough: max ~2^(64 + 32*8 + 16) < 2^448
+  uint32_t w[14];
+#pragma unroll
+  for (int i = 0; i < 14; i++) w[i] = 0;
+  uint64_t carry = 0;
+  // even part: word i gets lo(e[i]) + hi(e[i-1]) + carry
+#pragma unroll
+  for (int i = 0; i < 14; i++) {
+    uint64_t t = carry;
+    if (i < LimbAcc<CH>::NE) t += (uint32_t)a.e[i];
+    if (i >= 1 && i - 1 < LimbAcc<CH>::NE) t += a.e[i - 1] >> 32;
+    w[i] = (uint32_t)t;
+    carry = t >> 32;
+  }
+  if (CH != 1) {
+    // odd part (offset 16 bits): add sum_m o[m] 2^(32m+16)
+    uint64_t c2 = 0;
+#pragma unroll
+    for (int i = 0; i < 14; i++) {
+      // bits of the odd sum landing in word i: lo16(o[i]) << 16 | bits from o[i-1] >> 16 ...
+      uint64_t t = c2 + (uint64_t)w[i];
+      if (i < 9) t += (uint64_t)((uint32_t)a.o[i] & 0xffffu) << 16;
+      if (i >= 1 && i - 1 < 9) t += (a.o[i - 1] >> 16) & 0xffffffffull;
+      if (i >= 2 && i - 2 < 9) t += a.o[i - 2] >> 48;
+      w[i] = (uint32_t)t;
+      c2 = t >> 32;
+    }
+  }
+  fr_t lo, hi = Fr255::zero();
+#pragma unroll
+  for (int i = 0; i < 8; i++) lo.v[i] = w[i];
+#pragma unroll
+  for (int i = 8; i < 14; i++) hi.v[i - 8] = w[i];
+  lo = Fr255::reduce_once(Fr255::reduce_once(lo));  // lo < 2^256 < 3p
+  hi = Fr255::mul(hi, Fr255::r2());                 // hi < 2^192 < p: hi * 2^256 mod p
+  return Fr255::add(lo, hi);
+}
+
+// K[chunk] = OFF * sum_{i in chunk} x[i] mod p (storage form), one block per
+// chunk: wide 9-word sums, warp shuffles, one reduction mod p.
+template <int CH>
+__global__ void __launch_bounds__(256)
+    k_chunk_offsets(const fr_t* x, uint64_t n, uint64_t cch, fr_t* K) {
+  const uint64_t lo = blockIdx.x * cch, hi = lo + cch < n ? lo + cch : n;
+  uint32_t acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const fr_t v = x[i];
+    uint64_t c = 0;
+#pragma unroll
+    for (int l = 0; l < 8; l++) {
+      c += (uint64_t)acc[l] + v.v[l];
+      acc[l] = (uint32_t)c;
+      c >>= 32;
+    }
+    acc[8] += (uint32_t)c;
+  }
+  auto wadd = [](uint32_t (&a)[9], const uint32_t (&b)[9]) {
+    uint64_t c = 0;
+#pragma unroll
+    for (int l = 0; l < 9; l++) {
+      c += (uint64_t)a[l] + b[l];
+      a[l] = (uint32_t)c;
+      c >>= 32;
+    }
+  };
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    uint32_t o[9];
+#pragma unroll
+    for (int l = 0; l < 9; l++) o[l] = __shfl_down_sync(kFull, acc[l], off);
+    wadd(acc, o);
+  }
+  __shared__ uint32_t red[8][9];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+#pragma unroll
+    for (int l = 0; l < 9; l++) red[warp][l] = acc[l];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) wadd(t, red[w]);
+    fr_t lo_, hi_ = Fr255::zero();
+#pragma unroll
+    for (int l = 0; l < 8; l++) lo_.v[l] = t[l];
+    hi_.v[0] = t[8];
+    lo_ = Fr255::reduce_once(Fr255::reduce_once(lo_));
+    const fr_t sum = Fr255::add(lo_, Fr255::mul(hi_, Fr255::r2()));
+    // OFF * sum: mont_mul(sum, OFF R^2) = sum OFF R, then one more R^-1
+    fr_t offm = Fr255::r2();
+    const int sh = CH == 1 ? 15 : 63;
+    for (int i = 0; i < sh; i++) offm = Fr255::add(offm, offm);
+    fr_t one_c = Fr255::zero();
+    one_c.v[0] = 1;
+    K[blockIdx.x] = Fr255::mul(Fr255::mul(sum, offm), one_c);
+  }
+}
+
+// row products, thread per row: y_part[chunk][r] = sum_{c in chunk} M[r,c] x[c]
+// 64-byte vector loads per thread per step (full DRAM sectors), x broadcast
+// from shared memory.
+template <class MT>
+__global__ void __launch_bounds__(256)
+    k_mvf_rows(const MT* M, uint64_t rows, uint64_t cols, const fr_t* x, uint64_t cch,
+               const fr_t* K, fr_t* part) {
+  constexpr int CH = sizeof(MT) == 2 ? 1 : 4;
+  constexpr int E = 64 / sizeof(MT);  // entries per 64-byte step
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  fr_t* xs = reinterpret_cast<fr_t*>(smem_raw);
+  const uint64_t c0 = blockIdx.y * cch;
+  const uint64_t c1 = c0 + cch < cols ? c0 + cch : cols;
+  const int n = (int)(c1 - c0);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) xs[i] = x[c0 + i];
+  __syncthreads();
+  const uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  LimbAcc<CH> acc;
+  acc.zero();
+  const MT* row = M + r * cols;
+  int c = 0;
+  const bool vec = ((uintptr_t)(row + c0) % 16) == 0;
+  if (vec) {
+    for (; c + E <= n; c += E) {
+      MT v[E];
+      const uint4* q = reinterpret_cast<const uint4*>(row + c0 + c);
+#pragma unroll
+      for (int i = 0; i < 4; i++) reinterpret_cast<uint4*>(v)[i] = __ldcs(q + i);
+#pragma unroll
+      for (int k = 0; k < E; k++) {
+        const fr_t xv = xs[c + k];
+        if constexpr (CH == 1)
+          mac_u16(acc, (uint32_t)((int32_t)v[k] + 32768), xv);
+        else
+          mac_u64(acc, (uint64_t)v[k] ^ 0x8000000000000000ull, xv);
+      }
+    }
+  }
+  for (; c < n; c++) {
+    const MT sv = row[c0 + c];
+    const fr_t xv = xs[c];
+    if constexpr (CH == 1)
+      mac_u16(acc, (uint32_t)((int32_t)sv + 32768), xv);
+    else
+      mac_u64(acc, (uint64_t)sv ^ 0x8000000000000000ull, xv);
+  }
+  part[blockIdx.y * rows + r] = Fr255::sub(limb_reduce<CH>(acc), K[blockIdx.y]);
+}
+
+// column products, thread per V consecutive columns: y_part[chunk][c] =
+// sum_{r in chunk} x[r] M[r, c]; coalesced row segments, x[r] broadcast.
+template <class MT, int V>
+__global__ void __launch_bounds__(256)
+    k_mvf_cols(const MT* M, uint64_t rows, uint64_t cols, const fr_t* x, uint64_t rch,
+               const fr_t* K, fr_t* part) {
+  constexpr int CH = sizeof(MT) == 2 ? 1 : 4;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  fr_t* xs = reinterpret_cast<fr_t*>(smem_raw);
+  const uint64_t r0 = blockIdx.y * rch;
+  const uint64_t r1 = r0 + rch < rows ? r0 + rch : rows;
+  const int n = (int)(r1 - r0);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) xs[i] = x[r0 + i];
+  __syncthreads();
+  const uint64_t c = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * V;
+  if (c >= cols) return;
+  LimbAcc<CH> acc[V];
+#pragma unroll
+  for (int v = 0; v < V; v++) acc[v].zero();
+  for (int i = 0; i < n; i++) {
+    const MT* p = M + (r0 + i) * cols + c;
+    MT vals[V];
+    if constexpr (sizeof(MT) * V == 8) {
+      *reinterpret_cast<uint2*>(vals) = __ldcs(reinterpret_cast<const uint2*>(p));
+    } else if constexpr (sizeof(MT) * V == 16) {
+      *reinterpret_cast<uint4*>(vals) = __ldcs(reinterpret_cast<const uint4*>(p));
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; v++) vals[v] = p[v];
+    }
+    const fr_t xv = xs[i];
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+      if constexpr (CH == 1)
+        mac_u16(acc[v], (uint32_t)((int32_t)vals[v] + 32768), xv);
+      else
+        mac_u64(acc[v], (uint64_t)vals[v] ^ 0x8000000000000000ull, xv);
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < V; v++)
+    part[blockIdx.y * cols + c + v] = Fr255::sub(limb_reduce<CH>(acc[v]), K[blockIdx.y]);
+}
+
+// returns kUnsupported when the shape does not suit the fast kernels
+template <class MT>
+static int matvec_fast(const MT* M, uint64_t rows, uint64_t cols, int transpose, const fr_t* x,
+                       fr_t* y, cudaStream_t s) {
+  // blocks to aim for (ZKL_MV_WANT overrides, for tuning)
+  static const uint64_t kWant = [] {
+    const char* e = getenv("ZKL_MV_WANT");
+    return e ? (uint64_t)atoi(e) : (uint64_t)(2 * kSMs);
+  }();
+  constexpr uint64_t kMaxChunk = 1u << 14;  // accumulator headroom (< 2^15 entries)
+  uint64_t nchunks, nout;
+  void* ws;
+  int rc;
+  if (!transpose) {
+    if (cols % 16) return kErrUnsupported;
+    const uint64_t rb = (rows + 255) / 256;
+    uint64_t cs = (kWant + rb - 1) / rb;
+    const uint64_t min_cs = (cols + kMaxChunk - 1) / kMaxChunk;
+    const uint64_t max_cs = (cols + 127) / 128;  // >= 128 columns per chunk
+    if (cs > max_cs) cs = max_cs;
+    if (cs < min_cs) cs = min_cs;
+    if (cs < 1) cs = 1;
+    uint64_t cch = (cols + cs - 1) / cs;
+    cch = (cch + 31) / 32 * 32;                 // keep 64-byte steps aligned
+    if (cch * sizeof(fr_t) > 48 * 1024) return kErrUnsupported;
+    nchunks = (cols + cch - 1) / cch;
+    nout = rows;
+    rc = scratch_reserve((nchunks * rows + nchunks) * sizeof(fr_t), &ws, s);
+    if (rc) return rc;
+    fr_t* K = (fr_t*)ws + nchunks * rows;
+    k_chunk_offsets<sizeof(MT) == 2 ? 1 : 4><<<(unsigned)nchunks, 256, 0, s>>>(x, cols, cch, K);
+    ZKL_LAUNCH_CHECK();
+    dim3 g((unsigned)rb, (unsigned)nchunks);
+    k_mvf_rows<MT><<<g, 256, cch * sizeof(fr_t), s>>>(M, rows, cols, x, cch, K, (fr_t*)ws);
+    ZKL_LAUNCH_CHECK();
+  } else {
+    constexpr int V = sizeof(MT) == 2 ? 4 : 2;
+    if (cols % V || cols < 64 * V) return kErrUnsupported;
+    const uint64_t cb = (cols / V + 255) / 256;
+    uint64_t rs = (kWant + cb - 1) / cb;
+    const uint64_t min_rs = (rows + kMaxChunk - 1) / kMaxChunk;
+    const uint64_t max_rs = (rows + 63) / 64;  // >= 64 rows per chunk
+    if (rs > max_rs) rs = max_rs;
+    if (rs < min_rs) rs = min_rs;
+    if (rs < 1) rs = 1;
+    uint64_t rch = (rows + rs - 1) / rs;
+    if (rch * sizeof(fr_t) > 48 * 1024) return kErrUnsupported;
+    nchunks = (rows + rch - 1) / rch;
+    if (nchunks > 65535) return kErrUnsupported;
+    nout = cols;
+    rc = scratch_reserve((nchunks * cols + nchunks) * sizeof(fr_t), &ws, s);
+    if (rc) return rc;
+    fr_t* K = (fr_t*)ws + nchunks * cols;
+    k_chunk_offsets<sizeof(MT) == 2 ? 1 : 4><<<(unsigned)nchunks, 256, 0, s>>>(x, rows, rch, K);
+    ZKL_LAUNCH_CHECK();
+    dim3 g((unsigned)cb, (unsigned)nchunks);
+    k_mvf_cols<MT, V><<<g, 256, rch * sizeof(fr_t), s>>>(M, rows, cols, x, rch, K, (fr_t*)ws);
+    ZKL_LAUNCH_CHECK();
+  }
+  k_mv_reduce<Fr255><<<grid_for(nout * 32, 256, 8), 256, 0, s>>>((const fr_t*)ws, nchunks, nout,
+                                                                   y);
+  ZKL_LAUNCH_CHECK();
+  return kOk;
+}
+
 template <class F, class MT>
 static int matvec_impl(const void* Mv, uint64_t rows, uint64_t cols, int transpose,
                        const void* xv, void* yv, cudaStream_t s) {
@@ -361,15 +675,37 @@ static int matvec_impl(const void* Mv, uint64_t rows, uint64_t cols, int transpo
   return kOk;
 }
 
+// ZKL_MATVEC_SLOW=1 forces the wide-accumulator kernels (cross-checks)
+static bool fast_enabled() {
+  static const bool on = getenv("ZKL_MATVEC_SLOW") == nullptr;
+  return on;
+}
+
 template <class F>
 int op_matvec(int mtype, const void* M, uint64_t rows, uint64_t cols, int transpose,
               const void* x, void* y, cudaStream_t s) {
   if (!rows || !cols) { set_error("matvec: empty matrix"); return kErrArg; }
   switch (mtype) {
     case 0: return matvec_impl<F, typename F::T>(M, rows, cols, transpose, x, y, s);
-    case 1: return matvec_impl<F, int16_t>(M, rows, cols, transpose, x, y, s);
+    case 1:
+      if constexpr (F::kId == 0) {
+        if (fast_enabled()) {
+          int rc = matvec_fast<int16_t>((const int16_t*)M, rows, cols, transpose,
+                                        (const fr_t*)x, (fr_t*)y, s);
+          if (rc != kErrUnsupported) return rc;
+        }
+      }
+      return matvec_impl<F, int16_t>(M, rows, cols, transpose, x, y, s);
     case 2: return matvec_impl<F, int32_t>(M, rows, cols, transpose, x, y, s);
-    case 3: return matvec_impl<F, int64_t>(M, rows, cols, transpose, x, y, s);
+    case 3:
+      if constexpr (F::kId == 0) {
+        if (fast_enabled()) {
+          int rc = matvec_fast<int64_t>((const int64_t*)M, rows, cols, transpose,
+                                        (const fr_t*)x, (fr_t*)y, s);
+          if (rc != kErrUnsupported) return rc;
+        }
+      }
+      return matvec_impl<F, int64_t>(M, rows, cols, transpose, x, y, s);
   }
   set_error("matvec: bad matrix type %d", mtype);
   return kErrArg;

@@ -143,6 +143,37 @@ def test_sumcheck_random_vs_oracle(field, k, degree, n):
     assert point == opoint and t1.state == t2.state
 
 
+# the recognised round shapes (persistent engine: lane-mode evaluators, the
+# grid-kernel -> cluster-kernel handoff at large n, unused tables folded too)
+SHAPES = {
+    "prod2": (2, [(0, 1)], 3),
+    "prod2-deg2": (2, [(1, 0)], 2),
+    "prod2-extra-tables": (4, [(3, 1)], 3),
+    "prod3": (3, [(0, 1, 2)], 3),
+    "sum2prod2": (3, [(0, 1), (0, 2)], 3),
+    "generic-mixed": (3, [(0, 1, 2), (1,), ()], 3),
+}
+
+
+@pytest.mark.parametrize("field,n", [("test", 16), ("big", 15), ("big", 6), ("test", 1)])
+@pytest.mark.parametrize("shape", list(SHAPES))
+def test_sumcheck_shapes_vs_oracle(field, n, shape):
+    p = FIELDS[field]
+    k, factor_sets, degree = SHAPES[shape]
+    rnd = random.Random(n * 31 + k)
+    tabs = [inputs.field_vec(rnd.randrange(1 << 30), 1 << n, p) for _ in range(k)]
+    terms = [zb.Term(rnd.randrange(p), f) for f in factor_sets]
+    claimed = rnd.randrange(p)
+    t1 = Transcript(b"shape", p, shape.encode())
+    proof, point = zb.prove_sumcheck(zb.SumcheckClaim(claimed, tabs, terms, degree, p), t1)
+    t2 = fs.FS(b"shape", p, shape.encode())
+    rounds, finals, opoint = sc.prove(claimed, tabs, [(x.coefficient, x.factors) for x in terms],
+                                      degree, t2)
+    assert [r.evaluations for r in proof.rounds] == rounds
+    assert proof.final_values == finals
+    assert point == opoint and t1.state == t2.state
+
+
 # --- zkMat ---------------------------------------------------------------------------
 
 
