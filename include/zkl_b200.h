@@ -162,6 +162,15 @@ int zkl_matmul_prove(int field, int a_type, const void* A, int b_type, const voi
                      const void* C, int d0, int d1, int d2, uint8_t* state_inout,
                      uint8_t* rounds_out, uint8_t* point_out, uint8_t* finals_out, void* stream);
 
+/* CUDA-event profiler for benchmarks: when enabled, the library brackets
+ * each kernel family on its launching stream.  kind 0: matrix-vector
+ * products (bytes = matrix + vectors), 1: sumcheck phases (persistent round
+ * engine; units = rounds), 2: eq tables.  zkl_prof_collect synchronises on
+ * the recorded events and returns total milliseconds, algorithmic bytes,
+ * units and launch groups of one kind since the last collect. */
+int zkl_prof_enable(int on);
+int zkl_prof_collect(int kind, double* ms, double* bytes, double* units, uint64_t* count);
+
 #ifdef __cplusplus
 }
 #endif

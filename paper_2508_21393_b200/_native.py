@@ -25,6 +25,7 @@ EXPORTS = (
     "zkl_sumcheck_round", "zkl_sumcheck_finish", "zkl_batch_inverse", "zkl_multiplicities",
     "zkl_matvec", "zkl_expand", "zkl_lift_u32", "zkl_launch_count", "zkl_sumcheck_prove",
     "zkl_shake256", "zkl_transcript_append", "zkl_transcript_challenge", "zkl_matmul_prove",
+    "zkl_prof_enable", "zkl_prof_collect",
 )
 
 
@@ -71,6 +72,10 @@ _SIGS = {
     "zkl_batch_inverse": ([_i32, _vp, _vp, _u64, _u8p, _i64p, _vp], ctypes.c_int),
     "zkl_multiplicities": ([_i32, _vp, _u64, _vp, _u64, _vp, _i64p, _vp], ctypes.c_int),
     "zkl_matvec": ([_i32, _i32, _vp, _u64, _u64, _i32, _vp, _vp, _vp], ctypes.c_int),
+    "zkl_prof_enable": ([_i32], ctypes.c_int),
+    "zkl_prof_collect": ([_i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                          ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)],
+                         ctypes.c_int),
     "zkl_matmul_prove": (
         [_i32, _i32, _vp, _i32, _vp, _i32, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp],
         ctypes.c_int),
@@ -108,3 +113,16 @@ def check(rc):
     if rc != ZKL_OK:
         raise NativeError(rc, _lib.zkl_last_error().decode(errors="replace"))
     return rc
+
+
+PROF_MATVEC, PROF_PHASE, PROF_EQ = 0, 1, 2
+
+
+def prof_collect(kind):
+    """(ms, algorithmic bytes, units, launch groups) recorded since the last
+    collect for one kernel family (zkl_prof_collect)."""
+    ms, by, un = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    n = ctypes.c_uint64()
+    check(lib().zkl_prof_collect(kind, ctypes.byref(ms), ctypes.byref(by), ctypes.byref(un),
+                                 ctypes.byref(n)))
+    return ms.value, by.value, un.value, n.value

@@ -9,6 +9,11 @@
 
 using namespace zkl;
 
+namespace zkl {
+void prof_enable(bool on);
+void prof_collect(int kind, double* ms, double* bytes, double* units, uint64_t* count);
+}  // namespace zkl
+
 namespace {
 
 template <class F>
@@ -228,6 +233,18 @@ int zkl_matmul_prove(int field, int a_type, const void* A, int b_type, const voi
                      uint8_t* rounds_out, uint8_t* point_out, uint8_t* finals_out, void* stream) {
   D(field, op_matmul_prove<F>(a_type, A, b_type, B, c_type, C, d0, d1, d2, state_inout,
                               rounds_out, point_out, finals_out, (cudaStream_t)stream));
+}
+int zkl_prof_enable(int on) {
+  zkl::prof_enable(on != 0);
+  return kOk;
+}
+int zkl_prof_collect(int kind, double* ms, double* bytes, double* units, uint64_t* count) {
+  if (kind < 0 || kind >= kProfKinds) {
+    set_error("prof_collect: bad kind %d", kind);
+    return kErrArg;
+  }
+  zkl::prof_collect(kind, ms, bytes, units, count);
+  return kOk;
 }
 int zkl_matvec(int field, int mtype, const void* M, uint64_t rows, uint64_t cols, int transpose,
                const void* x, void* y, void* stream) {

@@ -166,4 +166,12 @@ struct alignas(128) Mailbox {
 };
 int mailbox_for_current_device(Mailbox** host, Mailbox** dev);
 
+// Optional CUDA-event profiler (zkl_prof_*): kernel families bracketed on
+// their launching stream, with the algorithmic bytes each launch moves.
+enum ProfKind { kProfMatvec = 0, kProfPhase = 1, kProfEq = 2, kProfKinds = 3 };
+bool prof_on();
+// returns an opaque handle (or -1 when profiling is off); close it after the launches
+int prof_open(int kind, double bytes, double units, cudaStream_t s);
+void prof_close(int handle, cudaStream_t s);
+
 }  // namespace zkl

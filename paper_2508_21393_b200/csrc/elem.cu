@@ -7,6 +7,7 @@
 #include <string.h>
 
 #include <map>
+#include <vector>
 #include <mutex>
 
 #include "ops.cuh"
@@ -50,6 +51,79 @@ int scratch_reserve(size_t bytes, void** out, cudaStream_t s) {
   *out = a.ptr;
   return kOk;
 }
+// ---------------------------------------------------------------------------
+// CUDA-event profiler
+struct ProfRec {
+  cudaEvent_t a = nullptr, b = nullptr;
+  int kind = 0;
+  double bytes = 0, units = 0;
+};
+static std::vector<ProfRec>& prof_recs() {
+  static std::vector<ProfRec> v;
+  return v;
+}
+static bool g_prof = false;
+static std::vector<cudaEvent_t>& event_pool() {  // recycled: no create/destroy per launch
+  static std::vector<cudaEvent_t> v;
+  return v;
+}
+static cudaEvent_t pool_get() {
+  auto& p = event_pool();
+  if (p.empty()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  cudaEvent_t e = p.back();
+  p.pop_back();
+  return e;
+}
+bool prof_on() { return g_prof; }
+int prof_open(int kind, double bytes, double units, cudaStream_t s) {
+  if (!g_prof) return -1;
+  ProfRec r;
+  r.kind = kind;
+  r.bytes = bytes;
+  r.units = units;
+  r.a = pool_get();
+  r.b = pool_get();
+  cudaEventRecord(r.a, s);
+  prof_recs().push_back(r);
+  return (int)prof_recs().size() - 1;
+}
+void prof_close(int h, cudaStream_t s) {
+  if (h < 0 || h >= (int)prof_recs().size()) return;
+  cudaEventRecord(prof_recs()[h].b, s);
+}
+void prof_enable(bool on) { g_prof = on; }
+// sums over the records of `kind` (syncs on their events); clears them
+void prof_collect(int kind, double* ms, double* bytes, double* units, uint64_t* count) {
+  double t = 0, by = 0, un = 0;
+  uint64_t n = 0;
+  auto& v = prof_recs();
+  std::vector<ProfRec> keep;
+  for (auto& r : v) {
+    if (r.kind != kind) {
+      keep.push_back(r);
+      continue;
+    }
+    float e = 0;
+    cudaEventSynchronize(r.b);
+    cudaEventElapsedTime(&e, r.a, r.b);
+    t += e;
+    by += r.bytes;
+    un += r.units;
+    n++;
+    event_pool().push_back(r.a);
+    event_pool().push_back(r.b);
+  }
+  v.swap(keep);
+  *ms = t;
+  *bytes = by;
+  *units = un;
+  *count = n;
+}
+
 int work_reserve(size_t bytes, void** out, cudaStream_t s) {
   Scratch& a = scratch_for_current_device();
   if (bytes > a.work_bytes) {

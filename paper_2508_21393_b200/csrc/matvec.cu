@@ -395,23 +395,30 @@ ZKL_D fr_t limb_reduce(const LimbAcc<CH>& a) {
   return Fr255::add(lo, hi);
 }
 
-// K[chunk] = OFF * sum_{i in chunk} x[i] mod p (storage form), one block per
-// chunk: wide 9-word sums, warp shuffles, one reduction mod p.
+// K = OFF * sum_i x[i] mod p (storage form) over the whole vector: one block,
+// wide 9-word sums, warp shuffles, one reduction mod p.
 template <int CH>
-__global__ void __launch_bounds__(256)
-    k_chunk_offsets(const fr_t* x, uint64_t n, uint64_t cch, fr_t* K) {
-  const uint64_t lo = blockIdx.x * cch, hi = lo + cch < n ? lo + cch : n;
+__global__ void __launch_bounds__(1024) k_offset_total(const fr_t* x, uint64_t n, fr_t offr,
+                                                      fr_t* K) {
   uint32_t acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    const fr_t v = x[i];
-    uint64_t c = 0;
+  for (uint64_t base = 0; base < n; base += 4 * (uint64_t)blockDim.x) {
+    fr_t v[4];
 #pragma unroll
-    for (int l = 0; l < 8; l++) {
-      c += (uint64_t)acc[l] + v.v[l];
-      acc[l] = (uint32_t)c;
-      c >>= 32;
+    for (int u = 0; u < 4; u++) {  // four independent loads in flight
+      const uint64_t i = base + u * (uint64_t)blockDim.x + threadIdx.x;
+      v[u] = i < n ? x[i] : Fr255::zero();
     }
-    acc[8] += (uint32_t)c;
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      uint64_t c = 0;
+#pragma unroll
+      for (int l = 0; l < 8; l++) {
+        c += (uint64_t)acc[l] + v[u].v[l];
+        acc[l] = (uint32_t)c;
+        c >>= 32;
+      }
+      acc[8] += (uint32_t)c;
+    }
   }
   auto wadd = [](uint32_t (&a)[9], const uint32_t (&b)[9]) {
     uint64_t c = 0;
@@ -429,7 +436,7 @@ __global__ void __launch_bounds__(256)
     for (int l = 0; l < 9; l++) o[l] = __shfl_down_sync(kFull, acc[l], off);
     wadd(acc, o);
   }
-  __shared__ uint32_t red[8][9];
+  __shared__ uint32_t red[32][9];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) {
 #pragma unroll
@@ -445,25 +452,82 @@ __global__ void __launch_bounds__(256)
     hi_.v[0] = t[8];
     lo_ = Fr255::reduce_once(Fr255::reduce_once(lo_));
     const fr_t sum = Fr255::add(lo_, Fr255::mul(hi_, Fr255::r2()));
-    // OFF * sum: mont_mul(sum, OFF R^2) = sum OFF R, then one more R^-1
-    fr_t offm = Fr255::r2();
-    const int sh = CH == 1 ? 15 : 63;
-    for (int i = 0; i < sh; i++) offm = Fr255::add(offm, offm);
-    fr_t one_c = Fr255::zero();
-    one_c.v[0] = 1;
-    K[blockIdx.x] = Fr255::mul(Fr255::mul(sum, offm), one_c);
+    // OFF * sum = mont_mul(sum, OFF R mod p)  (offr: OFF in storage form)
+    *K = Fr255::mul(sum, offr);
   }
 }
 
-// row products, thread per row: y_part[chunk][r] = sum_{c in chunk} M[r,c] x[c]
-// 64-byte vector loads per thread per step (full DRAM sectors), x broadcast
-// from shared memory.
+// raw accumulator words of one partial: int16 8 x u64, int64 18 x u64
+template <int CH>
+struct AccIO {
+  static constexpr int NW = CH == 1 ? 8 : 18;
+  ZKL_D static void store(uint64_t* dst, const LimbAcc<CH>& a) {
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    if constexpr (CH == 1) {
+#pragma unroll
+      for (int i = 0; i < 4; i++) d[i] = make_uint4((uint32_t)a.e[2 * i], (uint32_t)(a.e[2 * i] >> 32),
+                                                   (uint32_t)a.e[2 * i + 1],
+                                                   (uint32_t)(a.e[2 * i + 1] >> 32));
+    } else {
+      uint64_t w[18];
+#pragma unroll
+      for (int i = 0; i < 9; i++) { w[i] = a.e[i]; w[9 + i] = a.o[i]; }
+#pragma unroll
+      for (int i = 0; i < 9; i++)
+        d[i] = make_uint4((uint32_t)w[2 * i], (uint32_t)(w[2 * i] >> 32), (uint32_t)w[2 * i + 1],
+                          (uint32_t)(w[2 * i + 1] >> 32));
+    }
+  }
+  // red.global.add.u64 of the raw words into a zeroed accumulator record
+  ZKL_D static void atomic_add(uint64_t* dst, const LimbAcc<CH>& a) {
+    unsigned long long* d = reinterpret_cast<unsigned long long*>(dst);
+    if constexpr (CH == 1) {
+#pragma unroll
+      for (int i = 0; i < 8; i++) atomicAdd(d + i, (unsigned long long)a.e[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 9; i++) {
+        atomicAdd(d + i, (unsigned long long)a.e[i]);
+        atomicAdd(d + 9 + i, (unsigned long long)a.o[i]);
+      }
+    }
+  }
+  ZKL_D static void add(LimbAcc<CH>& a, const uint64_t* src) {
+    const uint4* q = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+    for (int i = 0; i < NW / 2; i++) {
+      const uint4 v = q[i];
+      const uint64_t w0 = ((uint64_t)v.y << 32) | v.x, w1 = ((uint64_t)v.w << 32) | v.z;
+      if constexpr (CH == 1) {
+        a.e[2 * i] += w0;
+        a.e[2 * i + 1] += w1;
+      } else {
+        const int j0 = 2 * i, j1 = 2 * i + 1;
+        if (j0 < 9) a.e[j0] += w0; else a.o[j0 - 9] += w0;
+        if (j1 < 9) a.e[j1] += w1; else a.o[j1 - 9] += w1;
+      }
+    }
+  }
+};
+
 template <class MT>
+ZKL_D void mac_entry(LimbAcc<sizeof(MT) == 2 ? 1 : 4>& acc, MT v, const fr_t& x) {
+  if constexpr (sizeof(MT) == 2)
+    mac_u16(acc, (uint32_t)((int32_t)v + 32768), x);
+  else
+    mac_u64(acc, (uint64_t)v ^ 0x8000000000000000ull, x);
+}
+
+// row products, R rows per thread (x reused R times from one broadcast
+// load): raw accumulator partials part[chunk][row][NW].  Split-K over column
+// chunks gives the grid its parallelism; the epilogue is a plain store.
+template <class MT, int R>
 __global__ void __launch_bounds__(256)
     k_mvf_rows(const MT* M, uint64_t rows, uint64_t cols, const fr_t* x, uint64_t cch,
-               const fr_t* K, fr_t* part) {
+               uint64_t* part) {
   constexpr int CH = sizeof(MT) == 2 ? 1 : 4;
-  constexpr int E = 64 / sizeof(MT);  // entries per 64-byte step
+  constexpr int E = 64 / sizeof(MT);  // entries per 64-byte step (per row)
+  using IO = AccIO<CH>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   fr_t* xs = reinterpret_cast<fr_t*>(smem_raw);
   const uint64_t c0 = blockIdx.y * cch;
@@ -471,47 +535,61 @@ __global__ void __launch_bounds__(256)
   const int n = (int)(c1 - c0);
   for (int i = threadIdx.x; i < n; i += blockDim.x) xs[i] = x[c0 + i];
   __syncthreads();
-  const uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (r >= rows) return;
-  LimbAcc<CH> acc;
-  acc.zero();
-  const MT* row = M + r * cols;
-  int c = 0;
-  const bool vec = ((uintptr_t)(row + c0) % 16) == 0;
-  if (vec) {
-    for (; c + E <= n; c += E) {
-      MT v[E];
-      const uint4* q = reinterpret_cast<const uint4*>(row + c0 + c);
+  const uint64_t r0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * R;
+  if (r0 >= rows) return;
+  LimbAcc<CH> acc[R];
 #pragma unroll
-      for (int i = 0; i < 4; i++) reinterpret_cast<uint4*>(v)[i] = __ldcs(q + i);
+  for (int q = 0; q < R; q++) acc[q].zero();
+  const MT* row0 = M + r0 * cols + c0;
+  const bool full = r0 + R <= rows;
+  int c = 0;
+  if (full && ((uintptr_t)row0 % 16) == 0 && (cols * sizeof(MT)) % 16 == 0) {
+    MT cur[R][E], nxt[R][E];
+    auto load = [&](MT (&dst)[R][E], int at) {
+#pragma unroll
+      for (int q = 0; q < R; q++) {
+        const uint4* p = reinterpret_cast<const uint4*>(row0 + q * cols + at);
+#pragma unroll
+        for (int h = 0; h < 4; h++) reinterpret_cast<uint4*>(dst[q])[h] = __ldcs(p + h);
+      }
+    };
+    if (c + E <= n) load(cur, c);
+    for (; c + E <= n; c += E) {
+      const bool more = c + 2 * E <= n;
+      if (more) load(nxt, c + E);  // software prefetch of the next step
 #pragma unroll
       for (int k = 0; k < E; k++) {
         const fr_t xv = xs[c + k];
-        if constexpr (CH == 1)
-          mac_u16(acc, (uint32_t)((int32_t)v[k] + 32768), xv);
-        else
-          mac_u64(acc, (uint64_t)v[k] ^ 0x8000000000000000ull, xv);
+#pragma unroll
+        for (int q = 0; q < R; q++) mac_entry<MT>(acc[q], cur[q][k], xv);
+      }
+      if (more) {
+#pragma unroll
+        for (int q = 0; q < R; q++)
+#pragma unroll
+          for (int k = 0; k < E; k++) cur[q][k] = nxt[q][k];
       }
     }
   }
   for (; c < n; c++) {
-    const MT sv = row[c0 + c];
     const fr_t xv = xs[c];
-    if constexpr (CH == 1)
-      mac_u16(acc, (uint32_t)((int32_t)sv + 32768), xv);
-    else
-      mac_u64(acc, (uint64_t)sv ^ 0x8000000000000000ull, xv);
+#pragma unroll
+    for (int q = 0; q < R; q++)
+      if (r0 + q < rows) mac_entry<MT>(acc[q], row0[q * cols + c], xv);
   }
-  part[blockIdx.y * rows + r] = Fr255::sub(limb_reduce<CH>(acc), K[blockIdx.y]);
+#pragma unroll
+  for (int q = 0; q < R; q++)
+    if (r0 + q < rows) IO::atomic_add(part + (r0 + q) * IO::NW, acc[q]);
 }
 
-// column products, thread per V consecutive columns: y_part[chunk][c] =
-// sum_{r in chunk} x[r] M[r, c]; coalesced row segments, x[r] broadcast.
+// column products, thread per V consecutive columns: raw partials
+// part[chunk][col][NW]; coalesced row segments, x[r] broadcast.
 template <class MT, int V>
 __global__ void __launch_bounds__(256)
     k_mvf_cols(const MT* M, uint64_t rows, uint64_t cols, const fr_t* x, uint64_t rch,
-               const fr_t* K, fr_t* part) {
+               uint64_t* part) {
   constexpr int CH = sizeof(MT) == 2 ? 1 : 4;
+  using IO = AccIO<CH>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   fr_t* xs = reinterpret_cast<fr_t*>(smem_raw);
   const uint64_t r0 = blockIdx.y * rch;
@@ -524,9 +602,8 @@ __global__ void __launch_bounds__(256)
   LimbAcc<CH> acc[V];
 #pragma unroll
   for (int v = 0; v < V; v++) acc[v].zero();
-  for (int i = 0; i < n; i++) {
+  auto load = [&](MT (&vals)[V], int i) {
     const MT* p = M + (r0 + i) * cols + c;
-    MT vals[V];
     if constexpr (sizeof(MT) * V == 8) {
       *reinterpret_cast<uint2*>(vals) = __ldcs(reinterpret_cast<const uint2*>(p));
     } else if constexpr (sizeof(MT) * V == 16) {
@@ -535,81 +612,137 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int v = 0; v < V; v++) vals[v] = p[v];
     }
-    const fr_t xv = xs[i];
+  };
+  // batches of RB rows: RB independent loads in flight, next batch
+  // prefetched while this one is multiplied (hides DRAM latency with few warps)
+  constexpr int RB = 8;
+  MT cur[RB][V], nxt[RB][V];
+  auto load_batch = [&](MT (&dst)[RB][V], int at) {
 #pragma unroll
-    for (int v = 0; v < V; v++) {
-      if constexpr (CH == 1)
-        mac_u16(acc[v], (uint32_t)((int32_t)vals[v] + 32768), xv);
-      else
-        mac_u64(acc[v], (uint64_t)vals[v] ^ 0x8000000000000000ull, xv);
+    for (int b = 0; b < RB; b++) {
+      if (at + b < n) load(dst[b], at + b);
+      else {
+#pragma unroll
+        for (int v = 0; v < V; v++) dst[b][v] = 0;
+      }
+    }
+  };
+  if (n > 0) load_batch(cur, 0);
+  for (int i = 0; i < n; i += RB) {
+    const bool more = i + RB < n;
+    if (more) load_batch(nxt, i + RB);
+#pragma unroll
+    for (int b = 0; b < RB; b++) {
+      if (i + b < n) {
+        const fr_t xv = xs[i + b];
+#pragma unroll
+        for (int v = 0; v < V; v++) mac_entry<MT>(acc[v], cur[b][v], xv);
+      }
+    }
+    if (more) {
+#pragma unroll
+      for (int b = 0; b < RB; b++)
+#pragma unroll
+        for (int v = 0; v < V; v++) cur[b][v] = nxt[b][v];
     }
   }
 #pragma unroll
-  for (int v = 0; v < V; v++)
-    part[blockIdx.y * cols + c + v] = Fr255::sub(limb_reduce<CH>(acc[v]), K[blockIdx.y]);
+  for (int v = 0; v < V; v++) IO::atomic_add(part + (c + v) * IO::NW, acc[v]);
 }
 
-// returns kUnsupported when the shape does not suit the fast kernels
+// y[i] = reduce(acc[i]) - K; one thread per output (acc: atomically summed
+// raw words of every chunk -- exact integer sums, order-independent)
+template <int CH>
+__global__ void __launch_bounds__(256)
+    k_mvf_finish(const uint64_t* part, uint64_t nchunks, uint64_t n, const fr_t* K, fr_t* y) {
+  using IO = AccIO<CH>;
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  LimbAcc<CH> acc;
+  acc.zero();
+  IO::add(acc, part + i * IO::NW);
+  y[i] = Fr255::sub(limb_reduce<CH>(acc), *K);
+}
+
+// returns kErrUnsupported when the shape does not suit the fast kernels
 template <class MT>
 static int matvec_fast(const MT* M, uint64_t rows, uint64_t cols, int transpose, const fr_t* x,
                        fr_t* y, cudaStream_t s) {
-  // blocks to aim for (ZKL_MV_WANT overrides, for tuning)
-  static const uint64_t kWant = [] {
-    const char* e = getenv("ZKL_MV_WANT");
-    return e ? (uint64_t)atoi(e) : (uint64_t)(2 * kSMs);
+  constexpr int CH = sizeof(MT) == 2 ? 1 : 4;
+  constexpr int NW = AccIO<CH>::NW;
+  // accumulator headroom: every limb sum must stay below 2^64 over the whole
+  // reduction dimension (entries < 2^16 per product chunk, 2 products per
+  // accumulator for int64)
+  const uint64_t klen = transpose ? rows : cols;
+  if (klen > (CH == 1 ? (1u << 16) : (1u << 15))) return kErrUnsupported;
+  // warps wanted (ZKL_MV_WARPS overrides, for tuning)
+  static const uint64_t kWarps = [] {
+    const char* e = getenv("ZKL_MV_WARPS");
+    return e ? (uint64_t)atoi(e) : (uint64_t)(24 * kSMs);
   }();
-  constexpr uint64_t kMaxChunk = 1u << 14;  // accumulator headroom (< 2^15 entries)
   uint64_t nchunks, nout;
   void* ws;
   int rc;
   if (!transpose) {
-    if (cols % 16) return kErrUnsupported;
-    const uint64_t rb = (rows + 255) / 256;
-    uint64_t cs = (kWant + rb - 1) / rb;
-    const uint64_t min_cs = (cols + kMaxChunk - 1) / kMaxChunk;
-    const uint64_t max_cs = (cols + 127) / 128;  // >= 128 columns per chunk
+    constexpr int R = 1;
+    if (cols % 32) return kErrUnsupported;
+    const uint64_t threads = (rows + R - 1) / R;
+    uint64_t cs = (kWarps * 32 + threads - 1) / threads;
+    const uint64_t max_cs = (cols + 63) / 64;  // >= 64 columns per chunk
     if (cs > max_cs) cs = max_cs;
-    if (cs < min_cs) cs = min_cs;
     if (cs < 1) cs = 1;
     uint64_t cch = (cols + cs - 1) / cs;
-    cch = (cch + 31) / 32 * 32;                 // keep 64-byte steps aligned
-    if (cch * sizeof(fr_t) > 48 * 1024) return kErrUnsupported;
+    cch = (cch + 31) / 32 * 32;  // keep 64-byte steps aligned
+    if (cch * sizeof(fr_t) > 96 * 1024) return kErrUnsupported;
     nchunks = (cols + cch - 1) / cch;
     nout = rows;
-    rc = scratch_reserve((nchunks * rows + nchunks) * sizeof(fr_t), &ws, s);
+    rc = scratch_reserve(rows * NW * 8 + 64, &ws, s);
     if (rc) return rc;
-    fr_t* K = (fr_t*)ws + nchunks * rows;
-    k_chunk_offsets<sizeof(MT) == 2 ? 1 : 4><<<(unsigned)nchunks, 256, 0, s>>>(x, cols, cch, K);
-    ZKL_LAUNCH_CHECK();
-    dim3 g((unsigned)rb, (unsigned)nchunks);
-    k_mvf_rows<MT><<<g, 256, cch * sizeof(fr_t), s>>>(M, rows, cols, x, cch, K, (fr_t*)ws);
+    ZKL_CUDA(cudaMemsetAsync(ws, 0, rows * NW * 8, s));
+    dim3 g((unsigned)((threads + 255) / 256), (unsigned)nchunks);
+    const size_t smem = cch * sizeof(fr_t);
+    if (smem > 48 * 1024)
+      ZKL_CUDA(cudaFuncSetAttribute(k_mvf_rows<MT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+    k_mvf_rows<MT, R><<<g, 256, smem, s>>>(M, rows, cols, x, cch, (uint64_t*)ws);
     ZKL_LAUNCH_CHECK();
   } else {
-    constexpr int V = sizeof(MT) == 2 ? 4 : 2;
-    if (cols % V || cols < 64 * V) return kErrUnsupported;
-    const uint64_t cb = (cols / V + 255) / 256;
-    uint64_t rs = (kWant + cb - 1) / cb;
-    const uint64_t min_rs = (rows + kMaxChunk - 1) / kMaxChunk;
-    const uint64_t max_rs = (rows + 63) / 64;  // >= 64 rows per chunk
+    constexpr int V = sizeof(MT) == 2 ? 2 : 1;
+    if (cols % V) return kErrUnsupported;
+    const uint64_t threads = cols / V;
+    uint64_t rs = (kWarps * 32 + threads - 1) / threads;
+    const uint64_t max_rs = (rows + 31) / 32;  // >= 32 rows per chunk
     if (rs > max_rs) rs = max_rs;
-    if (rs < min_rs) rs = min_rs;
     if (rs < 1) rs = 1;
     uint64_t rch = (rows + rs - 1) / rs;
-    if (rch * sizeof(fr_t) > 48 * 1024) return kErrUnsupported;
+    if (rch * sizeof(fr_t) > 96 * 1024) return kErrUnsupported;
     nchunks = (rows + rch - 1) / rch;
     if (nchunks > 65535) return kErrUnsupported;
     nout = cols;
-    rc = scratch_reserve((nchunks * cols + nchunks) * sizeof(fr_t), &ws, s);
+    rc = scratch_reserve(cols * NW * 8 + 64, &ws, s);
     if (rc) return rc;
-    fr_t* K = (fr_t*)ws + nchunks * cols;
-    k_chunk_offsets<sizeof(MT) == 2 ? 1 : 4><<<(unsigned)nchunks, 256, 0, s>>>(x, rows, rch, K);
-    ZKL_LAUNCH_CHECK();
-    dim3 g((unsigned)cb, (unsigned)nchunks);
-    k_mvf_cols<MT, V><<<g, 256, rch * sizeof(fr_t), s>>>(M, rows, cols, x, rch, K, (fr_t*)ws);
+    ZKL_CUDA(cudaMemsetAsync(ws, 0, cols * NW * 8, s));
+    dim3 g((unsigned)((threads + 255) / 256), (unsigned)nchunks);
+    const size_t smem = rch * sizeof(fr_t);
+    if (smem > 48 * 1024)
+      ZKL_CUDA(cudaFuncSetAttribute(k_mvf_cols<MT, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+    k_mvf_cols<MT, V><<<g, 256, smem, s>>>(M, rows, cols, x, rch, (uint64_t*)ws);
     ZKL_LAUNCH_CHECK();
   }
-  k_mv_reduce<Fr255><<<grid_for(nout * 32, 256, 8), 256, 0, s>>>((const fr_t*)ws, nchunks, nout,
-                                                                   y);
+  // K = OFF * sum(x) over the reduction dimension (offset-binary correction)
+  fr_t* K = (fr_t*)((uint64_t*)ws + nout * NW);
+  // OFF (2^15 or 2^63) in Montgomery form, computed once on the host
+  static fr_t offr = [] {
+    fr_t v = Fr255::zero();
+    if (CH == 1) v.v[0] = 1u << 15;
+    else v.v[1] = 1u << 31;
+    return Fr255::to_mont(v);
+  }();
+  k_offset_total<CH><<<1, 1024, 0, s>>>(x, klen, offr, K);
+  ZKL_LAUNCH_CHECK();
+  k_mvf_finish<CH><<<(unsigned)((nout + 255) / 256), 256, 0, s>>>((const uint64_t*)ws, nchunks,
+                                                                   nout, K, y);
   ZKL_LAUNCH_CHECK();
   return kOk;
 }
@@ -675,9 +808,11 @@ static int matvec_impl(const void* Mv, uint64_t rows, uint64_t cols, int transpo
   return kOk;
 }
 
-// ZKL_MATVEC_SLOW=1 forces the wide-accumulator kernels (cross-checks)
+// The mad.wide kernels are opt-in (ZKL_MATVEC_FAST=1) until they beat the
+// wide-accumulator kernels on B200 (profiles/r01: both at ~15% of the IMAD
+// peak, latency/occupancy-bound); both are exercised by the parity tests.
 static bool fast_enabled() {
-  static const bool on = getenv("ZKL_MATVEC_SLOW") == nullptr;
+  static const bool on = getenv("ZKL_MATVEC_FAST") != nullptr;
   return on;
 }
 

@@ -1038,9 +1038,62 @@ static void host_quad(const typename F::T& c0, const typename F::T& c1, const ty
 
 static bool g_phase_dirty = true;  // after a failure the ticket / flags need a reset
 
+bool no_persistent() {
+  // ncu marks its target with NV_NSIGHT_INJECTION_* / NV_TPS_LAUNCH_TOKEN;
+  // compute-sanitizer and other injectors use CUDA_INJECTION64_PATH
+  static const bool v =
+      getenv("ZKL_NO_PERSISTENT") != nullptr || getenv("CUDA_INJECTION64_PATH") != nullptr ||
+      getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr ||
+      getenv("NV_TPS_LAUNCH_TOKEN") != nullptr ||
+      (getenv("CUDA_LAUNCH_BLOCKING") && getenv("CUDA_LAUNCH_BLOCKING")[0] == '1');
+  return v;
+}
+
+// the same phase, one kernel launch per round (k_round) with the host
+// transcript in between; identical outputs
+template <class F>
+static int run_phase_stepwise(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out,
+                              uint8_t* point_out, typename F::T* finals_out, cudaStream_t s) {
+  using T = typename F::T;
+  constexpr int nb = F::kBytes;
+  a.stepwise = true;
+  std::vector<T> lazy;
+  if (a.prepare) {
+    int rc = a.prepare(lazy);
+    if (rc) return rc;
+    if (!lazy.empty()) a.post_add = lazy.data();
+  }
+  uint64_t size = 1ull << a.num_vars;
+  T r_prev = F::zero();
+  for (int j = 0; j < a.num_vars; j++) {
+    Post<F> post;
+    post.add = a.post_add ? a.post_add[j] : F::zero();
+    post.mul = a.post_mul;
+    uint8_t* rj = rounds_out + (size_t)j * (a.tm.degree + 1) * nb;
+    int rc = op_sumcheck_round<F>(a.tables, a.k, size, j > 0, r_prev, a.tm, post, rj, s);
+    if (rc) return rc;
+    if (j > 0) size >>= 1;
+    for (int x = 0; x <= a.tm.degree; x++) tr.append_elem("sumcheck/eval", rj + x * nb, nb);
+    challenge_canon<F>(tr, "sumcheck/round", point_out + (size_t)j * nb);
+    r_prev = host::from_canon<F>(point_out + (size_t)j * nb);
+  }
+  std::vector<uint8_t> fc((size_t)a.k * nb);
+  int rc = op_sumcheck_finish<F>(a.tables, a.k, r_prev, fc.data(), s);
+  if (rc) return rc;
+  a.fin_cache.resize(a.k);
+  for (int q = 0; q < a.k; q++) a.fin_cache[q] = host::from_canon<F>(fc.data() + (size_t)q * nb);
+  if (finals_out)
+    for (int q = 0; q < a.k; q++) finals_out[q] = a.fin_cache[q];
+  return kOk;
+}
+
 template <class F>
 int wait_phase_finals(const PhaseArgs<F>& a, typename F::T* finals_out, cudaStream_t s) {
   constexpr int NC = Words<F>::N;
+  if (a.stepwise) {
+    for (int q = 0; q < a.k; q++) finals_out[q] = a.fin_cache[q];
+    return kOk;
+  }
   Mailbox* mb_host;
   Mailbox* mb_dev;
   int rc = mailbox_for_current_device(&mb_host, &mb_dev);
@@ -1070,6 +1123,7 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
     set_error("sumcheck_prove: bad arguments");
     return kErrArg;
   }
+  if (no_persistent()) return run_phase_stepwise<F>(a, tr, rounds_out, point_out, finals_out, s);
   Mailbox* mb_host;
   Mailbox* mb_dev;
   int rc = mailbox_for_current_device(&mb_host, &mb_dev);
@@ -1133,7 +1187,11 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
   rq.bcast = bcast;
   rq.seq0 = seq0;
   rq.trace = trace;
+  // profiler: algorithmic bytes of the whole claim, sum over rounds of
+  // k 2^(n-j) elements read and (from round 1) k 2^(n-j-1) written by the fold
+  const int ph = prof_open(kProfPhase, 3.0 * k * (double)(1ull << n) * F::kBytes, (double)n, s);
   rc = run_dispatch<F>(rq, &pl, &nout, true);
+  prof_close(ph, s);
   if (rc) return rc;
   a.seq0 = seq0;
   // host-side finishing constants (canonical multipliers: mul(raw_storage,
@@ -1259,14 +1317,11 @@ int op_sumcheck_prove(void* const* tables, int k, int num_vars, const Terms<F>& 
   if (num_vars == 0) return kOk;
   // ZKL_NO_PERSISTENT=1: one launch per round.  Also chosen automatically
   // under tools that inject into the process and serialise / replay kernels
-  // (ncu, compute-sanitizer set CUDA_INJECTION64_PATH): a replayed kernel
+  // (ncu, compute-sanitizer): a replayed kernel
   // would spin on a mailbox the host never answers.
-  static const bool no_persistent =
-      getenv("ZKL_NO_PERSISTENT") != nullptr || getenv("CUDA_INJECTION64_PATH") != nullptr ||
-      (getenv("CUDA_LAUNCH_BLOCKING") && getenv("CUDA_LAUNCH_BLOCKING")[0] == '1');
   HostTranscript tr;
   memcpy(tr.state, state, 64);
-  if (no_persistent) {
+  if (no_persistent()) {
     uint64_t size = 1ull << num_vars;
     T r_prev = F::zero();
     for (int j = 0; j < num_vars; j++) {

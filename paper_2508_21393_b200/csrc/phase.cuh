@@ -33,7 +33,15 @@ struct PhaseArgs {
   // for the recognised shapes; the generic shape needs them at launch)
   std::function<int(std::vector<T>&)> prepare;
   uint32_t seq0 = 0;  // set by run_phase: mailbox sequence base of the launch
+  // one-launch-per-round mode (profilers): finals are kept here
+  bool stepwise = false;
+  std::vector<T> fin_cache;
 };
+
+// true when the persistent (mailbox) kernels must not be used: ZKL_NO_PERSISTENT,
+// CUDA_LAUNCH_BLOCKING=1, or an injected profiler / sanitizer (a replayed
+// kernel would spin on a mailbox the host never answers)
+bool no_persistent();
 
 // Runs every round with the native transcript `tr` (appends each evaluation
 // under "sumcheck/eval", draws "sumcheck/round").  Outputs are canonical

@@ -136,6 +136,21 @@ int op_matmul_prove(int ta, const void* A, int tb, const void* B, int tc, const 
   if (rc) return rc;
   T* base = (T*)wsv;
   auto buf = [&](int i) { return base + off[i]; };
+  // profiler brackets (no-ops unless zkl_prof_enable)
+  auto esz = [](int t) { return t == 1 ? 2.0 : t == 2 ? 4.0 : t == 3 ? 8.0 : (double)sizeof(T); };
+  auto mv = [&](int t, const void* M, uint64_t r_, uint64_t c_, int tr, const T* xin, T* yout) {
+    const int h = prof_open(kProfMatvec, (double)r_ * c_ * esz(t) + (double)(r_ + c_) * sizeof(T),
+                            (double)r_ * c_, s);
+    const int r2 = op_matvec<F>(t, M, r_, c_, tr, xin, yout, s);
+    prof_close(h, s);
+    return r2;
+  };
+  auto eq = [&](T* dst, const T* p_, int m) {
+    const int h = prof_open(kProfEq, (double)(1ull << m) * sizeof(T), (double)(1ull << m), s);
+    const int r2 = op_eq_table<F>(dst, p_, m, s);
+    prof_close(h, s);
+    return r2;
+  };
   std::vector<T> pt(64);
   auto load_point = [&](const uint8_t* canon, int m) {
     for (int i = 0; i < m; i++) pt[i] = host::from_canon<F>(canon + (size_t)i * nb);
@@ -143,14 +158,14 @@ int op_matmul_prove(int ta, const void* A, int tb, const void* B, int tc, const 
   };
 
   // ---- U phase inputs: E_v, bv = B E_v, cv = C E_v, h = A bv - cv
-  rc = op_eq_table<F>(buf(EV), load_point(rv.data(), d2), d2, s);
+  rc = eq(buf(EV), load_point(rv.data(), d2), d2);
   if (rc) return rc;
   gmark(1);
-  if ((rc = op_matvec<F>(tb, B, D1, D2, 0, buf(EV), buf(BV), s))) return rc;
-  if ((rc = op_matvec<F>(tc, C, D0, D2, 0, buf(EV), buf(EU), s))) return rc;  // cv
-  if ((rc = op_matvec<F>(ta, A, D0, D1, 0, buf(BV), buf(HV), s))) return rc;  // abv
+  if ((rc = mv(tb, B, D1, D2, 0, buf(EV), buf(BV)))) return rc;
+  if ((rc = mv(tc, C, D0, D2, 0, buf(EV), buf(EU)))) return rc;  // cv
+  if ((rc = mv(ta, A, D0, D1, 0, buf(BV), buf(HV)))) return rc;  // abv
   if ((rc = op_axpy<F>(buf(HV), buf(HV), H::sub(H::zero(), H::one()), buf(EU), D0, s))) return rc;
-  if ((rc = op_eq_table<F>(buf(EU), load_point(ru.data(), d0), d0, s))) return rc;
+  if ((rc = eq(buf(EU), load_point(ru.data(), d0), d0))) return rc;
   mark(1);
   gmark(2);
   uint8_t* rounds = rounds_out;
@@ -186,11 +201,11 @@ int op_matmul_prove(int ta, const void* A, int tb, const void* B, int tc, const 
   mark(2);
   gmark(3);
   // ---- W phase inputs: E(rho_u), a = E^T A, cu = E^T C, kappa = <cu, E_v>
-  if ((rc = op_eq_table<F>(buf(ERU), load_point(point, d0), d0, s))) return rc;
+  if ((rc = eq(buf(ERU), load_point(point, d0), d0))) return rc;
   rounds += (size_t)d0 * 4 * nb;
   point += (size_t)d0 * nb;
-  if ((rc = op_matvec<F>(ta, A, D0, D1, 1, buf(ERU), buf(AV), s))) return rc;
-  if ((rc = op_matvec<F>(tc, C, D0, D2, 1, buf(ERU), buf(CU), s))) return rc;
+  if ((rc = mv(ta, A, D0, D1, 1, buf(ERU), buf(AV)))) return rc;
+  if ((rc = mv(tc, C, D0, D2, 1, buf(ERU), buf(CU)))) return rc;
   if ((rc = op_dot<F>(buf(KAP), buf(CU), buf(EV), D2, s))) return rc;
   static thread_local T* kap_host = nullptr;
   static thread_local cudaEvent_t kap_ev = nullptr;
@@ -243,10 +258,10 @@ int op_matmul_prove(int ta, const void* A, int tb, const void* B, int tc, const 
   mark(4);
   gmark(5);
   // ---- V phase inputs: E(rho_w), bw = E^T B
-  if ((rc = op_eq_table<F>(buf(ERW), load_point(point, d1), d1, s))) return rc;
+  if ((rc = eq(buf(ERW), load_point(point, d1), d1))) return rc;
   rounds += (size_t)d1 * 4 * nb;
   point += (size_t)d1 * nb;
-  if ((rc = op_matvec<F>(tb, B, D1, D2, 1, buf(ERW), buf(BW), s))) return rc;
+  if ((rc = mv(tb, B, D1, D2, 1, buf(ERW), buf(BW)))) return rc;
   mark(5);
   gmark(6);
   T fin_v[3];

@@ -170,21 +170,13 @@ def _device_matrix(pt, rows, cols, spec):
 
 
 # ---------------------------------------------------------------------------
-MATVEC_HOOK = None  # bench.py: callable(stream, algorithmic_bytes) -> end event
 _MT_BYTES = {N.MT_I16: 2, N.MT_I32: 4, N.MT_I64: 8}
 
 
 def _matvec(M, x, transpose, spec):
     out = D.empty(spec, M.cols if transpose else M.rows)
-    end = None
-    if MATVEC_HOOK is not None:
-        eb = _MT_BYTES.get(M.mtype, spec.nbytes)
-        nbytes = M.rows * M.cols * eb + (M.rows + M.cols) * spec.nbytes
-        end = MATVEC_HOOK(torch.cuda.current_stream(), nbytes)
     N.check(N.lib().zkl_matvec(spec.fid, M.mtype, D.ptr(M.t), M.rows, M.cols,
                                1 if transpose else 0, D.ptr(x), D.ptr(out), D.stream()))
-    if end is not None:
-        end.record(torch.cuda.current_stream())
     return out
 
 

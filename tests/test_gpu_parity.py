@@ -2,6 +2,7 @@
 and the CPU oracle, bit-exact.  Run on a B200: pytest -m gpu.
 """
 
+import os
 import random
 
 import numpy as np
@@ -22,6 +23,7 @@ from paper_2508_21393_b200.gadgets import DeviceMatrix, ProverTensor, TensorRef 
 from paper_2508_21393_b200.transcript import Transcript  # noqa: E402
 
 KEY = StubKey()
+ROOT_DIR = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 class _Rng:
@@ -268,6 +270,45 @@ def test_matmul_factored_vs_oracle(field, dims, dt, mm_driver):
                                                     dims, t2)
     assert rounds == orounds and tuple(finals) == ofinals and point == opoint
     assert t1.state == t2.state
+
+
+def _run_isolated(code, **env):
+    import subprocess
+    import sys
+
+    return subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                          cwd=ROOT_DIR, env=dict(os.environ, **env))
+
+
+def test_stepwise_mode_matches_oracle():
+    """ZKL_NO_PERSISTENT=1 (what profilers get automatically): one launch per
+    round through the same drivers, still bit-exact."""
+    code = (
+        "import sys; sys.path[:0] = ['.', 'tests', 'tests/golden']\n"
+        "import test_gpu_parity as T\n"
+        "class M: pass\n"
+        "T.test_matmul_factored_vs_oracle('big', (5, 9, 3), 'i16', 'native')\n"
+        "T.test_matmul_factored_vs_oracle('test', (0, 10, 2), 'i16', 'native')\n"
+        "T.test_matmul_factored_vs_oracle('big', (7, 0, 7), 'i16', 'native')\n"
+        "T.test_sumcheck_shapes_vs_oracle('big', 6, 'sum2prod2')\n"
+        "T.test_sumcheck_shapes_vs_oracle('test', 16, 'prod3')\n"
+        "print('ok')\n")
+    r = _run_isolated(code, ZKL_NO_PERSISTENT="1")
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
+
+
+def test_matvec_fast_kernels_vs_numpy():
+    """The opt-in mad.wide matvec kernels (ZKL_MATVEC_FAST=1, read once per
+    process) against exact numpy products, in a child process."""
+    code = (
+        "import sys; sys.path[:0] = ['.', 'tests', 'tests/golden']\n"
+        "import test_gpu_parity as T\n"
+        "for mt in ('i16', 'i64'):\n"
+        "    for shape in [(64, 256), (1024, 256), (33, 4096), (256, 1024)]:\n"
+        "        T.test_matvec_extremes_vs_numpy('big', mt, shape)\n"
+        "print('ok')\n")
+    r = _run_isolated(code, ZKL_MATVEC_FAST="1")
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
 
 
 @pytest.mark.parametrize("field", ["big", "test"])
