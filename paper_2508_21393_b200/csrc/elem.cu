@@ -277,6 +277,62 @@ __global__ void k_eq_outer(typename F::T* dst, const typename F::T* hi, const ty
     dst[i] = F::mul(hi[i >> ml], lo[i & mask]);
 }
 
+// eq over m <= 16 coordinates with a product tree of depth ~log2(m):
+// level 1 (per block, in shared memory): coordinates in pairs, 4 entries per
+// pair = one product each; level 2 (per output): product of the <= 8 pair
+// values as a balanced tree.  ~4 dependent Montgomery products for m = 12
+// instead of m/2 in the two-chain direct form.
+template <class F>
+__global__ void __launch_bounds__(256) k_eq_tree(typename F::T* dst, PointArg<F> pt, int off,
+                                                 int m) {
+  using T = typename F::T;
+  __shared__ T grp[8][4];
+  const int G = (m + 1) / 2;
+  const int t = threadIdx.x;
+  if (t < 4 * G) {
+    const int g = t >> 2, e = t & 3;
+    const int j0 = 2 * g, j1 = 2 * g + 1;
+    const T a = (e >> 1) ? pt.r[off + j0] : pt.omr[off + j0];
+    if (j1 < m) {
+      const T b = (e & 1) ? pt.r[off + j1] : pt.omr[off + j1];
+      grp[g][e] = F::mul(a, b);
+    } else {
+      grp[g][e] = a;  // odd m: single-coordinate group (entries 0/2 and 1/3 alias)
+    }
+  }
+  __syncthreads();
+  const uint64_t n = 1ull << m;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + t; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    T v[8];
+#pragma unroll
+    for (int g = 0; g < 8; g++) {
+      if (g < G) {
+        const int j0 = 2 * g;
+        const int b0 = (int)((i >> (m - 1 - j0)) & 1);
+        const int b1 = j0 + 1 < m ? (int)((i >> (m - 2 - j0)) & 1) : 0;
+        v[g] = grp[g][(b0 << 1) | b1];
+      } else {
+        v[g] = F::one();
+      }
+    }
+    // balanced product tree over 8 slots (slots >= G are one)
+    T a, b, c, d;
+    if (G > 4) {
+      F::mul4(v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], a, b, c, d);
+      F::mul2(a, b, c, d, a, c);
+      dst[i] = F::mul(a, c);
+    } else if (G > 2) {
+      F::mul2(v[0], v[1], v[2], v[3], a, c);
+      dst[i] = F::mul(a, c);
+    } else if (G == 2) {
+      dst[i] = F::mul(v[0], v[1]);
+    } else {
+      dst[i] = v[0];
+    }
+  }
+}
+
 template <class F>
 int op_eq_table(void* dst, const typename F::T* point, int m, cudaStream_t s) {
   using T = typename F::T;
@@ -287,20 +343,26 @@ int op_eq_table(void* dst, const typename F::T* point, int m, cudaStream_t s) {
     pt.omr[j] = F::sub(F::one(), point[j]);
   }
   T* out = (T*)dst;
-  if (m <= 12) {
-    k_eq_direct<F><<<grid_for(1ull << m, 256), 256, 0, s>>>(out, pt, 0, m);
+  if (m == 0) {
+    k_eq_direct<F><<<1, 32, 0, s>>>(out, pt, 0, m);
     ZKL_LAUNCH_CHECK();
     return kOk;
   }
+  if (m <= 16) {
+    k_eq_tree<F><<<grid_for(1ull << m, 256), 256, 0, s>>>(out, pt, 0, m);
+    ZKL_LAUNCH_CHECK();
+    return kOk;
+  }
+  if (m > 32) { set_error("eq_table: 2^%d entries is beyond device memory", m); return kErrArg; }
   int mh = m / 2, ml = m - mh;
   void* ws;
   int rc = scratch_reserve(((1ull << mh) + (1ull << ml)) * sizeof(T), &ws, s);
   if (rc) return rc;
   T* hi = (T*)ws;
   T* lo = hi + (1ull << mh);
-  k_eq_direct<F><<<grid_for(1ull << mh, 256), 256, 0, s>>>(hi, pt, 0, mh);
+  k_eq_tree<F><<<grid_for(1ull << mh, 256), 256, 0, s>>>(hi, pt, 0, mh);
   ZKL_LAUNCH_CHECK();
-  k_eq_direct<F><<<grid_for(1ull << ml, 256), 256, 0, s>>>(lo, pt, mh, ml);
+  k_eq_tree<F><<<grid_for(1ull << ml, 256), 256, 0, s>>>(lo, pt, mh, ml);
   ZKL_LAUNCH_CHECK();
   k_eq_outer<F><<<grid_for(1ull << m, 256), 256, 0, s>>>(out, hi, lo, ml, 1ull << m);
   ZKL_LAUNCH_CHECK();
