@@ -58,6 +58,12 @@ int zkl_from_mont(int field, void* dst, const void* src, uint64_t n, void* strea
  * (from_signed) as used by QuantizedTensor.from_field, quantize.py:176-183. */
 int zkl_lift(int field, int int_type, void* dst, const void* src, uint64_t n, void* stream);
 
+/* Pair-table compression of a two-column lookup (gadgets.py:659-666 for the
+ * secret, tables.py:131-140 for the table): dst[i] = x[i] + alpha * y[i]
+ * mod p for signed integer columns x, y (ZKL_MT_I16 / I32 / I64). */
+int zkl_pair_combine(int field, void* dst, const void* x, int x_type, const void* y, int y_type,
+                     uint64_t n, const uint8_t* alpha_canon, void* stream);
+
 /* eq(point, .) over {0,1}^m, point[0] = MSB: mle.py:67-82 (eq_table).
  * point_canon: m canonical scalars (host). */
 int zkl_eq_table(int field, void* dst, const uint8_t* point_canon, int m, void* stream);

@@ -27,6 +27,7 @@ from .gadgets import (  # noqa: F401
     matmul_sumcheck,
     prove_elementprod,
     prove_matmul,
+    prove_pair_lookup,
 )
 from .lookup import (  # noqa: F401
     ElementNotInTable,

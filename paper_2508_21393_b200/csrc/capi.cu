@@ -135,6 +135,11 @@ int zkl_to_mont(int field, void* dst, const void* src, uint64_t n, void* stream)
 int zkl_from_mont(int field, void* dst, const void* src, uint64_t n, void* stream) {
   D(field, op_from_mont<F>(dst, src, n, (cudaStream_t)stream));
 }
+int zkl_pair_combine(int field, void* dst, const void* x, int x_type, const void* y, int y_type,
+                     uint64_t n, const uint8_t* alpha_canon, void* stream) {
+  D(field, op_pair_combine<F>(dst, x, x_type, y, y_type, n, scalar<F>(alpha_canon),
+                              (cudaStream_t)stream));
+}
 int zkl_lift(int field, int int_type, void* dst, const void* src, uint64_t n, void* stream) {
   D(field, op_lift<F>(dst, src, int_type, n, (cudaStream_t)stream));
 }

@@ -205,6 +205,45 @@ __global__ void k_lift(typename F::T* dst, const I* src, uint64_t n) {
     dst[i] = F::from_i64((int64_t)src[i]);
 }
 
+// pair-table compression (gadgets.py:659-666, tables.py:131-140):
+// dst[i] = x[i] + alpha * y[i] with signed integer columns lifted on the fly
+template <class F, class IX, class IY>
+__global__ void k_pair_combine(typename F::T* dst, const IX* x, const IY* y, uint64_t n,
+                               typename F::T alpha) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = F::add(F::from_i64((int64_t)x[i]), F::mul(alpha, F::from_i64((int64_t)y[i])));
+}
+
+template <class F, class IX>
+static int pair_combine_y(typename F::T* d, const IX* x, const void* y, int ty, uint64_t n,
+                          typename F::T a, cudaStream_t s) {
+  const unsigned g = grid_for(n, 256);
+  switch (ty) {
+    case 1: k_pair_combine<F, IX, int16_t><<<g, 256, 0, s>>>(d, x, (const int16_t*)y, n, a); break;
+    case 2: k_pair_combine<F, IX, int32_t><<<g, 256, 0, s>>>(d, x, (const int32_t*)y, n, a); break;
+    case 3: k_pair_combine<F, IX, int64_t><<<g, 256, 0, s>>>(d, x, (const int64_t*)y, n, a); break;
+    default: set_error("pair_combine: bad y type %d", ty); return kErrArg;
+  }
+  ZKL_LAUNCH_CHECK();
+  return kOk;
+}
+
+template <class F>
+int op_pair_combine(void* dst, const void* x, int tx, const void* y, int ty, uint64_t n,
+                    typename F::T alpha, cudaStream_t s) {
+  if (!n) return kOk;
+  using T = typename F::T;
+  T* d = (T*)dst;
+  switch (tx) {
+    case 1: return pair_combine_y<F, int16_t>(d, (const int16_t*)x, y, ty, n, alpha, s);
+    case 2: return pair_combine_y<F, int32_t>(d, (const int32_t*)x, y, ty, n, alpha, s);
+    case 3: return pair_combine_y<F, int64_t>(d, (const int64_t*)x, y, ty, n, alpha, s);
+  }
+  set_error("pair_combine: bad x type %d", tx);
+  return kErrArg;
+}
+
 template <class F>
 int op_to_mont(void* dst, const void* src, uint64_t n, cudaStream_t s) {
   if (!n) return kOk;
@@ -486,6 +525,8 @@ int op_read(uint8_t* host, const void* src, uint64_t n, cudaStream_t s) {
   template int op_to_mont<F>(void*, const void*, uint64_t, cudaStream_t);                 \
   template int op_from_mont<F>(void*, const void*, uint64_t, cudaStream_t);               \
   template int op_lift<F>(void*, const void*, int, uint64_t, cudaStream_t);               \
+  template int op_pair_combine<F>(void*, const void*, int, const void*, int, uint64_t, F::T,  \
+                                  cudaStream_t);                                             \
   template int op_eq_table<F>(void*, const F::T*, int, cudaStream_t);                     \
   template int op_fold<F>(void*, const void*, uint64_t, F::T, cudaStream_t);              \
   template int op_axpy<F>(void*, const void*, F::T, const void*, uint64_t, cudaStream_t); \

@@ -13,6 +13,10 @@ template <class F> int op_to_mont(void* dst, const void* src, uint64_t n, cudaSt
 template <class F> int op_from_mont(void* dst, const void* src, uint64_t n, cudaStream_t s);
 // mtype: 1 = int16, 2 = int32, 3 = int64 (signed; negatives -> p - |x|)
 template <class F> int op_lift(void* dst, const void* src, int mtype, uint64_t n, cudaStream_t s);
+// dst[i] = x[i] + alpha * y[i], signed integer columns (types 1..3 = int16/32/64)
+template <class F>
+int op_pair_combine(void* dst, const void* x, int tx, const void* y, int ty, uint64_t n,
+                    typename F::T alpha, cudaStream_t s);
 template <class F>
 int op_eq_table(void* dst, const typename F::T* point, int m, cudaStream_t s);
 template <class F>

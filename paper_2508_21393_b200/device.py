@@ -136,3 +136,49 @@ def dot(a, b, spec, n):
     N.check(N.lib().zkl_dot(spec.fid, raw, ptr(a), ptr(b) if b is not None else None, n,
                             stream()))
     return int.from_bytes(bytes(raw), "little")
+
+
+class DeviceVector:
+    """n field elements resident on the GPU (storage form).
+
+    Accepted wherever the reference passes a tuple of field residues
+    (SecretVector / LookupTable entries, multiplicity vectors), so large
+    lookups never round-trip through Python ints.
+    """
+
+    __slots__ = ("buf", "n", "spec")
+
+    def __init__(self, buf, n, spec):
+        self.buf, self.n, self.spec = buf, n, spec
+
+    def __len__(self):
+        return self.n
+
+    def to_list(self):
+        return download(self.buf, self.spec, self.n)
+
+
+def field_buffer(values, spec):
+    """Device storage for a DeviceVector or a sequence of residues."""
+    if isinstance(values, DeviceVector):
+        return values.buf
+    return upload(list(values), spec)
+
+
+def as_list(values):
+    return values.to_list() if isinstance(values, DeviceVector) else list(values)
+
+
+_INT_TYPES = {torch.int16: N.MT_I16, torch.int32: N.MT_I32, torch.int64: N.MT_I64}
+
+
+def pair_combine(x, y, alpha, spec):
+    """x + alpha * y for signed integer CUDA tensors (tables.py:131-140)."""
+    x = x.contiguous().view(-1)
+    y = y.contiguous().view(-1)
+    n = x.numel()
+    out = empty(spec, n)
+    N.check(N.lib().zkl_pair_combine(spec.fid, ptr(out), ptr(x), _INT_TYPES[x.dtype], ptr(y),
+                                     _INT_TYPES[y.dtype], n, scalar_bytes(alpha, spec),
+                                     stream()))
+    return DeviceVector(out, n, spec)

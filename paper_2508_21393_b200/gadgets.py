@@ -345,3 +345,63 @@ def prove_elementprod(a, b, c, key, tr, rng):
     ab_opening = _open_tables(key, committed, point, tr, rng, values=vals) if committed else None
     return TYPES["ElementprodProof"](shape=shape, c_opening=c_opening, sumcheck=sc_proof,
                                      ab_opening=ab_opening)
+
+
+# ---------------------------------------------------------------------------
+# pair-table lookups (gadgets.py:659-688)
+def _combine_commitments(key, commitments, coefficients):
+    """commit.combine_commitments, or the stub's (same num_vars) for StubKey."""
+    if getattr(key, "is_stub", False):
+        from .commit_stub import StubCommitment
+
+        return StubCommitment(commitments[0].num_vars)
+    import zklora.commit as zc
+
+    return zc.combine_commitments(key.group, commitments, coefficients)
+
+
+def _int_column(entries):
+    """A device integer column (torch int16/32/64 CUDA tensor) or None."""
+    return entries if torch.is_tensor(entries) and entries.is_cuda else None
+
+
+def prove_pair_lookup(label, x, y, pair_table, key, tr, rng):
+    """Mirror of zklora.gadgets._prove_pair_lookup (gadgets.py:679-688).
+
+    Same transcript traffic: x / y digests, alpha, then prove_lookup on the
+    compressed secret x + alpha*y against the compressed table
+    (tables.py:131-140).  When x / y carry device integer matrices and the
+    pair table's columns are device integer tensors, the compression,
+    multiplicities and the whole lookup stay on the GPU (DeviceVector
+    entries); otherwise the reference's list semantics apply.
+    """
+    from .lookup import LookupTable, SecretVector, compute_multiplicities, prove_lookup
+
+    p = tr.modulus
+    tr.append(label + b"/x", x.ref.digest(key.group))
+    tr.append(label + b"/y", y.ref.digest(key.group))
+    alpha = tr.challenge(label + b"/alpha")
+    spec = D.spec_for(p)
+    xd, yd = getattr(x, "device", None), getattr(y, "device", None)
+    tx, ty = _int_column(pair_table.x.entries), _int_column(pair_table.y.entries)
+    secret_com = _combine_commitments(key, [x.ref.commitment, y.ref.commitment], [1, alpha])
+    table_com = _combine_commitments(key, [pair_table.x.commitment, pair_table.y.commitment],
+                                     [1, alpha])
+    rows = 1 << ((x.ref.num_vars + 1) // 2)
+    bx = list(x.blinding) if x.blinding else [0] * rows
+    by = list(y.blinding) if y.blinding else [0] * rows
+    blinding = tuple((a + alpha * b) % p for a, b in zip(bx, by))
+    if (xd is not None and yd is not None and xd.mtype != N.MT_FIELD
+            and yd.mtype != N.MT_FIELD and tx is not None and ty is not None):
+        secret = SecretVector(D.pair_combine(xd.t, yd.t, alpha, spec), secret_com, blinding)
+        table = LookupTable(D.pair_combine(tx, ty, alpha, spec), table_com,
+                            pair_table.name + "+a*y")
+    else:
+        xs, ys = x.flat(), y.flat()
+        secret = SecretVector(tuple((a + alpha * b) % p for a, b in zip(xs, ys)), secret_com,
+                              blinding)
+        table = LookupTable(tuple((a + alpha * b) % p for a, b in
+                                  zip(pair_table.x.entries, pair_table.y.entries)),
+                            table_com, pair_table.name + "+a*y")
+    counts = compute_multiplicities(secret.entries, table)
+    return prove_lookup(secret, counts, table, key, tr, rng)

@@ -111,7 +111,22 @@ def multiplicities_device(secret_buf, d, table_buf, n, spec):
 
 
 def compute_multiplicities(secret_entries, table, modulus=None):
-    """Drop-in for zklora.lookup.compute_multiplicities (lookup.py:91-99)."""
+    """Drop-in for zklora.lookup.compute_multiplicities (lookup.py:91-99).
+
+    With device-resident entries (DeviceVector) the counts stay on the GPU
+    and come back as a DeviceVector of field elements."""
+    if isinstance(secret_entries, D.DeviceVector) or isinstance(table.entries, D.DeviceVector):
+        spec = (secret_entries.spec if isinstance(secret_entries, D.DeviceVector)
+                else table.entries.spec)
+        sbuf = D.field_buffer(secret_entries, spec)
+        tbuf = D.field_buffer(table.entries, spec)
+        d, n = len(secret_entries), len(table.entries)
+        counts, miss = multiplicities_device(sbuf, d, tbuf, n, spec)
+        if miss is not None:
+            raise TYPES["ElementNotInTable"](miss, D.read_scalar(sbuf, spec, miss))
+        out = D.empty(spec, n)
+        N.check(N.lib().zkl_lift_u32(spec.fid, D.ptr(out), D.ptr(counts), n, D.stream()))
+        return D.DeviceVector(out, n, spec)
     entries = list(secret_entries)
     tab = list(table.entries)
     if modulus is None:
@@ -166,14 +181,14 @@ def prove_lookup(secret, multiplicities, table, key, tr, rng):
     # m commitment + setup absorption (lookup.py:158-161)
     m_rows, _ = be.split_shape(table.num_vars)
     m_blinding = rng.vector(m_rows)
-    m_commitment = be.commit(key, list(multiplicities), m_blinding)
+    m_commitment = be.commit(key, _Sized(n) if stub else D.as_list(multiplicities), m_blinding)
     tr.append(b"lookup/table", table.commitment.serialize(group))
     tr.append(b"lookup/secret", secret.commitment.serialize(group))
     tr.append(b"lookup/mult", m_commitment.serialize(group))
 
-    s_buf = D.upload(list(entries), spec)
-    t_buf = D.upload(list(table.entries), spec)
-    m_buf = D.upload(list(multiplicities), spec)
+    s_buf = D.field_buffer(entries, spec)
+    t_buf = D.field_buffer(table.entries, spec)
+    m_buf = D.field_buffer(multiplicities, spec)
 
     # beta with pole retries (lookup.py:163-171): a pole is exactly a zero in
     # beta + s or beta + t, which the device batch inversion reports.
@@ -261,10 +276,10 @@ def prove_lookup(secret, multiplicities, table, key, tr, rng):
             key, None, None, table_point, tr, rng, values=t_vals)
     else:
         secret_values, secret_opening = be.open_batch(
-            key, [inv_s_host, list(entries)], [list(a_blinding), list(secret.blinding)],
+            key, [inv_s_host, D.as_list(entries)], [list(a_blinding), list(secret.blinding)],
             secret_point, tr, rng)
         table_values, table_opening = be.open_batch(
-            key, [list(multiplicities), inv_t_host, list(table.entries)],
+            key, [D.as_list(multiplicities), inv_t_host, D.as_list(table.entries)],
             [list(m_blinding), zero_blind, zero_blind], table_point, tr, rng)
     return TYPES["LookupProof"](
         secret.num_vars, retries, m_commitment, a_commitment, b_commitment, sc_proof,

@@ -358,6 +358,39 @@ def test_elementprod_golden():
 # --- logUp -----------------------------------------------------------------------------
 
 
+class _PairTable:
+    def __init__(self, x, y, name):
+        self.x, self.y, self.name = x, y, name
+
+
+def test_pair_lookup_golden_device():
+    """SiLU pair lookup (gadgets.py:679-688) entirely on the GPU: device int
+    columns -> x + alpha*y compression -> multiplicities -> logUp; bit-exact
+    with the reference's own run (tests/golden/pair_lookup.json)."""
+    for c in load_golden("pair_lookup.json"):
+        p = FIELDS[c["field"]]
+        n = len(c["x"])
+        nv = (n - 1).bit_length()
+
+        def pt(vals):
+            ref = TensorRef("committed", nv // 2, nv - nv // 2, commitment=StubCommitment(nv))
+            t = torch.tensor(vals, dtype=torch.int32).cuda().view(1 << (nv // 2), -1)
+            return ProverTensor(None, ref, (), device=DeviceMatrix.from_int_tensor(t))
+
+        tx = torch.tensor(c["table_x"], dtype=torch.int32).cuda()
+        ty = torch.tensor(c["table_y"], dtype=torch.int32).cuda()
+        pair = _PairTable(zb.LookupTable(tx, StubCommitment(7)), zb.LookupTable(ty, StubCommitment(7)),
+                          "silu")
+        t = _tr(c["state_before"], p)
+        pr = zb.prove_pair_lookup(b"swiglu/act", pt(c["x"]), pt(c["y"]), pair, KEY, t, RNG)
+        assert pr.beta_retries == c["beta_retries"]
+        assert [list(r.evaluations) for r in pr.sumcheck.rounds] == c["rounds"]
+        assert list(pr.sumcheck.final_values) == c["final_values"]
+        assert list(pr.secret_values) == c["secret_values"]
+        assert list(pr.table_values) == c["table_values"]
+        assert t.state.hex() == c["state_end"]
+
+
 def test_multiplicities_golden():
     for c in load_golden("lookup.json")["multiplicities"]:
         table = zb.LookupTable(tuple(c["table"]), None)
