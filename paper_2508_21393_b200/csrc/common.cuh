@@ -154,7 +154,8 @@ constexpr size_t kFixedBcast = 256;   // challenge broadcast slot (tagged words,
 // 32), written and read with single 8-byte accesses, so a reader knows a
 // message is complete when every word carries the expected sequence number:
 // no flag word and no system-scope fence on either side.
-constexpr int kMbEvalWords = 8 * 9;   // up to 8 outputs x 9 words (wide Fr sums)
+constexpr int kMbMaxOut = 16;         // raw outputs per round (LOGUP shape: 16)
+constexpr int kMbEvalWords = kMbMaxOut * 9;  // x 9 words (wide Fr sums)
 constexpr int kMbFinalWords = 8 * 8;  // up to 8 tables x 8 words
 struct alignas(128) Mailbox {
   volatile uint64_t ev[kMbEvalWords];   // device -> host: round sums

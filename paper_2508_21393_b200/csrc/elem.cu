@@ -109,7 +109,10 @@ void prof_collect(int kind, double* ms, double* bytes, double* units, uint64_t* 
     }
     float e = 0;
     cudaEventSynchronize(r.b);
-    cudaEventElapsedTime(&e, r.a, r.b);
+    if (cudaEventElapsedTime(&e, r.a, r.b) != cudaSuccess) {
+      e = 0;  // bracket never closed: do not leave a sticky error behind
+      cudaGetLastError();
+    }
     t += e;
     by += r.bytes;
     un += r.units;

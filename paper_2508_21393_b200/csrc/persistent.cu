@@ -136,7 +136,7 @@ struct Red<M61> {
 // fold product + one (PROD2, SUM2PROD2) or two (PROD3) evaluation products.
 inline int lanes_for(int shape, int k) {
   if (shape == kGeneric) return 0;
-  const int nout = shape == kProd2 ? 3 : shape == kProd3 ? 4 : 6;
+  const int nout = shape == kProd2 ? 3 : shape == kProd3 ? 4 : shape == kLogup ? 16 : 6;
   const int need = 2 * k > nout ? 2 * k : nout;  // fold lanes / output lanes
   return need <= 4 ? 4 : need <= 8 ? 8 : 16;
 }
@@ -319,6 +319,105 @@ struct EvProd3 {
     if (x == 3) qq = qx[3];
     const T m = F::mul(qq, bx);
     return (active && q < 4) ? m : F::zero();
+  }
+};
+
+// logUp Eq.-7 claim (lookup.py:116-126): terms
+//   c0 E A S + c1 E I + c2 E B T + c3 A + c4 M B
+// (E eq, A 1/(beta+s), S s+beta, I indicator, B 1/(beta+t), T t+beta, M
+// multiplicities).  Raw sums returned for the host to combine with c0..c4:
+//   [0..3] sum E(x) (AS)(x)      x = 0..3   (AS quadratic from 3 products)
+//   [4..6] E I   as (lo lo, hi hi, slope slope)
+//   [7..10] sum E(x) (BT)(x)     x = 0..3
+//   [11..12] sum A lo, sum A slope (linear)
+//   [13..15] M B  as (lo lo, hi hi, slope slope)
+// 20 products per pair instead of ~44 for the generic term loop.
+template <class F, int MAXK>
+struct EvLogup {
+  using T = typename F::T;
+  static constexpr int NA = 16, NOUT = 16;
+  struct Idx {
+    int e, a, s, i, b, t, m;
+  };
+  ZKL_D static Idx idx(const Terms<F>& tm) {
+    return Idx{tm.fi[0][0], tm.fi[0][1], tm.fi[0][2], tm.fi[1][1],
+               tm.fi[2][1], tm.fi[2][2], tm.fi[4][0]};
+  }
+  ZKL_D static void pair(T (&cur)[MAXK], const T (&df)[MAXK], int, const Terms<F>& tm,
+                         T (&acc)[NA]) {
+    const Idx x = idx(tm);
+    const T e0 = select_tab<F, MAXK>(cur, x.e), ed = select_tab<F, MAXK>(df, x.e);
+    const T a0 = select_tab<F, MAXK>(cur, x.a), ad = select_tab<F, MAXK>(df, x.a);
+    const T s0 = select_tab<F, MAXK>(cur, x.s), sd = select_tab<F, MAXK>(df, x.s);
+    const T i0 = select_tab<F, MAXK>(cur, x.i), id = select_tab<F, MAXK>(df, x.i);
+    const T b0 = select_tab<F, MAXK>(cur, x.b), bd = select_tab<F, MAXK>(df, x.b);
+    const T t0 = select_tab<F, MAXK>(cur, x.t), td = select_tab<F, MAXK>(df, x.t);
+    const T m0 = select_tab<F, MAXK>(cur, x.m), md = select_tab<F, MAXK>(df, x.m);
+    const T e1 = F::add(e0, ed), a1 = F::add(a0, ad), s1 = F::add(s0, sd);
+    const T b1 = F::add(b0, bd), t1 = F::add(t0, td), i1 = F::add(i0, id);
+    const T m1 = F::add(m0, md);
+    T as[4], bt[4], p[4], q[4];
+    F::mul4(a0, s0, a1, s1, ad, sd, b0, t0, p[0], p[1], p[2], q[0]);
+    F::mul2(b1, t1, bd, td, q[1], q[2]);
+    quad_evals<F>(p[0], p[1], p[2], as);
+    quad_evals<F>(q[0], q[1], q[2], bt);
+    const T e2 = F::add(e1, ed), e3 = F::add(e2, ed);
+    T o[8];
+    F::mul4(e0, as[0], e1, as[1], e2, as[2], e3, as[3], o[0], o[1], o[2], o[3]);
+    F::mul4(e0, bt[0], e1, bt[1], e2, bt[2], e3, bt[3], o[4], o[5], o[6], o[7]);
+    T ei[3], mb[3];
+    F::mul3(e0, i0, e1, i1, ed, id, ei[0], ei[1], ei[2]);
+    F::mul3(m0, b0, m1, b1, md, bd, mb[0], mb[1], mb[2]);
+#pragma unroll
+    for (int k = 0; k < 4; k++) acc[k] = F::add(acc[k], o[k]);
+#pragma unroll
+    for (int k = 0; k < 3; k++) acc[4 + k] = F::add(acc[4 + k], ei[k]);
+#pragma unroll
+    for (int k = 0; k < 4; k++) acc[7 + k] = F::add(acc[7 + k], o[4 + k]);
+    acc[11] = F::add(acc[11], a0);
+    acc[12] = F::add(acc[12], ad);
+#pragma unroll
+    for (int k = 0; k < 3; k++) acc[13 + k] = F::add(acc[13 + k], mb[k]);
+  }
+  ZKL_D static void finish(const T (&acc)[NA], T (&out)[NOUT]) {
+#pragma unroll
+    for (int q = 0; q < 16; q++) out[q] = acc[q];
+  }
+  // lane mode (L = 16): level-1 products on lanes 0-2 (A S), 4-6 (E I, outputs),
+  // 7-9 (B T), 13-15 (M B, outputs); level-2 E(x) (AS)(x) on lanes 0-3 and
+  // E(x) (BT)(x) on lanes 7-10; lanes 11/12 carry A lo / A slope.
+  ZKL_D static T lane(const T& v, int q, int gb, bool active, const Terms<F>& tm) {
+    const Idx x = idx(tm);
+    int X = x.a, Y = x.a, sel = 0;
+    if (q < 3) { X = x.a; Y = x.s; sel = q; }
+    else if (q >= 4 && q < 7) { X = x.e; Y = x.i; sel = q - 4; }
+    else if (q >= 7 && q < 10) { X = x.b; Y = x.t; sel = q - 7; }
+    else if (q >= 13) { X = x.m; Y = x.b; sel = q - 13; }
+    const T xl = shfl_elem<F>(v, gb + 2 * X), xh = shfl_elem<F>(v, gb + 2 * X + 1);
+    const T yl = shfl_elem<F>(v, gb + 2 * Y), yh = shfl_elem<F>(v, gb + 2 * Y + 1);
+    const T p1 = F::mul(pick3<F>(xl, xh, sel), pick3<F>(yl, yh, sel));
+    const int base = q < 7 ? 0 : 7;  // which quadratic feeds level 2
+    const T c0 = shfl_elem<F>(p1, gb + base), c1 = shfl_elem<F>(p1, gb + base + 1);
+    const T c2 = shfl_elem<F>(p1, gb + base + 2);
+    T qx[4];
+    quad_evals<F>(c0, c1, c2, qx);
+    const T el = shfl_elem<F>(v, gb + 2 * x.e), eh = shfl_elem<F>(v, gb + 2 * x.e + 1);
+    const T ed = F::sub(eh, el);
+    const int xx = (q < 4 ? q : q - 7) & 3;
+    T ex = xx == 0 ? el : eh, qv = qx[0];
+    if (xx >= 2) ex = F::add(ex, ed);
+    if (xx == 3) ex = F::add(ex, ed);
+    if (xx == 1) qv = qx[1];
+    if (xx == 2) qv = qx[2];
+    if (xx == 3) qv = qx[3];
+    const T p2 = F::mul(ex, qv);
+    const T al = shfl_elem<F>(v, gb + 2 * x.a), ah = shfl_elem<F>(v, gb + 2 * x.a + 1);
+    T out;
+    if (q < 4 || (q >= 7 && q < 11)) out = p2;
+    else if (q == 11) out = al;
+    else if (q == 12) out = F::sub(ah, al);
+    else out = p1;  // 4-6 (E I) and 13-15 (M B)
+    return active ? out : F::zero();
   }
 };
 
@@ -903,6 +1002,10 @@ int detect_shape(const Terms<F>& tm) {
   if (tm.nterms == 2 && tm.nf[0] == 2 && tm.nf[1] == 2 && tm.fi[0][0] == tm.fi[1][0] &&
       tm.degree >= 2)
     return kSum2Prod2;
+  if (tm.nterms == 5 && tm.degree == 3 && tm.nf[0] == 3 && tm.nf[1] == 2 && tm.nf[2] == 3 &&
+      tm.nf[3] == 1 && tm.nf[4] == 2 && tm.fi[1][0] == tm.fi[0][0] &&
+      tm.fi[2][0] == tm.fi[0][0] && tm.fi[3][0] == tm.fi[0][1] && tm.fi[4][1] == tm.fi[2][1])
+    return kLogup;
   return kGeneric;
 }
 
@@ -921,8 +1024,14 @@ struct LaunchReq {
 };
 
 // query (pl != null, launch == false): fill the plan; launch: both kernels
+// launch: 0 = plan only, 1 = the grid kernel (rounds [0, j_switch)),
+// 2 = the cluster kernel (rounds [j_switch, n)).  The host launches the
+// cluster part only once the grid kernel no longer waits on it (at the
+// handoff round): a launch that blocks -- e.g. lazy loading of the kernel
+// image on first use -- must never sit between a device kernel and the host
+// answer it is spinning for.
 template <class F, int MAXK>
-static int dispatch(const LaunchReq<F>& q, Plan* pl, int* nout, bool launch) {
+static int dispatch(const LaunchReq<F>& q, Plan* pl, int* nout, int launch) {
 #define ZKL_SHAPE(EVT)                                                                      \
   {                                                                                         \
     using P = Persistent<F, MAXK, EVT<F, MAXK>>;                                            \
@@ -931,26 +1040,26 @@ static int dispatch(const LaunchReq<F>& q, Plan* pl, int* nout, bool launch) {
       *pl = P::plan(q.num_vars, lanes_for(q.shape, q.k));                                  \
       return kOk;                                                                           \
     }                                                                                       \
-    int rc_ = kOk;                                                                          \
-    if (pl->j_switch > 0)                                                                   \
-      rc_ = P::launch_grid(*pl, q.tables, q.k, q.num_vars, *q.tm, q.mb, q.partials,         \
-                           q.ticket, q.bcast, q.fail, q.seq0, q.trace, q.s);                \
-    if (rc_ == kOk && pl->j_switch < q.num_vars)                                            \
-      rc_ = P::launch_cluster(*pl, q.tables, q.k, q.num_vars, *q.tm, q.mb, q.fail, q.seq0,  \
-                              q.trace, q.s);                                                \
-    return rc_;                                                                             \
+    if (launch == 1)                                                                        \
+      return P::launch_grid(*pl, q.tables, q.k, q.num_vars, *q.tm, q.mb, q.partials,        \
+                            q.ticket, q.bcast, q.fail, q.seq0, q.trace, q.s);               \
+    return P::launch_cluster(*pl, q.tables, q.k, q.num_vars, *q.tm, q.mb, q.fail, q.seq0,   \
+                             q.trace, q.s);                                                 \
   }
   switch (q.shape) {
     case kProd2: ZKL_SHAPE(EvProd2)
     case kProd3: ZKL_SHAPE(EvProd3)
     case kSum2Prod2: ZKL_SHAPE(EvSum2Prod2)
+    case kLogup:
+      if constexpr (MAXK >= 8) ZKL_SHAPE(EvLogup)
+      else ZKL_SHAPE(EvGeneric)
     default: ZKL_SHAPE(EvGeneric)
   }
 #undef ZKL_SHAPE
 }
 
 template <class F>
-static int run_dispatch(const LaunchReq<F>& q, Plan* pl, int* nout, bool launch) {
+static int run_dispatch(const LaunchReq<F>& q, Plan* pl, int* nout, int launch) {
   if (q.k <= 2) return dispatch<F, 2>(q, pl, nout, launch);
   if (q.k <= 4) return dispatch<F, 4>(q, pl, nout, launch);
   return dispatch<F, 8>(q, pl, nout, launch);
@@ -1128,7 +1237,8 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
   Mailbox* mb_dev;
   int rc = mailbox_for_current_device(&mb_host, &mb_dev);
   if (rc) return rc;
-  const int shape = detect_shape<F>(tm);
+  int shape = detect_shape<F>(tm);
+  if (shape == kLogup && k <= 4) shape = kGeneric;  // the LOGUP evaluator is built for MAXK 8
   LaunchReq<F> rq;
   rq.shape = shape;
   rq.k = k;
@@ -1138,9 +1248,9 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
   rq.s = s;
   Plan pl;
   int nout = 4;
-  run_dispatch<F>(rq, &pl, &nout, false);
+  run_dispatch<F>(rq, &pl, &nout, 0);
   void* ws;
-  rc = scratch_reserve((size_t)pl.grid * 8 * sizeof(W), &ws, s);
+  rc = scratch_reserve((size_t)pl.grid * kMbMaxOut * sizeof(W), &ws, s);
   if (rc) return rc;
   void* fx;
   rc = fixed_words(&fx);
@@ -1190,13 +1300,13 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
   // profiler: algorithmic bytes of the whole claim, sum over rounds of
   // k 2^(n-j) elements read and (from round 1) k 2^(n-j-1) written by the fold
   const int ph = prof_open(kProfPhase, 3.0 * k * (double)(1ull << n) * F::kBytes, (double)n, s);
-  rc = run_dispatch<F>(rq, &pl, &nout, true);
-  prof_close(ph, s);
+  rc = run_dispatch<F>(rq, &pl, &nout, pl.j_switch > 0 ? 1 : 2);
+  if (pl.j_switch == 0 || pl.j_switch >= n) prof_close(ph, s);  // else: at the handoff
   if (rc) return rc;
   a.seq0 = seq0;
   // host-side finishing constants (canonical multipliers: mul(raw_storage,
   // K_canon) = value * K in canonical form), set at round 0 after prepare()
-  T Kc[2];
+  T Kc[5];
   T pm = a.post_mul;
   std::vector<T> lazy_add;
   bool prepared = !a.prepare;
@@ -1231,11 +1341,11 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
       if (shape == kGeneric) {
         Kc[0] = host::canon_of<F>(pm);
       } else {
-        Kc[0] = host::canon_of<F>(H::mul(pm, a.tm.coef[0]));
-        if (shape == kSum2Prod2) Kc[1] = host::canon_of<F>(H::mul(pm, a.tm.coef[1]));
+        const int nk = shape == kLogup ? 5 : shape == kSum2Prod2 ? 2 : 1;
+        for (int t = 0; t < nk; t++) Kc[t] = host::canon_of<F>(H::mul(pm, a.tm.coef[t]));
       }
     }
-    T raw[8];
+    T raw[kMbMaxOut];
     for (int q = 0; q < nout; q++) raw[q] = HostRed<F>::reduce(words + q * NW);
     T ev[4];
     if (shape == kProd2) {
@@ -1246,6 +1356,18 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
       host_quad<F>(raw[0], raw[1], raw[2], e1);
       host_quad<F>(raw[3], raw[4], raw[5], e2);
       for (int x = 0; x < 4; x++) ev[x] = H::add(H::mul(e1[x], Kc[0]), H::mul(e2[x], Kc[1]));
+    } else if (shape == kLogup) {
+      T ei[4], mb[4];
+      host_quad<F>(raw[4], raw[5], raw[6], ei);
+      host_quad<F>(raw[13], raw[14], raw[15], mb);
+      T ax = raw[11];  // A lo + x A slope
+      for (int x = 0; x < 4; x++) {
+        if (x) ax = H::add(ax, raw[12]);
+        T v = H::add(H::mul(raw[x], Kc[0]), H::mul(ei[x], Kc[1]));
+        v = H::add(v, H::mul(raw[7 + x], Kc[2]));
+        v = H::add(v, H::mul(ax, Kc[3]));
+        ev[x] = H::add(v, H::mul(mb[x], Kc[4]));
+      }
     } else {
       for (int x = 0; x < 4; x++) ev[x] = H::mul(raw[x], Kc[0]);
     }
@@ -1269,6 +1391,15 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
     for (int w = 0; w < NC; w++) mb_host->ch[w] = tg | cw[w];
     std::atomic_thread_fence(std::memory_order_seq_cst);  // drain the store buffer now
     if (tracing) h_sent[j] = now_us();
+    if (pl.j_switch > 0 && j == pl.j_switch - 1 && pl.j_switch < n) {
+      // handoff: the grid kernel has published its last round and exits
+      rc = run_dispatch<F>(rq, &pl, &nout, 2);
+      prof_close(ph, s);
+      if (rc) {
+        g_phase_dirty = true;
+        return rc;
+      }
+    }
     tr.challenge_absorb(rawc);
   }
   if (finals_out) {

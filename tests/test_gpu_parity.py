@@ -154,6 +154,9 @@ SHAPES = {
     "prod3": (3, [(0, 1, 2)], 3),
     "sum2prod2": (3, [(0, 1), (0, 2)], 3),
     "generic-mixed": (3, [(0, 1, 2), (1,), ()], 3),
+    "logup": (7, [(0, 1, 2), (0, 3), (0, 4, 5), (1,), (6, 4)], 3),
+    "logup-permuted": (7, [(3, 6, 0), (3, 2), (3, 5, 1), (6,), (4, 5)], 3),
+    "logup-repeated-k4": (4, [(0, 1, 2), (0, 3), (0, 1, 3), (1,), (2, 1)], 3),
 }
 
 
