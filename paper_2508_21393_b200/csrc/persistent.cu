@@ -176,6 +176,7 @@ ZKL_D typename F::T pick3(const typename F::T& lo, const typename F::T& hi, int 
 template <class F, int MAXK>
 struct EvGeneric {
   using T = typename F::T;
+  static constexpr bool kGeneric = true;
   static constexpr int NA = 4, NOUT = 4;
   ZKL_D static void pair(T (&cur)[MAXK], const T (&df)[MAXK], int k, const Terms<F>& tm,
                          T (&acc)[NA]) {
@@ -200,6 +201,7 @@ struct EvGeneric {
 template <class F, int MAXK>
 struct EvProd2 {
   using T = typename F::T;
+  static constexpr bool kGeneric = false;
   static constexpr int NA = 3, NOUT = 3;
   ZKL_D static void pair(T (&cur)[MAXK], const T (&df)[MAXK], int, const Terms<F>& tm,
                          T (&acc)[NA]) {
@@ -230,6 +232,7 @@ struct EvProd2 {
 template <class F, int MAXK>
 struct EvSum2Prod2 {
   using T = typename F::T;
+  static constexpr bool kGeneric = false;
   static constexpr int NA = 6, NOUT = 6;
   ZKL_D static void pair(T (&cur)[MAXK], const T (&df)[MAXK], int, const Terms<F>& tm,
                          T (&acc)[NA]) {
@@ -275,6 +278,7 @@ ZKL_D void quad_evals(const typename F::T& c0, const typename F::T& c1, const ty
 template <class F, int MAXK>
 struct EvProd3 {
   using T = typename F::T;
+  static constexpr bool kGeneric = false;
   static constexpr int NA = 4, NOUT = 4;
   ZKL_D static void pair(T (&cur)[MAXK], const T (&df)[MAXK], int, const Terms<F>& tm,
                          T (&acc)[NA]) {
@@ -335,6 +339,7 @@ struct EvProd3 {
 template <class F, int MAXK>
 struct EvLogup {
   using T = typename F::T;
+  static constexpr bool kGeneric = false;
   static constexpr int NA = 16, NOUT = 16;
   struct Idx {
     int e, a, s, i, b, t, m;
@@ -573,6 +578,9 @@ struct Words {
 // evaluates its pairs (lane mode when L > 0, else one pair per thread), then
 // leaves the warp's wide sums in wsum[warp][0..NOUT).  Every thread of the
 // block must call it (it ends with the warp shuffles).
+// Lane mode for small rounds (L > 0), one pair per thread otherwise (large
+// rounds: more independent products per thread, no shuffles; measured 45 vs
+// 74 ms for the 2^25 logUp claim with lane mode forced everywhere).
 template <class F, int MAXK, class EV>
 ZKL_D void accumulate_round(const TablePtrs<F, MAXK>& tabs, int k, const Terms<F>& tm,
                             uint64_t half, bool fold, const typename F::T& r, int L,
@@ -582,7 +590,7 @@ ZKL_D void accumulate_round(const TablePtrs<F, MAXK>& tabs, int k, const Terms<F
   using R = Red<F>;
   using W = typename R::W;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (L > 0) {
+  if (!EV::kGeneric && L > 0) {
     // lane mode: groups of L lanes, one pair per group per pass
     const uint64_t ngroups = nthreads / (unsigned)L;
     const int q = lane & (L - 1), gb = lane & ~(L - 1);
@@ -598,6 +606,7 @@ ZKL_D void accumulate_round(const TablePtrs<F, MAXK>& tabs, int k, const Terms<F
     for (int off = 16; off >= L; off >>= 1) w = R::add(w, R::shfl_down(w, off));
     if (lane < EV::NOUT) wsum[warp][lane] = w;  // lane q < L holds output q
   } else {
+    (void)L;
     T acc[EV::NA];
 #pragma unroll
     for (int q = 0; q < EV::NA; q++) acc[q] = F::zero();
@@ -847,7 +856,8 @@ __global__ void __launch_bounds__(kClusterThreads)
     const bool tr0 = trace && rank == 0 && threadIdx.x == 0;
     if (tr0) trace[j * 8 + 0] = globaltimer();
     const uint64_t half = 1ull << (num_vars - 1 - j);
-    accumulate_round<F, MAXK, EV>(tabs, k, tm, half, fold, r, L, gtid, nthreads, wsum);
+    const int Lr = (L > 0 && half * (uint64_t)L <= nthreads) ? L : 0;
+    accumulate_round<F, MAXK, EV>(tabs, k, tm, half, fold, r, Lr, gtid, nthreads, wsum);
     if (tr0) trace[j * 8 + 1] = globaltimer();
     __syncthreads();
     if (warp == 0) {
