@@ -232,12 +232,46 @@ static int pair_combine_y(typename F::T* d, const IX* x, const void* y, int ty, 
   return kOk;
 }
 
+// int16 x int16 columns: two 2^16-entry lookup tables (lift(v) and
+// alpha * lift(v) for every int16 v, 2 MB each, L2-resident), so each secret
+// entry costs two L2 loads and one field add instead of three Montgomery
+// products.
+template <class F>
+__global__ void k_pair_luts(typename F::T* lx, typename F::T* ly, typename F::T alpha) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 65536) {
+    const typename F::T v = F::from_i64((int64_t)i - 32768);
+    lx[i] = v;
+    ly[i] = F::mul(alpha, v);
+  }
+}
+template <class F>
+__global__ void k_pair_combine_lut(typename F::T* dst, const int16_t* x, const int16_t* y,
+                                   uint64_t n, const typename F::T* lx, const typename F::T* ly) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = F::add(lx[(int)x[i] + 32768], ly[(int)y[i] + 32768]);
+}
+
 template <class F>
 int op_pair_combine(void* dst, const void* x, int tx, const void* y, int ty, uint64_t n,
                     typename F::T alpha, cudaStream_t s) {
   if (!n) return kOk;
   using T = typename F::T;
   T* d = (T*)dst;
+  if (tx == 1 && ty == 1 && n >= (1u << 18)) {
+    void* ws;
+    int rc = scratch_reserve(2 * 65536 * sizeof(T), &ws, s);
+    if (rc) return rc;
+    T* lx = (T*)ws;
+    T* ly = lx + 65536;
+    k_pair_luts<F><<<256, 256, 0, s>>>(lx, ly, alpha);
+    ZKL_LAUNCH_CHECK();
+    k_pair_combine_lut<F><<<grid_for(n, 256), 256, 0, s>>>(d, (const int16_t*)x,
+                                                           (const int16_t*)y, n, lx, ly);
+    ZKL_LAUNCH_CHECK();
+    return kOk;
+  }
   switch (tx) {
     case 1: return pair_combine_y<F, int16_t>(d, (const int16_t*)x, y, ty, n, alpha, s);
     case 2: return pair_combine_y<F, int32_t>(d, (const int32_t*)x, y, ty, n, alpha, s);

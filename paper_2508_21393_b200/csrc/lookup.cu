@@ -45,20 +45,31 @@ __global__ void k_ht_insert(const typename F::T* table, uint32_t n, uint32_t* sl
   }
 }
 
+// One probe per secret entry; equal hits inside a warp are merged with
+// __match_any_sync so each distinct table index takes ONE atomicAdd per warp
+// (skewed inputs -- e.g. the zero padding of a lookup, or activations
+// concentrated near 0 -- would otherwise serialise on a few counters).
 template <class F>
 __global__ void k_ht_count(const typename F::T* secret, uint64_t d, const typename F::T* table,
                            const uint32_t* slots, uint32_t mask, uint32_t* counts,
                            unsigned long long* first_miss) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < d;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    typename F::T v = secret[i];
-    uint32_t h = hash_elem(v) & mask;
-    while (true) {
-      uint32_t e = slots[h];
-      if (e == kEmpty) { atomicMin(first_miss, (unsigned long long)i); break; }
-      if (F::eq(table[e], v)) { atomicAdd(&counts[e], 1u); break; }
-      h = (h + 1) & mask;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < d; base += stride) {
+    const uint64_t i = base + threadIdx.x;
+    uint32_t hit = kEmpty;
+    if (i < d) {
+      const typename F::T v = ld_stream(secret + i);
+      uint32_t h = hash_elem(v) & mask;
+      while (true) {
+        const uint32_t e = __ldg(slots + h);
+        if (e == kEmpty) { atomicMin(first_miss, (unsigned long long)i); break; }
+        if (F::eq(table[e], v)) { hit = e; break; }
+        h = (h + 1) & mask;
+      }
     }
+    const unsigned peers = __match_any_sync(kFull, hit);
+    const int leader = __ffs(peers) - 1;
+    if (hit != kEmpty && (threadIdx.x & 31) == leader) atomicAdd(&counts[hit], __popc(peers));
   }
 }
 

@@ -394,6 +394,39 @@ def test_pair_lookup_golden_device():
         assert t.state.hex() == c["state_end"]
 
 
+@pytest.mark.parametrize("field", ["big", "test"])
+@pytest.mark.parametrize("n", [1000, (1 << 18) + 3])
+def test_pair_combine_vs_python(field, n):
+    """x + alpha*y over signed int16 columns (gadgets.py:659-666): the
+    lookup-table path (n >= 2^18) and the direct path, incl. -32768/32767."""
+    p = FIELDS[field]
+    spec = D.spec_for(p)
+    g = inputs.rng(n)
+    x = g.integers(-32768, 32768, size=n).astype(np.int16)
+    y = g.integers(-32768, 32768, size=n).astype(np.int16)
+    x[:2] = (-32768, 32767)
+    y[:2] = (32767, -32768)
+    alpha = (p - 12345) * 3 % p
+    dv = D.pair_combine(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), alpha, spec)
+    m = min(n, 4096)
+    got = D.download(dv.buf, spec, m)
+    want = [(int(a) + alpha * int(b)) % p for a, b in zip(x[:m], y[:m])]
+    assert got == want
+    tail = D.download(dv.buf, spec, n)[-100:]
+    assert tail == [(int(a) + alpha * int(b)) % p for a, b in zip(x[-100:], y[-100:])]
+
+
+def test_multiplicities_skewed_warp_aggregation():
+    """Heavily repeated secrets (the zero padding of a lookup) through the
+    warp-aggregated histogram."""
+    p = P_TEST
+    table = list(range(1000, 1000 + 4096))
+    secret = [1000] * 5000 + [1000 + (i * 7) % 4096 for i in range(3000)] + [5095] * 192
+    tab = zb.LookupTable(tuple(table), None)
+    got = zb.compute_multiplicities(secret, tab, p)
+    assert got == logup.multiplicities(secret, table)
+
+
 def test_multiplicities_golden():
     for c in load_golden("lookup.json")["multiplicities"]:
         table = zb.LookupTable(tuple(c["table"]), None)
