@@ -395,68 +395,6 @@ ZKL_D fr_t limb_reduce(const LimbAcc<CH>& a) {
   return Fr255::add(lo, hi);
 }
 
-// K = OFF * sum_i x[i] mod p (storage form) over the whole vector: one block,
-// wide 9-word sums, warp shuffles, one reduction mod p.
-template <int CH>
-__global__ void __launch_bounds__(1024) k_offset_total(const fr_t* x, uint64_t n, fr_t offr,
-                                                      fr_t* K) {
-  uint32_t acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  for (uint64_t base = 0; base < n; base += 4 * (uint64_t)blockDim.x) {
-    fr_t v[4];
-#pragma unroll
-    for (int u = 0; u < 4; u++) {  // four independent loads in flight
-      const uint64_t i = base + u * (uint64_t)blockDim.x + threadIdx.x;
-      v[u] = i < n ? x[i] : Fr255::zero();
-    }
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-      uint64_t c = 0;
-#pragma unroll
-      for (int l = 0; l < 8; l++) {
-        c += (uint64_t)acc[l] + v[u].v[l];
-        acc[l] = (uint32_t)c;
-        c >>= 32;
-      }
-      acc[8] += (uint32_t)c;
-    }
-  }
-  auto wadd = [](uint32_t (&a)[9], const uint32_t (&b)[9]) {
-    uint64_t c = 0;
-#pragma unroll
-    for (int l = 0; l < 9; l++) {
-      c += (uint64_t)a[l] + b[l];
-      a[l] = (uint32_t)c;
-      c >>= 32;
-    }
-  };
-#pragma unroll
-  for (int off = 16; off; off >>= 1) {
-    uint32_t o[9];
-#pragma unroll
-    for (int l = 0; l < 9; l++) o[l] = __shfl_down_sync(kFull, acc[l], off);
-    wadd(acc, o);
-  }
-  __shared__ uint32_t red[32][9];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) {
-#pragma unroll
-    for (int l = 0; l < 9; l++) red[warp][l] = acc[l];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t t[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++) wadd(t, red[w]);
-    fr_t lo_, hi_ = Fr255::zero();
-#pragma unroll
-    for (int l = 0; l < 8; l++) lo_.v[l] = t[l];
-    hi_.v[0] = t[8];
-    lo_ = Fr255::reduce_once(Fr255::reduce_once(lo_));
-    const fr_t sum = Fr255::add(lo_, Fr255::mul(hi_, Fr255::r2()));
-    // OFF * sum = mont_mul(sum, OFF R mod p)  (offr: OFF in storage form)
-    *K = Fr255::mul(sum, offr);
-  }
-}
-
 // raw accumulator words of one partial: int16 8 x u64, int64 18 x u64
 template <int CH>
 struct AccIO {
@@ -535,6 +473,7 @@ __global__ void __launch_bounds__(256)
   const int n = (int)(c1 - c0);
   for (int i = threadIdx.x; i < n; i += blockDim.x) xs[i] = x[c0 + i];
   __syncthreads();
+  if (blockIdx.x == 0) chunk_sum_atomic(x, c0, n, part + rows * IO::NW);
   const uint64_t r0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * R;
   if (r0 >= rows) return;
   LimbAcc<CH> acc[R];
@@ -597,6 +536,7 @@ __global__ void __launch_bounds__(256)
   const int n = (int)(r1 - r0);
   for (int i = threadIdx.x; i < n; i += blockDim.x) xs[i] = x[r0 + i];
   __syncthreads();
+  if (blockIdx.x == 0) chunk_sum_atomic(x, r0, n, part + cols * IO::NW);
   const uint64_t c = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * V;
   if (c >= cols) return;
   LimbAcc<CH> acc[V];
@@ -650,18 +590,125 @@ __global__ void __launch_bounds__(256)
   for (int v = 0; v < V; v++) IO::atomic_add(part + (c + v) * IO::NW, acc[v]);
 }
 
+// sum_{i<n} x[c0 + i] as a wide integer, added limb by limb into sumx[0..8]
+// (u64, red.add) by warp 0 of one block per chunk: the offset-binary
+// correction OFF * sum(x) is then formed by the finish kernel, no extra pass.
+ZKL_D void chunk_sum_atomic(const fr_t* x, uint64_t c0, int n, uint64_t* sumx) {
+  if ((threadIdx.x >> 5) != 0) return;
+  const int lane = threadIdx.x & 31;
+  uint64_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int i = lane; i < n; i += 32) {
+    const fr_t v = x[c0 + i];
+#pragma unroll
+    for (int l = 0; l < 8; l++) acc[l] += v.v[l];  // <= 2^16 terms < 2^48
+  }
+#pragma unroll
+  for (int l = 0; l < 8; l++) {
+#pragma unroll
+    for (int off = 16; off; off >>= 1) acc[l] += __shfl_xor_sync(kFull, acc[l], off);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int l = 0; l < 8; l++) atomicAdd((unsigned long long*)sumx + l, (unsigned long long)acc[l]);
+  }
+}
+
+// Row products with lanes along COLUMNS (coalesced 256-byte row segments per
+// warp), R rows per warp sharing each x load, x staged limb-major (SoA) so
+// every lane's 16-byte shared load is conflict-free.  Per step a lane takes 4
+// consecutive columns of R rows: 4R int16 entries, 32R mad.wide.  The lanes'
+// raw u64 accumulators are summed with warp shuffles; lane 0 adds them to the
+// row's record (red.add.u64: exact, order-free across column chunks).
+template <int R>
+__global__ void __launch_bounds__(256)
+    k_mvw_rows(const int16_t* M, uint64_t rows, uint64_t cols, const fr_t* x, uint64_t cch,
+               uint64_t* acc_out) {
+  extern __shared__ __align__(16) uint32_t xsm[];  // 8 limbs x cch
+  const uint64_t c0 = blockIdx.y * cch;
+  const int n = (int)((c0 + cch < cols ? c0 + cch : cols) - c0);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const fr_t v = x[c0 + i];
+#pragma unroll
+    for (int l = 0; l < 8; l++) xsm[l * cch + i] = v.v[l];
+  }
+  __syncthreads();
+  if (blockIdx.x == 0) chunk_sum_atomic(x, c0, n, acc_out + rows * 8);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t r0 = (blockIdx.x * (uint64_t)(blockDim.x >> 5) + warp) * R;
+  if (r0 >= rows) return;
+  LimbAcc<1> acc[R];
+#pragma unroll
+  for (int q = 0; q < R; q++) acc[q].zero();
+  const int16_t* base = M + r0 * cols + c0;
+  auto load = [&](uint2 (&dst)[R], int c) {
+#pragma unroll
+    for (int q = 0; q < R; q++)
+      dst[q] = (r0 + q < rows && c < n)
+                   ? __ldcs(reinterpret_cast<const uint2*>(base + q * cols + c))
+                   : make_uint2(0, 0);
+  };
+  uint2 nxt[R];
+  load(nxt, lane * 4);
+  for (int c = lane * 4; c < n; c += 128) {
+    uint2 mv[R];
+#pragma unroll
+    for (int q = 0; q < R; q++) mv[q] = nxt[q];
+    load(nxt, c + 128);  // next step's entries in flight while this one multiplies
+    uint4 xv[8];
+#pragma unroll
+    for (int l = 0; l < 8; l++) xv[l] = *reinterpret_cast<const uint4*>(xsm + l * cch + c);
+#pragma unroll
+    for (int v = 0; v < 4; v++) {
+#pragma unroll
+      for (int q = 0; q < R; q++) {
+        const uint32_t word = v < 2 ? mv[q].x : mv[q].y;
+        const int16_t sv = (int16_t)(v & 1 ? word >> 16 : word & 0xffffu);
+        const uint32_t u = (uint32_t)((int32_t)sv + 32768);
+#pragma unroll
+        for (int l = 0; l < 8; l++) {
+          const uint32_t xl = v == 0 ? xv[l].x : v == 1 ? xv[l].y : v == 2 ? xv[l].z : xv[l].w;
+          acc[q].e[l] = madw(u, xl, acc[q].e[l]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < R; q++) {
+#pragma unroll
+    for (int l = 0; l < 8; l++) {
+      uint64_t t = acc[q].e[l];
+#pragma unroll
+      for (int off = 16; off; off >>= 1) t += __shfl_xor_sync(kFull, t, off);
+      acc[q].e[l] = t;
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < R; q++)
+      if (r0 + q < rows) AccIO<1>::atomic_add(acc_out + (r0 + q) * 8, acc[q]);
+  }
+}
+
 // y[i] = reduce(acc[i]) - K; one thread per output (acc: atomically summed
 // raw words of every chunk -- exact integer sums, order-independent)
 template <int CH>
 __global__ void __launch_bounds__(256)
-    k_mvf_finish(const uint64_t* part, uint64_t nchunks, uint64_t n, const fr_t* K, fr_t* y) {
+    k_mvf_finish(const uint64_t* part, uint64_t n, const uint64_t* sumx, fr_t offr, fr_t* y) {
   using IO = AccIO<CH>;
+  __shared__ fr_t s_k;
+  if (threadIdx.x == 0) {  // K = OFF * sum(x) mod p (sumx: 8 u64 limb sums)
+    LimbAcc<1> sa;
+#pragma unroll
+    for (int l = 0; l < 8; l++) sa.e[l] = sumx[l];
+    s_k = Fr255::mul(limb_reduce<1>(sa), offr);
+  }
+  __syncthreads();
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   LimbAcc<CH> acc;
   acc.zero();
   IO::add(acc, part + i * IO::NW);
-  y[i] = Fr255::sub(limb_reduce<CH>(acc), *K);
+  y[i] = Fr255::sub(limb_reduce<CH>(acc), s_k);
 }
 
 // returns kErrUnsupported when the shape does not suit the fast kernels
@@ -683,7 +730,34 @@ static int matvec_fast(const MT* M, uint64_t rows, uint64_t cols, int transpose,
   uint64_t nchunks, nout;
   void* ws;
   int rc;
-  if (!transpose) {
+  if (!transpose && CH == 1) {
+    // warp-per-row-group kernel (lanes along columns)
+    constexpr int RW = 4;
+    if (cols % 128) return kErrUnsupported;
+    const uint64_t rblocks = (rows + 8 * RW - 1) / (8 * RW);
+    uint64_t cs = (2 * (uint64_t)kSMs + rblocks - 1) / rblocks;  // >= 2 blocks per SM
+    const uint64_t max_cs = cols / 512;  // >= 512 columns per chunk
+    if (cs > max_cs) cs = max_cs;
+    if (cs < 1) cs = 1;
+    uint64_t cch = (cols + cs - 1) / cs;
+    cch = (cch + 127) / 128 * 128;
+    if (cch * 32 > 160 * 1024) return kErrUnsupported;
+    nchunks = (cols + cch - 1) / cch;
+    nout = rows;
+    rc = scratch_reserve(rows * NW * 8 + 128, &ws, s);
+    if (rc) return rc;
+    ZKL_CUDA(cudaMemsetAsync(ws, 0, rows * NW * 8 + 64, s));
+    const size_t smem = cch * 32;
+    static bool attr = false;
+    if (!attr) {
+      ZKL_CUDA(cudaFuncSetAttribute(k_mvw_rows<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    160 * 1024));
+      attr = true;
+    }
+    dim3 g((unsigned)rblocks, (unsigned)nchunks);
+    k_mvw_rows<RW><<<g, 256, smem, s>>>((const int16_t*)M, rows, cols, x, cch, (uint64_t*)ws);
+    ZKL_LAUNCH_CHECK();
+  } else if (!transpose) {
     constexpr int R = 1;
     if (cols % 32) return kErrUnsupported;
     const uint64_t threads = (rows + R - 1) / R;
@@ -696,9 +770,9 @@ static int matvec_fast(const MT* M, uint64_t rows, uint64_t cols, int transpose,
     if (cch * sizeof(fr_t) > 96 * 1024) return kErrUnsupported;
     nchunks = (cols + cch - 1) / cch;
     nout = rows;
-    rc = scratch_reserve(rows * NW * 8 + 64, &ws, s);
+    rc = scratch_reserve(rows * NW * 8 + 128, &ws, s);
     if (rc) return rc;
-    ZKL_CUDA(cudaMemsetAsync(ws, 0, rows * NW * 8, s));
+    ZKL_CUDA(cudaMemsetAsync(ws, 0, rows * NW * 8 + 64, s));
     dim3 g((unsigned)((threads + 255) / 256), (unsigned)nchunks);
     const size_t smem = cch * sizeof(fr_t);
     if (smem > 48 * 1024)
@@ -719,9 +793,9 @@ static int matvec_fast(const MT* M, uint64_t rows, uint64_t cols, int transpose,
     nchunks = (rows + rch - 1) / rch;
     if (nchunks > 65535) return kErrUnsupported;
     nout = cols;
-    rc = scratch_reserve(cols * NW * 8 + 64, &ws, s);
+    rc = scratch_reserve(cols * NW * 8 + 128, &ws, s);
     if (rc) return rc;
-    ZKL_CUDA(cudaMemsetAsync(ws, 0, cols * NW * 8, s));
+    ZKL_CUDA(cudaMemsetAsync(ws, 0, cols * NW * 8 + 64, s));
     dim3 g((unsigned)((threads + 255) / 256), (unsigned)nchunks);
     const size_t smem = rch * sizeof(fr_t);
     if (smem > 48 * 1024)
@@ -730,19 +804,16 @@ static int matvec_fast(const MT* M, uint64_t rows, uint64_t cols, int transpose,
     k_mvf_cols<MT, V><<<g, 256, smem, s>>>(M, rows, cols, x, rch, (uint64_t*)ws);
     ZKL_LAUNCH_CHECK();
   }
-  // K = OFF * sum(x) over the reduction dimension (offset-binary correction)
-  fr_t* K = (fr_t*)((uint64_t*)ws + nout * NW);
-  // OFF (2^15 or 2^63) in Montgomery form, computed once on the host
+  // y = reduce(acc) - OFF * sum(x); OFF (2^15 or 2^63) in Montgomery form
   static fr_t offr = [] {
     fr_t v = Fr255::zero();
     if (CH == 1) v.v[0] = 1u << 15;
     else v.v[1] = 1u << 31;
     return Fr255::to_mont(v);
   }();
-  k_offset_total<CH><<<1, 1024, 0, s>>>(x, klen, offr, K);
-  ZKL_LAUNCH_CHECK();
-  k_mvf_finish<CH><<<(unsigned)((nout + 255) / 256), 256, 0, s>>>((const uint64_t*)ws, nchunks,
-                                                                   nout, K, y);
+  const uint64_t* sumx = (const uint64_t*)ws + nout * NW;
+  k_mvf_finish<CH><<<(unsigned)((nout + 255) / 256), 256, 0, s>>>((const uint64_t*)ws, nout, sumx,
+                                                                   offr, y);
   ZKL_LAUNCH_CHECK();
   return kOk;
 }
@@ -808,11 +879,11 @@ static int matvec_impl(const void* Mv, uint64_t rows, uint64_t cols, int transpo
   return kOk;
 }
 
-// The mad.wide kernels are opt-in (ZKL_MATVEC_FAST=1) until they beat the
-// wide-accumulator kernels on B200 (profiles/r01: both at ~15% of the IMAD
-// peak, latency/occupancy-bound); both are exercised by the parity tests.
+// mad.wide kernels: default for int16 matrices (faster on B200); int64 stays
+// on the wide-accumulator kernels unless ZKL_MATVEC_FAST64 is set (the
+// 4-chunk mad.wide form measured slower).  ZKL_MATVEC_SLOW=1 disables them.
 static bool fast_enabled() {
-  static const bool on = getenv("ZKL_MATVEC_FAST") != nullptr;
+  static const bool on = getenv("ZKL_MATVEC_SLOW") == nullptr;
   return on;
 }
 
@@ -834,7 +905,7 @@ int op_matvec(int mtype, const void* M, uint64_t rows, uint64_t cols, int transp
     case 2: return matvec_impl<F, int32_t>(M, rows, cols, transpose, x, y, s);
     case 3:
       if constexpr (F::kId == 0) {
-        if (fast_enabled()) {
+        if (fast_enabled() && getenv("ZKL_MATVEC_FAST64")) {
           int rc = matvec_fast<int64_t>((const int64_t*)M, rows, cols, transpose,
                                         (const fr_t*)x, (fr_t*)y, s);
           if (rc != kErrUnsupported) return rc;

@@ -339,17 +339,19 @@ def test_stepwise_mode_matches_oracle():
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
 
 
-def test_matvec_fast_kernels_vs_numpy():
-    """The opt-in mad.wide matvec kernels (ZKL_MATVEC_FAST=1, read once per
-    process) against exact numpy products, in a child process."""
+@pytest.mark.parametrize("env", [{"ZKL_MATVEC_SLOW": "1"}, {"ZKL_MATVEC_FAST64": "1"}])
+def test_matvec_alternate_kernels_vs_numpy(env):
+    """The non-default matvec kernels (wide-accumulator everywhere, or the
+    mad.wide form for int64 too; the switches are read once per process)
+    against exact numpy products, in a child process."""
     code = (
         "import sys; sys.path[:0] = ['.', 'tests', 'tests/golden']\n"
         "import test_gpu_parity as T\n"
         "for mt in ('i16', 'i64'):\n"
-        "    for shape in [(64, 256), (1024, 256), (33, 4096), (256, 1024)]:\n"
+        "    for shape in [(64, 256), (1024, 256), (33, 4096), (256, 1024), (3, 70)]:\n"
         "        T.test_matvec_extremes_vs_numpy('big', mt, shape)\n"
         "print('ok')\n")
-    r = _run_isolated(code, ZKL_MATVEC_FAST="1")
+    r = _run_isolated(code, **env)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
 
 
