@@ -168,6 +168,19 @@ int zkl_matmul_prove(int field, int a_type, const void* A, int b_type, const voi
                      const void* C, int d0, int d1, int d2, uint8_t* state_inout,
                      uint8_t* rounds_out, uint8_t* point_out, uint8_t* finals_out, void* stream);
 
+/* The logUp Eq.-7 sumcheck (lookup.py:188-219) for a secret larger than the
+ * table (d = 2^num_vars > n = 2^tile_log): runs the first `rounds` =
+ * num_vars - tile_log rounds without materialising the replicated table side
+ * (B, T+beta, M read at index mod n, the indicator == 1), appends exactly the
+ * reference's transcript bytes, then folds E, A, S+beta by the last challenge.
+ * tables: E, A, S+beta (2^num_vars, consumed) and B, T+beta, M (2^tile_log);
+ * coeffs: the five term coefficients (lookup.py:116-126), canonical.  The
+ * remaining tile_log rounds run through zkl_sumcheck_prove on 7 tables of
+ * 2^tile_log (indicator = ones).  ZKL_ERR_UNSUPPORTED in stepwise mode. */
+int zkl_logup_tiled_rounds(int field, void* const* tables, int tile_log, int num_vars, int rounds,
+                           const uint8_t* coeffs_canon, uint8_t* state_inout, uint8_t* rounds_out,
+                           uint8_t* point_out, void* stream);
+
 /* CUDA-event profiler for benchmarks: when enabled, the library brackets
  * each kernel family on its launching stream.  kind 0: matrix-vector
  * products (bytes = matrix + vectors), 1: sumcheck phases (persistent round

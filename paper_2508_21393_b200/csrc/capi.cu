@@ -239,6 +239,24 @@ int zkl_matmul_prove(int field, int a_type, const void* A, int b_type, const voi
   D(field, op_matmul_prove<F>(a_type, A, b_type, B, c_type, C, d0, d1, d2, state_inout,
                               rounds_out, point_out, finals_out, (cudaStream_t)stream));
 }
+int zkl_logup_tiled_rounds(int field, void* const* tables, int tile_log, int num_vars, int rounds,
+                           const uint8_t* coeffs_canon, uint8_t* state_inout, uint8_t* rounds_out,
+                           uint8_t* point_out, void* stream) {
+  if (field == ZKL_FIELD_BLS12_381_FR) {
+    Fr255::T c[5];
+    for (int t = 0; t < 5; t++) c[t] = load_canon<Fr255>(coeffs_canon + 32 * t);
+    return op_logup_tiled<Fr255>(tables, tile_log, num_vars, rounds, c, state_inout, rounds_out,
+                                 point_out, (cudaStream_t)stream);
+  }
+  if (field == ZKL_FIELD_M61) {
+    M61::T c[5];
+    for (int t = 0; t < 5; t++) c[t] = load_canon<M61>(coeffs_canon + 8 * t);
+    return op_logup_tiled<M61>(tables, tile_log, num_vars, rounds, c, state_inout, rounds_out,
+                               point_out, (cudaStream_t)stream);
+  }
+  set_error("unknown field id %d", field);
+  return kErrArg;
+}
 int zkl_prof_enable(int on) {
   zkl::prof_enable(on != 0);
   return kOk;

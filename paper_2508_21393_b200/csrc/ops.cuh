@@ -43,6 +43,7 @@ struct Terms {
   int nf[kMaxTerms];
   int fi[kMaxTerms][3];
   typename F::T coef[kMaxTerms];
+  int tile_log;  // LOGUP_TILED: tables 3..5 have 2^tile_log entries, read at i mod 2^tile_log
 };
 template <class F>
 struct Post {
@@ -78,6 +79,12 @@ int op_multiplicities(const void* secret, uint64_t d, const void* table, uint64_
 template <class F>
 int op_matvec(int mtype, const void* M, uint64_t rows, uint64_t cols, int transpose,
               const void* x, void* y, cudaStream_t s);
+
+// replicated logUp claim, first rounds with the tiled evaluator (persistent.cu)
+template <class F>
+int op_logup_tiled(void* const* tables, int tile_log, int num_vars, int rounds,
+                   const typename F::T* coefs, uint8_t* state, uint8_t* rounds_out,
+                   uint8_t* point_out, cudaStream_t s);
 
 // native zkMat driver (zkmat.cu): gadgets.py:241-251, factored
 template <class F>

@@ -135,7 +135,7 @@ struct Red<M61> {
 // shuffles, and each lane computes one output product.  Critical path: one
 // fold product + one (PROD2, SUM2PROD2) or two (PROD3) evaluation products.
 inline int lanes_for(int shape, int k) {
-  if (shape == kGeneric) return 0;
+  if (shape == kGeneric || shape == kLogupTiled) return 0;
   const int nout = shape == kProd2 ? 3 : shape == kProd3 ? 4 : shape == kLogup ? 16 : 6;
   const int need = 2 * k > nout ? 2 * k : nout;  // fold lanes / output lanes
   return need <= 4 ? 4 : need <= 8 ? 8 : 16;
@@ -426,6 +426,96 @@ struct EvLogup {
   }
 };
 
+// logUp Eq.-7 claim in its replicated form (lookup.py:188-202, secret
+// larger than the table), for the rounds that bind the high log2(d/n)
+// variables: tables [E, A, S] are folded as usual, while the table side
+// [B, T, M] depends only on the low tile_log index bits -- lo == hi, folding
+// is the identity, so they are never materialised at 2^n, folded or
+// written -- and the indicator is identically 1.  Same 16 raw outputs as
+// EvLogup (the host finishing is shared); 17 products per pair instead of 34.
+template <class F, int MAXK>
+struct EvLogupTiled {
+  using T = typename F::T;
+  static constexpr bool kGeneric = false;
+  static constexpr bool kTiled = true;
+  static constexpr int NA = 16, NOUT = 16;
+  template <bool FOLD>
+  ZKL_D static void pair_tiled(const TablePtrs<F, MAXK>& tabs, uint64_t i, uint64_t half,
+                               const T& r, const Terms<F>& tm, T (&acc)[NA]) {
+    T lo[3], df[3];
+    if (FOLD) {
+      T a0[3], b0[3], da[3], db[3];
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        const T* t = tabs.t[j];
+        a0[j] = ld_cg(t + i);
+        b0[j] = ld_cg(t + i + half);
+        da[j] = F::sub(ld_cg(t + i + 2 * half), a0[j]);
+        db[j] = F::sub(ld_cg(t + i + 3 * half), b0[j]);
+      }
+      F::mul4r(r, da[0], db[0], da[1], db[1]);
+      F::mul2(r, da[2], r, db[2], da[2], db[2]);
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        T* t = tabs.t[j];
+        const T l = F::add(a0[j], da[j]), h = F::add(b0[j], db[j]);
+        t[i] = l;
+        t[i + half] = h;
+        lo[j] = l;
+        df[j] = F::sub(h, l);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        const T* t = tabs.t[j];
+        lo[j] = ld_cg(t + i);
+        df[j] = F::sub(ld_cg(t + i + half), lo[j]);
+      }
+    }
+    const uint64_t ti = i & ((1ull << tm.tile_log) - 1);
+    const T b = tabs.t[3][ti], tt = tabs.t[4][ti], m = tabs.t[5][ti];
+    const T e0 = lo[0], ed = df[0], a0 = lo[1], ad = df[1], s0 = lo[2], sd = df[2];
+    const T e1 = F::add(e0, ed), a1 = F::add(a0, ad), s1 = F::add(s0, sd);
+    T p[3], bt, mb;
+    F::mul4(a0, s0, a1, s1, ad, sd, b, tt, p[0], p[1], p[2], bt);
+    T as[4];
+    quad_evals<F>(p[0], p[1], p[2], as);
+    const T e2 = F::add(e1, ed), e3 = F::add(e2, ed);
+    T o[4], eb0, eb1;
+    F::mul4(e0, as[0], e1, as[1], e2, as[2], e3, as[3], o[0], o[1], o[2], o[3]);
+    F::mul3(e0, bt, e1, bt, m, b, eb0, eb1, mb);
+    const T ebd = F::sub(eb1, eb0);
+    const T eb2 = F::add(eb1, ebd), eb3 = F::add(eb2, ebd);
+#pragma unroll
+    for (int k = 0; k < 4; k++) acc[k] = F::add(acc[k], o[k]);
+    acc[4] = F::add(acc[4], e0);  // E I with I = 1: (e0, e1, ed * 0)
+    acc[5] = F::add(acc[5], e1);
+    acc[7] = F::add(acc[7], eb0);
+    acc[8] = F::add(acc[8], eb1);
+    acc[9] = F::add(acc[9], eb2);
+    acc[10] = F::add(acc[10], eb3);
+    acc[11] = F::add(acc[11], a0);
+    acc[12] = F::add(acc[12], ad);
+    acc[13] = F::add(acc[13], mb);  // M B constant across the pair: (mb, mb, 0)
+    acc[14] = F::add(acc[14], mb);
+  }
+  ZKL_D static void pair(T (&)[MAXK], const T (&)[MAXK], int, const Terms<F>&, T (&)[NA]) {}
+  ZKL_D static void finish(const T (&acc)[NA], T (&out)[NOUT]) {
+#pragma unroll
+    for (int q = 0; q < 16; q++) out[q] = acc[q];
+  }
+  ZKL_D static T lane(const T&, int, int, bool, const Terms<F>&) { return F::zero(); }
+};
+
+template <class EV>
+struct IsTiled {
+  template <class U>
+  static constexpr bool test(decltype(U::kTiled)*) { return U::kTiled; }
+  template <class U>
+  static constexpr bool test(...) { return false; }
+  static constexpr bool value = test<EV>(nullptr);
+};
+
 // Load the pair (i, i + half) of every table, folding first when FOLD:
 // cur = low value, df = high - low.  All 2k fold products go through the
 // 4-wide multiply (one product latency per 4 folds).
@@ -610,13 +700,20 @@ ZKL_D void accumulate_round(const TablePtrs<F, MAXK>& tabs, int k, const Terms<F
     T acc[EV::NA];
 #pragma unroll
     for (int q = 0; q < EV::NA; q++) acc[q] = F::zero();
-    for (uint64_t i = gtid; i < half; i += nthreads) {
-      T cur[MAXK], df[MAXK];
-      if (fold)
-        load_fold_pair<F, MAXK, true>(tabs, k, i, half, r, cur, df);
-      else
-        load_fold_pair<F, MAXK, false>(tabs, k, i, half, r, cur, df);
-      EV::pair(cur, df, k, tm, acc);
+    if constexpr (IsTiled<EV>::value) {
+      for (uint64_t i = gtid; i < half; i += nthreads) {
+        if (fold) EV::template pair_tiled<true>(tabs, i, half, r, tm, acc);
+        else EV::template pair_tiled<false>(tabs, i, half, r, tm, acc);
+      }
+    } else {
+      for (uint64_t i = gtid; i < half; i += nthreads) {
+        T cur[MAXK], df[MAXK];
+        if (fold)
+          load_fold_pair<F, MAXK, true>(tabs, k, i, half, r, cur, df);
+        else
+          load_fold_pair<F, MAXK, false>(tabs, k, i, half, r, cur, df);
+        EV::pair(cur, df, k, tm, acc);
+      }
     }
     T out[EV::NOUT];
     EV::finish(acc, out);
@@ -1063,6 +1160,9 @@ static int dispatch(const LaunchReq<F>& q, Plan* pl, int* nout, int launch) {
     case kLogup:
       if constexpr (MAXK >= 8) ZKL_SHAPE(EvLogup)
       else ZKL_SHAPE(EvGeneric)
+    case kLogupTiled:
+      if constexpr (MAXK >= 8) ZKL_SHAPE(EvLogupTiled)
+      else ZKL_SHAPE(EvGeneric)
     default: ZKL_SHAPE(EvGeneric)
   }
 #undef ZKL_SHAPE
@@ -1247,8 +1347,13 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
   Mailbox* mb_dev;
   int rc = mailbox_for_current_device(&mb_host, &mb_dev);
   if (rc) return rc;
-  int shape = detect_shape<F>(tm);
-  if (shape == kLogup && k <= 4) shape = kGeneric;  // the LOGUP evaluator is built for MAXK 8
+  int shape = a.forced_shape >= 0 ? a.forced_shape : detect_shape<F>(tm);
+  if ((shape == kLogup || shape == kLogupTiled) && k <= 4) shape = kGeneric;  // built for MAXK 8
+  const int nrun = a.rounds_limit > 0 ? a.rounds_limit : n;
+  if (nrun < n && finals_out) {
+    set_error("sumcheck phase: a partial phase has no finals");
+    return kErrArg;
+  }
   LaunchReq<F> rq;
   rq.shape = shape;
   rq.k = k;
@@ -1259,6 +1364,7 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
   Plan pl;
   int nout = 4;
   run_dispatch<F>(rq, &pl, &nout, 0);
+  if (nrun < n) pl.j_switch = nrun;  // grid kernel only, stops after round nrun-1
   void* ws;
   rc = scratch_reserve((size_t)pl.grid * kMbMaxOut * sizeof(W), &ws, s);
   if (rc) return rc;
@@ -1309,9 +1415,13 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
   rq.trace = trace;
   // profiler: algorithmic bytes of the whole claim, sum over rounds of
   // k 2^(n-j) elements read and (from round 1) k 2^(n-j-1) written by the fold
-  const int ph = prof_open(kProfPhase, 3.0 * k * (double)(1ull << n) * F::kBytes, (double)n, s);
+  // (the tiled logUp phase moves only its 3 full-size tables; the 2^tile_log
+  // table side stays in L2)
+  const int k_full = shape == kLogupTiled ? 3 : k;
+  const int ph = prof_open(kProfPhase, 3.0 * k_full * (double)(1ull << n) * F::kBytes,
+                           (double)nrun, s);
   rc = run_dispatch<F>(rq, &pl, &nout, pl.j_switch > 0 ? 1 : 2);
-  if (pl.j_switch == 0 || pl.j_switch >= n) prof_close(ph, s);  // else: at the handoff
+  if (pl.j_switch == 0 || pl.j_switch >= n || nrun < n) prof_close(ph, s);  // else: at handoff
   if (rc) return rc;
   a.seq0 = seq0;
   // host-side finishing constants (canonical multipliers: mul(raw_storage,
@@ -1323,7 +1433,7 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
   uint32_t words[kMbEvalWords];
   std::vector<double> h_first;
   if (tracing) h_first.resize(n);
-  for (int j = 0; j < n; j++) {
+  for (int j = 0; j < nrun; j++) {
     if (tracing) {  // first tagged word of this round visible
       while ((uint32_t)(mb_host->ev[0] >> 32) != seq0 + j + 1 && !mb_host->status) {
       }
@@ -1351,7 +1461,7 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
       if (shape == kGeneric) {
         Kc[0] = host::canon_of<F>(pm);
       } else {
-        const int nk = shape == kLogup ? 5 : shape == kSum2Prod2 ? 2 : 1;
+        const int nk = (shape == kLogup || shape == kLogupTiled) ? 5 : shape == kSum2Prod2 ? 2 : 1;
         for (int t = 0; t < nk; t++) Kc[t] = host::canon_of<F>(H::mul(pm, a.tm.coef[t]));
       }
     }
@@ -1366,7 +1476,7 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
       host_quad<F>(raw[0], raw[1], raw[2], e1);
       host_quad<F>(raw[3], raw[4], raw[5], e2);
       for (int x = 0; x < 4; x++) ev[x] = H::add(H::mul(e1[x], Kc[0]), H::mul(e2[x], Kc[1]));
-    } else if (shape == kLogup) {
+    } else if (shape == kLogup || shape == kLogupTiled) {
       T ei[4], mb[4];
       host_quad<F>(raw[4], raw[5], raw[6], ei);
       host_quad<F>(raw[13], raw[14], raw[15], mb);
@@ -1401,7 +1511,7 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
     for (int w = 0; w < NC; w++) mb_host->ch[w] = tg | cw[w];
     std::atomic_thread_fence(std::memory_order_seq_cst);  // drain the store buffer now
     if (tracing) h_sent[j] = now_us();
-    if (pl.j_switch > 0 && j == pl.j_switch - 1 && pl.j_switch < n) {
+    if (pl.j_switch > 0 && j == pl.j_switch - 1 && pl.j_switch < n && nrun == n) {
       // handoff: the grid kernel has published its last round and exits
       rc = run_dispatch<F>(rq, &pl, &nout, 2);
       prof_close(ph, s);
@@ -1417,6 +1527,7 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
     if (rc) return rc;
   }
   if (tracing) {
+    const int n = nrun;  // rounds actually run
     std::vector<uint64_t> tv((size_t)n * 8);
     cudaMemcpyAsync(tv.data(), trace, tv.size() * 8, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
@@ -1495,7 +1606,59 @@ int op_sumcheck_prove(void* const* tables, int k, int num_vars, const Terms<F>& 
   return kOk;
 }
 
+// The replicated logUp claim's first `rounds` rounds (the high log2(d/n)
+// variables) with the tiled evaluator, then E, A, S folded by the last
+// challenge (the next phase runs the remaining rounds over 2^tile_log-entry
+// tables).  tables: [E, A, S+beta] (2^num_vars) and [B, T+beta, M]
+// (2^tile_log); coefs: the five Eq.-7 term coefficients (storage form).
+template <class F>
+int op_logup_tiled(void* const* tables, int tile_log, int num_vars, int rounds,
+                   const typename F::T* coefs, uint8_t* state, uint8_t* rounds_out,
+                   uint8_t* point_out, cudaStream_t s) {
+  using T = typename F::T;
+  if (no_persistent()) {
+    set_error("logup_tiled: needs the persistent engine (stepwise mode active)");
+    return kErrUnsupported;
+  }
+  if (rounds < 1 || tile_log < 1 || rounds + tile_log != num_vars) {
+    set_error("logup_tiled: bad rounds/tile sizes");
+    return kErrArg;
+  }
+  Terms<F> tm;
+  memset(&tm, 0, sizeof(tm));
+  tm.nterms = 5;
+  tm.degree = 3;
+  const int nf[5] = {3, 2, 3, 1, 2};
+  const int fi[5][3] = {{0, 1, 2}, {0, 6, 0}, {0, 3, 4}, {1, 0, 0}, {5, 3, 0}};
+  for (int t = 0; t < 5; t++) {
+    tm.nf[t] = nf[t];
+    for (int q = 0; q < 3; q++) tm.fi[t][q] = fi[t][q];
+    tm.coef[t] = coefs[t];
+  }
+  tm.tile_log = tile_log;
+  HostTranscript tr;
+  memcpy(tr.state, state, 64);
+  PhaseArgs<F> a;
+  a.tables = tables;
+  a.k = 6;
+  a.num_vars = num_vars;
+  a.tm = tm;
+  a.post_mul = host::For<F>::H::one();
+  a.rounds_limit = rounds;
+  a.forced_shape = kLogupTiled;
+  int rc = run_phase<F>(a, tr, rounds_out, point_out, nullptr, s);
+  if (rc) return rc;
+  const T r = host::from_canon<F>(point_out + (size_t)(rounds - 1) * F::kBytes);
+  const uint64_t half = 1ull << (num_vars - rounds);
+  for (int j = 0; j < 3; j++)
+    if ((rc = op_fold<F>(tables[j], tables[j], half, r, s))) return rc;
+  memcpy(state, tr.state, 64);
+  return kOk;
+}
+
 #define ZKL_INST_PERSIST(F)                                                                   \
+  template int op_logup_tiled<F>(void* const*, int, int, int, const F::T*, uint8_t*,          \
+                                 uint8_t*, uint8_t*, cudaStream_t); \
   template int detect_shape<F>(const Terms<F>&);                                              \
   template int run_phase<F>(PhaseArgs<F>&, HostTranscript&, uint8_t*, uint8_t*, F::T*,         \
                             cudaStream_t);                                                    \

@@ -9,7 +9,7 @@
 
 namespace zkl {
 
-enum Shape { kGeneric = 0, kProd2 = 1, kProd3 = 2, kSum2Prod2 = 3, kLogup = 4 };
+enum Shape { kGeneric = 0, kProd2 = 1, kProd3 = 2, kSum2Prod2 = 3, kLogup = 4, kLogupTiled = 5 };
 
 template <class F>
 int detect_shape(const Terms<F>& tm);
@@ -33,6 +33,12 @@ struct PhaseArgs {
   // for the recognised shapes; the generic shape needs them at launch)
   std::function<int(std::vector<T>&)> prepare;
   uint32_t seq0 = 0;  // set by run_phase: mailbox sequence base of the launch
+  // > 0: run only the first `rounds_limit` rounds (no finals; the caller folds
+  // by the last challenge and continues with another phase).  Required for
+  // the LOGUP_TILED shape, whose structure holds only while the bound
+  // variables are above the tiled tables' index bits.
+  int rounds_limit = 0;
+  int forced_shape = -1;
   // one-launch-per-round mode (profilers): finals are kept here
   bool stepwise = false;
   std::vector<T> fin_cache;

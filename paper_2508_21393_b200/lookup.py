@@ -6,6 +6,9 @@ on the device: beta + s and beta + t are inverted by one hierarchical
 Montgomery-trick pass each (whose zero detection IS the pole test of
 lookup.py:163-171), the seven lifted columns of lookup.py:188-202 are built
 by zkl_expand, and the degree-3 sumcheck runs on the fused round engine.
+When the secret is larger than the table the replicated table side is never
+materialised: the first log2(d/n) rounds run with a tiled evaluator
+(zkl_logup_tiled_rounds) and the rest over seven n-entry tables.
 compute_multiplicities (lookup.py:91-99) is a device hash-table histogram.
 """
 
@@ -18,7 +21,7 @@ from .field import batch_inverse_device, inverse
 from .gadgets import commit_backend
 from .mle import mle_evaluate_device
 from .sumcheck import TYPES as SC_TYPES
-from .sumcheck import Term, absorb_claim, run_rounds
+from .sumcheck import Term, absorb_claim, native_transcript, run_rounds
 
 MAX_BETA_RETRIES = 3
 
@@ -228,6 +231,22 @@ def prove_lookup(secret, multiplicities, table, key, tr, rng):
     u = tr.challenge_vector(b"lookup/u", num_vars)
     ratio = inverse(big // n, p)
 
+    terms = _terms(alpha, ratio, p)
+    claimed = alpha * alpha % p
+    tuples = [(t.coefficient, t.factors) for t in terms]
+
+    # secret larger than the table: the replicated table side (lookup.py:196-202)
+    # is never materialised -- tiled rounds first, then 7 tables of n entries
+    if d > n > 1 and TILED and native_transcript(tr, spec):
+        tiled = _tiled_sumcheck(spec, tr, d, n, s_buf, inv_s, t_buf, inv_t, m_buf, beta, u,
+                                terms, tuples, claimed, num_vars)
+        if tiled is not None:
+            rounds, point, finals = tiled
+            return _finish_lookup(spec, p, key, be, stub, tr, rng, secret, table, multiplicities,
+                                  entries, beta, retries, m_commitment, a_commitment, b_commitment,
+                                  m_blinding, m_rows, a_blinding, inv_s, inv_s_host, inv_t_host,
+                                  s_buf, num_vars, rounds, point, finals, d, n)
+
     # lifted columns (lookup.py:188-202)
     if d <= n:
         A = _expand(spec, n, inv_s, d, 0)
@@ -244,16 +263,72 @@ def prove_lookup(secret, multiplicities, table, key, tr, rng):
         Tb = _expand(spec, d, t_buf, n, 1, add=beta)
         Mt = _expand(spec, d, m_buf, n, 1)
     E = D.eq_table(u, spec)
-    terms = _terms(alpha, ratio, p)
-    claimed = alpha * alpha % p
     absorb_claim(tr, claimed, terms, 3, num_vars)
-    tuples = [(t.coefficient, t.factors) for t in terms]
     if num_vars:
         rounds, point, finals = run_rounds(spec, [E, A, Sb, ind, Bt, Tb, Mt], num_vars, tuples,
                                            3, tr)
     else:
         rounds, point = [], []
         finals = [D.read_scalar(x, spec) for x in (E, A, Sb, ind, Bt, Tb, Mt)]
+    return _finish_lookup(spec, p, key, be, stub, tr, rng, secret, table, multiplicities, entries,
+                          beta, retries, m_commitment, a_commitment, b_commitment, m_blinding,
+                          m_rows, a_blinding, inv_s, inv_s_host, inv_t_host, s_buf, num_vars,
+                          rounds, point, finals, d, n)
+
+
+TILED = True  # tests flip this to compare with the fully materialised claim
+
+
+def _tiled_sumcheck(spec, tr, d, n, s_buf, inv_s, t_buf, inv_t, m_buf, beta, u, terms, tuples,
+                    claimed, num_vars):
+    """zkl_logup_tiled_rounds for the high log2(d/n) variables, then the
+    remaining log2(n) rounds over 7 tables of n entries (indicator = ones).
+    Returns None (nothing consumed, transcript untouched) when the native
+    engine declines (stepwise mode under profilers)."""
+    tile_log = (n - 1).bit_length()
+    r1 = num_vars - tile_log
+    E = D.eq_table(u, spec)
+    # inv_s / inv_t are consumed in place: with d > n the openings use the
+    # sumcheck finals, and the commitment path downloaded them already
+    A = inv_s
+    Sb = _expand(spec, d, s_buf, d, 1, add=beta)
+    Bb = inv_t
+    Tb = _expand(spec, n, t_buf, n, 1, add=beta)
+    Mb = m_buf.clone()  # may be the caller's DeviceVector buffer
+    nb = spec.nbytes
+    before = bytes(tr.state)
+    absorb_claim(tr, claimed, terms, 3, num_vars)
+    state = ctypes.create_string_buffer(bytes(tr.state), 64)
+    rbuf = (ctypes.c_uint8 * (r1 * 4 * nb))()
+    pbuf = (ctypes.c_uint8 * (r1 * nb))()
+    ptrs = (ctypes.c_void_p * 6)(*[t.data_ptr() for t in (E, A, Sb, Bb, Tb, Mb)])
+    coeffs = D.scalars_bytes([t.coefficient for t in terms], spec)
+    rc = N.lib().zkl_logup_tiled_rounds(spec.fid, ptrs, tile_log, num_vars, r1, coeffs, state,
+                                        rbuf, pbuf, D.stream())
+    if rc == N.ZKL_ERR_UNSUPPORTED:
+        tr.state = before
+        log = getattr(tr, "log", None)
+        if log is not None:
+            del log[-(2 + 2 * len(terms)):]
+        return None
+    N.check(rc)
+    flat = D.decode(bytes(rbuf), spec, 4 * r1)
+    rounds = [tuple(flat[4 * j:4 * j + 4]) for j in range(r1)]
+    point = D.decode(bytes(pbuf), spec, r1)
+    tr.state = state.raw[:64]
+    log = getattr(tr, "log", None)
+    if log is not None:
+        log.extend((b"sumcheck/eval", (e.bit_length() + 7) // 8 or 1) for e in flat)
+    ind = _expand(spec, n, None, n, 0, add=1, pad=0)
+    r2, p2, finals = run_rounds(spec, [E[:n], A[:n], Sb[:n], ind, Bb, Tb, Mb], tile_log, tuples,
+                                3, tr)
+    return rounds + r2, point + p2, finals
+
+
+def _finish_lookup(spec, p, key, be, stub, tr, rng, secret, table, multiplicities, entries, beta,
+                   retries, m_commitment, a_commitment, b_commitment, m_blinding, m_rows,
+                   a_blinding, inv_s, inv_s_host, inv_t_host, s_buf, num_vars, rounds, point,
+                   finals, d, n):
     RP = SC_TYPES["RoundPolynomial"]
     sc_proof = SC_TYPES["SumcheckProof"]([RP(e) for e in rounds], tuple(finals))
 

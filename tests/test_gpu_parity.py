@@ -468,6 +468,33 @@ def test_multiplicities_skewed_warp_aggregation():
     assert got == logup.multiplicities(secret, table)
 
 
+@pytest.mark.parametrize("field", ["big", "test"])
+@pytest.mark.parametrize("d,n", [(1 << 18, 1 << 12), (1 << 12, 1 << 2), (1 << 16, 1 << 15)])
+def test_lookup_tiled_matches_materialised(field, d, n, monkeypatch):
+    """The tiled logUp path (replicated table side never materialised) and the
+    fully materialised 7-table claim give identical proofs."""
+    from paper_2508_21393_b200 import lookup as L
+
+    p = FIELDS[field]
+    spec = D.spec_for(p)
+    rnd = np.random.default_rng(d + n)
+    table = [int(v) for v in rnd.integers(0, 2**40, size=n)]
+    idx = rnd.integers(0, n, size=d)
+    sec = D.upload([table[int(i)] for i in idx], spec)
+    tab = zb.LookupTable(D.DeviceVector(D.upload(table, spec), n, spec), StubCommitment(
+        (n - 1).bit_length()))
+    secret = zb.SecretVector(D.DeviceVector(sec, d, spec), StubCommitment((d - 1).bit_length()), ())
+    out = []
+    for tiled in (True, False):
+        monkeypatch.setattr(L, "TILED", tiled)
+        m = zb.compute_multiplicities(secret.entries, tab)
+        t = Transcript(b"tiled", p, b"x")
+        pr = zb.prove_lookup(secret, m, tab, KEY, t, RNG)
+        out.append(([r.evaluations for r in pr.sumcheck.rounds], pr.sumcheck.final_values,
+                     pr.secret_values, pr.table_values, t.state))
+    assert out[0] == out[1]
+
+
 def test_multiplicities_golden():
     for c in load_golden("lookup.json")["multiplicities"]:
         table = zb.LookupTable(tuple(c["table"]), None)
