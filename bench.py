@@ -298,9 +298,10 @@ def run_cfg3(steps, warmup, N):
             "kernel": "k_sumcheck_persistent -> k_sumcheck_cluster (7-table Eq.-7 claim, "
                       "fused fold + degree-3 evaluation)",
             "bound": "hbm", "achieved": (ph_bytes / (ph_ms / 1000.0) / 1e9) if ph_ms else 0.0,
-            "unit": "GB/s", "note": "algorithmic bytes: 3 k 2^n 32 per phase (k = 3 full-size "
-                                    "tables in the tiled phase, 7 x 2^16 after); IMAD-bound: 17 "
-                                    "(tiled) / 34 Montgomery products per pair"},
+            "unit": "GB/s", "note": "algorithmic bytes: 3 k 2^n 32 per phase (k = 2 full-size "
+                                    "tables A, S+beta in the tiled phase -- E is factored through "
+                                    "the eq point --, 7 x 2^16 after); IMAD-bound: 2 (round 0) / "
+                                    "10 (tiled) / 34 Montgomery products per pair"},
     }
 
 

@@ -146,6 +146,21 @@ int zkl_batch_inverse(int field, void* dst, const void* src, uint64_t n, const u
 int zkl_multiplicities(int field, const void* secret, uint64_t d, const void* table, uint64_t n,
                        uint32_t* counts, int64_t* first_miss, void* stream);
 
+/* zkl_multiplicities plus, per secret entry, the table index it matched
+ * (index_out: d uint32 on the device; 0xffffffff where it missed).  With
+ * it the lookup prover gathers 1/(beta + s_i) = 1/(beta + t_idx(i)) from
+ * the table-side inversion (lookup.py:163-171) instead of inverting d
+ * secret entries. */
+int zkl_multiplicities_index(int field, const void* secret, uint64_t d, const void* table,
+                             uint64_t n, uint32_t* counts, uint32_t* index_out,
+                             int64_t* first_miss, void* stream);
+
+/* dst[i] = src[idx[i]] (+ add when add_canon != NULL), i < n; every idx[i]
+ * must be < src_n (caller-checked).  The secret-side logUp columns
+ * (lookup.py:175-202) of a lookup whose secret entries are table entries. */
+int zkl_gather(int field, void* dst, const void* src, uint64_t src_n, const uint32_t* idx,
+               uint64_t n, const uint8_t* add_canon, void* stream);
+
 /* y = M x (transpose 0) or M^T x (transpose 1); M row-major rows x cols of
  * type mtype (ZKL_MT_*), x/y device field vectors.  The MLE partial
  * evaluations behind the factored zkMat prover (gadgets.py:210-251). */
@@ -169,17 +184,24 @@ int zkl_matmul_prove(int field, int a_type, const void* A, int b_type, const voi
                      uint8_t* rounds_out, uint8_t* point_out, uint8_t* finals_out, void* stream);
 
 /* The logUp Eq.-7 sumcheck (lookup.py:188-219) for a secret larger than the
- * table (d = 2^num_vars > n = 2^tile_log): runs the first `rounds` =
- * num_vars - tile_log rounds without materialising the replicated table side
- * (B, T+beta, M read at index mod n, the indicator == 1), appends exactly the
- * reference's transcript bytes, then folds E, A, S+beta by the last challenge.
- * tables: E, A, S+beta (2^num_vars, consumed) and B, T+beta, M (2^tile_log);
- * coeffs: the five term coefficients (lookup.py:116-126), canonical.  The
- * remaining tile_log rounds run through zkl_sumcheck_prove on 7 tables of
- * 2^tile_log (indicator = ones).  ZKL_ERR_UNSUPPORTED in stepwise mode. */
+ * table (d = 2^num_vars > n = 2^tile_log, tile_log >= 5): runs the first
+ * `rounds` = num_vars - tile_log rounds and appends exactly the reference's
+ * transcript bytes, without materialising the replicated table side (B,
+ * T+beta, M depend on index mod n; the indicator == 1) or the eq table E (it
+ * is factored through the eq point u).  Afterwards A and S+beta are folded by
+ * the last challenge (their first n entries hold the bound tables) and
+ * tables[0] holds E bound at the point (n entries).
+ * tables: E_out (n entries, written), A, S+beta (2^num_vars, consumed),
+ * B, T+beta, M (n entries, read).  u_canon: the eq point (num_vars scalars);
+ * coeffs: the five term coefficients (lookup.py:116-126), canonical.
+ * flags bit 0: A = 1/(S+beta) entrywise (lets round 0 skip two products).
+ * The remaining tile_log rounds run through zkl_sumcheck_prove on the 7
+ * tables of n entries (indicator = ones).  ZKL_ERR_UNSUPPORTED in stepwise
+ * mode or for n < 32. */
 int zkl_logup_tiled_rounds(int field, void* const* tables, int tile_log, int num_vars, int rounds,
-                           const uint8_t* coeffs_canon, uint8_t* state_inout, uint8_t* rounds_out,
-                           uint8_t* point_out, void* stream);
+                           const uint8_t* u_canon, const uint8_t* coeffs_canon, int flags,
+                           uint8_t* state_inout, uint8_t* rounds_out, uint8_t* point_out,
+                           void* stream);
 
 /* CUDA-event profiler for benchmarks: when enabled, the library brackets
  * each kernel family on its launching stream.  kind 0: matrix-vector

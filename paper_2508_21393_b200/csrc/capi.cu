@@ -118,9 +118,26 @@ int dot_impl(uint8_t* out, const void* a, const void* b, uint64_t n, cudaStream_
   } while (0)
 #define D(field, EXPR) DISPATCH(field, EXPR, EXPR)
 
+template <class F>
+static int logup_tiled_impl(void* const* tables, int tile_log, int num_vars, int rounds,
+                            const uint8_t* u_canon, const uint8_t* coeffs_canon, int flags,
+                            uint8_t* state_inout, uint8_t* rounds_out, uint8_t* point_out,
+                            void* stream) {
+  using T = typename F::T;
+  if (num_vars < 1 || num_vars > 63) {
+    set_error("logup_tiled: bad num_vars");
+    return kErrArg;
+  }
+  T c[5];
+  for (int t = 0; t < 5; t++) c[t] = load_canon<F>(coeffs_canon + F::kBytes * t);
+  std::vector<T> u(num_vars);
+  for (int j = 0; j < num_vars; j++) u[j] = load_canon<F>(u_canon + (size_t)F::kBytes * j);
+  return op_logup_tiled<F>(tables, tile_log, num_vars, rounds, u.data(), c, flags & 1,
+                           state_inout, rounds_out, point_out, (cudaStream_t)stream);
+}
 extern "C" {
 
-int zkl_abi_version(void) { return 2; }
+int zkl_abi_version(void) { return 3; }
 uint64_t zkl_launch_count(void) { return g_launches; }
 const char* zkl_last_error(void) { return get_error(); }
 int zkl_elem_bytes(int field) {
@@ -233,6 +250,17 @@ int zkl_multiplicities(int field, const void* secret, uint64_t d, const void* ta
                        uint32_t* counts, int64_t* first_miss, void* stream) {
   D(field, op_multiplicities<F>(secret, d, table, n, counts, first_miss, (cudaStream_t)stream));
 }
+int zkl_multiplicities_index(int field, const void* secret, uint64_t d, const void* table,
+                             uint64_t n, uint32_t* counts, uint32_t* index_out,
+                             int64_t* first_miss, void* stream) {
+  D(field, op_multiplicities<F>(secret, d, table, n, counts, first_miss, (cudaStream_t)stream,
+                                index_out));
+}
+int zkl_gather(int field, void* dst, const void* src, uint64_t src_n, const uint32_t* idx,
+               uint64_t n, const uint8_t* add_canon, void* stream) {
+  D(field, op_gather<F>(dst, src, src_n, idx, n, scalar<F>(add_canon), add_canon != nullptr,
+                        (cudaStream_t)stream));
+}
 int zkl_matmul_prove(int field, int a_type, const void* A, int b_type, const void* B, int c_type,
                      const void* C, int d0, int d1, int d2, uint8_t* state_inout,
                      uint8_t* rounds_out, uint8_t* point_out, uint8_t* finals_out, void* stream) {
@@ -240,22 +268,11 @@ int zkl_matmul_prove(int field, int a_type, const void* A, int b_type, const voi
                               rounds_out, point_out, finals_out, (cudaStream_t)stream));
 }
 int zkl_logup_tiled_rounds(int field, void* const* tables, int tile_log, int num_vars, int rounds,
-                           const uint8_t* coeffs_canon, uint8_t* state_inout, uint8_t* rounds_out,
-                           uint8_t* point_out, void* stream) {
-  if (field == ZKL_FIELD_BLS12_381_FR) {
-    Fr255::T c[5];
-    for (int t = 0; t < 5; t++) c[t] = load_canon<Fr255>(coeffs_canon + 32 * t);
-    return op_logup_tiled<Fr255>(tables, tile_log, num_vars, rounds, c, state_inout, rounds_out,
-                                 point_out, (cudaStream_t)stream);
-  }
-  if (field == ZKL_FIELD_M61) {
-    M61::T c[5];
-    for (int t = 0; t < 5; t++) c[t] = load_canon<M61>(coeffs_canon + 8 * t);
-    return op_logup_tiled<M61>(tables, tile_log, num_vars, rounds, c, state_inout, rounds_out,
-                               point_out, (cudaStream_t)stream);
-  }
-  set_error("unknown field id %d", field);
-  return kErrArg;
+                           const uint8_t* u_canon, const uint8_t* coeffs_canon, int flags,
+                           uint8_t* state_inout, uint8_t* rounds_out, uint8_t* point_out,
+                           void* stream) {
+  D(field, logup_tiled_impl<F>(tables, tile_log, num_vars, rounds, u_canon, coeffs_canon, flags,
+                               state_inout, rounds_out, point_out, stream));
 }
 int zkl_prof_enable(int on) {
   zkl::prof_enable(on != 0);

@@ -481,6 +481,23 @@ int op_axpy(void* y, const void* a, typename F::T k, const void* b, uint64_t n, 
   return kOk;
 }
 
+// pointwise product dst[i] = a[i] b[i]
+template <class F>
+__global__ void k_mul(typename F::T* dst, const typename F::T* a, const typename F::T* b,
+                      uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = F::mul(a[i], b[i]);
+}
+template <class F>
+int op_mul(void* dst, const void* a, const void* b, uint64_t n, cudaStream_t s) {
+  if (!n) return kOk;
+  k_mul<F><<<grid_for(n, 256), 256, 0, s>>>((typename F::T*)dst, (const typename F::T*)a,
+                                             (const typename F::T*)b, n);
+  ZKL_LAUNCH_CHECK();
+  return kOk;
+}
+
 // single-block dot / sum (vectors here are <= a few 2^12 entries)
 template <class F>
 __global__ void k_dot(typename F::T* out, const typename F::T* a, const typename F::T* b,
@@ -529,6 +546,33 @@ int op_expand(void* dst, uint64_t dst_n, const void* src, uint64_t src_n, int mo
   return kOk;
 }
 
+// dst[i] = src[idx[i]] (+ add): the secret-side logUp columns of a lookup
+// whose secret entries are known table entries (idx from
+// zkl_multiplicities_index), e.g. 1/(beta + s_i) = 1/(beta + t_idx(i)).
+template <class F, bool ADD>
+__global__ void k_gather(typename F::T* dst, const typename F::T* src, const uint32_t* idx,
+                         uint64_t n, typename F::T add) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    typename F::T v = src[__ldg(idx + i)];
+    if (ADD) v = F::add(v, add);
+    dst[i] = v;
+  }
+}
+template <class F>
+int op_gather(void* dst, const void* src, uint64_t src_n, const uint32_t* idx, uint64_t n,
+              typename F::T add, bool has_add, cudaStream_t s) {
+  if (!n) return kOk;
+  if (!src_n) { set_error("gather: empty source"); return kErrArg; }
+  using T = typename F::T;
+  if (has_add)
+    k_gather<F, true><<<grid_for(n, 256), 256, 0, s>>>((T*)dst, (const T*)src, idx, n, add);
+  else
+    k_gather<F, false><<<grid_for(n, 256), 256, 0, s>>>((T*)dst, (const T*)src, idx, n, add);
+  ZKL_LAUNCH_CHECK();
+  return kOk;
+}
+
 // u32 counts -> field
 template <class F>
 __global__ void k_lift_u32(typename F::T* dst, const uint32_t* src, uint64_t n) {
@@ -567,11 +611,14 @@ int op_read(uint8_t* host, const void* src, uint64_t n, cudaStream_t s) {
   template int op_eq_table<F>(void*, const F::T*, int, cudaStream_t);                     \
   template int op_fold<F>(void*, const void*, uint64_t, F::T, cudaStream_t);              \
   template int op_axpy<F>(void*, const void*, F::T, const void*, uint64_t, cudaStream_t); \
+  template int op_mul<F>(void*, const void*, const void*, uint64_t, cudaStream_t);          \
   template int op_read<F>(uint8_t*, const void*, uint64_t, cudaStream_t);                 \
   template int op_dot<F>(F::T*, const void*, const void*, uint64_t, cudaStream_t);          \
   template int op_expand<F>(void*, uint64_t, const void*, uint64_t, int, F::T, F::T,        \
                             cudaStream_t);                                                  \
-  template int op_lift_u32<F>(void*, const uint32_t*, uint64_t, cudaStream_t);
+  template int op_lift_u32<F>(void*, const uint32_t*, uint64_t, cudaStream_t);                \
+  template int op_gather<F>(void*, const void*, uint64_t, const uint32_t*, uint64_t, F::T, bool, \
+                            cudaStream_t);
 ZKL_INST(Fr255)
 ZKL_INST(M61)
 

@@ -8,7 +8,9 @@
 // Device design: open-addressing hash table over table indices (2x load),
 // built with atomicCAS / atomicMax (duplicates keep the largest index), then
 // one probe per secret entry with atomicAdd on the counts and atomicMin on
-// the first miss.
+// the first miss.  Optionally each secret entry's table index is written
+// out (0xffffffff for a miss), which lets the lookup prover gather the
+// secret-side columns from the table side instead of inverting d entries.
 #include "ops.cuh"
 
 namespace zkl {
@@ -52,7 +54,7 @@ __global__ void k_ht_insert(const typename F::T* table, uint32_t n, uint32_t* sl
 template <class F>
 __global__ void k_ht_count(const typename F::T* secret, uint64_t d, const typename F::T* table,
                            const uint32_t* slots, uint32_t mask, uint32_t* counts,
-                           unsigned long long* first_miss) {
+                           unsigned long long* first_miss, uint32_t* index_out) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < d; base += stride) {
     const uint64_t i = base + threadIdx.x;
@@ -67,6 +69,7 @@ __global__ void k_ht_count(const typename F::T* secret, uint64_t d, const typena
         h = (h + 1) & mask;
       }
     }
+    if (index_out != nullptr && i < d) index_out[i] = hit;
     const unsigned peers = __match_any_sync(kFull, hit);
     const int leader = __ffs(peers) - 1;
     if (hit != kEmpty && (threadIdx.x & 31) == leader) atomicAdd(&counts[hit], __popc(peers));
@@ -75,7 +78,8 @@ __global__ void k_ht_count(const typename F::T* secret, uint64_t d, const typena
 
 template <class F>
 int op_multiplicities(const void* secret, uint64_t d, const void* table, uint64_t n,
-                      uint32_t* counts, int64_t* first_miss, cudaStream_t s) {
+                      uint32_t* counts, int64_t* first_miss, cudaStream_t s,
+                      uint32_t* index_out) {
   using T = typename F::T;
   *first_miss = -1;
   if (n == 0 || n > (1ull << 31)) { set_error("multiplicities: bad table size"); return kErrArg; }
@@ -94,7 +98,7 @@ int op_multiplicities(const void* secret, uint64_t d, const void* table, uint64_
   ZKL_LAUNCH_CHECK();
   if (d) {
     k_ht_count<F><<<grid_for(d, 256), 256, 0, s>>>((const T*)secret, d, (const T*)table, slots,
-                                                    (uint32_t)(cap - 1), counts, flag);
+                                                    (uint32_t)(cap - 1), counts, flag, index_out);
     ZKL_LAUNCH_CHECK();
   }
   unsigned long long fm;
@@ -109,8 +113,8 @@ int op_multiplicities(const void* secret, uint64_t d, const void* table, uint64_
 }
 
 template int op_multiplicities<Fr255>(const void*, uint64_t, const void*, uint64_t, uint32_t*,
-                                      int64_t*, cudaStream_t);
+                                      int64_t*, cudaStream_t, uint32_t*);
 template int op_multiplicities<M61>(const void*, uint64_t, const void*, uint64_t, uint32_t*,
-                                    int64_t*, cudaStream_t);
+                                    int64_t*, cudaStream_t, uint32_t*);
 
 }  // namespace zkl

@@ -24,6 +24,8 @@ int op_fold(void* dst, const void* src, uint64_t half, typename F::T r, cudaStre
 // y = a + k * b
 template <class F>
 int op_axpy(void* y, const void* a, typename F::T k, const void* b, uint64_t n, cudaStream_t s);
+template <class F>
+int op_mul(void* dst, const void* a, const void* b, uint64_t n, cudaStream_t s);
 // canonical host copy of n device elements (synchronises)
 template <class F> int op_read(uint8_t* host, const void* src, uint64_t n, cudaStream_t s);
 // out = sum_i a[i]*b[i] (b == nullptr: sum_i a[i]); device scalar (Montgomery)
@@ -43,7 +45,8 @@ struct Terms {
   int nf[kMaxTerms];
   int fi[kMaxTerms][3];
   typename F::T coef[kMaxTerms];
-  int tile_log;  // LOGUP_TILED: tables 3..5 have 2^tile_log entries, read at i mod 2^tile_log
+  int tile_log;  // LOGUP_TILED: log2 of the table side's size (the low index bits)
+  int inv_pair;  // LOGUP_TILED: A = 1/S entrywise before the first fold
 };
 template <class F>
 struct Post {
@@ -72,7 +75,11 @@ int op_batch_inverse(void* dst, const void* src, uint64_t n, typename F::T add, 
 // multiplicities ---------------------------------------------------------------
 template <class F>
 int op_multiplicities(const void* secret, uint64_t d, const void* table, uint64_t n,
-                      uint32_t* counts, int64_t* first_miss, cudaStream_t s);
+                      uint32_t* counts, int64_t* first_miss, cudaStream_t s,
+                      uint32_t* index_out = nullptr);
+template <class F>
+int op_gather(void* dst, const void* src, uint64_t src_n, const uint32_t* idx, uint64_t n,
+              typename F::T add, bool has_add, cudaStream_t s);
 
 // matrix x field-vector ------------------------------------------------------------
 // mtype: 0 = field (Montgomery), 1 = int16, 2 = int32, 3 = int64
@@ -83,8 +90,8 @@ int op_matvec(int mtype, const void* M, uint64_t rows, uint64_t cols, int transp
 // replicated logUp claim, first rounds with the tiled evaluator (persistent.cu)
 template <class F>
 int op_logup_tiled(void* const* tables, int tile_log, int num_vars, int rounds,
-                   const typename F::T* coefs, uint8_t* state, uint8_t* rounds_out,
-                   uint8_t* point_out, cudaStream_t s);
+                   const typename F::T* u, const typename F::T* coefs, int inv_pair,
+                   uint8_t* state, uint8_t* rounds_out, uint8_t* point_out, cudaStream_t s);
 
 // native zkMat driver (zkmat.cu): gadgets.py:241-251, factored
 template <class F>

@@ -428,81 +428,108 @@ struct EvLogup {
 
 // logUp Eq.-7 claim in its replicated form (lookup.py:188-202, secret
 // larger than the table), for the rounds that bind the high log2(d/n)
-// variables: tables [E, A, S] are folded as usual, while the table side
-// [B, T, M] depends only on the low tile_log index bits -- lo == hi, folding
-// is the identity, so they are never materialised at 2^n, folded or
-// written -- and the indicator is identically 1.  Same 16 raw outputs as
-// EvLogup (the host finishing is shared); 17 products per pair instead of 34.
+// variables.  Three structural facts remove most of the work:
+//  * the table side [B, T, M] depends only on the low tile_log index bits,
+//    so lo == hi inside every pair: sum E B T = C_j l(x) sum_ti BT(ti)
+//    eq_lo(ti) (eq tables sum to 1) and sum M B = (half / 2^tile_log)
+//    sum_ti M B -- two constants the host computes once;
+//  * the indicator is 1, and sum E I = C_j l(x);
+//  * E is an eq table: after binding r_0..r_{j-1} it is
+//    C_j * l_j(x) * eq_hi_j(k) * eq_lo(ti) for the pair (i, i + half) with
+//    i = k 2^tile_log + ti, where l_j(x) = (1 - u_j) + x (2 u_j - 1) and
+//    C_j = prod_{t<j} l_t(r_t).  E is never materialised or folded.
+// The device sums, per round, P_c = sum_i eq_hi(k) eq_lo(ti) q_c(i) with
+// q_0 = a0 s0, q_1 = a1 s1, q_2 = (a1 - a0)(s1 - s0) (A S at x = 0, 1 and
+// its x^2 coefficient) plus sum a0 and sum (a1 - a0); the host builds the
+// four evaluations.  Per pair: 4 products to fold A, S, 3 for q, 3 for the
+// eq_hi weights (the eq_lo weight is applied once per (ti, k-slice) unit).
+// In round 0, when A = 1/S entrywise (tm.inv_pair), q_0 = q_1 = 1 and P_0 =
+// P_1 = 1: two products per pair.
+// Tables: [eq_hi (all rounds, round j's 2^(r-1-j) entries at offset
+// 2^(r-1-j) - 1), A, S + beta, eq_lo (2^tile_log)].
 template <class F, int MAXK>
 struct EvLogupTiled {
   using T = typename F::T;
   static constexpr bool kGeneric = false;
   static constexpr bool kTiled = true;
-  static constexpr int NA = 16, NOUT = 16;
-  template <bool FOLD>
-  ZKL_D static void pair_tiled(const TablePtrs<F, MAXK>& tabs, uint64_t i, uint64_t half,
-                               const T& r, const Terms<F>& tm, T (&acc)[NA]) {
-    T lo[3], df[3];
-    if (FOLD) {
-      T a0[3], b0[3], da[3], db[3];
-#pragma unroll
-      for (int j = 0; j < 3; j++) {
-        const T* t = tabs.t[j];
-        a0[j] = ld_cg(t + i);
-        b0[j] = ld_cg(t + i + half);
-        da[j] = F::sub(ld_cg(t + i + 2 * half), a0[j]);
-        db[j] = F::sub(ld_cg(t + i + 3 * half), b0[j]);
+  static constexpr int NA = 5, NOUT = 5;
+  ZKL_D static void accumulate(const TablePtrs<F, MAXK>& tabs, uint64_t half, bool fold,
+                               const T& r, const Terms<F>& tm, uint64_t gtid,
+                               uint64_t nthreads, T (&acc)[NA]) {
+    const int tl = tm.tile_log;
+    const uint64_t K = half >> tl;            // pairs per low index ti
+    const int s_log = K >= 8 ? 3 : (K >= 4 ? 2 : (K >= 2 ? 1 : 0));
+    const uint64_t S = 1ull << s_log;         // k-slices per ti block
+    const int nblk_log = tl - 5;               // blocks of 32 consecutive ti
+    const uint64_t units = S << nblk_log;
+    const uint64_t nw = nthreads >> 5;
+    const int lane = threadIdx.x & 31;
+    const T* eh = tabs.t[0] + (K - 1);
+    const T* A = tabs.t[1];
+    const T* Sb = tabs.t[2];
+    const T* el = tabs.t[3];
+    const bool inv0 = !fold && tm.inv_pair;
+    for (uint64_t u = gtid >> 5; u < units; u += nw) {
+      const uint64_t ti = ((u & ((1ull << nblk_log) - 1)) << 5) | lane;
+      T p0 = F::zero(), p1 = F::zero(), p2 = F::zero();
+      for (uint64_t kk = u >> nblk_log; kk < K; kk += S) {
+        const uint64_t i = (kk << tl) | ti;
+        T a0, ad, s0, sd;
+        if (fold) {
+          T* At = tabs.t[1];
+          T* St = tabs.t[2];
+          const T xa = ld_cg(At + i), ya = ld_cg(At + i + half);
+          const T xs = ld_cg(St + i), ys = ld_cg(St + i + half);
+          T da = F::sub(ld_cg(At + i + 2 * half), xa), db = F::sub(ld_cg(At + i + 3 * half), ya);
+          T ds = F::sub(ld_cg(St + i + 2 * half), xs), dt = F::sub(ld_cg(St + i + 3 * half), ys);
+          F::mul4r(r, da, db, ds, dt);
+          a0 = F::add(xa, da);
+          const T a1 = F::add(ya, db);
+          s0 = F::add(xs, ds);
+          const T s1 = F::add(ys, dt);
+          At[i] = a0;
+          At[i + half] = a1;
+          St[i] = s0;
+          St[i + half] = s1;
+          ad = F::sub(a1, a0);
+          sd = F::sub(s1, s0);
+        } else {
+          a0 = ld_cg(A + i);
+          ad = F::sub(ld_cg(A + i + half), a0);
+          s0 = ld_cg(Sb + i);
+          sd = F::sub(ld_cg(Sb + i + half), s0);
+        }
+        acc[3] = F::add(acc[3], a0);
+        acc[4] = F::add(acc[4], ad);
+        const T w = eh[kk];
+        if (inv0) {
+          T q2 = F::mul(ad, sd);
+          p2 = F::add(p2, F::mul(w, q2));
+        } else {
+          const T a1 = F::add(a0, ad), s1 = F::add(s0, sd);
+          T q0, q1, q2;
+          F::mul3(a0, s0, a1, s1, ad, sd, q0, q1, q2);
+          F::mul3(w, q0, w, q1, w, q2, q0, q1, q2);
+          p0 = F::add(p0, q0);
+          p1 = F::add(p1, q1);
+          p2 = F::add(p2, q2);
+        }
       }
-      F::mul4r(r, da[0], db[0], da[1], db[1]);
-      F::mul2(r, da[2], r, db[2], da[2], db[2]);
-#pragma unroll
-      for (int j = 0; j < 3; j++) {
-        T* t = tabs.t[j];
-        const T l = F::add(a0[j], da[j]), h = F::add(b0[j], db[j]);
-        t[i] = l;
-        t[i + half] = h;
-        lo[j] = l;
-        df[j] = F::sub(h, l);
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 3; j++) {
-        const T* t = tabs.t[j];
-        lo[j] = ld_cg(t + i);
-        df[j] = F::sub(ld_cg(t + i + half), lo[j]);
+      const T wl = el[ti];
+      if (inv0) {
+        acc[2] = F::add(acc[2], F::mul(wl, p2));
+      } else {
+        F::mul3(wl, p0, wl, p1, wl, p2, p0, p1, p2);
+        acc[0] = F::add(acc[0], p0);
+        acc[1] = F::add(acc[1], p1);
+        acc[2] = F::add(acc[2], p2);
       }
     }
-    const uint64_t ti = i & ((1ull << tm.tile_log) - 1);
-    const T b = tabs.t[3][ti], tt = tabs.t[4][ti], m = tabs.t[5][ti];
-    const T e0 = lo[0], ed = df[0], a0 = lo[1], ad = df[1], s0 = lo[2], sd = df[2];
-    const T e1 = F::add(e0, ed), a1 = F::add(a0, ad), s1 = F::add(s0, sd);
-    T p[3], bt, mb;
-    F::mul4(a0, s0, a1, s1, ad, sd, b, tt, p[0], p[1], p[2], bt);
-    T as[4];
-    quad_evals<F>(p[0], p[1], p[2], as);
-    const T e2 = F::add(e1, ed), e3 = F::add(e2, ed);
-    T o[4], eb0, eb1;
-    F::mul4(e0, as[0], e1, as[1], e2, as[2], e3, as[3], o[0], o[1], o[2], o[3]);
-    F::mul3(e0, bt, e1, bt, m, b, eb0, eb1, mb);
-    const T ebd = F::sub(eb1, eb0);
-    const T eb2 = F::add(eb1, ebd), eb3 = F::add(eb2, ebd);
-#pragma unroll
-    for (int k = 0; k < 4; k++) acc[k] = F::add(acc[k], o[k]);
-    acc[4] = F::add(acc[4], e0);  // E I with I = 1: (e0, e1, ed * 0)
-    acc[5] = F::add(acc[5], e1);
-    acc[7] = F::add(acc[7], eb0);
-    acc[8] = F::add(acc[8], eb1);
-    acc[9] = F::add(acc[9], eb2);
-    acc[10] = F::add(acc[10], eb3);
-    acc[11] = F::add(acc[11], a0);
-    acc[12] = F::add(acc[12], ad);
-    acc[13] = F::add(acc[13], mb);  // M B constant across the pair: (mb, mb, 0)
-    acc[14] = F::add(acc[14], mb);
   }
   ZKL_D static void pair(T (&)[MAXK], const T (&)[MAXK], int, const Terms<F>&, T (&)[NA]) {}
   ZKL_D static void finish(const T (&acc)[NA], T (&out)[NOUT]) {
 #pragma unroll
-    for (int q = 0; q < 16; q++) out[q] = acc[q];
+    for (int q = 0; q < NOUT; q++) out[q] = acc[q];
   }
   ZKL_D static T lane(const T&, int, int, bool, const Terms<F>&) { return F::zero(); }
 };
@@ -701,10 +728,7 @@ ZKL_D void accumulate_round(const TablePtrs<F, MAXK>& tabs, int k, const Terms<F
 #pragma unroll
     for (int q = 0; q < EV::NA; q++) acc[q] = F::zero();
     if constexpr (IsTiled<EV>::value) {
-      for (uint64_t i = gtid; i < half; i += nthreads) {
-        if (fold) EV::template pair_tiled<true>(tabs, i, half, r, tm, acc);
-        else EV::template pair_tiled<false>(tabs, i, half, r, tm, acc);
-      }
+      EV::accumulate(tabs, half, fold, r, tm, gtid, nthreads, acc);
     } else {
       for (uint64_t i = gtid; i < half; i += nthreads) {
         T cur[MAXK], df[MAXK];
@@ -1161,7 +1185,7 @@ static int dispatch(const LaunchReq<F>& q, Plan* pl, int* nout, int launch) {
       if constexpr (MAXK >= 8) ZKL_SHAPE(EvLogup)
       else ZKL_SHAPE(EvGeneric)
     case kLogupTiled:
-      if constexpr (MAXK >= 8) ZKL_SHAPE(EvLogupTiled)
+      if constexpr (MAXK >= 4) ZKL_SHAPE(EvLogupTiled)
       else ZKL_SHAPE(EvGeneric)
     default: ZKL_SHAPE(EvGeneric)
   }
@@ -1348,7 +1372,7 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
   int rc = mailbox_for_current_device(&mb_host, &mb_dev);
   if (rc) return rc;
   int shape = a.forced_shape >= 0 ? a.forced_shape : detect_shape<F>(tm);
-  if ((shape == kLogup || shape == kLogupTiled) && k <= 4) shape = kGeneric;  // built for MAXK 8
+  if (shape == kLogup && k <= 4) shape = kGeneric;  // built for MAXK 8
   const int nrun = a.rounds_limit > 0 ? a.rounds_limit : n;
   if (nrun < n && finals_out) {
     set_error("sumcheck phase: a partial phase has no finals");
@@ -1417,7 +1441,7 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
   // k 2^(n-j) elements read and (from round 1) k 2^(n-j-1) written by the fold
   // (the tiled logUp phase moves only its 3 full-size tables; the 2^tile_log
   // table side stays in L2)
-  const int k_full = shape == kLogupTiled ? 3 : k;
+  const int k_full = shape == kLogupTiled ? 2 : k;
   const int ph = prof_open(kProfPhase, 3.0 * k_full * (double)(1ull << n) * F::kBytes,
                            (double)nrun, s);
   rc = run_dispatch<F>(rq, &pl, &nout, pl.j_switch > 0 ? 1 : 2);
@@ -1428,6 +1452,7 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
   // K_canon) = value * K in canonical form), set at round 0 after prepare()
   T Kc[5];
   T pm = a.post_mul;
+  T lq_c = H::one();  // LOGUP_TILED: C_j
   std::vector<T> lazy_add;
   bool prepared = !a.prepare;
   uint32_t words[kMbEvalWords];
@@ -1468,7 +1493,28 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
     T raw[kMbMaxOut];
     for (int q = 0; q < nout; q++) raw[q] = HostRed<F>::reduce(words + q * NW);
     T ev[4];
-    if (shape == kProd2) {
+    if (shape == kLogupTiled) {
+      // EvLogupTiled: raw = [P0, P1, P2, sum a0, sum ad] (storage form)
+      if (j == 0 && a.tm.inv_pair) raw[0] = raw[1] = H::one();
+      T qx[4];
+      host_quad<F>(raw[0], raw[1], raw[2], qx);
+      const T& u = a.lq_u[j];
+      const T l0 = H::sub(H::one(), u), ld = H::sub(H::add(u, u), H::one());
+      T npairs = H::one();  // half / 2^tile_log
+      for (int b = 0; b < n - 1 - j - a.tm.tile_log; b++) npairs = H::add(npairs, npairs);
+      const T cst = H::add(a.tm.coef[1], H::mul(a.tm.coef[2], a.lq_k3));
+      const T mbt = H::mul(a.tm.coef[4], H::mul(npairs, a.lq_smb));
+      T lx = l0, ax = raw[3];
+      for (int x = 0; x < 4; x++) {
+        if (x) {
+          lx = H::add(lx, ld);
+          ax = H::add(ax, raw[4]);
+        }
+        T v = H::mul(H::mul(lq_c, lx), H::add(H::mul(a.tm.coef[0], qx[x]), cst));
+        v = H::add(v, H::mul(a.tm.coef[3], ax));
+        ev[x] = host::canon_of<F>(H::add(v, mbt));
+      }
+    } else if (shape == kProd2) {
       host_quad<F>(raw[0], raw[1], raw[2], ev);
       for (int x = 0; x < 4; x++) ev[x] = H::mul(ev[x], Kc[0]);
     } else if (shape == kSum2Prod2) {
@@ -1505,6 +1551,10 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
     uint8_t* rcan = point_out + (size_t)j * nb;
     reduce512<F>(rawc, rcan);
     const T rm = host::from_canon<F>(rcan);
+    if (shape == kLogupTiled) {  // C_{j+1} = C_j ((1 - u_j) + r_j (2 u_j - 1))
+      const T& u = a.lq_u[j];
+      lq_c = H::mul(lq_c, H::add(H::sub(H::one(), u), H::mul(rm, H::sub(H::add(u, u), H::one()))));
+    }
     uint32_t cw[NC];
     memcpy(cw, &rm, nb);
     const uint64_t tg = (uint64_t)(seq0 + j + 1) << 32;
@@ -1607,58 +1657,109 @@ int op_sumcheck_prove(void* const* tables, int k, int num_vars, const Terms<F>& 
 }
 
 // The replicated logUp claim's first `rounds` rounds (the high log2(d/n)
-// variables) with the tiled evaluator, then E, A, S folded by the last
-// challenge (the next phase runs the remaining rounds over 2^tile_log-entry
-// tables).  tables: [E, A, S+beta] (2^num_vars) and [B, T+beta, M]
-// (2^tile_log); coefs: the five Eq.-7 term coefficients (storage form).
+// variables) with the eq-factored tiled evaluator (EvLogupTiled), then A, S
+// folded by the last challenge and the eq table of the remaining tile_log
+// variables (E folded at the bound point) written to tables[0], ready for
+// the next phase over 2^tile_log-entry tables.
+// tables: [E_out (2^tile_log, written), A, S+beta (2^num_vars, folded in
+// place), B, T+beta, M (2^tile_log)]; u: the eq point (num_vars, storage
+// form); coefs: the five Eq.-7 term coefficients (storage form);
+// inv_pair: A = 1/S entrywise (the prover's construction).
 template <class F>
 int op_logup_tiled(void* const* tables, int tile_log, int num_vars, int rounds,
-                   const typename F::T* coefs, uint8_t* state, uint8_t* rounds_out,
-                   uint8_t* point_out, cudaStream_t s) {
+                   const typename F::T* u, const typename F::T* coefs, int inv_pair,
+                   uint8_t* state, uint8_t* rounds_out, uint8_t* point_out, cudaStream_t s) {
   using T = typename F::T;
+  using H = typename host::For<F>::H;
   if (no_persistent()) {
     set_error("logup_tiled: needs the persistent engine (stepwise mode active)");
     return kErrUnsupported;
   }
-  if (rounds < 1 || tile_log < 1 || rounds + tile_log != num_vars) {
+  if (rounds < 1 || rounds > 40 || tile_log < 1 || rounds + tile_log != num_vars) {
     set_error("logup_tiled: bad rounds/tile sizes");
     return kErrArg;
   }
+  if (tile_log < 5) {
+    set_error("logup_tiled: table side below 32 entries");
+    return kErrUnsupported;
+  }
+  const uint64_t ntile = 1ull << tile_log;
+  // eq_hi for every round: round j uses eq(u_{j+1..rounds-1}, k) over
+  // 2^(rounds-1-j) entries at offset 2^(rounds-1-j) - 1 (MSB-first, like
+  // mle.eq_table); built on the host (2^rounds - 1 entries)
+  const size_t nhi = ((size_t)1 << rounds) - 1;
+  std::vector<T> hi(nhi);
+  for (int j = 0; j < rounds; j++) {
+    const int m = rounds - 1 - j;
+    T* t = hi.data() + (((size_t)1 << m) - 1);
+    t[0] = H::one();
+    for (int c = 0; c < m; c++) {  // append coordinate u_{j+1+c} as the new low bit
+      const T uc = u[j + 1 + c], vc = H::sub(H::one(), uc);
+      for (int64_t q = ((int64_t)1 << c) - 1; q >= 0; q--) {
+        t[2 * q + 1] = H::mul(t[q], uc);
+        t[2 * q] = H::mul(t[q], vc);
+      }
+    }
+  }
+  // the work arena, not scratch: run_phase keeps its block partials in scratch
+  void* ws;
+  int rc = work_reserve(nhi * sizeof(T) + ntile * sizeof(T) + 2 * sizeof(T), &ws, s);
+  if (rc) return rc;
+  T* d_hi = (T*)ws;
+  T* d_bt = d_hi + nhi;
+  T* d_dot = d_bt + ntile;
+  ZKL_CUDA(cudaMemcpyAsync(d_hi, hi.data(), nhi * sizeof(T), cudaMemcpyHostToDevice, s));
+  // eq_lo = eq(u_rounds.., ti) into the E_out buffer; table-side constants
+  T* eq_lo = (T*)tables[0];
+  if ((rc = op_eq_table<F>(eq_lo, u + rounds, tile_log, s))) return rc;
+  if ((rc = op_mul<F>(d_bt, tables[3], tables[4], ntile, s))) return rc;
+  if ((rc = op_dot<F>(d_dot, d_bt, eq_lo, ntile, s))) return rc;
+  if ((rc = op_dot<F>(d_dot + 1, tables[5], tables[3], ntile, s))) return rc;
+  T consts[2];
+  ZKL_CUDA(cudaMemcpyAsync(consts, d_dot, 2 * sizeof(T), cudaMemcpyDeviceToHost, s));
+  ZKL_CUDA(cudaStreamSynchronize(s));
   Terms<F> tm;
   memset(&tm, 0, sizeof(tm));
   tm.nterms = 5;
   tm.degree = 3;
-  const int nf[5] = {3, 2, 3, 1, 2};
-  const int fi[5][3] = {{0, 1, 2}, {0, 6, 0}, {0, 3, 4}, {1, 0, 0}, {5, 3, 0}};
-  for (int t = 0; t < 5; t++) {
-    tm.nf[t] = nf[t];
-    for (int q = 0; q < 3; q++) tm.fi[t][q] = fi[t][q];
-    tm.coef[t] = coefs[t];
-  }
+  for (int t = 0; t < 5; t++) tm.coef[t] = coefs[t];
   tm.tile_log = tile_log;
+  tm.inv_pair = inv_pair ? 1 : 0;
+  void* phase_tables[4] = {d_hi, tables[1], tables[2], eq_lo};
   HostTranscript tr;
   memcpy(tr.state, state, 64);
   PhaseArgs<F> a;
-  a.tables = tables;
-  a.k = 6;
+  a.tables = phase_tables;
+  a.k = 4;
   a.num_vars = num_vars;
   a.tm = tm;
-  a.post_mul = host::For<F>::H::one();
+  a.post_mul = H::one();
   a.rounds_limit = rounds;
   a.forced_shape = kLogupTiled;
-  int rc = run_phase<F>(a, tr, rounds_out, point_out, nullptr, s);
+  a.lq_u = u;
+  a.lq_k3 = consts[0];
+  a.lq_smb = consts[1];
+  rc = run_phase<F>(a, tr, rounds_out, point_out, nullptr, s);
   if (rc) return rc;
   const T r = host::from_canon<F>(point_out + (size_t)(rounds - 1) * F::kBytes);
   const uint64_t half = 1ull << (num_vars - rounds);
-  for (int j = 0; j < 3; j++)
+  for (int j = 1; j < 3; j++)
     if ((rc = op_fold<F>(tables[j], tables[j], half, r, s))) return rc;
+  // E at the bound point: C * eq_lo with C = prod_j ((1 - u_j) + r_j (2 u_j - 1))
+  T c = H::one();
+  for (int j = 0; j < rounds; j++) {
+    const T rj = host::from_canon<F>(point_out + (size_t)j * F::kBytes);
+    const T uj = u[j];
+    c = H::mul(c, H::add(H::sub(H::one(), uj), H::mul(rj, H::sub(H::add(uj, uj), H::one()))));
+  }
+  if ((rc = op_axpy<F>(eq_lo, eq_lo, H::sub(c, H::one()), eq_lo, ntile, s))) return rc;
   memcpy(state, tr.state, 64);
   return kOk;
 }
 
 #define ZKL_INST_PERSIST(F)                                                                   \
-  template int op_logup_tiled<F>(void* const*, int, int, int, const F::T*, uint8_t*,          \
-                                 uint8_t*, uint8_t*, cudaStream_t); \
+  template int op_logup_tiled<F>(void* const*, int, int, int, const F::T*, const F::T*, int,  \
+                                 uint8_t*, uint8_t*, uint8_t*, cudaStream_t);                 \
   template int detect_shape<F>(const Terms<F>&);                                              \
   template int run_phase<F>(PhaseArgs<F>&, HostTranscript&, uint8_t*, uint8_t*, F::T*,         \
                             cudaStream_t);                                                    \

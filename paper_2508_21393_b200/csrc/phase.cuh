@@ -39,6 +39,10 @@ struct PhaseArgs {
   // variables are above the tiled tables' index bits.
   int rounds_limit = 0;
   int forced_shape = -1;
+  // LOGUP_TILED host finishing: the eq point u (num_vars, storage form) and
+  // the table-side constants K3 = sum_ti B T eq_lo, SMB = sum_ti M B
+  const T* lq_u = nullptr;
+  T lq_k3, lq_smb;
   // one-launch-per-round mode (profilers): finals are kept here
   bool stepwise = false;
   std::vector<T> fin_cache;

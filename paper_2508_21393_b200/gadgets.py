@@ -375,7 +375,8 @@ def prove_pair_lookup(label, x, y, pair_table, key, tr, rng):
     multiplicities and the whole lookup stay on the GPU (DeviceVector
     entries); otherwise the reference's list semantics apply.
     """
-    from .lookup import LookupTable, SecretVector, compute_multiplicities, prove_lookup
+    from .lookup import (LookupTable, SecretVector, compute_multiplicities,
+                         multiplicities_indexed, prove_lookup)
 
     p = tr.modulus
     tr.append(label + b"/x", x.ref.digest(key.group))
@@ -403,5 +404,8 @@ def prove_pair_lookup(label, x, y, pair_table, key, tr, rng):
         table = LookupTable(tuple((a + alpha * b) % p for a, b in
                                   zip(pair_table.x.entries, pair_table.y.entries)),
                             table_com, pair_table.name + "+a*y")
+    if isinstance(secret.entries, D.DeviceVector):
+        counts, index = multiplicities_indexed(secret.entries, table)
+        return prove_lookup(secret, counts, table, key, tr, rng, secret_index=index)
     counts = compute_multiplicities(secret.entries, table)
     return prove_lookup(secret, counts, table, key, tr, rng)

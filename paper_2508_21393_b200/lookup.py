@@ -99,18 +99,52 @@ def _check_canonical(values, p, what):
         raise NotImplementedError("%s must be canonical residues for the GPU path" % what)
 
 
-def multiplicities_device(secret_buf, d, table_buf, n, spec):
-    """Device histogram; returns (uint32 counts tensor, first_miss or None)."""
+def multiplicities_device(secret_buf, d, table_buf, n, spec, index=None):
+    """Device histogram; returns (uint32 counts tensor, first_miss or None).
+    `index` (int32 tensor of d entries) also receives each secret entry's
+    table index."""
     import torch
 
     counts = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
     fm = ctypes.c_int64(-1)
-    rc = N.lib().zkl_multiplicities(spec.fid, D.ptr(secret_buf), d, D.ptr(table_buf), n,
-                                    D.ptr(counts), ctypes.byref(fm), D.stream())
+    if index is None:
+        rc = N.lib().zkl_multiplicities(spec.fid, D.ptr(secret_buf), d, D.ptr(table_buf), n,
+                                        D.ptr(counts), ctypes.byref(fm), D.stream())
+    else:
+        rc = N.lib().zkl_multiplicities_index(spec.fid, D.ptr(secret_buf), d, D.ptr(table_buf),
+                                              n, D.ptr(counts), D.ptr(index), ctypes.byref(fm),
+                                              D.stream())
     if rc == N.ZKL_ERR_MISSING:
         return counts, fm.value
     N.check(rc)
     return counts, None
+
+
+def multiplicities_indexed(secret, table):
+    """compute_multiplicities for device-resident entries, plus the table
+    index of every secret entry (a uint32 device tensor of len(secret)).
+    Raises ElementNotInTable like the reference (lookup.py:96-98)."""
+    import torch
+
+    spec = secret.spec
+    sbuf = D.field_buffer(secret, spec)
+    tbuf = D.field_buffer(table.entries, spec)
+    d, n = len(secret), len(table.entries)
+    index = torch.empty(max(d, 1), dtype=torch.int32, device="cuda")
+    counts, miss = multiplicities_device(sbuf, d, tbuf, n, spec, index=index)
+    if miss is not None:
+        raise TYPES["ElementNotInTable"](miss, D.read_scalar(sbuf, spec, miss))
+    out = D.empty(spec, n)
+    N.check(N.lib().zkl_lift_u32(spec.fid, D.ptr(out), D.ptr(counts), n, D.stream()))
+    return D.DeviceVector(out, n, spec), index
+
+
+def _gather(spec, src, src_n, index, n, add=None):
+    out = D.empty(spec, n)
+    N.check(N.lib().zkl_gather(spec.fid, D.ptr(out), D.ptr(src), src_n, D.ptr(index), n,
+                               D.scalar_bytes(add, spec) if add is not None else None,
+                               D.stream()))
+    return out
 
 
 def compute_multiplicities(secret_entries, table, modulus=None):
@@ -167,8 +201,15 @@ def _expand(spec, dst_n, src, src_n, mode, add=None, pad=None):
     return out
 
 
-def prove_lookup(secret, multiplicities, table, key, tr, rng):
-    """Drop-in for zklora.lookup.prove_lookup (lookup.py:143-251)."""
+def prove_lookup(secret, multiplicities, table, key, tr, rng, secret_index=None):
+    """Drop-in for zklora.lookup.prove_lookup (lookup.py:143-251).
+
+    secret_index (optional, from multiplicities_indexed): the table index of
+    every secret entry.  The secret-side column 1/(beta + s_i) is then
+    gathered from the table-side inversion instead of inverting d entries;
+    since every s_i equals t_index(i), beta hits a secret pole only if it
+    hits a table pole, so the retry decisions of lookup.py:163-171 are
+    unchanged."""
     p = tr.modulus
     spec = D.spec_for(p)
     group = key.group
@@ -198,10 +239,16 @@ def prove_lookup(secret, multiplicities, table, key, tr, rng):
     retries = 0
     beta = tr.challenge(b"lookup/beta")
     while True:
-        inv_s, z1 = batch_inverse_device(s_buf, d, spec, add=beta)
-        z2 = None
-        if z1 is None:
+        if secret_index is not None:
+            z1 = None
             inv_t, z2 = batch_inverse_device(t_buf, n, spec, add=beta)
+            if z2 is None:
+                inv_s = _gather(spec, inv_t, n, secret_index, d)
+        else:
+            inv_s, z1 = batch_inverse_device(s_buf, d, spec, add=beta)
+            z2 = None
+            if z1 is None:
+                inv_t, z2 = batch_inverse_device(t_buf, n, spec, add=beta)
         if z1 is None and z2 is None:
             break
         retries += 1
@@ -239,7 +286,7 @@ def prove_lookup(secret, multiplicities, table, key, tr, rng):
     # is never materialised -- tiled rounds first, then 7 tables of n entries
     if d > n > 1 and TILED and native_transcript(tr, spec):
         tiled = _tiled_sumcheck(spec, tr, d, n, s_buf, inv_s, t_buf, inv_t, m_buf, beta, u,
-                                terms, tuples, claimed, num_vars)
+                                terms, tuples, claimed, num_vars, secret_index)
         if tiled is not None:
             rounds, point, finals = tiled
             return _finish_lookup(spec, p, key, be, stub, tr, rng, secret, table, multiplicities,
@@ -280,21 +327,25 @@ TILED = True  # tests flip this to compare with the fully materialised claim
 
 
 def _tiled_sumcheck(spec, tr, d, n, s_buf, inv_s, t_buf, inv_t, m_buf, beta, u, terms, tuples,
-                    claimed, num_vars):
-    """zkl_logup_tiled_rounds for the high log2(d/n) variables, then the
-    remaining log2(n) rounds over 7 tables of n entries (indicator = ones).
-    Returns None (nothing consumed, transcript untouched) when the native
-    engine declines (stepwise mode under profilers)."""
+                    claimed, num_vars, secret_index=None):
+    """zkl_logup_tiled_rounds for the high log2(d/n) variables (the replicated
+    table side and the eq table are never materialised), then the remaining
+    log2(n) rounds over 7 tables of n entries (indicator = ones).  Returns
+    None (nothing consumed, transcript untouched) when the native engine
+    declines (stepwise mode under profilers, n < 32)."""
     tile_log = (n - 1).bit_length()
     r1 = num_vars - tile_log
-    E = D.eq_table(u, spec)
     # inv_s / inv_t are consumed in place: with d > n the openings use the
     # sumcheck finals, and the commitment path downloaded them already
     A = inv_s
-    Sb = _expand(spec, d, s_buf, d, 1, add=beta)
-    Bb = inv_t
     Tb = _expand(spec, n, t_buf, n, 1, add=beta)
+    if secret_index is not None:  # s_i + beta == t_index(i) + beta
+        Sb = _gather(spec, Tb, n, secret_index, d)
+    else:
+        Sb = _expand(spec, d, s_buf, d, 1, add=beta)
+    Bb = inv_t
     Mb = m_buf.clone()  # may be the caller's DeviceVector buffer
+    E = D.empty(spec, n)
     nb = spec.nbytes
     before = bytes(tr.state)
     absorb_claim(tr, claimed, terms, 3, num_vars)
@@ -303,8 +354,9 @@ def _tiled_sumcheck(spec, tr, d, n, s_buf, inv_s, t_buf, inv_t, m_buf, beta, u, 
     pbuf = (ctypes.c_uint8 * (r1 * nb))()
     ptrs = (ctypes.c_void_p * 6)(*[t.data_ptr() for t in (E, A, Sb, Bb, Tb, Mb)])
     coeffs = D.scalars_bytes([t.coefficient for t in terms], spec)
-    rc = N.lib().zkl_logup_tiled_rounds(spec.fid, ptrs, tile_log, num_vars, r1, coeffs, state,
-                                        rbuf, pbuf, D.stream())
+    ub = D.scalars_bytes(list(u), spec)
+    rc = N.lib().zkl_logup_tiled_rounds(spec.fid, ptrs, tile_log, num_vars, r1, ub, coeffs, 1,
+                                        state, rbuf, pbuf, D.stream())
     if rc == N.ZKL_ERR_UNSUPPORTED:
         tr.state = before
         log = getattr(tr, "log", None)
@@ -320,7 +372,7 @@ def _tiled_sumcheck(spec, tr, d, n, s_buf, inv_s, t_buf, inv_t, m_buf, beta, u, 
     if log is not None:
         log.extend((b"sumcheck/eval", (e.bit_length() + 7) // 8 or 1) for e in flat)
     ind = _expand(spec, n, None, n, 0, add=1, pad=0)
-    r2, p2, finals = run_rounds(spec, [E[:n], A[:n], Sb[:n], ind, Bb, Tb, Mb], tile_log, tuples,
+    r2, p2, finals = run_rounds(spec, [E, A[:n], Sb[:n], ind, Bb, Tb, Mb], tile_log, tuples,
                                 3, tr)
     return rounds + r2, point + p2, finals
 

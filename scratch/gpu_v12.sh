@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gputest_v12.log 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/gputest_v12.log
+timeout 600 python bench.py > gpurun_out/bench_v12.json 2> gpurun_out/bench_v12.err; echo "bench rc=$?"
+python -c "
+import json;d=json.loads(open('gpurun_out/bench_v12.json').read().strip().splitlines()[-1])
+print(d['ms_per_step'], d['e2e']['value'], d['cfg3']['ms_per_proof'], d['cfg3']['sumcheck_ms_per_proof'])"

@@ -495,6 +495,83 @@ def test_lookup_tiled_matches_materialised(field, d, n, monkeypatch):
     assert out[0] == out[1]
 
 
+def _indexed_lookup_proofs(p, table, secret_vals, monkeypatch, label=b"x"):
+    """One proof per (tiled, indexed) combination over device-resident entries."""
+    from paper_2508_21393_b200 import lookup as L
+
+    spec = D.spec_for(p)
+    d, n = len(secret_vals), len(table)
+    tab = zb.LookupTable(D.DeviceVector(D.upload(table, spec), n, spec), StubCommitment(
+        (n - 1).bit_length()))
+    secret = zb.SecretVector(D.DeviceVector(D.upload(secret_vals, spec), d, spec),
+                             StubCommitment((d - 1).bit_length()), ())
+    out = []
+    for tiled in (True, False):
+        for indexed in (False, True):
+            monkeypatch.setattr(L, "TILED", tiled)
+            t = Transcript(b"tiled", p, label)
+            if indexed:
+                m, index = L.multiplicities_indexed(secret.entries, tab)
+                pr = zb.prove_lookup(secret, m, tab, KEY, t, RNG, secret_index=index)
+            else:
+                m = zb.compute_multiplicities(secret.entries, tab)
+                pr = zb.prove_lookup(secret, m, tab, KEY, t, RNG)
+            out.append((pr.beta_retries, [r.evaluations for r in pr.sumcheck.rounds],
+                        pr.sumcheck.final_values, pr.secret_values, pr.table_values, t.state))
+    return out
+
+
+@pytest.mark.parametrize("field", ["big", "test"])
+@pytest.mark.parametrize("d,n", [(1 << 16, 1 << 10), (1 << 8, 1 << 12), (1 << 12, 1 << 12)])
+def test_lookup_indexed_matches_plain(field, d, n, monkeypatch):
+    """Secret-side columns gathered through the multiplicity index (no
+    d-entry inversion) give the same proofs as inverting the secret, on the
+    tiled and the materialised path; the table holds duplicate values (the
+    index points at the last one, lookup.py:94)."""
+    p = FIELDS[field]
+    rnd = np.random.default_rng(d * 3 + n)
+    table = [int(v) for v in rnd.integers(0, 2**40, size=n)]
+    table[1] = table[n - 1]
+    table[2] = table[n // 2]
+    sec = [table[int(i)] for i in rnd.integers(0, n, size=d)]
+    sec[0] = table[1]
+    out = _indexed_lookup_proofs(p, table, sec, monkeypatch)
+    assert all(o == out[0] for o in out[1:])
+
+
+def test_lookup_indexed_pole_retry(monkeypatch):
+    """beta landing on a pole (beta + t_j == 0, with t_j also a secret entry):
+    the indexed path retries exactly like the plain one (lookup.py:163-171)."""
+    p = P_BIG
+    rnd = np.random.default_rng(77)
+    n, d = 1 << 8, 1 << 12
+    table = [int(v) for v in rnd.integers(0, 2**40, size=n)]
+    sec = [table[int(i)] for i in rnd.integers(0, n, size=d)]
+
+    betas = []
+
+    class _Capture(Transcript):
+        def challenge(self, label):
+            v = super().challenge(label)
+            if label == b"lookup/beta":
+                betas.append(v)
+            return v
+
+    spec = D.spec_for(p)
+    tab = zb.LookupTable(D.DeviceVector(D.upload(table, spec), n, spec), StubCommitment(8))
+    secret = zb.SecretVector(D.DeviceVector(D.upload(sec, spec), d, spec), StubCommitment(12), ())
+    t = _Capture(b"tiled", p, b"pole")
+    zb.prove_lookup(secret, zb.compute_multiplicities(secret.entries, tab), tab, KEY, t, RNG)
+    pole = (p - betas[0]) % p  # the stub commitments do not depend on the entries
+    old = table[5]
+    table[5] = pole
+    sec = [table[6] if v == old else v for v in sec]
+    sec[100] = pole
+    out = _indexed_lookup_proofs(p, table, sec, monkeypatch, label=b"pole")
+    assert out[0][0] >= 1
+    assert all(o == out[0] for o in out[1:])
+
+
 def test_multiplicities_golden():
     for c in load_golden("lookup.json")["multiplicities"]:
         table = zb.LookupTable(tuple(c["table"]), None)

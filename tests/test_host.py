@@ -32,7 +32,7 @@ def test_library_loads_and_exports_header_symbols():
     for name in declared:
         assert hasattr(lib, name), name
     assert set(declared) == set(N.EXPORTS)
-    assert lib.zkl_abi_version() == 2
+    assert lib.zkl_abi_version() == 3
     assert lib.zkl_elem_bytes(0) == 32 and lib.zkl_elem_bytes(1) == 8
     assert lib.zkl_elem_bytes(7) < 0
 
