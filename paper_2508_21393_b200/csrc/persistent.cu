@@ -447,11 +447,15 @@ struct EvLogup {
 // P_1 = 1: two products per pair.
 // Tables: [eq_hi (all rounds, round j's 2^(r-1-j) entries at offset
 // 2^(r-1-j) - 1), A, S + beta, eq_lo (2^tile_log)].
+#ifndef ZKL_TILED_MINB
+#define ZKL_TILED_MINB 2
+#endif
 template <class F, int MAXK>
 struct EvLogupTiled {
   using T = typename F::T;
   static constexpr bool kGeneric = false;
   static constexpr bool kTiled = true;
+  static constexpr int kMinBlocks = ZKL_TILED_MINB;
   static constexpr int NA = 5, NOUT = 5;
   ZKL_D static void accumulate(const TablePtrs<F, MAXK>& tabs, uint64_t half, bool fold,
                                const T& r, const Terms<F>& tm, uint64_t gtid,
@@ -532,6 +536,18 @@ struct EvLogupTiled {
     for (int q = 0; q < NOUT; q++) out[q] = acc[q];
   }
   ZKL_D static T lane(const T&, int, int, bool, const Terms<F>&) { return F::zero(); }
+};
+
+// blocks per SM the grid kernel is compiled for (register budget): 2 for
+// evaluators whose per-pair state fits 128 registers, so two blocks share an
+// SM and hide the Montgomery carry-chain latency
+template <class EV>
+struct MinBlocks {
+  template <class U>
+  static constexpr int test(decltype(U::kMinBlocks)*) { return U::kMinBlocks; }
+  template <class U>
+  static constexpr int test(...) { return 1; }
+  static constexpr int value = test<EV>(nullptr);
 };
 
 template <class EV>
@@ -811,7 +827,7 @@ ZKL_D void publish_finals(const TablePtrs<F, MAXK>& tabs, int k, const typename 
 // challenge and relays it through an L2 slot.  When j1 < num_vars the
 // remaining rounds continue in the cluster kernel (no finals here).
 template <class F, int MAXK, class EV>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, MinBlocks<EV>::value)
     k_sumcheck_persistent(TablePtrs<F, MAXK> tabs, int k, int num_vars, int j0, int j1,
                           Terms<F> tm, Mailbox* mb, typename Red<F>::W* partials,
                           unsigned* ticket, uint64_t* bcast, unsigned* fail, uint32_t seq0,
