@@ -182,3 +182,43 @@ def pair_combine(x, y, alpha, spec):
                                      _INT_TYPES[y.dtype], n, scalar_bytes(alpha, spec),
                                      stream()))
     return DeviceVector(out, n, spec)
+
+
+class Staged:
+    """Host -> device staging on a copy stream: `stage(host_tensors)` queues
+    the copies (pinned host memory: truly asynchronous on the copy engine)
+    and returns the device tensors; `ready(i)` makes the current stream wait
+    for item i only.  A caller proving a batch of claims stages them all up
+    front and proves claim i as soon as its own operands have landed, so the
+    PCIe transfer of claim i+1 overlaps the proof of claim i."""
+
+    def __init__(self):
+        import torch
+
+        self.torch = torch
+        self.copy = torch.cuda.Stream()
+
+    def stage(self, groups, out=None):
+        """groups: list of tuples of pinned host tensors -> list of tuples of
+        device tensors (reusing `out`'s buffers when given)."""
+        torch = self.torch
+        start = torch.cuda.Event()
+        start.record(torch.cuda.current_stream())
+        self.events = []
+        dev = []
+        with torch.cuda.stream(self.copy):
+            self.copy.wait_event(start)  # after the caller's earlier work
+            for g, grp in enumerate(groups):
+                bufs = out[g] if out is not None else tuple(
+                    torch.empty_like(h, device="cuda") for h in grp)
+                for d, h in zip(bufs, grp):
+                    d.copy_(h, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.copy)
+                self.events.append(ev)
+                dev.append(bufs)
+        return dev
+
+    def ready(self, i):
+        self.torch.cuda.current_stream().wait_event(self.events[i])
+
