@@ -442,7 +442,7 @@ struct EvLogup {
 // q_0 = a0 s0, q_1 = a1 s1, q_2 = (a1 - a0)(s1 - s0) (A S at x = 0, 1 and
 // its x^2 coefficient) plus sum a0 and sum (a1 - a0); the host builds the
 // four evaluations.  Per pair: 4 products to fold A, S, 3 for q, 3 for the
-// eq_hi weights (the eq_lo weight is applied once per (ti, k-slice) unit).
+// eq_hi weights (the eq_lo weight is applied once per run of one ti block).
 // In round 0, when A = 1/S entrywise (tm.inv_pair), q_0 = q_1 = 1 and P_0 =
 // P_1 = 1: two products per pair.
 // Tables: [eq_hi (all rounds, round j's 2^(r-1-j) entries at offset
@@ -461,65 +461,27 @@ struct EvLogupTiled {
                                const T& r, const Terms<F>& tm, uint64_t gtid,
                                uint64_t nthreads, T (&acc)[NA]) {
     const int tl = tm.tile_log;
-    const uint64_t K = half >> tl;            // pairs per low index ti
-    const int s_log = K >= 8 ? 3 : (K >= 4 ? 2 : (K >= 2 ? 1 : 0));
-    const uint64_t S = 1ull << s_log;         // k-slices per ti block
-    const int nblk_log = tl - 5;               // blocks of 32 consecutive ti
-    const uint64_t units = S << nblk_log;
-    const uint64_t nw = nthreads >> 5;
+    const uint64_t K = half >> tl;  // pairs per low index ti (a power of two)
+    const int k_log = 63 - __clzll(K);
+    // warp-steps (a block of 32 consecutive ti, one k) in ti-block-major
+    // order, split into equal contiguous ranges per warp; a warp crosses few
+    // ti blocks, so the eq_lo weight is applied at only a few flushes per
+    // warp.  (Handing out chunks from an atomic counter measured no faster:
+    // the SM is issue-bound, and the second block on an SM finishing after
+    // the first is just the scheduler's order within the same total.)
+    const uint64_t steps = (1ull << (tl - 5)) << k_log;
+    const uint64_t nw = nthreads >> 5, gw = gtid >> 5;
+    const uint64_t f0 = steps * gw / nw, f1 = steps * (gw + 1) / nw;
     const int lane = threadIdx.x & 31;
     const T* eh = tabs.t[0] + (K - 1);
     const T* A = tabs.t[1];
     const T* Sb = tabs.t[2];
     const T* el = tabs.t[3];
     const bool inv0 = !fold && tm.inv_pair;
-    for (uint64_t u = gtid >> 5; u < units; u += nw) {
-      const uint64_t ti = ((u & ((1ull << nblk_log) - 1)) << 5) | lane;
-      T p0 = F::zero(), p1 = F::zero(), p2 = F::zero();
-      for (uint64_t kk = u >> nblk_log; kk < K; kk += S) {
-        const uint64_t i = (kk << tl) | ti;
-        T a0, ad, s0, sd;
-        if (fold) {
-          T* At = tabs.t[1];
-          T* St = tabs.t[2];
-          const T xa = ld_cg(At + i), ya = ld_cg(At + i + half);
-          const T xs = ld_cg(St + i), ys = ld_cg(St + i + half);
-          T da = F::sub(ld_cg(At + i + 2 * half), xa), db = F::sub(ld_cg(At + i + 3 * half), ya);
-          T ds = F::sub(ld_cg(St + i + 2 * half), xs), dt = F::sub(ld_cg(St + i + 3 * half), ys);
-          F::mul4r(r, da, db, ds, dt);
-          a0 = F::add(xa, da);
-          const T a1 = F::add(ya, db);
-          s0 = F::add(xs, ds);
-          const T s1 = F::add(ys, dt);
-          At[i] = a0;
-          At[i + half] = a1;
-          St[i] = s0;
-          St[i + half] = s1;
-          ad = F::sub(a1, a0);
-          sd = F::sub(s1, s0);
-        } else {
-          a0 = ld_cg(A + i);
-          ad = F::sub(ld_cg(A + i + half), a0);
-          s0 = ld_cg(Sb + i);
-          sd = F::sub(ld_cg(Sb + i + half), s0);
-        }
-        acc[3] = F::add(acc[3], a0);
-        acc[4] = F::add(acc[4], ad);
-        const T w = eh[kk];
-        if (inv0) {
-          T q2 = F::mul(ad, sd);
-          p2 = F::add(p2, F::mul(w, q2));
-        } else {
-          const T a1 = F::add(a0, ad), s1 = F::add(s0, sd);
-          T q0, q1, q2;
-          F::mul3(a0, s0, a1, s1, ad, sd, q0, q1, q2);
-          F::mul3(w, q0, w, q1, w, q2, q0, q1, q2);
-          p0 = F::add(p0, q0);
-          p1 = F::add(p1, q1);
-          p2 = F::add(p2, q2);
-        }
-      }
-      const T wl = el[ti];
+    T p0 = F::zero(), p1 = F::zero(), p2 = F::zero();
+    uint64_t cur = ~0ull;
+    auto flush = [&](uint64_t tib) {
+      const T wl = el[(tib << 5) | lane];
       if (inv0) {
         acc[2] = F::add(acc[2], F::mul(wl, p2));
       } else {
@@ -528,7 +490,57 @@ struct EvLogupTiled {
         acc[1] = F::add(acc[1], p1);
         acc[2] = F::add(acc[2], p2);
       }
+      p0 = p1 = p2 = F::zero();
+    };
+    for (uint64_t f = f0; f < f1; f++) {
+      const uint64_t tib = f >> k_log, kk = f & (K - 1);
+      if (tib != cur) {
+        if (cur != ~0ull) flush(cur);
+        cur = tib;
+      }
+      const uint64_t i = (kk << tl) | (tib << 5) | lane;
+      T a0, ad, s0, sd;
+      if (fold) {
+        T* At = tabs.t[1];
+        T* St = tabs.t[2];
+        const T xa = ld_cg(At + i), ya = ld_cg(At + i + half);
+        const T xs = ld_cg(St + i), ys = ld_cg(St + i + half);
+        T da = F::sub(ld_cg(At + i + 2 * half), xa), db = F::sub(ld_cg(At + i + 3 * half), ya);
+        T ds = F::sub(ld_cg(St + i + 2 * half), xs), dt = F::sub(ld_cg(St + i + 3 * half), ys);
+        F::mul4r(r, da, db, ds, dt);
+        a0 = F::add(xa, da);
+        const T a1 = F::add(ya, db);
+        s0 = F::add(xs, ds);
+        const T s1 = F::add(ys, dt);
+        At[i] = a0;
+        At[i + half] = a1;
+        St[i] = s0;
+        St[i + half] = s1;
+        ad = F::sub(a1, a0);
+        sd = F::sub(s1, s0);
+      } else {
+        a0 = ld_cg(A + i);
+        ad = F::sub(ld_cg(A + i + half), a0);
+        s0 = ld_cg(Sb + i);
+        sd = F::sub(ld_cg(Sb + i + half), s0);
+      }
+      acc[3] = F::add(acc[3], a0);
+      acc[4] = F::add(acc[4], ad);
+      const T w = eh[kk];
+      if (inv0) {
+        T q2 = F::mul(ad, sd);
+        p2 = F::add(p2, F::mul(w, q2));
+      } else {
+        const T a1 = F::add(a0, ad), s1 = F::add(s0, sd);
+        T q0, q1, q2;
+        F::mul3(a0, s0, a1, s1, ad, sd, q0, q1, q2);
+        F::mul3(w, q0, w, q1, w, q2, q0, q1, q2);
+        p0 = F::add(p0, q0);
+        p1 = F::add(p1, q1);
+        p2 = F::add(p2, q2);
+      }
     }
+    if (cur != ~0ull) flush(cur);
   }
   ZKL_D static void pair(T (&)[MAXK], const T (&)[MAXK], int, const Terms<F>&, T (&)[NA]) {}
   ZKL_D static void finish(const T (&acc)[NA], T (&out)[NOUT]) {
@@ -850,11 +862,18 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<EV>::value)
     const bool fold = j > 0;
     const bool tr0 = trace && blockIdx.x == 0 && threadIdx.x == 0;
     if (tr0) trace[j * 8 + 0] = globaltimer();
+    const uint64_t tb0 = trace ? globaltimer() : 0;
     const uint64_t half = 1ull << (num_vars - 1 - j);
     const int Lr = (L > 0 && half * (uint64_t)L <= nthreads) ? L : 0;
     accumulate_round<F, MAXK, EV>(tabs, k, tm, half, fold, r, Lr, gtid, nthreads, wsum);
     if (tr0) trace[j * 8 + 1] = globaltimer();
     __syncthreads();
+    if (trace && threadIdx.x == 0) {  // per-block accumulate time and SM (ZKL_TRACE)
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      trace[(size_t)num_vars * 8 + ((size_t)j * G + blockIdx.x) * 2] = globaltimer() - tb0;
+      trace[(size_t)num_vars * 8 + ((size_t)j * G + blockIdx.x) * 2 + 1] = smid;
+    }
     if (warp == 0) {
       W v[EV::NOUT];
       block_total<F, EV::NOUT>(wsum, nwarps, v);
@@ -992,11 +1011,18 @@ __global__ void __launch_bounds__(kClusterThreads)
     const bool fold = j > 0;
     const bool tr0 = trace && rank == 0 && threadIdx.x == 0;
     if (tr0) trace[j * 8 + 0] = globaltimer();
+    const uint64_t tb0 = trace ? globaltimer() : 0;
     const uint64_t half = 1ull << (num_vars - 1 - j);
     const int Lr = (L > 0 && half * (uint64_t)L <= nthreads) ? L : 0;
     accumulate_round<F, MAXK, EV>(tabs, k, tm, half, fold, r, Lr, gtid, nthreads, wsum);
     if (tr0) trace[j * 8 + 1] = globaltimer();
     __syncthreads();
+    if (trace && threadIdx.x == 0) {  // per-block accumulate time and SM (ZKL_TRACE)
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      trace[(size_t)num_vars * 8 + ((size_t)j * gridDim.x + blockIdx.x) * 2] = globaltimer() - tb0;
+      trace[(size_t)num_vars * 8 + ((size_t)j * gridDim.x + blockIdx.x) * 2 + 1] = smid;
+    }
     if (warp == 0) {
       W v[EV::NOUT];
       block_total<F, EV::NOUT>(wsum, nwarps, v);
@@ -1436,7 +1462,7 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
   uint64_t* trace = nullptr;
   std::vector<double> h_seen, h_sent;
   if (tracing) {
-    ZKL_CUDA(cudaMalloc(&trace, (size_t)n * 8 * 8));
+    ZKL_CUDA(cudaMalloc(&trace, (size_t)n * 8 * 8 + (size_t)n * 2 * 8 * 4096));
     ZKL_CUDA(cudaMemsetAsync(trace, 0, (size_t)n * 8 * 8, s));
     h_seen.resize(n);
     h_sent.resize(n);
@@ -1597,6 +1623,18 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
     std::vector<uint64_t> tv((size_t)n * 8);
     cudaMemcpyAsync(tv.data(), trace, tv.size() * 8, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
+    if (getenv("ZKL_TRACE")[0] == '3' && pl.j_switch > 0) {  // per-block accumulate times
+      const int G = pl.grid, jn = pl.j_switch < n ? pl.j_switch : n;
+      std::vector<uint64_t> bt((size_t)jn * G * 2);
+      cudaMemcpy(bt.data(), trace + (size_t)a.num_vars * 8, bt.size() * 8, cudaMemcpyDeviceToHost);
+      for (int j = 0; j < jn; j++) {
+        fprintf(stderr, "[zkl trace] round %d block us (block:sm:us):", j);
+        for (int b = 0; b < G; b++)
+          fprintf(stderr, " %d:%d:%.0f", b, (int)bt[((size_t)j * G + b) * 2 + 1],
+                  bt[((size_t)j * G + b) * 2] / 1e3);
+        fprintf(stderr, "\n");
+      }
+    }
     cudaFree(trace);
     double acc[5] = {0}, hs = 0, loop = 0, hgap = 0, hfill = 0;
     for (int j = 0; j < n; j++) {
@@ -1609,6 +1647,10 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
       acc[3] += t[4] ? (t[4] - (t[3] ? t[3] : t[2])) / 1e3 : 0;  // wait for challenge
       if (j + 1 < n && t[4]) loop += (tv[(size_t)(j + 1) * 8] - t[4]) / 1e3;
       hs += h_sent[j] - h_seen[j];
+      if (getenv("ZKL_TRACE")[0] == '2')
+        fprintf(stderr, "[zkl trace] round %d: accum %.2f reduce %.2f publish %.2f wait %.2f\n", j,
+                (t[1] - t[0]) / 1e3, (t[2] - t[1]) / 1e3, t[3] ? (t[3] - t[2]) / 1e3 : 0.0,
+                t[4] ? (t[4] - (t[3] ? t[3] : t[2])) / 1e3 : 0.0);
     }
     fprintf(stderr,
             "[zkl trace] n=%d k=%d shape=%d grid=%dx%d->%d cluster=%dx%d per-round us: accum "
