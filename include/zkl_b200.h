@@ -155,6 +155,21 @@ int zkl_multiplicities_index(int field, const void* secret, uint64_t d, const vo
                              uint64_t n, uint32_t* counts, uint32_t* index_out,
                              int64_t* first_miss, void* stream);
 
+/* zkl_multiplicities_index for a pair lookup (gadgets.py:679-688) whose table
+ * x column is the consecutive range table_x0 .. table_x0 + n - 1
+ * (tables.py:142-152): query i with 0 <= x[i] - table_x0 < n and
+ * y[i] == table_y[x[i] - table_x0] is binned directly; every other query is
+ * looked up by its combined value secret[i] = x[i] + alpha y[i].  x, y:
+ * ZKL_MT_I16 / ZKL_MT_I32 device columns of d entries; table_y: int32, n
+ * entries; table: the combined table (n field elements).  Same outputs and
+ * errors as zkl_multiplicities_index; ZKL_ERR_UNSUPPORTED (nothing written
+ * but the hash slots) when the combined table has duplicate values or the
+ * column types are not int16/int32. */
+int zkl_pair_multiplicities(int field, const void* x, int x_type, const void* y, int y_type,
+                            uint64_t d, int64_t table_x0, const int32_t* table_y,
+                            const void* secret, const void* table, uint64_t n, uint32_t* counts,
+                            uint32_t* index_out, int64_t* first_miss, void* stream);
+
 /* dst[i] = src[idx[i]] (+ add when add_canon != NULL), i < n; every idx[i]
  * must be < src_n (caller-checked).  The secret-side logUp columns
  * (lookup.py:175-202) of a lookup whose secret entries are table entries. */

@@ -26,7 +26,7 @@ EXPORTS = (
     "zkl_matvec", "zkl_expand", "zkl_lift_u32", "zkl_launch_count", "zkl_sumcheck_prove",
     "zkl_shake256", "zkl_transcript_append", "zkl_transcript_challenge", "zkl_matmul_prove",
     "zkl_prof_enable", "zkl_prof_collect", "zkl_pair_combine", "zkl_logup_tiled_rounds",
-    "zkl_multiplicities_index", "zkl_gather",
+    "zkl_multiplicities_index", "zkl_gather", "zkl_pair_multiplicities",
 )
 
 
@@ -80,6 +80,8 @@ _SIGS = {
     "zkl_multiplicities_index": ([_i32, _vp, _u64, _vp, _u64, _vp, _vp, _i64p, _vp],
                                  ctypes.c_int),
     "zkl_gather": ([_i32, _vp, _vp, _u64, _vp, _u64, _u8p, _vp], ctypes.c_int),
+    "zkl_pair_multiplicities": ([_i32, _vp, _i32, _vp, _i32, _u64, ctypes.c_int64, _vp, _vp, _vp,
+                                 _u64, _vp, _vp, _i64p, _vp], ctypes.c_int),
     "zkl_pair_combine": ([_i32, _vp, _vp, _i32, _vp, _i32, _u64, _u8p, _vp], ctypes.c_int),
     "zkl_prof_collect": ([_i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                           ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)],

@@ -256,6 +256,13 @@ int zkl_multiplicities_index(int field, const void* secret, uint64_t d, const vo
   D(field, op_multiplicities<F>(secret, d, table, n, counts, first_miss, (cudaStream_t)stream,
                                 index_out));
 }
+int zkl_pair_multiplicities(int field, const void* x, int x_type, const void* y, int y_type,
+                            uint64_t d, int64_t table_x0, const int32_t* table_y,
+                            const void* secret, const void* table, uint64_t n, uint32_t* counts,
+                            uint32_t* index_out, int64_t* first_miss, void* stream) {
+  D(field, op_pair_multiplicities<F>(x, x_type, y, y_type, d, table_x0, table_y, secret, table, n,
+                                     counts, index_out, first_miss, (cudaStream_t)stream));
+}
 int zkl_gather(int field, void* dst, const void* src, uint64_t src_n, const uint32_t* idx,
                uint64_t n, const uint8_t* add_canon, void* stream) {
   D(field, op_gather<F>(dst, src, src_n, idx, n, scalar<F>(add_canon), add_canon != nullptr,

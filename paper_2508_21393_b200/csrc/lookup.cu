@@ -31,7 +31,7 @@ constexpr uint32_t kEmpty = 0xffffffffu;
 
 template <class F>
 __global__ void k_ht_insert(const typename F::T* table, uint32_t n, uint32_t* slots,
-                            uint32_t mask) {
+                            uint32_t mask, unsigned* dup) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     typename F::T v = table[j];
     uint32_t h = hash_elem(v) & mask;
@@ -40,11 +40,34 @@ __global__ void k_ht_insert(const typename F::T* table, uint32_t n, uint32_t* sl
       if (old == kEmpty) break;
       if (F::eq(table[old], v)) {  // duplicate value: keep the last index
         atomicMax(&slots[h], j);
+        if (dup) atomicOr(dup, 1u);
         break;
       }
       h = (h + 1) & mask;
     }
   }
+}
+
+// Count one warp's hits.  Equal hits are merged with __match_any_sync (one
+// atomicAdd per distinct bin); a warp whose 32 hits share one bin keeps a
+// running count instead, flushed when its bin changes -- the zero padding of
+// a lookup (millions of queries on one bin) would otherwise serialise on one
+// counter.
+ZKL_D void count_hit(uint32_t hit, uint32_t* counts, uint32_t& run_bin, uint32_t& run_cnt) {
+  const unsigned peers = __match_any_sync(kFull, hit);
+  if (peers == kFull) {
+    if (hit == kEmpty) return;  // no lane hit (tail of the range, or all missed)
+    if (hit == run_bin) {
+      run_cnt += 32;
+    } else {
+      if (run_cnt && (threadIdx.x & 31) == 0) atomicAdd(&counts[run_bin], run_cnt);
+      run_bin = hit;
+      run_cnt = 32;
+    }
+    return;
+  }
+  const int leader = __ffs(peers) - 1;
+  if (hit != kEmpty && (threadIdx.x & 31) == leader) atomicAdd(&counts[hit], __popc(peers));
 }
 
 // One probe per secret entry; equal hits inside a warp are merged with
@@ -56,6 +79,7 @@ __global__ void k_ht_count(const typename F::T* secret, uint64_t d, const typena
                            const uint32_t* slots, uint32_t mask, uint32_t* counts,
                            unsigned long long* first_miss, uint32_t* index_out) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t run_bin = kEmpty, run_cnt = 0;  // whole-warp hits on one bin, summed locally
   for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < d; base += stride) {
     const uint64_t i = base + threadIdx.x;
     uint32_t hit = kEmpty;
@@ -70,10 +94,9 @@ __global__ void k_ht_count(const typename F::T* secret, uint64_t d, const typena
       }
     }
     if (index_out != nullptr && i < d) index_out[i] = hit;
-    const unsigned peers = __match_any_sync(kFull, hit);
-    const int leader = __ffs(peers) - 1;
-    if (hit != kEmpty && (threadIdx.x & 31) == leader) atomicAdd(&counts[hit], __popc(peers));
+    count_hit(hit, counts, run_bin, run_cnt);
   }
+  if (run_cnt && (threadIdx.x & 31) == 0) atomicAdd(&counts[run_bin], run_cnt);
 }
 
 template <class F>
@@ -94,7 +117,7 @@ int op_multiplicities(const void* secret, uint64_t d, const void* table, uint64_
   ZKL_CUDA(cudaMemsetAsync(flag, 0xff, 8, s));
   ZKL_CUDA(cudaMemsetAsync(counts, 0, n * 4, s));
   k_ht_insert<F><<<grid_for(n, 256), 256, 0, s>>>((const T*)table, (uint32_t)n, slots,
-                                                   (uint32_t)(cap - 1));
+                                                   (uint32_t)(cap - 1), nullptr);
   ZKL_LAUNCH_CHECK();
   if (d) {
     k_ht_count<F><<<grid_for(d, 256), 256, 0, s>>>((const T*)secret, d, (const T*)table, slots,
@@ -111,6 +134,107 @@ int op_multiplicities(const void* secret, uint64_t d, const void* table, uint64_
   if (fm != ~0ull) { *first_miss = (int64_t)fm; return kErrMissing; }
   return kOk;
 }
+
+// Pair lookups (gadgets.py:679-688) whose table x column is the consecutive
+// range x0 .. x0+n-1 (tables.py:142-152): a query (x_i, y_i) with
+// 0 <= x_i - x0 < n and y_i == table_y[x_i - x0] has s_i = t_(x_i - x0)
+// exactly, so its bin comes from two small integer loads instead of a hash
+// probe on the 32-byte combined value.  Every other query takes the hash
+// probe on s_i (identical semantics: a miss is ElementNotInTable).  Used
+// only when the combined table has no duplicate values (checked here with
+// the hash insert; the reference maps duplicates to the last index).
+template <class F, class TX, class TY>
+__global__ void k_pair_count(const TX* xs, const TY* ys, uint64_t d, int64_t x0,
+                             const int32_t* ty, uint32_t n, const typename F::T* secret,
+                             const typename F::T* table, const uint32_t* slots, uint32_t mask,
+                             uint32_t* counts, unsigned long long* first_miss,
+                             uint32_t* index_out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t run_bin = kEmpty, run_cnt = 0;  // whole-warp hits on one bin, summed locally
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < d; base += stride) {
+    const uint64_t i = base + threadIdx.x;
+    uint32_t hit = kEmpty;
+    if (i < d) {
+      const int64_t xi = (int64_t)xs[i], yi = (int64_t)ys[i];
+      const int64_t idx = xi - x0;
+      if (idx >= 0 && idx < (int64_t)n && (int64_t)__ldg(ty + idx) == yi) {
+        hit = (uint32_t)idx;
+      } else {
+        const typename F::T v = secret[i];
+        uint32_t h = hash_elem(v) & mask;
+        while (true) {
+          const uint32_t e = __ldg(slots + h);
+          if (e == kEmpty) { atomicMin(first_miss, (unsigned long long)i); break; }
+          if (F::eq(table[e], v)) { hit = e; break; }
+          h = (h + 1) & mask;
+        }
+      }
+      if (index_out) index_out[i] = hit;
+    }
+    count_hit(hit, counts, run_bin, run_cnt);
+  }
+  if (run_cnt && (threadIdx.x & 31) == 0) atomicAdd(&counts[run_bin], run_cnt);
+}
+
+template <class F>
+int op_pair_multiplicities(const void* x, int xt, const void* y, int yt, uint64_t d, int64_t x0,
+                           const int32_t* ty, const void* secret, const void* table, uint64_t n,
+                           uint32_t* counts, uint32_t* index_out, int64_t* first_miss,
+                           cudaStream_t s) {
+  using T = typename F::T;
+  *first_miss = -1;
+  if (n == 0 || n > (1ull << 31)) { set_error("pair multiplicities: bad table size"); return kErrArg; }
+  uint64_t cap = 1;
+  while (cap < 2 * n) cap <<= 1;
+  void* ws;
+  int rc = scratch_reserve(cap * 4 + 64, &ws, s);
+  if (rc) return rc;
+  uint32_t* slots = (uint32_t*)ws;
+  unsigned long long* flag = (unsigned long long*)((char*)ws + cap * 4);
+  unsigned* dup = (unsigned*)((char*)ws + cap * 4 + 8);
+  ZKL_CUDA(cudaMemsetAsync(slots, 0xff, cap * 4, s));
+  ZKL_CUDA(cudaMemsetAsync(flag, 0xff, 8, s));
+  ZKL_CUDA(cudaMemsetAsync(dup, 0, 4, s));
+  ZKL_CUDA(cudaMemsetAsync(counts, 0, n * 4, s));
+  k_ht_insert<F><<<grid_for(n, 256), 256, 0, s>>>((const T*)table, (uint32_t)n, slots,
+                                                   (uint32_t)(cap - 1), dup);
+  ZKL_LAUNCH_CHECK();
+  void* pin;
+  if ((rc = pinned_reserve(16, &pin))) return rc;
+  ZKL_CUDA(cudaMemcpyAsync(pin, dup, 4, cudaMemcpyDeviceToHost, s));
+  ZKL_CUDA(cudaStreamSynchronize(s));
+  unsigned has_dup;
+  memcpy(&has_dup, pin, 4);
+  if (has_dup) return kErrUnsupported;  // caller takes the hash path
+  if (d) {
+    const unsigned g = grid_for(d, 256);
+    const T* sec = (const T*)secret;
+    const T* tab = (const T*)table;
+    const uint32_t m = (uint32_t)(cap - 1);
+#define ZKL_PC(TX, TY)                                                                         \
+  k_pair_count<F, TX, TY><<<g, 256, 0, s>>>((const TX*)x, (const TY*)y, d, x0, ty, (uint32_t)n, \
+                                            sec, tab, slots, m, counts, flag, index_out)
+    if (xt == 1 && yt == 1) ZKL_PC(int16_t, int16_t);
+    else if (xt == 1 && yt == 2) ZKL_PC(int16_t, int32_t);
+    else if (xt == 2 && yt == 1) ZKL_PC(int32_t, int16_t);
+    else if (xt == 2 && yt == 2) ZKL_PC(int32_t, int32_t);
+    else { set_error("pair multiplicities: int16/int32 columns only"); return kErrUnsupported; }
+#undef ZKL_PC
+    ZKL_LAUNCH_CHECK();
+  }
+  unsigned long long fm;
+  ZKL_CUDA(cudaMemcpyAsync(pin, flag, 8, cudaMemcpyDeviceToHost, s));
+  ZKL_CUDA(cudaStreamSynchronize(s));
+  memcpy(&fm, pin, 8);
+  if (fm != ~0ull) { *first_miss = (int64_t)fm; return kErrMissing; }
+  return kOk;
+}
+template int op_pair_multiplicities<Fr255>(const void*, int, const void*, int, uint64_t, int64_t,
+                                           const int32_t*, const void*, const void*, uint64_t,
+                                           uint32_t*, uint32_t*, int64_t*, cudaStream_t);
+template int op_pair_multiplicities<M61>(const void*, int, const void*, int, uint64_t, int64_t,
+                                         const int32_t*, const void*, const void*, uint64_t,
+                                         uint32_t*, uint32_t*, int64_t*, cudaStream_t);
 
 template int op_multiplicities<Fr255>(const void*, uint64_t, const void*, uint64_t, uint32_t*,
                                       int64_t*, cudaStream_t, uint32_t*);

@@ -78,6 +78,11 @@ int op_multiplicities(const void* secret, uint64_t d, const void* table, uint64_
                       uint32_t* counts, int64_t* first_miss, cudaStream_t s,
                       uint32_t* index_out = nullptr);
 template <class F>
+int op_pair_multiplicities(const void* x, int xt, const void* y, int yt, uint64_t d, int64_t x0,
+                           const int32_t* ty, const void* secret, const void* table, uint64_t n,
+                           uint32_t* counts, uint32_t* index_out, int64_t* first_miss,
+                           cudaStream_t s);
+template <class F>
 int op_gather(void* dst, const void* src, uint64_t src_n, const uint32_t* idx, uint64_t n,
               typename F::T add, bool has_add, cudaStream_t s);
 

@@ -376,7 +376,7 @@ def prove_pair_lookup(label, x, y, pair_table, key, tr, rng):
     entries); otherwise the reference's list semantics apply.
     """
     from .lookup import (LookupTable, SecretVector, compute_multiplicities,
-                         multiplicities_indexed, prove_lookup)
+                         multiplicities_indexed, multiplicities_pair, prove_lookup)
 
     p = tr.modulus
     tr.append(label + b"/x", x.ref.digest(key.group))
@@ -405,7 +405,10 @@ def prove_pair_lookup(label, x, y, pair_table, key, tr, rng):
                                   zip(pair_table.x.entries, pair_table.y.entries)),
                             table_com, pair_table.name + "+a*y")
     if isinstance(secret.entries, D.DeviceVector):
-        counts, index = multiplicities_indexed(secret.entries, table)
+        got = None
+        if xd is not None and yd is not None and tx is not None and ty is not None:
+            got = multiplicities_pair(secret.entries, table, xd.t, yd.t, tx, ty)
+        counts, index = got if got is not None else multiplicities_indexed(secret.entries, table)
         return prove_lookup(secret, counts, table, key, tr, rng, secret_index=index)
     counts = compute_multiplicities(secret.entries, table)
     return prove_lookup(secret, counts, table, key, tr, rng)

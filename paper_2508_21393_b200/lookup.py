@@ -139,6 +139,46 @@ def multiplicities_indexed(secret, table):
     return D.DeviceVector(out, n, spec), index
 
 
+def multiplicities_pair(secret, table, x, y, tx, ty):
+    """multiplicities_indexed for a pair lookup whose table x column is a
+    consecutive integer range (tables.py:142-152): queries are binned from
+    their int16/int32 (x, y) directly (zkl_pair_multiplicities).  Returns
+    None when that does not apply (the caller then hashes combined values)."""
+    import torch
+
+    if x.dtype not in (torch.int16, torch.int32) or y.dtype not in (torch.int16, torch.int32):
+        return None
+    n = len(table.entries)
+    tx = tx.reshape(-1)
+    if tx.numel() != n or n == 0:
+        return None
+    x0 = int(tx[0])
+    if not torch.equal(tx.long(), torch.arange(x0, x0 + n, device=tx.device)):
+        return None
+    ty = ty.reshape(-1).to(torch.int32).contiguous()
+    spec = secret.spec
+    sbuf = D.field_buffer(secret, spec)
+    tbuf = D.field_buffer(table.entries, spec)
+    d = len(secret)
+    xs = x.contiguous().view(-1)
+    ys = y.contiguous().view(-1)
+    counts = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    index = torch.empty(max(d, 1), dtype=torch.int32, device="cuda")
+    fm = ctypes.c_int64(-1)
+    rc = N.lib().zkl_pair_multiplicities(spec.fid, D.ptr(xs), D._INT_TYPES[xs.dtype], D.ptr(ys),
+                                         D._INT_TYPES[ys.dtype], d, x0, D.ptr(ty), D.ptr(sbuf),
+                                         D.ptr(tbuf), n, D.ptr(counts), D.ptr(index),
+                                         ctypes.byref(fm), D.stream())
+    if rc == N.ZKL_ERR_UNSUPPORTED:
+        return None
+    if rc == N.ZKL_ERR_MISSING:
+        raise TYPES["ElementNotInTable"](fm.value, D.read_scalar(sbuf, spec, fm.value))
+    N.check(rc)
+    out = D.empty(spec, n)
+    N.check(N.lib().zkl_lift_u32(spec.fid, D.ptr(out), D.ptr(counts), n, D.stream()))
+    return D.DeviceVector(out, n, spec), index
+
+
 def _gather(spec, src, src_n, index, n, add=None):
     out = D.empty(spec, n)
     N.check(N.lib().zkl_gather(spec.fid, D.ptr(out), D.ptr(src), src_n, D.ptr(index), n,

@@ -17,7 +17,7 @@ def wrap(mod, name, label=None):
         return r
     setattr(mod, name, w)
 wrap(D, "pair_combine")
-wrap(L, "multiplicities_indexed")
+wrap(L, "multiplicities_indexed"); wrap(L, "multiplicities_pair")
 wrap(L, "batch_inverse_device")
 wrap(L, "_gather"); wrap(L, "_expand"); wrap(L, "_tiled_sumcheck"); wrap(L, "run_rounds"); wrap(L, "_finish_lookup")
 wrap(L, "absorb_claim")

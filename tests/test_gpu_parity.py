@@ -572,6 +572,68 @@ def test_lookup_indexed_pole_retry(monkeypatch):
     assert all(o == out[0] for o in out[1:])
 
 
+@pytest.mark.parametrize("xdt", [torch.int16, torch.int32])
+def test_pair_multiplicities_direct(xdt):
+    """Direct binning of pair queries (table x column = consecutive range) gives
+    the same counts, indices and first miss as hashing the combined values,
+    including queries whose y disagrees with the table (hash fallback)."""
+    from paper_2508_21393_b200 import lookup as L
+
+    p = P_BIG
+    spec = D.spec_for(p)
+    rnd = np.random.default_rng(5)
+    n, d, x0 = 4096, 1 << 16, -2048
+    tx = torch.arange(x0, x0 + n, dtype=torch.int32).cuda()
+    ty = torch.from_numpy(rnd.integers(-30000, 30000, size=n).astype(np.int32)).cuda()
+    idx = rnd.integers(0, n, size=d)
+    xq = torch.from_numpy((idx + x0).astype(np.int64)).to(xdt).cuda()
+    yq = ty.cpu()[torch.from_numpy(idx)].to(xdt).cuda()
+    alpha = 987654321987654321
+    tab = zb.LookupTable(D.pair_combine(tx, ty, alpha, spec), None)
+    sec = D.pair_combine(xq, yq, alpha, spec)
+    got = L.multiplicities_pair(sec, tab, xq, yq, tx, ty)
+    assert got is not None
+    want = L.multiplicities_indexed(sec, tab)
+    assert D.as_list(got[0]) == D.as_list(want[0])
+    assert torch.equal(got[1][:d], want[1][:d])
+    # a query whose (x, y) is not a table pair but whose combined value is a
+    # table value takes the hash fallback and still lands in its bin
+    xq3 = xq.clone()
+    xq3[9] = x0 + n + 5
+    got3 = L.multiplicities_pair(sec, tab, xq3, yq, tx, ty)
+    assert D.as_list(got3[0]) == D.as_list(want[0])
+    assert torch.equal(got3[1][:d], want[1][:d])
+    yq2 = yq.clone()
+    yq2[7] = yq2[7] + 1  # now (x, y) is not a table pair: combined value misses
+    sec2 = D.pair_combine(xq, yq2, alpha, spec)
+    with pytest.raises(zb.ElementNotInTable) as e1:
+        L.multiplicities_pair(sec2, tab, xq, yq2, tx, ty)
+    with pytest.raises(zb.ElementNotInTable) as e2:
+        L.multiplicities_indexed(sec2, tab)
+    assert e1.value.index == e2.value.index == 7
+
+
+def test_pair_multiplicities_duplicate_table_declines():
+    """A combined table with a repeated value (the reference maps it to the
+    last index) is left to the hash path."""
+    from paper_2508_21393_b200 import lookup as L
+
+    p = P_TEST
+    spec = D.spec_for(p)
+    n = 64
+    tx = torch.arange(0, n, dtype=torch.int32).cuda()
+    ty = torch.zeros(n, dtype=torch.int32).cuda()
+    vals = list(range(n))
+    vals[10] = vals[20]  # duplicate combined value
+    tab = zb.LookupTable(D.DeviceVector(D.upload(vals, spec), n, spec), None)
+    xq = torch.tensor([3, 20, 10], dtype=torch.int16).cuda()
+    yq = torch.zeros(3, dtype=torch.int16).cuda()
+    sec = D.DeviceVector(D.upload([3, 20, 20], spec), 3, spec)
+    assert L.multiplicities_pair(sec, tab, xq, yq, tx, ty) is None
+    counts, index = L.multiplicities_indexed(sec, tab)
+    assert D.as_list(counts)[20] == 2 and D.as_list(counts)[10] == 0
+
+
 def test_multiplicities_golden():
     for c in load_golden("lookup.json")["multiplicities"]:
         table = zb.LookupTable(tuple(c["table"]), None)
