@@ -250,15 +250,15 @@ def prove_lookup(secret, multiplicities, table, key, tr, rng, secret_index=None)
     since every s_i equals t_index(i), beta hits a secret pole only if it
     hits a table pole, so the retry decisions of lookup.py:163-171 are
     unchanged."""
-    p = tr.modulus
-    spec = D.spec_for(p)
-    group = key.group
     entries = secret.entries
     d, n = len(entries), table.size
     if d == 0 or d & (d - 1):
         raise ValueError("secret length must be a power of two")
     if len(multiplicities) != n:
         raise ValueError("multiplicity vector must match the table size")
+    p = tr.modulus
+    spec = D.spec_for(p)
+    group = key.group
     be = commit_backend(key)
     stub = be.__name__.endswith("commit_stub")
 

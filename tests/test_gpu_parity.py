@@ -634,6 +634,54 @@ def test_pair_multiplicities_duplicate_table_declines():
     assert D.as_list(counts)[20] == 2 and D.as_list(counts)[10] == 0
 
 
+@pytest.mark.parametrize("indexed", [False, True])
+def test_lookup_pole_collision_after_max_retries(indexed):
+    """beta hitting a pole four times in a row raises PoleCollision
+    (lookup.py:165-171: three retries, each absorbing b"lookup/beta-retry"),
+    like the oracle; three poles still prove with beta_retries == 3."""
+    from oracle.stubcommit import stub_bytes
+    from paper_2508_21393_b200 import lookup as L
+
+    p = P_BIG
+    spec = D.spec_for(p)
+    rnd = np.random.default_rng(91)
+    n, d = 1 << 8, 1 << 10
+    base = [int(v) for v in rnd.integers(0, 2**40, size=n)]
+    betas = []
+
+    class _Capture(Transcript):
+        def challenge(self, label):
+            v = super().challenge(label)
+            if label == b"lookup/beta":
+                betas.append(v)
+            return v
+
+    def run(table, tr_cls=Transcript):
+        tab = zb.LookupTable(D.DeviceVector(D.upload(table, spec), n, spec), StubCommitment(8))
+        sec = zb.SecretVector(D.DeviceVector(D.upload([table[10]] * d, spec), d, spec),
+                              StubCommitment(10), ())
+        t = tr_cls(b"pole", p, b"x")
+        if indexed:
+            m, index = L.multiplicities_indexed(sec.entries, tab)
+            return zb.prove_lookup(sec, m, tab, KEY, t, RNG, secret_index=index)
+        return zb.prove_lookup(sec, zb.compute_multiplicities(sec.entries, tab), tab, KEY, t, RNG)
+
+    table = list(base)
+    for k in range(4):  # place -beta_k at position k: the next run retries once more
+        betas.clear()
+        pr = run(table, _Capture)
+        assert pr.beta_retries == k
+        table[k] = (p - betas[-1]) % p
+        if k == 3:
+            break
+    with pytest.raises(zb.PoleCollision):
+        run(table)
+    with pytest.raises(logup.Pole):
+        mult = logup.multiplicities([table[10]] * d, table)
+        logup.prove([table[10]] * d, mult, table, stub_bytes(8), stub_bytes(10),
+                    fs.FS(b"pole", p, b"x"), StubBackend(p))
+
+
 def test_multiplicities_golden():
     for c in load_golden("lookup.json")["multiplicities"]:
         table = zb.LookupTable(tuple(c["table"]), None)

@@ -200,3 +200,31 @@ def test_install_swaps_reference_import_sites():
         assert (zs.prove_sumcheck, zl.prove_lookup, zg.prove_matmul) == before
     finally:
         sys.path.remove(REF_SRC)
+
+
+def test_boundary_errors_before_any_device_work():
+    """Argument errors of the drop-in entry points are raised on the host,
+    with the reference's exception types (SURVEY sec. 8b "Errors"):
+    ShapeMismatch (gadgets.py:235-239), ValueError for a non-power-of-two
+    secret or a multiplicity vector of the wrong length (lookup.py:153-156)."""
+    from paper_2508_21393_b200.commit_stub import StubCommitment, StubKey
+    from paper_2508_21393_b200.gadgets import ProverTensor, TensorRef
+
+    key = StubKey()
+
+    def pt(rv, cv):
+        ref = TensorRef("committed", rv, cv, commitment=StubCommitment(rv + cv))
+        return ProverTensor([0] * (1 << (rv + cv)), ref, ())
+
+    tr = Transcript(b"e", P_TEST, b"s")
+    with pytest.raises(zb.ShapeMismatch):
+        zb.prove_matmul(pt(2, 3), pt(2, 2), pt(2, 2), key, tr, None)
+    with pytest.raises(zb.ShapeMismatch):
+        zb.prove_matmul(pt(2, 3), pt(3, 2), pt(3, 2), key, tr, None)
+    table = zb.LookupTable(tuple(range(8)), StubCommitment(3))
+    with pytest.raises(ValueError):
+        zb.prove_lookup(zb.SecretVector((1, 2, 3), StubCommitment(2), ()), [0] * 8, table, key,
+                        tr, None)
+    with pytest.raises(ValueError):
+        zb.prove_lookup(zb.SecretVector((1, 2, 3, 4), StubCommitment(2), ()), [0] * 7, table,
+                        key, tr, None)
