@@ -24,7 +24,7 @@ import torch
 
 from . import _native as N
 from . import device as D
-from .field import inverse
+from .field import inverse_pow2
 from .sumcheck import TYPES as SC_TYPES
 from .sumcheck import Term, absorb_claim, native_transcript, run_rounds
 
@@ -209,7 +209,7 @@ def _matmul_native(A, B, C, dims, tr, spec):
     log = getattr(tr, "log", None)
     if log is not None:  # the appends the reference makes (transcript.py:33-35)
         p = spec.modulus
-        cneg = (-inverse(1 << d1, p)) % p
+        cneg = (-inverse_pow2(d1, p)) % p
         ln = lambda v: (v.bit_length() + 7) // 8 or 1  # noqa: E731
         log.extend([(b"sumcheck/sum", 1), (b"sumcheck/shape", 3), (b"sumcheck/coeff", 1),
                     (b"sumcheck/factors", 3), (b"sumcheck/coeff", ln(cneg)),
@@ -235,7 +235,7 @@ def matmul_sumcheck(A, B, C, dims, tr):
         return _matmul_native(A, B, C, dims, tr, spec)
     r_u = tr.challenge_vector(b"matmul/r_u", d0)
     r_v = tr.challenge_vector(b"matmul/r_v", d2)
-    cneg = (-inverse(1 << d1, p)) % p
+    cneg = (-inverse_pow2(d1, p)) % p
     absorb_claim(tr, 0, [Term(1, (0, 1, 2)), Term(cneg, (0, 3))], 3, d0 + d1 + d2)
     E_v = D.eq_table(r_v, spec)
 

@@ -17,7 +17,7 @@ from dataclasses import dataclass
 
 from . import _native as N
 from . import device as D
-from .field import batch_inverse_device, inverse
+from .field import batch_inverse_device, inverse_pow2
 from .gadgets import commit_backend
 from .mle import mle_evaluate_device
 from .sumcheck import TYPES as SC_TYPES
@@ -316,7 +316,7 @@ def prove_lookup(secret, multiplicities, table, key, tr, rng, secret_index=None)
     big = max(d, n)
     num_vars = (big - 1).bit_length()
     u = tr.challenge_vector(b"lookup/u", num_vars)
-    ratio = inverse(big // n, p)
+    ratio = inverse_pow2((big // n).bit_length() - 1, p)  # big / n is a power of two
 
     terms = _terms(alpha, ratio, p)
     claimed = alpha * alpha % p
