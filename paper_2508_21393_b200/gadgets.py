@@ -391,7 +391,10 @@ def prove_pair_lookup(label, x, y, pair_table, key, tr, rng):
     rows = 1 << ((x.ref.num_vars + 1) // 2)
     bx = list(x.blinding) if x.blinding else [0] * rows
     by = list(y.blinding) if y.blinding else [0] * rows
-    blinding = tuple((a + alpha * b) % p for a, b in zip(bx, by))
+    if any(by):
+        blinding = tuple((a + alpha * b) % p for a, b in zip(bx, by))
+    else:  # (the stub / unblinded case: skip 2^13 bigint products per lookup)
+        blinding = tuple(a % p for a in bx)
     if (xd is not None and yd is not None and xd.mtype != N.MT_FIELD
             and yd.mtype != N.MT_FIELD and tx is not None and ty is not None):
         secret = SecretVector(D.pair_combine(xd.t, yd.t, alpha, spec), secret_com, blinding)
