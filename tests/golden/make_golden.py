@@ -429,8 +429,95 @@ def gen_field_mle():
     dump("field_mle.json", out)
 
 
+def _lookup_rec(lp):
+    return dict(beta_retries=lp.beta_retries,
+                rounds=[list(x.evaluations) for x in lp.sumcheck.rounds],
+                final_values=list(lp.sumcheck.final_values),
+                secret_values=list(lp.secret_values), table_values=list(lp.table_values))
+
+
+def gen_nonlinear():
+    """prove_rescale / prove_swiglu (phi, phi_prime) / prove_rsqrt
+    (gadgets.py:585-622, 761-771, 842-847) on 16x16 tensors, both fields."""
+    from zklora.quantize import centered_divmod
+
+    params = QuantParams(gamma_fp=2**4, bound=2**6, zeta=2**4, xi=2**9,
+                         radices=(8, 8, 8), act_bound=4)
+    eps = 2.0 ** -6
+    half = params.act_bound * params.gamma_fp
+    cases = []
+    for fname, p in FIELDS.items():
+        # build_table_set's params_digest packs the modulus into 16 bytes
+        # (tables.py:192), which overflows for BLS12-381 Fr: assemble the same
+        # TableSet fields directly (tables.py:217-238)
+        ts = TB.TableSet(
+            params, eps, p, b"", (),
+            TB._pair("silu", TB.silu_entries(params), KEY, p),
+            TB._pair("silu_deriv", TB.silu_deriv_entries(params), KEY, p),
+            TB._pair("rsqrt", TB.rsqrt_entries(params, eps), KEY, p),
+            L.make_lookup_table(TB._encode_column(TB.quant_range_entries(params), p), KEY,
+                                "quant_range"),
+            L.make_lookup_table(TB._encode_column(TB.residue_range_entries(params), p), KEY,
+                                "residue_range"))
+        g = inputs.rng(11)
+        enc = lambda vals: [int(v) % p for v in vals]
+        # rescale, divisor = zeta (lift 1) and divisor = zeta/4 (lift 4)
+        for divisor in (params.zeta, params.zeta // 4):
+            lift = params.zeta // divisor
+            q0 = g.integers(-half, half, size=256)
+            r0 = g.integers(-(divisor // 2), divisor // 2, size=256)
+            wide = [int(divisor * a + b) for a, b in zip(q0, r0)]
+            qr = [centered_divmod(w, divisor) for w in wide]
+            narrow = [q for q, _ in qr]
+            resid = [r * lift for _, r in qr]
+            tr = Transcript(b"zkl/golden/rescale", p, b"d%d" % divisor)
+            start = tr.state
+            pr = G.prove_rescale(_pt(enc(wide), 4, 4), _pt(enc(narrow), 4, 4),
+                                 _pt(enc(resid), 4, 4), divisor, ts, KEY, tr, RNG)
+            cases.append(dict(gadget="rescale", field=fname, divisor=divisor, wide=wide,
+                              narrow=narrow, resid=resid, state_before=hx(start),
+                              identity=list(pr.identity_opening.values),
+                              lookups=[_lookup_rec(pr.quant_lookup), _lookup_rec(pr.resid_lookup)],
+                              state_end=hx(tr.state)))
+        for mode in ("phi", "phi_prime"):
+            fn = TB.silu_value if mode == "phi" else TB.silu_deriv_value
+            q0 = g.integers(-half, half, size=256)
+            r0 = g.integers(-(params.zeta // 2), params.zeta // 2, size=256)
+            wide = [int(params.zeta * a + b) for a, b in zip(q0, r0)]
+            qr = [centered_divmod(w, params.zeta) for w in wide]
+            narrow = [q for q, _ in qr]
+            resid = [r for _, r in qr]
+            out = [fn(params, q) for q in narrow]
+            tr = Transcript(b"zkl/golden/swiglu", p, mode.encode())
+            start = tr.state
+            pr = G.prove_swiglu(_pt(enc(wide), 4, 4), _pt(enc(out), 4, 4), _pt(enc(narrow), 4, 4),
+                                _pt(enc(resid), 4, 4), mode, ts, KEY, tr, RNG)
+            cases.append(dict(gadget="swiglu", mode=mode, field=fname, wide=wide, narrow=narrow,
+                              resid=resid, out=out, state_before=hx(start),
+                              identity=list(pr.identity_opening.values),
+                              lookups=[_lookup_rec(pr.activation_lookup),
+                                       _lookup_rec(pr.resid_lookup)],
+                              state_end=hx(tr.state)))
+        v = [int(x) for x in g.integers(0, half, size=64)]
+        u = [TB.rsqrt_value(params, eps, x) for x in v]
+        tr = Transcript(b"zkl/golden/rsqrt", p, b"r")
+        start = tr.state
+        pr = G.prove_rsqrt(_pt(enc(v), 3, 3), _pt(enc(u), 3, 3), ts, KEY, tr, RNG)
+        cases.append(dict(gadget="rsqrt", field=fname, v=v, u=u, state_before=hx(start),
+                          lookups=[_lookup_rec(pr.lookup)], state_end=hx(tr.state)))
+    tabs = {}
+    for name in ("silu", "silu_deriv", "rsqrt"):
+        pt_ = getattr(ts, name)
+        tabs[name] = dict(x=[F.to_signed(v, p) for v in pt_.x.entries],
+                          y=[F.to_signed(v, p) for v in pt_.y.entries])
+    tabs["quant_range"] = [F.to_signed(v, p) for v in ts.quant_range.entries]
+    tabs["residue_range"] = [F.to_signed(v, p) for v in ts.residue_range.entries]
+    dump("nonlinear.json", dict(params=dict(gamma=16, zeta=16, act_bound=4, eps=eps),
+                                tables=tabs, cases=cases))
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["transcript", "sumcheck", "matmul", "elementprod", "lookup",
-                             "pair_lookup", "tables", "field_mle"]
+                             "pair_lookup", "tables", "field_mle", "nonlinear"]
     for w in which:
         globals()["gen_" + w]()

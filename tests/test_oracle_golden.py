@@ -213,3 +213,49 @@ def test_silu_table_restatement_matches_reference():
     # spot values: silu(0) = 0, silu is ~identity for large x
     assert ys[32768] == 0
     assert abs(int(ys[-1]) - 32767) < 40
+
+
+# --- non-linear gadgets (rescale / swiglu / rsqrt) ---------------------------
+
+
+def _nl_check(out, c):
+    for got, want in zip(out["lookups"], c["lookups"]):
+        assert [list(x) for x in got["rounds"]] == want["rounds"]
+        assert list(got["final_values"]) == want["final_values"]
+        assert list(got["secret_values"]) == want["secret_values"]
+        assert list(got["table_values"]) == want["table_values"]
+        assert got["beta_retries"] == want["beta_retries"]
+    if "identity" in c:
+        assert list(out["identity"]) == c["identity"]
+
+
+def test_nonlinear_golden():
+    """oracle/gadgets.py against the reference's prove_rescale / prove_swiglu /
+    prove_rsqrt (gadgets.py:600-622, 761-782, 842-847) on both fields."""
+    from oracle import gadgets as og
+
+    g = load_golden("nonlinear.json")
+    tabs, prm = g["tables"], g["params"]
+    seen = set()
+    for c in g["cases"]:
+        p = FIELDS[c["field"]]
+        enc = lambda vals: [v % p for v in vals]  # noqa: E731
+        t = _tr(b"", p, b"", c["state_before"])
+        be = StubBackend(p)
+        if c["gadget"] == "rescale":
+            out = og.rescale(enc(c["wide"]), enc(c["narrow"]), enc(c["resid"]), (4, 4),
+                             c["divisor"], prm["zeta"], enc(tabs["quant_range"]),
+                             enc(tabs["residue_range"]), t, be)
+        elif c["gadget"] == "swiglu":
+            pair = tabs["silu" if c["mode"] == "phi" else "silu_deriv"]
+            out = og.swiglu(enc(c["wide"]), enc(c["out"]), enc(c["narrow"]), enc(c["resid"]),
+                            (4, 4), c["mode"], (enc(pair["x"]), enc(pair["y"])),
+                            enc(tabs["residue_range"]), t, be)
+        else:
+            pair = tabs["rsqrt"]
+            out = og.rsqrt(enc(c["v"]), enc(c["u"]), (3, 3), (enc(pair["x"]), enc(pair["y"])),
+                           t, be)
+        _nl_check(out, c)
+        assert t.state.hex() == c["state_end"]
+        seen.add((c["gadget"], c["field"]))
+    assert len(seen) == 6
