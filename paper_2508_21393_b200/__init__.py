@@ -39,6 +39,14 @@ from .lookup import (  # noqa: F401
     prove_lookup,
 )
 from .mle import eq_table, fold_table, mle_evaluate  # noqa: F401
+from .nonlinear import (  # noqa: F401
+    PairTable,
+    RangeViolation,
+    TableSet,
+    prove_rescale,
+    prove_rsqrt,
+    prove_swiglu,
+)
 from .sumcheck import (  # noqa: F401
     DegreeOverflow,
     RoundPolynomial,

@@ -179,6 +179,18 @@ def multiplicities_pair(secret, table, x, y, tx, ty):
     return D.DeviceVector(out, n, spec), index
 
 
+def multiplicities_range(secret, table, col, tcol):
+    """multiplicities_indexed for a single-column table whose entries are the
+    consecutive integers tcol (quant_range / residue_range, tables.py:109-117)
+    and a secret given by its int16/int32 device column: bins by offset
+    (zkl_pair_multiplicities with y = x).  None when that does not apply."""
+    import torch
+
+    if col.dtype not in (torch.int16, torch.int32):
+        return None
+    return multiplicities_pair(secret, table, col, col, tcol, tcol)
+
+
 def _gather(spec, src, src_n, index, n, add=None):
     out = D.empty(spec, n)
     N.check(N.lib().zkl_gather(spec.fid, D.ptr(out), D.ptr(src), src_n, D.ptr(index), n,

@@ -60,9 +60,25 @@ def mle_evaluate(table, point, modulus):
     return mle_evaluate_device(D.upload(list(table), spec), n, list(point), spec)
 
 
+def mle_evaluate_matrix(M, point, spec):
+    """MLE of an integer DeviceMatrix (row bits || column bits) at `point`:
+    eq(point_rows)^T (M eq(point_cols)), one matrix-vector pass over the
+    integers (zkl_matvec) instead of lifting 2^n entries to field elements."""
+    from .gadgets import _matvec
+
+    rv, cv = (M.rows - 1).bit_length(), (M.cols - 1).bit_length()
+    if rv + cv != len(point):
+        raise DimensionMismatch("point has %d coordinates, polynomial has %d variables"
+                                % (len(point), rv + cv))
+    y = _matvec(M, D.eq_table(point[rv:], spec), False, spec)
+    return D.dot(D.eq_table(point[:rv], spec), y, spec, M.rows)
+
+
 def mle_evaluate_any(table, point, modulus):
     """Python list or DeviceMatrix / device vector."""
     spec = D.spec_for(modulus)
+    if getattr(table, "mtype", N.MT_FIELD) != N.MT_FIELD:
+        return mle_evaluate_matrix(table, list(point), spec)
     lifted = getattr(table, "as_field_vector", None)
     if lifted is not None:
         return mle_evaluate_device(lifted(spec), len(point), list(point), spec)

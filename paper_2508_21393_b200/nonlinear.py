@@ -1,0 +1,196 @@
+"""Device-resident non-linear gadget provers: rescale, SwiGLU, rsqrt.
+
+Mirrors of zklora.gadgets (reference gadgets.py):
+  prove_rescale  gadgets.py:600-622  (quotient + residue range lookups)
+  prove_swiglu   gadgets.py:761-782  (activation pair lookup + residue lookup)
+  prove_rsqrt    gadgets.py:842-847  (pair lookup)
+with the same transcript traffic, argument meaning and exceptions.  They
+exist so that tensors that live on the GPU as int16/int32/int64 matrices
+(DeviceMatrix) are proven without ever building Python lists: the lookup
+secrets are lifted on the device, multiplicities are binned on the device
+and the logUp sumchecks run on the round engine (lookup.py).  With host
+ProverTensors they behave like the reference functions (which, once
+install() has run, already reach this backend through prove_lookup).
+
+Tables: `TableSet` holds the same fields as tables.py:156-168; its single
+column tables may carry DeviceVector entries and its pair tables int32
+device columns (`device_table_set`).
+"""
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _native as N
+from . import device as D
+from .gadgets import ShapeMismatch, _absorb_operands, _open_tables, prove_pair_lookup
+from .lookup import (LookupTable, SecretVector, compute_multiplicities, multiplicities_indexed,
+                     multiplicities_range, prove_lookup)
+
+
+class RangeViolation(ValueError):
+    """gadgets.py RangeViolation (witness outside a table domain)."""
+
+
+@dataclass(frozen=True)
+class PairTable:
+    """tables.py:120-153: aligned (input, output) columns."""
+
+    x: LookupTable
+    y: LookupTable
+    name: str
+
+    @property
+    def size(self):
+        return self.x.size
+
+
+@dataclass(frozen=True)
+class TableSet:
+    """tables.py:156-168 (the fields the gadgets read)."""
+
+    params: object
+    eps: float
+    modulus: int
+    digest: bytes
+    exp_segments: tuple
+    silu: PairTable
+    silu_deriv: PairTable
+    rsqrt: PairTable
+    quant_range: LookupTable
+    residue_range: LookupTable
+
+
+@dataclass
+class RescaleProof:
+    tag = "rescale"
+    divisor: int
+    shape: tuple
+    identity_opening: object
+    quant_lookup: object
+    resid_lookup: object
+
+
+@dataclass
+class SwigluProof:
+    tag = "swiglu"
+    mode: str
+    shape: tuple
+    narrow_ref: object
+    resid_ref: object
+    identity_opening: object
+    activation_lookup: object
+    resid_lookup: object
+
+
+@dataclass
+class RsqrtProof:
+    tag = "rsqrt"
+    shape: tuple
+    lookup: object
+
+
+TYPES = {"RescaleProof": RescaleProof, "SwigluProof": SwigluProof, "RsqrtProof": RsqrtProof}
+
+
+# ---------------------------------------------------------------------------
+def device_range_table(lo, n, spec, commitment, name):
+    """A consecutive-integer single-column table [lo, lo+n) lifted on the GPU
+    (quant_range_entries / residue_range_entries, tables.py:109-117)."""
+    col = torch.arange(lo, lo + n, dtype=torch.int32, device="cuda")
+    t = LookupTable(D.DeviceVector(D.lift(col, spec), n, spec), commitment, name)
+    object.__setattr__(t, "int_column", col)  # lets multiplicities bin by offset
+    return t
+
+
+def device_pair_table(xs, ys, commitment_x, commitment_y, name):
+    """A pair table with int32 device columns (tables.py:208-214)."""
+    tx = torch.as_tensor(xs, dtype=torch.int32).cuda()
+    ty = torch.as_tensor(ys, dtype=torch.int32).cuda()
+    return PairTable(LookupTable(tx, commitment_x, name + ".x"),
+                     LookupTable(ty, commitment_y, name + ".y"), name)
+
+
+def _int_matrix(pt):
+    dev = getattr(pt, "device", None)
+    if dev is not None and dev.mtype != N.MT_FIELD:
+        return dev.t
+    return None
+
+
+def _range_lookup(pt, table, key, tr, rng):
+    """prove_lookup(pt.as_secret_vector(), compute_multiplicities(...), table)
+    (gadgets.py:606-613) for a committed operand."""
+    if pt.ref.kind != "committed":
+        raise ValueError("public operands have no secret vector")
+    col = _int_matrix(pt)
+    if col is not None and isinstance(table.entries, D.DeviceVector):
+        spec = table.entries.spec
+        flat = col.reshape(-1)
+        secret = SecretVector(D.DeviceVector(D.lift(flat, spec), flat.numel(), spec),
+                              pt.ref.commitment, tuple(pt.blinding))
+        got = None
+        tcol = getattr(table, "int_column", None)
+        if tcol is not None:
+            got = multiplicities_range(secret.entries, table, flat, tcol)
+        counts, index = got if got is not None else multiplicities_indexed(secret.entries, table)
+        return prove_lookup(secret, counts, table, key, tr, rng, secret_index=index)
+    secret = SecretVector(tuple(pt.flat()), pt.ref.commitment, tuple(pt.blinding))
+    return prove_lookup(secret, compute_multiplicities(secret.entries, table), table, key, tr,
+                        rng)
+
+
+def _shape(pt):
+    return (pt.ref.row_vars, pt.ref.col_vars)
+
+
+def prove_rescale(wide, narrow, resid, divisor, tables, key, tr, rng):
+    """Drop-in for zklora.gadgets.prove_rescale (gadgets.py:600-622): proves
+    (zeta/div)*wide = zeta*narrow + resid with narrow in quant_range and
+    resid in residue_range."""
+    zeta = tables.params.zeta
+    if divisor <= 0 or zeta % divisor:
+        raise ValueError("divisor must divide zeta")
+    shape = _shape(wide)
+    for t in (narrow, resid):
+        if _shape(t) != shape:
+            raise ShapeMismatch("rescale operands must share a shape")
+    _absorb_operands(tr, b"rescale", [wide.ref, narrow.ref, resid.ref], key.group)
+    tr.append(b"rescale/divisor", divisor)
+    point = tr.challenge_vector(b"rescale/point", wide.ref.num_vars)
+    identity_opening = _open_tables(key, [wide, narrow, resid], point, tr, rng)
+    quant_lookup = _range_lookup(narrow, tables.quant_range, key, tr, rng)
+    resid_lookup = _range_lookup(resid, tables.residue_range, key, tr, rng)
+    return TYPES["RescaleProof"](divisor=divisor, shape=shape, identity_opening=identity_opening,
+                                 quant_lookup=quant_lookup, resid_lookup=resid_lookup)
+
+
+def prove_swiglu(wide, out, narrow, resid, mode, tables, key, tr, rng):
+    """Drop-in for zklora.gadgets.prove_swiglu (gadgets.py:761-782): proves
+    out = activation(round(wide / zeta)) with a ranged residue."""
+    if mode not in ("phi", "phi_prime"):
+        raise ValueError("mode must be phi or phi_prime")
+    shape = _shape(wide)
+    for t in (out, narrow, resid):
+        if _shape(t) != shape:
+            raise ShapeMismatch("swiglu operands must share a shape")
+    pair = tables.silu if mode == "phi" else tables.silu_deriv
+    _absorb_operands(tr, b"swiglu", [wide.ref, out.ref], key.group)
+    tr.append(b"swiglu/mode", mode.encode())
+    _absorb_operands(tr, b"swiglu/wit", [narrow.ref, resid.ref], key.group)
+    point = tr.challenge_vector(b"swiglu/point", wide.ref.num_vars)
+    identity_opening = _open_tables(key, [wide, narrow, resid], point, tr, rng)
+    activation_lookup = prove_pair_lookup(b"swiglu/act", narrow, out, pair, key, tr, rng)
+    resid_lookup = _range_lookup(resid, tables.residue_range, key, tr, rng)
+    return TYPES["SwigluProof"](mode=mode, shape=shape, narrow_ref=narrow.ref,
+                                resid_ref=resid.ref, identity_opening=identity_opening,
+                                activation_lookup=activation_lookup, resid_lookup=resid_lookup)
+
+
+def prove_rsqrt(v, u, tables, key, tr, rng):
+    """Drop-in for zklora.gadgets.prove_rsqrt (gadgets.py:842-847)."""
+    if _shape(u) != _shape(v):
+        raise ShapeMismatch("rsqrt operands must share a shape")
+    _absorb_operands(tr, b"rsqrt", [v.ref, u.ref], key.group)
+    lookup = prove_pair_lookup(b"rsqrt/pair", v, u, tables.rsqrt, key, tr, rng)
+    return TYPES["RsqrtProof"](shape=_shape(v), lookup=lookup)

@@ -1,0 +1,70 @@
+"""Host-side lookup-table generation (restates zklora.tables, tables.py:40-117).
+
+Table values come from float64 host code in the reference (np.exp, math.exp,
+math.sqrt with round-half-away, quantize.py:81-85).  They are generated here
+with the same scalar operations in the same order (SURVEY.md sec. 7 hard
+part 8: never recompute them on the device), then uploaded as int32 device
+columns.  tests/test_host.py pins every table against the reference's own
+output (tests/golden/tables_g4096.json).
+"""
+
+import math
+
+import numpy as np
+
+
+def round_half_away(x):
+    """quantize.py:81-85."""
+    if x >= 0:
+        return int(np.floor(x + 0.5))
+    return -int(np.floor(-x + 0.5))
+
+
+def _silu_real(x):  # tables.py:40-42 (0-d float64 array, as the reference calls it)
+    x = np.asarray(x, dtype=np.float64)
+    return x / (1.0 + np.exp(-x))
+
+
+def _silu_deriv_real(x):  # tables.py:45-48
+    x = np.asarray(x, dtype=np.float64)
+    s = 1.0 / (1.0 + np.exp(-x))
+    return s * (1.0 + x * (1.0 - s))
+
+
+def silu_entries(gamma, act_bound):
+    """tables.py:65-69, 92-95: x in [-act*gamma, act*gamma)."""
+    half = act_bound * gamma
+    xs = range(-half, half)
+    return list(xs), [round_half_away(gamma * float(_silu_real(x / gamma))) for x in xs]
+
+
+def silu_deriv_entries(gamma, act_bound):
+    """tables.py:72-76, 98-101."""
+    half = act_bound * gamma
+    xs = range(-half, half)
+    return list(xs), [round_half_away(gamma * float(_silu_deriv_real(x / gamma))) for x in xs]
+
+
+def exp_segment_entries(gamma, radices, k):
+    """tables.py:56-62, 86-89: digit -> round(gamma * exp(-digit * base_k / gamma))."""
+    base = 1
+    for r in radices[:k]:
+        base *= r
+    xs = range(radices[k])
+    return list(xs), [round_half_away(gamma * math.exp(-d * (base / gamma))) for d in xs]
+
+
+def rsqrt_entries(gamma, act_bound, eps):
+    """tables.py:79-83, 104-106: x in [0, act*gamma)."""
+    xs = range(act_bound * gamma)
+    return list(xs), [round_half_away(gamma / math.sqrt(x / gamma + eps)) for x in xs]
+
+
+def quant_range(gamma, act_bound):
+    """tables.py:109-111: (first value, size)."""
+    return -act_bound * gamma, 2 * act_bound * gamma
+
+
+def residue_range(zeta):
+    """tables.py:114-117."""
+    return -(zeta // 2), zeta

@@ -395,7 +395,10 @@ def gen_tables():
     params = QuantParams(gamma_fp=2**12, bound=2**16, zeta=2**12, xi=2**64,
                          radices=(2**16,) * 4, act_bound=8)
     out = {}
-    for name, fn in (("silu", TB.silu_entries), ("silu_deriv", TB.silu_deriv_entries)):
+    fns = (("silu", TB.silu_entries), ("silu_deriv", TB.silu_deriv_entries),
+           ("exp0", lambda q: TB.exp_segment_entries(q, 0)),
+           ("rsqrt_eps1e-5", lambda q: TB.rsqrt_entries(q, 1e-5)))
+    for name, fn in fns:
         xs, ys = fn(params)
         arr = np.asarray(ys, dtype="<i4")
         out[name] = dict(x0=xs[0], n=len(xs),
@@ -516,8 +519,104 @@ def gen_nonlinear():
                                 tables=tabs, cases=cases))
 
 
+class RefBlockProver:
+    """Drives the REFERENCE's gadget provers (stub commitments) through
+    paper_2508_21393_b200.block.prove_block's schedule on CPU tensors, so the
+    GPU block proof can be checked byte for byte (tests/test_gpu_block.py)."""
+
+    def __init__(self, tr, ts, fp, p):
+        import torch
+        from paper_2508_21393_b200 import block as BK
+
+        self.BK, self.torch = BK, torch
+        self.tr, self.ts, self.fp, self.p = tr, ts, fp, p
+        ys = lambda pair: torch.tensor([F.to_signed(v, p) for v in pair.y.entries],  # noqa: E731
+                                       dtype=torch.int32)
+        self.luts = {"silu": ys(ts.silu), "silu_deriv": ys(ts.silu_deriv),
+                     "rsqrt": ys(ts.rsqrt), "exp": ys(ts.exp_segments[0])}
+        self.clipped = 0
+        self.log = []
+
+    def pt(self, t):
+        rv, cv = (t.shape[0] - 1).bit_length(), (t.shape[1] - 1).bit_length()
+        return _pt([int(v) % self.p for v in t.reshape(-1).tolist()], rv, cv)
+
+    def matmul(self, a, b, c):
+        pr = G.prove_matmul(self.pt(a), self.pt(b), self.pt(c), KEY, self.tr, RNG)
+        self.log.append(["matmul", len(pr.sumcheck.rounds)])
+
+    def eprod(self, a, b, c):
+        pr = G.prove_elementprod(self.pt(a), self.pt(b), self.pt(c), KEY, self.tr, RNG)
+        self.log.append(["elementprod", len(pr.sumcheck.rounds)])
+
+    def rescale(self, wide):
+        q, r, clipped = self.BK._divmod(wide, self.fp)
+        self.clipped += clipped
+        pr = G.prove_rescale(self.pt(wide), self.pt(q), self.pt(r), self.fp.zeta, self.ts, KEY,
+                             self.tr, RNG)
+        self.log.append(["rescale", len(pr.quant_lookup.sumcheck.rounds),
+                         len(pr.resid_lookup.sumcheck.rounds)])
+        return q
+
+    def swiglu(self, wide, mode):
+        q, r, clipped = self.BK._divmod(wide, self.fp)
+        self.clipped += clipped
+        out = self.BK._lut(self.luts["silu" if mode == "phi" else "silu_deriv"], q,
+                           self.fp.qmin).to(self.torch.int16)
+        pr = G.prove_swiglu(self.pt(wide), self.pt(out), self.pt(q), self.pt(r), mode, self.ts,
+                            KEY, self.tr, RNG)
+        self.log.append(["swiglu", len(pr.activation_lookup.sumcheck.rounds),
+                         len(pr.resid_lookup.sumcheck.rounds)])
+        return out
+
+    def rsqrt(self, v, u):
+        pr = G.prove_rsqrt(self.pt(v), self.pt(u), self.ts, KEY, self.tr, RNG)
+        self.log.append(["rsqrt", len(pr.lookup.sumcheck.rounds)])
+
+    def exp_lookup(self, v, e):
+        pr = G._prove_pair_lookup(b"softmax/exp0", self.pt(v), self.pt(e), self.ts.exp_segments[0],
+                                  KEY, self.tr, RNG)
+        self.log.append(["softmax_exp", len(pr.sumcheck.rounds)])
+
+
+def gen_block():
+    """A tiny LoRA block (2 heads, FFN padded 24 -> 32, LoRA on q, v, o) proven
+    by the reference's gadgets in prove_block's order, test field and big
+    field; the end transcript state pins the whole composition."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from paper_2508_21393_b200 import block as BK
+
+    shape = BK.BlockShape("tiny", 16, 16, 2, 8, 24, 2, ("q", "v", "o"))
+    fp = BK.FixedPoint(gamma_fp=16, zeta=16, act_bound=4, exp_n=64, eps=2.0 ** -6)
+    params = QuantParams(gamma_fp=16, bound=2**6, zeta=16, xi=2**9, radices=(64, 8),
+                         act_bound=4)
+    cases = []
+    for fname, p in FIELDS.items():
+        ts = TB.TableSet(
+            params, fp.eps, p, b"", (TB._pair("exp0", TB.exp_segment_entries(params, 0), KEY, p),),
+            TB._pair("silu", TB.silu_entries(params), KEY, p),
+            TB._pair("silu_deriv", TB.silu_deriv_entries(params), KEY, p),
+            TB._pair("rsqrt", TB.rsqrt_entries(params, fp.eps), KEY, p),
+            L.make_lookup_table(TB._encode_column(TB.quant_range_entries(params), p), KEY,
+                                "quant_range"),
+            L.make_lookup_table(TB._encode_column(TB.residue_range_entries(params), p), KEY,
+                                "residue_range"))
+        w = BK.BlockWitness(shape, seed=3, fp=fp, device="cpu")
+        tr = Transcript(b"zkl/golden/block", p, fname.encode())
+        start = tr.state
+        t0 = time.time()
+        P = BK.prove_block(w, RefBlockProver(tr, ts, fp, p))
+        print("block", fname, "%.1f s" % (time.time() - t0), len(P.log), "gadgets")
+        cases.append(dict(field=fname, seed=3, state_before=hx(start), log=P.log,
+                          clipped=P.clipped, state_end=hx(tr.state)))
+    dump("block.json", dict(shape=[shape.seq, shape.hidden, shape.heads, shape.head_dim,
+                                   shape.ffn, shape.rank, list(shape.lora)],
+                            fp=[fp.gamma_fp, fp.zeta, fp.act_bound, fp.exp_n, fp.eps],
+                            cases=cases))
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["transcript", "sumcheck", "matmul", "elementprod", "lookup",
-                             "pair_lookup", "tables", "field_mle", "nonlinear"]
+                             "pair_lookup", "tables", "field_mle", "nonlinear", "block"]
     for w in which:
         globals()["gen_" + w]()

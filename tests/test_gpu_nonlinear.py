@@ -1,0 +1,150 @@
+"""GPU parity of the non-linear gadget mirrors (rescale, SwiGLU, rsqrt) and of
+device MLE evaluation of integer matrices.
+
+The goldens (tests/golden/nonlinear.json) come from the reference's own
+prove_rescale / prove_swiglu / prove_rsqrt (gadgets.py:600-622, 761-782,
+842-847) run with the stub commitment; tests/test_oracle_golden.py pins the
+oracle restatement to the same file."""
+
+from types import SimpleNamespace
+
+import pytest
+
+from conftest import FIELDS, load_golden
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2508_21393_b200 as zb  # noqa: E402
+from paper_2508_21393_b200 import device as D  # noqa: E402
+from paper_2508_21393_b200 import mle as M  # noqa: E402
+from paper_2508_21393_b200 import nonlinear as NL  # noqa: E402
+from paper_2508_21393_b200.commit_stub import StubCommitment, StubKey  # noqa: E402
+from paper_2508_21393_b200.gadgets import DeviceMatrix, ProverTensor, TensorRef  # noqa: E402
+from paper_2508_21393_b200.transcript import Transcript  # noqa: E402
+
+KEY = StubKey()
+
+
+class _Rng:
+    def vector(self, n):
+        return [0] * n
+
+
+def _log2(n):
+    return (n - 1).bit_length()
+
+
+def _tables(g, p, where):
+    t = g["tables"]
+    spec = D.spec_for(p)
+    enc = lambda vals: tuple(v % p for v in vals)  # noqa: E731
+
+    def rng_table(vals, name):
+        c = StubCommitment(_log2(len(vals)))
+        if where == "device":
+            return NL.device_range_table(vals[0], len(vals), spec, c, name)
+        return zb.LookupTable(enc(vals), c, name)
+
+    def pair(name):
+        xs, ys = t[name]["x"], t[name]["y"]
+        c = StubCommitment(_log2(len(xs)))
+        if where == "device":
+            return NL.device_pair_table(xs, ys, c, c, name)
+        return NL.PairTable(zb.LookupTable(enc(xs), c, name + ".x"),
+                            zb.LookupTable(enc(ys), c, name + ".y"), name)
+
+    return NL.TableSet(SimpleNamespace(zeta=g["params"]["zeta"]), g["params"]["eps"], p, b"", (),
+                       pair("silu"), pair("silu_deriv"), pair("rsqrt"),
+                       rng_table(t["quant_range"], "quant_range"),
+                       rng_table(t["residue_range"], "residue_range"))
+
+
+def _operand(vals, rv, cv, p, where, dtype=torch.int32):
+    ref = TensorRef("committed", rv, cv, commitment=StubCommitment(rv + cv))
+    if where == "device":
+        t = torch.tensor(vals, dtype=dtype).cuda().view(1 << rv, 1 << cv)
+        return ProverTensor(None, ref, (), device=DeviceMatrix.from_int_tensor(t))
+    return ProverTensor(SimpleNamespace(data=[v % p for v in vals]), ref, ())
+
+
+def _check_lookup(got, want):
+    assert got.beta_retries == want["beta_retries"]
+    assert [list(r.evaluations) for r in got.sumcheck.rounds] == want["rounds"]
+    assert list(got.sumcheck.final_values) == want["final_values"]
+    assert list(got.secret_values) == want["secret_values"]
+    assert list(got.table_values) == want["table_values"]
+
+
+@pytest.mark.parametrize("where", ["device", "host"])
+def test_nonlinear_golden(where):
+    g = load_golden("nonlinear.json")
+    seen = set()
+    for c in g["cases"]:
+        p = FIELDS[c["field"]]
+        ts = _tables(g, p, where)
+        tr = Transcript.from_state(bytes.fromhex(c["state_before"]), p)
+        op = lambda vals, k=4: _operand(vals, k, k, p, where)  # noqa: E731
+        if c["gadget"] == "rescale":
+            pr = zb.prove_rescale(op(c["wide"]), op(c["narrow"]), op(c["resid"]), c["divisor"], ts,
+                                  KEY, tr, _Rng())
+            assert pr.divisor == c["divisor"] and pr.shape == (4, 4)
+            lookups = [pr.quant_lookup, pr.resid_lookup]
+        elif c["gadget"] == "swiglu":
+            pr = zb.prove_swiglu(op(c["wide"]), op(c["out"]), op(c["narrow"]), op(c["resid"]),
+                                 c["mode"], ts, KEY, tr, _Rng())
+            assert pr.mode == c["mode"]
+            lookups = [pr.activation_lookup, pr.resid_lookup]
+        else:
+            pr = zb.prove_rsqrt(op(c["v"], 3), op(c["u"], 3), ts, KEY, tr, _Rng())
+            lookups = [pr.lookup]
+        if "identity" in c:
+            assert list(pr.identity_opening.values) == c["identity"]
+        for got, want in zip(lookups, c["lookups"]):
+            _check_lookup(got, want)
+        assert tr.state.hex() == c["state_end"], (c["gadget"], c["field"])
+        seen.add((c["gadget"], c["field"]))
+    assert len(seen) == 6
+
+
+def test_rescale_errors_like_reference():
+    g = load_golden("nonlinear.json")
+    p = FIELDS["test"]
+    ts = _tables(g, p, "device")
+    c = [c for c in g["cases"] if c["gadget"] == "rescale"][0]
+    op = lambda vals, k=4: _operand(vals, k, k, p, "device")  # noqa: E731
+    with pytest.raises(ValueError):
+        zb.prove_rescale(op(c["wide"]), op(c["narrow"]), op(c["resid"]), 3, ts, KEY,
+                         Transcript(b"x", p, b""), _Rng())
+    with pytest.raises(zb.ShapeMismatch):
+        zb.prove_rescale(op(c["wide"]), op(c["narrow"][:64], 3), op(c["resid"]), 16, ts, KEY,
+                         Transcript(b"x", p, b""), _Rng())
+    # a quotient outside quant_range: ElementNotInTable at the first bad index
+    bad = list(c["narrow"])
+    bad[37] = 1000
+    bad[90] = -1000
+    with pytest.raises(zb.ElementNotInTable) as e:
+        zb.prove_rescale(op(c["wide"]), op(bad), op(c["resid"]), 16, ts, KEY,
+                         Transcript(b"x", p, b""), _Rng())
+    assert e.value.index == 37
+
+
+@pytest.mark.parametrize("field", ["big", "test"])
+@pytest.mark.parametrize("shape", [(0, 0), (0, 5), (5, 0), (3, 4), (7, 6)])
+@pytest.mark.parametrize("dtype", [torch.int16, torch.int32, torch.int64])
+def test_mle_of_int_matrix(field, shape, dtype):
+    """mle_evaluate_matrix (one integer matvec) == the lifted-vector fold."""
+    import random
+
+    p = FIELDS[field]
+    spec = D.spec_for(p)
+    rv, cv = shape
+    gen = torch.Generator().manual_seed(rv * 16 + cv)
+    hi = {torch.int16: 1 << 15, torch.int32: 1 << 31, torch.int64: 1 << 62}[dtype]
+    t = torch.randint(-hi, hi, (1 << rv, 1 << cv), generator=gen, dtype=torch.int64).to(dtype)
+    rnd = random.Random(rv + cv)
+    pt = [rnd.randrange(p) for _ in range(rv + cv)]
+    Mx = DeviceMatrix.from_int_tensor(t.cuda())
+    got = M.mle_evaluate_any(Mx, pt, p)
+    want = M.mle_evaluate([int(v) % p for v in t.reshape(-1).tolist()], pt, p)
+    assert got == want

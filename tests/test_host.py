@@ -228,3 +228,30 @@ def test_boundary_errors_before_any_device_work():
     with pytest.raises(ValueError):
         zb.prove_lookup(zb.SecretVector((1, 2, 3, 4), StubCommitment(2), ()), [0] * 7, table,
                         key, tr, None)
+
+
+@pytest.mark.parametrize("name", ["silu", "silu_deriv", "exp0", "rsqrt_eps1e-5"])
+def test_table_generation_matches_reference(name):
+    """paper_2508_21393_b200.tables restates tables.py:40-117; every entry must
+    equal the reference's own table at gamma = 2^12, act_bound = 8, radices
+    (2^16,)*4 (tests/golden/tables_g4096.json, written by the reference)."""
+    import base64
+    import zlib
+
+    import numpy as np
+
+    from paper_2508_21393_b200 import tables as T
+
+    g = load_golden("tables_g4096.json")[name]
+    want = np.frombuffer(zlib.decompress(base64.b64decode(g["y_zlib_b64"])), dtype="<i4")
+    if name == "silu":
+        xs, ys = T.silu_entries(4096, 8)
+    elif name == "silu_deriv":
+        xs, ys = T.silu_deriv_entries(4096, 8)
+    elif name == "exp0":
+        xs, ys = T.exp_segment_entries(4096, (1 << 16,) * 4, 0)
+    else:
+        xs, ys = T.rsqrt_entries(4096, 8, 1e-5)
+    assert xs[0] == g["x0"] and len(xs) == g["n"]
+    assert np.array_equal(np.asarray(ys, dtype=np.int64), want.astype(np.int64))
+    assert T.quant_range(4096, 8) == (-32768, 65536) and T.residue_range(4096) == (-2048, 4096)
