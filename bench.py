@@ -356,6 +356,80 @@ def run_cfg4(steps, warmup, shape_name="7b"):
     }
 
 
+CFG5 = ("cfg5 sweep: the reference's replicated zkMat claim (gadgets.py:241-251, four "
+        "2^n-entry tables) of uniform int16 matrices, dims (n/3, n - 2 n/3, n/3), on the dense "
+        "fused round/fold engine (k_sumcheck_persistent, zkMat evaluator), the factored prover "
+        "on the same claim beside it")
+
+
+def run_sweep(ns, mont_peak=None):
+    """BASELINE config 5's scaling sweep on one GPU.  Per n: table build and
+    sumcheck timed separately (CUDA events on the proving stream), the
+    factored prover on the same transcript, and a bit-exactness check
+    between the two."""
+    import torch
+
+    import paper_2508_21393_b200 as zb
+    from paper_2508_21393_b200 import device as D
+    from paper_2508_21393_b200 import gadgets as G
+    from paper_2508_21393_b200.sumcheck import Term, absorb_claim, run_rounds
+
+    spec = D.spec_for(P_BIG)
+    stream = torch.cuda.current_stream()
+    out = []
+    for n in ns:
+        d0 = d2 = n // 3
+        d1 = n - 2 * d0
+        g = torch.Generator(device="cuda").manual_seed(n)
+        a = torch.randint(-32768, 32768, (1 << d0, 1 << d1), device="cuda", generator=g,
+                          dtype=torch.int32).short()
+        b = torch.randint(-32768, 32768, (1 << d1, 1 << d2), device="cuda", generator=g,
+                          dtype=torch.int32).short()
+        c = torch.matmul(a.double(), b.double()).round().long()
+        A, B, C = (G.DeviceMatrix.from_int_tensor(x) for x in (a, b, c))
+        tr = zb.Transcript(b"zklora-b200/sweep", P_BIG, b"%d" % n)
+        tr2 = zb.Transcript(b"zklora-b200/sweep", P_BIG, b"%d" % n)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        torch.cuda.synchronize()
+        ev[0].record(stream)
+        r_u = tr.challenge_vector(b"matmul/r_u", d0)
+        r_v = tr.challenge_vector(b"matmul/r_v", d2)
+        cneg = (-pow(2, -d1, P_BIG)) % P_BIG
+        tables = G.replicated_tables(A, B, C, (d0, d1, d2), r_u, r_v, spec)
+        ev[1].record(stream)
+        absorb_claim(tr, 0, [Term(1, (0, 1, 2)), Term(cneg, (0, 3))], 3, n)
+        rounds, point, finals = run_rounds(spec, tables, n, [(1, (0, 1, 2)), (cneg, (0, 3))], 3, tr)
+        ev[2].record(stream)
+        del tables
+        A2, B2, C2 = (G.DeviceMatrix.from_int_tensor(x) for x in (a, b, c))
+        torch.cuda.synchronize()
+        ev[3].record(stream)
+        r2 = zb.matmul_sumcheck(A2, B2, C2, (d0, d1, d2), tr2)
+        e4 = torch.cuda.Event(enable_timing=True)
+        e4.record(stream)
+        e4.synchronize()
+        build_ms = ev[0].elapsed_time(ev[1])
+        sc_ms = ev[1].elapsed_time(ev[2])
+        fac_ms = ev[3].elapsed_time(e4)
+        elems = 4 << n
+        nbytes = 96 * 4 * (1 << n)  # sec. 8d: k 2^(n-j) 32 read + k 2^(n-j-1) 32 written, summed
+        products = 10 * (1 << (n - 1)) + 18 * ((1 << (n - 1)) - 1)
+        row = {"n": n, "dims": [d0, d1, d2], "table_build_ms": build_ms, "sumcheck_ms": sc_ms,
+               "field_elems_per_s": elems / (sc_ms / 1000.0),
+               "achieved_gbs": nbytes / (sc_ms / 1000.0) / 1e9,
+               "mont_products_per_s": products / (sc_ms / 1000.0),
+               "factored_ms": fac_ms,
+               "bit_exact_dense_vs_factored": bool(
+                   [tuple(x) for x in rounds] == [tuple(x) for x in r2[0]]
+                   and tuple(finals) == tuple(r2[2]) and tr.state == tr2.state)}
+        if mont_peak:
+            row["mont_frac"] = row["mont_products_per_s"] / mont_peak
+        out.append(row)
+        del A, B, C, A2, B2, C2, a, b, c
+        torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -367,6 +441,7 @@ def main():
     ap.add_argument("--no-cfg3", action="store_true")
     ap.add_argument("--no-cfg4", action="store_true")
     ap.add_argument("--cfg4-shape", default="7b", choices=["7b", "13b"])
+    ap.add_argument("--no-cfg5", action="store_true")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -509,6 +584,15 @@ def main():
     if not args.no_cfg4:
         cfg4 = run_cfg4(max(1, args.steps // 10), 1, args.cfg4_shape)
 
+    cfg5 = None
+    if not args.no_cfg5:
+        mont_peak = 4.2e10  # Fr255 Montgomery products/s, tools/mont_bench.cu (profiles/r01)
+        cfg5 = {"workload": CFG5, "mont_peak_products_per_s": mont_peak,
+                "mont_peak_source": "tools/mont_bench.cu on this B200 (3 independent "
+                                    "products per call, 2 blocks/SM)",
+                "sweep": run_sweep([20, 22, 24, 26, 28, 30], mont_peak),
+                "block_13b": run_cfg4(1, 1, "13b")}
+
     cpu = None
     if not args.no_cpu:
         el, sec = cpu_reference_sample(0)
@@ -555,6 +639,7 @@ def main():
         "parity": parity,
         "cfg3": cfg3,
         "cfg4": cfg4,
+        "cfg5": cfg5,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -162,6 +162,7 @@ class BlockProver:
         self.stats = defaultdict(lambda: [0, 0, 0, 0.0])  # count, rounds, elems, seconds
         self.clipped = 0
         self.log = []  # [kind, rounds of each sumcheck] per gadget, in proof order
+        self.seconds = []  # per gadget, same order as log
 
     class _Rng:
         def vector(self, n):
@@ -178,8 +179,10 @@ class BlockProver:
         out = fn(*args)
         torch.cuda.synchronize()
         s = self.stats[kind]
+        dt = time.perf_counter() - t0
         s[0] += 1
-        s[3] += time.perf_counter() - t0
+        s[3] += dt
+        self.seconds.append(dt)
         return out
 
     def _count(self, kind, rounds, elems):

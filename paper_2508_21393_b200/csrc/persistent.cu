@@ -136,7 +136,8 @@ struct Red<M61> {
 // fold product + one (PROD2, SUM2PROD2) or two (PROD3) evaluation products.
 inline int lanes_for(int shape, int k) {
   if (shape == kGeneric || shape == kLogupTiled) return 0;
-  const int nout = shape == kProd2 ? 3 : shape == kProd3 ? 4 : shape == kLogup ? 16 : 6;
+  const int nout = shape == kProd2 ? 3 : shape == kProd3 ? 4 : shape == kLogup ? 16
+                 : shape == kZkMat ? 7 : 6;
   const int need = 2 * k > nout ? 2 * k : nout;  // fold lanes / output lanes
   return need <= 4 ? 4 : need <= 8 ? 8 : 16;
 }
@@ -323,6 +324,73 @@ struct EvProd3 {
     if (x == 3) qq = qx[3];
     const T m = F::mul(qq, bx);
     return (active && q < 4) ? m : F::zero();
+  }
+};
+
+// The reference's replicated zkMat claim (gadgets.py:241-251): terms
+//   c0 E A B + c1 E C   (E shared).
+// Raw sums: [0..3] sum E(x) A(x) B(x), x = 0..3 (as PROD3: 7 products);
+// [4..6] E C as (lo lo, hi hi, slope slope) (3 products).  10 products per
+// pair instead of the generic term loop.
+template <class F, int MAXK>
+struct EvZkMat {
+  using T = typename F::T;
+  static constexpr bool kGeneric = false;
+  static constexpr int NA = 7, NOUT = 7;
+  ZKL_D static void pair(T (&cur)[MAXK], const T (&df)[MAXK], int, const Terms<F>& tm,
+                         T (&acc)[NA]) {
+    const int ie = tm.fi[0][0], ia = tm.fi[0][1], ib = tm.fi[0][2], ic = tm.fi[1][1];
+    const T e0 = select_tab<F, MAXK>(cur, ie), ed = select_tab<F, MAXK>(df, ie);
+    const T a0 = select_tab<F, MAXK>(cur, ia), ad = select_tab<F, MAXK>(df, ia);
+    const T b0 = select_tab<F, MAXK>(cur, ib), bd = select_tab<F, MAXK>(df, ib);
+    const T c0 = select_tab<F, MAXK>(cur, ic), cd = select_tab<F, MAXK>(df, ic);
+    const T e1 = F::add(e0, ed);
+    T q[4], q0, q1, qc, m4, m5;
+    F::mul4(e0, a0, e1, F::add(a0, ad), ed, ad, e0, c0, q0, q1, qc, m4);
+    quad_evals<F>(q0, q1, qc, q);
+    const T b1 = F::add(b0, bd), b2 = F::add(b1, bd), b3 = F::add(b2, bd);
+    T m[4];
+    F::mul4(q[0], b0, q[1], b1, q[2], b2, q[3], b3, m[0], m[1], m[2], m[3]);
+    T m6;
+    F::mul2(e1, F::add(c0, cd), ed, cd, m5, m6);
+#pragma unroll
+    for (int x = 0; x < 4; x++) acc[x] = F::add(acc[x], m[x]);
+    acc[4] = F::add(acc[4], m4);
+    acc[5] = F::add(acc[5], m5);
+    acc[6] = F::add(acc[6], m6);
+  }
+  ZKL_D static void finish(const T (&acc)[NA], T (&out)[NOUT]) {
+#pragma unroll
+    for (int x = 0; x < NOUT; x++) out[x] = acc[x];
+  }
+  // lane mode: lanes 0..3 are PROD3's two levels (q(x) = e(x) a(x), then
+  // q(x) b(x)); lanes 4..6 compute e c at (lo, hi, slope) in the second level
+  ZKL_D static T lane(const T& v, int q, int gb, bool active, const Terms<F>& tm) {
+    const int ie = tm.fi[0][0], ia = tm.fi[0][1], ib = tm.fi[0][2], ic = tm.fi[1][1];
+    const T el = shfl_elem<F>(v, gb + 2 * ie), eh = shfl_elem<F>(v, gb + 2 * ie + 1);
+    const T al = shfl_elem<F>(v, gb + 2 * ia), ah = shfl_elem<F>(v, gb + 2 * ia + 1);
+    const int s = q < 3 ? q : 0;
+    const T p1 = F::mul(pick3<F>(el, eh, s), pick3<F>(al, ah, s));
+    const T q0 = shfl_elem<F>(p1, gb), q1 = shfl_elem<F>(p1, gb + 1);
+    const T qc = shfl_elem<F>(p1, gb + 2);
+    T qx[4];
+    quad_evals<F>(q0, q1, qc, qx);
+    const T bl = shfl_elem<F>(v, gb + 2 * ib), bh = shfl_elem<F>(v, gb + 2 * ib + 1);
+    const T cl = shfl_elem<F>(v, gb + 2 * ic), ch = shfl_elem<F>(v, gb + 2 * ic + 1);
+    const T bd = F::sub(bh, bl);
+    const int x = q & 3;
+    T bx = x == 0 ? bl : bh;
+    if (x >= 2) bx = F::add(bx, bd);
+    if (x == 3) bx = F::add(bx, bd);
+    T qq = qx[0];
+    if (x == 1) qq = qx[1];
+    if (x == 2) qq = qx[2];
+    if (x == 3) qq = qx[3];
+    const int s2 = q >= 4 && q < 7 ? q - 4 : 0;
+    const T lhs = q < 4 ? qq : pick3<F>(el, eh, s2);
+    const T rhs = q < 4 ? bx : pick3<F>(cl, ch, s2);
+    const T m = F::mul(lhs, rhs);
+    return (active && q < 7) ? m : F::zero();
   }
 };
 
@@ -1175,6 +1243,9 @@ int detect_shape(const Terms<F>& tm) {
   if (tm.nterms == 2 && tm.nf[0] == 2 && tm.nf[1] == 2 && tm.fi[0][0] == tm.fi[1][0] &&
       tm.degree >= 2)
     return kSum2Prod2;
+  if (tm.nterms == 2 && tm.nf[0] == 3 && tm.nf[1] == 2 && tm.fi[1][0] == tm.fi[0][0] &&
+      tm.degree == 3)
+    return kZkMat;
   if (tm.nterms == 5 && tm.degree == 3 && tm.nf[0] == 3 && tm.nf[1] == 2 && tm.nf[2] == 3 &&
       tm.nf[3] == 1 && tm.nf[4] == 2 && tm.fi[1][0] == tm.fi[0][0] &&
       tm.fi[2][0] == tm.fi[0][0] && tm.fi[3][0] == tm.fi[0][1] && tm.fi[4][1] == tm.fi[2][1])
@@ -1223,6 +1294,9 @@ static int dispatch(const LaunchReq<F>& q, Plan* pl, int* nout, int launch) {
     case kProd2: ZKL_SHAPE(EvProd2)
     case kProd3: ZKL_SHAPE(EvProd3)
     case kSum2Prod2: ZKL_SHAPE(EvSum2Prod2)
+    case kZkMat:
+      if constexpr (MAXK >= 4) ZKL_SHAPE(EvZkMat)
+      else ZKL_SHAPE(EvGeneric)
     case kLogup:
       if constexpr (MAXK >= 8) ZKL_SHAPE(EvLogup)
       else ZKL_SHAPE(EvGeneric)
@@ -1528,7 +1602,8 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
       if (shape == kGeneric) {
         Kc[0] = host::canon_of<F>(pm);
       } else {
-        const int nk = (shape == kLogup || shape == kLogupTiled) ? 5 : shape == kSum2Prod2 ? 2 : 1;
+        const int nk = (shape == kLogup || shape == kLogupTiled) ? 5
+                       : (shape == kSum2Prod2 || shape == kZkMat) ? 2 : 1;
         for (int t = 0; t < nk; t++) Kc[t] = host::canon_of<F>(H::mul(pm, a.tm.coef[t]));
       }
     }
@@ -1559,6 +1634,10 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
     } else if (shape == kProd2) {
       host_quad<F>(raw[0], raw[1], raw[2], ev);
       for (int x = 0; x < 4; x++) ev[x] = H::mul(ev[x], Kc[0]);
+    } else if (shape == kZkMat) {
+      T ec[4];
+      host_quad<F>(raw[4], raw[5], raw[6], ec);
+      for (int x = 0; x < 4; x++) ev[x] = H::add(H::mul(raw[x], Kc[0]), H::mul(ec[x], Kc[1]));
     } else if (shape == kSum2Prod2) {
       T e1[4], e2[4];
       host_quad<F>(raw[0], raw[1], raw[2], e1);

@@ -9,7 +9,10 @@
 
 namespace zkl {
 
-enum Shape { kGeneric = 0, kProd2 = 1, kProd3 = 2, kSum2Prod2 = 3, kLogup = 4, kLogupTiled = 5 };
+enum Shape {
+  kGeneric = 0, kProd2 = 1, kProd3 = 2, kSum2Prod2 = 3, kLogup = 4, kLogupTiled = 5,
+  kZkMat = 6
+};
 
 template <class F>
 int detect_shape(const Terms<F>& tm);

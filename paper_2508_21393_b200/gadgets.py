@@ -279,6 +279,42 @@ def matmul_sumcheck(A, B, C, dims, tr):
     return rounds_u + rounds_w + rounds_v, pt_u + pt_w + pt_v, finals
 
 
+def replicated_tables(A, B, C, dims, r_u, r_v, spec):
+    """The reference's four zkMat tables (gadgets.py:210-227) materialised on
+    the device: [eq(r_u,u) eq(r_v,v), A(u,w), B(w,v), C(u,v)] over the index
+    u || w || v (MSB first), 2^(d0+d1+d2) field elements each."""
+    d0, d1, d2 = dims
+    D0, D1, D2 = 1 << d0, 1 << d1, 1 << d2
+    W = spec.nbytes // 8
+    uv = D.eq_table(list(r_u) + list(r_v), spec)  # eq(r_u,u) eq(r_v,v) over u || v
+    a = A.as_field_vector(spec).view(D0, D1, 1, W)
+    b = B.as_field_vector(spec).view(1, D1, D2, W)
+    c = C.as_field_vector(spec).view(D0, 1, D2, W)
+    shape = (D0, D1, D2, W)
+    return [uv.view(D0, 1, D2, W).expand(shape).reshape(-1, W),
+            a.expand(shape).reshape(-1, W), b.expand(shape).reshape(-1, W),
+            c.expand(shape).reshape(-1, W)]
+
+
+def matmul_sumcheck_replicated(A, B, C, dims, tr):
+    """The reference's own zkMat sumcheck form (gadgets.py:241-251): the four
+    replicated tables materialised and proven by the dense fused round/fold
+    engine over d0+d1+d2 rounds.  Same transcript traffic and outputs as
+    matmul_sumcheck (the factored prover); it exists for the like-for-like
+    scaling sweep (BASELINE config 5) and as a cross-check of the factored
+    path at sizes the CPU oracle cannot reach."""
+    p = tr.modulus
+    spec = D.spec_for(p)
+    d0, d1, d2 = dims
+    r_u = tr.challenge_vector(b"matmul/r_u", d0)
+    r_v = tr.challenge_vector(b"matmul/r_v", d2)
+    cneg = (-inverse_pow2(d1, p)) % p
+    tables = replicated_tables(A, B, C, dims, r_u, r_v, spec)
+    n = d0 + d1 + d2
+    absorb_claim(tr, 0, [Term(1, (0, 1, 2)), Term(cneg, (0, 3))], 3, n)
+    return run_rounds(spec, tables, n, [(1, (0, 1, 2)), (cneg, (0, 3))], 3, tr)
+
+
 def prove_matmul(a, b, c, key, tr, rng):
     """Drop-in for zklora.gadgets.prove_matmul (gadgets.py:230-265)."""
     p = tr.modulus
