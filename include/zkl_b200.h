@@ -170,6 +170,17 @@ int zkl_pair_multiplicities(int field, const void* x, int x_type, const void* y,
                             const void* secret, const void* table, uint64_t n, uint32_t* counts,
                             uint32_t* index_out, int64_t* first_miss, void* stream);
 
+/* compute_multiplicities (lookup.py:91-99) for a single-column table that is
+ * the consecutive integer range table_x0 .. table_x0+n-1 (quant_range /
+ * residue_range, tables.py:109-117) and a secret given as a signed int16 /
+ * int32 / int64 device column (x_type 1 / 2 / 3): counts[n] (uint32), the
+ * table index of every entry in index_out[d] (may be NULL), ZKL_ERR_MISSING
+ * with *first_miss = the first entry outside the range.  Field-independent:
+ * the secret is never lifted. */
+int zkl_range_multiplicities(const void* x, int x_type, uint64_t d, int64_t table_x0,
+                             uint64_t n, uint32_t* counts, uint32_t* index_out,
+                             int64_t* first_miss, void* stream);
+
 /* dst[i] = src[idx[i]] (+ add when add_canon != NULL), i < n; every idx[i]
  * must be < src_n (caller-checked).  The secret-side logUp columns
  * (lookup.py:175-202) of a lookup whose secret entries are table entries. */
@@ -210,6 +221,11 @@ int zkl_matmul_prove(int field, int a_type, const void* A, int b_type, const voi
  * B, T+beta, M (n entries, read).  u_canon: the eq point (num_vars scalars);
  * coeffs: the five term coefficients (lookup.py:116-126), canonical.
  * flags bit 0: A = 1/(S+beta) entrywise (lets round 0 skip two products).
+ * flags bit 1 (indexed, rounds >= 2): tables[6] is the uint32 query -> table
+ * index of a lookup whose secret entries are table entries; A = B[index] and
+ * S+beta = (T+beta)[index] are read through it in rounds 0 and 1 and never
+ * materialised, and tables[1], tables[2] are 2^(num_vars-1)-entry outputs
+ * written by the first fold.
  * The remaining tile_log rounds run through zkl_sumcheck_prove on the 7
  * tables of n entries (indicator = ones).  ZKL_ERR_UNSUPPORTED in stepwise
  * mode or for n < 32. */

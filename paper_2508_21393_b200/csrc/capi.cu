@@ -132,7 +132,7 @@ static int logup_tiled_impl(void* const* tables, int tile_log, int num_vars, int
   for (int t = 0; t < 5; t++) c[t] = load_canon<F>(coeffs_canon + F::kBytes * t);
   std::vector<T> u(num_vars);
   for (int j = 0; j < num_vars; j++) u[j] = load_canon<F>(u_canon + (size_t)F::kBytes * j);
-  return op_logup_tiled<F>(tables, tile_log, num_vars, rounds, u.data(), c, flags & 1,
+  return op_logup_tiled<F>(tables, tile_log, num_vars, rounds, u.data(), c, flags & 3,
                            state_inout, rounds_out, point_out, (cudaStream_t)stream);
 }
 extern "C" {
@@ -262,6 +262,12 @@ int zkl_pair_multiplicities(int field, const void* x, int x_type, const void* y,
                             uint32_t* index_out, int64_t* first_miss, void* stream) {
   D(field, op_pair_multiplicities<F>(x, x_type, y, y_type, d, table_x0, table_y, secret, table, n,
                                      counts, index_out, first_miss, (cudaStream_t)stream));
+}
+int zkl_range_multiplicities(const void* x, int x_type, uint64_t d, int64_t table_x0,
+                             uint64_t n, uint32_t* counts, uint32_t* index_out,
+                             int64_t* first_miss, void* stream) {
+  return op_range_multiplicities(x, x_type, d, table_x0, n, counts, index_out, first_miss,
+                                 (cudaStream_t)stream);
 }
 int zkl_gather(int field, void* dst, const void* src, uint64_t src_n, const uint32_t* idx,
                uint64_t n, const uint8_t* add_canon, void* stream) {

@@ -229,6 +229,89 @@ int op_pair_multiplicities(const void* x, int xt, const void* y, int yt, uint64_
   if (fm != ~0ull) { *first_miss = (int64_t)fm; return kErrMissing; }
   return kOk;
 }
+// Single-column lookups against a table that IS the consecutive integer
+// range x0 .. x0+n-1 (quant_range / residue_range, tables.py:109-117): a
+// query's bin is its offset, and a query outside the range is in no table
+// entry, so no field value is needed at all (the secret is never lifted).
+// Small tables (n <= kRangeSmemBins) count in shared memory and flush once per
+// block: the 2^12-entry residue table otherwise serialises 2^27 global
+// atomics on 4096 counters.
+constexpr uint32_t kRangeSmemBins = 12288;  // 48 KB of uint32 counters
+
+template <class TX, bool SMEM>
+__global__ void __launch_bounds__(256) k_range_count(const TX* xs, uint64_t d, int64_t x0,
+                                                     uint32_t n, uint32_t* counts,
+                                                     unsigned long long* first_miss,
+                                                     uint32_t* index_out) {
+  extern __shared__ uint32_t sh_bins[];
+  if constexpr (SMEM) {
+    for (uint32_t b = threadIdx.x; b < n; b += blockDim.x) sh_bins[b] = 0;
+    __syncthreads();
+  }
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t run_bin = kEmpty, run_cnt = 0;
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < d; base += stride) {
+    const uint64_t i = base + threadIdx.x;
+    uint32_t hit = kEmpty;
+    if (i < d) {
+      const int64_t idx = (int64_t)xs[i] - x0;
+      if (idx >= 0 && idx < (int64_t)n) hit = (uint32_t)idx;
+      else atomicMin(first_miss, (unsigned long long)i);
+      if (index_out) index_out[i] = hit;
+    }
+    if constexpr (SMEM) {
+      if (hit != kEmpty) atomicAdd(&sh_bins[hit], 1u);
+    } else {
+      count_hit(hit, counts, run_bin, run_cnt);
+    }
+  }
+  if constexpr (SMEM) {
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < n; b += blockDim.x)
+      if (sh_bins[b]) atomicAdd(&counts[b], sh_bins[b]);
+  } else {
+    if (run_cnt && (threadIdx.x & 31) == 0) atomicAdd(&counts[run_bin], run_cnt);
+  }
+}
+
+int op_range_multiplicities(const void* x, int xt, uint64_t d, int64_t x0, uint64_t n,
+                            uint32_t* counts, uint32_t* index_out, int64_t* first_miss,
+                            cudaStream_t s) {
+  *first_miss = -1;
+  if (n == 0 || n > (1ull << 31)) { set_error("range multiplicities: bad table size"); return kErrArg; }
+  void* ws;
+  int rc = scratch_reserve(64, &ws, s);
+  if (rc) return rc;
+  unsigned long long* flag = (unsigned long long*)ws;
+  ZKL_CUDA(cudaMemsetAsync(flag, 0xff, 8, s));
+  ZKL_CUDA(cudaMemsetAsync(counts, 0, n * 4, s));
+  if (d) {
+    const bool smem = n <= kRangeSmemBins;
+    // shared-memory bins: a few blocks per SM, each flushes n counters once
+    const unsigned g = smem ? grid_for(d, 256, 2) : grid_for(d, 256);
+    const size_t sb = smem ? n * 4 : 0;
+#define ZKL_RC(TX)                                                                          \
+  (smem ? k_range_count<TX, true><<<g, 256, sb, s>>>((const TX*)x, d, x0, (uint32_t)n, counts, \
+                                                     flag, index_out)                       \
+        : k_range_count<TX, false><<<g, 256, 0, s>>>((const TX*)x, d, x0, (uint32_t)n, counts, \
+                                                     flag, index_out))
+    if (xt == 1) ZKL_RC(int16_t);
+    else if (xt == 2) ZKL_RC(int32_t);
+    else if (xt == 3) ZKL_RC(int64_t);
+    else { set_error("range multiplicities: int16/int32/int64 columns only"); return kErrArg; }
+#undef ZKL_RC
+    ZKL_LAUNCH_CHECK();
+  }
+  void* pin;
+  if ((rc = pinned_reserve(16, &pin))) return rc;
+  unsigned long long fm;
+  ZKL_CUDA(cudaMemcpyAsync(pin, flag, 8, cudaMemcpyDeviceToHost, s));
+  ZKL_CUDA(cudaStreamSynchronize(s));
+  memcpy(&fm, pin, 8);
+  if (fm != ~0ull) { *first_miss = (int64_t)fm; return kErrMissing; }
+  return kOk;
+}
+
 template int op_pair_multiplicities<Fr255>(const void*, int, const void*, int, uint64_t, int64_t,
                                            const int32_t*, const void*, const void*, uint64_t,
                                            uint32_t*, uint32_t*, int64_t*, cudaStream_t);

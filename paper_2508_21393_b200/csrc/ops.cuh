@@ -47,6 +47,14 @@ struct Terms {
   typename F::T coef[kMaxTerms];
   int tile_log;  // LOGUP_TILED: log2 of the table side's size (the low index bits)
   int inv_pair;  // LOGUP_TILED: A = 1/S entrywise before the first fold
+  // LOGUP_TILED, indexed: the secret-side columns are never gathered.  Entry i
+  // of A / S+beta is side_a / side_s[sidx[i]] (the table side, indexed by the
+  // multiplicity histogram's query -> table index) until the first fold has
+  // written them; rounds 0 and 1 (half == sidx_d / 4) read through sidx.
+  const uint32_t* sidx;
+  const typename F::T* side_a;
+  const typename F::T* side_s;
+  uint64_t sidx_d;
 };
 template <class F>
 struct Post {
@@ -77,6 +85,9 @@ template <class F>
 int op_multiplicities(const void* secret, uint64_t d, const void* table, uint64_t n,
                       uint32_t* counts, int64_t* first_miss, cudaStream_t s,
                       uint32_t* index_out = nullptr);
+int op_range_multiplicities(const void* x, int xt, uint64_t d, int64_t x0, uint64_t n,
+                            uint32_t* counts, uint32_t* index_out, int64_t* first_miss,
+                            cudaStream_t s);
 template <class F>
 int op_pair_multiplicities(const void* x, int xt, const void* y, int yt, uint64_t d, int64_t x0,
                            const int32_t* ty, const void* secret, const void* table, uint64_t n,

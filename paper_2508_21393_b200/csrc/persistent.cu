@@ -546,6 +546,7 @@ struct EvLogupTiled {
     const T* Sb = tabs.t[2];
     const T* el = tabs.t[3];
     const bool inv0 = !fold && tm.inv_pair;
+    const bool idx_fold = fold && tm.sidx != nullptr && (half << 2) == tm.sidx_d;
     T p0 = F::zero(), p1 = F::zero(), p2 = F::zero();
     uint64_t cur = ~0ull;
     auto flush = [&](uint64_t tib) {
@@ -571,10 +572,28 @@ struct EvLogupTiled {
       if (fold) {
         T* At = tabs.t[1];
         T* St = tabs.t[2];
-        const T xa = ld_cg(At + i), ya = ld_cg(At + i + half);
-        const T xs = ld_cg(St + i), ys = ld_cg(St + i + half);
-        T da = F::sub(ld_cg(At + i + 2 * half), xa), db = F::sub(ld_cg(At + i + 3 * half), ya);
-        T ds = F::sub(ld_cg(St + i + 2 * half), xs), dt = F::sub(ld_cg(St + i + 3 * half), ys);
+        T xa, ya, xs, ys, da, db, ds, dt;
+        if (idx_fold) {  // first fold: the unfolded columns are table entries
+          const uint32_t j0 = __ldg(tm.sidx + i), j1 = __ldg(tm.sidx + i + half);
+          const uint32_t j2 = __ldg(tm.sidx + i + 2 * half), j3 = __ldg(tm.sidx + i + 3 * half);
+          xa = tm.side_a[j0];
+          ya = tm.side_a[j1];
+          xs = tm.side_s[j0];
+          ys = tm.side_s[j1];
+          da = F::sub(tm.side_a[j2], xa);
+          db = F::sub(tm.side_a[j3], ya);
+          ds = F::sub(tm.side_s[j2], xs);
+          dt = F::sub(tm.side_s[j3], ys);
+        } else {
+          xa = ld_cg(At + i);
+          ya = ld_cg(At + i + half);
+          xs = ld_cg(St + i);
+          ys = ld_cg(St + i + half);
+          da = F::sub(ld_cg(At + i + 2 * half), xa);
+          db = F::sub(ld_cg(At + i + 3 * half), ya);
+          ds = F::sub(ld_cg(St + i + 2 * half), xs);
+          dt = F::sub(ld_cg(St + i + 3 * half), ys);
+        }
         F::mul4r(r, da, db, ds, dt);
         a0 = F::add(xa, da);
         const T a1 = F::add(ya, db);
@@ -586,6 +605,12 @@ struct EvLogupTiled {
         St[i + half] = s1;
         ad = F::sub(a1, a0);
         sd = F::sub(s1, s0);
+      } else if (tm.sidx) {
+        const uint32_t j0 = __ldg(tm.sidx + i), j1 = __ldg(tm.sidx + i + half);
+        a0 = tm.side_a[j0];
+        ad = F::sub(tm.side_a[j1], a0);
+        s0 = tm.side_s[j0];
+        sd = F::sub(tm.side_s[j1], s0);
       } else {
         a0 = ld_cg(A + i);
         ad = F::sub(ld_cg(A + i + half), a0);
@@ -1801,13 +1826,20 @@ int op_sumcheck_prove(void* const* tables, int k, int num_vars, const Terms<F>& 
 // tables: [E_out (2^tile_log, written), A, S+beta (2^num_vars, folded in
 // place), B, T+beta, M (2^tile_log)]; u: the eq point (num_vars, storage
 // form); coefs: the five Eq.-7 term coefficients (storage form);
-// inv_pair: A = 1/S entrywise (the prover's construction).
+// flags: 1 = A is 1/S entrywise (the prover's construction); 2 = indexed:
+// tables[6] is the uint32 query -> table index, A = B[index], S = T[index]
+// are never materialised, and tables[1], tables[2] are 2^(num_vars-1)-entry
+// outputs that the first fold writes.
 template <class F>
 int op_logup_tiled(void* const* tables, int tile_log, int num_vars, int rounds,
-                   const typename F::T* u, const typename F::T* coefs, int inv_pair,
+                   const typename F::T* u, const typename F::T* coefs, int flags,
                    uint8_t* state, uint8_t* rounds_out, uint8_t* point_out, cudaStream_t s) {
   using T = typename F::T;
   using H = typename host::For<F>::H;
+  if ((flags & 2) && rounds < 2) {
+    set_error("logup_tiled: the indexed mode needs at least two tiled rounds");
+    return kErrArg;
+  }
   if (no_persistent()) {
     set_error("logup_tiled: needs the persistent engine (stepwise mode active)");
     return kErrUnsupported;
@@ -1861,7 +1893,13 @@ int op_logup_tiled(void* const* tables, int tile_log, int num_vars, int rounds,
   tm.degree = 3;
   for (int t = 0; t < 5; t++) tm.coef[t] = coefs[t];
   tm.tile_log = tile_log;
-  tm.inv_pair = inv_pair ? 1 : 0;
+  tm.inv_pair = (flags & 1) ? 1 : 0;
+  if (flags & 2) {  // indexed: tables[6] = query -> table index, A / S written from round 1
+    tm.sidx = (const uint32_t*)tables[6];
+    tm.side_a = (const T*)tables[3];
+    tm.side_s = (const T*)tables[4];
+    tm.sidx_d = 1ull << num_vars;
+  }
   void* phase_tables[4] = {d_hi, tables[1], tables[2], eq_lo};
   HostTranscript tr;
   memcpy(tr.state, state, 64);

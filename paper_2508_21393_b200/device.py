@@ -158,6 +158,30 @@ class DeviceVector:
         return download(self.buf, self.spec, self.n)
 
 
+class LiftedColumn(DeviceVector):
+    """A DeviceVector backed by a signed integer device column (x mod p):
+    the 32-byte field buffer is lifted only when something reads it.  Range
+    lookups bin and gather straight from the integers (lookup.py), so their
+    secrets are usually never lifted."""
+
+    __slots__ = ("col", "_buf")
+
+    def __init__(self, col, spec):
+        self.col = col.reshape(-1)
+        self._buf = None
+        self.n, self.spec = self.col.numel(), spec
+
+    @property
+    def buf(self):
+        if self._buf is None:
+            self._buf = lift(self.col, self.spec)
+        return self._buf
+
+    def value(self, i):
+        """Entry i as a canonical residue, without lifting the column."""
+        return int(self.col[i]) % self.spec.modulus
+
+
 def field_buffer(values, spec):
     """Device storage for a DeviceVector or a sequence of residues."""
     if isinstance(values, DeviceVector):

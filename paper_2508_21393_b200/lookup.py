@@ -182,13 +182,33 @@ def multiplicities_pair(secret, table, x, y, tx, ty):
 def multiplicities_range(secret, table, col, tcol):
     """multiplicities_indexed for a single-column table whose entries are the
     consecutive integers tcol (quant_range / residue_range, tables.py:109-117)
-    and a secret given by its int16/int32 device column: bins by offset
-    (zkl_pair_multiplicities with y = x).  None when that does not apply."""
+    and a secret given by its signed int device column: bins by offset
+    (zkl_range_multiplicities), never lifting the secret.  A secret entry
+    outside the range is in no table entry: ElementNotInTable with the first
+    such index, like lookup.py:96-98."""
     import torch
 
-    if col.dtype not in (torch.int16, torch.int32):
+    if col.dtype not in (torch.int16, torch.int32, torch.int64):
         return None
-    return multiplicities_pair(secret, table, col, col, tcol, tcol)
+    n = len(table.entries)
+    x0 = int(tcol[0])
+    spec = secret.spec
+    xs = col.contiguous().view(-1)
+    d = xs.numel()
+    counts = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    index = torch.empty(max(d, 1), dtype=torch.int32, device="cuda")
+    fm = ctypes.c_int64(-1)
+    rc = N.lib().zkl_range_multiplicities(D.ptr(xs), D._INT_TYPES[xs.dtype], d, x0, n,
+                                          D.ptr(counts), D.ptr(index), ctypes.byref(fm),
+                                          D.stream())
+    if rc == N.ZKL_ERR_MISSING:
+        value = (secret.value(fm.value) if isinstance(secret, D.LiftedColumn)
+                 else D.read_scalar(D.field_buffer(secret, spec), spec, fm.value))
+        raise TYPES["ElementNotInTable"](fm.value, value)
+    N.check(rc)
+    out = D.empty(spec, n)
+    N.check(N.lib().zkl_lift_u32(spec.fid, D.ptr(out), D.ptr(counts), n, D.stream()))
+    return D.DeviceVector(out, n, spec), index
 
 
 def _gather(spec, src, src_n, index, n, add=None):
@@ -282,7 +302,10 @@ def prove_lookup(secret, multiplicities, table, key, tr, rng, secret_index=None)
     tr.append(b"lookup/secret", secret.commitment.serialize(group))
     tr.append(b"lookup/mult", m_commitment.serialize(group))
 
-    s_buf = D.field_buffer(entries, spec)
+    # a LiftedColumn secret is only lifted when a path below needs the field
+    # values (the indexed, tiled d >= n path never does)
+    lazy = isinstance(entries, D.LiftedColumn) and secret_index is not None and d >= n
+    s_buf = None if lazy else D.field_buffer(entries, spec)
     t_buf = D.field_buffer(table.entries, spec)
     m_buf = D.field_buffer(multiplicities, spec)
 
@@ -294,8 +317,7 @@ def prove_lookup(secret, multiplicities, table, key, tr, rng, secret_index=None)
         if secret_index is not None:
             z1 = None
             inv_t, z2 = batch_inverse_device(t_buf, n, spec, add=beta)
-            if z2 is None:
-                inv_s = _gather(spec, inv_t, n, secret_index, d)
+            inv_s = None  # gathered from inv_t on first use (the tiled path reads through the index)
         else:
             inv_s, z1 = batch_inverse_device(s_buf, d, spec, add=beta)
             z2 = None
@@ -312,11 +334,15 @@ def prove_lookup(secret, multiplicities, table, key, tr, rng, secret_index=None)
     # helper-column commitments (lookup.py:175-180)
     a_rows, _ = be.split_shape(secret.num_vars)
     a_blinding = rng.vector(a_rows)
+    def gathered_inv_s():
+        return inv_s if inv_s is not None else _gather(spec, inv_t, n, secret_index, d)
+
     if stub:
         inv_s_host = inv_t_host = None
         a_commitment = be.commit(key, _Sized(d), a_blinding)
         b_commitment = be.commit(key, _Sized(n))
     else:
+        inv_s = gathered_inv_s()
         inv_s_host = D.download(inv_s, spec, d)
         inv_t_host = D.download(inv_t, spec, n)
         a_commitment = be.commit(key, inv_s_host, a_blinding)
@@ -346,6 +372,9 @@ def prove_lookup(secret, multiplicities, table, key, tr, rng, secret_index=None)
                                   m_blinding, m_rows, a_blinding, inv_s, inv_s_host, inv_t_host,
                                   s_buf, num_vars, rounds, point, finals, d, n)
 
+    if s_buf is None:
+        s_buf = D.field_buffer(entries, spec)
+    inv_s = gathered_inv_s()
     # lifted columns (lookup.py:188-202)
     if d <= n:
         A = _expand(spec, n, inv_s, d, 0)
@@ -387,14 +416,22 @@ def _tiled_sumcheck(spec, tr, d, n, s_buf, inv_s, t_buf, inv_t, m_buf, beta, u, 
     declines (stepwise mode under profilers, n < 32)."""
     tile_log = (n - 1).bit_length()
     r1 = num_vars - tile_log
-    # inv_s / inv_t are consumed in place: with d > n the openings use the
-    # sumcheck finals, and the commitment path downloaded them already
-    A = inv_s
+    # indexed: A_i = 1/(beta + t_idx(i)) and S_i = t_idx(i) + beta are read
+    # through the index in rounds 0-1 and never materialised; the first fold
+    # writes d/2-entry tables
+    indexed = secret_index is not None and r1 >= 2
     Tb = _expand(spec, n, t_buf, n, 1, add=beta)
-    if secret_index is not None:  # s_i + beta == t_index(i) + beta
-        Sb = _gather(spec, Tb, n, secret_index, d)
+    if indexed:
+        A = D.empty(spec, d // 2)
+        Sb = D.empty(spec, d // 2)
     else:
-        Sb = _expand(spec, d, s_buf, d, 1, add=beta)
+        # inv_s / inv_t are consumed in place: with d > n the openings use the
+        # sumcheck finals, and the commitment path downloaded them already
+        A = inv_s if inv_s is not None else _gather(spec, inv_t, n, secret_index, d)
+        if secret_index is not None:  # s_i + beta == t_index(i) + beta
+            Sb = _gather(spec, Tb, n, secret_index, d)
+        else:
+            Sb = _expand(spec, d, s_buf, d, 1, add=beta)
     Bb = inv_t
     Mb = m_buf.clone()  # may be the caller's DeviceVector buffer
     E = D.empty(spec, n)
@@ -404,11 +441,13 @@ def _tiled_sumcheck(spec, tr, d, n, s_buf, inv_s, t_buf, inv_t, m_buf, beta, u, 
     state = ctypes.create_string_buffer(bytes(tr.state), 64)
     rbuf = (ctypes.c_uint8 * (r1 * 4 * nb))()
     pbuf = (ctypes.c_uint8 * (r1 * nb))()
-    ptrs = (ctypes.c_void_p * 6)(*[t.data_ptr() for t in (E, A, Sb, Bb, Tb, Mb)])
+    ptrs = (ctypes.c_void_p * 7)(*[t.data_ptr() for t in (E, A, Sb, Bb, Tb, Mb)],
+                                 secret_index.data_ptr() if indexed else None)
     coeffs = D.scalars_bytes([t.coefficient for t in terms], spec)
     ub = D.scalars_bytes(list(u), spec)
-    rc = N.lib().zkl_logup_tiled_rounds(spec.fid, ptrs, tile_log, num_vars, r1, ub, coeffs, 1,
-                                        state, rbuf, pbuf, D.stream())
+    rc = N.lib().zkl_logup_tiled_rounds(spec.fid, ptrs, tile_log, num_vars, r1, ub, coeffs,
+                                        1 | (2 if indexed else 0), state, rbuf, pbuf,
+                                        D.stream())
     if rc == N.ZKL_ERR_UNSUPPORTED:
         tr.state = before
         log = getattr(tr, "log", None)

@@ -6,15 +6,16 @@ Mirrors of zklora.gadgets (reference gadgets.py):
   prove_rsqrt    gadgets.py:842-847  (pair lookup)
 with the same transcript traffic, argument meaning and exceptions.  They
 exist so that tensors that live on the GPU as int16/int32/int64 matrices
-(DeviceMatrix) are proven without ever building Python lists: the lookup
-secrets are lifted on the device, multiplicities are binned on the device
-and the logUp sumchecks run on the round engine (lookup.py).  With host
+(DeviceMatrix) are proven without ever building Python lists: range-table
+lookups bin their integer secrets by offset (the secret is lifted to field
+elements only if a path needs it), pair lookups compress on the device, and
+the logUp sumchecks run on the round engine (lookup.py).  With host
 ProverTensors they behave like the reference functions (which, once
 install() has run, already reach this backend through prove_lookup).
 
 Tables: `TableSet` holds the same fields as tables.py:156-168; its single
 column tables may carry DeviceVector entries and its pair tables int32
-device columns (`device_table_set`).
+device columns (`device_range_table`, `device_pair_table`).
 """
 
 from dataclasses import dataclass
@@ -127,11 +128,11 @@ def _range_lookup(pt, table, key, tr, rng):
     if col is not None and isinstance(table.entries, D.DeviceVector):
         spec = table.entries.spec
         flat = col.reshape(-1)
-        secret = SecretVector(D.DeviceVector(D.lift(flat, spec), flat.numel(), spec),
-                              pt.ref.commitment, tuple(pt.blinding))
+        secret = SecretVector(D.LiftedColumn(flat, spec), pt.ref.commitment,
+                              tuple(pt.blinding))
         got = None
         tcol = getattr(table, "int_column", None)
-        if tcol is not None:
+        if tcol is not None:  # the table is exactly the range tcol[0] .. tcol[0]+n-1
             got = multiplicities_range(secret.entries, table, flat, tcol)
         counts, index = got if got is not None else multiplicities_indexed(secret.entries, table)
         return prove_lookup(secret, counts, table, key, tr, rng, secret_index=index)

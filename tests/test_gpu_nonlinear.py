@@ -182,3 +182,35 @@ def test_replicated_dense_matmul_matches_factored_and_oracle(field, dims):
     out = zkmat.prove_dense(A, B, C, dims, t3)
     assert [list(x) for x in r1[0]] == [list(x) for x in out[0]]
     assert t3.state == t1.state
+
+
+@pytest.mark.parametrize("n", [16, 4096, 1 << 16])
+@pytest.mark.parametrize("dtype", [torch.int16, torch.int32, torch.int64])
+def test_range_multiplicities_vs_bincount(n, dtype):
+    """zkl_range_multiplicities (shared-memory bins for n <= 12288, warp-merged
+    global atomics above) against torch.bincount, skewed inputs included."""
+    from paper_2508_21393_b200 import lookup as L
+
+    p = FIELDS["big"]
+    spec = D.spec_for(p)
+    lo = -(n // 2)
+    tab = NL.device_range_table(lo, n, spec, StubCommitment(_log2(n)), "r")
+    g = torch.Generator(device="cuda").manual_seed(n)
+    x = torch.randint(lo, lo + n, (1 << 20,), device="cuda", generator=g, dtype=torch.int64)
+    x[: 1 << 18] = lo + n // 3  # one hot bin (padding-like skew)
+    col = x.to(dtype)
+    sec = D.LiftedColumn(col, spec)
+    counts, index = L.multiplicities_range(sec, tab, col, tab.int_column)
+    want = torch.bincount((x - lo).long(), minlength=n)
+    got = torch.tensor(D.download(counts.buf, spec, n), dtype=torch.int64)
+    assert torch.equal(got, want.cpu())
+    assert torch.equal(index[: x.numel()].long(), (x - lo).long())
+    assert sec._buf is None  # never lifted
+    if dtype == torch.int16 and n == 1 << 16:
+        return  # every int16 is in the table
+    bad = col.clone()
+    bad[777] = lo + n
+    bad[900] = lo - 1
+    with pytest.raises(zb.ElementNotInTable) as e:
+        L.multiplicities_range(D.LiftedColumn(bad, spec), tab, bad, tab.int_column)
+    assert e.value.index == 777 and e.value.value == int(bad[777]) % p
