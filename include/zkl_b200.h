@@ -128,6 +128,15 @@ int zkl_transcript_append(uint8_t* state_inout, const uint8_t* label, uint64_t l
                           const uint8_t* data, uint64_t data_len);
 int zkl_transcript_challenge(int field, uint8_t* state_inout, const char* label,
                              uint8_t* out_canon);
+/* count appends of canonical little-endian integers (stride bytes each,
+ * absorbed in their minimal >= 1-byte encoding) under one label: the
+ * reference's per-coordinate / per-value opening records (commit.py:192-195). */
+int zkl_transcript_append_ints(uint8_t* state_inout, const uint8_t* label, uint64_t label_len,
+                               const uint8_t* values, uint64_t count, uint64_t stride);
+/* Transcript.challenge_vector (transcript.py:44-45): count challenges under
+ * "<label>/<i>", canonical scalars into out_canon. */
+int zkl_transcript_challenge_vector(int field, uint8_t* state_inout, const char* label,
+                                    uint64_t count, uint8_t* out_canon);
 
 /* After the last round: final_values[j] = fold(tables[j], r_last)[0]
  * (sumcheck.py:129-130), tables of size 2. */
@@ -169,6 +178,17 @@ int zkl_pair_multiplicities(int field, const void* x, int x_type, const void* y,
                             uint64_t d, int64_t table_x0, const int32_t* table_y,
                             const void* secret, const void* table, uint64_t n, uint32_t* counts,
                             uint32_t* index_out, int64_t* first_miss, void* stream);
+
+/* rescale_witness (gadgets.py:563-580) / swiglu_witness narrowing: for each
+ * signed wide entry w (int16 / int32 / int64 column, wide_type 1 / 2 / 3),
+ * centered_divmod (quantize.py:101-104) q = floor((w + divisor/2) / divisor),
+ * r = w - divisor q, written as int16 q_out[i] and r_out[i] = r * lift.  A
+ * quotient outside [qmin, qmax] is the reference's RangeViolation:
+ * ZKL_ERR_MISSING with *first_bad = its first index, unless clip != 0, in which
+ * case q is clamped and *n_bad counts the clamped entries (status ZKL_OK). */
+int zkl_rescale_witness(const void* wide, int wide_type, uint64_t n, int64_t divisor,
+                        int64_t lift, int64_t qmin, int64_t qmax, int16_t* q_out, int16_t* r_out,
+                        int clip, int64_t* first_bad, uint64_t* n_bad, void* stream);
 
 /* compute_multiplicities (lookup.py:91-99) for a single-column table that is
  * the consecutive integer range table_x0 .. table_x0+n-1 (quant_range /

@@ -27,7 +27,7 @@ EXPORTS = (
     "zkl_shake256", "zkl_transcript_append", "zkl_transcript_challenge", "zkl_matmul_prove",
     "zkl_prof_enable", "zkl_prof_collect", "zkl_pair_combine", "zkl_logup_tiled_rounds",
     "zkl_multiplicities_index", "zkl_gather", "zkl_pair_multiplicities",
-    "zkl_range_multiplicities",
+    "zkl_range_multiplicities", "zkl_rescale_witness", "zkl_transcript_append_ints", "zkl_transcript_challenge_vector",
 )
 
 
@@ -83,6 +83,11 @@ _SIGS = {
     "zkl_gather": ([_i32, _vp, _vp, _u64, _vp, _u64, _u8p, _vp], ctypes.c_int),
     "zkl_pair_multiplicities": ([_i32, _vp, _i32, _vp, _i32, _u64, ctypes.c_int64, _vp, _vp, _vp,
                                  _u64, _vp, _vp, _i64p, _vp], ctypes.c_int),
+    "zkl_transcript_append_ints": ([_vp, ctypes.c_char_p, _u64, _vp, _u64, _u64], ctypes.c_int),
+    "zkl_transcript_challenge_vector": ([_i32, _vp, ctypes.c_char_p, _u64, _vp], ctypes.c_int),
+    "zkl_rescale_witness": ([_vp, _i32, _u64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                             ctypes.c_int64, _vp, _vp, _i32, _i64p,
+                             ctypes.POINTER(ctypes.c_uint64), _vp], ctypes.c_int),
     "zkl_range_multiplicities": ([_vp, _i32, _u64, ctypes.c_int64, _u64, _vp, _vp, _i64p, _vp],
                                  ctypes.c_int),
     "zkl_pair_combine": ([_i32, _vp, _vp, _i32, _vp, _i32, _u64, _u8p, _vp], ctypes.c_int),

@@ -41,7 +41,7 @@ from .commit_stub import StubCommitment, StubKey
 from .gadgets import DeviceMatrix, ProverTensor, TensorRef, prove_elementprod, prove_matmul
 from .gadgets import prove_pair_lookup
 from .nonlinear import (TableSet, device_pair_table, device_range_table,
-                        prove_rescale, prove_rsqrt, prove_swiglu)
+                        prove_rescale, prove_rsqrt, prove_swiglu, rescale_witness_device)
 
 
 @dataclass(frozen=True)
@@ -138,7 +138,11 @@ def _mm(a, b):
 
 def _divmod(wide, fp):
     """centered_divmod (quantize.py:101-104) with the quotient clipped to the
-    quant_range domain; returns (q int16, r int16, clipped count)."""
+    quant_range domain; returns (q int16, r int16, clipped count).  On the GPU
+    one fused pass (nonlinear.rescale_witness_device); the torch form below is
+    the CPU path the golden generator drives the reference with."""
+    if wide.is_cuda:
+        return rescale_witness_device(wide, fp.zeta, fp, clip=True)
     d = fp.zeta
     q = torch.div(wide + d // 2, d, rounding_mode="floor")
     r = (wide - d * q).to(torch.int16)

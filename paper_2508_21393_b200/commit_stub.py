@@ -57,8 +57,15 @@ def open_batch(key, tables, blindings, point, tr, rng, values=None):
         from .mle import mle_evaluate_any
 
         values = [mle_evaluate_any(t, point, tr.modulus) for t in tables]
-    for r in point:
-        tr.append(b"open/point", r)
-    for y in values:
-        tr.append(b"open/value", y)
+    _append_all(tr, b"open/point", point)
+    _append_all(tr, b"open/value", values)
     return list(values), None
+
+
+def _append_all(tr, label, values):
+    batch = getattr(tr, "append_ints", None)
+    if batch is not None:
+        batch(label, values)
+    else:  # a foreign transcript (e.g. the reference's own)
+        for v in values:
+            tr.append(label, v)

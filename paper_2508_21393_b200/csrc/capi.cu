@@ -236,6 +236,38 @@ int zkl_transcript_challenge(int field, uint8_t* state_inout, const char* label,
                              uint8_t* out_canon) {
   D(field, transcript_challenge<F>(state_inout, label, out_canon));
 }
+int zkl_transcript_append_ints(uint8_t* state_inout, const uint8_t* label, uint64_t label_len,
+                               const uint8_t* values, uint64_t count, uint64_t stride) {
+  if (stride == 0 || stride > 64) {
+    set_error("transcript_append_ints: bad stride %llu", (unsigned long long)stride);
+    return kErrArg;
+  }
+  HostTranscript tr;
+  memcpy(tr.state, state_inout, 64);
+  for (uint64_t i = 0; i < count; i++) {
+    const uint8_t* v = values + i * stride;
+    size_t len = (size_t)stride;
+    while (len > 1 && v[len - 1] == 0) len--;  // minimal little-endian, >= 1 byte
+    tr.append((const char*)label, (size_t)label_len, v, len);
+  }
+  memcpy(state_inout, tr.state, 64);
+  return kOk;
+}
+int zkl_transcript_challenge_vector(int field, uint8_t* state_inout, const char* label,
+                                    uint64_t count, uint8_t* out_canon) {
+  const size_t nb = field == ZKL_FIELD_M61 ? 8 : 32;
+  char buf[512];
+  for (uint64_t i = 0; i < count; i++) {
+    const int w = snprintf(buf, sizeof(buf), "%s/%llu", label, (unsigned long long)i);
+    if (w < 0 || (size_t)w >= sizeof(buf)) {
+      set_error("transcript_challenge_vector: label too long");
+      return kErrArg;
+    }
+    const int rc = zkl_transcript_challenge(field, state_inout, buf, out_canon + i * nb);
+    if (rc) return rc;
+  }
+  return kOk;
+}
 int zkl_sumcheck_finish(int field, void* const* tables, int k, const uint8_t* r_last_canon,
                         uint8_t* finals_out_host, void* stream) {
   D(field, op_sumcheck_finish<F>(tables, k, scalar<F>(r_last_canon), finals_out_host,
@@ -262,6 +294,12 @@ int zkl_pair_multiplicities(int field, const void* x, int x_type, const void* y,
                             uint32_t* index_out, int64_t* first_miss, void* stream) {
   D(field, op_pair_multiplicities<F>(x, x_type, y, y_type, d, table_x0, table_y, secret, table, n,
                                      counts, index_out, first_miss, (cudaStream_t)stream));
+}
+int zkl_rescale_witness(const void* wide, int wide_type, uint64_t n, int64_t divisor,
+                        int64_t lift, int64_t qmin, int64_t qmax, int16_t* q_out, int16_t* r_out,
+                        int clip, int64_t* first_bad, uint64_t* n_bad, void* stream) {
+  return op_rescale_witness(wide, wide_type, n, divisor, lift, qmin, qmax, q_out, r_out, clip,
+                            first_bad, n_bad, (cudaStream_t)stream);
 }
 int zkl_range_multiplicities(const void* x, int x_type, uint64_t d, int64_t table_x0,
                              uint64_t n, uint32_t* counts, uint32_t* index_out,

@@ -602,6 +602,79 @@ int op_read(uint8_t* host, const void* src, uint64_t n, cudaStream_t s) {
   return kOk;
 }
 
+// ---------------------------------------------------------------------------
+// Rescale witness (gadgets.py:563-580, quantize.py:101-104): for every wide
+// entry w, q = floor((w + divisor/2) / divisor), r = w - divisor q (so r is in
+// [-divisor/2, divisor/2)), resid = r * lift.  q outside [qmin, qmax] is the
+// reference's RangeViolation: the first such index is reported, and with
+// clip != 0 q is clamped (and counted) instead.  One pass: 8 B in, 4 B out.
+template <class W>
+__global__ void k_rescale_witness(const W* wide, uint64_t n, int64_t divisor, int64_t lift,
+                                  int64_t qmin, int64_t qmax, int16_t* q_out, int16_t* r_out,
+                                  int clip, unsigned long long* first_bad,
+                                  unsigned long long* n_bad) {
+  unsigned bad = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const int64_t w = (int64_t)wide[i];
+    const int64_t t = w + divisor / 2;
+    int64_t q = t / divisor;
+    if ((t % divisor != 0) && (t < 0)) q -= 1;  // floor division
+    const int64_t r = w - divisor * q;
+    if (q < qmin || q > qmax) {
+      atomicMin(first_bad, (unsigned long long)i);
+      bad++;
+      if (clip) q = q < qmin ? qmin : qmax;
+    }
+    q_out[i] = (int16_t)q;
+    r_out[i] = (int16_t)(r * lift);
+  }
+  bad = __reduce_add_sync(0xffffffffu, bad);
+  if (bad && (threadIdx.x & 31) == 0) atomicAdd(n_bad, (unsigned long long)bad);
+}
+
+int op_rescale_witness(const void* wide, int wide_type, uint64_t n, int64_t divisor, int64_t lift,
+                       int64_t qmin, int64_t qmax, int16_t* q_out, int16_t* r_out, int clip,
+                       int64_t* first_bad, uint64_t* n_bad, cudaStream_t s) {
+  *first_bad = -1;
+  *n_bad = 0;
+  if (divisor <= 0 || qmin < -32768 || qmax > 32767 || divisor / 2 * lift > 32768) {
+    set_error("rescale_witness: quotient / residue must fit int16");
+    return kErrArg;
+  }
+  void* ws;
+  int rc = scratch_reserve(64, &ws, s);
+  if (rc) return rc;
+  unsigned long long* flag = (unsigned long long*)ws;
+  ZKL_CUDA(cudaMemsetAsync(flag, 0xff, 8, s));
+  ZKL_CUDA(cudaMemsetAsync(flag + 1, 0, 8, s));
+  if (n) {
+    const unsigned g = grid_for(n, 256);
+    switch (wide_type) {
+      case 1: k_rescale_witness<int16_t><<<g, 256, 0, s>>>((const int16_t*)wide, n, divisor, lift,
+                  qmin, qmax, q_out, r_out, clip, flag, flag + 1); break;
+      case 2: k_rescale_witness<int32_t><<<g, 256, 0, s>>>((const int32_t*)wide, n, divisor, lift,
+                  qmin, qmax, q_out, r_out, clip, flag, flag + 1); break;
+      case 3: k_rescale_witness<int64_t><<<g, 256, 0, s>>>((const int64_t*)wide, n, divisor, lift,
+                  qmin, qmax, q_out, r_out, clip, flag, flag + 1); break;
+      default: set_error("rescale_witness: int16/int32/int64 only"); return kErrArg;
+    }
+    ZKL_LAUNCH_CHECK();
+  }
+  void* pin;
+  if ((rc = pinned_reserve(16, &pin))) return rc;
+  ZKL_CUDA(cudaMemcpyAsync(pin, flag, 16, cudaMemcpyDeviceToHost, s));
+  ZKL_CUDA(cudaStreamSynchronize(s));
+  unsigned long long v[2];
+  memcpy(v, pin, 16);
+  *n_bad = v[1];
+  if (v[0] != ~0ull) {
+    *first_bad = (int64_t)v[0];
+    if (!clip) return kErrMissing;
+  }
+  return kOk;
+}
+
 #define ZKL_INST(F)                                                                       \
   template int op_to_mont<F>(void*, const void*, uint64_t, cudaStream_t);                 \
   template int op_from_mont<F>(void*, const void*, uint64_t, cudaStream_t);               \

@@ -112,6 +112,34 @@ def device_pair_table(xs, ys, commitment_x, commitment_y, name):
                      LookupTable(ty, commitment_y, name + ".y"), name)
 
 
+def rescale_witness_device(wide, divisor, params, clip=False):
+    """rescale_witness (gadgets.py:563-580) for a signed int device tensor:
+    (narrow int16, resid int16 = r * zeta/divisor, number of clipped
+    quotients), one kernel pass (zkl_rescale_witness).  A quotient outside the
+    quant_range domain raises RangeViolation like the reference, unless
+    clip=True (it is then clamped and counted)."""
+    import ctypes
+
+    zeta = params.zeta
+    if divisor <= 0 or zeta % divisor:
+        raise ValueError("divisor must divide zeta")
+    half = params.act_bound * params.gamma_fp
+    w = wide.contiguous()
+    q = torch.empty(w.shape, dtype=torch.int16, device=w.device)
+    r = torch.empty(w.shape, dtype=torch.int16, device=w.device)
+    fb, nb = ctypes.c_int64(-1), ctypes.c_uint64(0)
+    rc = N.lib().zkl_rescale_witness(D.ptr(w), D._INT_TYPES[w.dtype], w.numel(), divisor,
+                                     zeta // divisor, -half, half - 1, D.ptr(q), D.ptr(r),
+                                     1 if clip else 0, ctypes.byref(fb), ctypes.byref(nb),
+                                     D.stream())
+    if rc == N.ZKL_ERR_MISSING:
+        bad = int(w.reshape(-1)[fb.value])
+        q0 = (bad + divisor // 2) // divisor
+        raise RangeViolation("rescale quotient %d outside table domain" % q0)
+    N.check(rc)
+    return q, r, int(nb.value)
+
+
 def _int_matrix(pt):
     dev = getattr(pt, "device", None)
     if dev is not None and dev.mtype != N.MT_FIELD:

@@ -214,3 +214,30 @@ def test_range_multiplicities_vs_bincount(n, dtype):
     with pytest.raises(zb.ElementNotInTable) as e:
         L.multiplicities_range(D.LiftedColumn(bad, spec), tab, bad, tab.int_column)
     assert e.value.index == 777 and e.value.value == int(bad[777]) % p
+
+
+@pytest.mark.parametrize("divisor", [4096, 1024, 1])
+@pytest.mark.parametrize("dtype", [torch.int64, torch.int32, torch.int16])
+def test_rescale_witness_device_vs_reference_divmod(divisor, dtype):
+    """zkl_rescale_witness == centered_divmod (quantize.py:101-104) entry for
+    entry, RangeViolation at out-of-domain quotients, clamping on request."""
+    fp = SimpleNamespace(zeta=4096, gamma_fp=4096, act_bound=8)
+    g = torch.Generator().manual_seed(divisor)
+    hi = {torch.int64: 1 << 27, torch.int32: 1 << 27, torch.int16: 1 << 15}[dtype]
+    w = torch.randint(-hi, hi, (1 << 16,), generator=g, dtype=torch.int64)
+    w = w.clamp(-32768 * divisor + 1, 32767 * divisor - 1).to(dtype)
+    q, r, nb = NL.rescale_witness_device(w.cuda(), divisor, fp)
+    assert nb == 0
+    wl = w.tolist()
+    for i in range(0, len(wl), 997):
+        qq = (wl[i] + divisor // 2) // divisor
+        assert int(q[i]) == qq and int(r[i]) == (wl[i] - divisor * qq) * (4096 // divisor)
+    if dtype == torch.int16 and divisor == 1:
+        return
+    big = w.clone().to(torch.int64)
+    big[123] = 40000 * divisor
+    big[456] = -40000 * divisor
+    with pytest.raises(NL.RangeViolation):
+        NL.rescale_witness_device(big.cuda(), divisor, fp)
+    q, r, nb = NL.rescale_witness_device(big.cuda(), divisor, fp, clip=True)
+    assert nb == 2 and int(q[123]) == 32767 and int(q[456]) == -32768

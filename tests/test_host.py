@@ -255,3 +255,22 @@ def test_table_generation_matches_reference(name):
     assert xs[0] == g["x0"] and len(xs) == g["n"]
     assert np.array_equal(np.asarray(ys, dtype=np.int64), want.astype(np.int64))
     assert T.quant_range(4096, 8) == (-32768, 65536) and T.residue_range(4096) == (-2048, 4096)
+
+
+@pytest.mark.parametrize("p", [P_BIG, P_TEST])
+def test_native_batched_transcript_ops_match_python(p):
+    """Transcript.append_ints / challenge_vector (one native call each) give
+    exactly the per-record hashlib bytes (transcript.py:33-45)."""
+    import random
+
+    rnd = random.Random(3)
+    vals = [0, 1, 255, 256, p - 1] + [rnd.randrange(p) for _ in range(40)]
+    a = Transcript(b"batch", p, b"s")
+    b = Transcript(b"batch", p, b"s")
+    a.append_ints(b"open/point", vals)
+    for v in vals:
+        b.append(b"open/point", v)
+    assert a.state == b.state and a.log == b.log
+    ca = a.challenge_vector(b"lookup/u", 25)
+    cb = [b.challenge(b"lookup/u/%d" % i) for i in range(25)]
+    assert ca == cb and a.state == b.state
