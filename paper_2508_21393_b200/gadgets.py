@@ -349,6 +349,57 @@ def prove_matmul(a, b, c, key, tr, rng):
     )
 
 
+def _consumable(M, spec):
+    """A fresh field copy of a DeviceMatrix that a sumcheck may fold in place
+    (integer matrices are lifted straight into it)."""
+    if M.mtype == N.MT_FIELD:
+        return M.t.clone()
+    return D.lift(M.t.reshape(-1), spec)
+
+
+EQ_FACTORED_MIN_VARS = 20  # below this the dense engine's eq table costs nothing
+EQ_TILE_LOG = 16
+
+
+def _eq_factored_prod3(spec, tr, r, ta, tb, n):
+    """The elementprod claim sum_i eq(r, i) A(i) B(i) (gadgets.py:396-405)
+    without materialising eq(r, .): the first n - 16 rounds run on the
+    eq-factored tiled evaluator of the logUp engine (eq = C_j l_j(x)
+    eq_hi(k) eq_lo(t); term coefficients (1, 0, 0, 0, 0) reduce its claim to
+    E A S; 6 Montgomery products per pair in round 0 and 10 after, against 7
+    and 13 with the table), then the last 16 rounds over E bound at the point,
+    A and B.  Same rounds, point and finals as the dense claim; None when the
+    native engine declines (stepwise mode under profilers)."""
+    if not native_transcript(tr, spec):
+        return None
+    tile_log = EQ_TILE_LOG
+    r1 = n - tile_log
+    nt = 1 << tile_log
+    E = D.empty(spec, nt)
+    side = D.empty(spec, nt).zero_()  # the logUp table-side columns: unused (coefficients 0)
+    nb = spec.nbytes
+    state = ctypes.create_string_buffer(bytes(tr.state), 64)
+    rbuf = (ctypes.c_uint8 * (r1 * 4 * nb))()
+    pbuf = (ctypes.c_uint8 * (r1 * nb))()
+    ptrs = (ctypes.c_void_p * 6)(*[t.data_ptr() for t in (E, ta, tb, side, side, side)])
+    coeffs = D.scalars_bytes([1, 0, 0, 0, 0], spec)
+    rc = N.lib().zkl_logup_tiled_rounds(spec.fid, ptrs, tile_log, n, r1,
+                                        D.scalars_bytes(list(r), spec), coeffs, 0, state, rbuf,
+                                        pbuf, D.stream())
+    if rc == N.ZKL_ERR_UNSUPPORTED:
+        return None
+    N.check(rc)
+    flat = D.decode(bytes(rbuf), spec, 4 * r1)
+    rounds = [tuple(flat[4 * j:4 * j + 4]) for j in range(r1)]
+    point = D.decode(bytes(pbuf), spec, r1)
+    tr.state = state.raw[:64]
+    log = getattr(tr, "log", None)
+    if log is not None:
+        log.extend((b"sumcheck/eval", (e.bit_length() + 7) // 8 or 1) for e in flat)
+    r2, p2, finals = run_rounds(spec, [E, ta[:nt], tb[:nt]], tile_log, [(1, (0, 1, 2))], 3, tr)
+    return rounds + r2, point + p2, finals
+
+
 def prove_elementprod(a, b, c, key, tr, rng):
     """Drop-in for zklora.gadgets.prove_elementprod (gadgets.py:383-410)."""
     p = tr.modulus
@@ -364,11 +415,14 @@ def prove_elementprod(a, b, c, key, tr, rng):
     claimed = c_opening.values[0]
     spec = D.spec_for(p)
     rows, cols = 1 << shape[0], 1 << shape[1]
-    ta = _device_matrix(a, rows, cols, spec).as_field_vector(spec).clone()
-    tb = _device_matrix(b, rows, cols, spec).as_field_vector(spec).clone()
+    ta = _consumable(_device_matrix(a, rows, cols, spec), spec)
+    tb = _consumable(_device_matrix(b, rows, cols, spec), spec)
     term = Term(1, (0, 1, 2))
     absorb_claim(tr, claimed, [term], 3, n)
-    if n:
+    got = _eq_factored_prod3(spec, tr, r, ta, tb, n) if n >= EQ_FACTORED_MIN_VARS else None
+    if got is not None:
+        rounds, point, finals = got
+    elif n:
         rounds, point, finals = run_rounds(spec, [D.eq_table(r, spec), ta, tb], n,
                                            [(1, (0, 1, 2))], 3, tr)
     else:

@@ -62,6 +62,8 @@ def _tables(g, p, where):
 
 def _operand(vals, rv, cv, p, where, dtype=torch.int32):
     ref = TensorRef("committed", rv, cv, commitment=StubCommitment(rv + cv))
+    if vals is None:
+        return ProverTensor(None, ref, ())
     if where == "device":
         t = torch.tensor(vals, dtype=dtype).cuda().view(1 << rv, 1 << cv)
         return ProverTensor(None, ref, (), device=DeviceMatrix.from_int_tensor(t))
@@ -241,3 +243,36 @@ def test_rescale_witness_device_vs_reference_divmod(divisor, dtype):
         NL.rescale_witness_device(big.cuda(), divisor, fp)
     q, r, nb = NL.rescale_witness_device(big.cuda(), divisor, fp, clip=True)
     assert nb == 2 and int(q[123]) == 32767 and int(q[456]) == -32768
+
+
+@pytest.mark.parametrize("field", ["big", "test"])
+@pytest.mark.parametrize("n", [6, 9, 13, 21])
+def test_eq_factored_elementprod_matches_dense(field, n, monkeypatch):
+    """prove_elementprod's eq-factored path (tiled logUp engine with term
+    coefficients (1,0,0,0,0)) gives the dense engine's proof byte for byte."""
+    from paper_2508_21393_b200 import gadgets as G
+
+    p = FIELDS[field]
+    g = torch.Generator().manual_seed(n)
+    rv = n // 2
+    a = torch.randint(-32768, 32768, (1 << rv, 1 << (n - rv)), generator=g).short()
+    b = torch.randint(-32768, 32768, (1 << rv, 1 << (n - rv)), generator=g).short()
+    c = a.long() * b.long()
+    c[0, 1] += 5  # a false claim too: every evaluation is computed, not derived
+
+    def run(factored):
+        monkeypatch.setattr(G, "EQ_FACTORED_MIN_VARS", 6 if factored else 99)
+        monkeypatch.setattr(G, "EQ_TILE_LOG", 5 if n < 21 else 16)
+        tr = Transcript(b"ep", p, b"s")
+        ops = [_operand(None, rv, n - rv, p, "device") for _ in range(3)]
+        ops = [ProverTensor(None, o.ref, (), device=DeviceMatrix.from_int_tensor(t.cuda()))
+               for o, t in zip(ops, (a, b, c))]
+        pr = zb.prove_elementprod(*ops, KEY, tr, _Rng())
+        return pr, tr.state
+
+    p1, s1 = run(True)
+    p2, s2 = run(False)
+    assert [tuple(r.evaluations) for r in p1.sumcheck.rounds] == \
+        [tuple(r.evaluations) for r in p2.sumcheck.rounds]
+    assert tuple(p1.sumcheck.final_values) == tuple(p2.sumcheck.final_values)
+    assert s1 == s2
