@@ -620,22 +620,10 @@ ZKL_D void chunk_sum_atomic(const fr_t* x, uint64_t c0, int n, uint64_t* sumx) {
 // raw u64 accumulators are summed with warp shuffles; lane 0 adds them to the
 // row's record (red.add.u64: exact, order-free across column chunks).
 template <int R>
-__global__ void __launch_bounds__(256)
-    k_mvw_rows(const int16_t* M, uint64_t rows, uint64_t cols, const fr_t* x, uint64_t cch,
-               uint64_t* acc_out) {
-  extern __shared__ __align__(16) uint32_t xsm[];  // 8 limbs x cch
-  const uint64_t c0 = blockIdx.y * cch;
-  const int n = (int)((c0 + cch < cols ? c0 + cch : cols) - c0);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const fr_t v = x[c0 + i];
-#pragma unroll
-    for (int l = 0; l < 8; l++) xsm[l * cch + i] = v.v[l];
-  }
-  __syncthreads();
-  if (blockIdx.x == 0) chunk_sum_atomic(x, c0, n, acc_out + rows * 8);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t r0 = (blockIdx.x * (uint64_t)(blockDim.x >> 5) + warp) * R;
-  if (r0 >= rows) return;
+__device__ __forceinline__ void mvw_rows_group(const int16_t* M, uint64_t rows,
+                                                    uint64_t cols, const uint32_t* xsm,
+                                                    uint64_t cch, int n, uint64_t c0,
+                                                    uint64_t r0, int lane, uint64_t* acc_out) {
   LimbAcc<1> acc[R];
 #pragma unroll
   for (int q = 0; q < R; q++) acc[q].zero();
@@ -689,6 +677,41 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+template <int R>
+__global__ void __launch_bounds__(256, (R == 2 ? 3 : 2))
+    k_mvw_rows(const int16_t* M, uint64_t rows, uint64_t cols, const fr_t* x, uint64_t cch,
+               uint64_t* acc_out) {
+  extern __shared__ __align__(16) uint32_t xsm[];  // 8 limbs x cch
+  const uint64_t c0 = blockIdx.y * cch;
+  const int n = (int)((c0 + cch < cols ? c0 + cch : cols) - c0);
+  // stage x: every thread issues all of its loads before the first store
+  // (one L2 round trip instead of one per element)
+  constexpr int kFill = 8;  // cch <= 8 * 256
+  fr_t xr[kFill];
+#pragma unroll
+  for (int k = 0; k < kFill; k++) {
+    const int i = threadIdx.x + k * 256;
+    if (i < n) xr[k] = x[c0 + i];
+  }
+#pragma unroll
+  for (int k = 0; k < kFill; k++) {
+    const int i = threadIdx.x + k * 256;
+    if (i < n) {
+#pragma unroll
+      for (int l = 0; l < 8; l++) xsm[l * cch + i] = xr[k].v[l];
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0) chunk_sum_atomic(x, c0, n, acc_out + rows * 8);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // the block's x chunk is staged once and reused for every row group the
+  // block's warps take (grid-stride over rows)
+  const uint64_t rstride = (uint64_t)gridDim.x * (blockDim.x >> 5) * R;
+  for (uint64_t r0 = (blockIdx.x * (uint64_t)(blockDim.x >> 5) + warp) * R; r0 < rows;
+       r0 += rstride)
+    mvw_rows_group<R>(M, rows, cols, xsm, cch, n, c0, r0, lane, acc_out);
+}
+
 // y[i] = reduce(acc[i]) - K; one thread per output (acc: atomically summed
 // raw words of every chunk -- exact integer sums, order-independent)
 template <int CH>
@@ -731,17 +754,32 @@ static int matvec_fast(const MT* M, uint64_t rows, uint64_t cols, int transpose,
   void* ws;
   int rc;
   if (!transpose && CH == 1) {
-    // warp-per-row-group kernel (lanes along columns)
-    constexpr int RW = 4;
+    // warp-per-row-group kernel (lanes along columns); ZKL_MVW_RW (2 / 4 rows
+    // per warp) and ZKL_MVW_WAVES (target blocks per SM) are tuning overrides
+    static const int kRw = [] {
+      const char* e = getenv("ZKL_MVW_RW");
+      return e && atoi(e) == 4 ? 4 : 2;
+    }();
+    static const uint64_t kWaves = [] {
+      const char* e = getenv("ZKL_MVW_WAVES");
+      return e ? (uint64_t)atoi(e) : (uint64_t)2;
+    }();
+    const int RW = kRw;
     if (cols % 128) return kErrUnsupported;
     const uint64_t rblocks = (rows + 8 * RW - 1) / (8 * RW);
-    uint64_t cs = (2 * (uint64_t)kSMs + rblocks - 1) / rblocks;  // >= 2 blocks per SM
+    uint64_t cs = (kWaves * (uint64_t)kSMs + rblocks - 1) / rblocks;  // >= kWaves blocks per SM
     const uint64_t max_cs = cols / 512;  // >= 512 columns per chunk
     if (cs > max_cs) cs = max_cs;
     if (cs < 1) cs = 1;
     uint64_t cch = (cols + cs - 1) / cs;
     cch = (cch + 127) / 128 * 128;
-    if (cch * 32 > 160 * 1024) return kErrUnsupported;
+    if (cch > 2048) {  // the x staging holds at most 8 elements per thread
+      cch = 2048;
+    }
+    static const uint64_t kGroups = [] {  // row groups per warp (grid-stride)
+      const char* e = getenv("ZKL_MVW_GROUPS");
+      return e ? (uint64_t)atoi(e) : (uint64_t)1;
+    }();
     nchunks = (cols + cch - 1) / cch;
     nout = rows;
     rc = scratch_reserve(rows * NW * 8 + 128, &ws, s);
@@ -750,12 +788,17 @@ static int matvec_fast(const MT* M, uint64_t rows, uint64_t cols, int transpose,
     const size_t smem = cch * 32;
     static bool attr = false;
     if (!attr) {
-      ZKL_CUDA(cudaFuncSetAttribute(k_mvw_rows<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      ZKL_CUDA(cudaFuncSetAttribute(k_mvw_rows<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    160 * 1024));
+      ZKL_CUDA(cudaFuncSetAttribute(k_mvw_rows<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     160 * 1024));
       attr = true;
     }
-    dim3 g((unsigned)rblocks, (unsigned)nchunks);
-    k_mvw_rows<RW><<<g, 256, smem, s>>>((const int16_t*)M, rows, cols, x, cch, (uint64_t*)ws);
+    dim3 g((unsigned)((rblocks + kGroups - 1) / kGroups), (unsigned)nchunks);
+    if (RW == 2)
+      k_mvw_rows<2><<<g, 256, smem, s>>>((const int16_t*)M, rows, cols, x, cch, (uint64_t*)ws);
+    else
+      k_mvw_rows<4><<<g, 256, smem, s>>>((const int16_t*)M, rows, cols, x, cch, (uint64_t*)ws);
     ZKL_LAUNCH_CHECK();
   } else if (!transpose) {
     constexpr int R = 1;
