@@ -40,12 +40,17 @@ from .lookup import (  # noqa: F401
 )
 from .mle import eq_table, fold_table, mle_evaluate  # noqa: F401
 from .nonlinear import (  # noqa: F401
+    DigitOutOfRange,
+    NormalizationBudgetExceeded,
     PairTable,
     RangeViolation,
+    SoftmaxRowProof,
     TableSet,
     prove_rescale,
     prove_rsqrt,
+    prove_softmax_row,
     prove_swiglu,
+    softmax_row_witness,
 )
 from .sumcheck import (  # noqa: F401
     DegreeOverflow,

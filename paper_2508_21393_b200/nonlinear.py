@@ -33,6 +33,14 @@ class RangeViolation(ValueError):
     """gadgets.py RangeViolation (witness outside a table domain)."""
 
 
+class DigitOutOfRange(ValueError):
+    """quantize.py DigitOutOfRange (shifted exponent outside [0, xi))."""
+
+
+class NormalizationBudgetExceeded(ValueError):
+    """gadgets.py NormalizationBudgetExceeded (softmax row sum drift)."""
+
+
 @dataclass(frozen=True)
 class PairTable:
     """tables.py:120-153: aligned (input, output) columns."""
@@ -91,7 +99,25 @@ class RsqrtProof:
     lookup: object
 
 
-TYPES = {"RescaleProof": RescaleProof, "SwigluProof": SwigluProof, "RsqrtProof": RsqrtProof}
+@dataclass
+class SoftmaxRowProof:
+    tag = "softmax_row"
+    num_vars: int
+    xi_prime: int
+    digit_refs: tuple
+    partial_refs: tuple
+    chain_wide_refs: tuple
+    chain_narrow_refs: tuple
+    chain_resid_refs: tuple
+    decomposition_opening: object
+    digit_lookups: tuple
+    chain_prod_proofs: tuple
+    chain_rescale_proofs: tuple
+    normalization_opening: object
+
+
+TYPES = {"RescaleProof": RescaleProof, "SwigluProof": SwigluProof, "RsqrtProof": RsqrtProof,
+         "SoftmaxRowProof": SoftmaxRowProof}
 
 
 # ---------------------------------------------------------------------------
@@ -223,3 +249,157 @@ def prove_rsqrt(v, u, tables, key, tr, rng):
     _absorb_operands(tr, b"rsqrt", [v.ref, u.ref], key.group)
     lookup = prove_pair_lookup(b"rsqrt/pair", v, u, tables.rsqrt, key, tr, rng)
     return TYPES["RsqrtProof"](shape=_shape(v), lookup=lookup)
+
+
+# ---------------------------------------------------------------------------
+# softmax (one row): gadgets.py:878-1036
+def softmax_row_witness(z_row, params, modulus):
+    """Host restatement of gadgets.py:878-922 (float64 host code, like the
+    reference: SURVEY.md sec. 7 hard part 8).  Returns (xi_prime, digits[k][i],
+    partials[k][i], chain [(wide, narrow, resid)], p_row) as signed ints."""
+    import math
+
+    from .tables import exp_segment_value, radix_bases, round_half_away
+
+    radices = tuple(params.radices)
+    if len(radices) < 2:
+        raise ValueError("softmax needs at least two radix positions")
+    if len(z_row) & (len(z_row) - 1):
+        raise ShapeMismatch("softmax rows must have power-of-two length")
+    g, zeta = params.gamma_fp, params.zeta
+    m = max(z_row)
+    total = sum(math.exp((z - m) / g) for z in z_row)
+    xi_prime = m + round_half_away(g * math.log(total))
+    bases = radix_bases(radices)
+    digits, partials = [], []
+    for z in z_row:
+        v = xi_prime - z
+        if v < 0 or v >= params.xi:
+            raise DigitOutOfRange("shifted exponent %d outside [0, xi)" % v)
+        ds, rest = [], v
+        for b in radices:  # quantize.py:121-135, least significant first
+            ds.append(rest % b)
+            rest //= b
+        if rest:
+            raise DigitOutOfRange("value %d exceeds the radix capacity" % v)
+        digits.append(ds)
+        partials.append([exp_segment_value(g, radices, k, d) for k, d in enumerate(ds)])
+    kc = len(radices)
+    digit_cols = [[digits[i][k] for i in range(len(z_row))] for k in range(kc)]
+    partial_cols = [[partials[i][k] for i in range(len(z_row))] for k in range(kc)]
+    chain, current = [], list(partial_cols[0])
+    for k in range(1, kc):
+        wide = [c * y for c, y in zip(current, partial_cols[k])]
+        narrow = [(w + zeta // 2) // zeta for w in wide]
+        resid = [w - zeta * q for w, q in zip(wide, narrow)]
+        chain.append((wide, narrow, resid))
+        current = narrow
+    return xi_prime, digit_cols, partial_cols, chain, current
+
+
+def normalization_budget(row_len, params):
+    """gadgets.py:925-927."""
+    return row_len * (len(params.radices) + 1)
+
+
+def _committed_vector(values, key, rng, dtype=torch.int32):
+    """commit_tensor (gadgets.py:120-128) of a 1 x len(values) signed vector
+    as a device operand under the stub key."""
+    from .gadgets import DeviceMatrix, ProverTensor, TensorRef, commit_backend
+
+    n = (len(values) - 1).bit_length()
+    be = commit_backend(key)
+    rows, _ = be.split_shape(n)
+    blinding = tuple(rng.vector(rows))
+    t = torch.tensor(values, dtype=dtype, device="cuda").view(1, -1)
+    return ProverTensor(None, TensorRef("committed", 0, n, commitment=be.commit_size(n)), blinding,
+                        device=DeviceMatrix.from_int_tensor(t))
+
+
+def prove_softmax_row(z_row, p_row, witness, tables, key, tr, rng):
+    """Drop-in for zklora.gadgets.prove_softmax_row (gadgets.py:930-1036):
+    digit decomposition opening, one exp pair lookup per radix position, the
+    product chain (elementprod + rescale per step), the half-point
+    normalisation opening with its drift budget.  Witness columns become
+    device operands (stub commitments) when z_row lives on the GPU."""
+    from types import SimpleNamespace
+
+    from .gadgets import ProverTensor, TensorRef, commit_backend, prove_elementprod
+    from .field import inverse
+
+    p = tr.modulus
+    params = tables.params
+    xi_prime, digit_cols, partial_cols, chain, final = witness
+    n = z_row.ref.num_vars
+    row_len = 1 << n
+    if p_row.ref.num_vars != n:
+        raise ShapeMismatch("probability row shape differs from score row")
+    kc = len(params.radices)
+    be = commit_backend(key)
+    device = getattr(z_row, "device", None) is not None and be.__name__.endswith("commit_stub")
+    if device:
+        got = p_row.device.t.reshape(-1).tolist() if getattr(p_row, "device", None) is not None \
+            else None
+    else:
+        from .field import to_signed
+
+        got = [to_signed(v, p) for v in p_row.flat()]
+    if got is not None and [int(v) for v in got] != [int(v) for v in final]:
+        raise ValueError("p_row does not match the witness chain output")
+
+    def vec(values):
+        if device:
+            dtype = torch.int64 if max(abs(int(v)) for v in values) >= (1 << 31) else torch.int32
+            return _committed_vector(values, key, rng, dtype)
+        rows, _ = be.split_shape(n)
+        blinding = tuple(rng.vector(rows))
+        entries = [int(v) % p for v in values]
+        com = be.commit(key, entries, list(blinding) if blinding else None)
+        return ProverTensor(SimpleNamespace(data=entries), TensorRef("committed", 0, n,
+                                                                     commitment=com), blinding)
+
+    digit_ts = [vec(digit_cols[k]) for k in range(kc)]
+    partial_ts = [vec(partial_cols[k]) for k in range(kc)]
+    wide_ts, narrow_ts, resid_ts = [], [], []
+    for idx, (wide, narrow, resid) in enumerate(chain):
+        wide_ts.append(vec(wide))
+        narrow_ts.append(p_row if idx == len(chain) - 1 else vec(narrow))
+        resid_ts.append(vec(resid))
+
+    _absorb_operands(tr, b"softmax", [z_row.ref, p_row.ref], key.group)
+    tr.append(b"softmax/xi", xi_prime % p)
+    for t in digit_ts + partial_ts + wide_ts + narrow_ts[:-1] + resid_ts:
+        tr.append(b"softmax/witness", t.ref.digest(key.group))
+    rho = tr.challenge_vector(b"softmax/decomp", n)
+    decomposition_opening = _open_tables(key, digit_ts + [z_row], rho, tr, rng)
+    digit_lookups = tuple(
+        prove_pair_lookup(b"softmax/exp%d" % k, digit_ts[k], partial_ts[k],
+                          tables.exp_segments[k], key, tr, rng)
+        for k in range(kc))
+    chain_prod_proofs, chain_rescale_proofs = [], []
+    current = partial_ts[0]
+    for idx in range(len(chain)):
+        chain_prod_proofs.append(
+            prove_elementprod(current, partial_ts[idx + 1], wide_ts[idx], key, tr, rng))
+        chain_rescale_proofs.append(
+            prove_rescale(wide_ts[idx], narrow_ts[idx], resid_ts[idx], params.zeta, tables, key,
+                          tr, rng))
+        current = narrow_ts[idx]
+    half = inverse(2, p)
+    normalization_opening = _open_tables(key, [p_row], [half] * n, tr, rng)
+    total = (1 << n) * normalization_opening.values[0] % p
+    drift = total - params.gamma_fp
+    drift = (drift + p // 2) % p - p // 2  # to_signed
+    if abs(drift) > normalization_budget(row_len, params):
+        raise NormalizationBudgetExceeded(
+            "row sum off by %d units (budget %d)" % (drift, normalization_budget(row_len, params)))
+    return TYPES["SoftmaxRowProof"](
+        num_vars=n, xi_prime=xi_prime, digit_refs=tuple(t.ref for t in digit_ts),
+        partial_refs=tuple(t.ref for t in partial_ts),
+        chain_wide_refs=tuple(t.ref for t in wide_ts),
+        chain_narrow_refs=tuple(t.ref for t in narrow_ts[:-1]),
+        chain_resid_refs=tuple(t.ref for t in resid_ts),
+        decomposition_opening=decomposition_opening, digit_lookups=digit_lookups,
+        chain_prod_proofs=tuple(chain_prod_proofs),
+        chain_rescale_proofs=tuple(chain_rescale_proofs),
+        normalization_opening=normalization_opening)

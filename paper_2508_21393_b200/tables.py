@@ -68,3 +68,20 @@ def quant_range(gamma, act_bound):
 def residue_range(zeta):
     """tables.py:114-117."""
     return -(zeta // 2), zeta
+
+
+def radix_bases(radices):
+    """quantize.py:111-118: base_k = product of the radices before position k."""
+    bases, acc = [], 1
+    for b in radices:
+        bases.append(acc)
+        acc *= b
+    return bases
+
+
+def exp_segment_value(gamma, radices, k, digit):
+    """tables.py:56-62 for one digit."""
+    if not 0 <= digit < radices[k]:
+        raise KeyError("digit %d outside segment %d" % (digit, k))
+    base = radix_bases(radices)[k]
+    return round_half_away(gamma * math.exp(-digit * (base / gamma)))

@@ -615,8 +615,60 @@ def gen_block():
                             cases=cases))
 
 
+def gen_softmax():
+    """prove_softmax_row (gadgets.py:930-1036) on 8- and 16-entry rows at the
+    reference tests' DESK parameters, both fields."""
+    params = QuantParams(gamma_fp=2**7, bound=2**11, zeta=2**7, xi=2**21,
+                         radices=(2**7, 2**7, 2**7), act_bound=16)
+    eps = 1e-5
+    g = params.gamma_fp
+    cases = []
+    tabs = None
+    for fname, p in FIELDS.items():
+        exps = tuple(TB._pair("exp%d" % k, TB.exp_segment_entries(params, k), KEY, p)
+                     for k in range(params.num_radices))
+        ts = TB.TableSet(
+            params, eps, p, b"", exps,
+            TB._pair("silu", TB.silu_entries(params), KEY, p),
+            TB._pair("silu_deriv", TB.silu_deriv_entries(params), KEY, p),
+            TB._pair("rsqrt", TB.rsqrt_entries(params, eps), KEY, p),
+            L.make_lookup_table(TB._encode_column(TB.quant_range_entries(params), p), KEY,
+                                "quant_range"),
+            L.make_lookup_table(TB._encode_column(TB.residue_range_entries(params), p), KEY,
+                                "residue_range"))
+        if tabs is None:
+            tabs = dict(exp=[[F.to_signed(v, p) for v in e.y.entries] for e in exps],
+                        quant_range=[F.to_signed(v, p) for v in ts.quant_range.entries],
+                        residue_range=[F.to_signed(v, p) for v in ts.residue_range.entries])
+        rnd = random.Random(92)
+        for row_len in (8, 16):
+            zs = [rnd.randint(-3 * g, 3 * g) for _ in range(row_len)]
+            wit = G.softmax_row_witness(zs, params, p)
+            n = (row_len - 1).bit_length()
+            z_t = _pt([z % p for z in zs], 0, n)
+            p_t = _pt([v % p for v in wit[4]], 0, n)
+            tr = Transcript(b"zkl/golden/softmax", p, b"%d" % row_len)
+            start = tr.state
+            pr = G.prove_softmax_row(z_t, p_t, wit, ts, KEY, tr, RNG)
+            cases.append(dict(
+                field=fname, z=zs, xi_prime=wit[0], digits=wit[1], partials=wit[2],
+                chain=[[list(w), list(q), list(r)] for w, q, r in wit[3]], p=list(wit[4]),
+                state_before=hx(start),
+                decomposition=list(pr.decomposition_opening.values),
+                digit_lookups=[_lookup_rec(x) for x in pr.digit_lookups],
+                chain_prods=[[list(r.evaluations) for r in x.sumcheck.rounds]
+                             for x in pr.chain_prod_proofs],
+                chain_rescales=[[_lookup_rec(x.quant_lookup), _lookup_rec(x.resid_lookup)]
+                                for x in pr.chain_rescale_proofs],
+                normalization=list(pr.normalization_opening.values),
+                state_end=hx(tr.state)))
+    dump("softmax.json", dict(params=dict(gamma=g, zeta=params.zeta, act_bound=16,
+                                          radices=list(params.radices), xi=params.xi),
+                              tables=tabs, cases=cases))
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["transcript", "sumcheck", "matmul", "elementprod", "lookup",
-                             "pair_lookup", "tables", "field_mle", "nonlinear", "block"]
+                             "pair_lookup", "tables", "field_mle", "nonlinear", "block", "softmax"]
     for w in which:
         globals()["gen_" + w]()

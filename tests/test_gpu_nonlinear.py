@@ -276,3 +276,54 @@ def test_eq_factored_elementprod_matches_dense(field, n, monkeypatch):
         [tuple(r.evaluations) for r in p2.sumcheck.rounds]
     assert tuple(p1.sumcheck.final_values) == tuple(p2.sumcheck.final_values)
     assert s1 == s2
+
+
+@pytest.mark.parametrize("where", ["device", "host"])
+def test_softmax_row_golden(where):
+    """prove_softmax_row (gadgets.py:930-1036) bit-exact with the reference's
+    own run: decomposition and normalisation openings, the three exp digit
+    pair lookups, the chain's elementprods and rescales, the end state."""
+    g = load_golden("softmax.json")
+    prm = g["params"]
+    params = SimpleNamespace(gamma_fp=prm["gamma"], zeta=prm["zeta"], xi=prm["xi"],
+                             radices=tuple(prm["radices"]), act_bound=prm["act_bound"])
+    for c in g["cases"]:
+        p = FIELDS[c["field"]]
+        spec = D.spec_for(p)
+        t = g["tables"]
+        enc = lambda vals: tuple(v % p for v in vals)  # noqa: E731
+
+        def pair(k):
+            ys = t["exp"][k]
+            xs = list(range(len(ys)))
+            com = StubCommitment(_log2(len(ys)))
+            if where == "device":
+                return NL.device_pair_table(xs, ys, com, com, "exp%d" % k)
+            return NL.PairTable(zb.LookupTable(enc(xs), com, "exp%d.x" % k),
+                                zb.LookupTable(enc(ys), com, "exp%d.y" % k), "exp%d" % k)
+
+        def rng_table(vals, name):
+            com = StubCommitment(_log2(len(vals)))
+            if where == "device":
+                return NL.device_range_table(vals[0], len(vals), spec, com, name)
+            return zb.LookupTable(enc(vals), com, name)
+
+        ts = NL.TableSet(params, 1e-5, p, b"", tuple(pair(k) for k in range(3)), None, None, None,
+                         rng_table(t["quant_range"], "quant_range"),
+                         rng_table(t["residue_range"], "residue_range"))
+        n = _log2(len(c["z"]))
+        z_t = _operand(c["z"], 0, n, p, where)
+        p_t = _operand(c["p"], 0, n, p, where)
+        wit = (c["xi_prime"], c["digits"], c["partials"], [tuple(x) for x in c["chain"]], c["p"])
+        tr = Transcript.from_state(bytes.fromhex(c["state_before"]), p)
+        pr = zb.prove_softmax_row(z_t, p_t, wit, ts, KEY, tr, _Rng())
+        assert list(pr.decomposition_opening.values) == c["decomposition"]
+        for got, want in zip(pr.digit_lookups, c["digit_lookups"]):
+            _check_lookup(got, want)
+        assert [[list(r.evaluations) for r in x.sumcheck.rounds] for x in pr.chain_prod_proofs] \
+            == c["chain_prods"]
+        for got, want in zip(pr.chain_rescale_proofs, c["chain_rescales"]):
+            _check_lookup(got.quant_lookup, want[0])
+            _check_lookup(got.resid_lookup, want[1])
+        assert list(pr.normalization_opening.values) == c["normalization"]
+        assert tr.state.hex() == c["state_end"]

@@ -274,3 +274,22 @@ def test_native_batched_transcript_ops_match_python(p):
     ca = a.challenge_vector(b"lookup/u", 25)
     cb = [b.challenge(b"lookup/u/%d" % i) for i in range(25)]
     assert ca == cb and a.state == b.state
+
+
+def test_softmax_row_witness_restatement_matches_reference():
+    """nonlinear.softmax_row_witness restates gadgets.py:878-922 (float64
+    host code): identical xi', digits, partials, chain and probabilities to
+    the reference's own witness (tests/golden/softmax.json)."""
+    from types import SimpleNamespace
+
+    from paper_2508_21393_b200.nonlinear import softmax_row_witness
+
+    g = load_golden("softmax.json")
+    prm = g["params"]
+    params = SimpleNamespace(gamma_fp=prm["gamma"], zeta=prm["zeta"], xi=prm["xi"],
+                             radices=tuple(prm["radices"]), act_bound=prm["act_bound"])
+    for c in g["cases"]:
+        w = softmax_row_witness(c["z"], params, FIELDS[c["field"]])
+        assert w[0] == c["xi_prime"] and w[1] == c["digits"] and w[2] == c["partials"]
+        assert [[list(a), list(b), list(r)] for a, b, r in w[3]] == c["chain"]
+        assert list(w[4]) == c["p"]
