@@ -5,7 +5,10 @@ Module-attribute swap at every by-name import site:
   prove_lookup,
   compute_multiplicities -> zklora.lookup, zklora.gadgets
   prove_matmul,
-  prove_elementprod      -> zklora.gadgets, zklora.pipeline
+  prove_elementprod,
+  prove_rescale, prove_swiglu,
+  prove_rsqrt,
+  prove_softmax_row      -> zklora.gadgets, zklora.pipeline
   batch_inverse          -> zklora.field, zklora.lookup
   eq_table               -> zklora.mle, zklora.lookup, zklora.gadgets, zklora.commit
   fold_table             -> zklora.mle, zklora.sumcheck
@@ -18,7 +21,8 @@ import importlib
 
 
 def install(pkg=None):
-    from . import field as bf, gadgets as bg, lookup as bl, mle as bm, sumcheck as bs
+    from . import field as bf, gadgets as bg, lookup as bl, mle as bm, nonlinear as bn
+    from . import sumcheck as bs
 
     z = pkg or importlib.import_module("zklora")
     name = z.__name__
@@ -35,12 +39,15 @@ def install(pkg=None):
 
     # result / error classes of the reference
     type_saves = [(bs.TYPES, dict(bs.TYPES)), (bg.TYPES, dict(bg.TYPES)),
-                  (bl.TYPES, dict(bl.TYPES))]
+                  (bl.TYPES, dict(bl.TYPES)), (bn.TYPES, dict(bn.TYPES))]
     bs.TYPES.update(RoundPolynomial=zs.RoundPolynomial, SumcheckProof=zs.SumcheckProof)
     bg.TYPES.update(Opening=zg.Opening, MatmulProof=zg.MatmulProof,
                     ElementprodProof=zg.ElementprodProof)
     bl.TYPES.update(LookupProof=zl.LookupProof, ElementNotInTable=zl.ElementNotInTable,
                     PoleCollision=zl.PoleCollision)
+    bn.TYPES.update({k: getattr(zg, k) for k in ("RescaleProof", "SwigluProof", "RsqrtProof",
+                                                  "SoftmaxRowProof", "NormalizationBudgetExceeded")
+                     if hasattr(zg, k)})
 
     def batch_inverse(values, modulus):
         try:
@@ -56,6 +63,8 @@ def install(pkg=None):
     for m in (zg, mods["pipeline"]):
         swap(m, "prove_matmul", bg.prove_matmul)
         swap(m, "prove_elementprod", bg.prove_elementprod)
+        for name in ("prove_rescale", "prove_swiglu", "prove_rsqrt", "prove_softmax_row"):
+            swap(m, name, getattr(bn, name))
     for m in (mods["field"], zl):
         swap(m, "batch_inverse", batch_inverse)
     for m in (mods["mle"], zl, zg, mods["commit"]):

@@ -117,7 +117,8 @@ class SoftmaxRowProof:
 
 
 TYPES = {"RescaleProof": RescaleProof, "SwigluProof": SwigluProof, "RsqrtProof": RsqrtProof,
-         "SoftmaxRowProof": SoftmaxRowProof}
+         "SoftmaxRowProof": SoftmaxRowProof,
+         "NormalizationBudgetExceeded": NormalizationBudgetExceeded}
 
 
 # ---------------------------------------------------------------------------
@@ -391,7 +392,7 @@ def prove_softmax_row(z_row, p_row, witness, tables, key, tr, rng):
     drift = total - params.gamma_fp
     drift = (drift + p // 2) % p - p // 2  # to_signed
     if abs(drift) > normalization_budget(row_len, params):
-        raise NormalizationBudgetExceeded(
+        raise TYPES["NormalizationBudgetExceeded"](
             "row sum off by %d units (budget %d)" % (drift, normalization_budget(row_len, params)))
     return TYPES["SoftmaxRowProof"](
         num_vars=n, xi_prime=xi_prime, digit_refs=tuple(t.ref for t in digit_ts),

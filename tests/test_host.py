@@ -192,6 +192,12 @@ def test_install_swaps_reference_import_sites():
             import zklora.pipeline as zp
 
             assert zp.prove_matmul is zb.prove_matmul
+            for name in ("prove_rescale", "prove_swiglu", "prove_rsqrt", "prove_softmax_row"):
+                assert getattr(zg, name) is getattr(zb, name)
+                assert getattr(zp, name) is getattr(zb, name)
+            from paper_2508_21393_b200 import nonlinear as bn
+
+            assert bn.TYPES["RescaleProof"] is zg.RescaleProof
             from paper_2508_21393_b200 import sumcheck as bs
 
             assert bs.TYPES["SumcheckProof"] is zs.SumcheckProof
