@@ -430,6 +430,59 @@ def run_sweep(ns, mont_peak=None):
     return out
 
 
+def run_hbm_kernels(peak_gbs):
+    """The HBM-bound passes of the path, timed live with CUDA events on the
+    proving stream (10 launches each, 2^27-entry inputs > L2): achieved GB/s
+    against the algorithmic bytes, and the fraction of the measured HBM peak."""
+    import ctypes
+
+    import torch
+
+    from paper_2508_21393_b200 import device as D
+    from paper_2508_21393_b200 import lookup as L
+    from paper_2508_21393_b200 import nonlinear as NL
+    from paper_2508_21393_b200.commit_stub import StubCommitment
+    from types import SimpleNamespace
+
+    spec = D.spec_for(P_BIG)
+    n = 1 << 27
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x16 = torch.randint(-32768, 32768, (n,), device="cuda", generator=g, dtype=torch.int32).short()
+    w64 = torch.randint(-(1 << 26), 1 << 26, (n,), device="cuda", generator=g, dtype=torch.int64)
+    fp = SimpleNamespace(zeta=4096, gamma_fp=4096, act_bound=8)
+    tab = NL.device_range_table(-32768, 1 << 16, spec, StubCommitment(16), "quant_range")
+    out = D.empty(spec, n)
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, nbytes, reps=10):
+        fn()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        gbs = nbytes / (ms / 1000.0) / 1e9
+        return {"ms": ms, "bytes": nbytes, "achieved_gbs": gbs, "frac": gbs / peak_gbs}
+
+    lifted = D.LiftedColumn(x16, spec)
+    res = {
+        "k_lift (int16 -> Fr, 2^27)": timed(lambda: D.lift(x16, spec, out=out), n * (2 + 32)),
+        "k_rescale_witness (int64 -> q, r int16, 2^27)": timed(
+            lambda: NL.rescale_witness_device(w64, 4096, fp, clip=True), n * (8 + 2 + 2)),
+        "k_range_count (int16 vs 2^16 range, index out, 2^27)": timed(
+            lambda: L.multiplicities_range(lifted, tab, x16, tab.int_column), n * (2 + 4)),
+    }
+    del out, x16, w64
+    torch.cuda.empty_cache()
+    return {"note": "algorithmic bytes: input read + outputs written once; each call "
+                    "includes its host wrapper (allocation, one stream sync)",
+            "peak_gbs": peak_gbs, "kernels": res}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -584,6 +637,8 @@ def main():
     if not args.no_cfg4:
         cfg4 = run_cfg4(max(1, args.steps // 10), 1, args.cfg4_shape)
 
+    hbm = run_hbm_kernels(float(peaks.get("hbm_gbs", 6650.0)))
+
     cfg5 = None
     if not args.no_cfg5:
         mont_peak = 4.2e10  # Fr255 Montgomery products/s, tools/mont_bench.cu (profiles/r01)
@@ -640,6 +695,7 @@ def main():
         "cfg3": cfg3,
         "cfg4": cfg4,
         "cfg5": cfg5,
+        "hbm_kernels": hbm,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -297,11 +297,133 @@ int op_from_mont(void* dst, const void* src, uint64_t n, cudaStream_t s) {
   ZKL_LAUNCH_CHECK();
   return kOk;
 }
+// Fr255 lift through look-up tables (one Montgomery product per table entry,
+// built once per process and device, 10 MB, L2-resident): int16 values index
+// a signed 2^16-entry table; wider values are split into 16-bit chunks c_k of
+// |x| and summed as sum_k T_k[c_k] with T_k[c] = (c 2^(16k)) R mod p, then
+// negated.  The per-element Montgomery product of from_i64 made the lift
+// IMAD-bound (2^27 entries: 3.1 ms, 22% of HBM); the tables make it a
+// gather + adds, bound by the 32-byte writes.
+template <class F>
+__global__ void k_lift_luts(typename F::T* t16, typename F::T* chunks) {
+  using T = typename F::T;
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 65536) return;
+  t16[i] = F::from_i64((int64_t)i - 32768);
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    const uint64_t m = (uint64_t)i << (16 * k);
+    T a = F::zero();
+    a.v[0] = (uint32_t)m;
+    a.v[1] = (uint32_t)(m >> 32);
+    chunks[k * 65536 + i] = F::mul(a, F::r2());
+  }
+}
+// A warp's 32 consecutive 32-byte elements stored as 64 consecutive 16-byte
+// chunks, lane t writing chunks t and 32 + t (halves exchanged by shuffles):
+// every store instruction fills whole 32-byte sectors (one element per lane,
+// written as two 16-byte halves, leaves each sector half-written per
+// instruction and triples the L2 sector writes).
+ZKL_D void store_warp_fr(fr_t* dst_warp, const fr_t& v, int lane) {
+  const uint4 lo = make_uint4(v.v[0], v.v[1], v.v[2], v.v[3]);
+  const uint4 hi = make_uint4(v.v[4], v.v[5], v.v[6], v.v[7]);
+  uint4* out = reinterpret_cast<uint4*>(dst_warp);
+#pragma unroll
+  for (int part = 0; part < 2; part++) {
+    const int src = part * 16 + (lane >> 1);
+    uint4 a, b;
+    a.x = __shfl_sync(0xffffffffu, lo.x, src);
+    a.y = __shfl_sync(0xffffffffu, lo.y, src);
+    a.z = __shfl_sync(0xffffffffu, lo.z, src);
+    a.w = __shfl_sync(0xffffffffu, lo.w, src);
+    b.x = __shfl_sync(0xffffffffu, hi.x, src);
+    b.y = __shfl_sync(0xffffffffu, hi.y, src);
+    b.z = __shfl_sync(0xffffffffu, hi.z, src);
+    b.w = __shfl_sync(0xffffffffu, hi.w, src);
+    out[part * 32 + lane] = (lane & 1) ? b : a;
+  }
+}
+
+template <class F>
+__global__ void k_lift16_lut(typename F::T* dst, const int16_t* src, uint64_t n,
+                             const typename F::T* t16) {
+  using T = typename F::T;
+  // four entries per thread per step: all four L2 table loads are in flight
+  // before the first store; full warps store whole sectors (store_warp_fr)
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  for (; i - lane + 31 + 3 * stride < n; i += 4 * stride) {  // warp-uniform condition
+    T v[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) v[k] = t16[(int)src[i + k * stride] + 32768];
+    if constexpr (F::kId == 0) {
+#pragma unroll
+      for (int k = 0; k < 4; k++) store_warp_fr(dst + (i - lane) + k * stride, v[k], lane);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; k++) dst[i + k * stride] = v[k];
+    }
+  }
+  for (; i < n; i += stride) dst[i] = t16[(int)src[i] + 32768];
+}
+template <class F, class I>
+__global__ void k_lift_chunks(typename F::T* dst, const I* src, uint64_t n,
+                              const typename F::T* chunks) {
+  using T = typename F::T;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const int64_t x = (int64_t)src[i];
+    const uint64_t m = x < 0 ? (uint64_t)(-(x + 1)) + 1u : (uint64_t)x;
+    T r = chunks[m & 0xffffu];
+    if (m >> 16) {
+      r = F::add(r, chunks[65536 + ((m >> 16) & 0xffffu)]);
+      if (m >> 32) {
+        r = F::add(r, chunks[2 * 65536 + ((m >> 32) & 0xffffu)]);
+        if (m >> 48) r = F::add(r, chunks[3 * 65536 + (m >> 48)]);
+      }
+    }
+    dst[i] = x < 0 ? F::sub(F::zero(), r) : r;
+  }
+}
+// per-device tables, built on first use (the C-ABI is single-owner)
+static std::mutex g_lut_mu;
+static std::map<int, void*> g_lift_luts;
+static int lift_luts_fr(const fr_t** t16, const fr_t** chunks, cudaStream_t s) {
+  int dev = 0;
+  ZKL_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_lut_mu);
+  void*& p = g_lift_luts[dev];
+  if (!p) {
+    ZKL_CUDA(cudaMalloc(&p, 5 * 65536 * sizeof(fr_t)));
+    fr_t* base = (fr_t*)p;
+    k_lift_luts<Fr255><<<256, 256, 0, s>>>(base, base + 65536);
+    ZKL_LAUNCH_CHECK();
+  }
+  *t16 = (const fr_t*)p;
+  *chunks = (const fr_t*)p + 65536;
+  return kOk;
+}
+
 template <class F>
 int op_lift(void* dst, const void* src, int mtype, uint64_t n, cudaStream_t s) {
   if (!n) return kOk;
   auto* d = (typename F::T*)dst;
   unsigned g = grid_for(n, 256);
+  if constexpr (F::kId == 0) {
+    if (n >= 4096 && mtype >= 1 && mtype <= 3) {
+      const fr_t *t16, *ch;
+      int rc = lift_luts_fr(&t16, &ch, s);
+      if (rc) return rc;
+      switch (mtype) {
+        case 1: k_lift16_lut<F><<<g, 256, 0, s>>>(d, (const int16_t*)src, n, t16); break;
+        case 2: k_lift_chunks<F, int32_t><<<g, 256, 0, s>>>(d, (const int32_t*)src, n, ch); break;
+        default: k_lift_chunks<F, int64_t><<<g, 256, 0, s>>>(d, (const int64_t*)src, n, ch); break;
+      }
+      ZKL_LAUNCH_CHECK();
+      return kOk;
+    }
+  }
   switch (mtype) {
     case 1: k_lift<F, int16_t><<<g, 256, 0, s>>>(d, (const int16_t*)src, n); break;
     case 2: k_lift<F, int32_t><<<g, 256, 0, s>>>(d, (const int32_t*)src, n); break;
@@ -609,17 +731,22 @@ int op_read(uint8_t* host, const void* src, uint64_t n, cudaStream_t s) {
 // reference's RangeViolation: the first such index is reported, and with
 // clip != 0 q is clamped (and counted) instead.  One pass: 8 B in, 4 B out.
 template <class W>
-__global__ void k_rescale_witness(const W* wide, uint64_t n, int64_t divisor, int64_t lift,
-                                  int64_t qmin, int64_t qmax, int16_t* q_out, int16_t* r_out,
-                                  int clip, unsigned long long* first_bad,
+__global__ void k_rescale_witness(const W* wide, uint64_t n, int64_t divisor, int shift,
+                                  int64_t lift, int64_t qmin, int64_t qmax, int16_t* q_out,
+                                  int16_t* r_out, int clip, unsigned long long* first_bad,
                                   unsigned long long* n_bad) {
   unsigned bad = 0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const int64_t w = (int64_t)wide[i];
     const int64_t t = w + divisor / 2;
-    int64_t q = t / divisor;
-    if ((t % divisor != 0) && (t < 0)) q -= 1;  // floor division
+    int64_t q;
+    if (shift >= 0) {
+      q = t >> shift;  // arithmetic shift = floor division by 2^shift
+    } else {
+      q = t / divisor;
+      if ((t % divisor != 0) && (t < 0)) q -= 1;  // floor division
+    }
     const int64_t r = w - divisor * q;
     if (q < qmin || q > qmax) {
       atomicMin(first_bad, (unsigned long long)i);
@@ -648,14 +775,19 @@ int op_rescale_witness(const void* wide, int wide_type, uint64_t n, int64_t divi
   unsigned long long* flag = (unsigned long long*)ws;
   ZKL_CUDA(cudaMemsetAsync(flag, 0xff, 8, s));
   ZKL_CUDA(cudaMemsetAsync(flag + 1, 0, 8, s));
+  int shift = -1;  // divisor = 2^shift: shifts instead of 64-bit division
+  if ((divisor & (divisor - 1)) == 0) {
+    shift = 0;
+    while ((1ll << shift) < divisor) shift++;
+  }
   if (n) {
     const unsigned g = grid_for(n, 256);
     switch (wide_type) {
-      case 1: k_rescale_witness<int16_t><<<g, 256, 0, s>>>((const int16_t*)wide, n, divisor, lift,
+      case 1: k_rescale_witness<int16_t><<<g, 256, 0, s>>>((const int16_t*)wide, n, divisor, shift, lift,
                   qmin, qmax, q_out, r_out, clip, flag, flag + 1); break;
-      case 2: k_rescale_witness<int32_t><<<g, 256, 0, s>>>((const int32_t*)wide, n, divisor, lift,
+      case 2: k_rescale_witness<int32_t><<<g, 256, 0, s>>>((const int32_t*)wide, n, divisor, shift, lift,
                   qmin, qmax, q_out, r_out, clip, flag, flag + 1); break;
-      case 3: k_rescale_witness<int64_t><<<g, 256, 0, s>>>((const int64_t*)wide, n, divisor, lift,
+      case 3: k_rescale_witness<int64_t><<<g, 256, 0, s>>>((const int64_t*)wide, n, divisor, shift, lift,
                   qmin, qmax, q_out, r_out, clip, flag, flag + 1); break;
       default: set_error("rescale_witness: int16/int32/int64 only"); return kErrArg;
     }

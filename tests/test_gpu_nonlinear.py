@@ -327,3 +327,20 @@ def test_softmax_row_golden(where):
             _check_lookup(got.resid_lookup, want[1])
         assert list(pr.normalization_opening.values) == c["normalization"]
         assert tr.state.hex() == c["state_end"]
+
+
+@pytest.mark.parametrize("field", ["big", "test"])
+@pytest.mark.parametrize("dtype", [torch.int16, torch.int32, torch.int64])
+@pytest.mark.parametrize("n", [100, (1 << 16) + 3])
+def test_lift_signed_ints(field, dtype, n):
+    """D.lift (field.py:54-55 from_signed; look-up-table path for n >= 4096)
+    equals v mod p for every entry, extremes included."""
+    p = FIELDS[field]
+    spec = D.spec_for(p)
+    info = torch.iinfo(dtype)
+    g = torch.Generator().manual_seed(n)
+    t = torch.randint(info.min, info.max, (n,), generator=g, dtype=torch.int64).to(dtype)
+    edge = [info.min, info.max, 0, 1, -1, 65535 % (info.max + 1), -65536 % info.min if dtype != torch.int16 else -32768]
+    t[: len(edge)] = torch.tensor(edge, dtype=torch.int64).to(dtype)
+    got = D.download(D.lift(t.cuda(), spec), spec, n)
+    assert got == [int(v) % p for v in t.tolist()]
