@@ -712,6 +712,160 @@ __global__ void __launch_bounds__(256, (R == 2 ? 3 : 2))
     mvw_rows_group<R>(M, rows, cols, xsm, cch, n, c0, r0, lane, acc_out);
 }
 
+// Tensor-core int16 row products (mma.sync m16n8k32 u8 x u8 -> s32).  The
+// field vector is split into its 32 bytes and each offset-binary entry
+// u = s + 2^15 into two bytes, so y_r = sum_c u_rc x_c is
+//   sum_{s in lo,hi} sum_{n < 32} 2^(8(n+s)) * (sum_c u_s[r][c] x_n[c]),
+// a 16-row x 32-byte x K GEMM per warp whose int32 outputs are exact (each
+// < 255 * 255 * K, K <= 256 per chunk).  The byte sums are folded into the
+// same per-limb u64 row records as k_mvw_rows (limb b/4, shift 8 (b % 4);
+// the top byte b = 32 goes to limb 7 << 32), so k_mvf_finish and the
+// OFF * sum(x) correction are shared.  x is staged as 32 byte planes with a
+// 16-byte skew per plane (conflict-free B-fragment loads); the integer pipe
+// then only assembles fragments: the IMAD-bound MAC loop becomes a load
+// stream.
+constexpr int kTcK = 256;  // columns per chunk: 8 k-steps, all loads issued up front
+
+ZKL_D void mma_u8(uint32_t (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__global__ void __launch_bounds__(256)
+    k_mvt_rows(const int16_t* M, uint64_t rows, uint64_t cols, const fr_t* x,
+               uint64_t* acc_out) {
+  // plane stride: a 32-byte skew keeps the per-half-warp 8-byte B loads
+  // (plane 8t + g, offset 8 tig) on distinct banks
+  constexpr int PS = kTcK + 32;
+  constexpr int kSteps = kTcK / 32;
+  extern __shared__ __align__(16) uint8_t planes[];  // 32 x PS
+  const uint64_t c0 = blockIdx.y * (uint64_t)kTcK;
+  const int n = (int)((c0 + kTcK < cols ? c0 + kTcK : cols) - c0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tig = lane & 3;
+  const uint64_t r0 = (blockIdx.x * 8ull + warp) * 16;
+  const bool active = r0 < rows;
+  // The reduction order over k is free, so each thread's A fragment holds the
+  // 8 consecutive columns it loads with one 16-byte load per row (k slots
+  // tig*4..+3 <- columns 8 tig..+3, slots 16 + tig*4.. <- 8 tig + 4..7), and
+  // its B fragment is the matching 8 bytes of one x byte plane.  The warp's
+  // whole 16 x kTcK tile is requested first, so its latency overlaps the x
+  // staging below.
+  const int16_t* rowA = M + (r0 + g) * cols + c0 + tig * 8;
+  const int16_t* rowB = rowA + 8 * cols;
+  uint4 buf[kSteps][2];
+#pragma unroll
+  for (int st = 0; st < kSteps; st++) {
+    const int k = st * 32;
+    if (active && k < n) {
+      buf[st][0] = __ldcs(reinterpret_cast<const uint4*>(rowA + k));
+      buf[st][1] = __ldcs(reinterpret_cast<const uint4*>(rowB + k));
+    }
+  }
+  // stage x[c0 .. c0+n) as byte planes: a thread takes 4 consecutive elements
+  for (int j4 = threadIdx.x * 4; j4 < n; j4 += blockDim.x * 4) {
+    uint32_t w[4][8];
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const fr_t v = j4 + e < n ? x[c0 + j4 + e] : fr_t{};
+#pragma unroll
+      for (int l = 0; l < 8; l++) w[e][l] = v.v[l];
+    }
+#pragma unroll
+    for (int l = 0; l < 8; l++) {
+#pragma unroll
+      for (int b = 0; b < 4; b++) {
+        // byte b of limb l of the 4 elements -> plane 4l+b, offset j4
+        const uint32_t lo = __byte_perm(w[0][l], w[1][l], 0x0040 + b * 0x0011) & 0xffffu;
+        const uint32_t hi = __byte_perm(w[2][l], w[3][l], 0x0040 + b * 0x0011) & 0xffffu;
+        *reinterpret_cast<uint32_t*>(planes + (4 * l + b) * PS + j4) = lo | (hi << 16);
+      }
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0) chunk_sum_atomic(x, c0, n, acc_out + rows * 8);
+  if (!active) return;
+  uint32_t acc[2][4][4];
+#pragma unroll
+  for (int sl = 0; sl < 2; sl++)
+#pragma unroll
+    for (int t = 0; t < 4; t++)
+#pragma unroll
+      for (int q = 0; q < 4; q++) acc[sl][t][q] = 0;
+#pragma unroll
+  for (int st = 0; st < kSteps; st++) {
+    const int k = st * 32;
+    if (k >= n) break;
+    uint32_t alo[4], ahi[4];
+    // a0 / a2: row g, columns 8 tig + 0..3 / 4..7; a1 / a3: row g + 8.
+    // Offset binary: flip each int16's sign bit.
+    const uint4 ra = buf[st][0], rb = buf[st][1];
+    const uint32_t wa[4] = {ra.x ^ 0x80008000u, ra.y ^ 0x80008000u, ra.z ^ 0x80008000u,
+                            ra.w ^ 0x80008000u};
+    const uint32_t wb[4] = {rb.x ^ 0x80008000u, rb.y ^ 0x80008000u, rb.z ^ 0x80008000u,
+                            rb.w ^ 0x80008000u};
+    alo[0] = __byte_perm(wa[0], wa[1], 0x6420);
+    ahi[0] = __byte_perm(wa[0], wa[1], 0x7531);
+    alo[1] = __byte_perm(wb[0], wb[1], 0x6420);
+    ahi[1] = __byte_perm(wb[0], wb[1], 0x7531);
+    alo[2] = __byte_perm(wa[2], wa[3], 0x6420);
+    ahi[2] = __byte_perm(wa[2], wa[3], 0x7531);
+    alo[3] = __byte_perm(wb[2], wb[3], 0x6420);
+    ahi[3] = __byte_perm(wb[2], wb[3], 0x7531);
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      const uint2 bb =
+          *reinterpret_cast<const uint2*>(planes + (8 * t + g) * PS + k + tig * 8);
+      mma_u8(acc[0][t], alo, bb.x, bb.y);
+      mma_u8(acc[1][t], ahi, bb.x, bb.y);
+    }
+  }
+  // fold byte sums into per-limb records for rows g and g + 8: the sum for
+  // byte position b = 8t + rel (rel = 2 tig + (q & 1) + slice, 0..8) goes to
+  // limb 2t + (rel >> 2) shifted by 8 (rel & 3); b = 32 goes to limb 7 << 32
+  uint64_t e[2][8];
+#pragma unroll
+  for (int h = 0; h < 2; h++)
+#pragma unroll
+    for (int l = 0; l < 8; l++) e[h][l] = 0;
+#pragma unroll
+  for (int sl = 0; sl < 2; sl++)
+#pragma unroll
+    for (int t = 0; t < 4; t++)
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const int h = q >> 1;  // c0, c1: row g; c2, c3: row g + 8
+        const int rel = 2 * tig + (q & 1) + sl;
+        const uint64_t v = (uint64_t)acc[sl][t][q] << (8 * (rel & 3));
+        const int off = rel >> 2;
+        e[h][2 * t] += off == 0 ? v : 0;
+        e[h][2 * t + 1] += off == 1 ? v : 0;
+        if (t < 3) e[h][2 * t + 2] += off == 2 ? v : 0;
+        else e[h][7] += off == 2 ? ((uint64_t)acc[sl][t][q] << 32) : 0;
+      }
+#pragma unroll
+  for (int h = 0; h < 2; h++)
+#pragma unroll
+    for (int l = 0; l < 8; l++) {
+      e[h][l] += __shfl_xor_sync(kFull, e[h][l], 1);
+      e[h][l] += __shfl_xor_sync(kFull, e[h][l], 2);
+    }
+  if (tig == 0) {
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const uint64_t r = r0 + g + 8 * h;
+      if (r < rows) {
+        unsigned long long* d = reinterpret_cast<unsigned long long*>(acc_out + r * 8);
+#pragma unroll
+        for (int l = 0; l < 8; l++) atomicAdd(d + l, (unsigned long long)e[h][l]);
+      }
+    }
+  }
+}
+
 // y[i] = reduce(acc[i]) - K; one thread per output (acc: atomically summed
 // raw words of every chunk -- exact integer sums, order-independent)
 template <int CH>
@@ -764,6 +918,28 @@ static int matvec_fast(const MT* M, uint64_t rows, uint64_t cols, int transpose,
       const char* e = getenv("ZKL_MVW_WAVES");
       return e ? (uint64_t)atoi(e) : (uint64_t)2;
     }();
+    static const bool kTc = [] {
+      const char* e = getenv("ZKL_MV_TC");
+      return !(e && atoi(e) == 0);
+    }();
+    if (kTc && rows % 16 == 0 && cols % 32 == 0) {
+      nchunks = (cols + kTcK - 1) / kTcK;
+      nout = rows;
+      rc = scratch_reserve(rows * NW * 8 + 128, &ws, s);
+      if (rc) return rc;
+      ZKL_CUDA(cudaMemsetAsync(ws, 0, rows * NW * 8 + 64, s));
+      const size_t smem = 32 * (kTcK + 32);
+      static bool tc_attr = false;
+      if (!tc_attr) {
+        ZKL_CUDA(cudaFuncSetAttribute(k_mvt_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        tc_attr = true;
+      }
+      dim3 g((unsigned)((rows + 127) / 128), (unsigned)nchunks);
+      k_mvt_rows<<<g, 256, smem, s>>>((const int16_t*)M, rows, cols, x, (uint64_t*)ws);
+      ZKL_LAUNCH_CHECK();
+      goto finish;
+    }
     const int RW = kRw;
     if (cols % 128) return kErrUnsupported;
     const uint64_t rblocks = (rows + 8 * RW - 1) / (8 * RW);
@@ -847,6 +1023,7 @@ static int matvec_fast(const MT* M, uint64_t rows, uint64_t cols, int transpose,
     k_mvf_cols<MT, V><<<g, 256, smem, s>>>(M, rows, cols, x, rch, (uint64_t*)ws);
     ZKL_LAUNCH_CHECK();
   }
+finish:
   // y = reduce(acc) - OFF * sum(x); OFF (2^15 or 2^63) in Montgomery form
   static fr_t offr = [] {
     fr_t v = Fr255::zero();
