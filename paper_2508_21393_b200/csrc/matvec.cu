@@ -866,6 +866,182 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Tensor-core int16 COLUMN products y_c = sum_r M[r][c] x_r (M^T x), the
+// same byte-sliced GEMM as k_mvt_rows with the roles of the operands swapped:
+//   D[byte m][col c] = sum_r X[m][r] * U_slice[r][c]   (m16n8k32, u8 x u8),
+// A = the 32 byte planes of x (two 16-byte m-tiles), B = a slice of the
+// offset-binary matrix.  A block stages a 256-row x 128-column tile of M
+// row-major in shared memory (coalesced 16-byte loads); ldmatrix.trans
+// hands each thread M[8i + 2 tig + {0,1}][c0 + g] for the four 8-row groups
+// i, so the k slots of both fragments follow the permutation
+//   slot tig*4 + 2i' + j  <->  row 8 i' + 2 tig + j      (i' = 0, 1)
+//   slot 16 + tig*4 + 2i' + j <-> row 16 + 8 i' + 2 tig + j,
+// and x is staged into its byte planes in that slot order (one LDS.32 per A
+// register).  Each warp owns 16 columns (two n-tiles); the byte sums are
+// folded into the shared per-limb column records.
+constexpr int kTcR = 256;          // rows per block (K)
+constexpr int kTcC = 128;          // columns per block (8 warps x 16)
+constexpr int kTcMP = kTcC * 2 + 16;  // smem row pitch of the M tile (bytes)
+
+ZKL_D int slot_of_row(int r) {  // r in [0, 32): k slot of row r
+  const int half = r >> 4, rr = r & 15;
+  const int i = rr >> 3, t = (rr & 7) >> 1, j = r & 1;
+  return half * 16 + t * 4 + 2 * i + j;
+}
+
+__global__ void __launch_bounds__(256)
+    k_mvt_cols(const int16_t* M, uint64_t rows, uint64_t cols, const fr_t* x,
+               uint64_t* acc_out) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  uint8_t* mt = sm;                           // kTcR x kTcMP bytes
+  uint8_t* planes = sm + kTcR * kTcMP;        // 32 x (kTcR + 16)
+  constexpr int XP = kTcR + 16;
+  const uint64_t r0 = blockIdx.y * (uint64_t)kTcR;
+  const uint64_t c0 = blockIdx.x * (uint64_t)kTcC;
+  const int nr = (int)((r0 + kTcR < rows ? r0 + kTcR : rows) - r0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tig = lane & 3;
+  // stage the M tile (row-major, offset binary applied at fragment time)
+  {
+    constexpr int kPerRow = kTcC / 8;  // uint4 per tile row
+    uint4 v[kTcR * kPerRow / 256];
+#pragma unroll
+    for (int q = 0; q < kTcR * kPerRow / 256; q++) {
+      const int idx = threadIdx.x + q * 256;
+      const int r = idx / kPerRow, cq = idx % kPerRow;
+      v[q] = (r < nr && c0 + cq * 8 < cols)
+                 ? __ldcs(reinterpret_cast<const uint4*>(M + (r0 + r) * cols + c0 + cq * 8))
+                 : make_uint4(0x80008000u, 0x80008000u, 0x80008000u, 0x80008000u);
+    }
+#pragma unroll
+    for (int q = 0; q < kTcR * kPerRow / 256; q++) {
+      const int idx = threadIdx.x + q * 256;
+      const int r = idx / kPerRow, cq = idx % kPerRow;
+      *reinterpret_cast<uint4*>(mt + r * kTcMP + cq * 16) = v[q];
+    }
+  }
+  // stage x[r0 .. r0+nr) as byte planes in k-slot order (4 elements a thread)
+  for (int j4 = threadIdx.x * 4; j4 < kTcR; j4 += blockDim.x * 4) {
+    uint32_t w[4][8];
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const fr_t v = j4 + e < nr ? x[r0 + j4 + e] : fr_t{};
+#pragma unroll
+      for (int l = 0; l < 8; l++) w[e][l] = v.v[l];
+    }
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const int r = j4 + e;
+      const int pos = (r & ~31) + slot_of_row(r & 31);
+#pragma unroll
+      for (int l = 0; l < 8; l++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) planes[(4 * l + b) * XP + pos] = (uint8_t)(w[e][l] >> (8 * b));
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0) chunk_sum_atomic(x, r0, nr, acc_out + cols * 8);
+  const uint64_t wc = c0 + warp * 16;  // this warp's 16 columns
+  if (wc >= cols) return;
+  uint32_t acc[2][2][2][4];  // [m-tile][n-tile][slice][frag]
+#pragma unroll
+  for (int a = 0; a < 2; a++)
+#pragma unroll
+    for (int b = 0; b < 2; b++)
+#pragma unroll
+      for (int sl = 0; sl < 2; sl++)
+#pragma unroll
+        for (int q = 0; q < 4; q++) acc[a][b][sl][q] = 0;
+  const uint32_t mt_base = (uint32_t)__cvta_generic_to_shared(mt);
+  for (int k = 0; k < nr; k += 32) {
+    // A: x byte planes, rows in slot order: a0 / a2 plane m at slots tig*4 /
+    // 16 + tig*4, a1 / a3 plane m + 8
+    uint32_t afr[2][4];
+#pragma unroll
+    for (int mtile = 0; mtile < 2; mtile++) {
+      const uint8_t* p0 = planes + (16 * mtile + g) * XP + k + tig * 4;
+      const uint8_t* p1 = p0 + 8 * XP;
+      afr[mtile][0] = *reinterpret_cast<const uint32_t*>(p0);
+      afr[mtile][1] = *reinterpret_cast<const uint32_t*>(p1);
+      afr[mtile][2] = *reinterpret_cast<const uint32_t*>(p0 + 16);
+      afr[mtile][3] = *reinterpret_cast<const uint32_t*>(p1 + 16);
+    }
+#pragma unroll
+    for (int nt = 0; nt < 2; nt++) {
+      // ldmatrix.x4.trans: matrix i = rows k + 8i .. +7, columns wc + 8 nt .. +7
+      const int row = k + lane;  // lanes 8i..8i+7 address matrix i's rows
+      const uint32_t addr = mt_base + row * kTcMP + (uint32_t)((wc - c0) + 8 * nt) * 2;
+      uint32_t m0, m1, m2, m3;
+      asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(m0), "=r"(m1), "=r"(m2), "=r"(m3) : "r"(addr));
+      m0 ^= 0x80008000u; m1 ^= 0x80008000u; m2 ^= 0x80008000u; m3 ^= 0x80008000u;
+      // b0: rows 2tig+{0,1} (m0), 8+2tig+{0,1} (m1); b1: the same 16 rows on
+      const uint32_t blo0 = __byte_perm(m0, m1, 0x6420), bhi0 = __byte_perm(m0, m1, 0x7531);
+      const uint32_t blo1 = __byte_perm(m2, m3, 0x6420), bhi1 = __byte_perm(m2, m3, 0x7531);
+#pragma unroll
+      for (int mtile = 0; mtile < 2; mtile++) {
+        mma_u8(acc[mtile][nt][0], afr[mtile], blo0, blo1);
+        mma_u8(acc[mtile][nt][1], afr[mtile], bhi0, bhi1);
+      }
+    }
+  }
+  // fold: lane (g, tig) holds, for columns 2 tig, 2 tig + 1 of each n-tile,
+  // the byte sums of bytes m = g, g + 8 (m-tile 0) and g + 16, g + 24
+  uint64_t e[2][2][8];  // [n-tile][column parity][limb]
+#pragma unroll
+  for (int nt = 0; nt < 2; nt++)
+#pragma unroll
+    for (int cp = 0; cp < 2; cp++)
+#pragma unroll
+      for (int l = 0; l < 8; l++) e[nt][cp][l] = 0;
+#pragma unroll
+  for (int mtile = 0; mtile < 2; mtile++)
+#pragma unroll
+    for (int nt = 0; nt < 2; nt++)
+#pragma unroll
+      for (int sl = 0; sl < 2; sl++)
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const int cp = q & 1;
+          const int mrel = 16 * mtile + 8 * (q >> 1);  // byte = g + mrel
+          const int bpos = g + mrel + sl;              // 0 .. 32
+          const int l = bpos >> 2;                     // runtime (g): select below
+          const uint64_t v = (uint64_t)acc[mtile][nt][sl][q] << (8 * (bpos & 3));
+#pragma unroll
+          for (int ll = 0; ll < 8; ll++) {
+            // bpos 32 (g = 7, top m-tile row 24, hi slice) -> limb 7 << 32
+            const uint64_t add = (ll == 7 && bpos == 32) ? ((uint64_t)acc[mtile][nt][sl][q] << 32)
+                                 : (l == ll ? v : 0);
+            e[nt][cp][ll] += add;
+          }
+        }
+#pragma unroll
+  for (int nt = 0; nt < 2; nt++)
+#pragma unroll
+    for (int cp = 0; cp < 2; cp++)
+#pragma unroll
+      for (int l = 0; l < 8; l++) {
+        uint64_t t = e[nt][cp][l];
+        t += __shfl_xor_sync(kFull, t, 4);
+        t += __shfl_xor_sync(kFull, t, 8);
+        t += __shfl_xor_sync(kFull, t, 16);
+        e[nt][cp][l] = t;
+      }
+  if (g == 0) {
+#pragma unroll
+    for (int nt = 0; nt < 2; nt++)
+#pragma unroll
+      for (int cp = 0; cp < 2; cp++) {
+        const uint64_t c = wc + 8 * nt + 2 * tig + cp;
+        if (c < cols) {
+          unsigned long long* d = reinterpret_cast<unsigned long long*>(acc_out + c * 8);
+#pragma unroll
+          for (int l = 0; l < 8; l++) atomicAdd(d + l, (unsigned long long)e[nt][cp][l]);
+        }
+      }
+  }
+}
+
 // y[i] = reduce(acc[i]) - K; one thread per output (acc: atomically summed
 // raw words of every chunk -- exact integer sums, order-independent)
 template <int CH>
@@ -1000,6 +1176,29 @@ static int matvec_fast(const MT* M, uint64_t rows, uint64_t cols, int transpose,
     k_mvf_rows<MT, R><<<g, 256, smem, s>>>(M, rows, cols, x, cch, (uint64_t*)ws);
     ZKL_LAUNCH_CHECK();
   } else {
+    static const bool kTcCols = [] {
+      const char* e = getenv("ZKL_MV_TC");
+      return !(e && atoi(e) == 0);
+    }();
+    if (CH == 1 && kTcCols && cols % 16 == 0) {
+      nchunks = (rows + kTcR - 1) / kTcR;
+      if (nchunks > 65535) return kErrUnsupported;
+      nout = cols;
+      rc = scratch_reserve(cols * NW * 8 + 128, &ws, s);
+      if (rc) return rc;
+      ZKL_CUDA(cudaMemsetAsync(ws, 0, cols * NW * 8 + 64, s));
+      const size_t smem = kTcR * kTcMP + 32 * (kTcR + 16);
+      static bool tcc_attr = false;
+      if (!tcc_attr) {
+        ZKL_CUDA(cudaFuncSetAttribute(k_mvt_cols, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        tcc_attr = true;
+      }
+      dim3 g((unsigned)((cols + kTcC - 1) / kTcC), (unsigned)nchunks);
+      k_mvt_cols<<<g, 256, smem, s>>>((const int16_t*)M, rows, cols, x, (uint64_t*)ws);
+      ZKL_LAUNCH_CHECK();
+      goto finish;
+    }
     constexpr int V = sizeof(MT) == 2 ? 2 : 1;
     if (cols % V) return kErrUnsupported;
     const uint64_t threads = cols / V;

@@ -1,6 +1,6 @@
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15
 for tc in 1 0; do
-  ZKL_MV_TC=$tc ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:"k_mvt_rows|k_mvw_rows" --csv --log-file gpurun_out/mvt_tc$tc.csv python scratch/mv_bench.py > /dev/null 2>&1
+  ZKL_MV_TC=$tc ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:"k_mvt_|k_mvw_rows|k_mvf_cols" --csv --log-file gpurun_out/mvt_tc$tc.csv python scratch/mv_bench.py > /dev/null 2>&1
 done
 python - <<'PY'
 import csv, collections
