@@ -171,7 +171,9 @@ int zkl_multiplicities_index(int field, const void* secret, uint64_t d, const vo
  * looked up by its combined value secret[i] = x[i] + alpha y[i].  x, y:
  * ZKL_MT_I16 / ZKL_MT_I32 device columns of d entries; table_y: int32, n
  * entries; table: the combined table (n field elements).  Same outputs and
- * errors as zkl_multiplicities_index; ZKL_ERR_UNSUPPORTED (nothing written
+ * errors as zkl_multiplicities_index (secret may be NULL: a query off its table
+ * row is then reported as a miss without the hash probe, for an integer-only
+ * first pass); ZKL_ERR_UNSUPPORTED (nothing written
  * but the hash slots) when the combined table has duplicate values or the
  * column types are not int16/int32. */
 int zkl_pair_multiplicities(int field, const void* x, int x_type, const void* y, int y_type,

@@ -159,6 +159,8 @@ __global__ void k_pair_count(const TX* xs, const TY* ys, uint64_t d, int64_t x0,
       const int64_t idx = xi - x0;
       if (idx >= 0 && idx < (int64_t)n && (int64_t)__ldg(ty + idx) == yi) {
         hit = (uint32_t)idx;
+      } else if (secret == nullptr) {  // integer-only pass: the caller reruns with the values
+        atomicMin(first_miss, (unsigned long long)i);
       } else {
         const typename F::T v = secret[i];
         uint32_t h = hash_elem(v) & mask;

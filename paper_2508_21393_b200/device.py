@@ -182,6 +182,36 @@ class LiftedColumn(DeviceVector):
         return int(self.col[i]) % self.spec.modulus
 
 
+class PairColumn(DeviceVector):
+    """x + alpha*y over signed integer device columns (a pair lookup's
+    compressed secret, tables.py:131-140) as a DeviceVector whose 32-byte field
+    buffer is built only when something reads it: pair multiplicities bin from
+    the integers and the indexed logUp reads the table side, so for an
+    in-table secret the buffer is never written."""
+
+    __slots__ = ("x", "y", "alpha", "_buf")
+
+    def __init__(self, x, y, alpha, spec):
+        self.x, self.y = x.contiguous().view(-1), y.contiguous().view(-1)
+        self.alpha, self.spec = alpha, spec
+        self.n = self.x.numel()
+        self._buf = None
+
+    @property
+    def buf(self):
+        if self._buf is None:
+            self._buf = pair_combine(self.x, self.y, self.alpha, self.spec).buf
+        return self._buf
+
+    @property
+    def materialized(self):
+        return self._buf is not None
+
+    def value(self, i):
+        p = self.spec.modulus
+        return (int(self.x[i]) + self.alpha * int(self.y[i])) % p
+
+
 def field_buffer(values, spec):
     """Device storage for a DeviceVector or a sequence of residues."""
     if isinstance(values, DeviceVector):

@@ -487,7 +487,7 @@ def prove_pair_lookup(label, x, y, pair_table, key, tr, rng):
         blinding = tuple(a % p for a in bx)
     if (xd is not None and yd is not None and xd.mtype != N.MT_FIELD
             and yd.mtype != N.MT_FIELD and tx is not None and ty is not None):
-        secret = SecretVector(D.pair_combine(xd.t, yd.t, alpha, spec), secret_com, blinding)
+        secret = SecretVector(D.PairColumn(xd.t, yd.t, alpha, spec), secret_com, blinding)
         table = LookupTable(D.pair_combine(tx, ty, alpha, spec), table_com,
                             pair_table.name + "+a*y")
     else:

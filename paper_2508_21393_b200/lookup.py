@@ -157,7 +157,6 @@ def multiplicities_pair(secret, table, x, y, tx, ty):
         return None
     ty = ty.reshape(-1).to(torch.int32).contiguous()
     spec = secret.spec
-    sbuf = D.field_buffer(secret, spec)
     tbuf = D.field_buffer(table.entries, spec)
     d = len(secret)
     xs = x.contiguous().view(-1)
@@ -165,14 +164,25 @@ def multiplicities_pair(secret, table, x, y, tx, ty):
     counts = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
     index = torch.empty(max(d, 1), dtype=torch.int32, device="cuda")
     fm = ctypes.c_int64(-1)
-    rc = N.lib().zkl_pair_multiplicities(spec.fid, D.ptr(xs), D._INT_TYPES[xs.dtype], D.ptr(ys),
-                                         D._INT_TYPES[ys.dtype], d, x0, D.ptr(ty), D.ptr(sbuf),
-                                         D.ptr(tbuf), n, D.ptr(counts), D.ptr(index),
-                                         ctypes.byref(fm), D.stream())
+
+    def run(sbuf):
+        return N.lib().zkl_pair_multiplicities(
+            spec.fid, D.ptr(xs), D._INT_TYPES[xs.dtype], D.ptr(ys), D._INT_TYPES[ys.dtype], d, x0,
+            D.ptr(ty), D.ptr(sbuf) if sbuf is not None else None, D.ptr(tbuf), n, D.ptr(counts),
+            D.ptr(index), ctypes.byref(fm), D.stream())
+
+    # a lazy PairColumn is binned from its integers first (no field buffer);
+    # only a query off its table row needs the hash probe on x + alpha*y
+    lazy = isinstance(secret, D.PairColumn) and not secret.materialized
+    rc = run(None if lazy else D.field_buffer(secret, spec))
+    if lazy and rc == N.ZKL_ERR_MISSING:
+        rc = run(secret.buf)
     if rc == N.ZKL_ERR_UNSUPPORTED:
         return None
     if rc == N.ZKL_ERR_MISSING:
-        raise TYPES["ElementNotInTable"](fm.value, D.read_scalar(sbuf, spec, fm.value))
+        value = (secret.value(fm.value) if isinstance(secret, D.PairColumn)
+                 else D.read_scalar(D.field_buffer(secret, spec), spec, fm.value))
+        raise TYPES["ElementNotInTable"](fm.value, value)
     N.check(rc)
     out = D.empty(spec, n)
     N.check(N.lib().zkl_lift_u32(spec.fid, D.ptr(out), D.ptr(counts), n, D.stream()))
@@ -304,7 +314,8 @@ def prove_lookup(secret, multiplicities, table, key, tr, rng, secret_index=None)
 
     # a LiftedColumn secret is only lifted when a path below needs the field
     # values (the indexed, tiled d >= n path never does)
-    lazy = isinstance(entries, D.LiftedColumn) and secret_index is not None and d >= n
+    lazy = (isinstance(entries, (D.LiftedColumn, D.PairColumn)) and secret_index is not None
+            and d >= n)
     s_buf = None if lazy else D.field_buffer(entries, spec)
     t_buf = D.field_buffer(table.entries, spec)
     m_buf = D.field_buffer(multiplicities, spec)

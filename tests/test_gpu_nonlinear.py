@@ -344,3 +344,31 @@ def test_lift_signed_ints(field, dtype, n):
     t[: len(edge)] = torch.tensor(edge, dtype=torch.int64).to(dtype)
     got = D.download(D.lift(t.cuda(), spec), spec, n)
     assert got == [int(v) % p for v in t.tolist()]
+
+
+def test_pair_lookup_lazy_secret_miss_and_collision_free_path():
+    """prove_pair_lookup bins an in-table pair secret from its integers and
+    never builds the 32-byte x + alpha*y column; a query off its table row
+    falls back to the hash probe on the combined value and raises
+    ElementNotInTable(first index, x + alpha*y) like lookup.py:96-98."""
+    c = load_golden("pair_lookup.json")[0]
+    p = FIELDS[c["field"]]
+    n = len(c["x"])
+    nv = (n - 1).bit_length()
+
+    def pt(vals):
+        ref = TensorRef("committed", nv // 2, nv - nv // 2, commitment=StubCommitment(nv))
+        t = torch.tensor(vals, dtype=torch.int32).cuda().view(1 << (nv // 2), -1)
+        return ProverTensor(None, ref, (), device=DeviceMatrix.from_int_tensor(t))
+
+    tx = torch.tensor(c["table_x"], dtype=torch.int32).cuda()
+    ty = torch.tensor(c["table_y"], dtype=torch.int32).cuda()
+    pair = NL.PairTable(zb.LookupTable(tx, StubCommitment(7), "silu.x"),
+                        zb.LookupTable(ty, StubCommitment(7), "silu.y"), "silu")
+    y = list(c["y"])
+    y[40] += 1  # off its table row (and, with overwhelming probability, off the table)
+    y[90] += 3
+    tr = Transcript.from_state(bytes.fromhex(c["state_before"]), p)
+    with pytest.raises(zb.ElementNotInTable) as e:
+        zb.prove_pair_lookup(b"swiglu/act", pt(c["x"]), pt(y), pair, KEY, tr, _Rng())
+    assert e.value.index == 40 and 0 <= e.value.value < p
