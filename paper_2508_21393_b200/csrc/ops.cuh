@@ -55,6 +55,7 @@ struct Terms {
   const typename F::T* side_a;
   const typename F::T* side_s;
   uint64_t sidx_d;
+  uint64_t tiled_d;  // LOGUP_TILED: 2^num_vars (round 1 = the first fold: half * 4 == tiled_d)
 };
 template <class F>
 struct Post {

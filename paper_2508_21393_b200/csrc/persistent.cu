@@ -528,16 +528,18 @@ struct EvLogupTiled {
   ZKL_D static void accumulate(const TablePtrs<F, MAXK>& tabs, uint64_t half, bool fold,
                                const T& r, const Terms<F>& tm, uint64_t gtid,
                                uint64_t nthreads, T (&acc)[NA]) {
+    // S is kept weighted by eq_lo: S~(k, t) = eq_lo(t) S(k, t).  eq_lo depends
+    // only on the low index t, which folds never touch, so S~ folds like S,
+    // and a S~ = eq_lo a S puts the eq_lo weight into the q products for free.
+    // Warp-steps run k-major (t inner), so the eq_hi(k) weight is applied once
+    // per run of one k.  Products per pair: round 0 two (inv_pair) or five,
+    // round 1 (whose fold reads the unweighted column) nine, later rounds
+    // seven -- against 2 / 6 / 10 / 10 with both weights applied per pair.
+    // The host un-weights the n surviving entries after the last tiled round.
     const int tl = tm.tile_log;
-    const uint64_t K = half >> tl;  // pairs per low index ti (a power of two)
-    const int k_log = 63 - __clzll(K);
-    // warp-steps (a block of 32 consecutive ti, one k) in ti-block-major
-    // order, split into equal contiguous ranges per warp; a warp crosses few
-    // ti blocks, so the eq_lo weight is applied at only a few flushes per
-    // warp.  (Handing out chunks from an atomic counter measured no faster:
-    // the SM is issue-bound, and the second block on an SM finishing after
-    // the first is just the scheduler's order within the same total.)
-    const uint64_t steps = (1ull << (tl - 5)) << k_log;
+    const uint64_t K = half >> tl;  // pairs per low index t (a power of two)
+    const int tib_log = tl - 5;
+    const uint64_t steps = K << tib_log;
     const uint64_t nw = nthreads >> 5, gw = gtid >> 5;
     const uint64_t f0 = steps * gw / nw, f1 = steps * (gw + 1) / nw;
     const int lane = threadIdx.x & 31;
@@ -546,15 +548,16 @@ struct EvLogupTiled {
     const T* Sb = tabs.t[2];
     const T* el = tabs.t[3];
     const bool inv0 = !fold && tm.inv_pair;
-    const bool idx_fold = fold && tm.sidx != nullptr && (half << 2) == tm.sidx_d;
+    const bool first_fold = fold && (half << 2) == tm.tiled_d;  // reads the unweighted S
+    const bool idx_fold = first_fold && tm.sidx != nullptr;
     T p0 = F::zero(), p1 = F::zero(), p2 = F::zero();
     uint64_t cur = ~0ull;
-    auto flush = [&](uint64_t tib) {
-      const T wl = el[(tib << 5) | lane];
+    auto flush = [&](uint64_t kk) {
+      const T wh = eh[kk];
       if (inv0) {
-        acc[2] = F::add(acc[2], F::mul(wl, p2));
+        acc[2] = F::add(acc[2], F::mul(wh, p2));
       } else {
-        F::mul3(wl, p0, wl, p1, wl, p2, p0, p1, p2);
+        F::mul3(wh, p0, wh, p1, wh, p2, p0, p1, p2);
         acc[0] = F::add(acc[0], p0);
         acc[1] = F::add(acc[1], p1);
         acc[2] = F::add(acc[2], p2);
@@ -562,13 +565,14 @@ struct EvLogupTiled {
       p0 = p1 = p2 = F::zero();
     };
     for (uint64_t f = f0; f < f1; f++) {
-      const uint64_t tib = f >> k_log, kk = f & (K - 1);
-      if (tib != cur) {
+      const uint64_t kk = f >> tib_log, tib = f & ((1ull << tib_log) - 1);
+      if (kk != cur) {
         if (cur != ~0ull) flush(cur);
-        cur = tib;
+        cur = kk;
       }
-      const uint64_t i = (kk << tl) | (tib << 5) | lane;
-      T a0, ad, s0, sd;
+      const uint64_t t = (tib << 5) | lane;
+      const uint64_t i = (kk << tl) | t;
+      T a0, ad, s0, s1;
       if (fold) {
         T* At = tabs.t[1];
         T* St = tabs.t[2];
@@ -598,40 +602,49 @@ struct EvLogupTiled {
         a0 = F::add(xa, da);
         const T a1 = F::add(ya, db);
         s0 = F::add(xs, ds);
-        const T s1 = F::add(ys, dt);
+        s1 = F::add(ys, dt);
+        if (first_fold) {  // weight the folded S by eq_lo(t) from here on
+          const T wl = el[t];
+          F::mul2(wl, s0, wl, s1, s0, s1);
+        }
         At[i] = a0;
         At[i + half] = a1;
         St[i] = s0;
         St[i + half] = s1;
         ad = F::sub(a1, a0);
-        sd = F::sub(s1, s0);
-      } else if (tm.sidx) {
-        const uint32_t j0 = __ldg(tm.sidx + i), j1 = __ldg(tm.sidx + i + half);
-        a0 = tm.side_a[j0];
-        ad = F::sub(tm.side_a[j1], a0);
-        s0 = tm.side_s[j0];
-        sd = F::sub(tm.side_s[j1], s0);
       } else {
-        a0 = ld_cg(A + i);
-        ad = F::sub(ld_cg(A + i + half), a0);
-        s0 = ld_cg(Sb + i);
-        sd = F::sub(ld_cg(Sb + i + half), s0);
+        T ah, sh;
+        if (tm.sidx) {
+          const uint32_t j0 = __ldg(tm.sidx + i), j1 = __ldg(tm.sidx + i + half);
+          a0 = tm.side_a[j0];
+          ah = tm.side_a[j1];
+          s0 = tm.side_s[j0];
+          sh = tm.side_s[j1];
+        } else {
+          a0 = ld_cg(A + i);
+          ah = ld_cg(A + i + half);
+          s0 = ld_cg(Sb + i);
+          sh = ld_cg(Sb + i + half);
+        }
+        ad = F::sub(ah, a0);
+        const T wl = el[t];
+        if (inv0) {  // a S = 1 at both ends: only the slope product is needed
+          acc[3] = F::add(acc[3], a0);
+          acc[4] = F::add(acc[4], ad);
+          const T sd = F::mul(wl, F::sub(sh, s0));
+          p2 = F::add(p2, F::mul(ad, sd));
+          continue;
+        }
+        F::mul2(wl, s0, wl, sh, s0, s1);
       }
       acc[3] = F::add(acc[3], a0);
       acc[4] = F::add(acc[4], ad);
-      const T w = eh[kk];
-      if (inv0) {
-        T q2 = F::mul(ad, sd);
-        p2 = F::add(p2, F::mul(w, q2));
-      } else {
-        const T a1 = F::add(a0, ad), s1 = F::add(s0, sd);
-        T q0, q1, q2;
-        F::mul3(a0, s0, a1, s1, ad, sd, q0, q1, q2);
-        F::mul3(w, q0, w, q1, w, q2, q0, q1, q2);
-        p0 = F::add(p0, q0);
-        p1 = F::add(p1, q1);
-        p2 = F::add(p2, q2);
-      }
+      const T a1 = F::add(a0, ad);
+      T q0, q1, q2;
+      F::mul3(a0, s0, a1, s1, ad, F::sub(s1, s0), q0, q1, q2);
+      p0 = F::add(p0, q0);
+      p1 = F::add(p1, q1);
+      p2 = F::add(p2, q2);
     }
     if (cur != ~0ull) flush(cur);
   }
@@ -1853,6 +1866,15 @@ int op_logup_tiled(void* const* tables, int tile_log, int num_vars, int rounds,
     return kErrUnsupported;
   }
   const uint64_t ntile = 1ull << tile_log;
+  // the eq_lo-weighted S column needs eq_lo(t) != 0: no tile coordinate of u
+  // may be 0 or 1 (a challenge equal to either has probability ~2^-254; the
+  // caller then takes the materialised path)
+  for (int j = rounds; j < num_vars; j++) {
+    if (H::is_zero(u[j]) || H::is_zero(H::sub(u[j], H::one()))) {
+      set_error("logup_tiled: eq point coordinate 0 or 1 on the tile variables");
+      return kErrUnsupported;
+    }
+  }
   // eq_hi for every round: round j uses eq(u_{j+1..rounds-1}, k) over
   // 2^(rounds-1-j) entries at offset 2^(rounds-1-j) - 1 (MSB-first, like
   // mle.eq_table); built on the host (2^rounds - 1 entries)
@@ -1872,11 +1894,12 @@ int op_logup_tiled(void* const* tables, int tile_log, int num_vars, int rounds,
   }
   // the work arena, not scratch: run_phase keeps its block partials in scratch
   void* ws;
-  int rc = work_reserve(nhi * sizeof(T) + ntile * sizeof(T) + 2 * sizeof(T), &ws, s);
+  int rc = work_reserve(nhi * sizeof(T) + 2 * ntile * sizeof(T) + 2 * sizeof(T), &ws, s);
   if (rc) return rc;
   T* d_hi = (T*)ws;
   T* d_bt = d_hi + nhi;
   T* d_dot = d_bt + ntile;
+  T* d_inv_lo = d_dot + 2;  // 1 / eq_lo, for un-weighting S after the phase
   ZKL_CUDA(cudaMemcpyAsync(d_hi, hi.data(), nhi * sizeof(T), cudaMemcpyHostToDevice, s));
   // eq_lo = eq(u_rounds.., ti) into the E_out buffer; table-side constants
   T* eq_lo = (T*)tables[0];
@@ -1894,6 +1917,7 @@ int op_logup_tiled(void* const* tables, int tile_log, int num_vars, int rounds,
   for (int t = 0; t < 5; t++) tm.coef[t] = coefs[t];
   tm.tile_log = tile_log;
   tm.inv_pair = (flags & 1) ? 1 : 0;
+  tm.tiled_d = 1ull << num_vars;
   if (flags & 2) {  // indexed: tables[6] = query -> table index, A / S written from round 1
     tm.sidx = (const uint32_t*)tables[6];
     tm.side_a = (const T*)tables[3];
@@ -1920,6 +1944,14 @@ int op_logup_tiled(void* const* tables, int tile_log, int num_vars, int rounds,
   const uint64_t half = 1ull << (num_vars - rounds);
   for (int j = 1; j < 3; j++)
     if ((rc = op_fold<F>(tables[j], tables[j], half, r, s))) return rc;
+  // S was carried weighted by eq_lo (EvLogupTiled) from the first fold on (so
+  // only when the phase folded at all): divide the n survivors by it (eq_lo
+  // has no zero entry: checked before the phase)
+  if (rounds >= 2) {
+    int64_t z = -1;
+    if ((rc = op_batch_inverse<F>(d_inv_lo, eq_lo, ntile, H::zero(), false, &z, s))) return rc;
+    if ((rc = op_mul<F>(tables[2], tables[2], d_inv_lo, ntile, s))) return rc;
+  }
   // E at the bound point: C * eq_lo with C = prod_j ((1 - u_j) + r_j (2 u_j - 1))
   T c = H::one();
   for (int j = 0; j < rounds; j++) {
