@@ -15,6 +15,11 @@ reference's replicated-claim form (gadgets.py:241-251), bit-identical.
 metric: field-elem/s = sum over claims of k * 2^n (k = 4 tables,
 n = d0+d1+d2, the reference claim's size) / step time.
 
+The same JSON line also carries cfg3 (2^25-query SiLU pair lookup), cfg4 (one
+LLaMA-2-7B LoRA block proof: lora_block_proof_s), cfg5 (the dense zkMat sweep
+to 4 x 2^30 entries and one LLaMA-2-13B block) and the HBM-bound passes
+(hbm_kernels); --no-cfg3 / --no-cfg4 / --no-cfg5 skip them.
+
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 """
 
