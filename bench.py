@@ -297,6 +297,15 @@ def run_cfg3(steps, warmup, N):
     N.prof_collect(N.PROF_MATVEC)
     N.prof_collect(N.PROF_EQ)
     elems = 7 * (1 << logd)  # k tables x 2^n of the reference's Eq.-7 claim
+    # Montgomery products of the sumcheck: tiled rounds
+    # 2 / 9 / 7 per pair (round 0 / round 1 / later), eq_hi once per k run;
+    # the 16 tail rounds over 7 tables of 2^16: 20 evaluation + 14 fold
+    # products per pair
+    tile, r1 = 16, logd - 16
+    prods = 2 * (1 << (logd - 1)) + 9 * (1 << (logd - 2))
+    prods += sum(7 * (1 << (logd - 1 - j)) for j in range(2, r1))
+    prods += sum(34 * (1 << (tile - 1 - j)) for j in range(tile))
+    sc_s = ph_ms / steps / 1000.0
     return {
         "workload": CFG3, "field_elems_per_proof": elems, "rounds": len(pr.sumcheck.rounds),
         "ms_per_proof": ms, "field_elems_per_s": elems / (ms / 1000.0),
@@ -308,7 +317,14 @@ def run_cfg3(steps, warmup, N):
             "unit": "GB/s", "note": "algorithmic bytes: 3 k 2^n 32 per phase (k = 2 full-size "
                                     "tables A, S+beta in the tiled phase -- E is factored through "
                                     "the eq point --, 7 x 2^16 after); IMAD-bound: 2 (round 0) / "
-                                    "10 (tiled) / 34 Montgomery products per pair"},
+                                    "9 (round 1) / 7 (tiled) / 34 (tail) Montgomery products per "
+                                    "pair, see sumcheck_mont_roofline"},
+        "sumcheck_mont_roofline": {
+            "bound": "imad (Montgomery products)", "products_per_proof": prods,
+            "achieved_products_per_s": prods / sc_s if sc_s else 0.0,
+            "peak_products_per_s": 4.2e10,
+            "peak_source": "tools/mont_bench.cu on this B200 (profiles/r01 v25 ncu: ALU pipe 66%)",
+            "frac": (prods / sc_s / 4.2e10) if sc_s else 0.0},
     }
 
 
