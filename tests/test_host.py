@@ -299,3 +299,62 @@ def test_softmax_row_witness_restatement_matches_reference():
         assert w[0] == c["xi_prime"] and w[1] == c["digits"] and w[2] == c["partials"]
         assert [[list(a), list(b), list(r)] for a, b, r in w[3]] == c["chain"]
         assert list(w[4]) == c["p"]
+
+
+def test_block_schedule_census_on_cpu():
+    """paper_2508_21393_b200.block.prove_block drives the gadget schedule and
+    the fixed-point witness on any torch device: with a recording stand-in
+    prover on CPU tensors the tiny block's gadget sequence matches the one
+    the reference's own gadgets produced (tests/golden/block.json)."""
+    import torch
+
+    from paper_2508_21393_b200 import block as BK
+    from paper_2508_21393_b200 import tables as T
+
+    g = load_golden("block.json")
+    seq, hidden, heads, hd, ffn, rank, lora = g["shape"]
+    shape = BK.BlockShape("tiny", seq, hidden, heads, hd, ffn, rank, tuple(lora))
+    gm, z, a, en, eps = g["fp"]
+    fp = BK.FixedPoint(gamma_fp=gm, zeta=z, act_bound=a, exp_n=en, eps=eps)
+
+    class Recorder:
+        def __init__(self):
+            self.fp, self.log, self.clipped = fp, [], 0
+            col = lambda ys: torch.tensor(ys, dtype=torch.int32)  # noqa: E731
+            self.luts = {"silu": col(T.silu_entries(gm, a)[1]),
+                         "silu_deriv": col(T.silu_deriv_entries(gm, a)[1]),
+                         "rsqrt": col(T.rsqrt_entries(gm, a, eps)[1]),
+                         "exp": col(T.exp_segment_entries(gm, (en,), 0)[1])}
+
+        def matmul(self, a_, b_, c_):
+            assert torch.equal(BK._mm(a_, b_), c_)  # honest claims
+            self.log.append("matmul")
+
+        def eprod(self, a_, b_, c_):
+            assert torch.equal(a_.long() * b_.long(), c_)
+            self.log.append("elementprod")
+
+        def rescale(self, wide):
+            q, r, clipped = BK._divmod(wide, fp)
+            self.clipped += clipped
+            assert torch.equal(q.long() * fp.zeta + r.long(), wide) or clipped
+            self.log.append("rescale")
+            return q
+
+        def swiglu(self, wide, mode):
+            q, r, clipped = BK._divmod(wide, fp)
+            self.clipped += clipped
+            self.log.append("swiglu")
+            lut = self.luts["silu" if mode == "phi" else "silu_deriv"]
+            return BK._lut(lut, q, fp.qmin).to(torch.int16)
+
+        def rsqrt(self, v, u):
+            self.log.append("rsqrt")
+
+        def exp_lookup(self, v, e):
+            self.log.append("softmax_exp")
+
+    c = g["cases"][0]
+    P = BK.prove_block(BK.BlockWitness(shape, seed=c["seed"], fp=fp, device="cpu"), Recorder())
+    assert P.log == [x[0] for x in c["log"]]
+    assert P.clipped == c["clipped"]
