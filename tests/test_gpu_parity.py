@@ -749,3 +749,22 @@ def test_lookup_vs_oracle(field, d, n):
     assert proof.secret_values == out["secret_values"]
     assert proof.table_values == out["table_values"]
     assert t1.state == t2.state
+
+
+def test_cfg2_xw_full_size_matches_oracle():
+    """BASELINE cfg2's largest claim, Y1 = X.W at LLaMA-2-7B shape (11,12,12:
+    the reference's replicated form would be 4 x 2^35 entries), proven on the
+    GPU and by the oracle's factored restatement (validated bit-exact against
+    the reference on small shapes): identical rounds, finals, end state."""
+    import bench
+
+    name, a, b, c, dims = bench.cfg2_claims(1234, "cuda")[0]
+    assert dims == (11, 12, 12)
+    tr1 = zb.Transcript(b"check", P_BIG, b"x")
+    r1 = zb.matmul_sumcheck(DeviceMatrix.from_int_tensor(a), DeviceMatrix.from_int_tensor(b),
+                            DeviceMatrix.from_int_tensor(c), dims, tr1)
+    tr2 = fs.FS(b"check", P_BIG, b"x")
+    r2 = zkmat.prove_factored(a.cpu().numpy().astype(np.int64).reshape(-1),
+                              b.cpu().numpy().astype(np.int64).reshape(-1),
+                              c.cpu().numpy().reshape(-1), dims, tr2)
+    assert r1[0] == r2[0] and tuple(r1[2]) == r2[1] and tr1.state == tr2.state
