@@ -219,20 +219,26 @@ class BlockProver:
     def rescale(self, wide):
         q, r, clipped = _divmod(wide, self.fp)
         self.clipped += clipped
+        self.rescale_w(wide, q, r)
+        return q
+
+    def rescale_w(self, wide, q, r):
         pr = self._run("rescale", prove_rescale, self.pt(wide), self.pt(q), self.pt(r),
                        self.fp.zeta, self.tables, self.key, self.tr, self._Rng())
         self._lookups("rescale", (pr.quant_lookup, pr.resid_lookup))
-        return q
 
     def swiglu(self, wide, mode):
         q, r, clipped = _divmod(wide, self.fp)
         self.clipped += clipped
         table = self.luts["silu" if mode == "phi" else "silu_deriv"]
         out = _lut(table, q, self.fp.qmin).to(torch.int16)
+        self.swiglu_w(wide, out, q, r, mode)
+        return out
+
+    def swiglu_w(self, wide, out, q, r, mode):
         pr = self._run("swiglu", prove_swiglu, self.pt(wide), self.pt(out), self.pt(q),
                        self.pt(r), mode, self.tables, self.key, self.tr, self._Rng())
         self._lookups("swiglu", (pr.activation_lookup, pr.resid_lookup))
-        return out
 
     def rsqrt(self, v, u):
         pr = self._run("rsqrt", prove_rsqrt, self.pt(v), self.pt(u), self.tables, self.key,
@@ -243,6 +249,55 @@ class BlockProver:
         pr = self._run("softmax_exp", prove_pair_lookup, b"softmax/exp0", self.pt(v),
                        self.pt(e), self.tables.exp_segments[0], self.key, self.tr, self._Rng())
         self._lookups("softmax_exp", (pr,))
+
+
+class WitnessRecorder:
+    """The witness pass of a block: runs prove_block's schedule computing every
+    gadget's witness (narrowed quotients, residues, table outputs) and records
+    the gadget calls with their operands, proving nothing.  The reference's
+    gadget provers take their witnesses as inputs (prove_rescale(wide, narrow,
+    resid, ...), prove_swiglu(wide, out, narrow, resid, ...)), so
+    replay(BlockProver) proves exactly what the interleaved schedule proves,
+    with the witness computed before the timed region."""
+
+    def __init__(self, tables):
+        self.fp = tables.params
+        self.luts = block_luts(tables)
+        self.calls = []
+        self.clipped = 0
+
+    def matmul(self, a, b, c):
+        self.calls.append(("matmul", a, b, c))
+
+    def eprod(self, a, b, c):
+        self.calls.append(("eprod", a, b, c))
+
+    def rescale(self, wide):
+        q, r, clipped = _divmod(wide, self.fp)
+        self.clipped += clipped
+        self.calls.append(("rescale_w", wide, q, r))
+        return q
+
+    def swiglu(self, wide, mode):
+        q, r, clipped = _divmod(wide, self.fp)
+        self.clipped += clipped
+        table = self.luts["silu" if mode == "phi" else "silu_deriv"]
+        out = _lut(table, q, self.fp.qmin).to(torch.int16)
+        self.calls.append(("swiglu_w", wide, out, q, r, mode))
+        return out
+
+    def rsqrt(self, v, u):
+        self.calls.append(("rsqrt", v, u))
+
+    def exp_lookup(self, v, e):
+        self.calls.append(("exp_lookup", v, e))
+
+    def replay(self, P):
+        """Prove the recorded gadgets in order through P (a BlockProver)."""
+        for name, *args in self.calls:
+            getattr(P, name)(*args)
+        P.clipped = self.clipped
+        return P
 
 
 # ---------------------------------------------------------------------------

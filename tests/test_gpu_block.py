@@ -38,3 +38,20 @@ def test_tiny_block_matches_reference_gadgets(field):
     assert tr.state.hex() == c["state_end"]
     s = BK.summary(P)
     assert s["total"]["count"] == len(c["log"])
+
+
+@pytest.mark.parametrize("field", ["big"])
+def test_tiny_block_witness_pass_then_replay_matches(field):
+    """WitnessRecorder + replay proves exactly what the interleaved schedule
+    proves (same gadget log, same end transcript state as the reference)."""
+    g = load_golden("block.json")
+    shape, fp = _tiny(g)
+    c = [c for c in g["cases"] if c["field"] == field][0]
+    p = FIELDS[field]
+    tables = BK.block_tables(D.spec_for(p), fp)
+    w = BK.BlockWitness(shape, seed=c["seed"], fp=fp, device="cuda")
+    rec = BK.prove_block(w, BK.WitnessRecorder(tables))
+    tr = Transcript(b"zkl/golden/block", p, field.encode())
+    P = rec.replay(BK.BlockProver(tr, tables))
+    assert P.log == c["log"] and P.clipped == c["clipped"]
+    assert tr.state.hex() == c["state_end"]
