@@ -138,6 +138,7 @@ struct Scratch {
   size_t work_bytes = 0;
 };
 Scratch& scratch_for_current_device();
+cudaStream_t side_stream();  // per-device non-blocking stream with its own scratch arena
 int scratch_reserve(size_t bytes, void** out, cudaStream_t s);
 int pinned_reserve(size_t bytes, void** out);
 // driver work arena (stream-ordered; grows by sync + realloc)

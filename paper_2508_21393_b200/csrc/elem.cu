@@ -35,8 +35,30 @@ Scratch& scratch_for_current_device() {
   cudaGetDevice(&dev);
   return arenas()[dev];
 }
+// A per-device side stream for independent work inside one call (the zkMat
+// driver's concurrent matrix-vector products); work on it takes its own
+// scratch arena, so it never aliases the main stream's.
+static std::map<int, cudaStream_t>& side_streams() {
+  static std::map<int, cudaStream_t> m;
+  return m;
+}
+static std::map<int, Scratch>& side_arenas() {
+  static std::map<int, Scratch> m;
+  return m;
+}
+cudaStream_t side_stream() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaStream_t& st = side_streams()[dev];
+  if (!st) cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  return st;
+}
 int scratch_reserve(size_t bytes, void** out, cudaStream_t s) {
-  Scratch& a = scratch_for_current_device();
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto it = side_streams().find(dev);
+  const bool side = s != nullptr && it != side_streams().end() && it->second == s;
+  Scratch& a = side ? side_arenas()[dev] : scratch_for_current_device();
   if (bytes > a.bytes) {
     if (a.ptr) {
       ZKL_CUDA(cudaStreamSynchronize(s));

@@ -125,8 +125,8 @@ int op_matmul_prove(int ta, const void* A, int tb, const void* B, int tc, const 
   }
 
   // device vectors
-  const uint64_t sizes[] = {D2, D1, D0, D0, D0, D1, D2, D1, D2, 1};
-  enum { EV, BV, HV, EU, ERU, AV, CU, ERW, BW, KAP, NBUF };
+  const uint64_t sizes[] = {D2, D1, D0, D0, D0, D1, D2, D1, D2, 1, D0};
+  enum { EV, BV, HV, EU, ERU, AV, CU, ERW, BW, KAP, CV, NBUF };
   uint64_t off[NBUF + 1];
   off[0] = 0;
   for (int i = 0; i < NBUF; i++) off[i + 1] = off[i] + ((sizes[i] + 3) & ~3ull);
@@ -138,18 +138,41 @@ int op_matmul_prove(int ta, const void* A, int tb, const void* B, int tc, const 
   auto buf = [&](int i) { return base + off[i]; };
   // profiler brackets (no-ops unless zkl_prof_enable)
   auto esz = [](int t) { return t == 1 ? 2.0 : t == 2 ? 4.0 : t == 3 ? 8.0 : (double)sizeof(T); };
-  auto mv = [&](int t, const void* M, uint64_t r_, uint64_t c_, int tr, const T* xin, T* yout) {
+  auto mv_on = [&](cudaStream_t st, int t, const void* M, uint64_t r_, uint64_t c_, int tr,
+                   const T* xin, T* yout) {
     const int h = prof_open(kProfMatvec, (double)r_ * c_ * esz(t) + (double)(r_ + c_) * sizeof(T),
-                            (double)r_ * c_, s);
-    const int r2 = op_matvec<F>(t, M, r_, c_, tr, xin, yout, s);
-    prof_close(h, s);
+                            (double)r_ * c_, st);
+    const int r2 = op_matvec<F>(t, M, r_, c_, tr, xin, yout, st);
+    prof_close(h, st);
     return r2;
   };
-  auto eq = [&](T* dst, const T* p_, int m) {
-    const int h = prof_open(kProfEq, (double)(1ull << m) * sizeof(T), (double)(1ull << m), s);
-    const int r2 = op_eq_table<F>(dst, p_, m, s);
-    prof_close(h, s);
+  auto mv = [&](int t, const void* M, uint64_t r_, uint64_t c_, int tr, const T* xin, T* yout) {
+    return mv_on(s, t, M, r_, c_, tr, xin, yout);
+  };
+  auto eq_on = [&](cudaStream_t st, T* dst, const T* p_, int m) {
+    const int h = prof_open(kProfEq, (double)(1ull << m) * sizeof(T), (double)(1ull << m), st);
+    const int r2 = op_eq_table<F>(dst, p_, m, st);
+    prof_close(h, st);
     return r2;
+  };
+  auto eq = [&](T* dst, const T* p_, int m) { return eq_on(s, dst, p_, m); };
+  // independent products of a phase's inputs run concurrently on the side
+  // stream (its own scratch arena); fork / join through events
+  const cudaStream_t side = side_stream();
+  static thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  if (!ev_fork) {
+    ZKL_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    ZKL_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  }
+  auto fork = [&]() -> int {
+    ZKL_CUDA(cudaEventRecord(ev_fork, s));
+    ZKL_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+    return kOk;
+  };
+  auto join = [&]() -> int {
+    ZKL_CUDA(cudaEventRecord(ev_join, side));
+    ZKL_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+    return kOk;
   };
   std::vector<T> pt(64);
   auto load_point = [&](const uint8_t* canon, int m) {
@@ -161,11 +184,14 @@ int op_matmul_prove(int ta, const void* A, int tb, const void* B, int tc, const 
   rc = eq(buf(EV), load_point(rv.data(), d2), d2);
   if (rc) return rc;
   gmark(1);
+  // side: cv = C E_v and E_u; main: bv = B E_v, abv = A bv; then h = abv - cv
+  if ((rc = fork())) return rc;
+  if ((rc = mv_on(side, tc, C, D0, D2, 0, buf(EV), buf(CV)))) return rc;  // cv
+  if ((rc = eq_on(side, buf(EU), load_point(ru.data(), d0), d0))) return rc;
   if ((rc = mv(tb, B, D1, D2, 0, buf(EV), buf(BV)))) return rc;
-  if ((rc = mv(tc, C, D0, D2, 0, buf(EV), buf(EU)))) return rc;  // cv
   if ((rc = mv(ta, A, D0, D1, 0, buf(BV), buf(HV)))) return rc;  // abv
-  if ((rc = op_axpy<F>(buf(HV), buf(HV), H::sub(H::zero(), H::one()), buf(EU), D0, s))) return rc;
-  if ((rc = eq(buf(EU), load_point(ru.data(), d0), d0))) return rc;
+  if ((rc = join())) return rc;
+  if ((rc = op_axpy<F>(buf(HV), buf(HV), H::sub(H::zero(), H::one()), buf(CV), D0, s))) return rc;
   mark(1);
   gmark(2);
   uint8_t* rounds = rounds_out;
@@ -204,8 +230,10 @@ int op_matmul_prove(int ta, const void* A, int tb, const void* B, int tc, const 
   if ((rc = eq(buf(ERU), load_point(point, d0), d0))) return rc;
   rounds += (size_t)d0 * 4 * nb;
   point += (size_t)d0 * nb;
+  if ((rc = fork())) return rc;
+  if ((rc = mv_on(side, tc, C, D0, D2, 1, buf(ERU), buf(CU)))) return rc;  // cu (side)
   if ((rc = mv(ta, A, D0, D1, 1, buf(ERU), buf(AV)))) return rc;
-  if ((rc = mv(tc, C, D0, D2, 1, buf(ERU), buf(CU)))) return rc;
+  if ((rc = join())) return rc;
   if ((rc = op_dot<F>(buf(KAP), buf(CU), buf(EV), D2, s))) return rc;
   static thread_local T* kap_host = nullptr;
   static thread_local cudaEvent_t kap_ev = nullptr;
