@@ -700,8 +700,11 @@ def main():
                      "gpu_ms_per_step": mv_ms / args.steps,
                      "share_of_step": (mv_ms / args.steps) / ms_per_step,
                      "int_x_fr_macs_per_s": mac_rate,
-                     "note": "IMAD-bound, not HBM-bound: ~20 integer-pipe instructions per int16 "
-                             "x 256-bit MAC; IMAD peak 18.4 T/s measured (profiles/r01)",
+                     "note": "int16 products on tensor cores (k_mvt_rows / k_mvt_cols, byte-sliced "
+                             "mma.sync), int64 on IMAD carry chains; since v37 the zkMat driver "
+                             "runs independent products concurrently on a side stream, so "
+                             "per-launch durations overlap and understate each kernel's rate "
+                             "(kernel-alone times: profiles/r01 ncu summaries)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
         "round_engine": {"kernel": "k_sumcheck_cluster / k_sumcheck_persistent (persistent, "
                                    "one launch per sumcheck phase)",
