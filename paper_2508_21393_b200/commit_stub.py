@@ -54,9 +54,9 @@ def combine_commitments(group, commitments, coefficients):
 def open_batch(key, tables, blindings, point, tr, rng, values=None):
     """Stub opening; ``values`` may carry already-known evaluations."""
     if values is None:
-        from .mle import mle_evaluate_any
+        from .mle import mle_evaluate_many
 
-        values = [mle_evaluate_any(t, point, tr.modulus) for t in tables]
+        values = mle_evaluate_many(tables, point, tr.modulus)
     _append_all(tr, b"open/point", point)
     _append_all(tr, b"open/value", values)
     return list(values), None

@@ -74,6 +74,30 @@ def mle_evaluate_matrix(M, point, spec):
     return D.dot(D.eq_table(point[:rv], spec), y, spec, M.rows)
 
 
+def mle_evaluate_many(tables, point, modulus):
+    """mle_evaluate_any for several tables at one point (an opening batch,
+    commit.py:192-195): integer matrices of one shape share the two eq
+    tables."""
+    spec = D.spec_for(modulus)
+    point = list(point)
+    out, shared = [], {}
+    for t in tables:
+        if getattr(t, "mtype", N.MT_FIELD) != N.MT_FIELD:
+            rv = (t.rows - 1).bit_length()
+            if rv + (t.cols - 1).bit_length() != len(point):
+                raise DimensionMismatch("point has %d coordinates, matrix has %d variables"
+                                        % (len(point), rv + (t.cols - 1).bit_length()))
+            if rv not in shared:
+                shared[rv] = (D.eq_table(point[rv:], spec), D.eq_table(point[:rv], spec))
+            ec, er = shared[rv]
+            from .gadgets import _matvec
+
+            out.append(D.dot(er, _matvec(t, ec, False, spec), spec, t.rows))
+        else:
+            out.append(mle_evaluate_any(t, point, modulus))
+    return out
+
+
 def mle_evaluate_any(table, point, modulus):
     """Python list or DeviceMatrix / device vector."""
     spec = D.spec_for(modulus)
