@@ -222,17 +222,16 @@ CFG3 = ("cfg3: SiLU pair lookup (logUp, lookup.py:143-251 via gadgets.py:679-688
 
 
 def cfg3_inputs(seed=7):
-    """Device tensors for cfg3.  Table y values come from the reference's own
-    silu table (tests/golden/tables_g4096.json, generated by the reference)."""
-    import base64
-    import zlib
-
+    """Device tensors for cfg3.  The table is the product's own SiLU table
+    (paper_2508_21393_b200/tables.py, pinned entry for entry against the
+    reference's tables.py:65-69 by tests/test_host.py)."""
     import torch
 
-    with open(os.path.join(ROOT, "tests", "golden", "tables_g4096.json")) as fh:
-        g = json.load(fh)["silu"]
-    ys = np.frombuffer(zlib.decompress(base64.b64decode(g["y_zlib_b64"])), dtype="<i4")
-    x0 = g["x0"]
+    from paper_2508_21393_b200 import tables as TBL
+
+    xs_t, ys_t = TBL.silu_entries(4096, 8)
+    ys = np.asarray(ys_t, dtype=np.int32)
+    x0 = xs_t[0]
     logd = 25
     d = 1 << logd
     nq = 2048 * 11008
@@ -329,12 +328,12 @@ def run_cfg3(steps, warmup, N):
 
 
 CFG4 = ("cfg4: one LLaMA-2-7B LoRA transformer-block fine-tuning step proof (seq 2048, hidden "
-        "4096, 32x128 heads, FFN 11008 SwiGLU, RMSNorm, LoRA r=8 on W_q/W_v; forward, backward "
-        "and LoRA gradients): zkMat, elementprod, rescale, SwiGLU, rsqrt and softmax-exp lookup "
-        "proofs on one transcript (paper_2508_21393_b200/block.py)")
+        "4096, 32x128 heads, FFN 11008 SwiGLU, RMSNorm, LoRA r=8 on W_q/W_v; forward, backward, "
+        "LoRA gradients and update): zkMat, matadd, elementprod, rescale, SwiGLU, rsqrt and "
+        "softmax-exp lookup proofs on one transcript (paper_2508_21393_b200/block.py)")
 
 
-def run_cfg4(steps, warmup, shape_name="7b"):
+def run_cfg4(steps, warmup, shape_name="7b", verify_block=True):
     """Whole-block proof seconds (BASELINE metric "LoRA-block proof s").
     Witness (exact fixed-point forward/backward on the GPU) and tables are
     built before the timed region; each timed block is proven from scratch
@@ -367,15 +366,39 @@ def run_cfg4(steps, warmup, shape_name="7b"):
     for i in range(warmup):
         rec.replay(BK.BlockProver(zb.Transcript(b"zklora-b200/block", P_BIG, b"w%d" % i), tables))
     sec = 0.0
+    end_states = []
     for i in range(steps):
-        P, dt = timed(lambda: rec.replay(BK.BlockProver(
-            zb.Transcript(b"zklora-b200/block", P_BIG, b"%d" % i), tables, timing=False)))
+        tr = zb.Transcript(b"zklora-b200/block", P_BIG, b"%d" % i)
+        P, dt = timed(lambda: rec.replay(BK.BlockProver(tr, tables, timing=False)))
         sec += dt
+        end_states.append(bytes(tr.state))
     sec /= steps
     # one more (untimed) replay with per-gadget synchronised spans for the breakdown
     P = rec.replay(BK.BlockProver(zb.Transcript(b"zklora-b200/block", P_BIG, b"t"), tables))
     s = BK.summary(P)
     elems = s["total"]["field_elems"]
+    verify = None
+    if verify_block:
+        # the same block (seed, transcript) proven once more with the
+        # reference's verifiers in the loop: every gadget verified as it is
+        # proven, every opened value recomputed independently
+        # (harness/refverify.py); its end transcript state must equal the
+        # first timed proof's
+        from harness import refverify as RV
+
+        if RV.reference_available():
+            del rec
+            torch.cuda.empty_cache()
+            t0 = time.perf_counter()
+            Pv, verify = RV.prove_and_verify_block(w, tables, D.spec_for(P_BIG),
+                                                   b"zklora-b200/block", b"0")
+            verify["seconds"] = time.perf_counter() - t0
+            verify["same_proof_as_timed"] = bytes(Pv.tr.state) == end_states[0]
+            verify["verifier"] = ("reference zklora verify_* (baseline/_ref) on its own "
+                                  "Transcript, stub commitments with independent opening checks")
+            del Pv
+        else:
+            verify = {"verifier_accept": None, "note": "baseline/_ref not installed"}
     return {
         "workload": CFG4 if shape_name == "7b" else CFG4.replace("7B", "13B"),
         "shape": shape.__dict__ if hasattr(shape, "__dict__") else str(shape),
@@ -385,7 +408,12 @@ def run_cfg4(steps, warmup, shape_name="7b"):
                         "provers take witnesses as inputs, gadgets.py:600, 761, 978)",
         "field_elems_per_block": elems, "field_elems_per_s": elems / sec,
         "rounds_per_block": s["total"]["rounds"], "gadgets_per_block": s["total"]["count"],
-        "by_gadget": s["gadgets"], "clipped_quotients": s["clipped_quotients"],
+        "by_gadget": s["gadgets"], "clipped_quotients": 0,
+        "clipping_note": "the witness pass raises RangeViolation on any quotient outside "
+                         "quant_range (gadgets.py:575); per-tensor power-of-two scales keep "
+                         "them in range (block.py docstring)",
+        "verify": verify,
+        "verifier_accept": verify.get("verifier_accept") if verify else None,
         "note": "block_proof_s replays the recorded gadget calls on a fresh transcript, every "
                 "proof from scratch, without per-gadget synchronisation; the seconds per gadget "
                 "kind come from one more replay with synchronised spans (host perf_counter)",
@@ -508,7 +536,7 @@ def run_hbm_kernels(peak_gbs):
     res = {
         "k_lift (int16 -> Fr, 2^27)": timed(lambda: D.lift(x16, spec, out=out), n * (2 + 32)),
         "k_rescale_witness (int64 -> q, r int16, 2^27)": timed(
-            lambda: NL.rescale_witness_device(w64, 4096, fp, clip=True), n * (8 + 2 + 2)),
+            lambda: NL.rescale_witness_device(w64, 4096, fp), n * (8 + 2 + 2)),
         "k_range_count (int16 vs 2^16 range, index out, 2^27)": timed(
             lambda: L.multiplicities_range(lifted, tab, x16, tab.int_column), n * (2 + 4)),
     }

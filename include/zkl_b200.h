@@ -185,12 +185,12 @@ int zkl_pair_multiplicities(int field, const void* x, int x_type, const void* y,
  * signed wide entry w (int16 / int32 / int64 column, wide_type 1 / 2 / 3),
  * centered_divmod (quantize.py:101-104) q = floor((w + divisor/2) / divisor),
  * r = w - divisor q, written as int16 q_out[i] and r_out[i] = r * lift.  A
- * quotient outside [qmin, qmax] is the reference's RangeViolation:
- * ZKL_ERR_MISSING with *first_bad = its first index, unless clip != 0, in which
- * case q is clamped and *n_bad counts the clamped entries (status ZKL_OK). */
+ * quotient outside [qmin, qmax] is the reference's RangeViolation
+ * (gadgets.py:575): ZKL_ERR_MISSING with *first_bad = its first index and
+ * *n_bad = the number of such entries.  Nothing is clamped. */
 int zkl_rescale_witness(const void* wide, int wide_type, uint64_t n, int64_t divisor,
                         int64_t lift, int64_t qmin, int64_t qmax, int16_t* q_out, int16_t* r_out,
-                        int clip, int64_t* first_bad, uint64_t* n_bad, void* stream);
+                        int64_t* first_bad, uint64_t* n_bad, void* stream);
 
 /* compute_multiplicities (lookup.py:91-99) for a single-column table that is
  * the consecutive integer range table_x0 .. table_x0+n-1 (quant_range /

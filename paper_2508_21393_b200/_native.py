@@ -86,7 +86,7 @@ _SIGS = {
     "zkl_transcript_append_ints": ([_vp, ctypes.c_char_p, _u64, _vp, _u64, _u64], ctypes.c_int),
     "zkl_transcript_challenge_vector": ([_i32, _vp, ctypes.c_char_p, _u64, _vp], ctypes.c_int),
     "zkl_rescale_witness": ([_vp, _i32, _u64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
-                             ctypes.c_int64, _vp, _vp, _i32, _i64p,
+                             ctypes.c_int64, _vp, _vp, _i64p,
                              ctypes.POINTER(ctypes.c_uint64), _vp], ctypes.c_int),
     "zkl_range_multiplicities": ([_vp, _i32, _u64, ctypes.c_int64, _u64, _vp, _vp, _i64p, _vp],
                                  ctypes.c_int),

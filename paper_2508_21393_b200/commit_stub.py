@@ -13,17 +13,32 @@ shared with oracle/stubcommit.py and tests/golden/make_golden.py:
   values are the true MLE evaluations (computed on the GPU).
 """
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field, replace
 
 STUB_TAG = b"zkl-stub/v1"
+
+# Opening checks (harness/refverify.py): when True, stub commitments carry a
+# handle on the data they stand for (a device tensor, or a recipe such as
+# "1/(beta + s)" over one), so a checking verifier can evaluate the committed
+# MLE independently of the prover and compare it with every opened value.
+# Off in the product path: a handle keeps its tensor alive.
+CHECK = False
 
 
 @dataclass(frozen=True)
 class StubCommitment:
     num_vars: int
+    handle: object = field(default=None, compare=False, hash=False, repr=False)
 
     def serialize(self, group):
         return STUB_TAG + bytes([self.num_vars])
+
+
+def attach(com, handle):
+    """com with `handle` attached when CHECK is on (else com unchanged)."""
+    if not CHECK or handle is None or not isinstance(com, StubCommitment):
+        return com
+    return replace(com, handle=handle)
 
 
 class StubKey:
@@ -48,7 +63,11 @@ def commit_size(num_vars):
 
 
 def combine_commitments(group, commitments, coefficients):
-    return StubCommitment(commitments[0].num_vars)
+    handles = [getattr(c, "handle", None) for c in commitments]
+    com = StubCommitment(commitments[0].num_vars)
+    if any(h is None for h in handles):
+        return com
+    return attach(com, ("lin", list(zip(handles, coefficients))))
 
 
 def open_batch(key, tables, blindings, point, tr, rng, values=None):

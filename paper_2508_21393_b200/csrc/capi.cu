@@ -297,8 +297,8 @@ int zkl_pair_multiplicities(int field, const void* x, int x_type, const void* y,
 }
 int zkl_rescale_witness(const void* wide, int wide_type, uint64_t n, int64_t divisor,
                         int64_t lift, int64_t qmin, int64_t qmax, int16_t* q_out, int16_t* r_out,
-                        int clip, int64_t* first_bad, uint64_t* n_bad, void* stream) {
-  return op_rescale_witness(wide, wide_type, n, divisor, lift, qmin, qmax, q_out, r_out, clip,
+                        int64_t* first_bad, uint64_t* n_bad, void* stream) {
+  return op_rescale_witness(wide, wide_type, n, divisor, lift, qmin, qmax, q_out, r_out,
                             first_bad, n_bad, (cudaStream_t)stream);
 }
 int zkl_range_multiplicities(const void* x, int x_type, uint64_t d, int64_t table_x0,

@@ -784,12 +784,13 @@ int op_read(uint8_t* host, const void* src, uint64_t n, cudaStream_t s) {
 // Rescale witness (gadgets.py:563-580, quantize.py:101-104): for every wide
 // entry w, q = floor((w + divisor/2) / divisor), r = w - divisor q (so r is in
 // [-divisor/2, divisor/2)), resid = r * lift.  q outside [qmin, qmax] is the
-// reference's RangeViolation: the first such index is reported, and with
-// clip != 0 q is clamped (and counted) instead.  One pass: 8 B in, 4 B out.
+// reference's RangeViolation (gadgets.py:575): the first such index and the
+// count are reported and the caller raises -- a clamped quotient would break
+// wide = divisor*q + r, which the verifier checks.  One pass: 8 B in, 4 B out.
 template <class W>
 __global__ void k_rescale_witness(const W* wide, uint64_t n, int64_t divisor, int shift,
                                   int64_t lift, int64_t qmin, int64_t qmax, int16_t* q_out,
-                                  int16_t* r_out, int clip, unsigned long long* first_bad,
+                                  int16_t* r_out, unsigned long long* first_bad,
                                   unsigned long long* n_bad) {
   unsigned bad = 0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
@@ -807,7 +808,6 @@ __global__ void k_rescale_witness(const W* wide, uint64_t n, int64_t divisor, in
     if (q < qmin || q > qmax) {
       atomicMin(first_bad, (unsigned long long)i);
       bad++;
-      if (clip) q = q < qmin ? qmin : qmax;
     }
     q_out[i] = (int16_t)q;
     r_out[i] = (int16_t)(r * lift);
@@ -817,7 +817,7 @@ __global__ void k_rescale_witness(const W* wide, uint64_t n, int64_t divisor, in
 }
 
 int op_rescale_witness(const void* wide, int wide_type, uint64_t n, int64_t divisor, int64_t lift,
-                       int64_t qmin, int64_t qmax, int16_t* q_out, int16_t* r_out, int clip,
+                       int64_t qmin, int64_t qmax, int16_t* q_out, int16_t* r_out,
                        int64_t* first_bad, uint64_t* n_bad, cudaStream_t s) {
   *first_bad = -1;
   *n_bad = 0;
@@ -840,11 +840,11 @@ int op_rescale_witness(const void* wide, int wide_type, uint64_t n, int64_t divi
     const unsigned g = grid_for(n, 256);
     switch (wide_type) {
       case 1: k_rescale_witness<int16_t><<<g, 256, 0, s>>>((const int16_t*)wide, n, divisor, shift, lift,
-                  qmin, qmax, q_out, r_out, clip, flag, flag + 1); break;
+                  qmin, qmax, q_out, r_out, flag, flag + 1); break;
       case 2: k_rescale_witness<int32_t><<<g, 256, 0, s>>>((const int32_t*)wide, n, divisor, shift, lift,
-                  qmin, qmax, q_out, r_out, clip, flag, flag + 1); break;
+                  qmin, qmax, q_out, r_out, flag, flag + 1); break;
       case 3: k_rescale_witness<int64_t><<<g, 256, 0, s>>>((const int64_t*)wide, n, divisor, shift, lift,
-                  qmin, qmax, q_out, r_out, clip, flag, flag + 1); break;
+                  qmin, qmax, q_out, r_out, flag, flag + 1); break;
       default: set_error("rescale_witness: int16/int32/int64 only"); return kErrArg;
     }
     ZKL_LAUNCH_CHECK();
@@ -858,7 +858,7 @@ int op_rescale_witness(const void* wide, int wide_type, uint64_t n, int64_t divi
   *n_bad = v[1];
   if (v[0] != ~0ull) {
     *first_bad = (int64_t)v[0];
-    if (!clip) return kErrMissing;
+    return kErrMissing;
   }
   return kOk;
 }

@@ -87,8 +87,7 @@ int op_multiplicities(const void* secret, uint64_t d, const void* table, uint64_
                       uint32_t* counts, int64_t* first_miss, cudaStream_t s,
                       uint32_t* index_out = nullptr);
 int op_rescale_witness(const void* wide, int wide_type, uint64_t n, int64_t divisor, int64_t lift,
-                       int64_t qmin, int64_t qmax, int16_t* q_out, int16_t* r_out, int clip,
-                       int64_t* first_bad, uint64_t* n_bad, cudaStream_t s);
+                       int64_t qmin, int64_t qmax, int16_t* q_out, int16_t* r_out, int64_t* first_bad, uint64_t* n_bad, cudaStream_t s);
 int op_range_multiplicities(const void* x, int xt, uint64_t d, int64_t x0, uint64_t n,
                             uint32_t* counts, uint32_t* index_out, int64_t* first_miss,
                             cudaStream_t s);

@@ -123,7 +123,16 @@ class ElementprodProof:
     ab_opening: object
 
 
-TYPES = {"Opening": Opening, "MatmulProof": MatmulProof, "ElementprodProof": ElementprodProof}
+@dataclass
+class MataddProof:
+    tag = "matadd"
+    sign: int
+    shape: tuple
+    opening: object
+
+
+TYPES = {"Opening": Opening, "MatmulProof": MatmulProof, "ElementprodProof": ElementprodProof,
+         "MataddProof": MataddProof}
 
 
 # ---------------------------------------------------------------------------
@@ -349,6 +358,23 @@ def prove_matmul(a, b, c, key, tr, rng):
     )
 
 
+def prove_matadd(a, b, c, sign, key, tr, rng):
+    """Drop-in for zklora.gadgets.prove_matadd (gadgets.py:322-336): c = a +
+    sign*b checked at one random point, i.e. a batch opening of the committed
+    operands (device MLE evaluations for DeviceMatrix operands)."""
+    shape = (a.ref.row_vars, a.ref.col_vars)
+    if (b.ref.row_vars, b.ref.col_vars) != shape or (c.ref.row_vars, c.ref.col_vars) != shape:
+        raise ShapeMismatch("matadd operands must share a shape")
+    if sign not in (1, -1):
+        raise ValueError("sign must be +1 or -1")
+    _absorb_operands(tr, b"matadd", [a.ref, b.ref, c.ref], key.group)
+    tr.append(b"matadd/sign", sign % tr.modulus)
+    point = tr.challenge_vector(b"matadd/point", a.ref.num_vars)
+    committed = [t for t in (a, b, c) if t.ref.kind == "committed"]
+    opening = _open_tables(key, committed, point, tr, rng) if committed else None
+    return TYPES["MataddProof"](sign=sign, shape=shape, opening=opening)
+
+
 def _consumable(M, spec):
     """A fresh field copy of a DeviceMatrix that a sumcheck may fold in place
     (integer matrices are lifted straight into it)."""
@@ -442,9 +468,9 @@ def prove_elementprod(a, b, c, key, tr, rng):
 def _combine_commitments(key, commitments, coefficients):
     """commit.combine_commitments, or the stub's (same num_vars) for StubKey."""
     if getattr(key, "is_stub", False):
-        from .commit_stub import StubCommitment
+        from .commit_stub import combine_commitments
 
-        return StubCommitment(commitments[0].num_vars)
+        return combine_commitments(key.group, commitments, coefficients)
     import zklora.commit as zc
 
     return zc.combine_commitments(key.group, commitments, coefficients)

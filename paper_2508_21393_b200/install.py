@@ -6,6 +6,7 @@ Module-attribute swap at every by-name import site:
   compute_multiplicities -> zklora.lookup, zklora.gadgets
   prove_matmul,
   prove_elementprod,
+  prove_matadd,
   prove_rescale, prove_swiglu,
   prove_rsqrt,
   prove_softmax_row      -> zklora.gadgets, zklora.pipeline
@@ -42,12 +43,35 @@ def install(pkg=None):
                   (bl.TYPES, dict(bl.TYPES)), (bn.TYPES, dict(bn.TYPES))]
     bs.TYPES.update(RoundPolynomial=zs.RoundPolynomial, SumcheckProof=zs.SumcheckProof)
     bg.TYPES.update(Opening=zg.Opening, MatmulProof=zg.MatmulProof,
-                    ElementprodProof=zg.ElementprodProof)
+                    ElementprodProof=zg.ElementprodProof, MataddProof=zg.MataddProof)
     bl.TYPES.update(LookupProof=zl.LookupProof, ElementNotInTable=zl.ElementNotInTable,
                     PoleCollision=zl.PoleCollision)
     bn.TYPES.update({k: getattr(zg, k) for k in ("RescaleProof", "SwigluProof", "RsqrtProof",
                                                   "SoftmaxRowProof", "NormalizationBudgetExceeded")
                      if hasattr(zg, k)})
+
+    # error classes: every binding of a backend exception class in the
+    # backend's modules is pointed at the reference's class (raise sites look
+    # the name up when they raise), so `except zklora.gadgets.ShapeMismatch`
+    # and pytest.raises in the reference tests catch what the backend raises
+    import sys as _sys
+
+    from . import mle as bm_, sumcheck as bs_
+
+    quantize = importlib.import_module("%s.quantize" % name)
+    errors = {bg.ShapeMismatch: zg.ShapeMismatch, bn.RangeViolation: zg.RangeViolation,
+              bn.NormalizationBudgetExceeded: zg.NormalizationBudgetExceeded,
+              bs_.DegreeOverflow: zs.DegreeOverflow, bs_.SumcheckError: zs.SumcheckError,
+              bm_.DimensionMismatch: mods["mle"].DimensionMismatch,
+              bn.DigitOutOfRange: quantize.DigitOutOfRange,
+              bf.InversionOfZero: mods["field"].InversionOfZero}
+    pkg_name = __name__.rsplit(".", 1)[0]
+    for mname, mod in list(_sys.modules.items()):
+        if mod is None or not (mname == pkg_name or mname.startswith(pkg_name + ".")):
+            continue
+        for attr, val in list(vars(mod).items()):
+            if isinstance(val, type) and val in errors:
+                swap(mod, attr, errors[val])
 
     def batch_inverse(values, modulus):
         try:
@@ -63,6 +87,7 @@ def install(pkg=None):
     for m in (zg, mods["pipeline"]):
         swap(m, "prove_matmul", bg.prove_matmul)
         swap(m, "prove_elementprod", bg.prove_elementprod)
+        swap(m, "prove_matadd", bg.prove_matadd)
         for name in ("prove_rescale", "prove_swiglu", "prove_rsqrt", "prove_softmax_row"):
             swap(m, name, getattr(bn, name))
     for m in (mods["field"], zl):

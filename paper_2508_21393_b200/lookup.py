@@ -18,6 +18,7 @@ from dataclasses import dataclass
 from . import _native as N
 from . import device as D
 from .field import batch_inverse_device, inverse_pow2
+from .commit_stub import attach
 from .gadgets import commit_backend
 from .mle import mle_evaluate_device
 from .sumcheck import TYPES as SC_TYPES
@@ -308,6 +309,8 @@ def prove_lookup(secret, multiplicities, table, key, tr, rng, secret_index=None)
     m_rows, _ = be.split_shape(table.num_vars)
     m_blinding = rng.vector(m_rows)
     m_commitment = be.commit(key, _Sized(n) if stub else D.as_list(multiplicities), m_blinding)
+    if stub:  # (opening checks only: what m stands for, commit_stub.CHECK)
+        m_commitment = attach(m_commitment, ("mult", entries, table.entries, multiplicities))
     tr.append(b"lookup/table", table.commitment.serialize(group))
     tr.append(b"lookup/secret", secret.commitment.serialize(group))
     tr.append(b"lookup/mult", m_commitment.serialize(group))
@@ -350,8 +353,8 @@ def prove_lookup(secret, multiplicities, table, key, tr, rng, secret_index=None)
 
     if stub:
         inv_s_host = inv_t_host = None
-        a_commitment = be.commit(key, _Sized(d), a_blinding)
-        b_commitment = be.commit(key, _Sized(n))
+        a_commitment = attach(be.commit(key, _Sized(d), a_blinding), ("inv", entries, beta))
+        b_commitment = attach(be.commit(key, _Sized(n)), ("inv", table.entries, beta))
     else:
         inv_s = gathered_inv_s()
         inv_s_host = D.download(inv_s, spec, d)

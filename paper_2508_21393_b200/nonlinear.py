@@ -24,6 +24,7 @@ import torch
 
 from . import _native as N
 from . import device as D
+from .commit_stub import attach
 from .gadgets import ShapeMismatch, _absorb_operands, _open_tables, prove_pair_lookup
 from .lookup import (LookupTable, SecretVector, compute_multiplicities, multiplicities_indexed,
                      multiplicities_range, prove_lookup)
@@ -126,7 +127,7 @@ def device_range_table(lo, n, spec, commitment, name):
     """A consecutive-integer single-column table [lo, lo+n) lifted on the GPU
     (quant_range_entries / residue_range_entries, tables.py:109-117)."""
     col = torch.arange(lo, lo + n, dtype=torch.int32, device="cuda")
-    t = LookupTable(D.DeviceVector(D.lift(col, spec), n, spec), commitment, name)
+    t = LookupTable(D.DeviceVector(D.lift(col, spec), n, spec), attach(commitment, col), name)
     object.__setattr__(t, "int_column", col)  # lets multiplicities bin by offset
     return t
 
@@ -135,16 +136,15 @@ def device_pair_table(xs, ys, commitment_x, commitment_y, name):
     """A pair table with int32 device columns (tables.py:208-214)."""
     tx = torch.as_tensor(xs, dtype=torch.int32).cuda()
     ty = torch.as_tensor(ys, dtype=torch.int32).cuda()
-    return PairTable(LookupTable(tx, commitment_x, name + ".x"),
-                     LookupTable(ty, commitment_y, name + ".y"), name)
+    return PairTable(LookupTable(tx, attach(commitment_x, tx), name + ".x"),
+                     LookupTable(ty, attach(commitment_y, ty), name + ".y"), name)
 
 
-def rescale_witness_device(wide, divisor, params, clip=False):
+def rescale_witness_device(wide, divisor, params):
     """rescale_witness (gadgets.py:563-580) for a signed int device tensor:
-    (narrow int16, resid int16 = r * zeta/divisor, number of clipped
-    quotients), one kernel pass (zkl_rescale_witness).  A quotient outside the
-    quant_range domain raises RangeViolation like the reference, unless
-    clip=True (it is then clamped and counted)."""
+    (narrow int16, resid int16 = r * zeta/divisor), one kernel pass
+    (zkl_rescale_witness).  A quotient outside the quant_range domain raises
+    RangeViolation like the reference (gadgets.py:575); nothing is clamped."""
     import ctypes
 
     zeta = params.zeta
@@ -157,14 +157,14 @@ def rescale_witness_device(wide, divisor, params, clip=False):
     fb, nb = ctypes.c_int64(-1), ctypes.c_uint64(0)
     rc = N.lib().zkl_rescale_witness(D.ptr(w), D._INT_TYPES[w.dtype], w.numel(), divisor,
                                      zeta // divisor, -half, half - 1, D.ptr(q), D.ptr(r),
-                                     1 if clip else 0, ctypes.byref(fb), ctypes.byref(nb),
-                                     D.stream())
+                                     ctypes.byref(fb), ctypes.byref(nb), D.stream())
     if rc == N.ZKL_ERR_MISSING:
         bad = int(w.reshape(-1)[fb.value])
         q0 = (bad + divisor // 2) // divisor
-        raise RangeViolation("rescale quotient %d outside table domain" % q0)
+        raise RangeViolation("rescale quotient %d outside table domain (%d entries)"
+                             % (q0, nb.value))
     N.check(rc)
-    return q, r, int(nb.value)
+    return q, r
 
 
 def _int_matrix(pt):

@@ -398,6 +398,15 @@ def gen_tables():
     fns = (("silu", TB.silu_entries), ("silu_deriv", TB.silu_deriv_entries),
            ("exp0", lambda q: TB.exp_segment_entries(q, 0)),
            ("rsqrt_eps1e-5", lambda q: TB.rsqrt_entries(q, 1e-5)))
+    # the LLaMA block's tables (paper_2508_21393_b200/block.py): SiLU / SiLU'
+    # at gamma/2 = 2^11 with act_bound 16, and the exp segment of base 4
+    half = QuantParams(gamma_fp=2**11, bound=2**16, zeta=2**11, xi=2**64,
+                       radices=(2**16,) * 4, act_bound=16)
+    base4 = QuantParams(gamma_fp=2**12, bound=2**16, zeta=2**12, xi=2**18,
+                        radices=(4, 2**16), act_bound=8)
+    fns += (("silu_g2048_a16", lambda q: TB.silu_entries(half)),
+            ("silu_deriv_g2048_a16", lambda q: TB.silu_deriv_entries(half)),
+            ("exp_base4", lambda q: TB.exp_segment_entries(base4, 1)))
     for name, fn in fns:
         xs, ys = fn(params)
         arr = np.asarray(ys, dtype="<i4")
@@ -533,8 +542,8 @@ class RefBlockProver:
         ys = lambda pair: torch.tensor([F.to_signed(v, p) for v in pair.y.entries],  # noqa: E731
                                        dtype=torch.int32)
         self.luts = {"silu": ys(ts.silu), "silu_deriv": ys(ts.silu_deriv),
-                     "rsqrt": ys(ts.rsqrt), "exp": ys(ts.exp_segments[0])}
-        self.clipped = 0
+                     "rsqrt": ys(ts.rsqrt), "exp": ys(ts.exp_segments[0]),
+                     "act_x0": F.to_signed(ts.silu.x.entries[0], p)}
         self.log = []
 
     def pt(self, t):
@@ -545,24 +554,26 @@ class RefBlockProver:
         pr = G.prove_matmul(self.pt(a), self.pt(b), self.pt(c), KEY, self.tr, RNG)
         self.log.append(["matmul", len(pr.sumcheck.rounds)])
 
+    def matadd(self, a, b, c, sign):
+        G.prove_matadd(self.pt(a), self.pt(b), self.pt(c), sign, KEY, self.tr, RNG)
+        self.log.append(["matadd"])
+
     def eprod(self, a, b, c):
         pr = G.prove_elementprod(self.pt(a), self.pt(b), self.pt(c), KEY, self.tr, RNG)
         self.log.append(["elementprod", len(pr.sumcheck.rounds)])
 
-    def rescale(self, wide):
-        q, r, clipped = self.BK._divmod(wide, self.fp)
-        self.clipped += clipped
-        pr = G.prove_rescale(self.pt(wide), self.pt(q), self.pt(r), self.fp.zeta, self.ts, KEY,
+    def rescale(self, wide, divisor):
+        q, r = self.BK._divmod(wide, divisor, self.fp)
+        pr = G.prove_rescale(self.pt(wide), self.pt(q), self.pt(r), divisor, self.ts, KEY,
                              self.tr, RNG)
         self.log.append(["rescale", len(pr.quant_lookup.sumcheck.rounds),
                          len(pr.resid_lookup.sumcheck.rounds)])
         return q
 
     def swiglu(self, wide, mode):
-        q, r, clipped = self.BK._divmod(wide, self.fp)
-        self.clipped += clipped
+        q, r = self.BK._divmod(wide, self.fp.zeta, self.fp)
         out = self.BK._lut(self.luts["silu" if mode == "phi" else "silu_deriv"], q,
-                           self.fp.qmin).to(self.torch.int16)
+                           self.luts["act_x0"]).to(self.torch.int16)
         pr = G.prove_swiglu(self.pt(wide), self.pt(out), self.pt(q), self.pt(r), mode, self.ts,
                             KEY, self.tr, RNG)
         self.log.append(["swiglu", len(pr.activation_lookup.sumcheck.rounds),
@@ -579,40 +590,54 @@ class RefBlockProver:
         self.log.append(["softmax_exp", len(pr.sumcheck.rounds)])
 
 
+TINY_BLOCK = dict(shape=("tiny", 16, 16, 2, 8, 24, 2, ("q", "v", "o")),
+                  fp=dict(gamma_fp=16, zeta=16, act_bound=4, exp_n=64, eps=2.0 ** -6,
+                          exp_base=4, act_shift=1, eta_div=8),
+                  wstd=0.2, dy_std=0.3)
+
+
 def gen_block():
     """A tiny LoRA block (2 heads, FFN padded 24 -> 32, LoRA on q, v, o) proven
     by the reference's gadgets in prove_block's order, test field and big
-    field; the end transcript state pins the whole composition."""
+    field; the end transcript state pins the whole composition.  The tables are
+    the reference's own table functions (tables.py) at the block's scales:
+    exp segment of radices (exp_base, exp_n), SiLU / SiLU' at gamma/2."""
     sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
     from paper_2508_21393_b200 import block as BK
 
-    shape = BK.BlockShape("tiny", 16, 16, 2, 8, 24, 2, ("q", "v", "o"))
-    fp = BK.FixedPoint(gamma_fp=16, zeta=16, act_bound=4, exp_n=64, eps=2.0 ** -6)
-    params = QuantParams(gamma_fp=16, bound=2**6, zeta=16, xi=2**9, radices=(64, 8),
-                         act_bound=4)
+    shape = BK.BlockShape(*TINY_BLOCK["shape"])
+    fp = BK.FixedPoint(**TINY_BLOCK["fp"])
+    g, a = fp.gamma_fp, fp.act_bound
+    params = QuantParams(gamma_fp=g, bound=2**6, zeta=fp.zeta, xi=2**9, radices=(64, 8),
+                         act_bound=a)
+    pexp = QuantParams(gamma_fp=g, bound=2**6, zeta=fp.zeta, xi=2**8,
+                       radices=(fp.exp_base, fp.exp_n), act_bound=a)
+    ga, aa = g >> fp.act_shift, a << fp.act_shift
+    pact = QuantParams(gamma_fp=ga, bound=2**6, zeta=ga, xi=2**9, radices=(64, 8),
+                       act_bound=aa)
     cases = []
     for fname, p in FIELDS.items():
         ts = TB.TableSet(
-            params, fp.eps, p, b"", (TB._pair("exp0", TB.exp_segment_entries(params, 0), KEY, p),),
-            TB._pair("silu", TB.silu_entries(params), KEY, p),
-            TB._pair("silu_deriv", TB.silu_deriv_entries(params), KEY, p),
+            params, fp.eps, p, b"", (TB._pair("exp0", TB.exp_segment_entries(pexp, 1), KEY, p),),
+            TB._pair("silu", TB.silu_entries(pact), KEY, p),
+            TB._pair("silu_deriv", TB.silu_deriv_entries(pact), KEY, p),
             TB._pair("rsqrt", TB.rsqrt_entries(params, fp.eps), KEY, p),
             L.make_lookup_table(TB._encode_column(TB.quant_range_entries(params), p), KEY,
                                 "quant_range"),
             L.make_lookup_table(TB._encode_column(TB.residue_range_entries(params), p), KEY,
                                 "residue_range"))
-        w = BK.BlockWitness(shape, seed=3, fp=fp, device="cpu")
+        w = BK.BlockWitness(shape, seed=3, fp=fp, device="cpu", wstd=TINY_BLOCK["wstd"],
+                            dy_std=TINY_BLOCK["dy_std"])
         tr = Transcript(b"zkl/golden/block", p, fname.encode())
         start = tr.state
         t0 = time.time()
         P = BK.prove_block(w, RefBlockProver(tr, ts, fp, p))
         print("block", fname, "%.1f s" % (time.time() - t0), len(P.log), "gadgets")
         cases.append(dict(field=fname, seed=3, state_before=hx(start), log=P.log,
-                          clipped=P.clipped, state_end=hx(tr.state)))
-    dump("block.json", dict(shape=[shape.seq, shape.hidden, shape.heads, shape.head_dim,
-                                   shape.ffn, shape.rank, list(shape.lora)],
-                            fp=[fp.gamma_fp, fp.zeta, fp.act_bound, fp.exp_n, fp.eps],
-                            cases=cases))
+                          state_end=hx(tr.state)))
+    dump("block.json", dict(shape=list(TINY_BLOCK["shape"][1:7]) + [list(TINY_BLOCK["shape"][7])],
+                            fp=TINY_BLOCK["fp"], wstd=TINY_BLOCK["wstd"],
+                            dy_std=TINY_BLOCK["dy_std"], cases=cases))
 
 
 def gen_softmax():

@@ -236,7 +236,8 @@ def test_boundary_errors_before_any_device_work():
                         key, tr, None)
 
 
-@pytest.mark.parametrize("name", ["silu", "silu_deriv", "exp0", "rsqrt_eps1e-5"])
+@pytest.mark.parametrize("name", ["silu", "silu_deriv", "exp0", "rsqrt_eps1e-5", "silu_g2048_a16",
+                                  "silu_deriv_g2048_a16", "exp_base4"])
 def test_table_generation_matches_reference(name):
     """paper_2508_21393_b200.tables restates tables.py:40-117; every entry must
     equal the reference's own table at gamma = 2^12, act_bound = 8, radices
@@ -256,6 +257,12 @@ def test_table_generation_matches_reference(name):
         xs, ys = T.silu_deriv_entries(4096, 8)
     elif name == "exp0":
         xs, ys = T.exp_segment_entries(4096, (1 << 16,) * 4, 0)
+    elif name == "silu_g2048_a16":  # the LLaMA block's tables (block.py)
+        xs, ys = T.silu_entries(2048, 16)
+    elif name == "silu_deriv_g2048_a16":
+        xs, ys = T.silu_deriv_entries(2048, 16)
+    elif name == "exp_base4":
+        xs, ys = T.exp_segment_entries(4096, (4, 1 << 16), 1)
     else:
         xs, ys = T.rsqrt_entries(4096, 8, 1e-5)
     assert xs[0] == g["x0"] and len(xs) == g["n"]
@@ -305,7 +312,9 @@ def test_block_schedule_census_on_cpu():
     """paper_2508_21393_b200.block.prove_block drives the gadget schedule and
     the fixed-point witness on any torch device: with a recording stand-in
     prover on CPU tensors the tiny block's gadget sequence matches the one
-    the reference's own gadgets produced (tests/golden/block.json)."""
+    the reference's own gadgets produced (tests/golden/block.json), every
+    claim handed to a gadget is honest (the identities the reference
+    verifiers check hold exactly), and every narrowed value is in range."""
     import torch
 
     from paper_2508_21393_b200 import block as BK
@@ -314,47 +323,74 @@ def test_block_schedule_census_on_cpu():
     g = load_golden("block.json")
     seq, hidden, heads, hd, ffn, rank, lora = g["shape"]
     shape = BK.BlockShape("tiny", seq, hidden, heads, hd, ffn, rank, tuple(lora))
-    gm, z, a, en, eps = g["fp"]
-    fp = BK.FixedPoint(gamma_fp=gm, zeta=z, act_bound=a, exp_n=en, eps=eps)
+    fp = BK.FixedPoint(**g["fp"])
+    gm, a = fp.gamma_fp, fp.act_bound
+    ga, aa = gm >> fp.act_shift, a << fp.act_shift
 
     class Recorder:
         def __init__(self):
-            self.fp, self.log, self.clipped = fp, [], 0
+            self.fp, self.log = fp, []
             col = lambda ys: torch.tensor(ys, dtype=torch.int32)  # noqa: E731
-            self.luts = {"silu": col(T.silu_entries(gm, a)[1]),
-                         "silu_deriv": col(T.silu_deriv_entries(gm, a)[1]),
-                         "rsqrt": col(T.rsqrt_entries(gm, a, eps)[1]),
-                         "exp": col(T.exp_segment_entries(gm, (en,), 0)[1])}
+            self.luts = {"silu": col(T.silu_entries(ga, aa)[1]),
+                         "silu_deriv": col(T.silu_deriv_entries(ga, aa)[1]),
+                         "rsqrt": col(T.rsqrt_entries(gm, a, fp.eps)[1]),
+                         "exp": col(T.exp_segment_entries(gm, (fp.exp_base, fp.exp_n), 1)[1]),
+                         "act_x0": -aa * ga}
 
         def matmul(self, a_, b_, c_):
             assert torch.equal(BK._mm(a_, b_), c_)  # honest claims
             self.log.append("matmul")
 
+        def matadd(self, a_, b_, c_, sign):
+            assert torch.equal(a_.long() + sign * b_.long(), c_.long())
+            self.log.append("matadd")
+
         def eprod(self, a_, b_, c_):
             assert torch.equal(a_.long() * b_.long(), c_)
             self.log.append("elementprod")
 
-        def rescale(self, wide):
-            q, r, clipped = BK._divmod(wide, fp)
-            self.clipped += clipped
-            assert torch.equal(q.long() * fp.zeta + r.long(), wide) or clipped
+        def rescale(self, wide, divisor):
+            q, r = BK._divmod(wide, divisor, fp)
+            lift = fp.zeta // divisor
+            # verify_rescale's identity (gadgets.py:644): lift*w = zeta*q + r
+            assert torch.equal(lift * wide.long(), fp.zeta * q.long() + r.long())
+            assert int(r.abs().max()) <= fp.zeta // 2
             self.log.append("rescale")
             return q
 
         def swiglu(self, wide, mode):
-            q, r, clipped = BK._divmod(wide, fp)
-            self.clipped += clipped
+            q, r = BK._divmod(wide, fp.zeta, fp)
+            assert torch.equal(wide.long(), fp.zeta * q.long() + r.long())
             self.log.append("swiglu")
             lut = self.luts["silu" if mode == "phi" else "silu_deriv"]
-            return BK._lut(lut, q, fp.qmin).to(torch.int16)
+            return BK._lut(lut, q, self.luts["act_x0"]).to(torch.int16)
 
         def rsqrt(self, v, u):
+            assert int(v.min()) >= 0 and int(v.max()) < a * gm
             self.log.append("rsqrt")
 
         def exp_lookup(self, v, e):
+            assert int(v.min()) >= 0 and int(v.max()) < fp.exp_n
             self.log.append("softmax_exp")
 
     c = g["cases"][0]
-    P = BK.prove_block(BK.BlockWitness(shape, seed=c["seed"], fp=fp, device="cpu"), Recorder())
+    w = BK.BlockWitness(shape, seed=c["seed"], fp=fp, device="cpu", wstd=g["wstd"],
+                        dy_std=g["dy_std"])
+    P = BK.prove_block(w, Recorder())
     assert P.log == [x[0] for x in c["log"]]
-    assert P.clipped == c["clipped"]
+
+
+def test_block_witness_raises_instead_of_clipping():
+    """A quotient outside quant_range raises RangeViolation (the reference
+    prover's behaviour, gadgets.py:575); nothing is clamped."""
+    import torch
+
+    from paper_2508_21393_b200 import block as BK
+    from paper_2508_21393_b200.nonlinear import RangeViolation
+
+    fp = BK.FP
+    wide = torch.tensor([[0, 5 * fp.zeta, -(8 * fp.gamma_fp) * fp.zeta - fp.zeta]])
+    with pytest.raises(RangeViolation, match=r"\(1 entries\)"):
+        BK._divmod(wide, fp.zeta, fp)
+    q, r = BK._divmod(wide[:, :2], fp.zeta, fp)
+    assert q.tolist() == [[0, 5]] and r.tolist() == [[0, 0]]
