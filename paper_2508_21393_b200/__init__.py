@@ -60,7 +60,6 @@ from .sumcheck import (  # noqa: F401
     SumcheckProof,
     Term,
     prove_sumcheck,
-    verify_sumcheck,
 )
 from .transcript import Transcript  # noqa: F401
 

@@ -215,38 +215,3 @@ def prove_sumcheck(claim, tr):
     rounds, point, finals = run_rounds(spec, dev, n, terms, degree, tr)
     RP = TYPES["RoundPolynomial"]
     return TYPES["SumcheckProof"]([RP(e) for e in rounds], tuple(finals)), point
-
-
-def _interpolate(evals, x, modulus):
-    d = len(evals) - 1
-    total = 0
-    for j, y in enumerate(evals):
-        num, den = 1, 1
-        for k in range(d + 1):
-            if k != j:
-                num = num * ((x - k) % modulus) % modulus
-                den *= j - k
-        total = (total + y * num % modulus * inverse(den % modulus, modulus)) % modulus
-    return total
-
-
-def verify_sumcheck(claimed_sum, terms, degree, num_vars, proof, tr):
-    """Host verifier with the semantics of sumcheck.py:148-172."""
-    p = tr.modulus
-    if len(proof.rounds) != num_vars:
-        return False, [], 0
-    absorb_claim(tr, claimed_sum, terms, degree, num_vars)
-    running = claimed_sum % p
-    point = []
-    for rp in proof.rounds:
-        evals = rp.evaluations
-        if len(evals) != degree + 1:
-            return False, [], 0
-        if (evals[0] + evals[1]) % p != running:
-            return False, [], 0
-        for e in evals:
-            tr.append(b"sumcheck/eval", e)
-        r = tr.challenge(b"sumcheck/round")
-        point.append(r)
-        running = _interpolate(evals, r, p)
-    return True, point, running

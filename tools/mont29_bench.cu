@@ -1,4 +1,4 @@
-// 9 x 29-bit unsaturated Montgomery product (csrc/mont29.cuh) against the
+// 9 x 29-bit unsaturated Montgomery product (tools/mont29.cuh) against the
 // library's 32-bit CIOS: host correctness check (no GPU needed, "check"),
 // then device throughput (3 independent products per call) and latency
 // (one dependent chain per warp).
@@ -9,7 +9,7 @@
 #include <cstring>
 
 #include "../paper_2508_21393_b200/csrc/field.cuh"
-#include "../paper_2508_21393_b200/csrc/mont29.cuh"
+#include "mont29.cuh"
 
 using namespace zkl;
 using T = fr_t;
