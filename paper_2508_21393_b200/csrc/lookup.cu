@@ -276,6 +276,79 @@ __global__ void __launch_bounds__(256) k_range_count(const TX* xs, uint64_t d, i
   }
 }
 
+// Range tables up to 2^16 entries (quant_range is exactly 2^16): per-block
+// 16-bit bins in shared memory, two per 32-bit word (128 KB for 2^16 bins),
+// so every count is a shared-memory atomic and each block flushes its n bins
+// once.  A half-word that reaches 0x8000 is moved to the global counter by
+// the one thread that saw it get there (atomicAdd returns the old value); the
+// other threads can add at most blockDim more before that subtraction lands,
+// so a half never carries into its neighbour.  Each thread reads 8 int16
+// entries per 16-byte load and writes their 8 indices with two 16-byte
+// stores: 2 B in + 4 B out per query, coalesced.
+constexpr uint32_t kRange16Threads = 1024;
+
+__device__ __forceinline__ void bin16_add(uint32_t* words, uint32_t* counts, uint32_t b) {
+  const uint32_t sh = (b & 1) * 16;
+  const uint32_t old = atomicAdd(&words[b >> 1], 1u << sh);
+  if (((old >> sh) & 0xffffu) == 0x7fffu) {  // this add made the half 0x8000
+    atomicSub(&words[b >> 1], 0x8000u << sh);
+    atomicAdd(&counts[b], 0x8000u);
+  }
+}
+
+__global__ void __launch_bounds__(kRange16Threads)
+    k_range_count16(const int16_t* xs, uint64_t d, int32_t x0, uint32_t n, uint32_t* counts,
+                    unsigned long long* first_miss, uint32_t* index_out) {
+  extern __shared__ uint32_t words[];  // ceil(n / 2) words
+  const uint32_t nw = (n + 1) / 2;
+  for (uint32_t w = threadIdx.x; w < nw; w += blockDim.x) words[w] = 0;
+  __syncthreads();
+  const uint64_t nvec = d / 8;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint4* xv = reinterpret_cast<const uint4*>(xs);
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nvec; v += stride) {
+    const uint4 raw = __ldcs(xv + v);
+    const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
+    uint32_t idx[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const int32_t val = (int32_t)(int16_t)(w4[k >> 1] >> (16 * (k & 1)));
+      const int32_t o = val - x0;
+      if (o >= 0 && o < (int32_t)n) {
+        idx[k] = (uint32_t)o;
+        bin16_add(words, counts, (uint32_t)o);
+      } else {
+        idx[k] = kEmpty;
+        atomicMin(first_miss, (unsigned long long)(8 * v + k));
+      }
+    }
+    if (index_out) {
+      uint4* out = reinterpret_cast<uint4*>(index_out + 8 * v);
+      __stcs(out, make_uint4(idx[0], idx[1], idx[2], idx[3]));
+      __stcs(out + 1, make_uint4(idx[4], idx[5], idx[6], idx[7]));
+    }
+  }
+  // the d % 8 tail (block 0)
+  if (blockIdx.x == 0 && threadIdx.x < d - 8 * nvec) {
+    const uint64_t i = 8 * nvec + threadIdx.x;
+    const int32_t o = (int32_t)xs[i] - x0;
+    uint32_t hit = kEmpty;
+    if (o >= 0 && o < (int32_t)n) {
+      hit = (uint32_t)o;
+      bin16_add(words, counts, hit);
+    } else {
+      atomicMin(first_miss, (unsigned long long)i);
+    }
+    if (index_out) index_out[i] = hit;
+  }
+  __syncthreads();
+  for (uint32_t w = threadIdx.x; w < nw; w += blockDim.x) {
+    const uint32_t c = words[w];
+    if (c & 0xffffu) atomicAdd(&counts[2 * w], c & 0xffffu);
+    if ((c >> 16) && 2 * w + 1 < n) atomicAdd(&counts[2 * w + 1], c >> 16);
+  }
+}
+
 int op_range_multiplicities(const void* x, int xt, uint64_t d, int64_t x0, uint64_t n,
                             uint32_t* counts, uint32_t* index_out, int64_t* first_miss,
                             cudaStream_t s) {
@@ -287,7 +360,25 @@ int op_range_multiplicities(const void* x, int xt, uint64_t d, int64_t x0, uint6
   unsigned long long* flag = (unsigned long long*)ws;
   ZKL_CUDA(cudaMemsetAsync(flag, 0xff, 8, s));
   ZKL_CUDA(cudaMemsetAsync(counts, 0, n * 4, s));
-  if (d) {
+  // int16 queries against a range of <= 2^16 entries (every rescale's
+  // quant_range lookup): the vectorised 16-bit-bin kernel; its 16-byte loads
+  // need an aligned column
+  if (d && xt == 1 && n <= 65536 && n > kRangeSmemBins && x0 >= INT32_MIN &&
+      x0 <= INT32_MAX && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+      (!index_out || (reinterpret_cast<uintptr_t>(index_out) & 15) == 0)) {
+    const size_t sb = ((n + 1) / 2) * 4;
+    static bool attr = false;
+    if (!attr) {
+      ZKL_CUDA(cudaFuncSetAttribute(k_range_count16, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    128 * 1024));
+      attr = true;
+    }
+    const unsigned per_sm = sb <= 64 * 1024 ? 2 : 1;
+    const unsigned g = grid_for((d + 7) / 8, kRange16Threads, per_sm);
+    k_range_count16<<<g, kRange16Threads, sb, s>>>((const int16_t*)x, d, (int32_t)x0,
+                                                    (uint32_t)n, counts, flag, index_out);
+    ZKL_LAUNCH_CHECK();
+  } else if (d) {
     const bool smem = n <= kRangeSmemBins;
     // shared-memory bins: a few blocks per SM, each flushes n counters once
     const unsigned g = smem ? grid_for(d, 256, 2) : grid_for(d, 256);

@@ -786,10 +786,27 @@ ZKL_D bool poll_tagged(const volatile uint64_t* src, uint32_t seq, uint32_t (&ou
 // words (independent loads, one PCIe round trip per poll; a single thread
 // issuing the loads back to back pays one round trip per load).  Every lane
 // of the warp must call it; on success out[0..NW) holds the payload.
+// Recorded-challenge replay (ZKL_PROFILE_REPLAY, run_phase_replay): when set,
+// a poll of the host challenge slot `ch` for round tag seq reads the
+// pre-drawn challenge from device memory instead, so a profiler that replays
+// the persistent / cluster kernels (ncu restores device memory between
+// passes) sees exactly the production kernels with no host in the loop.
+struct RecordedChallenges {
+  const uint32_t* words;  // round j's challenge at words[j * NW] (storage form)
+  const volatile uint64_t* ch;
+  uint32_t seq0;
+};
+__device__ RecordedChallenges g_rec = {nullptr, nullptr, 0};
+
 template <int NW>
 ZKL_D bool warp_poll(const volatile uint64_t* src, uint32_t seq, uint32_t* out,
                      const volatile uint32_t* abort_flag) {
   const int lane = threadIdx.x & 31;
+  if (g_rec.words && src == g_rec.ch) {
+    if (lane < NW) out[lane] = g_rec.words[(size_t)(seq - g_rec.seq0 - 1) * NW + lane];
+    __syncwarp();
+    return true;
+  }
   const uint64_t t0 = globaltimer();
   for (uint32_t spin = 1;; spin++) {
     uint64_t a = (uint64_t)seq << 32, b = a;
@@ -1507,8 +1524,19 @@ int wait_phase_finals(const PhaseArgs<F>& a, typename F::T* finals_out, cudaStre
 }
 
 template <class F>
+static int run_phase_replay(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out,
+                            uint8_t* point_out, typename F::T* finals_out, cudaStream_t s);
+
+static bool profile_replay() {
+  static const bool v = getenv("ZKL_PROFILE_REPLAY") != nullptr;
+  return v;
+}
+
+template <class F>
 int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t* point_out,
               typename F::T* finals_out, cudaStream_t s) {
+  if (profile_replay() && !a.replaying && a.rounds_limit <= 0)
+    return run_phase_replay<F>(a, tr, rounds_out, point_out, finals_out, s);
   using T = typename F::T;
   using H = typename host::For<F>::H;
   using W = typename Red<F>::W;
@@ -1520,7 +1548,8 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
     set_error("sumcheck_prove: bad arguments");
     return kErrArg;
   }
-  if (no_persistent()) return run_phase_stepwise<F>(a, tr, rounds_out, point_out, finals_out, s);
+  if (no_persistent() && !a.replaying)
+    return run_phase_stepwise<F>(a, tr, rounds_out, point_out, finals_out, s);
   Mailbox* mb_host;
   Mailbox* mb_dev;
   int rc = mailbox_for_current_device(&mb_host, &mb_dev);
@@ -1598,6 +1627,20 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
   const int k_full = shape == kLogupTiled ? 2 : k;
   const int ph = prof_open(kProfPhase, 3.0 * k_full * (double)(1ull << n) * F::kBytes,
                            (double)nrun, s);
+  if (a.replaying) {
+    // recorded challenges: point the device-side poll at them, launch the
+    // grid kernel and (stream-ordered behind it) the cluster kernel, wait
+    const uint32_t* rec = (const uint32_t*)a.replay_words;
+    RecordedChallenges gr = {rec, mb_dev->ch, seq0};
+    ZKL_CUDA(cudaMemcpyToSymbolAsync(g_rec, &gr, sizeof gr, 0, cudaMemcpyHostToDevice, s));
+    rc = run_dispatch<F>(rq, &pl, &nout, pl.j_switch > 0 ? 1 : 2);
+    if (!rc && pl.j_switch > 0 && pl.j_switch < n) rc = run_dispatch<F>(rq, &pl, &nout, 2);
+    prof_close(ph, s);
+    RecordedChallenges none = {nullptr, nullptr, 0};
+    ZKL_CUDA(cudaMemcpyToSymbolAsync(g_rec, &none, sizeof none, 0, cudaMemcpyHostToDevice, s));
+    ZKL_CUDA(cudaStreamSynchronize(s));
+    return rc;
+  }
   rc = run_dispatch<F>(rq, &pl, &nout, pl.j_switch > 0 ? 1 : 2);
   if (pl.j_switch == 0 || pl.j_switch >= n || nrun < n) prof_close(ph, s);  // else: at handoff
   if (rc) return rc;
@@ -1777,6 +1820,74 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
             n > 1 ? loop / (n - 1) : 0.0, hs / n, n > 1 ? hgap / (n - 1) : 0.0, hfill / n);
   }
   return kOk;
+}
+
+// ZKL_PROFILE_REPLAY=1 (profiling only): every phase is proven once
+// stepwise (k_round per round, host transcript in between: the proof), then
+// its input tables are restored and the production kernels run the same
+// phase again reading the recorded challenges from device memory
+// (RecordedChallenges).  Under ncu the second run is what to capture
+// (-k regex:"k_sumcheck_(persistent|cluster)"): the persistent / cluster
+// kernels, replayable, with no host in the loop.  Their folded tables are
+// compared with the stepwise run's so a replay that diverged is an error.
+template <class F>
+static int run_phase_replay(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out,
+                            uint8_t* point_out, typename F::T* finals_out, cudaStream_t s) {
+  using T = typename F::T;
+  constexpr int nb = F::kBytes;
+  const int n = a.num_vars, k = a.k;
+  if (a.prepare) {  // lazily computed round constants: no replay, prove as usual
+    a.replaying = true;
+    int rc = run_phase_stepwise<F>(a, tr, rounds_out, point_out, finals_out, s);
+    a.replaying = false;
+    return rc;
+  }
+  const size_t bytes = ((size_t)1 << n) * sizeof(T);
+  std::vector<void*> saved(k, nullptr);
+  for (int q = 0; q < k; q++) {
+    ZKL_CUDA(cudaMalloc(&saved[q], bytes));
+    ZKL_CUDA(cudaMemcpyAsync(saved[q], a.tables[q], bytes, cudaMemcpyDeviceToDevice, s));
+  }
+  std::vector<T> fin(k);
+  int rc = run_phase_stepwise<F>(a, tr, rounds_out, point_out, fin.data(), s);
+  if (finals_out)
+    for (int q = 0; q < k; q++) finals_out[q] = fin[q];
+  std::vector<uint32_t> words((size_t)n * (nb / 4));
+  for (int j = 0; j < n && !rc; j++) {
+    const T r = host::from_canon<F>(point_out + (size_t)j * nb);
+    memcpy(words.data() + (size_t)j * (nb / 4), &r, nb);
+  }
+  void* dw = nullptr;
+  if (!rc) {
+    ZKL_CUDA(cudaMalloc(&dw, words.size() * 4));
+    ZKL_CUDA(cudaMemcpyAsync(dw, words.data(), words.size() * 4, cudaMemcpyHostToDevice, s));
+    for (int q = 0; q < k; q++)
+      ZKL_CUDA(cudaMemcpyAsync(a.tables[q], saved[q], bytes, cudaMemcpyDeviceToDevice, s));
+    HostTranscript scratch = tr;  // the replay appends nothing: the host loop is skipped
+    a.replaying = true;
+    a.replay_words = dw;
+    rc = run_phase<F>(a, scratch, rounds_out, point_out, nullptr, s);
+    a.replaying = false;
+    a.replay_words = nullptr;
+    a.stepwise = true;  // finals come from the stepwise run (fin_cache)
+  }
+  if (!rc) {  // the replay must end on the stepwise run's folded values
+    for (int q = 0; q < k; q++) {
+      T v[2];
+      ZKL_CUDA(cudaMemcpyAsync(v, a.tables[q], 2 * sizeof(T), cudaMemcpyDeviceToHost, s));
+      ZKL_CUDA(cudaStreamSynchronize(s));
+      using H = typename host::For<F>::H;
+      const T r = host::from_canon<F>(point_out + (size_t)(n - 1) * nb);
+      const T f = H::add(v[0], H::mul(r, H::sub(v[1], v[0])));
+      if (memcmp(&f, &fin[q], sizeof(T)) != 0) {
+        set_error("profile replay: the production kernels diverged from the stepwise proof");
+        rc = kErrArg;
+      }
+    }
+  }
+  for (void* p : saved) cudaFree(p);
+  if (dw) cudaFree(dw);
+  return rc;
 }
 
 template <class F>

@@ -49,6 +49,9 @@ struct PhaseArgs {
   // one-launch-per-round mode (profilers): finals are kept here
   bool stepwise = false;
   std::vector<T> fin_cache;
+  // ZKL_PROFILE_REPLAY: second run of the phase on recorded challenges
+  bool replaying = false;
+  const void* replay_words = nullptr;
 };
 
 // true when the persistent (mailbox) kernels must not be used: ZKL_NO_PERSISTENT,

@@ -369,3 +369,34 @@ def test_pair_lookup_lazy_secret_miss_and_collision_free_path():
     with pytest.raises(zb.ElementNotInTable) as e:
         zb.prove_pair_lookup(b"swiglu/act", pt(c["x"]), pt(y), pair, KEY, tr, _Rng())
     assert e.value.index == 40 and 0 <= e.value.value < p
+
+
+@pytest.mark.parametrize("n,d", [(1 << 16, (1 << 21) + 5), (20000, 100003), (1 << 16, 7)])
+def test_range_count16_hot_bins_tails_and_misses(n, d):
+    """The vectorised 16-bit-bin histogram (k_range_count16: int16 queries,
+    12288 < n <= 2^16): half-word overflow flushes (a bin hit 2^20 times),
+    d % 8 tails, misses reported at their first index, and an unaligned
+    column taking the fallback kernel -- all against torch.bincount."""
+    from paper_2508_21393_b200 import lookup as L
+
+    spec = D.spec_for(FIELDS["big"])
+    lo = -(n // 2)
+    tab = NL.device_range_table(lo, n, spec, StubCommitment(_log2(n)), "r")
+    g = torch.Generator(device="cuda").manual_seed(d)
+    x = torch.randint(lo, lo + n, (d,), device="cuda", generator=g, dtype=torch.int64)
+    x[: min(d, 1 << 20)] = lo + 1  # one very hot bin: many 0x8000 flushes
+    x[3 * d // 4:] = lo + n - 1
+    col = x.to(torch.int16)
+    for c in (col, torch.cat([col[:1], col])[1:]):  # aligned, then a misaligned view
+        counts, index = L.multiplicities_range(D.LiftedColumn(c, spec), tab, c, tab.int_column)
+        want = torch.bincount((x - lo).long(), minlength=n)
+        got = torch.tensor(D.download(counts.buf, spec, n), dtype=torch.int64)
+        assert torch.equal(got, want.cpu())
+        assert torch.equal(index[:d].long(), (x - lo).long())
+    if n < (1 << 16):
+        bad = col.clone()
+        bad[d - 1] = lo + n  # in the tail
+        bad[d // 2] = lo - 1
+        with pytest.raises(zb.ElementNotInTable) as e:
+            L.multiplicities_range(D.LiftedColumn(bad, spec), tab, bad, tab.int_column)
+        assert e.value.index == min(d // 2, d - 1)

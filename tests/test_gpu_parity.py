@@ -339,6 +339,26 @@ def test_stepwise_mode_matches_oracle():
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
 
 
+def test_profile_replay_mode_matches_oracle():
+    """ZKL_PROFILE_REPLAY=1 (the ncu capture mode for the production
+    kernels): each phase is proven stepwise, then re-run by the persistent /
+    cluster kernels on recorded challenges, whose final folded values must
+    equal the proof's (the driver raises otherwise).  Proofs stay bit-exact,
+    including a dense claim large enough for the grid -> cluster handoff."""
+    code = (
+        "import sys; sys.path[:0] = ['.', 'tests', 'tests/golden']\n"
+        "import test_gpu_parity as T\n"
+        "T.test_sumcheck_shapes_vs_oracle('big', 6, 'sum2prod2')\n"
+        "T.test_sumcheck_shapes_vs_oracle('test', 16, 'prod3')\n"
+        "T.test_sumcheck_random_vs_oracle('big', 7, 3, 12)\n"
+        "T.test_matmul_factored_vs_oracle('big', (5, 9, 3), 'i16', 'native')\n"
+        "import test_gpu_parity_scale as S\n"
+        "S.test_cfg5_dense_replicated_claim_matches_oracle()\n"
+        "print('ok')\n")
+    r = _run_isolated(code, ZKL_PROFILE_REPLAY="1")
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
+
+
 @pytest.mark.parametrize("env", [{"ZKL_MATVEC_SLOW": "1"}, {"ZKL_MATVEC_FAST64": "1"}])
 def test_matvec_alternate_kernels_vs_numpy(env):
     """The non-default matvec kernels (wide-accumulator everywhere, or the
