@@ -121,6 +121,27 @@ int zkl_sumcheck_prove(int field, void* const* tables, int k, int num_vars, int 
                        const uint8_t* post_mul_canon, uint8_t* state_inout, uint8_t* rounds_out,
                        uint8_t* point_out, uint8_t* finals_out, void* stream);
 
+/* Multi-GPU (ranks = processes of one node, one GPU each).
+ * zkl_shard_open joins the rank set `name` (POSIX shared memory /zkl-<name>;
+ * world a power of two) -- the host-side all-reduce / all-gather of per-round
+ * partial sums.  zkl_sumcheck_prove_sharded is zkl_sumcheck_prove for a claim
+ * whose hypercube is sharded cyclically on its low log2(world) index bits:
+ * `tables` are this rank's shard (entries i*world + rank, 2^(num_vars -
+ * log2 world) each), num_vars / post_add are the global claim's, and every
+ * rank returns the same rounds, point, finals and end state as the unsharded
+ * prover (replaces prove_sumcheck, sumcheck.py:98-130, for one shard).
+ * zkl_shard_exchange: all-gather of nbytes per rank (out: world * nbytes). */
+int zkl_shard_open(const char* name, int rank, int world);
+int zkl_shard_close(void);
+int zkl_shard_world(void);
+int zkl_shard_exchange(const void* mine, uint64_t nbytes, void* out);
+int zkl_sumcheck_prove_sharded(int field, void* const* tables, int k, int num_vars, int degree,
+                               int nterms, const int32_t* nfactors, const int32_t* factors,
+                               const uint8_t* coeffs_canon, const uint8_t* post_add_canon,
+                               const uint8_t* post_mul_canon, uint8_t* state_inout,
+                               uint8_t* rounds_out, uint8_t* point_out, uint8_t* finals_out,
+                               void* stream);
+
 /* Host SHAKE-256 (FIPS 202) and transcript primitives (transcript.py:13-42),
  * exported for cross-checks against hashlib; no GPU involved. */
 int zkl_shake256(const uint8_t* in, uint64_t len, uint8_t* out, uint64_t outlen);

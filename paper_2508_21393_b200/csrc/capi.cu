@@ -89,6 +89,30 @@ int sumcheck_prove(void* const* tables, int k, int num_vars, int degree, int nte
 }
 
 template <class F>
+int sumcheck_prove_sharded(void* const* tables, int k, int num_vars, int degree, int nterms,
+                           const int32_t* nfactors, const int32_t* factors, const uint8_t* coeffs,
+                           const uint8_t* post_add, const uint8_t* post_mul, uint8_t* state,
+                           uint8_t* rounds_out, uint8_t* point_out, uint8_t* finals_out,
+                           cudaStream_t s) {
+  if (nterms < 0 || nterms > kMaxTerms || num_vars < 0 || num_vars > 63 || k < 1 ||
+      k > kMaxTables) {
+    set_error("sumcheck_prove_sharded: bad nterms/num_vars/k");
+    return kErrArg;
+  }
+  int err;
+  Terms<F> tm = make_terms<F>(degree, nterms, nfactors, factors, coeffs, k, &err);
+  if (err) { set_error("sumcheck_prove_sharded: bad term factors"); return kErrArg; }
+  std::vector<typename F::T> adds;
+  if (post_add) {
+    adds.resize(num_vars > 0 ? num_vars : 1);
+    for (int j = 0; j < num_vars; j++) adds[j] = load_canon<F>(post_add + (size_t)j * F::kBytes);
+  }
+  typename F::T mul = post_mul ? scalar<F>(post_mul) : F::one();
+  return op_sumcheck_prove_sharded<F>(tables, k, num_vars, tm, post_add ? adds.data() : nullptr,
+                                      mul, state, rounds_out, point_out, finals_out, s);
+}
+
+template <class F>
 int transcript_challenge(uint8_t* state, const char* label, uint8_t* out) {
   HostTranscript tr;
   memcpy(tr.state, state, 64);
@@ -219,6 +243,16 @@ int zkl_sumcheck_prove(int field, void* const* tables, int k, int num_vars, int 
   D(field, sumcheck_prove<F>(tables, k, num_vars, degree, nterms, nfactors, factors,
                              coeffs_canon, post_add_canon, post_mul_canon, state_inout,
                              rounds_out, point_out, finals_out, (cudaStream_t)stream));
+}
+int zkl_sumcheck_prove_sharded(int field, void* const* tables, int k, int num_vars, int degree,
+                               int nterms, const int32_t* nfactors, const int32_t* factors,
+                               const uint8_t* coeffs_canon, const uint8_t* post_add_canon,
+                               const uint8_t* post_mul_canon, uint8_t* state_inout,
+                               uint8_t* rounds_out, uint8_t* point_out, uint8_t* finals_out,
+                               void* stream) {
+  D(field, sumcheck_prove_sharded<F>(tables, k, num_vars, degree, nterms, nfactors, factors,
+                                     coeffs_canon, post_add_canon, post_mul_canon, state_inout,
+                                     rounds_out, point_out, finals_out, (cudaStream_t)stream));
 }
 int zkl_shake256(const uint8_t* in, uint64_t len, uint8_t* out, uint64_t outlen) {
   shake256(in, (size_t)len, out, (size_t)outlen);

@@ -72,6 +72,14 @@ int op_sumcheck_prove(void* const* tables, int k, int num_vars, const Terms<F>& 
                       uint8_t* state, uint8_t* rounds_out, uint8_t* point_out,
                       uint8_t* finals_out, cudaStream_t s);
 template <class F>
+int op_sumcheck_prove_sharded(void* const* tables, int k, int num_vars, const Terms<F>& tm,
+                      const typename F::T* post_add, const typename F::T& post_mul,
+                      uint8_t* state, uint8_t* rounds_out, uint8_t* point_out,
+                      uint8_t* finals_out, cudaStream_t s);
+int shard_world();
+int shard_rank();
+int shard_exchange(const void* mine, size_t nbytes, uint8_t* out);
+template <class F>
 int op_sumcheck_finish(void* const* tables, int k, typename F::T r, uint8_t* finals_host,
                        cudaStream_t s);
 

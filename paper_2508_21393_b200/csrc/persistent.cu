@@ -1880,7 +1880,9 @@ static int run_phase_replay(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds
       const T r = host::from_canon<F>(point_out + (size_t)(n - 1) * nb);
       const T f = H::add(v[0], H::mul(r, H::sub(v[1], v[0])));
       if (memcmp(&f, &fin[q], sizeof(T)) != 0) {
-        set_error("profile replay: the production kernels diverged from the stepwise proof");
+        set_error("profile replay: the production kernels diverged from the stepwise proof "
+                  "(table %d of %d, %d rounds, shape %d)", q, k, n,
+                  a.forced_shape >= 0 ? a.forced_shape : detect_shape<F>(a.tm));
         rc = kErrArg;
       }
     }

@@ -24,6 +24,7 @@ import torch
 
 from . import _native as N
 from . import device as D
+from . import shard
 from .field import inverse_pow2
 from .sumcheck import TYPES as SC_TYPES
 from .sumcheck import Term, absorb_claim, native_transcript, run_rounds
@@ -318,10 +319,44 @@ def matmul_sumcheck_replicated(A, B, C, dims, tr):
     r_u = tr.challenge_vector(b"matmul/r_u", d0)
     r_v = tr.challenge_vector(b"matmul/r_v", d2)
     cneg = (-inverse_pow2(d1, p)) % p
-    tables = replicated_tables(A, B, C, dims, r_u, r_v, spec)
     n = d0 + d1 + d2
+    terms = [(1, (0, 1, 2)), (cneg, (0, 3))]
+    g = shard.active()
+    if shard.wants(n) and (1 << d2) >= g.world and native_transcript(tr, spec):
+        # multi-GPU: the low index bits are v's, so this rank's shard of the
+        # four tables is the replicated claim over the columns v = v' G + rank
+        tables = replicated_tables_shard(A, B, C, dims, r_u, r_v, spec, g.rank, g.world)
+        absorb_claim(tr, 0, [Term(c, f) for c, f in terms], 3, n)
+        return shard.run_rounds_sharded(spec, tables, n, terms, 3, tr)
+    tables = replicated_tables(A, B, C, dims, r_u, r_v, spec)
     absorb_claim(tr, 0, [Term(1, (0, 1, 2)), Term(cneg, (0, 3))], 3, n)
-    return run_rounds(spec, tables, n, [(1, (0, 1, 2)), (cneg, (0, 3))], 3, tr)
+    return run_rounds(spec, tables, n, terms, 3, tr)
+
+
+def replicated_tables_shard(A, B, C, dims, r_u, r_v, spec, rank, world):
+    """Rank `rank`'s cyclic shard of replicated_tables: global index
+    u || w || v with v = v' world + rank, i.e. the replicated claim of the
+    column slices B[:, rank::world], C[:, rank::world] and the eq weights
+    eq(r_u, u) eq(r_v, v' world + rank)."""
+    d0, d1, d2 = dims
+    D0, D1, D2 = 1 << d0, 1 << d1, (1 << d2) // world
+    W = spec.nbytes // 8
+    uv = shard.eq_shard(list(r_u) + list(r_v), spec, rank, world)  # over u || v'
+    a = A.as_field_vector(spec).view(D0, D1, 1, W)
+    def cols(M, rows):
+        if M.mtype == N.MT_FIELD:
+            t = M.t.view(rows, 1 << d2, W)[:, rank::world].reshape(-1, W).contiguous()
+            return DeviceMatrix(t, rows, D2, N.MT_FIELD, spec).as_field_vector(spec)
+        t = M.t.view(rows, 1 << d2)[:, rank::world].contiguous()
+        return DeviceMatrix.from_int_tensor(t).as_field_vector(spec)
+
+    b, c = cols(B, D1), cols(C, D0)
+    b = b.view(1, D1, D2, W)
+    c = c.view(D0, 1, D2, W)
+    shape = (D0, D1, D2, W)
+    return [uv.view(D0, 1, D2, W).expand(shape).reshape(-1, W),
+            a.expand(shape).reshape(-1, W), b.expand(shape).reshape(-1, W),
+            c.expand(shape).reshape(-1, W)]
 
 
 def prove_matmul(a, b, c, key, tr, rng):
@@ -441,9 +476,18 @@ def prove_elementprod(a, b, c, key, tr, rng):
     claimed = c_opening.values[0]
     spec = D.spec_for(p)
     rows, cols = 1 << shape[0], 1 << shape[1]
+    term = Term(1, (0, 1, 2))
+    if shard.wants(n) and native_transcript(tr, spec):
+        # multi-GPU: this rank's cyclic shard of eq(r, .), A and B (shard.py)
+        g = shard.active()
+        absorb_claim(tr, claimed, [term], 3, n)
+        loc = [shard.eq_shard(r, spec, g.rank, g.world),
+               _shard_matrix(_device_matrix(a, rows, cols, spec), spec, g),
+               _shard_matrix(_device_matrix(b, rows, cols, spec), spec, g)]
+        rounds, point, finals = shard.run_rounds_sharded(spec, loc, n, [(1, (0, 1, 2))], 3, tr)
+        return _elementprod_proof(key, tr, rng, a, b, shape, c_opening, rounds, point, finals)
     ta = _consumable(_device_matrix(a, rows, cols, spec), spec)
     tb = _consumable(_device_matrix(b, rows, cols, spec), spec)
-    term = Term(1, (0, 1, 2))
     absorb_claim(tr, claimed, [term], 3, n)
     got = _eq_factored_prod3(spec, tr, r, ta, tb, n) if n >= EQ_FACTORED_MIN_VARS else None
     if got is not None:
@@ -454,6 +498,18 @@ def prove_elementprod(a, b, c, key, tr, rng):
     else:
         rounds, point = [], []
         finals = [1, D.read_scalar(ta, spec), D.read_scalar(tb, spec)]
+    return _elementprod_proof(key, tr, rng, a, b, shape, c_opening, rounds, point, finals)
+
+
+def _shard_matrix(M, spec, g):
+    """This rank's cyclic shard (entries i*G + rank of the row-major matrix)
+    as a fresh field vector: integer matrices are sliced first, then lifted."""
+    if M.mtype == N.MT_FIELD:
+        return shard.shard_of(M.t, spec, g.rank, g.world)
+    return D.lift(M.t.reshape(-1)[g.rank::g.world].contiguous(), spec)
+
+
+def _elementprod_proof(key, tr, rng, a, b, shape, c_opening, rounds, point, finals):
     RP = SC_TYPES["RoundPolynomial"]
     sc_proof = SC_TYPES["SumcheckProof"]([RP(e) for e in rounds], tuple(finals))
     committed = [t for t in (a, b) if t.ref.kind == "committed"]
