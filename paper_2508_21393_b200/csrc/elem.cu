@@ -389,6 +389,90 @@ __global__ void k_lift16_lut(typename F::T* dst, const int16_t* src, uint64_t n,
   }
   for (; i < n; i += stride) dst[i] = t16[(int)src[i] + 32768];
 }
+// int16 -> Fr255 Montgomery form without a table: x R mod p = m R1 - q p for
+// m = |x| < 2^15 (R1 = R mod p), q = floor(m R1 / p) estimated in float64
+// (off by at most one, corrected), then negated for x < 0.  16 IMAD.WIDE and
+// two carry chains per entry in registers, so the kernel is bound by its 2 B
+// read + 32 B write stream, not by the L2 table gathers of k_lift16_lut.
+ZKL_D fr_t lift16_direct(int x) {
+  const uint32_t R1[8] = {0xfffffffeu, 0x00000001u, 0x00034802u, 0x5884b7fau,
+                          0xecbc4ff5u, 0x998c4fefu, 0xacc5056fu, 0x1824b159u};
+  const uint32_t P[8] = {Fr255::P0, Fr255::P1, Fr255::P2, Fr255::P3,
+                         Fr255::P4, Fr255::P5, Fr255::P6, Fr255::P7};
+  const uint32_t m = (uint32_t)(x < 0 ? -x : x);
+  const uint32_t q = (uint32_t)((double)m * 0.20826083002509044);  // R1 / p
+  // t = m R1 - q p (both < 2^271; the difference is in (-p, 2p))
+  uint64_t ca = 0, cb = 0;
+  int64_t br = 0;
+  uint32_t t[9];
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    ca += (uint64_t)m * R1[k];
+    cb += (uint64_t)q * P[k];
+    const int64_t d = (int64_t)(uint32_t)ca - (int64_t)(uint32_t)cb + br;
+    t[k] = (uint32_t)d;
+    br = d >> 32;  // -1, 0 (arithmetic shift)
+    ca >>= 32;
+    cb >>= 32;
+  }
+  t[8] = (uint32_t)((int64_t)ca - (int64_t)cb + br);  // 0, or all ones when negative
+  fr_t r;
+#pragma unroll
+  for (int k = 0; k < 8; k++) r.v[k] = t[k];
+  if ((int32_t)t[8] < 0) {  // q was one too large: add p
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const uint64_t v = (uint64_t)r.v[k] + P[k] + c;
+      r.v[k] = (uint32_t)v;
+      c = (uint32_t)(v >> 32);
+    }
+  } else {
+    // q one too small: r >= p (r < 2p < 2^256 always fits the 8 limbs)
+    bool ge = true;
+#pragma unroll
+    for (int k = 7; k >= 0; k--) {
+      if (r.v[k] != P[k]) {
+        ge = r.v[k] > P[k];
+        break;
+      }
+    }
+    if (ge) {
+      int64_t b = 0;
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const int64_t v = (int64_t)r.v[k] - P[k] + b;
+        r.v[k] = (uint32_t)v;
+        b = v >> 32;
+      }
+    }
+  }
+  if (x < 0) {  // p - r (r != 0 for x != 0)
+    int64_t b = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const int64_t v = (int64_t)P[k] - r.v[k] + b;
+      r.v[k] = (uint32_t)v;
+      b = v >> 32;
+    }
+  }
+  return r;
+}
+
+__global__ void k_lift16_direct(fr_t* dst, const int16_t* src, uint64_t n) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  for (; i - lane + 31 + 3 * stride < n; i += 4 * stride) {  // warp-uniform condition
+    int x[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) x[k] = __ldcs(src + i + k * stride);
+#pragma unroll
+    for (int k = 0; k < 4; k++) store_warp_fr(dst + (i - lane) + k * stride, lift16_direct(x[k]), lane);
+  }
+  for (; i < n; i += stride) dst[i] = lift16_direct(src[i]);
+}
+
 template <class F, class I>
 __global__ void k_lift_chunks(typename F::T* dst, const I* src, uint64_t n,
                               const typename F::T* chunks) {
@@ -438,7 +522,16 @@ int op_lift(void* dst, const void* src, int mtype, uint64_t n, cudaStream_t s) {
       int rc = lift_luts_fr(&t16, &ch, s);
       if (rc) return rc;
       switch (mtype) {
-        case 1: k_lift16_lut<F><<<g, 256, 0, s>>>(d, (const int16_t*)src, n, t16); break;
+        case 1:
+          if constexpr (F::kId == 0) {
+            static const bool lut = getenv("ZKL_LIFT_LUT") != nullptr;
+            if (!lut) {
+              k_lift16_direct<<<g, 256, 0, s>>>((fr_t*)d, (const int16_t*)src, n);
+              break;
+            }
+          }
+          k_lift16_lut<F><<<g, 256, 0, s>>>(d, (const int16_t*)src, n, t16);
+          break;
         case 2: k_lift_chunks<F, int32_t><<<g, 256, 0, s>>>(d, (const int32_t*)src, n, ch); break;
         default: k_lift_chunks<F, int64_t><<<g, 256, 0, s>>>(d, (const int64_t*)src, n, ch); break;
       }

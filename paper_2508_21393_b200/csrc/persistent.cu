@@ -797,6 +797,12 @@ struct RecordedChallenges {
   uint32_t seq0;
 };
 __device__ RecordedChallenges g_rec = {nullptr, nullptr, 0};
+// replay only: blocks of the grid kernel that finished each round.  Live, the
+// challenge of round j exists only after every block finished round j (the
+// host draws it from the published sums), which is what orders the next
+// round's reads after the other blocks' in-place folds; a recorded challenge
+// is available at once, so block 0 first waits for this count.
+__device__ unsigned g_rec_done = 0;
 
 template <int NW>
 ZKL_D bool warp_poll(const volatile uint64_t* src, uint32_t seq, uint32_t* out,
@@ -1005,6 +1011,7 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<EV>::value)
         for (int q = 0; q < EV::NOUT; q++) partials[(size_t)blockIdx.x * EV::NOUT + q] = v[q];
         __threadfence();
         const unsigned t = atomicAdd(ticket, 1u);
+        if (g_rec.words) atomicAdd(&g_rec_done, 1u);
         s_flag = (t == G * (unsigned)(j - j0 + 1) - 1) ? 1 : 0;
         if (tr0) trace[j * 8 + 2] = globaltimer();
       }
@@ -1044,6 +1051,11 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<EV>::value)
       __shared__ uint32_t cw[NC];
       bool ok;
       if (direct || blockIdx.x == 0) {
+        if (g_rec.words) {
+          const unsigned want = G * (unsigned)(j - j0 + 1);
+          while (*(volatile unsigned*)&g_rec_done < want) {
+          }
+        }
         ok = warp_poll<NC>(mb->ch, seq, cw, &mb->abort);
         if (!direct && ok && lane < NC)
           reinterpret_cast<volatile uint64_t*>(bcast)[lane] = tag(cw[lane], seq);
@@ -1632,7 +1644,10 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
     // grid kernel and (stream-ordered behind it) the cluster kernel, wait
     const uint32_t* rec = (const uint32_t*)a.replay_words;
     RecordedChallenges gr = {rec, mb_dev->ch, seq0};
+    const unsigned zero = 0;
     ZKL_CUDA(cudaMemcpyToSymbolAsync(g_rec, &gr, sizeof gr, 0, cudaMemcpyHostToDevice, s));
+    ZKL_CUDA(cudaMemcpyToSymbolAsync(g_rec_done, &zero, sizeof zero, 0, cudaMemcpyHostToDevice,
+                                     s));
     rc = run_dispatch<F>(rq, &pl, &nout, pl.j_switch > 0 ? 1 : 2);
     if (!rc && pl.j_switch > 0 && pl.j_switch < n) rc = run_dispatch<F>(rq, &pl, &nout, 2);
     prof_close(ph, s);

@@ -400,3 +400,16 @@ def test_range_count16_hot_bins_tails_and_misses(n, d):
         with pytest.raises(zb.ElementNotInTable) as e:
             L.multiplicities_range(D.LiftedColumn(bad, spec), tab, bad, tab.int_column)
         assert e.value.index == min(d // 2, d - 1)
+
+
+@pytest.mark.parametrize("field", ["big", "test"])
+def test_lift_int16_exhaustive(field):
+    """Every int16 value (the table-free k_lift16_direct path for Fr255:
+    m R1 - q p with a float64 quotient estimate and one correction) lifts to
+    v mod p; a ragged length exercises the tail loop."""
+    p = FIELDS[field]
+    spec = D.spec_for(p)
+    t = torch.arange(-32768, 32768, dtype=torch.int64).to(torch.int16)
+    t = torch.cat([t, t[:1234]])
+    got = D.download(D.lift(t.cuda(), spec), spec, t.numel())
+    assert got == [int(v) % p for v in t.tolist()]

@@ -179,45 +179,6 @@ def test_sumcheck_shapes_vs_oracle(field, n, shape):
     assert point == opoint and t1.state == t2.state
 
 
-@pytest.mark.parametrize("G", [2, 4, 8])
-@pytest.mark.parametrize("field,n", [("big", 10), ("test", 13)])
-def test_sharded_device_rounds_match_unsharded(field, n, G):
-    """The sharded protocol (paper_2508_21393_b200/shard.py) with G cyclic
-    low-bit shards of one claim, each shard's rounds on the device, the
-    per-round sums and final gather on the host: identical to the unsharded
-    oracle prover, post scalars included."""
-    from paper_2508_21393_b200 import shard
-
-    p = FIELDS[field]
-    spec = D.spec_for(p)
-    rnd = random.Random(n * 7 + G)
-    tabs = [inputs.field_vec(rnd.randrange(1 << 30), 1 << n, p) for _ in range(3)]
-    terms = [(rnd.randrange(p), (0, 1, 2)), (rnd.randrange(p), (1,)), (rnd.randrange(p), (0, 2))]
-    post_add = [rnd.randrange(p) for _ in range(n)]
-    post_mul = rnd.randrange(p)
-    t1 = Transcript(b"shard", p, b"seed")
-    zb.sumcheck.absorb_claim(t1, 0, [zb.Term(c, f) for c, f in terms], 3, n)
-    dev = [D.upload(t, spec) for t in tabs]
-    rounds, point, finals = shard.prove_device_sharded_local(spec, dev, terms, 3, n, t1, G,
-                                                             post_add=post_add,
-                                                             post_mul=post_mul)
-    t2 = fs.FS(b"shard", p, b"seed")
-    sc.absorb_claim(t2, 0, terms, 3, n)
-    cur = [list(t) for t in tabs]
-    want = []
-    for j in range(n):
-        ev = sc.round_evals(cur, terms, 3, p)
-        ev = tuple(post_mul * (e + post_add[j]) % p for e in ev)
-        want.append(ev)
-        for e in ev:
-            t2.append(b"sumcheck/eval", e)
-        r = t2.challenge(b"sumcheck/round")
-        cur = [multilinear.fold_msb(t, r, p) for t in cur]
-    assert [tuple(r) for r in rounds] == want
-    assert list(finals) == [t[0] for t in cur]
-    assert t1.state == t2.state
-
-
 # --- zkMat ---------------------------------------------------------------------------
 
 

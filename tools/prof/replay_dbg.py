@@ -9,3 +9,11 @@ for name, fn in [("s2p2", lambda: T.test_sumcheck_shapes_vs_oracle('big', 6, 'su
         fn(); print(name, "ok", flush=True)
     except Exception as e:
         print(name, "FAIL", str(e)[:300], flush=True)
+import test_gpu_parity_scale as S
+for name, fn in [("cfg5-24", S.test_cfg5_dense_replicated_claim_matches_oracle),
+                 ("prod3-16", lambda: T.test_sumcheck_shapes_vs_oracle('test', 16, 'prod3')),
+                 ("s2p2-15", lambda: T.test_sumcheck_shapes_vs_oracle('big', 15, 'sum2prod2'))]:
+    try:
+        fn(); print(name, "ok", flush=True)
+    except Exception as e:
+        print(name, "FAIL", str(e)[:300], flush=True)
