@@ -505,6 +505,60 @@ def run_sweep(ns, mont_peak=None):
     return out
 
 
+STRONG = ("strong scaling (N > 1 only; SURVEY.md sec. 8e): the hypercube of each large claim "
+          "sharded cyclically on its low log2(N) index bits across the N ranks "
+          "(paper_2508_21393_b200/shard.py, csrc/shard.cu): the cfg5 dense zkMat claim at "
+          "n = 28 and the LLaMA-2-7B block proof (its elementprods >= 2^22 sharded, the rest "
+          "proven redundantly on every rank); seconds = max over ranks")
+
+
+def run_strong(world, rank, n=28):
+    """Strong scaling under torchrun: every rank proves the same claims with
+    the large ones sharded; returns (seconds max over ranks) per workload."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2508_21393_b200 as zb
+    from paper_2508_21393_b200 import gadgets as G
+    from paper_2508_21393_b200 import shard
+
+    def tmax(sec):
+        t = torch.tensor([sec], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    out = {"workload": STRONG, "n_gpus": world}
+    with shard.ShardGroup.from_torch_distributed():
+        d0 = d2 = n // 3
+        d1 = n - 2 * d0
+        g = torch.Generator(device="cuda").manual_seed(n)
+        a = torch.randint(-32768, 32768, (1 << d0, 1 << d1), device="cuda", generator=g,
+                          dtype=torch.int32).short()
+        b = torch.randint(-32768, 32768, (1 << d1, 1 << d2), device="cuda", generator=g,
+                          dtype=torch.int32).short()
+        c = torch.matmul(a.double(), b.double()).round().long()
+        A, B, C = (G.DeviceMatrix.from_int_tensor(x) for x in (a, b, c))
+        states = []
+        for rep in range(3):
+            tr = zb.Transcript(b"zklora-b200/strong", P_BIG, b"%d" % n)
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            G.matmul_sumcheck_replicated(A, B, C, (d0, d1, d2), tr)
+            torch.cuda.synchronize()
+            sec = time.perf_counter() - t0
+            states.append(bytes(tr.state))
+        out["dense_zkmat"] = {"n": n, "field_elems": 4 << n, "seconds": tmax(sec),
+                              "field_elems_per_s": (4 << n) / tmax(sec),
+                              "same_proof_every_rep": len(set(states)) == 1}
+        del A, B, C, a, b, c
+        torch.cuda.empty_cache()
+        blk = run_cfg4(1, 1, "7b", verify_block=False)
+        out["block_7b"] = {"block_proof_s": tmax(blk["block_proof_s"]),
+                           "gadgets": blk["gadgets_per_block"]}
+    return out
+
+
 def run_hbm_kernels(peak_gbs):
     """The HBM-bound passes of the path, timed live with CUDA events on the
     proving stream (10 launches each, 2^27-entry inputs > L2): achieved GB/s
@@ -581,9 +635,17 @@ def main():
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
+    # one GPU per rank; ZKL_BENCH_OVERSUBSCRIBE=1 lets N ranks share the
+    # visible GPUs (a smoke test of the N > 1 path on a 1-GPU box, over gloo:
+    # NCCL refuses two ranks on one device)
+    over = os.environ.get("ZKL_BENCH_OVERSUBSCRIBE") == "1"
+    dev_id = local % torch.cuda.device_count() if over else local
+    torch.cuda.set_device(dev_id)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if over:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_id))
 
     import paper_2508_21393_b200 as zb
     from paper_2508_21393_b200 import _native as N
@@ -606,7 +668,7 @@ def main():
         prove_step(claims, s, DeviceMatrix, zb.matmul_sumcheck, zb.Transcript)
 
     # ---- device-resident timing (value) ----
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev_id)
     launches0 = lib.zkl_launch_count()
     step_ms = []
     barrier()
@@ -679,6 +741,8 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_value = elems * world / (float(t.item()) / 1000.0 / args.steps)
+
+    strong = run_strong(world, rank) if world > 1 else None
 
     if rank != 0:
         if world > 1:
@@ -786,6 +850,7 @@ def main():
         "cfg4": cfg4,
         "cfg5": cfg5,
         "hbm_kernels": hbm,
+        "strong_scaling": strong,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

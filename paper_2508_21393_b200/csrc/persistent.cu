@@ -1926,7 +1926,7 @@ int op_sumcheck_prove(void* const* tables, int k, int num_vars, const Terms<F>& 
   // would spin on a mailbox the host never answers.
   HostTranscript tr;
   memcpy(tr.state, state, 64);
-  if (no_persistent()) {
+  if (no_persistent() && !profile_replay()) {
     uint64_t size = 1ull << num_vars;
     T r_prev = F::zero();
     for (int j = 0; j < num_vars; j++) {
