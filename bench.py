@@ -804,6 +804,15 @@ def main():
                 extrapolated_seconds_per_proof=lad["fit_intercept_s"] + lad["fit_s_per_elem"] * e3,
                 extrapolated_field_elems_per_s=1.0 / lad["fit_s_per_elem"],
                 note="EXTRAPOLATED to cfg3's 7 x 2^25 claim from the fitted per-element cost")
+            # commitments: outside the optimisation target, timed separately (north star)
+            cm = CR.ref_commit_sample(12)
+            cpu["commitment_reference"] = dict(
+                cm, kind="reference", cores=1,
+                sample="reference Hyrax row-Pedersen commit (commit.py:97-115, real "
+                       "CommitmentKey, 262-bit Schnorr group) of a 2^12-entry table",
+                extrapolated_cfg3_secret_s=cm["s_per_entry"] * (1 << 25),
+                note="not part of any proof-seconds figure here: every GPU proof uses the "
+                     "deterministic stub commitment on both sides (SURVEY.md sec. 8c)")
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -138,3 +138,23 @@ def factored_cpu_cfg2(claims_host):
         zkmat.prove_factored(a.astype(np.int64).reshape(-1), b.astype(np.int64).reshape(-1),
                              c.reshape(-1), dims, fs.FS(b"zklora-b200/cpu", P_BIG, name.encode()))
     return time.perf_counter() - t0
+
+
+def ref_commit_sample(n_log=12, seed=0):
+    """Seconds per committed entry of the reference's Hyrax row-Pedersen
+    commitment (commit.py:97-115: one multi-exponentiation per row in the
+    ~262-bit Schnorr group of group.py:69-76), with a real CommitmentKey.
+    Commitments are outside the optimisation target (BASELINE north star:
+    "timed separately"); this is that timing, on the host."""
+    _zklora()
+    import zklora.commit as C
+    import zklora.group as GR
+
+    group = GR.group_for_modulus(P_BIG)
+    key = C.keygen(n_log, b"zklora-b200/commit-timing", group)
+    rng = np.random.default_rng(seed)
+    table = [int(v) % P_BIG for v in rng.integers(-2 ** 15, 2 ** 15, size=1 << n_log)]
+    t0 = time.perf_counter()
+    C.commit(key, table)
+    sec = time.perf_counter() - t0
+    return {"entries": 1 << n_log, "seconds": sec, "s_per_entry": sec / (1 << n_log)}

@@ -15,6 +15,10 @@
  *   ZKL_ERR_MISSING -> zklora.lookup.ElementNotInTable (lookup.py:94-98)
  * with the FIRST offending index written to the int64 out-parameter.
  *
+ * Threading: the transcript is single-owner.  One host thread
+ * proves on a device at a time: the per-device scratch arenas, mailbox and
+ * the zkMat side stream are shared by the calls on that device.
+ *
  * Each entry point names the reference interface it replaces.
  */
 #ifndef ZKL_B200_H
@@ -147,17 +151,18 @@ int zkl_sumcheck_prove_sharded(int field, void* const* tables, int k, int num_va
 int zkl_shake256(const uint8_t* in, uint64_t len, uint8_t* out, uint64_t outlen);
 int zkl_transcript_append(uint8_t* state_inout, const uint8_t* label, uint64_t label_len,
                           const uint8_t* data, uint64_t data_len);
-int zkl_transcript_challenge(int field, uint8_t* state_inout, const char* label,
-                             uint8_t* out_canon);
+int zkl_transcript_challenge(int field, uint8_t* state_inout, const uint8_t* label,
+                             uint64_t label_len, uint8_t* out_canon);
 /* count appends of canonical little-endian integers (stride bytes each,
  * absorbed in their minimal >= 1-byte encoding) under one label: the
  * reference's per-coordinate / per-value opening records (commit.py:192-195). */
 int zkl_transcript_append_ints(uint8_t* state_inout, const uint8_t* label, uint64_t label_len,
                                const uint8_t* values, uint64_t count, uint64_t stride);
 /* Transcript.challenge_vector (transcript.py:44-45): count challenges under
- * "<label>/<i>", canonical scalars into out_canon. */
-int zkl_transcript_challenge_vector(int field, uint8_t* state_inout, const char* label,
-                                    uint64_t count, uint8_t* out_canon);
+ * "<label>/<i>", canonical scalars into out_canon.  Labels are (pointer,
+ * length): any length, embedded NULs hashed as given. */
+int zkl_transcript_challenge_vector(int field, uint8_t* state_inout, const uint8_t* label,
+                                    uint64_t label_len, uint64_t count, uint8_t* out_canon);
 
 /* After the last round: final_values[j] = fold(tables[j], r_last)[0]
  * (sumcheck.py:129-130), tables of size 2. */

@@ -79,7 +79,7 @@ _SIGS = {
     "zkl_shard_world": ([], ctypes.c_int),
     "zkl_shard_exchange": ([_vp, _u64, _vp], ctypes.c_int),
     "zkl_transcript_append": ([_vp, _u8p, _u64, _u8p, _u64], ctypes.c_int),
-    "zkl_transcript_challenge": ([_i32, _vp, _u8p, _vp], ctypes.c_int),
+    "zkl_transcript_challenge": ([_i32, _vp, _u8p, _u64, _vp], ctypes.c_int),
     "zkl_batch_inverse": ([_i32, _vp, _vp, _u64, _u8p, _i64p, _vp], ctypes.c_int),
     "zkl_multiplicities": ([_i32, _vp, _u64, _vp, _u64, _vp, _i64p, _vp], ctypes.c_int),
     "zkl_matvec": ([_i32, _i32, _vp, _u64, _u64, _i32, _vp, _vp, _vp], ctypes.c_int),
@@ -93,7 +93,8 @@ _SIGS = {
     "zkl_pair_multiplicities": ([_i32, _vp, _i32, _vp, _i32, _u64, ctypes.c_int64, _vp, _vp, _vp,
                                  _u64, _vp, _vp, _i64p, _vp], ctypes.c_int),
     "zkl_transcript_append_ints": ([_vp, ctypes.c_char_p, _u64, _vp, _u64, _u64], ctypes.c_int),
-    "zkl_transcript_challenge_vector": ([_i32, _vp, ctypes.c_char_p, _u64, _vp], ctypes.c_int),
+    "zkl_transcript_challenge_vector": ([_i32, _vp, ctypes.c_char_p, _u64, _u64, _vp],
+                                        ctypes.c_int),
     "zkl_rescale_witness": ([_vp, _i32, _u64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                              ctypes.c_int64, _vp, _vp, _i64p,
                              ctypes.POINTER(ctypes.c_uint64), _vp], ctypes.c_int),

@@ -113,10 +113,12 @@ int sumcheck_prove_sharded(void* const* tables, int k, int num_vars, int degree,
 }
 
 template <class F>
-int transcript_challenge(uint8_t* state, const char* label, uint8_t* out) {
+int transcript_challenge(uint8_t* state, const char* label, size_t llen, uint8_t* out) {
   HostTranscript tr;
   memcpy(tr.state, state, 64);
-  challenge_canon<F>(tr, label, out);
+  uint8_t raw[64];
+  tr.challenge_raw(label, llen, raw);
+  reduce512<F>(raw, out);
   memcpy(state, tr.state, 64);
   return kOk;
 }
@@ -266,9 +268,10 @@ int zkl_transcript_append(uint8_t* state_inout, const uint8_t* label, uint64_t l
   memcpy(state_inout, tr.state, 64);
   return kOk;
 }
-int zkl_transcript_challenge(int field, uint8_t* state_inout, const char* label,
-                             uint8_t* out_canon) {
-  D(field, transcript_challenge<F>(state_inout, label, out_canon));
+int zkl_transcript_challenge(int field, uint8_t* state_inout, const uint8_t* label,
+                             uint64_t label_len, uint8_t* out_canon) {
+  D(field, transcript_challenge<F>(state_inout, (const char*)label, (size_t)label_len,
+                                   out_canon));
 }
 int zkl_transcript_append_ints(uint8_t* state_inout, const uint8_t* label, uint64_t label_len,
                                const uint8_t* values, uint64_t count, uint64_t stride) {
@@ -287,17 +290,18 @@ int zkl_transcript_append_ints(uint8_t* state_inout, const uint8_t* label, uint6
   memcpy(state_inout, tr.state, 64);
   return kOk;
 }
-int zkl_transcript_challenge_vector(int field, uint8_t* state_inout, const char* label,
-                                    uint64_t count, uint8_t* out_canon) {
+int zkl_transcript_challenge_vector(int field, uint8_t* state_inout, const uint8_t* label,
+                                    uint64_t label_len, uint64_t count, uint8_t* out_canon) {
+  // label bytes as given (any length, NULs included) + "/<i>"
   const size_t nb = field == ZKL_FIELD_M61 ? 8 : 32;
-  char buf[512];
+  std::vector<uint8_t> buf(label, label + label_len);
   for (uint64_t i = 0; i < count; i++) {
-    const int w = snprintf(buf, sizeof(buf), "%s/%llu", label, (unsigned long long)i);
-    if (w < 0 || (size_t)w >= sizeof(buf)) {
-      set_error("transcript_challenge_vector: label too long");
-      return kErrArg;
-    }
-    const int rc = zkl_transcript_challenge(field, state_inout, buf, out_canon + i * nb);
+    char num[24];
+    const int w = snprintf(num, sizeof(num), "/%llu", (unsigned long long)i);
+    buf.resize(label_len);
+    buf.insert(buf.end(), num, num + w);
+    const int rc = zkl_transcript_challenge(field, state_inout, buf.data(), buf.size(),
+                                            out_canon + i * nb);
     if (rc) return rc;
   }
   return kOk;

@@ -762,8 +762,13 @@ __global__ void k_dot_partial(typename F::T* part, const typename F::T* a,
   block_sum<F, 1>(acc, sm);
   if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
 }
-static std::map<int, void*>& dot_partials() {  // per device, main-stream use
-  static std::map<int, void*> m;
+// partial sums of the grid-wide dot, one buffer per (device, stream): two
+// streams running dots concurrently (the zkMat side stream, callers on other
+// torch streams) must not share it.  Not the scratch arena, whose current
+// reservation may hold the caller's output.
+static std::mutex g_dot_mu;
+static std::map<std::pair<int, cudaStream_t>, void*>& dot_partials() {
+  static std::map<std::pair<int, cudaStream_t>, void*> m;
   return m;
 }
 template <class F>
@@ -777,8 +782,13 @@ int op_dot(typename F::T* out_dev, const void* a, const void* b, uint64_t n, cud
   }
   int dev = 0;
   cudaGetDevice(&dev);
-  void*& part = dot_partials()[dev];
-  if (!part) ZKL_CUDA(cudaMalloc(&part, kMaxParts * 32));
+  void* part;
+  {
+    std::lock_guard<std::mutex> lk(g_dot_mu);
+    void*& slot = dot_partials()[{dev, s}];
+    if (!slot) ZKL_CUDA(cudaMalloc(&slot, kMaxParts * 32));
+    part = slot;
+  }
   unsigned g = (unsigned)((n + 255) / 256);
   if (g > kMaxParts) g = kMaxParts;
   k_dot_partial<F><<<g, 256, 0, s>>>((T*)part, (const T*)a, (const T*)b, n);

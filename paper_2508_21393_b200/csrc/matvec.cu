@@ -238,6 +238,25 @@ __global__ void __launch_bounds__(256)
   P::init(acc);
   const MT* row = M + r * cols;
   uint64_t c = c0;
+  // U vector loads issued before their multiply-adds: a thread per row walks
+  // its own row, so memory-level parallelism comes from loads in flight per
+  // thread (ncu: long-scoreboard stalls dominated the one-load-at-a-time loop)
+  constexpr int U = VEC == 1 ? 8 : 4;
+  for (; c + U * VEC <= c1; c += U * VEC) {
+    MT v[U][VEC];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      if constexpr (VEC == 1)
+        v[u][0] = row[c + u];
+      else
+        load_vec<MT, VEC>(row + c + u * VEC, v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++)
+#pragma unroll
+      for (int k = 0; k < VEC; k++)
+        P::mac(acc, v[u][k], xp + (c - c0) + u * VEC + k, xn + (c - c0) + u * VEC + k);
+  }
   for (; c + VEC <= c1; c += VEC) {
     MT v[VEC];
     if constexpr (VEC == 1)
@@ -271,8 +290,19 @@ __global__ void __launch_bounds__(256)
   const uint64_t c = blockIdx.x * (uint64_t)cw + tc;
   typename P::Acc acc;
   P::init(acc);
-  if (c < cols)
-    for (uint64_t r = r0 + rg; r < r1; r += ngrp) P::mac(acc, M[r * cols + c], xp + (r - r0), xn + (r - r0));
+  if (c < cols) {
+    // four rows' loads in flight before their multiply-adds (see k_mv_rows)
+    uint64_t r = r0 + rg;
+    for (; r + 3 * ngrp < r1; r += 4 * ngrp) {
+      MT v[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) v[u] = M[(r + u * ngrp) * cols + c];
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        P::mac(acc, v[u], xp + (r + u * ngrp - r0), xn + (r + u * ngrp - r0));
+    }
+    for (; r < r1; r += ngrp) P::mac(acc, M[r * cols + c], xp + (r - r0), xn + (r - r0));
+  }
   if (ngrp == 1) {
     if (c < cols) part[blockIdx.y * cols + c] = P::done(acc);
     return;

@@ -174,9 +174,17 @@ ZKL_D typename F::T pick3(const typename F::T& lo, const typename F::T& hi, int 
 
 // ---------------------------------------------------------------------------
 // evaluators: pair() accumulates NA field sums, finish() -> NOUT raw outputs
+// minimum resident blocks per SM for the grid kernel of the dense
+// evaluators (__launch_bounds__): 1 lets ptxas use 255 registers per thread
+// (8 warps / SM), 2 caps it at 128 (16 warps / SM, more latency hiding for
+// the Montgomery chains, some spilling); measured in DESIGN.md sec. 4e
+#ifndef ZKL_DENSE_MINB
+#define ZKL_DENSE_MINB 1
+#endif
 template <class F, int MAXK>
 struct EvGeneric {
   using T = typename F::T;
+  static constexpr int kMinBlocks = ZKL_DENSE_MINB;
   static constexpr bool kGeneric = true;
   static constexpr int NA = 4, NOUT = 4;
   ZKL_D static void pair(T (&cur)[MAXK], const T (&df)[MAXK], int k, const Terms<F>& tm,
@@ -202,6 +210,7 @@ struct EvGeneric {
 template <class F, int MAXK>
 struct EvProd2 {
   using T = typename F::T;
+  static constexpr int kMinBlocks = ZKL_DENSE_MINB;
   static constexpr bool kGeneric = false;
   static constexpr int NA = 3, NOUT = 3;
   ZKL_D static void pair(T (&cur)[MAXK], const T (&df)[MAXK], int, const Terms<F>& tm,
@@ -233,6 +242,7 @@ struct EvProd2 {
 template <class F, int MAXK>
 struct EvSum2Prod2 {
   using T = typename F::T;
+  static constexpr int kMinBlocks = ZKL_DENSE_MINB;
   static constexpr bool kGeneric = false;
   static constexpr int NA = 6, NOUT = 6;
   ZKL_D static void pair(T (&cur)[MAXK], const T (&df)[MAXK], int, const Terms<F>& tm,
@@ -279,6 +289,7 @@ ZKL_D void quad_evals(const typename F::T& c0, const typename F::T& c1, const ty
 template <class F, int MAXK>
 struct EvProd3 {
   using T = typename F::T;
+  static constexpr int kMinBlocks = ZKL_DENSE_MINB;
   static constexpr bool kGeneric = false;
   static constexpr int NA = 4, NOUT = 4;
   ZKL_D static void pair(T (&cur)[MAXK], const T (&df)[MAXK], int, const Terms<F>& tm,
@@ -335,6 +346,7 @@ struct EvProd3 {
 template <class F, int MAXK>
 struct EvZkMat {
   using T = typename F::T;
+  static constexpr int kMinBlocks = ZKL_DENSE_MINB;
   static constexpr bool kGeneric = false;
   static constexpr int NA = 7, NOUT = 7;
   ZKL_D static void pair(T (&cur)[MAXK], const T (&df)[MAXK], int, const Terms<F>& tm,
@@ -407,6 +419,7 @@ struct EvZkMat {
 template <class F, int MAXK>
 struct EvLogup {
   using T = typename F::T;
+  static constexpr int kMinBlocks = ZKL_DENSE_MINB;
   static constexpr bool kGeneric = false;
   static constexpr int NA = 16, NOUT = 16;
   struct Idx {

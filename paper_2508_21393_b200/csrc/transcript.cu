@@ -1,4 +1,5 @@
 // Host SHAKE-256 / Keccak-f[1600] (FIPS 202) and the transcript operations.
+#include <vector>
 #include "transcript.cuh"
 #include "hostfield.h"
 
@@ -114,8 +115,14 @@ void HostTranscript::challenge_raw(const char* label, size_t llen, uint8_t raw[6
 }
 
 void HostTranscript::challenge_squeeze(const char* label, size_t llen, uint8_t raw[64]) {
-  // raw = H(state || record("challenge", label))
-  uint8_t buf[64 + 2 + 9 + 8 + 256];
+  // raw = H(state || record("challenge", label)); long labels on the heap
+  uint8_t small[64 + 2 + 9 + 8 + 256];
+  std::vector<uint8_t> big;
+  uint8_t* buf = small;
+  if (llen > 256) {
+    big.resize(64 + 2 + 9 + 8 + llen);
+    buf = big.data();
+  }
   uint8_t* w = buf;
   memcpy(w, state, 64); w += 64;
   w[0] = 9; w[1] = 0; w += 2;

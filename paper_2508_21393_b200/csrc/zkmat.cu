@@ -130,7 +130,10 @@ int op_matmul_prove(int ta, const void* A, int tb, const void* B, int tc, const 
   uint64_t off[NBUF + 1];
   off[0] = 0;
   for (int i = 0; i < NBUF; i++) off[i + 1] = off[i] + ((sizes[i] + 3) & ~3ull);
-  // cv shares the buffer of EU until E_u is built (h = abv - cv consumes it)
+  // every vector has its own slot (cv included: the side stream writes EU and
+  // CV concurrently).  The side stream, its events and the side scratch arena
+  // are per device, so matmul_prove is single-threaded per device: one host
+  // thread proves on a device at a time (include/zkl_b200.h, threading).
   void* wsv;
   int rc = work_reserve(off[NBUF] * sizeof(T) + 64, &wsv, s);
   if (rc) return rc;

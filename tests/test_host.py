@@ -104,7 +104,7 @@ def test_native_transcript_matches_python(field):
             lib.zkl_transcript_append(st, label, len(label), data, len(data))
         else:
             out = (ctypes.c_uint8 * nb)()
-            lib.zkl_transcript_challenge(0 if field == "big" else 1, st, label, out)
+            lib.zkl_transcript_challenge(0 if field == "big" else 1, st, label, len(label), out)
             assert int.from_bytes(bytes(out), "little") == py.challenge(label)
         assert st.raw[:64] == py.state
 
@@ -409,3 +409,18 @@ def test_block_witness_raises_instead_of_clipping():
         BK._divmod(wide, fp.zeta, fp)
     q, r = BK._divmod(wide[:, :2], fp.zeta, fp)
     assert q.tolist() == [[0, 5]] and r.tolist() == [[0, 0]]
+
+
+@pytest.mark.parametrize("p", [P_BIG, P_TEST])
+def test_native_challenge_vector_long_and_nul_labels(p):
+    """zkl_transcript_challenge_vector takes the label as (pointer, length):
+    a 480-byte label (past the old 256-byte stack buffer) and a label with an
+    embedded NUL hash exactly as hashlib does (transcript.py:38-45)."""
+    from oracle import fs
+
+    for label in (b"L" * 480, b"lookup\x00/u", b"x" * 300 + b"\x00" + b"y" * 5):
+        t1 = Transcript(b"long", p, b"s")
+        t2 = fs.FS(b"long", p, b"s")
+        got = t1.challenge_vector(label, 6)
+        want = [t2.challenge(label + b"/%d" % i) for i in range(6)]
+        assert got == want and t1.state == t2.state
