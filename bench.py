@@ -705,6 +705,18 @@ def main():
     except OSError:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    # DRAM bytes per matvec launch from the committed ncu capture
+    # (profiles/r02/matvec_traffic.json, dram__bytes_read.sum + write.sum)
+    traffic = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "matvec_traffic.json")) as fh:
+            t = json.load(fh)
+        traffic = {"traffic_bytes_per_launch": t["traffic_bytes_per_launch"],
+                   "note": "ncu DRAM bytes per launch over one step's captured X.W / dY.W^T "
+                           "matvec launches = %.2f x their algorithmic bytes (%s)"
+                           % (t["traffic_over_algorithmic"], "profiles/r02/matvec_traffic.json")}
+    except (OSError, KeyError, ValueError):
+        pass
     mv_avg_ms = mv_ms / max(mv_n, 1)
     achieved = (mv_bytes / max(mv_n, 1)) / (mv_avg_ms / 1000.0) / 1e9 if mv_avg_ms else 0.0
     mac_rate = mv_macs / (mv_ms / 1000.0) if mv_ms else 0.0
@@ -829,7 +841,8 @@ def main():
         "roofline": {"kernel": "zkl_matvec (int16/int64 matrix x Fr vector MLE partial "
                                "evaluations; one launch group = products + chunk reduction)",
                      "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None,
+                     "frac": achieved / hbm_peak, "traffic": traffic.get("traffic_bytes_per_launch"),
+                     "traffic_note": traffic.get("note"),
                      "launches_per_step": mv_n // args.steps,
                      "gpu_ms_per_step": mv_ms / args.steps,
                      "share_of_step": (mv_ms / args.steps) / ms_per_step,
