@@ -1560,7 +1560,7 @@ static bool profile_replay() {
 template <class F>
 int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t* point_out,
               typename F::T* finals_out, cudaStream_t s) {
-  if (profile_replay() && !a.replaying && a.rounds_limit <= 0)
+  if (profile_replay() && !a.replaying && !a.sharded && a.rounds_limit <= 0)
     return run_phase_replay<F>(a, tr, rounds_out, point_out, finals_out, s);
   using T = typename F::T;
   using H = typename host::For<F>::H;
@@ -1718,6 +1718,28 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
     }
     T raw[kMbMaxOut];
     for (int q = 0; q < nout; q++) raw[q] = HostRed<F>::reduce(words + q * NW);
+    if (a.sharded) {
+      // every rank's raw sums (storage form) through the shared-memory
+      // all-gather; the host finishing below is linear in them
+      const int G = shard_world();
+      std::vector<uint8_t> all((size_t)G * nout * sizeof(T));
+      rc = shard_exchange(raw, (size_t)nout * sizeof(T), all.data());
+      if (rc) {
+        mb_host->abort = 1;
+        cudaStreamSynchronize(s);
+        g_phase_dirty = true;
+        return rc;
+      }
+      for (int q = 0; q < nout; q++) {
+        T acc = H::zero();
+        for (int g = 0; g < G; g++) {
+          T v;
+          memcpy(&v, all.data() + ((size_t)g * nout + q) * sizeof(T), sizeof(T));
+          acc = H::add(acc, v);
+        }
+        raw[q] = acc;
+      }
+    }
     T ev[4];
     if (shape == kLogupTiled) {
       // EvLogupTiled: raw = [P0, P1, P2, sum a0, sum ad] (storage form)

@@ -52,6 +52,9 @@ struct PhaseArgs {
   // ZKL_PROFILE_REPLAY: second run of the phase on recorded challenges
   bool replaying = false;
   const void* replay_words = nullptr;
+  // multi-GPU (csrc/shard.cu): the tables are this rank's shard; every
+  // round's raw sums are added across the ranks before the host finishes them
+  bool sharded = false;
 };
 
 // true when the persistent (mailbox) kernels must not be used: ZKL_NO_PERSISTENT,

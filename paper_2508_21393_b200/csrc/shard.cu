@@ -40,6 +40,7 @@
 #include "field.cuh"
 #include "hostfield.h"
 #include "ops.cuh"
+#include "phase.cuh"
 #include "transcript.cuh"
 
 namespace zkl {
@@ -153,14 +154,36 @@ int op_sumcheck_prove_sharded(void* const* tables, int k, int num_vars, const Te
     challenge_canon<F>(tr, "sumcheck/round", point_out + (size_t)j * nb);
     return host::from_canon<F>(point_out + (size_t)j * nb);
   };
-  // local rounds: raw evaluations (no post scalars) summed over the ranks
+  // local rounds: raw evaluations (no post scalars) summed over the ranks.
+  // With the persistent engine (each rank on its own GPU) the exchange runs
+  // inside run_phase's host loop while the rank's kernel waits for its
+  // challenge; without it (ZKL_NO_PERSISTENT, profilers, ranks sharing a GPU)
+  // every round is one fold + evaluation launch.
   std::vector<uint8_t> mine(4 * nb), all((size_t)G * 4 * nb);
+  std::vector<uint8_t> fin((size_t)k * nb), allf((size_t)G * k * nb);
   Post<F> raw_post;
   raw_post.add = F::zero();
   raw_post.mul = H::one();
   uint64_t size = 1ull << nl;
   T r = F::zero();
-  for (int j = 0; j < nl; j++) {
+  bool have_fin = false;
+  if (nl > 0 && !no_persistent()) {
+    PhaseArgs<F> a;
+    a.tables = tables;
+    a.k = k;
+    a.num_vars = nl;
+    a.tm = tm;
+    a.post_add = post_add;  // global round j = local round j for the first nl rounds
+    a.post_mul = post_mul;
+    a.sharded = true;
+    std::vector<T> lf(k);
+    int rc = run_phase<F>(a, tr, rounds_out, point_out, lf.data(), s);
+    if (rc) return rc;
+    for (int q = 0; q < k; q++) host::to_canon<F>(fin.data() + (size_t)q * nb, lf[q]);
+    r = host::from_canon<F>(point_out + (size_t)(nl - 1) * nb);
+    have_fin = true;
+  }
+  for (int j = 0; j < nl && !have_fin; j++) {
     int rc = op_sumcheck_round<F>(tables, k, size, j > 0, r, tm, raw_post, mine.data(), s);
     if (rc) return rc;
     if (j > 0) size >>= 1;
@@ -175,8 +198,8 @@ int op_sumcheck_prove_sharded(void* const* tables, int k, int num_vars, const Te
     r = emit(j, ev);
   }
   // every rank's one entry per table (folded by the last local challenge)
-  std::vector<uint8_t> fin((size_t)k * nb), allf((size_t)G * k * nb);
-  if (nl > 0) {
+  if (have_fin) {
+  } else if (nl > 0) {
     int rc = op_sumcheck_finish<F>(tables, k, r, fin.data(), s);
     if (rc) return rc;
   } else {

@@ -17,6 +17,7 @@ from dataclasses import dataclass
 
 from . import _native as N
 from . import device as D
+from . import shard
 from .field import batch_inverse_device, inverse_pow2
 from .commit_stub import attach
 from .gadgets import commit_backend
@@ -374,6 +375,21 @@ def prove_lookup(secret, multiplicities, table, key, tr, rng, secret_index=None)
     claimed = alpha * alpha % p
     tuples = [(t.coefficient, t.factors) for t in terms]
 
+    # multi-GPU (shard.py): with >= SHARD_LOOKUP_MIN_WORLD ranks every rank
+    # materialises its cyclic shard of the seven Eq.-7 columns (1/G of the
+    # replicated claim) and runs the dense logUp evaluator on it; below that
+    # the single-GPU tiled path does less work than a shard of the dense claim
+    g = shard.active()
+    if (stub and g is not None and g.world >= shard.SHARD_LOOKUP_MIN_WORLD and d >= n >= g.world
+            and shard.wants(num_vars) and native_transcript(tr, spec)):
+        rounds, point, finals = _sharded_claim(spec, tr, g, d, n, s_buf, inv_s, t_buf, inv_t,
+                                               m_buf, beta, u, terms, tuples, claimed, num_vars,
+                                               secret_index, entries)
+        return _finish_lookup(spec, p, key, be, stub, tr, rng, secret, table, multiplicities,
+                              entries, beta, retries, m_commitment, a_commitment, b_commitment,
+                              m_blinding, m_rows, a_blinding, inv_s, inv_s_host, inv_t_host,
+                              s_buf, num_vars, rounds, point, finals, d, n)
+
     # secret larger than the table: the replicated table side (lookup.py:196-202)
     # is never materialised -- tiled rounds first, then 7 tables of n entries
     if d > n > 1 and TILED and native_transcript(tr, spec):
@@ -419,6 +435,36 @@ def prove_lookup(secret, multiplicities, table, key, tr, rng, secret_index=None)
 
 
 TILED = True  # tests flip this to compare with the fully materialised claim
+
+
+def _sharded_claim(spec, tr, g, d, n, s_buf, inv_s, t_buf, inv_t, m_buf, beta, u, terms,
+                   tuples, claimed, num_vars, secret_index, entries):
+    """This rank's cyclic shard (global entries i = i' G + rank) of the Eq.-7
+    claim's seven columns for d >= n (lookup.py:196-202: the table side
+    replicated d / n times), proven through the sharded engine.  Global entry
+    i's table index is i mod n, which is congruent to the rank mod G, so the
+    replicated table columns are the table's own cyclic shard, tiled."""
+    G, rk = g.world, g.rank
+    W = spec.words
+    dl, nl = d // G, n // G
+    E = shard.eq_shard(u, spec, rk, G)
+    Tb_full = _expand(spec, n, t_buf, n, 1, add=beta)
+    if secret_index is not None:  # every s_i is the table entry at its index
+        idx = secret_index[:d][rk::G].contiguous()
+        A = _gather(spec, inv_t, n, idx, dl)
+        Sb = _gather(spec, Tb_full, n, idx, dl)
+    else:
+        sb = s_buf if s_buf is not None else D.field_buffer(entries, spec)
+        A = inv_s.view(-1, W)[:d][rk::G].contiguous()
+        Sb = _expand(spec, dl, sb.view(-1, W)[:d][rk::G].contiguous(), dl, 1, add=beta)
+    ind = _expand(spec, dl, None, dl, 0, add=1, pad=0)
+
+    def tiled(col):
+        return _expand(spec, dl, col.view(-1, W)[:n][rk::G].contiguous(), nl, 1)
+
+    Bt, Tb, Mt = tiled(inv_t), tiled(Tb_full), tiled(m_buf)
+    absorb_claim(tr, claimed, terms, 3, num_vars)
+    return shard.run_rounds_sharded(spec, [E, A, Sb, ind, Bt, Tb, Mt], num_vars, tuples, 3, tr)
 
 
 def _tiled_sumcheck(spec, tr, d, n, s_buf, inv_s, t_buf, inv_t, m_buf, beta, u, terms, tuples,

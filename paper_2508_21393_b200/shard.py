@@ -20,9 +20,12 @@ Which provers shard (when a group is active and the claim is large):
   matmul_sumcheck_replicated (the reference's dense zkMat claim,
   gadgets.py:210-251; the cfg5 sweep): the replicated tables' shards, built
   from column slices of B and C (the low index bits are v's).
-The tiled logUp claims (lookup.py:143-251 with d > n) are not sharded: their
-first rounds bind the query index's high bits through the eq-factored
-evaluator, which would need the rank's k offset inside the kernel.
+  prove_lookup (lookup.py:143-251, d >= n) from SHARD_LOOKUP_MIN_WORLD ranks:
+  each rank materialises its shard of the seven Eq.-7 columns (the secret
+  side gathered through the multiplicity index, the replicated table side
+  as the table's own cyclic shard, tiled) and runs the dense evaluator.
+Below that world size the single-GPU tiled logUp (eq-factored, table side
+never replicated) does less work than a shard of the dense claim.
 """
 
 import ctypes
@@ -33,6 +36,10 @@ from . import _native as N
 from . import device as D
 
 SHARD_MIN_VARS = 22  # below this a claim is latency-bound: one GPU proves it
+# logUp with d >= n: a rank's shard of the dense 7-column claim costs ~20/G
+# Montgomery products per query against ~8 on one GPU's tiled path (DESIGN.md
+# sec. 4b), so lookups shard from 4 ranks up
+SHARD_LOOKUP_MIN_WORLD = 4
 
 _ACTIVE = None
 
