@@ -1479,7 +1479,11 @@ static bool g_phase_dirty = true;  // after a failure the ticket / flags need a 
 
 bool no_persistent() {
   // ncu marks its target with NV_NSIGHT_INJECTION_* / NV_TPS_LAUNCH_TOKEN;
-  // compute-sanitizer and other injectors use CUDA_INJECTION64_PATH
+  // compute-sanitizer and other injectors use CUDA_INJECTION64_PATH.
+  // ZKL_FORCE_PERSISTENT=1 keeps the persistent engine under an injector that
+  // does not replay kernels (compute-sanitizer memcheck / racecheck: the host
+  // still answers every round, just slowly)
+  if (getenv("ZKL_FORCE_PERSISTENT") != nullptr) return false;
   static const bool v =
       getenv("ZKL_NO_PERSISTENT") != nullptr || getenv("CUDA_INJECTION64_PATH") != nullptr ||
       getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr ||
