@@ -135,6 +135,13 @@ int zkl_sumcheck_prove(int field, void* const* tables, int k, int num_vars, int 
  * rank returns the same rounds, point, finals and end state as the unsharded
  * prover (replaces prove_sumcheck, sumcheck.py:98-130, for one shard).
  * zkl_shard_exchange: all-gather of nbytes per rank (out: world * nbytes). */
+/* Exact C = A B for row-major int16 A (M x K), B (K x N) into int64 C
+ * (M x N), on the tensor cores (byte-sliced mma.sync s8/u8): the wide
+ * products of the LoRA-block witness (model.py:479-487 computes them with a
+ * Python triple loop).  Any shape; K unbounded (int64 accumulation). */
+int zkl_igemm_i16(const int16_t* A, const int16_t* B, int64_t* C, int M, int K, int N,
+                  void* stream);
+
 int zkl_shard_open(const char* name, int rank, int world);
 int zkl_shard_close(void);
 int zkl_shard_world(void);

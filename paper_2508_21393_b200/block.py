@@ -68,6 +68,7 @@ import torch
 
 from . import tables as TBL
 from .commit_stub import StubCommitment, StubKey, attach
+from .device import igemm16
 from .gadgets import (DeviceMatrix, ProverTensor, TensorRef, prove_elementprod, prove_matadd,
                       prove_matmul, prove_pair_lookup)
 from .nonlinear import (RangeViolation, TableSet, device_pair_table, device_range_table,
@@ -179,7 +180,12 @@ def _q16(rng, shape, std, rows, cols, scale, device):
 
 
 def _mm(a, b):
-    """Exact int64 a @ b of integer matrices (float64 GEMM; |sums| < 2^53)."""
+    """Exact int64 a @ b of integer matrices: int16 x int16 on the GPU through
+    the byte-sliced tensor-core GEMM (device.igemm16); the ones-vector row sums
+    and broadcasts (int32 / int64 operands) and CPU tensors through a float64
+    GEMM, exact because every partial sum stays below 2^53 (checked)."""
+    if a.is_cuda and a.dtype == torch.int16 and b.dtype == torch.int16:
+        return igemm16(a, b)
     out = torch.matmul(a.double(), b.double())
     assert float(out.abs().max()) < 2.0 ** 52 if out.numel() else True
     return out.round_().long()

@@ -256,6 +256,10 @@ int zkl_sumcheck_prove_sharded(int field, void* const* tables, int k, int num_va
                                      coeffs_canon, post_add_canon, post_mul_canon, state_inout,
                                      rounds_out, point_out, finals_out, (cudaStream_t)stream));
 }
+int zkl_igemm_i16(const int16_t* A, const int16_t* B, int64_t* C, int M, int K, int N,
+                  void* stream) {
+  return op_igemm16(A, B, C, M, K, N, (cudaStream_t)stream);
+}
 int zkl_shake256(const uint8_t* in, uint64_t len, uint8_t* out, uint64_t outlen) {
   shake256(in, (size_t)len, out, (size_t)outlen);
   return kOk;

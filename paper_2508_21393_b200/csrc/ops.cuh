@@ -76,6 +76,8 @@ int op_sumcheck_prove_sharded(void* const* tables, int k, int num_vars, const Te
                       const typename F::T* post_add, const typename F::T& post_mul,
                       uint8_t* state, uint8_t* rounds_out, uint8_t* point_out,
                       uint8_t* finals_out, cudaStream_t s);
+int op_igemm16(const int16_t* A, const int16_t* B, int64_t* C, int M, int K, int N,
+               cudaStream_t s);
 int shard_world();
 int shard_rank();
 int shard_exchange(const void* mine, size_t nbytes, uint8_t* out);
