@@ -23,10 +23,10 @@ namespace zkl {
 
 namespace {
 
-constexpr int kTM = 128, kTN = 64, kTK = 32;
+constexpr int kTM = 128, kTN = 64, kTK = 64;
 constexpr int kKChunk = 1 << 14;
-constexpr int kAPitch = kTK + 8;  // int16 per smem row (16-byte skew)
-constexpr int kBPitch = kTK + 8;
+constexpr int kPitch = kTK + 8;  // int16 per smem row (16-byte skew)
+constexpr int kStage = (kTM + kTN) * kPitch;  // int16 per pipeline stage
 
 ZKL_D void mma_s8s8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -63,15 +63,71 @@ ZKL_D void split4(uint32_t w0, uint32_t w1, uint32_t& hi, uint32_t& lo) {
   lo = __byte_perm(w0, w1, 0x6420);
 }
 
+// one K step's global tile in registers: A 128 x 64 (4 runs of 8 per thread),
+// B 64 x 64 (2 runs of 8 along n per thread); zero outside the matrices
+struct Regs {
+  uint4 a[4];
+  uint4 b[2];
+};
+
+ZKL_D uint4 load8(const int16_t* base, bool full, int row_ok, int avail) {
+  if (full) return *reinterpret_cast<const uint4*>(base);
+  int16_t v[8];
+#pragma unroll
+  for (int t = 0; t < 8; t++) v[t] = (row_ok && t < avail) ? base[t] : (int16_t)0;
+  return *reinterpret_cast<uint4*>(v);
+}
+
+ZKL_D void fetch(Regs& R, const int16_t* A, const int16_t* B, int M, int K, int N, int m0, int n0,
+                 int k0, int kend, int tid, bool a_al, bool b_al) {
+#pragma unroll
+  for (int rep = 0; rep < 4; rep++) {
+    const int e = tid + rep * 256;  // 1024 runs of 8: row e / 8, k 8 (e % 8)
+    const int r = e >> 3, c8 = (e & 7) * 8;
+    const int gr = m0 + r, gc = k0 + c8;
+    const int avail = kend - gc;
+    R.a[rep] = load8(A + (size_t)(gr < M ? gr : 0) * K + (gc < kend ? gc : 0),
+                     a_al && gr < M && avail >= 8, gr < M, avail);
+  }
+#pragma unroll
+  for (int rep = 0; rep < 2; rep++) {
+    const int e = tid + rep * 256;  // 512 runs of 8 along n: k row e / 8
+    const int r = e >> 3, c8 = (e & 7) * 8;
+    const int gr = k0 + r, gc = n0 + c8;
+    const int avail = N - gc;
+    R.b[rep] = load8(B + (size_t)(gr < kend ? gr : 0) * N + (gc < N ? gc : 0),
+                     b_al && gr < kend && avail >= 8, gr < kend, avail);
+  }
+}
+
+ZKL_D void stash(const Regs& R, int16_t* st, int tid) {
+  int16_t* sa = st;
+  int16_t* sb = st + kTM * kPitch;  // transposed: [n][k]
+#pragma unroll
+  for (int rep = 0; rep < 4; rep++) {
+    const int e = tid + rep * 256;
+    *reinterpret_cast<uint4*>(sa + (e >> 3) * kPitch + (e & 7) * 8) = R.a[rep];
+  }
+#pragma unroll
+  for (int rep = 0; rep < 2; rep++) {
+    const int e = tid + rep * 256;
+    const int r = e >> 3, c8 = (e & 7) * 8;
+    const int16_t* v = reinterpret_cast<const int16_t*>(&R.b[rep]);
+#pragma unroll
+    for (int t = 0; t < 8; t++) sb[(c8 + t) * kPitch + r] = v[t];
+  }
+}
+
 __global__ void __launch_bounds__(256)
     k_igemm16(const int16_t* __restrict__ A, const int16_t* __restrict__ B,
               int64_t* __restrict__ C, int M, int K, int N) {
-  __shared__ __align__(16) int16_t sa[kTM * kAPitch];
-  __shared__ __align__(16) int16_t sb[kTN * kBPitch];  // transposed: [n][k]
+  extern __shared__ __align__(16) int16_t smem[];  // 2 stages
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tig = lane & 3;
   const int wm = warp & 3, wn = warp >> 2;  // warp tile origin (wm * 32, wn * 32)
   const int m0 = blockIdx.y * kTM, n0 = blockIdx.x * kTN;
+  const bool a_al = (K & 7) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0;
+  const bool b_al = (N & 7) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0;
   long long tot[2][4][4];
 #pragma unroll
   for (int i = 0; i < 2; i++)
@@ -88,70 +144,53 @@ __global__ void __launch_bounds__(256)
       for (int j = 0; j < 4; j++)
 #pragma unroll
         for (int q = 0; q < 4; q++) hh[i][j][q] = mx[i][j][q] = ll[i][j][q] = 0;
+    // software pipeline: the next step's tile is in registers while this
+    // step's (in shared memory) feeds the MMAs; two shared stages
+    Regs R;
+    fetch(R, A, B, M, K, N, m0, n0, kc, kend, tid, a_al, b_al);
+    stash(R, smem, tid);
+    __syncthreads();
+    int stage = 0;
     for (int k0 = kc; k0 < kend; k0 += kTK) {
-      // stage A (128 x 32): each thread two rows' 8-entry runs
+      const bool more = k0 + kTK < kend;
+      if (more) fetch(R, A, B, M, K, N, m0, n0, k0 + kTK, kend, tid, a_al, b_al);
+      const int16_t* sa = smem + stage * kStage;
+      const int16_t* sb = sa + kTM * kPitch;
 #pragma unroll
-      for (int rep = 0; rep < 2; rep++) {
-        const int e = tid + rep * 256;  // 512 runs of 8
-        const int r = e >> 2, c8 = (e & 3) * 8;
-        const int gr = m0 + r, gc = k0 + c8;
-        int16_t v[8];
-        if (gr < M && gc + 8 <= kend && ((reinterpret_cast<uintptr_t>(A + (size_t)gr * K + gc) & 15) == 0)) {
-          *reinterpret_cast<uint4*>(v) = *reinterpret_cast<const uint4*>(A + (size_t)gr * K + gc);
-        } else {
+      for (int ks = 0; ks < kTK; ks += 32) {
+        uint32_t ahi[2][4], alo[2][4];
 #pragma unroll
-          for (int t = 0; t < 8; t++)
-            v[t] = (gr < M && gc + t < kend) ? A[(size_t)gr * K + gc + t] : (int16_t)0;
-        }
-        *reinterpret_cast<uint4*>(sa + r * kAPitch + c8) = *reinterpret_cast<uint4*>(v);
-      }
-      // stage B (32 x 64) transposed into sb[n][k]
-      {
-        const int r = tid >> 3, c8 = (tid & 7) * 8;  // 256 runs of 8 along n
-        const int gr = k0 + r, gc = n0 + c8;
-        int16_t v[8];
-        if (gr < kend && gc + 8 <= N && ((reinterpret_cast<uintptr_t>(B + (size_t)gr * N + gc) & 15) == 0)) {
-          *reinterpret_cast<uint4*>(v) = *reinterpret_cast<const uint4*>(B + (size_t)gr * N + gc);
-        } else {
+        for (int i = 0; i < 2; i++) {
+          const int rb = wm * 32 + i * 16;
 #pragma unroll
-          for (int t = 0; t < 8; t++)
-            v[t] = (gr < kend && gc + t < N) ? B[(size_t)gr * N + gc + t] : (int16_t)0;
+          for (int h = 0; h < 2; h++)
+#pragma unroll
+            for (int rr = 0; rr < 2; rr++) {
+              const int16_t* p = sa + (rb + g + 8 * rr) * kPitch + ks + 16 * h + 4 * tig;
+              const uint2 w = *reinterpret_cast<const uint2*>(p);
+              split4(w.x, w.y, ahi[i][2 * h + rr], alo[i][2 * h + rr]);
+            }
         }
 #pragma unroll
-        for (int t = 0; t < 8; t++) sb[(c8 + t) * kBPitch + r] = v[t];
-      }
-      __syncthreads();
-      // fragments: A rows wm*32 + i*16 + {g, g+8}, k slots 4 tig.. and 16 + 4 tig..
-      uint32_t ahi[2][4], alo[2][4];
+        for (int j = 0; j < 4; j++) {
+          const int16_t* p = sb + (wn * 32 + j * 8 + g) * kPitch + ks + 4 * tig;
+          const uint2 w0 = *reinterpret_cast<const uint2*>(p);
+          const uint2 w1 = *reinterpret_cast<const uint2*>(p + 16);
+          uint32_t bh0, bl0, bh1, bl1;
+          split4(w0.x, w0.y, bh0, bl0);
+          split4(w1.x, w1.y, bh1, bl1);
 #pragma unroll
-      for (int i = 0; i < 2; i++) {
-        const int rb = wm * 32 + i * 16;
-#pragma unroll
-        for (int h = 0; h < 2; h++) {      // k half: 0 -> slots 0..15, 1 -> 16..31
-#pragma unroll
-          for (int rr = 0; rr < 2; rr++) {  // row g / g + 8
-            const int16_t* p = sa + (rb + g + 8 * rr) * kAPitch + 16 * h + 4 * tig;
-            const uint2 w = *reinterpret_cast<const uint2*>(p);
-            split4(w.x, w.y, ahi[i][2 * h + rr], alo[i][2 * h + rr]);
+          for (int i = 0; i < 2; i++) {
+            mma_s8s8(hh[i][j], ahi[i], bh0, bh1);
+            mma_s8u8(mx[i][j], ahi[i], bl0, bl1);
+            mma_u8s8(mx[i][j], alo[i], bh0, bh1);
+            mma_u8u8(ll[i][j], alo[i], bl0, bl1);
           }
         }
       }
-#pragma unroll
-      for (int j = 0; j < 4; j++) {
-        const int cb = wn * 32 + j * 8 + g;  // this thread's B column
-        const int16_t* p = sb + cb * kBPitch + 4 * tig;
-        const uint2 w0 = *reinterpret_cast<const uint2*>(p);
-        const uint2 w1 = *reinterpret_cast<const uint2*>(p + 16);
-        uint32_t bh0, bl0, bh1, bl1;
-        split4(w0.x, w0.y, bh0, bl0);
-        split4(w1.x, w1.y, bh1, bl1);
-#pragma unroll
-        for (int i = 0; i < 2; i++) {
-          mma_s8s8(hh[i][j], ahi[i], bh0, bh1);
-          mma_s8u8(mx[i][j], ahi[i], bl0, bl1);
-          mma_u8s8(mx[i][j], alo[i], bh0, bh1);
-          mma_u8u8(ll[i][j], alo[i], bl0, bl1);
-        }
+      if (more) {
+        stage ^= 1;
+        stash(R, smem + stage * kStage, tid);  // the other stage: nobody reads it now
       }
       __syncthreads();
     }
@@ -170,10 +209,16 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int j = 0; j < 4; j++)
 #pragma unroll
-      for (int q = 0; q < 4; q++) {
+      for (int q = 0; q < 4; q += 2) {
         const int r = m0 + wm * 32 + i * 16 + g + 8 * (q >> 1);
-        const int c = n0 + wn * 32 + j * 8 + 2 * tig + (q & 1);
-        if (r < M && c < N) C[(size_t)r * N + c] = tot[i][j][q];
+        const int c = n0 + wn * 32 + j * 8 + 2 * tig;
+        if (r < M && c + 1 < N && ((N & 1) == 0)) {
+          *reinterpret_cast<longlong2*>(C + (size_t)r * N + c) =
+              make_longlong2(tot[i][j][q], tot[i][j][q + 1]);
+        } else {
+          if (r < M && c < N) C[(size_t)r * N + c] = tot[i][j][q];
+          if (r < M && c + 1 < N) C[(size_t)r * N + c + 1] = tot[i][j][q + 1];
+        }
       }
 }
 
@@ -194,7 +239,14 @@ int op_igemm16(const int16_t* A, const int16_t* B, int64_t* C, int M, int K, int
     set_error("igemm16: M = %d too large", M);
     return kErrArg;
   }
-  k_igemm16<<<grid, 256, 0, s>>>(A, B, C, M, K, N);
+  static bool attr = false;
+  const size_t smem = 2 * kStage * sizeof(int16_t);
+  if (!attr) {
+    ZKL_CUDA(cudaFuncSetAttribute(k_igemm16, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    attr = true;
+  }
+  k_igemm16<<<grid, 256, smem, s>>>(A, B, C, M, K, N);
   ZKL_LAUNCH_CHECK();
   return kOk;
 }
