@@ -11,8 +11,9 @@
 // longer contractions flush the chunk sums into int64 every 2^14 columns.
 //
 // CTA tile 128 x 64 outputs, 8 warps as 4 (M) x 2 (N), each warp 32 x 32
-// (2 m16 x 4 n8 mma tiles); K steps of 32 staged in shared memory (A
-// row-major, B transposed so a B fragment is two 32-bit loads); out-of-range
+// (2 m16 x 4 n8 mma tiles); K steps of 64 staged in shared memory (A
+// row-major, B transposed so a B fragment is two 32-bit loads), two stages:
+// step s+1 is loaded into registers while step s feeds the MMAs.  Out-of-range
 // rows / columns / k are zero-filled, so any M, N, K works.
 #include <cstdint>
 
