@@ -89,11 +89,11 @@ def upload(values, spec, out=None):
     return out
 
 
-def decode(raw, spec, n):
+def decode(raw, spec, n, _fb=int.from_bytes):
     if spec.words == 1:
-        return [int(x) for x in np.frombuffer(raw, dtype=np.uint64, count=n)]
-    mv = memoryview(raw)
-    return [int.from_bytes(mv[32 * i: 32 * i + 32], "little") for i in range(n)]
+        return np.frombuffer(raw, dtype=np.uint64, count=n).tolist()
+    raw = bytes(raw)
+    return [_fb(raw[i:i + 32], "little") for i in range(0, 32 * n, 32)]
 
 
 def download(buf, spec, n):

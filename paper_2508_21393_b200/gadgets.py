@@ -220,11 +220,11 @@ def _matmul_native(A, B, C, dims, tr, spec):
     if log is not None:  # the appends the reference makes (transcript.py:33-35)
         p = spec.modulus
         cneg = (-inverse_pow2(d1, p)) % p
-        ln = lambda v: (v.bit_length() + 7) // 8 or 1  # noqa: E731
         log.extend([(b"sumcheck/sum", 1), (b"sumcheck/shape", 3), (b"sumcheck/coeff", 1),
-                    (b"sumcheck/factors", 3), (b"sumcheck/coeff", ln(cneg)),
+                    (b"sumcheck/factors", 3),
+                    (b"sumcheck/coeff", (cneg.bit_length() + 7) >> 3 or 1),
                     (b"sumcheck/factors", 2)])
-        log.extend((b"sumcheck/eval", ln(e)) for e in flat)
+        log += [(b"sumcheck/eval", (e.bit_length() + 7) >> 3 or 1) for e in flat]
     return rounds, point, finals
 
 

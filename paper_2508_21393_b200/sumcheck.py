@@ -134,8 +134,9 @@ def native_transcript(tr, spec):
 NATIVE_TRANSCRIPT = True  # tests flip this to exercise the per-round host path
 
 
-def _decode(raw, nb, count):
-    return [int.from_bytes(raw[nb * i: nb * i + nb], "little") for i in range(count)]
+def _decode(raw, nb, count, _fb=int.from_bytes):
+    raw = bytes(raw)
+    return [_fb(raw[i:i + nb], "little") for i in range(0, nb * count, nb)]
 
 
 def run_rounds(spec, tables, num_vars, terms, degree, tr, post_add=None, post_mul=None):
