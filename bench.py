@@ -49,6 +49,17 @@ CPU_SAMPLE = "the reference's own zkMat sumcheck (baseline/_ref zklora: gadgets.
              "of the cfg2 X.W claim"
 
 
+# Fr255 Montgomery-product ceilings on this B200:
+# MONT_BENCH_PEAK: the library's product in a throughput loop (tools/mont_bench.cu,
+# 3 independent products per call, 2 blocks/SM; profiles/r02/mont_bench.txt).
+# MONT_PIPE_BOUND: the pipe model of that product -- 128 IMAD.WIDE.U32 (measured
+# 7.35e12/s on the fmaheavy pipe) and ~320 ALU carry-chain ops (18.5e12/s) per
+# product; the fmaheavy side binds (tools/probes/fp64_rate.cu,
+# profiles/r02/pipe_rates.txt).
+MONT_BENCH_PEAK = 4.26e10
+MONT_PIPE_BOUND = 7.35e12 / 128
+
+
 def round_half_away(a):
     return np.sign(a) * np.floor(np.abs(a) + 0.5)
 
@@ -359,9 +370,11 @@ def run_cfg3(steps, warmup, N):
         "sumcheck_mont_roofline": {
             "bound": "imad (Montgomery products)", "products_per_proof": prods,
             "achieved_products_per_s": prods / sc_s if sc_s else 0.0,
-            "peak_products_per_s": 4.2e10,
-            "peak_source": "tools/mont_bench.cu on this B200 (profiles/r01 v25 ncu: ALU pipe 66%)",
-            "frac": (prods / sc_s / 4.2e10) if sc_s else 0.0},
+            "peak_products_per_s": MONT_BENCH_PEAK,
+            "peak_source": "tools/mont_bench.cu on this B200 (profiles/r02/mont_bench.txt)",
+            "frac": (prods / sc_s / MONT_BENCH_PEAK) if sc_s else 0.0,
+            "pipe_bound_products_per_s": MONT_PIPE_BOUND,
+            "pipe_frac": (prods / sc_s / MONT_PIPE_BOUND) if sc_s else 0.0},
     }
 
 
@@ -533,6 +546,7 @@ def run_sweep(ns, mont_peak=None):
                    and tuple(finals) == tuple(r2[2]) and tr.state == tr2.state)}
         if mont_peak:
             row["mont_frac"] = row["mont_products_per_s"] / mont_peak
+            row["mont_pipe_frac"] = row["mont_products_per_s"] / MONT_PIPE_BOUND
         out.append(row)
         del A, B, C, A2, B2, C2, a, b, c
         torch.cuda.empty_cache()
@@ -866,10 +880,13 @@ def main():
 
     cfg5 = None
     if not args.no_cfg5:
-        mont_peak = 4.2e10  # Fr255 Montgomery products/s, tools/mont_bench.cu (profiles/r01)
+        mont_peak = MONT_BENCH_PEAK
         cfg5 = {"workload": CFG5, "mont_peak_products_per_s": mont_peak,
                 "mont_peak_source": "tools/mont_bench.cu on this B200 (3 independent "
                                     "products per call, 2 blocks/SM)",
+                "mont_pipe_bound_products_per_s": MONT_PIPE_BOUND,
+                "mont_pipe_bound_source": "128 IMAD.WIDE.U32 per product at the measured "
+                                          "7.35e12/s (tools/probes/fp64_rate.cu)",
                 "sweep": run_sweep([20, 22, 24, 26, 28, 30], mont_peak),
                 "block_13b": run_cfg4(1, 1, "13b")}
 
