@@ -24,6 +24,7 @@ to 4 x 2^30 entries and one LLaMA-2-13B block) and the HBM-bound passes
 """
 
 import argparse
+import itertools
 import json
 import os
 import statistics
@@ -141,6 +142,23 @@ def elems_of(claims):
 
 def rounds_of(claims):
     return sum(sum(c[4]) for c in claims)
+
+
+def prove_step_batched(claim_groups, step_seed, zb):
+    """One cfg2 step through the batch API (matmul_sumcheck_batch): each group
+    of claims is one native call, the per-claim transcript records passed in.
+    The same transcript bytes and proofs as prove_step's per-claim loop
+    (tests/test_gpu_parity.py::test_matmul_batch_matches_per_claim)."""
+    tr = zb.Transcript(b"zklora-b200/bench", P_BIG, b"cfg2/%d" % step_seed)
+    finals = []
+    for group in claim_groups:
+        group = list(group)
+        mats = [(zb.DeviceMatrix.from_int_tensor(a), zb.DeviceMatrix.from_int_tensor(b),
+                 zb.DeviceMatrix.from_int_tensor(c), dims) for _, a, b, c, dims in group]
+        pre = [[(b"gadget/tag", b"matmul"), (b"bench/claim", name.encode())]
+               for name, *_ in group]
+        finals.extend(f for _, _, f in zb.matmul_sumcheck_batch(mats, tr, pre))
+    return finals, tr.state
 
 
 def prove_step(claims, step_seed, DeviceMatrix, matmul_sumcheck, Transcript, ready=None):
@@ -712,8 +730,11 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    # the batched step proves exactly what the per-claim loop proves
+    assert prove_step_batched([claims], 0, zb) == prove_step(claims, 0, DeviceMatrix,
+                                                            zb.matmul_sumcheck, zb.Transcript)
     for s in range(args.warmup):
-        prove_step(claims, s, DeviceMatrix, zb.matmul_sumcheck, zb.Transcript)
+        prove_step_batched([claims], s, zb)
 
     # ---- device-resident timing (value) ----
     clocks = ClockSampler(dev_id)
@@ -726,7 +747,7 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        prove_step(claims, 100 + s, DeviceMatrix, zb.matmul_sumcheck, zb.Transcript)
+        prove_step_batched([claims], 100 + s, zb)
         e1.record(stream)
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
@@ -796,7 +817,7 @@ def main():
         assert all(torch.equal(x, y) for x, y in zip(got[1:4], want[1:4])), got[0]
     stager = D.Staged()
 
-    def e2e_run(make_claims, steps, seed0):
+    def e2e_run(make_step, steps, seed0):
         out = []
         barrier()
         for s in range(steps):
@@ -804,9 +825,7 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            step_claims, ready = make_claims()
-            prove_step(step_claims, seed0 + s, DeviceMatrix, zb.matmul_sumcheck, zb.Transcript,
-                       ready=ready)
+            make_step(seed0 + s)
             e1.record(stream)
             e1.synchronize()
             out.append(e0.elapsed_time(e1))
@@ -816,10 +835,12 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return elems * world / (float(t.item()) / 1000.0 / steps)
 
-    def from_layer():
-        # products on the proving stream, each just before its claim: a
-        # witness stream running them beside the round engine measured
-        # slower (8.2 vs 7.8 ms per step; the GEMM's CTAs take every SM)
+    def from_layer(seed):
+        # two batches: the LoRA-branch claims (X, A_L, B_L only) are proven
+        # while W and dY are still in flight, then the other six products
+        # and claims.  Products on the proving stream: a witness stream
+        # running them beside the round engine measured slower (8.2 vs 7.8 ms
+        # per step; the GEMM's CTAs take every SM)
         stager.stage(groups, out=gbufs)
         waited = set()
 
@@ -830,7 +851,8 @@ def main():
                 waited.add(g)
 
         X_d, W_d, AL_d, BL_d, dY_d = layer_dev
-        return cfg2_layer_claims(X_d, W_d, AL_d, BL_d, dY_d, igemm_exact, need=need), None
+        gen = cfg2_layer_claims(X_d, W_d, AL_d, BL_d, dY_d, igemm_exact, need=need)
+        prove_step_batched([itertools.islice(gen, 2), gen], seed, zb)
 
     e2e_value = e2e_run(from_layer, args.steps, 200)
 
@@ -843,10 +865,11 @@ def main():
     h2d_ops = sum(a.numel() * a.element_size() + b.numel() * b.element_size()
                   + c.numel() * c.element_size() for _, a, b, c, _ in host)
 
-    def operands_copied():
+    def operands_copied(seed):
+        # per-claim calls: claim i waits for its own operands only
         dev = stager.stage([(a, b, c) for _, a, b, c, _ in host], out=dev_bufs)
-        return ([(n, da, db, dc, d) for (n, _, _, _, d), (da, db, dc) in zip(host, dev)],
-                stager.ready)
+        prove_step([(n, da, db, dc, d) for (n, _, _, _, d), (da, db, dc) in zip(host, dev)], seed,
+                   DeviceMatrix, zb.matmul_sumcheck, zb.Transcript, ready=stager.ready)
 
     e2e_ops_value = e2e_run(operands_copied, args.steps, 300)
 

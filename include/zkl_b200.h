@@ -264,6 +264,22 @@ int zkl_matmul_prove(int field, int a_type, const void* A, int b_type, const voi
                      const void* C, int d0, int d1, int d2, uint8_t* state_inout,
                      uint8_t* rounds_out, uint8_t* point_out, uint8_t* finals_out, void* stream);
 
+/* zkl_matmul_prove for a sequence of claims on one transcript, with the
+ * records a caller appends between claims (e.g. a gadget tag) passed in:
+ * claim i is preceded by the transcript records pre[pre_off[i] ..
+ * pre_off[i+1]) -- each u16le |label| || label || u64le |data| || data, the
+ * framing of transcript.py:13-35 -- and then proven exactly as
+ * zkl_matmul_prove would.  Same bytes as the one-claim calls in a loop
+ * (gadgets.py:241-251 per claim), but the next claim's challenge draws and
+ * matvecs are queued while the previous claim's last fold runs.
+ * types / mats / dims: 3 entries per claim (A, B, C; d0, d1, d2).  Outputs
+ * are the per-claim outputs of zkl_matmul_prove concatenated in claim order.
+ * pre / pre_off may be NULL (no records). */
+int zkl_matmul_prove_batch(int field, int nclaims, const int* types, const void* const* mats,
+                           const int* dims, const uint8_t* pre, const uint64_t* pre_off,
+                           uint8_t* state_inout, uint8_t* rounds_out, uint8_t* point_out,
+                           uint8_t* finals_out, void* stream);
+
 /* The logUp Eq.-7 sumcheck (lookup.py:188-219) for a secret larger than the
  * table (d = 2^num_vars > n = 2^tile_log, tile_log >= 5): runs the first
  * `rounds` = num_vars - tile_log rounds and appends exactly the reference's

@@ -25,6 +25,7 @@ from .gadgets import (  # noqa: F401
     ShapeMismatch,
     TensorRef,
     matmul_sumcheck,
+    matmul_sumcheck_batch,
     prove_elementprod,
     prove_matmul,
     prove_pair_lookup,

@@ -29,7 +29,7 @@ EXPORTS = (
     "zkl_multiplicities_index", "zkl_gather", "zkl_pair_multiplicities",
     "zkl_range_multiplicities", "zkl_rescale_witness", "zkl_transcript_append_ints", "zkl_transcript_challenge_vector",
     "zkl_sumcheck_prove_sharded", "zkl_shard_open", "zkl_shard_close", "zkl_shard_world",
-    "zkl_shard_exchange", "zkl_igemm_i16",
+    "zkl_shard_exchange", "zkl_igemm_i16", "zkl_matmul_prove_batch",
 )
 
 
@@ -108,6 +108,8 @@ _SIGS = {
     "zkl_matmul_prove": (
         [_i32, _i32, _vp, _i32, _vp, _i32, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp],
         ctypes.c_int),
+    "zkl_matmul_prove_batch": (
+        [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
 }
 
 

@@ -360,6 +360,13 @@ int zkl_matmul_prove(int field, int a_type, const void* A, int b_type, const voi
   D(field, op_matmul_prove<F>(a_type, A, b_type, B, c_type, C, d0, d1, d2, state_inout,
                               rounds_out, point_out, finals_out, (cudaStream_t)stream));
 }
+int zkl_matmul_prove_batch(int field, int nclaims, const int* types, const void* const* mats,
+                           const int* dims, const uint8_t* pre, const uint64_t* pre_off,
+                           uint8_t* state_inout, uint8_t* rounds_out, uint8_t* point_out,
+                           uint8_t* finals_out, void* stream) {
+  D(field, op_matmul_prove_batch<F>(nclaims, types, mats, dims, pre, pre_off, state_inout,
+                                    rounds_out, point_out, finals_out, (cudaStream_t)stream));
+}
 int zkl_logup_tiled_rounds(int field, void* const* tables, int tile_log, int num_vars, int rounds,
                            const uint8_t* u_canon, const uint8_t* coeffs_canon, int flags,
                            uint8_t* state_inout, uint8_t* rounds_out, uint8_t* point_out,

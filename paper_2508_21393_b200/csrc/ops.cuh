@@ -127,5 +127,10 @@ template <class F>
 int op_matmul_prove(int ta, const void* A, int tb, const void* B, int tc, const void* C, int d0,
                     int d1, int d2, uint8_t* state, uint8_t* rounds_out, uint8_t* point_out,
                     uint8_t* finals_out, cudaStream_t s);
+template <class F>
+int op_matmul_prove_batch(int nclaims, const int* types, const void* const* mats, const int* dims,
+                          const uint8_t* pre, const uint64_t* pre_off, uint8_t* state,
+                          uint8_t* rounds_out, uint8_t* point_out, uint8_t* finals_out,
+                          cudaStream_t s);
 
 }  // namespace zkl

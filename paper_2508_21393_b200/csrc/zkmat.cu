@@ -62,154 +62,124 @@ static void absorb_elem(HostTranscript& tr, const char* label, const typename F:
   tr.append_elem(label, b, F::kBytes);
 }
 
+// One claim's prover state.  begin() draws r_u / r_v, absorbs the claim and
+// enqueues the U-phase inputs; prove() runs the U, W and V phases and returns
+// once the last challenge is published (the V phase's finals still in
+// flight); end() collects them.  A batch runs begin() of claim i+1 between
+// prove() and end() of claim i, so the next claim's challenge draws and
+// matvecs are queued behind the last fold of the previous one and the GPU
+// never waits for the host between claims.  Device buffers are stream-ordered
+// (claim i+1's writes queue behind claim i's kernels) and the pending finals
+// arrive through the mailbox, not from device memory.
 template <class F>
-int op_matmul_prove(int ta, const void* A, int tb, const void* B, int tc, const void* C, int d0,
-                    int d1, int d2, uint8_t* state, uint8_t* rounds_out, uint8_t* point_out,
-                    uint8_t* finals_out, cudaStream_t s) {
+struct MatmulJob {
   using T = typename F::T;
   using H = typename host::For<F>::H;
-  constexpr int nb = F::kBytes;
-  if (d0 < 0 || d1 < 0 || d2 < 0 || d0 > 30 || d1 > 30 || d2 > 30 || d0 + d1 + d2 > 62) {
-    set_error("matmul_prove: bad dims (%d,%d,%d)", d0, d1, d2);
-    return kErrArg;
-  }
-  const uint64_t D0 = 1ull << d0, D1 = 1ull << d1, D2 = 1ull << d2;
-  const int n = d0 + d1 + d2;
-  // ZKL_TRACE: host timestamps at the phase boundaries (stderr)
-  static const bool tracing = getenv("ZKL_TRACE") != nullptr;
+  static constexpr int nb = F::kBytes;
+  enum { EV, BV, HV, EU, ERU, AV, CU, ERW, BW, KAP, CV, NBUF };
+
+  int ta = 0, tb = 0, tc = 0;
+  const void *A = nullptr, *B = nullptr, *C = nullptr;
+  int d0 = 0, d1 = 0, d2 = 0;
+  uint8_t *rounds_out = nullptr, *point_out = nullptr, *finals_out = nullptr;
+  cudaStream_t s = nullptr;
+  HostTranscript* tr = nullptr;
+
+  uint64_t D0 = 0, D1 = 0, D2 = 0;
+  int n = 0;
+  T cneg{};
+  uint64_t off[NBUF + 1] = {};
+  T* base = nullptr;
+  std::vector<uint8_t> ru, rv;
+  std::vector<T> pt = std::vector<T>(64);
+  PhaseArgs<F> pu, pw, pv;
+  T e_hat{}, alpha_s{}, fin_v[3] = {};
+  bool have_e_hat = false, have_alpha = false;
+  uint8_t *rounds = nullptr, *point = nullptr;
+
+  // ZKL_TRACE: host and GPU timestamps at the phase boundaries (stderr)
+  bool tracing = false;
   double tmark[8] = {0};
-  auto mark = [&](int i) {
+  cudaEvent_t gev[8] = {};
+
+  static bool dims_ok(int a, int b, int c) {
+    return a >= 0 && b >= 0 && c >= 0 && a <= 30 && b <= 30 && c <= 30 && a + b + c <= 62;
+  }
+  // device workspace: every vector has its own slot (cv included: the side
+  // stream writes EU and CV concurrently).  The side stream, its events and
+  // the side scratch arena are per device, so matmul proving is
+  // single-threaded per device (include/zkl_b200.h, threading).
+  static size_t work_bytes(int a, int b, int c) {
+    const uint64_t sizes[NBUF] = {1ull << c, 1ull << b, 1ull << a, 1ull << a, 1ull << a,
+                                  1ull << b, 1ull << c, 1ull << b, 1ull << c, 1, 1ull << a};
+    uint64_t tot = 0;
+    for (int i = 0; i < NBUF; i++) tot += (sizes[i] + 3) & ~3ull;
+    return tot * sizeof(T) + 64;
+  }
+  T* buf(int i) { return base + off[i]; }
+  void mark(int i) {
     if (tracing)
       tmark[i] = std::chrono::duration<double, std::micro>(
                      std::chrono::steady_clock::now().time_since_epoch())
                      .count();
-  };
-  mark(0);
-  cudaEvent_t gev[8] = {};
-  auto gmark = [&](int i) {
+  }
+  void gmark(int i) {
     if (tracing) {
       if (!gev[i]) cudaEventCreate(&gev[i]);
       cudaEventRecord(gev[i], s);
     }
-  };
-  gmark(0);
-  HostTranscript tr;
-  memcpy(tr.state, state, 64);
-
-  // r_u, r_v (gadgets.py:241-242; transcript.py:44-45)
-  std::vector<uint8_t> ru((size_t)d0 * nb), rv((size_t)d2 * nb);
-  char label[64];
-  for (int i = 0; i < d0; i++) {
-    snprintf(label, sizeof(label), "matmul/r_u/%d", i);
-    challenge_canon<F>(tr, label, ru.data() + (size_t)i * nb);
   }
-  for (int i = 0; i < d2; i++) {
-    snprintf(label, sizeof(label), "matmul/r_v/%d", i);
-    challenge_canon<F>(tr, label, rv.data() + (size_t)i * nb);
+  static double esz(int t) {
+    return t == 1 ? 2.0 : t == 2 ? 4.0 : t == 3 ? 8.0 : (double)sizeof(T);
   }
-  // cneg = -2^-d1 (gadgets.py:246), claim absorbed (sumcheck.py:90-95)
-  T inv = H::one();
-  const T i2 = half_p_plus_1<F>();
-  for (int i = 0; i < d1; i++) inv = H::mul(inv, i2);
-  const T cneg = H::sub(H::zero(), inv);
-  {
-    const uint8_t zero = 0, one = 1;
-    const uint8_t shape[3] = {3, (uint8_t)n, 2};
-    const uint8_t f0[3] = {0, 1, 2}, f1[2] = {0, 3};
-    tr.append_str("sumcheck/sum", &zero, 1);
-    tr.append_str("sumcheck/shape", shape, 3);
-    tr.append_str("sumcheck/coeff", &one, 1);
-    tr.append_str("sumcheck/factors", f0, 3);
-    absorb_elem<F>(tr, "sumcheck/coeff", cneg);
-    tr.append_str("sumcheck/factors", f1, 2);
-  }
-
-  // device vectors
-  const uint64_t sizes[] = {D2, D1, D0, D0, D0, D1, D2, D1, D2, 1, D0};
-  enum { EV, BV, HV, EU, ERU, AV, CU, ERW, BW, KAP, CV, NBUF };
-  uint64_t off[NBUF + 1];
-  off[0] = 0;
-  for (int i = 0; i < NBUF; i++) off[i + 1] = off[i] + ((sizes[i] + 3) & ~3ull);
-  // every vector has its own slot (cv included: the side stream writes EU and
-  // CV concurrently).  The side stream, its events and the side scratch arena
-  // are per device, so matmul_prove is single-threaded per device: one host
-  // thread proves on a device at a time (include/zkl_b200.h, threading).
-  void* wsv;
-  int rc = work_reserve(off[NBUF] * sizeof(T) + 64, &wsv, s);
-  if (rc) return rc;
-  T* base = (T*)wsv;
-  auto buf = [&](int i) { return base + off[i]; };
   // profiler brackets (no-ops unless zkl_prof_enable)
-  auto esz = [](int t) { return t == 1 ? 2.0 : t == 2 ? 4.0 : t == 3 ? 8.0 : (double)sizeof(T); };
-  auto mv_on = [&](cudaStream_t st, int t, const void* M, uint64_t r_, uint64_t c_, int tr,
-                   const T* xin, T* yout) {
+  int mv_on(cudaStream_t st, int t, const void* M, uint64_t r_, uint64_t c_, int trn, const T* xin,
+            T* yout) {
     const int h = prof_open(kProfMatvec, (double)r_ * c_ * esz(t) + (double)(r_ + c_) * sizeof(T),
                             (double)r_ * c_, st);
-    const int r2 = op_matvec<F>(t, M, r_, c_, tr, xin, yout, st);
+    const int r2 = op_matvec<F>(t, M, r_, c_, trn, xin, yout, st);
     prof_close(h, st);
     return r2;
-  };
-  auto mv = [&](int t, const void* M, uint64_t r_, uint64_t c_, int tr, const T* xin, T* yout) {
-    return mv_on(s, t, M, r_, c_, tr, xin, yout);
-  };
-  auto eq_on = [&](cudaStream_t st, T* dst, const T* p_, int m) {
+  }
+  int mv(int t, const void* M, uint64_t r_, uint64_t c_, int trn, const T* xin, T* yout) {
+    return mv_on(s, t, M, r_, c_, trn, xin, yout);
+  }
+  int eq_on(cudaStream_t st, T* dst, const T* p_, int m) {
     const int h = prof_open(kProfEq, (double)(1ull << m) * sizeof(T), (double)(1ull << m), st);
     const int r2 = op_eq_table<F>(dst, p_, m, st);
     prof_close(h, st);
     return r2;
-  };
-  auto eq = [&](T* dst, const T* p_, int m) { return eq_on(s, dst, p_, m); };
+  }
+  int eq(T* dst, const T* p_, int m) { return eq_on(s, dst, p_, m); }
   // independent products of a phase's inputs run concurrently on the side
   // stream (its own scratch arena); fork / join through events
-  const cudaStream_t side = side_stream();
-  static thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  if (!ev_fork) {
-    ZKL_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-    ZKL_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  static cudaEvent_t& ev_fork() {
+    static thread_local cudaEvent_t e = nullptr;
+    return e;
   }
-  auto fork = [&]() -> int {
-    ZKL_CUDA(cudaEventRecord(ev_fork, s));
-    ZKL_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+  static cudaEvent_t& ev_join() {
+    static thread_local cudaEvent_t e = nullptr;
+    return e;
+  }
+  int fork() {
+    if (!ev_fork()) {
+      ZKL_CUDA(cudaEventCreateWithFlags(&ev_fork(), cudaEventDisableTiming));
+      ZKL_CUDA(cudaEventCreateWithFlags(&ev_join(), cudaEventDisableTiming));
+    }
+    ZKL_CUDA(cudaEventRecord(ev_fork(), s));
+    ZKL_CUDA(cudaStreamWaitEvent(side_stream(), ev_fork(), 0));
     return kOk;
-  };
-  auto join = [&]() -> int {
-    ZKL_CUDA(cudaEventRecord(ev_join, side));
-    ZKL_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+  }
+  int join() {
+    ZKL_CUDA(cudaEventRecord(ev_join(), side_stream()));
+    ZKL_CUDA(cudaStreamWaitEvent(s, ev_join(), 0));
     return kOk;
-  };
-  std::vector<T> pt(64);
-  auto load_point = [&](const uint8_t* canon, int m) {
+  }
+  const T* load_point(const uint8_t* canon, int m) {
     for (int i = 0; i < m; i++) pt[i] = host::from_canon<F>(canon + (size_t)i * nb);
     return pt.data();
-  };
-
-  // ---- U phase inputs: E_v, bv = B E_v, cv = C E_v, h = A bv - cv
-  rc = eq(buf(EV), load_point(rv.data(), d2), d2);
-  if (rc) return rc;
-  gmark(1);
-  // side: cv = C E_v and E_u; main: bv = B E_v, abv = A bv; then h = abv - cv
-  if ((rc = fork())) return rc;
-  if ((rc = mv_on(side, tc, C, D0, D2, 0, buf(EV), buf(CV)))) return rc;  // cv
-  if ((rc = eq_on(side, buf(EU), load_point(ru.data(), d0), d0))) return rc;
-  if ((rc = mv(tb, B, D1, D2, 0, buf(EV), buf(BV)))) return rc;
-  if ((rc = mv(ta, A, D0, D1, 0, buf(BV), buf(HV)))) return rc;  // abv
-  if ((rc = join())) return rc;
-  if ((rc = op_axpy<F>(buf(HV), buf(HV), H::sub(H::zero(), H::one()), buf(CV), D0, s))) return rc;
-  mark(1);
-  gmark(2);
-  uint8_t* rounds = rounds_out;
-  uint8_t* point = point_out;
-  // Phases are pipelined: run_phase returns once the last challenge is sent,
-  // the next phase's inputs are enqueued behind the still-running kernel, and
-  // the previous phase's finals (E_hat, alpha_s) are collected by the next
-  // phase's prepare() when its first round is finished on the host.
-  PhaseArgs<F> pu, pw, pv;
-  void* tabs_u[2] = {buf(EU), buf(HV)};
-  void* tabs_w[2] = {buf(AV), buf(BV)};
-  void* tabs_v[3] = {buf(EV), buf(BW), buf(CU)};
-  T e_hat = H::one(), alpha_s = H::one();
-  bool have_e_hat = d0 == 0;
-  auto get_e_hat = [&]() -> int {
+  }
+  int get_e_hat() {
     if (!have_e_hat) {
       T fin[2];
       int r = wait_phase_finals<F>(pu, fin, s);
@@ -218,65 +188,8 @@ int op_matmul_prove(int ta, const void* A, int tb, const void* B, int tc, const 
       have_e_hat = true;
     }
     return kOk;
-  };
-  if (d0) {
-    pu.tables = tabs_u;
-    pu.k = 2;
-    pu.num_vars = d0;
-    pu.tm = prod2_terms<F>(H::one());
-    pu.post_mul = H::one();
-    if ((rc = run_phase<F>(pu, tr, rounds, point, nullptr, s))) return rc;
   }
-  mark(2);
-  gmark(3);
-  // ---- W phase inputs: E(rho_u), a = E^T A, cu = E^T C, kappa = <cu, E_v>
-  if ((rc = eq(buf(ERU), load_point(point, d0), d0))) return rc;
-  rounds += (size_t)d0 * 4 * nb;
-  point += (size_t)d0 * nb;
-  if ((rc = fork())) return rc;
-  if ((rc = mv_on(side, tc, C, D0, D2, 1, buf(ERU), buf(CU)))) return rc;  // cu (side)
-  if ((rc = mv(ta, A, D0, D1, 1, buf(ERU), buf(AV)))) return rc;
-  if ((rc = join())) return rc;
-  if ((rc = op_dot<F>(buf(KAP), buf(CU), buf(EV), D2, s))) return rc;
-  static thread_local T* kap_host = nullptr;
-  static thread_local cudaEvent_t kap_ev = nullptr;
-  if (!kap_host) {
-    ZKL_CUDA(cudaHostAlloc((void**)&kap_host, 64, cudaHostAllocDefault));
-    ZKL_CUDA(cudaEventCreateWithFlags(&kap_ev, cudaEventDisableTiming));
-  }
-  ZKL_CUDA(cudaMemcpyAsync(kap_host, buf(KAP), sizeof(T), cudaMemcpyDeviceToHost, s));
-  ZKL_CUDA(cudaEventRecord(kap_ev, s));
-  mark(3);
-  gmark(4);
-  bool have_alpha = false;
-  if (d1) {
-    pw.tables = tabs_w;
-    pw.k = 2;
-    pw.num_vars = d1;
-    pw.tm = prod2_terms<F>(H::one());
-    pw.post_mul = H::one();
-    pw.prepare = [&](std::vector<T>& adds) -> int {
-      int r = get_e_hat();
-      if (r) return r;
-      pw.post_mul = e_hat;
-      ZKL_CUDA(cudaEventSynchronize(kap_ev));
-      const T kappa = *kap_host;
-      adds.resize(d1);
-      T c = H::mul(cneg, kappa);  // cneg 2^(d1-j-1) kappa, j = d1-1 .. 0
-      for (int j = d1 - 1; j >= 0; j--) {
-        adds[j] = c;
-        c = H::add(c, c);
-      }
-      return kOk;
-    };
-    if ((rc = run_phase<F>(pw, tr, rounds, point, nullptr, s))) return rc;
-  } else {
-    uint8_t b[32];
-    if ((rc = op_read<F>(b, buf(AV), 1, s))) return rc;
-    alpha_s = host::from_canon<F>(b);
-    have_alpha = true;
-  }
-  auto get_alpha = [&]() -> int {
+  int get_alpha() {
     if (!have_alpha) {
       T fin[2];
       int r = wait_phase_finals<F>(pw, fin, s);
@@ -285,58 +198,209 @@ int op_matmul_prove(int ta, const void* A, int tb, const void* B, int tc, const 
       have_alpha = true;
     }
     return kOk;
-  };
-  mark(4);
-  gmark(5);
-  // ---- V phase inputs: E(rho_w), bw = E^T B
-  if ((rc = eq(buf(ERW), load_point(point, d1), d1))) return rc;
-  rounds += (size_t)d1 * 4 * nb;
-  point += (size_t)d1 * nb;
-  if ((rc = mv(tb, B, D1, D2, 1, buf(ERW), buf(BW)))) return rc;
-  mark(5);
-  gmark(6);
-  T fin_v[3];
-  if (d2) {
-    pv.tables = tabs_v;
-    pv.k = 3;
-    pv.num_vars = d2;
-    Terms<F> tm;
-    memset(&tm, 0, sizeof(tm));
-    tm.nterms = 2;
-    tm.degree = 3;
-    tm.nf[0] = tm.nf[1] = 2;
-    tm.fi[0][0] = 0;
-    tm.fi[0][1] = 1;
-    tm.fi[1][0] = 0;
-    tm.fi[1][1] = 2;
-    tm.coef[0] = H::one();  // alpha_s, set by prepare (host-applied coefficient)
-    tm.coef[1] = cneg;
-    pv.tm = tm;
-    pv.post_mul = H::one();
-    pv.prepare = [&](std::vector<T>&) -> int {
-      int r = get_e_hat();
-      if (r) return r;
-      if ((r = get_alpha())) return r;
-      pv.post_mul = e_hat;
-      pv.tm.coef[0] = alpha_s;
-      return kOk;
-    };
-    if ((rc = run_phase<F>(pv, tr, rounds, point, fin_v, s))) return rc;
-  } else {
-    if ((rc = get_e_hat()) || (rc = get_alpha())) return rc;
-    uint8_t b[64];
-    if ((rc = op_read<F>(b, buf(BW), 1, s))) return rc;
-    if ((rc = op_read<F>(b + 32, buf(CU), 1, s))) return rc;
-    fin_v[0] = H::one();
-    fin_v[1] = host::from_canon<F>(b);
-    fin_v[2] = host::from_canon<F>(b + 32);
   }
-  const T finals[4] = {H::mul(e_hat, fin_v[0]), alpha_s, fin_v[1], fin_v[2]};
-  for (int q = 0; q < 4; q++) host::to_canon<F>(finals_out + (size_t)q * nb, finals[q]);
-  memcpy(state, tr.state, 64);
-  mark(6);
-  gmark(7);
-  if (tracing) {
+  static T*& kap_host() {
+    static thread_local T* p = nullptr;
+    return p;
+  }
+  static cudaEvent_t& kap_ev() {
+    static thread_local cudaEvent_t e = nullptr;
+    return e;
+  }
+
+  int begin() {
+    if (!dims_ok(d0, d1, d2)) {
+      set_error("matmul_prove: bad dims (%d,%d,%d)", d0, d1, d2);
+      return kErrArg;
+    }
+    D0 = 1ull << d0;
+    D1 = 1ull << d1;
+    D2 = 1ull << d2;
+    n = d0 + d1 + d2;
+    tracing = getenv("ZKL_TRACE") != nullptr;
+    mark(0);
+    gmark(0);
+    // r_u, r_v (gadgets.py:241-242; transcript.py:44-45)
+    ru.resize((size_t)d0 * nb);
+    rv.resize((size_t)d2 * nb);
+    char label[64];
+    for (int i = 0; i < d0; i++) {
+      snprintf(label, sizeof(label), "matmul/r_u/%d", i);
+      challenge_canon<F>(*tr, label, ru.data() + (size_t)i * nb);
+    }
+    for (int i = 0; i < d2; i++) {
+      snprintf(label, sizeof(label), "matmul/r_v/%d", i);
+      challenge_canon<F>(*tr, label, rv.data() + (size_t)i * nb);
+    }
+    // cneg = -2^-d1 (gadgets.py:246), claim absorbed (sumcheck.py:90-95)
+    T inv = H::one();
+    const T i2 = half_p_plus_1<F>();
+    for (int i = 0; i < d1; i++) inv = H::mul(inv, i2);
+    cneg = H::sub(H::zero(), inv);
+    {
+      const uint8_t zero = 0, one = 1;
+      const uint8_t shape[3] = {3, (uint8_t)n, 2};
+      const uint8_t f0[3] = {0, 1, 2}, f1[2] = {0, 3};
+      tr->append_str("sumcheck/sum", &zero, 1);
+      tr->append_str("sumcheck/shape", shape, 3);
+      tr->append_str("sumcheck/coeff", &one, 1);
+      tr->append_str("sumcheck/factors", f0, 3);
+      absorb_elem<F>(*tr, "sumcheck/coeff", cneg);
+      tr->append_str("sumcheck/factors", f1, 2);
+    }
+    const uint64_t sizes[NBUF] = {D2, D1, D0, D0, D0, D1, D2, D1, D2, 1, D0};
+    off[0] = 0;
+    for (int i = 0; i < NBUF; i++) off[i + 1] = off[i] + ((sizes[i] + 3) & ~3ull);
+    void* wsv;
+    int rc = work_reserve(work_bytes(d0, d1, d2), &wsv, s);
+    if (rc) return rc;
+    base = (T*)wsv;
+    // ---- U phase inputs: E_v, bv = B E_v, cv = C E_v, h = A bv - cv
+    if ((rc = eq(buf(EV), load_point(rv.data(), d2), d2))) return rc;
+    gmark(1);
+    // side: cv = C E_v and E_u; main: bv = B E_v, abv = A bv; then h = abv - cv
+    if ((rc = fork())) return rc;
+    if ((rc = mv_on(side_stream(), tc, C, D0, D2, 0, buf(EV), buf(CV)))) return rc;  // cv
+    if ((rc = eq_on(side_stream(), buf(EU), load_point(ru.data(), d0), d0))) return rc;
+    if ((rc = mv(tb, B, D1, D2, 0, buf(EV), buf(BV)))) return rc;
+    if ((rc = mv(ta, A, D0, D1, 0, buf(BV), buf(HV)))) return rc;  // abv
+    if ((rc = join())) return rc;
+    if ((rc = op_axpy<F>(buf(HV), buf(HV), H::sub(H::zero(), H::one()), buf(CV), D0, s)))
+      return rc;
+    mark(1);
+    gmark(2);
+    return kOk;
+  }
+
+  // Phases are pipelined: run_phase returns once the last challenge is sent,
+  // the next phase's inputs are enqueued behind the still-running kernel, and
+  // the previous phase's finals (E_hat, alpha_s) are collected by the next
+  // phase's prepare() when its first round is finished on the host.
+  int prove() {
+    int rc;
+    rounds = rounds_out;
+    point = point_out;
+    e_hat = H::one();
+    alpha_s = H::one();
+    have_e_hat = d0 == 0;
+    have_alpha = false;
+    void* tabs_u[2] = {buf(EU), buf(HV)};
+    void* tabs_w[2] = {buf(AV), buf(BV)};
+    void* tabs_v[3] = {buf(EV), buf(BW), buf(CU)};
+    if (d0) {
+      pu.tables = tabs_u;
+      pu.k = 2;
+      pu.num_vars = d0;
+      pu.tm = prod2_terms<F>(H::one());
+      pu.post_mul = H::one();
+      if ((rc = run_phase<F>(pu, *tr, rounds, point, nullptr, s))) return rc;
+    }
+    mark(2);
+    gmark(3);
+    // ---- W phase inputs: E(rho_u), a = E^T A, cu = E^T C, kappa = <cu, E_v>
+    if ((rc = eq(buf(ERU), load_point(point, d0), d0))) return rc;
+    rounds += (size_t)d0 * 4 * nb;
+    point += (size_t)d0 * nb;
+    if ((rc = fork())) return rc;
+    if ((rc = mv_on(side_stream(), tc, C, D0, D2, 1, buf(ERU), buf(CU)))) return rc;  // cu
+    if ((rc = mv(ta, A, D0, D1, 1, buf(ERU), buf(AV)))) return rc;
+    if ((rc = join())) return rc;
+    if ((rc = op_dot<F>(buf(KAP), buf(CU), buf(EV), D2, s))) return rc;
+    if (!kap_host()) {
+      ZKL_CUDA(cudaHostAlloc((void**)&kap_host(), 64, cudaHostAllocDefault));
+      ZKL_CUDA(cudaEventCreateWithFlags(&kap_ev(), cudaEventDisableTiming));
+    }
+    ZKL_CUDA(cudaMemcpyAsync(kap_host(), buf(KAP), sizeof(T), cudaMemcpyDeviceToHost, s));
+    ZKL_CUDA(cudaEventRecord(kap_ev(), s));
+    mark(3);
+    gmark(4);
+    if (d1) {
+      pw.tables = tabs_w;
+      pw.k = 2;
+      pw.num_vars = d1;
+      pw.tm = prod2_terms<F>(H::one());
+      pw.post_mul = H::one();
+      pw.prepare = [this](std::vector<T>& adds) -> int {
+        int r = get_e_hat();
+        if (r) return r;
+        pw.post_mul = e_hat;
+        ZKL_CUDA(cudaEventSynchronize(kap_ev()));
+        const T kappa = *kap_host();
+        adds.resize(d1);
+        T c = H::mul(cneg, kappa);  // cneg 2^(d1-j-1) kappa, j = d1-1 .. 0
+        for (int j = d1 - 1; j >= 0; j--) {
+          adds[j] = c;
+          c = H::add(c, c);
+        }
+        return kOk;
+      };
+      if ((rc = run_phase<F>(pw, *tr, rounds, point, nullptr, s))) return rc;
+    } else {
+      uint8_t b[32];
+      if ((rc = op_read<F>(b, buf(AV), 1, s))) return rc;
+      alpha_s = host::from_canon<F>(b);
+      have_alpha = true;
+    }
+    mark(4);
+    gmark(5);
+    // ---- V phase inputs: E(rho_w), bw = E^T B
+    if ((rc = eq(buf(ERW), load_point(point, d1), d1))) return rc;
+    rounds += (size_t)d1 * 4 * nb;
+    point += (size_t)d1 * nb;
+    if ((rc = mv(tb, B, D1, D2, 1, buf(ERW), buf(BW)))) return rc;
+    mark(5);
+    gmark(6);
+    if (d2) {
+      pv.tables = tabs_v;
+      pv.k = 3;
+      pv.num_vars = d2;
+      Terms<F> tm;
+      memset(&tm, 0, sizeof(tm));
+      tm.nterms = 2;
+      tm.degree = 3;
+      tm.nf[0] = tm.nf[1] = 2;
+      tm.fi[0][0] = 0;
+      tm.fi[0][1] = 1;
+      tm.fi[1][0] = 0;
+      tm.fi[1][1] = 2;
+      tm.coef[0] = H::one();  // alpha_s, set by prepare (host-applied coefficient)
+      tm.coef[1] = cneg;
+      pv.tm = tm;
+      pv.post_mul = H::one();
+      pv.prepare = [this](std::vector<T>&) -> int {
+        int r = get_e_hat();
+        if (r) return r;
+        if ((r = get_alpha())) return r;
+        pv.post_mul = e_hat;
+        pv.tm.coef[0] = alpha_s;
+        return kOk;
+      };
+      // the V finals are collected by end()
+      if ((rc = run_phase<F>(pv, *tr, rounds, point, nullptr, s))) return rc;
+    } else {
+      if ((rc = get_e_hat()) || (rc = get_alpha())) return rc;
+      uint8_t b[64];
+      if ((rc = op_read<F>(b, buf(BW), 1, s))) return rc;
+      if ((rc = op_read<F>(b + 32, buf(CU), 1, s))) return rc;
+      fin_v[0] = H::one();
+      fin_v[1] = host::from_canon<F>(b);
+      fin_v[2] = host::from_canon<F>(b + 32);
+    }
+    return kOk;
+  }
+
+  int end() {
+    int rc;
+    if (d2 && (rc = wait_phase_finals<F>(pv, fin_v, s))) return rc;
+    const T finals[4] = {H::mul(e_hat, fin_v[0]), alpha_s, fin_v[1], fin_v[2]};
+    for (int q = 0; q < 4; q++) host::to_canon<F>(finals_out + (size_t)q * nb, finals[q]);
+    mark(6);
+    gmark(7);
+    if (tracing) report();
+    return kOk;
+  }
+
+  void report() {
     cudaStreamSynchronize(s);
     float g[7];
     for (int i = 0; i < 7; i++) cudaEventElapsedTime(&g[i], gev[i], gev[i + 1]);
@@ -346,13 +410,112 @@ int op_matmul_prove(int ta, const void* A, int tb, const void* B, int tc, const 
             d0, d1, d2, g[0] * 1e3, g[1] * 1e3, g[2] * 1e3, g[3] * 1e3, g[4] * 1e3, g[5] * 1e3,
             g[6] * 1e3);
     for (int i = 0; i < 8; i++) cudaEventDestroy(gev[i]);
-  }
-  if (tracing)
     fprintf(stderr,
             "[zkl trace] matmul (%d,%d,%d) us: draw+enqueue %.1f | U %.1f | enqueue W %.1f | "
             "W %.1f | enqueue V %.1f | V %.1f | total %.1f\n",
             d0, d1, d2, tmark[1] - tmark[0], tmark[2] - tmark[1], tmark[3] - tmark[2],
             tmark[4] - tmark[3], tmark[5] - tmark[4], tmark[6] - tmark[5], tmark[6] - tmark[0]);
+  }
+};
+
+template <class F>
+int op_matmul_prove(int ta, const void* A, int tb, const void* B, int tc, const void* C, int d0,
+                    int d1, int d2, uint8_t* state, uint8_t* rounds_out, uint8_t* point_out,
+                    uint8_t* finals_out, cudaStream_t s) {
+  HostTranscript tr;
+  memcpy(tr.state, state, 64);
+  MatmulJob<F> job;
+  job.ta = ta; job.tb = tb; job.tc = tc;
+  job.A = A; job.B = B; job.C = C;
+  job.d0 = d0; job.d1 = d1; job.d2 = d2;
+  job.rounds_out = rounds_out; job.point_out = point_out; job.finals_out = finals_out;
+  job.s = s;
+  job.tr = &tr;
+  int rc;
+  if ((rc = job.begin()) || (rc = job.prove()) || (rc = job.end())) return rc;
+  memcpy(state, tr.state, 64);
+  return kOk;
+}
+
+// Transcript records appended before a claim: u16le |label| || label ||
+// u64le |data| || data, repeated (the framing of transcript.py:13-35).
+static int append_records(HostTranscript& tr, const uint8_t* p, uint64_t len) {
+  uint64_t o = 0;
+  while (o < len) {
+    if (len - o < 2) return kErrArg;
+    const size_t ll = (size_t)p[o] | ((size_t)p[o + 1] << 8);
+    o += 2;
+    if (len - o < ll + 8) return kErrArg;
+    const char* label = (const char*)(p + o);
+    o += ll;
+    uint64_t dl = 0;
+    for (int i = 0; i < 8; i++) dl |= (uint64_t)p[o + i] << (8 * i);
+    o += 8;
+    if (len - o < dl) return kErrArg;
+    tr.append(label, ll, p + o, (size_t)dl);
+    o += dl;
+  }
+  return kOk;
+}
+
+template <class F>
+int op_matmul_prove_batch(int nclaims, const int* types, const void* const* mats, const int* dims,
+                          const uint8_t* pre, const uint64_t* pre_off, uint8_t* state,
+                          uint8_t* rounds_out, uint8_t* point_out, uint8_t* finals_out,
+                          cudaStream_t s) {
+  constexpr int nb = F::kBytes;
+  if (nclaims < 0) return kErrArg;
+  if (nclaims == 0) return kOk;
+  HostTranscript tr;
+  memcpy(tr.state, state, 64);
+  // the largest claim's workspace up front: growing it mid-batch would
+  // synchronise the stream
+  size_t want = 0;
+  for (int i = 0; i < nclaims; i++) {
+    const int* d = dims + 3 * i;
+    if (!MatmulJob<F>::dims_ok(d[0], d[1], d[2])) {
+      set_error("matmul_prove_batch: claim %d has bad dims (%d,%d,%d)", i, d[0], d[1], d[2]);
+      return kErrArg;
+    }
+    const size_t w = MatmulJob<F>::work_bytes(d[0], d[1], d[2]);
+    want = w > want ? w : want;
+  }
+  void* ws;
+  int rc = work_reserve(want, &ws, s);
+  if (rc) return rc;
+  std::vector<MatmulJob<F>> jobs(2);
+  size_t roff = 0, poff = 0;
+  auto setup = [&](MatmulJob<F>& j, int i) -> int {
+    j = MatmulJob<F>();
+    const int* d = dims + 3 * i;
+    j.ta = types[3 * i]; j.tb = types[3 * i + 1]; j.tc = types[3 * i + 2];
+    j.A = mats[3 * i]; j.B = mats[3 * i + 1]; j.C = mats[3 * i + 2];
+    j.d0 = d[0]; j.d1 = d[1]; j.d2 = d[2];
+    j.rounds_out = rounds_out + roff * 4 * nb;
+    j.point_out = point_out + poff * nb;
+    j.finals_out = finals_out + (size_t)i * 4 * nb;
+    roff += (size_t)(d[0] + d[1] + d[2]);
+    poff += (size_t)(d[0] + d[1] + d[2]);
+    j.s = s;
+    j.tr = &tr;
+    if (pre && pre_off) {
+      const int r = append_records(tr, pre + pre_off[i], pre_off[i + 1] - pre_off[i]);
+      if (r) {
+        set_error("matmul_prove_batch: malformed transcript records before claim %d", i);
+        return r;
+      }
+    }
+    return j.begin();
+  };
+  if ((rc = setup(jobs[0], 0))) return rc;
+  for (int i = 0; i < nclaims; i++) {
+    MatmulJob<F>& cur = jobs[i & 1];
+    if ((rc = cur.prove())) return rc;
+    // the next claim's draws and inputs queue behind this claim's last fold
+    if (i + 1 < nclaims && (rc = setup(jobs[(i + 1) & 1], i + 1))) return rc;
+    if ((rc = cur.end())) return rc;
+  }
+  memcpy(state, tr.state, 64);
   return kOk;
 }
 
@@ -361,5 +524,11 @@ template int op_matmul_prove<Fr255>(int, const void*, int, const void*, int, con
                                     cudaStream_t);
 template int op_matmul_prove<M61>(int, const void*, int, const void*, int, const void*, int, int,
                                   int, uint8_t*, uint8_t*, uint8_t*, uint8_t*, cudaStream_t);
+template int op_matmul_prove_batch<Fr255>(int, const int*, const void* const*, const int*,
+                                          const uint8_t*, const uint64_t*, uint8_t*, uint8_t*,
+                                          uint8_t*, uint8_t*, cudaStream_t);
+template int op_matmul_prove_batch<M61>(int, const int*, const void* const*, const int*,
+                                        const uint8_t*, const uint64_t*, uint8_t*, uint8_t*,
+                                        uint8_t*, uint8_t*, cudaStream_t);
 
 }  // namespace zkl

@@ -228,6 +228,94 @@ def _matmul_native(A, B, C, dims, tr, spec):
     return rounds, point, finals
 
 
+def _records(pairs):
+    """Transcript records (label, data) in the reference's framing
+    (transcript.py:13-35): u16le |label| || label || u64le |data| || data."""
+    out = bytearray()
+    for label, data in pairs:
+        if isinstance(data, int):
+            data = data.to_bytes((data.bit_length() + 7) // 8 or 1, "little")
+        out += len(label).to_bytes(2, "little") + label + len(data).to_bytes(8, "little") + data
+    return bytes(out)
+
+
+def matmul_sumcheck_batch(claims, tr, pre=None):
+    """matmul_sumcheck for a sequence of claims on one transcript: claims is
+    [(A, B, C, dims)], pre (optional) a list of [(label, data)] records
+    appended to the transcript before each claim.  Returns the per-claim
+    (rounds, point, final_values) -- the same proofs, and the same
+    transcript, as
+
+        for (A, B, C, dims), recs in zip(claims, pre):
+            for label, data in recs: tr.append(label, data)
+            matmul_sumcheck(A, B, C, dims, tr)
+
+    With the native transcript the whole sequence is one C call
+    (zkl_matmul_prove_batch): the next claim's challenge draws and matvecs are
+    queued while the previous claim's last fold runs."""
+    claims = list(claims)
+    pre = list(pre) if pre is not None else [()] * len(claims)
+    if len(pre) != len(claims):
+        raise ValueError("one record list per claim")
+    p = tr.modulus
+    spec = D.spec_for(p)
+    for A, B, C, dims in claims:
+        d0, d1, d2 = dims
+        D0, D1, D2 = 1 << d0, 1 << d1, 1 << d2
+        if (A.rows, A.cols, B.rows, B.cols, C.rows, C.cols) != (D0, D1, D1, D2, D0, D2):
+            raise ShapeMismatch("device operands do not match dims %r" % (dims,))
+    if not (NATIVE_DRIVER and native_transcript(tr, spec)) or not claims:
+        out = []
+        for (A, B, C, dims), recs in zip(claims, pre):
+            for label, data in recs:
+                tr.append(label, data)
+            out.append(matmul_sumcheck(A, B, C, dims, tr))
+        return out
+    k = len(claims)
+    nb = spec.nbytes
+    types = (ctypes.c_int * (3 * k))(*[M.mtype for c in claims for M in c[:3]])
+    mats = (ctypes.c_void_p * (3 * k))(*[M.t.data_ptr() for c in claims for M in c[:3]])
+    dims = (ctypes.c_int * (3 * k))(*[d for c in claims for d in c[3]])
+    blobs = [_records(recs) for recs in pre]
+    offs = [0]
+    for b in blobs:
+        offs.append(offs[-1] + len(b))
+    blob = b"".join(blobs)
+    pre_off = (ctypes.c_uint64 * (k + 1))(*offs)
+    total = sum(sum(c[3]) for c in claims)
+    state = ctypes.create_string_buffer(bytes(tr.state), 64)
+    rbuf = (ctypes.c_uint8 * (max(total, 1) * 4 * nb))()
+    pbuf = (ctypes.c_uint8 * (max(total, 1) * nb))()
+    fbuf = (ctypes.c_uint8 * (4 * nb * k))()
+    N.check(N.lib().zkl_matmul_prove_batch(spec.fid, k, types, mats, dims, blob or None,
+                                           pre_off if blob else None, state, rbuf, pbuf, fbuf,
+                                           D.stream()))
+    flat = D.decode(bytes(rbuf), spec, 4 * total)
+    pts = D.decode(bytes(pbuf), spec, total)
+    fins = D.decode(bytes(fbuf), spec, 4 * k)
+    tr.state = state.raw[:64]
+    log = getattr(tr, "log", None)
+    out = []
+    o = 0
+    for i, ((A, B, C, dims), recs) in enumerate(zip(claims, pre)):
+        n = sum(dims)
+        ev = flat[4 * o:4 * (o + n)]
+        out.append(([tuple(ev[4 * j:4 * j + 4]) for j in range(n)], pts[o:o + n],
+                    tuple(fins[4 * i:4 * i + 4])))
+        if log is not None:
+            for label, data in recs:
+                ln = len(data) if not isinstance(data, int) else (data.bit_length() + 7) // 8 or 1
+                log.append((label, ln))
+            cneg = (-inverse_pow2(dims[1], p)) % p
+            log.extend([(b"sumcheck/sum", 1), (b"sumcheck/shape", 3), (b"sumcheck/coeff", 1),
+                        (b"sumcheck/factors", 3),
+                        (b"sumcheck/coeff", (cneg.bit_length() + 7) >> 3 or 1),
+                        (b"sumcheck/factors", 2)])
+            log += [(b"sumcheck/eval", (e.bit_length() + 7) >> 3 or 1) for e in ev]
+        o += n
+    return out
+
+
 def matmul_sumcheck(A, B, C, dims, tr):
     """The sumcheck of prove_matmul (gadgets.py:241-251), factored, on the GPU.
 

@@ -275,6 +275,50 @@ def test_matmul_factored_vs_oracle(field, dims, dt, mm_driver):
     assert t1.state == t2.state
 
 
+@pytest.mark.parametrize("field", ["big", "test"])
+def test_matmul_batch_matches_per_claim(field):
+    """matmul_sumcheck_batch (one native call, the next claim's draws and
+    matvecs queued behind the previous claim's last fold) against the
+    per-claim loop with the same transcript records: identical rounds,
+    points, finals, end state and transcript log; claims with empty
+    dimensions (d0 = 0, d1 = 0, d2 = 0), a false claim, and mixed integer
+    types, each checked against the oracle as well."""
+    p = FIELDS[field]
+    g = inputs.rng(31 + len(field))
+    specs = [((5, 9, 3), torch.int16), ((0, 10, 2), torch.int16), ((4, 6, 0), torch.int64),
+             ((8, 8, 8), torch.int16), ((7, 0, 7), torch.int32), ((6, 4, 9), torch.int16)]
+    claims, host = [], []
+    for i, (dims, tdt) in enumerate(specs):
+        d0, d1, d2 = dims
+        a = g.integers(-32768, 32768, size=(1 << d0, 1 << d1))
+        b = g.integers(-32768, 32768, size=(1 << d1, 1 << d2))
+        cm = a @ b
+        if i == 3:
+            cm[1, 2] -= 5  # a false claim
+        claims.append((_dev(a, tdt), _dev(b, tdt), _dev(cm, torch.int64), dims))
+        host.append((a, b, cm, dims))
+    pre = [[(b"gadget/tag", b"matmul"), (b"claim", b"%d" % i), (b"n", i * 1000 + 7)]
+           for i in range(len(claims))]
+    t1 = Transcript(b"batch", p, b"s")
+    got = zb.matmul_sumcheck_batch(claims, t1, pre)
+    t2 = Transcript(b"batch", p, b"s")
+    want = []
+    for c, recs in zip(claims, pre):
+        for label, data in recs:
+            t2.append(label, data)
+        want.append(zb.matmul_sumcheck(*c, t2))
+    assert got == want
+    assert t1.state == t2.state and t1.log == t2.log
+    t3 = fs.FS(b"batch", p, b"s")
+    for (a, b, cm, dims), recs, (rounds, point, finals) in zip(host, pre, got):
+        for label, data in recs:
+            t3.append(label, data)
+        orounds, ofinals, opoint = zkmat.prove_factored(a.reshape(-1), b.reshape(-1),
+                                                        cm.reshape(-1), dims, t3)
+        assert rounds == orounds and tuple(finals) == ofinals and point == opoint
+    assert t3.state == t1.state
+
+
 def _run_isolated(code, **env):
     import subprocess
     import sys
