@@ -17,7 +17,9 @@ static const uint64_t RC[24] = {
 // Keccak-f[1600], 25 lanes in registers, theta/rho/pi fused per lane
 // (b[y, 2x+3y] = rot(a[x,y] ^ d[x], rho[x,y])), then chi + iota.  ~1.3x the
 // speed of the table-driven loop; the transcript is on every round's
-// critical path (7 permutations per degree-3 round).
+// critical path (7 permutations per degree-3 round).  A second clone for
+// x86-64-v3 hosts (BMI2 rorx / andn), picked at load time through an ifunc.
+__attribute__((target_clones("default", "arch=x86-64-v3")))
 void keccak_f1600(uint64_t s[25]) {
   uint64_t a00=s[0],a01=s[1],a02=s[2],a03=s[3],a04=s[4],a05=s[5],a06=s[6],a07=s[7],a08=s[8],a09=s[9],
            a10=s[10],a11=s[11],a12=s[12],a13=s[13],a14=s[14],a15=s[15],a16=s[16],a17=s[17],a18=s[18],a19=s[19],
