@@ -1094,6 +1094,328 @@ __global__ void __launch_bounds__(256)
   y[i] = Fr255::sub(limb_reduce<CH>(acc), s_k);
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core int64 products (the zkMat C operands).  Each entry's offset-
+// binary value u = s + 2^63 is split into its 8 bytes (planes p = 0..7) and x
+// into its 32 bytes, so
+//   sum_c u_c x_c = sum_{p, m} 2^(8(p+m)) sum_c U_p[c] X_m[c],
+// one u8 x u8 GEMM per plane with M = the 32 x bytes (two m16 tiles, the A
+// operand from shared byte planes) and N = 8 matrix rows / columns per warp
+// (the B operand).  Every int32 sum is exact: < 255 * 255 * 512 < 2^25 per
+// 512-entry chunk.  The epilogue adds each lane's sums into per-position
+// totals in shared memory (position b = p + m, 39 of them per output), folds
+// them into ten 32-bit-spaced u64 limbs and red.adds those into the output's
+// record; k_mvt64_finish reduces the record mod p and subtracts
+// 2^63 * sum(x).  Per entry: one 8-byte load, 2 byte permutes, 16/32 MMA
+// slots -- the 32 carry-chained IMAD.WIDE of the wide-accumulator kernel
+// become a load stream.
+constexpr int kT64K = 512;             // entries of the reduction dimension per block
+constexpr int kT64Steps = kT64K / 32;  // k-steps of 32
+constexpr int kT64XP = kT64K + 16;     // x plane pitch (bytes)
+constexpr int kT64NW = 10;             // u64 limbs per output record
+
+// x[k0 .. k0+n) -> 32 byte planes (plane m holds byte m of every element),
+// zero past n; 128 threads, 4 elements each
+ZKL_D void t64_stage_x(const fr_t* x, uint64_t k0, int n, uint8_t* planes) {
+  for (int j4 = threadIdx.x * 4; j4 < kT64K; j4 += blockDim.x * 4) {
+    uint32_t w[4][8];
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const fr_t v = j4 + e < n ? x[k0 + j4 + e] : fr_t{};
+#pragma unroll
+      for (int l = 0; l < 8; l++) w[e][l] = v.v[l];
+    }
+#pragma unroll
+    for (int l = 0; l < 8; l++) {
+#pragma unroll
+      for (int b = 0; b < 4; b++) {
+        const uint32_t lo = __byte_perm(w[0][l], w[1][l], 0x0040 + b * 0x0011) & 0xffffu;
+        const uint32_t hi = __byte_perm(w[2][l], w[3][l], 0x0040 + b * 0x0011) & 0xffffu;
+        *reinterpret_cast<uint32_t*>(planes + (4 * l + b) * kT64XP + j4) = lo | (hi << 16);
+      }
+    }
+  }
+}
+
+// four int64 entries (words lo/hi) -> the 8 byte-plane registers of one B
+// half-fragment: reg p = byte p of e0..e3 (offset binary on plane 7)
+ZKL_D void t64_planes(const uint32_t (&lo)[4], const uint32_t (&hi)[4], uint32_t (&b)[8]) {
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    const uint32_t* w = h ? hi : lo;
+#pragma unroll
+    for (int q = 0; q < 2; q++) {  // planes 4h + 2q, 4h + 2q + 1
+      const uint32_t sel = (uint32_t)((2 * q) | ((2 * q + 4) << 4) | ((2 * q + 1) << 8) |
+                                      ((2 * q + 5) << 12));
+      const uint32_t t01 = __byte_perm(w[0], w[1], sel);  // e0.p, e1.p, e0.p+1, e1.p+1
+      const uint32_t t23 = __byte_perm(w[2], w[3], sel);
+      b[4 * h + 2 * q] = __byte_perm(t01, t23, 0x5410);
+      b[4 * h + 2 * q + 1] = __byte_perm(t01, t23, 0x7632);
+    }
+  }
+  b[7] ^= 0x80808080u;
+}
+
+// MMAs of one k-step: acc[p][mt] += X_planes(mt) x U_p
+ZKL_D void t64_mma(uint32_t (&acc)[8][2][4], const uint8_t* planes, int ks, int g, int tig,
+                   const uint32_t (&b0)[8], const uint32_t (&b1)[8]) {
+  uint32_t afr[2][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; mt++) {
+    const uint8_t* p0 = planes + (16 * mt + g) * kT64XP + ks * 32 + tig * 4;
+    const uint8_t* p1 = p0 + 8 * kT64XP;
+    afr[mt][0] = *reinterpret_cast<const uint32_t*>(p0);
+    afr[mt][1] = *reinterpret_cast<const uint32_t*>(p1);
+    afr[mt][2] = *reinterpret_cast<const uint32_t*>(p0 + 16);
+    afr[mt][3] = *reinterpret_cast<const uint32_t*>(p1 + 16);
+  }
+#pragma unroll
+  for (int p = 0; p < 8; p++)
+#pragma unroll
+    for (int mt = 0; mt < 2; mt++) mma_u8(acc[p][mt], afr[mt], b0[p], b1[p]);
+}
+
+// epilogue: lane (g, tig) holds D[m][n] for x bytes m = 16 mt + g (+ 8) and
+// outputs n = 2 tig, 2 tig + 1 of the warp's 8; position sums in shared
+// memory (distinct addresses per instruction), then limbs -> red.add
+ZKL_D void t64_epilogue(const uint32_t (&acc)[8][2][4], uint32_t* pos /* 8 x 40 */, int lane,
+                        int g, int tig, uint64_t out0, uint64_t nout, uint64_t* rec) {
+  for (int i = lane; i < 8 * 40; i += 32) pos[i] = 0;
+  __syncwarp();
+#pragma unroll
+  for (int p = 0; p < 8; p++)
+#pragma unroll
+    for (int mt = 0; mt < 2; mt++)
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const int m = 16 * mt + g + 8 * (q >> 1), n = 2 * tig + (q & 1);
+        atomicAdd(pos + n * 40 + m + p, acc[p][mt][q]);
+      }
+  __syncwarp();
+  for (int i = lane; i < 8 * kT64NW; i += 32) {
+    const int n = i / kT64NW, L = i % kT64NW;
+    const uint32_t* P = pos + n * 40 + 4 * L;
+    const uint64_t v = (uint64_t)P[0] + ((uint64_t)P[1] << 8) + ((uint64_t)P[2] << 16) +
+                       ((uint64_t)P[3] << 24);
+    if (out0 + n < nout && v)
+      atomicAdd(reinterpret_cast<unsigned long long*>(rec + (out0 + n) * kT64NW + L),
+                (unsigned long long)v);
+  }
+}
+
+// y_r = sum_c M[r][c] x_c: grid (rows / 32, ceil(cols / 512)), 4 warps x 8 rows
+__global__ void __launch_bounds__(128)
+    k_mvt64_rows(const int64_t* M, uint64_t rows, uint64_t cols, const fr_t* x, uint64_t* rec) {
+  __shared__ __align__(16) uint8_t planes[32 * kT64XP];
+  __shared__ uint32_t pos[4][8 * 40];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tig = lane & 3;
+  const uint64_t k0 = blockIdx.y * (uint64_t)kT64K;
+  const int n = (int)((k0 + kT64K < cols ? k0 + kT64K : cols) - k0);
+  const uint64_t r0 = blockIdx.x * 32ull + warp * 8;
+  const uint64_t row = r0 + g;
+  const bool live = row < rows;
+  const int64_t* base = M + (live ? row : 0) * cols + k0 + tig * 4;
+  // entries for k-step ks: columns 4 tig .. +3 and 16 + 4 tig .. +3 (32 B each)
+  auto load = [&](uint4 (&d)[4], int ks) {
+    const int c = ks * 32;
+    if (live && c + 32 <= n) {
+      const uint4* p = reinterpret_cast<const uint4*>(base + c);
+      d[0] = __ldcs(p);
+      d[1] = __ldcs(p + 1);
+      d[2] = __ldcs(p + 8);
+      d[3] = __ldcs(p + 9);
+    } else {
+      // ragged tail: u = 0 contributes nothing after the 2^63 correction,
+      // so pad with s = -2^63 (u = 0) and with x = 0 in the planes
+#pragma unroll
+      for (int h = 0; h < 4; h++) {
+        const int cc = c + (h >> 1) * 16 + tig * 4 + (h & 1) * 2;
+        int64_t v0 = (int64_t)0x8000000000000000ull, v1 = v0;
+        if (live && cc < n) v0 = base[c + (h >> 1) * 16 + (h & 1) * 2];
+        if (live && cc + 1 < n) v1 = base[c + (h >> 1) * 16 + (h & 1) * 2 + 1];
+        d[h] = make_uint4((uint32_t)v0, (uint32_t)((uint64_t)v0 >> 32), (uint32_t)v1,
+                          (uint32_t)((uint64_t)v1 >> 32));
+      }
+    }
+  };
+  uint4 cur[4], nxt[4];
+  load(cur, 0);
+  t64_stage_x(x, k0, n, planes);
+  __syncthreads();
+  if (blockIdx.x == 0) chunk_sum_atomic(x, k0, n, rec + rows * kT64NW);
+  uint32_t acc[8][2][4];
+#pragma unroll
+  for (int p = 0; p < 8; p++)
+#pragma unroll
+    for (int mt = 0; mt < 2; mt++)
+#pragma unroll
+      for (int q = 0; q < 4; q++) acc[p][mt][q] = 0;
+  const int steps = (n + 31) / 32;
+  for (int ks = 0; ks < steps; ks++) {
+    if (ks + 1 < steps) load(nxt, ks + 1);
+    uint32_t lo[4], hi[4], b0[8], b1[8];
+    lo[0] = cur[0].x; hi[0] = cur[0].y; lo[1] = cur[0].z; hi[1] = cur[0].w;
+    lo[2] = cur[1].x; hi[2] = cur[1].y; lo[3] = cur[1].z; hi[3] = cur[1].w;
+    t64_planes(lo, hi, b0);
+    lo[0] = cur[2].x; hi[0] = cur[2].y; lo[1] = cur[2].z; hi[1] = cur[2].w;
+    lo[2] = cur[3].x; hi[2] = cur[3].y; lo[3] = cur[3].z; hi[3] = cur[3].w;
+    t64_planes(lo, hi, b1);
+    t64_mma(acc, planes, ks, g, tig, b0, b1);
+#pragma unroll
+    for (int h = 0; h < 4; h++) cur[h] = nxt[h];
+  }
+  t64_epilogue(acc, pos[warp], lane, g, tig, r0, rows, rec);
+}
+
+// y_c = sum_r M[r][c] x_r: grid (cols / 32, ceil(rows / 512)), 4 warps x 8
+// columns; each k-step's 32 x 32 entry tile is staged in shared memory
+// (coalesced 16-byte loads, 272-byte row pitch: the four tig groups' 8-byte
+// column reads land on distinct banks)
+constexpr int kT64TP = 32 * 8 + 16;  // tile row pitch (bytes)
+
+__global__ void __launch_bounds__(128)
+    k_mvt64_cols(const int64_t* M, uint64_t rows, uint64_t cols, const fr_t* x, uint64_t* rec) {
+  __shared__ __align__(16) uint8_t planes[32 * kT64XP];
+  __shared__ __align__(16) uint8_t tile[2][32 * kT64TP];
+  __shared__ uint32_t pos[4][8 * 40];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tig = lane & 3;
+  const uint64_t k0 = blockIdx.y * (uint64_t)kT64K;  // first row of the chunk
+  const int n = (int)((k0 + kT64K < rows ? k0 + kT64K : rows) - k0);
+  const uint64_t c0 = blockIdx.x * 32ull;
+  // tile load: thread t takes rows t / 16 + 8 i (i < 4), 16 bytes at column pair 2 (t % 16)
+  const int tr = threadIdx.x >> 4, tc = (threadIdx.x & 15) * 2;
+  auto load = [&](uint4 (&d)[4], int ks) {
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const int r = ks * 32 + tr + 8 * i;
+      const uint64_t cc = c0 + tc;
+      if (r < n && cc + 1 < cols) {
+        d[i] = __ldcs(reinterpret_cast<const uint4*>(M + (k0 + r) * cols + cc));
+      } else {
+        const int64_t pad = (int64_t)0x8000000000000000ull;  // u = 0
+        const int64_t v0 = r < n && cc < cols ? M[(k0 + r) * cols + cc] : pad;
+        d[i] = make_uint4((uint32_t)v0, (uint32_t)((uint64_t)v0 >> 32), (uint32_t)pad,
+                          (uint32_t)((uint64_t)pad >> 32));
+      }
+    }
+  };
+  auto stash = [&](const uint4 (&d)[4], uint8_t* t) {
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+      *reinterpret_cast<uint4*>(t + (tr + 8 * i) * kT64TP + tc * 8) = d[i];
+  };
+  uint4 cur[4];
+  load(cur, 0);
+  t64_stage_x(x, k0, n, planes);
+  stash(cur, tile[0]);
+  __syncthreads();
+  if (blockIdx.x == 0) chunk_sum_atomic(x, k0, n, rec + cols * kT64NW);
+  uint32_t acc[8][2][4];
+#pragma unroll
+  for (int p = 0; p < 8; p++)
+#pragma unroll
+    for (int mt = 0; mt < 2; mt++)
+#pragma unroll
+      for (int q = 0; q < 4; q++) acc[p][mt][q] = 0;
+  const int steps = (n + 31) / 32;
+  const int col = warp * 8 + g;  // this lane's column within the tile
+  for (int ks = 0; ks < steps; ks++) {
+    const bool more = ks + 1 < steps;
+    if (more) load(cur, ks + 1);
+    const uint8_t* t = tile[ks & 1];
+    uint32_t lo[4], hi[4], b0[8], b1[8];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+#pragma unroll
+      for (int i = 0; i < 4; i++) {
+        const uint2 v = *reinterpret_cast<const uint2*>(t + (16 * h + 4 * tig + i) * kT64TP + col * 8);
+        lo[i] = v.x;
+        hi[i] = v.y;
+      }
+      t64_planes(lo, hi, h ? b1 : b0);
+    }
+    t64_mma(acc, planes, ks, g, tig, b0, b1);
+    if (more) stash(cur, tile[(ks + 1) & 1]);
+    __syncthreads();
+  }
+  t64_epilogue(acc, pos[warp], lane, g, tig, c0 + warp * 8, cols, rec);
+}
+
+// y[i] = reduce(sum_L rec[i][L] 2^(32 L)) - 2^63 sum(x)
+__global__ void __launch_bounds__(256)
+    k_mvt64_finish(const uint64_t* rec, uint64_t n, const uint64_t* sumx, fr_t offr, fr_t* y) {
+  __shared__ fr_t s_k;
+  if (threadIdx.x == 0) {
+    LimbAcc<1> sa;
+#pragma unroll
+    for (int l = 0; l < 8; l++) sa.e[l] = sumx[l];
+    s_k = Fr255::mul(limb_reduce<1>(sa), offr);
+  }
+  __syncthreads();
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  // u64 limbs at 32-bit spacing -> 12 words with carries
+  uint32_t w[12];
+  uint64_t carry = 0;
+#pragma unroll
+  for (int j = 0; j < 12; j++) {
+    uint64_t t = carry;
+    if (j < kT64NW) t += (uint32_t)rec[i * kT64NW + j];
+    if (j >= 1 && j - 1 < kT64NW) t += rec[i * kT64NW + j - 1] >> 32;
+    w[j] = (uint32_t)t;
+    carry = t >> 32;
+  }
+  fr_t lo, hi = Fr255::zero();
+#pragma unroll
+  for (int j = 0; j < 8; j++) lo.v[j] = w[j];
+#pragma unroll
+  for (int j = 8; j < 12; j++) hi.v[j - 8] = w[j];
+  lo = Fr255::reduce_once(Fr255::reduce_once(lo));
+  hi = Fr255::mul(hi, Fr255::r2());
+  y[i] = Fr255::sub(Fr255::add(lo, hi), s_k);
+}
+
+static bool t64_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("ZKL_MV_TC64");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
+// int64 matrix x Fr vector on the tensor cores; kErrUnsupported when the
+// reduction dimension exceeds the record headroom
+static int matvec_t64(const int64_t* M, uint64_t rows, uint64_t cols, int transpose,
+                      const fr_t* x, fr_t* y, cudaStream_t s) {
+  const uint64_t klen = transpose ? rows : cols, nout = transpose ? cols : rows;
+  // limb headroom: ceil(klen / 512) <= 2^11 chunks x < 2^53 each stays below
+  // 2^64; 16-byte loads need an even row length and an aligned base
+  if (klen > (1ull << 20) || (cols & 1) || ((uintptr_t)M & 15)) return kErrUnsupported;
+  void* ws;
+  const size_t bytes = (nout * kT64NW + 8) * 8;
+  int rc = scratch_reserve(bytes + 64, &ws, s);
+  if (rc) return rc;
+  ZKL_CUDA(cudaMemsetAsync(ws, 0, bytes, s));
+  uint64_t* rec = (uint64_t*)ws;
+  dim3 g((unsigned)((nout + 31) / 32), (unsigned)((klen + kT64K - 1) / kT64K));
+  if (transpose)
+    k_mvt64_cols<<<g, 128, 0, s>>>(M, rows, cols, x, rec);
+  else
+    k_mvt64_rows<<<g, 128, 0, s>>>(M, rows, cols, x, rec);
+  ZKL_LAUNCH_CHECK();
+  static fr_t offr = [] {
+    fr_t v = Fr255::zero();
+    v.v[1] = 1u << 31;  // 2^63
+    return Fr255::to_mont(v);
+  }();
+  k_mvt64_finish<<<(unsigned)((nout + 255) / 256), 256, 0, s>>>(rec, nout, rec + nout * kT64NW,
+                                                                 offr, y);
+  ZKL_LAUNCH_CHECK();
+  return kOk;
+}
+
 // returns kErrUnsupported when the shape does not suit the fast kernels
 template <class MT>
 static int matvec_fast(const MT* M, uint64_t rows, uint64_t cols, int transpose, const fr_t* x,
@@ -1354,6 +1676,11 @@ int op_matvec(int mtype, const void* M, uint64_t rows, uint64_t cols, int transp
     case 2: return matvec_impl<F, int32_t>(M, rows, cols, transpose, x, y, s);
     case 3:
       if constexpr (F::kId == 0) {
+        if (fast_enabled() && t64_enabled()) {
+          int rc = matvec_t64((const int64_t*)M, rows, cols, transpose, (const fr_t*)x, (fr_t*)y,
+                              s);
+          if (rc != kErrUnsupported) return rc;
+        }
         if (fast_enabled() && getenv("ZKL_MATVEC_FAST64")) {
           int rc = matvec_fast<int64_t>((const int64_t*)M, rows, cols, transpose,
                                         (const fr_t*)x, (fr_t*)y, s);

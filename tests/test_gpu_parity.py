@@ -364,11 +364,14 @@ def test_profile_replay_mode_matches_oracle():
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
 
 
-@pytest.mark.parametrize("env", [{"ZKL_MATVEC_SLOW": "1"}, {"ZKL_MATVEC_FAST64": "1"}])
+@pytest.mark.parametrize("env", [{"ZKL_MATVEC_SLOW": "1"},
+                                 {"ZKL_MV_TC64": "0", "ZKL_MATVEC_FAST64": "1"},
+                                 {"ZKL_MV_TC64": "0"}, {"ZKL_MV_TC": "0"}])
 def test_matvec_alternate_kernels_vs_numpy(env):
-    """The non-default matvec kernels (wide-accumulator everywhere, or the
-    mad.wide form for int64 too; the switches are read once per process)
-    against exact numpy products, in a child process."""
+    """The non-default matvec kernels (wide-accumulator everywhere; int64 on
+    mad.wide or on the wide-accumulator kernels instead of the tensor cores;
+    int16 on mad.wide; the switches are read once per process) against exact
+    numpy products, in a child process."""
     code = (
         "import sys; sys.path[:0] = ['.', 'tests', 'tests/golden']\n"
         "import test_gpu_parity as T\n"
@@ -382,7 +385,8 @@ def test_matvec_alternate_kernels_vs_numpy(env):
 
 @pytest.mark.parametrize("field", ["big", "test"])
 @pytest.mark.parametrize("mt", ["i16", "i32", "i64"])
-@pytest.mark.parametrize("shape", [(1, 1), (3, 70), (64, 5), (1024, 256), (33, 4096)])
+@pytest.mark.parametrize("shape", [(1, 1), (3, 70), (64, 5), (1024, 256), (33, 4096),
+                                   (40, 1030)])
 def test_matvec_extremes_vs_numpy(field, mt, shape):
     from paper_2508_21393_b200.gadgets import _matvec
 

@@ -17,7 +17,7 @@ spec = D.FR
 rows, cols = 2048, 4096
 g = torch.Generator(device="cuda").manual_seed(5)
 M = torch.randint(-(1 << 42), 1 << 42, (rows, cols), device="cuda", generator=g, dtype=torch.int64)
-out = {"variant": "fast64" if os.environ.get("ZKL_MATVEC_FAST64") else "wide-accumulator"}
+out = {"variant": "wide-accumulator" if os.environ.get("ZKL_MV_TC64") == "0" else "tensor cores"}
 for tr, n_in, n_out in ((0, cols, rows), (1, rows, cols)):
     x = D.upload([(i * 7919 + 13) ** 5 for i in range(n_in)], spec)
     y = D.empty(spec, n_out)
