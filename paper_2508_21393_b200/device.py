@@ -226,9 +226,10 @@ def as_list(values):
 _INT_TYPES = {torch.int16: N.MT_I16, torch.int32: N.MT_I32, torch.int64: N.MT_I64}
 
 
-def igemm16(a, b):
+def igemm16(a, b, out=None):
     """Exact int64 a @ b for int16 CUDA matrices (zkl_igemm_i16: byte-sliced
-    tensor-core GEMM, int64 accumulation)."""
+    tensor-core GEMM, int64 accumulation); `out` an optional preallocated
+    contiguous int64 result."""
     a, b = a.contiguous(), b.contiguous()
     if a.dtype != torch.int16 or b.dtype != torch.int16 or a.dim() != 2 or b.dim() != 2:
         raise TypeError("igemm16 takes two int16 matrices")
@@ -236,7 +237,12 @@ def igemm16(a, b):
     K2, Nn = b.shape
     if K != K2:
         raise ValueError("igemm16: inner dimensions %d and %d differ" % (K, K2))
-    c = torch.empty((M, Nn), dtype=torch.int64, device=a.device)
+    if out is None:
+        c = torch.empty((M, Nn), dtype=torch.int64, device=a.device)
+    else:
+        if out.shape != (M, Nn) or out.dtype != torch.int64 or not out.is_contiguous():
+            raise ValueError("igemm16: out must be a contiguous %dx%d int64 tensor" % (M, Nn))
+        c = out
     if M and Nn:
         N.check(N.lib().zkl_igemm_i16(ptr(a), ptr(b), ptr(c), M, K, Nn, stream()))
     return c
