@@ -100,7 +100,7 @@ CFG2_MATS = [("Hw=X.A", "X", "AL"), ("Y2=H.B", "H", "BL"), ("Y1=X.W", "X", "W"),
              ("dA=Xt.G", "X^T", "G"), ("dB=Ht.dY", "H^T", "dY")]
 
 
-def cfg2_layer_claims(X, W, AL, BL, dY, exact, need=None):
+def cfg2_layer_claims(X, W, AL, BL, dY, exact, need=None, keep=None):
     """The 8 zkMat claims of cfg2's LoRA projection (fwd + bwd) from the layer
     tensors, yielded one at a time: the narrowed intermediates H = X A_L and
     G = dY B_L^T and each claim's product C = A B are computed (by `exact`)
@@ -110,13 +110,23 @@ def cfg2_layer_claims(X, W, AL, BL, dY, exact, need=None):
     need = need or (lambda name: None)
     t = {"X": X, "W": W, "AL": AL, "BL": BL, "dY": dY}
 
+    def stable(name, v):  # keep: derived tensors in buffers reused across steps
+        if keep is None:
+            return v.contiguous()
+        buf = keep.get(name)
+        if buf is None:
+            buf = keep[name] = torch.empty(v.shape, dtype=v.dtype, device=v.device)
+        return buf.copy_(v)
+
     def get(name):
         base = name[:-2] if name.endswith("^T") else name
         if base not in t:  # H = narrow(X A_L), G = narrow(dY B_L^T)
             src = ("X", "AL") if base == "H" else ("dY", "BL^T")
-            t[base] = narrow16(exact(get(src[0]), get(src[1]).contiguous()))
+            t[base] = stable(base, narrow16(exact(get(src[0]), get(src[1]).contiguous())))
         need(base)
-        return t[base].t() if name.endswith("^T") else t[base]
+        return stable(name, t[base].t()) if name.endswith("^T") else t[base]
+
+    import torch
 
     for name, an, bn in CFG2_MATS:
         a = get(an).contiguous()
@@ -832,6 +842,7 @@ def main():
     # the timed steps write their products into buffers allocated once (a
     # caching-allocator miss inside a step would cudaMalloc / cudaFree)
     prod_bufs = {}
+    derived = {}  # H, G and the transposed operands, same buffers every step
     calls = [0]  # products so far in this step (10 per step, in a fixed order)
 
     def igemm_into(a, b):
@@ -887,7 +898,7 @@ def main():
 
         X_d, W_d, AL_d, BL_d, dY_d = layer_dev
         calls[0] = 0
-        gen = cfg2_layer_claims(X_d, W_d, AL_d, BL_d, dY_d, igemm_into, need=need)
+        gen = cfg2_layer_claims(X_d, W_d, AL_d, BL_d, dY_d, igemm_into, need=need, keep=derived)
         prove_step_batched([itertools.islice(gen, 2), gen], seed, zb)
 
     e2e_value = e2e_run(from_layer, args.steps, 200)

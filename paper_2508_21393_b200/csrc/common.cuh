@@ -143,6 +143,8 @@ int scratch_reserve(size_t bytes, void** out, cudaStream_t s);
 int pinned_reserve(size_t bytes, void** out);
 // driver work arena (stream-ordered; grows by sync + realloc)
 int work_reserve(size_t bytes, void** out, cudaStream_t s);
+// changes whenever a scratch / work arena is reallocated (graph validity)
+uint64_t arena_generation();
 // fixed device words (zero-initialised once per device)
 int fixed_words(void** out);
 constexpr size_t kFixedTicket = 0;    // u32, k_round last-block ticket (self-resetting)

@@ -26,6 +26,9 @@ void set_error(const char* fmt, ...) {
 }
 const char* get_error() { return g_err; }
 
+// bumped whenever a scratch or work arena moves: device pointers captured in a
+// CUDA graph (zkmat.cu) are valid only for the generation they were taken in
+static uint64_t g_arena_gen = 0;
 static std::map<int, Scratch>& arenas() {
   static std::map<int, Scratch> m;
   return m;
@@ -69,10 +72,12 @@ int scratch_reserve(size_t bytes, void** out, cudaStream_t s) {
     size_t want = bytes < (1u << 20) ? (1u << 20) : bytes + bytes / 4;
     ZKL_CUDA(cudaMalloc(&a.ptr, want));
     a.bytes = want;
+    ++g_arena_gen;
   }
   *out = a.ptr;
   return kOk;
 }
+uint64_t arena_generation() { return g_arena_gen; }
 // ---------------------------------------------------------------------------
 // CUDA-event profiler
 struct ProfRec {
@@ -161,6 +166,7 @@ int work_reserve(size_t bytes, void** out, cudaStream_t s) {
     size_t want = bytes < (1u << 20) ? (1u << 20) : bytes + bytes / 4;
     ZKL_CUDA(cudaMalloc(&a.work, want));
     a.work_bytes = want;
+    ++g_arena_gen;
   }
   *out = a.work;
   return kOk;
@@ -553,11 +559,6 @@ int op_lift(void* dst, const void* src, int mtype, uint64_t n, cudaStream_t s) {
 // eq table: eq[idx] = prod_j (bit_{m-1-j}(idx) ? r_j : 1 - r_j)   (mle.py:67-82)
 // Two-level: eq = hi (x) lo with hi over the first mh coordinates.
 template <class F>
-struct PointArg {
-  typename F::T r[kMaxPoint];
-  typename F::T omr[kMaxPoint];  // 1 - r
-};
-template <class F>
 __global__ void k_eq_direct(typename F::T* dst, PointArg<F> pt, int off, int m) {
   uint64_t n = 1ull << m;
   // two interleaved product chains (first / second half of the coordinates)
@@ -596,8 +597,7 @@ __global__ void k_eq_outer(typename F::T* dst, const typename F::T* hi, const ty
 // values as a balanced tree.  ~4 dependent Montgomery products for m = 12
 // instead of m/2 in the two-chain direct form.
 template <class F>
-__global__ void __launch_bounds__(256) k_eq_tree(typename F::T* dst, PointArg<F> pt, int off,
-                                                 int m) {
+ZKL_D void eq_tree_body(typename F::T* dst, const PointArg<F>& pt, int off, int m) {
   using T = typename F::T;
   __shared__ T grp[8][4];
   const int G = (m + 1) / 2;
@@ -644,6 +644,24 @@ __global__ void __launch_bounds__(256) k_eq_tree(typename F::T* dst, PointArg<F>
       dst[i] = v[0];
     }
   }
+}
+template <class F>
+__global__ void __launch_bounds__(256) k_eq_tree(typename F::T* dst, PointArg<F> pt, int off,
+                                                 int m) {
+  eq_tree_body<F>(dst, pt, off, m);
+}
+// the point read from device memory (a graph node refreshes it per replay)
+template <class F>
+__global__ void __launch_bounds__(256) k_eq_tree_dev(typename F::T* dst, const PointArg<F>* pt,
+                                                     int m) {
+  eq_tree_body<F>(dst, *pt, 0, m);
+}
+template <class F>
+int op_eq_table_dev(void* dst, const PointArg<F>* pt_dev, int m, cudaStream_t s) {
+  if (m < 1 || m > 16) { set_error("eq_table_dev: m=%d unsupported", m); return kErrArg; }
+  k_eq_tree_dev<F><<<grid_for(1ull << m, 256), 256, 0, s>>>((typename F::T*)dst, pt_dev, m);
+  ZKL_LAUNCH_CHECK();
+  return kOk;
 }
 
 template <class F>
@@ -978,6 +996,7 @@ int op_rescale_witness(const void* wide, int wide_type, uint64_t n, int64_t divi
   template int op_mul<F>(void*, const void*, const void*, uint64_t, cudaStream_t);          \
   template int op_read<F>(uint8_t*, const void*, uint64_t, cudaStream_t);                 \
   template int op_dot<F>(F::T*, const void*, const void*, uint64_t, cudaStream_t);          \
+  template int op_eq_table_dev<F>(void*, const PointArg<F>*, int, cudaStream_t);             \
   template int op_expand<F>(void*, uint64_t, const void*, uint64_t, int, F::T, F::T,        \
                             cudaStream_t);                                                  \
   template int op_lift_u32<F>(void*, const uint32_t*, uint64_t, cudaStream_t);                \

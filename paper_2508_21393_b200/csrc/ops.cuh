@@ -19,6 +19,15 @@ int op_pair_combine(void* dst, const void* x, int tx, const void* y, int ty, uin
                     typename F::T alpha, cudaStream_t s);
 template <class F>
 int op_eq_table(void* dst, const typename F::T* point, int m, cudaStream_t s);
+// an eq point as kernels take it: r and 1 - r in storage form
+template <class F>
+struct PointArg {
+  typename F::T r[kMaxPoint];
+  typename F::T omr[kMaxPoint];
+};
+// eq table from a device-resident point (m <= 16)
+template <class F>
+int op_eq_table_dev(void* dst, const PointArg<F>* pt_dev, int m, cudaStream_t s);
 template <class F>
 int op_fold(void* dst, const void* src, uint64_t half, typename F::T r, cudaStream_t s);
 // y = a + k * b

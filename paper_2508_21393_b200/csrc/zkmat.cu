@@ -14,6 +14,8 @@
 // host only runs the transcript (persistent.cu) and reads back kappa through
 // an event while the next phase's kernel is already queued.
 #include <chrono>
+#include <functional>
+#include <map>
 #include <cstdlib>
 #include <vector>
 
@@ -62,6 +64,124 @@ static void absorb_elem(HostTranscript& tr, const char* label, const typename F:
   tr.append_elem(label, b, F::kBytes);
 }
 
+// ---------------------------------------------------------------------------
+// The phase-input sequences (eq tables, matvecs on two streams, small vector
+// ops) are host-paced: a dozen launches and event calls per phase, each a
+// few microseconds of host time, while the GPU work between them is shorter.
+// They are replayed as CUDA graphs instead.  A sequence runs eagerly the first
+// time it is seen for a set of operands and buffers (so every arena reaches
+// its size), is captured the second time, and replayed after that; the eq
+// points travel through pinned host slots copied to device memory by a node
+// of the graph.  The profiler's event brackets and ZKL_TRACE need the eager
+// path; ZKL_NO_GRAPHS=1 forces it.
+struct GraphKey {
+  int field, which, ta, tb, tc, d0, d1, d2, slot;
+  const void *A, *B, *C, *base;
+  cudaStream_t s;
+  uint64_t gen;
+};
+struct GraphEntry {
+  GraphKey key;
+  cudaGraphExec_t exec = nullptr;
+  int seen = 0;
+  unsigned long long launches = 0;  // kernels inside (zkl_launch_count)
+};
+static std::vector<GraphEntry>& graph_cache() {
+  static std::vector<GraphEntry> v;
+  return v;
+}
+static bool graphs_allowed() {
+  static const bool env_off = getenv("ZKL_NO_GRAPHS") != nullptr || getenv("ZKL_TRACE") != nullptr;
+  return !env_off && !prof_on();
+}
+// a per-device stream to capture on (the caller's stream may be the legacy
+// default stream, which cannot capture; the graph is launched on it)
+static cudaStream_t capture_stream() {
+  static std::map<int, cudaStream_t> m;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaStream_t& st = m[dev];
+  if (!st) cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  return st;
+}
+// run body() through the cache entry for key: eagerly on s, or captured on
+// the capture stream (set_stream(cs) points the body at it) and launched on s
+template <class Body, class SetStream>
+static int run_graphed(GraphKey key, cudaStream_t s, Body&& body, SetStream&& set_stream) {
+  key.gen = arena_generation();
+  auto& cache = graph_cache();
+  GraphEntry* e = nullptr;
+  for (auto& c : cache)
+    if (!memcmp(&c.key, &key, sizeof(key))) e = &c;
+  if (!e) {
+    if (cache.size() >= 256) {  // bounded: drop the oldest half
+      for (size_t i = 0; i < cache.size() / 2; i++)
+        if (cache[i].exec) cudaGraphExecDestroy(cache[i].exec);
+      cache.erase(cache.begin(), cache.begin() + cache.size() / 2);
+    }
+    cache.push_back(GraphEntry());
+    e = &cache.back();
+    e->key = key;
+  }
+  if (e->exec) {
+    ZKL_CUDA(cudaGraphLaunch(e->exec, s));
+    g_launches += e->launches;
+    return kOk;
+  }
+  if (e->seen++ == 0) return body();  // eager: arenas and lazy state settle
+  const unsigned long long l0 = g_launches;
+  const cudaStream_t cs = capture_stream();
+  ZKL_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+  set_stream(cs);
+  const int rc = body();
+  set_stream(s);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+  if (rc || ce != cudaSuccess || arena_generation() != key.gen) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    if (rc) return rc;
+    return body();  // capture failed or an arena moved: run it eagerly
+  }
+  cudaGraphExec_t exec = nullptr;
+  ZKL_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  cudaGraphDestroy(graph);
+  e->exec = exec;
+  e->launches = g_launches - l0;
+  g_launches = l0;
+  ZKL_CUDA(cudaGraphLaunch(exec, s));
+  g_launches += e->launches;
+  return kOk;
+}
+
+// mapped pinned host slots for the eq points of the graphed sequences,
+// [job parity][point] (a batch has two claims in flight): the eq kernel reads
+// its point straight from host memory when it runs (one PCIe read per block,
+// no copy-engine hop in front of it)
+template <class F>
+struct PointSlots {
+  PointArg<F>* host = nullptr;
+  PointArg<F>* dev = nullptr;  // the same memory, device view
+  static constexpr int kN = 2 * 4;
+  int ensure() {
+    if (!host) {
+      ZKL_CUDA(cudaHostAlloc((void**)&host, kN * sizeof(PointArg<F>), cudaHostAllocMapped));
+      ZKL_CUDA(cudaHostGetDevicePointer((void**)&dev, host, 0));
+    }
+    return kOk;
+  }
+};
+
+// 32 bytes device -> mapped host memory by a kernel (kappa for the host)
+__global__ void k_to_host32(uint4* dst, const uint4* src) {
+  if (threadIdx.x < 2) dst[threadIdx.x] = src[threadIdx.x];
+}
+template <class F>
+static PointSlots<F>& point_slots() {
+  static thread_local PointSlots<F> p;
+  return p;
+}
+
 // One claim's prover state.  begin() draws r_u / r_v, absorbs the claim and
 // enqueues the U-phase inputs; prove() runs the U, W and V phases and returns
 // once the last challenge is published (the V phase's finals still in
@@ -96,6 +216,31 @@ struct MatmulJob {
   T e_hat{}, alpha_s{}, fin_v[3] = {};
   bool have_e_hat = false, have_alpha = false;
   uint8_t *rounds = nullptr, *point = nullptr;
+  int slot = 0;          // point-slot parity (a batch alternates it per claim)
+  bool graphed = false;  // phase inputs through the CUDA-graph cache
+
+  GraphKey key_for(int which) const {
+    GraphKey k;
+    memset(&k, 0, sizeof(k));
+    k.field = F::kId;
+    k.which = which; k.ta = ta; k.tb = tb; k.tc = tc; k.d0 = d0; k.d1 = d1; k.d2 = d2;
+    k.slot = slot; k.A = A; k.B = B; k.C = C; k.base = base; k.s = s;
+    return k;
+  }
+  // point p of this job's slot: host copy (filled now) and device copy (a
+  // memcpy node refreshes it when the graph runs)
+  PointArg<F>* host_pt(int p) { return point_slots<F>().host + slot * 4 + p; }
+  PointArg<F>* dev_pt(int p) { return point_slots<F>().dev + slot * 4 + p; }
+  void fill_point(int p, const uint8_t* canon, int m) {
+    PointArg<F>* h = host_pt(p);
+    for (int i = 0; i < m; i++) {
+      h->r[i] = host::from_canon<F>(canon + (size_t)i * nb);
+      h->omr[i] = H::sub(H::one(), h->r[i]);
+    }
+  }
+  int eq_dev_on(cudaStream_t st, T* dst, int p, int m) {
+    return op_eq_table_dev<F>(dst, dev_pt(p), m, st);
+  }
 
   // ZKL_TRACE: host and GPU timestamps at the phase boundaries (stderr)
   bool tracing = false;
@@ -203,6 +348,10 @@ struct MatmulJob {
     static thread_local T* p = nullptr;
     return p;
   }
+  static T*& kap_dev() {
+    static thread_local T* p = nullptr;
+    return p;
+  }
   static cudaEvent_t& kap_ev() {
     static thread_local cudaEvent_t e = nullptr;
     return e;
@@ -256,17 +405,36 @@ struct MatmulJob {
     if (rc) return rc;
     base = (T*)wsv;
     // ---- U phase inputs: E_v, bv = B E_v, cv = C E_v, h = A bv - cv
-    if ((rc = eq(buf(EV), load_point(rv.data(), d2), d2))) return rc;
-    gmark(1);
-    // side: cv = C E_v and E_u; main: bv = B E_v, abv = A bv; then h = abv - cv
-    if ((rc = fork())) return rc;
-    if ((rc = mv_on(side_stream(), tc, C, D0, D2, 0, buf(EV), buf(CV)))) return rc;  // cv
-    if ((rc = eq_on(side_stream(), buf(EU), load_point(ru.data(), d0), d0))) return rc;
-    if ((rc = mv(tb, B, D1, D2, 0, buf(EV), buf(BV)))) return rc;
-    if ((rc = mv(ta, A, D0, D1, 0, buf(BV), buf(HV)))) return rc;  // abv
-    if ((rc = join())) return rc;
-    if ((rc = op_axpy<F>(buf(HV), buf(HV), H::sub(H::zero(), H::one()), buf(CV), D0, s)))
+    graphed = graphs_allowed() && d0 >= 1 && d0 <= 16 && d1 >= 1 && d1 <= 16 && d2 >= 1 &&
+              d2 <= 16 && point_slots<F>().ensure() == kOk;
+    auto u_inputs = [&]() -> int {
+      int r;
+      if (graphed) {
+        if ((r = eq_dev_on(s, buf(EV), 0, d2))) return r;
+      } else if ((r = eq(buf(EV), load_point(rv.data(), d2), d2))) {
+        return r;
+      }
+      gmark(1);
+      // side: cv = C E_v and E_u; main: bv = B E_v, abv = A bv; then h = abv - cv
+      if ((r = fork())) return r;
+      if (graphed) {
+        if ((r = eq_dev_on(side_stream(), buf(EU), 1, d0))) return r;
+      } else if ((r = eq_on(side_stream(), buf(EU), load_point(ru.data(), d0), d0))) {
+        return r;
+      }
+      if ((r = mv_on(side_stream(), tc, C, D0, D2, 0, buf(EV), buf(CV)))) return r;  // cv
+      if ((r = mv(tb, B, D1, D2, 0, buf(EV), buf(BV)))) return r;
+      if ((r = mv(ta, A, D0, D1, 0, buf(BV), buf(HV)))) return r;  // abv
+      if ((r = join())) return r;
+      return op_axpy<F>(buf(HV), buf(HV), H::sub(H::zero(), H::one()), buf(CV), D0, s);
+    };
+    if (graphed) {
+      fill_point(0, rv.data(), d2);
+      fill_point(1, ru.data(), d0);
+      if ((rc = run_graphed(key_for(0), s, u_inputs, [this](cudaStream_t st) { s = st; }))) return rc;
+    } else if ((rc = u_inputs())) {
       return rc;
+    }
     mark(1);
     gmark(2);
     return kOk;
@@ -298,19 +466,37 @@ struct MatmulJob {
     mark(2);
     gmark(3);
     // ---- W phase inputs: E(rho_u), a = E^T A, cu = E^T C, kappa = <cu, E_v>
-    if ((rc = eq(buf(ERU), load_point(point, d0), d0))) return rc;
-    rounds += (size_t)d0 * 4 * nb;
-    point += (size_t)d0 * nb;
-    if ((rc = fork())) return rc;
-    if ((rc = mv_on(side_stream(), tc, C, D0, D2, 1, buf(ERU), buf(CU)))) return rc;  // cu
-    if ((rc = mv(ta, A, D0, D1, 1, buf(ERU), buf(AV)))) return rc;
-    if ((rc = join())) return rc;
-    if ((rc = op_dot<F>(buf(KAP), buf(CU), buf(EV), D2, s))) return rc;
     if (!kap_host()) {
-      ZKL_CUDA(cudaHostAlloc((void**)&kap_host(), 64, cudaHostAllocDefault));
+      ZKL_CUDA(cudaHostAlloc((void**)&kap_host(), 64, cudaHostAllocMapped));
+      ZKL_CUDA(cudaHostGetDevicePointer((void**)&kap_dev(), kap_host(), 0));
       ZKL_CUDA(cudaEventCreateWithFlags(&kap_ev(), cudaEventDisableTiming));
     }
-    ZKL_CUDA(cudaMemcpyAsync(kap_host(), buf(KAP), sizeof(T), cudaMemcpyDeviceToHost, s));
+    const uint8_t* rho_u = point;
+    auto w_inputs = [&]() -> int {
+      int r;
+      if (graphed) {
+        if ((r = eq_dev_on(s, buf(ERU), 2, d0))) return r;
+      } else if ((r = eq(buf(ERU), load_point(rho_u, d0), d0))) {
+        return r;
+      }
+      if ((r = fork())) return r;
+      if ((r = mv_on(side_stream(), tc, C, D0, D2, 1, buf(ERU), buf(CU)))) return r;  // cu
+      if ((r = mv(ta, A, D0, D1, 1, buf(ERU), buf(AV)))) return r;
+      if ((r = join())) return r;
+      if ((r = op_dot<F>(buf(KAP), buf(CU), buf(EV), D2, s))) return r;
+      k_to_host32<<<1, 32, 0, s>>>(reinterpret_cast<uint4*>(kap_dev()),
+                                   reinterpret_cast<const uint4*>(buf(KAP)));
+      ZKL_LAUNCH_CHECK();
+      return kOk;
+    };
+    if (graphed) {
+      fill_point(2, rho_u, d0);
+      if ((rc = run_graphed(key_for(1), s, w_inputs, [this](cudaStream_t st) { s = st; }))) return rc;
+    } else if ((rc = w_inputs())) {
+      return rc;
+    }
+    rounds += (size_t)d0 * 4 * nb;
+    point += (size_t)d0 * nb;
     ZKL_CUDA(cudaEventRecord(kap_ev(), s));
     mark(3);
     gmark(4);
@@ -344,10 +530,24 @@ struct MatmulJob {
     mark(4);
     gmark(5);
     // ---- V phase inputs: E(rho_w), bw = E^T B
-    if ((rc = eq(buf(ERW), load_point(point, d1), d1))) return rc;
+    const uint8_t* rho_w = point;
+    auto v_inputs = [&]() -> int {
+      int r;
+      if (graphed) {
+        if ((r = eq_dev_on(s, buf(ERW), 3, d1))) return r;
+      } else if ((r = eq(buf(ERW), load_point(rho_w, d1), d1))) {
+        return r;
+      }
+      return mv(tb, B, D1, D2, 1, buf(ERW), buf(BW));
+    };
+    if (graphed) {
+      fill_point(3, rho_w, d1);
+      if ((rc = run_graphed(key_for(2), s, v_inputs, [this](cudaStream_t st) { s = st; }))) return rc;
+    } else if ((rc = v_inputs())) {
+      return rc;
+    }
     rounds += (size_t)d1 * 4 * nb;
     point += (size_t)d1 * nb;
-    if ((rc = mv(tb, B, D1, D2, 1, buf(ERW), buf(BW)))) return rc;
     mark(5);
     gmark(6);
     if (d2) {
@@ -498,6 +698,7 @@ int op_matmul_prove_batch(int nclaims, const int* types, const void* const* mats
     poff += (size_t)(d[0] + d[1] + d[2]);
     j.s = s;
     j.tr = &tr;
+    j.slot = i & 1;
     if (pre && pre_off) {
       const int r = append_records(tr, pre + pre_off[i], pre_off[i + 1] - pre_off[i]);
       if (r) {
