@@ -650,11 +650,22 @@ __global__ void __launch_bounds__(256) k_eq_tree(typename F::T* dst, PointArg<F>
                                                  int m) {
   eq_tree_body<F>(dst, pt, off, m);
 }
-// the point read from device memory (a graph node refreshes it per replay)
+// the point read from memory the host rewrites between graph replays (mapped
+// host memory: one parallel burst of 4-byte loads into shared memory, so the
+// PCIe round trip is paid once per block, not per dependent read)
 template <class F>
 __global__ void __launch_bounds__(256) k_eq_tree_dev(typename F::T* dst, const PointArg<F>* pt,
                                                      int m) {
-  eq_tree_body<F>(dst, *pt, 0, m);
+  __shared__ PointArg<F> sp;
+  constexpr int kW = sizeof(typename F::T) / 4;
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(pt);
+  uint32_t* d = reinterpret_cast<uint32_t*>(&sp);
+  for (int i = threadIdx.x; i < 2 * m * kW; i += blockDim.x) {
+    const int w = i < m * kW ? i : kMaxPoint * kW + (i - m * kW);  // r[0..m), then omr[0..m)
+    d[w] = src[w];
+  }
+  __syncthreads();
+  eq_tree_body<F>(dst, sp, 0, m);
 }
 template <class F>
 int op_eq_table_dev(void* dst, const PointArg<F>* pt_dev, int m, cudaStream_t s) {
