@@ -121,7 +121,7 @@ ZKL_D void stash(const Regs& R, int16_t* st, int tid) {
 
 __global__ void __launch_bounds__(256)
     k_igemm16(const int16_t* __restrict__ A, const int16_t* __restrict__ B,
-              int64_t* __restrict__ C, int M, int K, int N) {
+              int64_t* __restrict__ C, int M, int K, int N, int kslice) {
   extern __shared__ __align__(16) int16_t smem[];  // 2 stages
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tig = lane & 3;
@@ -136,8 +136,12 @@ __global__ void __launch_bounds__(256)
     for (int j = 0; j < 4; j++)
 #pragma unroll
       for (int q = 0; q < 4; q++) tot[i][j][q] = 0;
-  for (int kc = 0; kc < K; kc += kKChunk) {
-    const int kend = kc + kKChunk < K ? kc + kKChunk : K;
+  // split-K (skinny products): blockIdx.z takes K columns [kb, ke) and adds
+  // its partial sums into the zeroed output
+  const int kb = blockIdx.z * kslice;
+  const int ke = kb + kslice < K ? kb + kslice : K;
+  for (int kc = kb; kc < ke; kc += kKChunk) {
+    const int kend = kc + kKChunk < ke ? kc + kKChunk : ke;
     int hh[2][4][4], mx[2][4][4], ll[2][4][4];
 #pragma unroll
     for (int i = 0; i < 2; i++)
@@ -213,7 +217,11 @@ __global__ void __launch_bounds__(256)
       for (int q = 0; q < 4; q += 2) {
         const int r = m0 + wm * 32 + i * 16 + g + 8 * (q >> 1);
         const int c = n0 + wn * 32 + j * 8 + 2 * tig;
-        if (r < M && c + 1 < N && ((N & 1) == 0)) {
+        if (gridDim.z > 1) {  // two's complement partial sums add exactly mod 2^64
+          unsigned long long* d = reinterpret_cast<unsigned long long*>(C + (size_t)r * N + c);
+          if (r < M && c < N) atomicAdd(d, (unsigned long long)tot[i][j][q]);
+          if (r < M && c + 1 < N) atomicAdd(d + 1, (unsigned long long)tot[i][j][q + 1]);
+        } else if (r < M && c + 1 < N && ((N & 1) == 0)) {
           *reinterpret_cast<longlong2*>(C + (size_t)r * N + c) =
               make_longlong2(tot[i][j][q], tot[i][j][q + 1]);
         } else {
@@ -240,6 +248,19 @@ int op_igemm16(const int16_t* A, const int16_t* B, int64_t* C, int M, int K, int
     set_error("igemm16: M = %d too large", M);
     return kErrArg;
   }
+  // skinny products (few output tiles, long K): split K so the grid covers
+  // about two waves of SMs, each slice a multiple of the 64-column K step
+  int kslice = K;
+  const int tiles = (int)(grid.x * grid.y);
+  if (tiles < kSMs && K >= 2 * 256) {
+    int splits = (2 * kSMs + tiles - 1) / tiles;
+    const int max_splits = K / 256;
+    if (splits > max_splits) splits = max_splits;
+    kslice = (K + splits - 1) / splits;
+    kslice = (kslice + kTK - 1) / kTK * kTK;
+    grid.z = (K + kslice - 1) / kslice;
+    ZKL_CUDA(cudaMemsetAsync(C, 0, (size_t)M * N * 8, s));
+  }
   static bool attr = false;
   const size_t smem = 2 * kStage * sizeof(int16_t);
   if (!attr) {
@@ -247,7 +268,7 @@ int op_igemm16(const int16_t* A, const int16_t* B, int64_t* C, int M, int K, int
                                   (int)smem));
     attr = true;
   }
-  k_igemm16<<<grid, 256, smem, s>>>(A, B, C, M, K, N);
+  k_igemm16<<<grid, 256, smem, s>>>(A, B, C, M, K, N, kslice);
   ZKL_LAUNCH_CHECK();
   return kOk;
 }

@@ -36,3 +36,18 @@ def test_igemm16_llama_shape_matches_fp64():
     got = D.igemm16(a, b)
     want = torch.matmul(a.double(), b.double()).round_().long()
     assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("M,K,N", [(2048, 4096, 16), (16, 2048, 4096), (4096, 2048, 16),
+                                   (128, 33000, 64)])
+def test_igemm16_split_k_skinny(M, K, N):
+    """Skinny products (the LoRA-rank GEMMs of a block and of cfg2's witness)
+    run split-K, the partial sums added into the output with 64-bit atomics:
+    still exact (checked against int64 products on the CPU)."""
+    g = torch.Generator().manual_seed(M + K + N)
+    a = torch.randint(-2 ** 15, 2 ** 15, (M, K), generator=g, dtype=torch.int64)
+    b = torch.randint(-2 ** 15, 2 ** 15, (K, N), generator=g, dtype=torch.int64)
+    a[:, 0] = -32768
+    b[0, :] = -32768
+    got = D.igemm16(a.to(torch.int16).cuda(), b.to(torch.int16).cuda()).cpu()
+    assert torch.equal(got, a @ b)

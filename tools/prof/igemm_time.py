@@ -8,7 +8,7 @@ import torch
 sys.path.insert(0, ".")
 from paper_2508_21393_b200 import device as D  # noqa: E402
 
-SHAPES = [(2048, 4096, 4096), (2048, 4096, 11008), (2048, 11008, 4096), (4096, 2048, 4096),
+SHAPES = [(2048, 4096, 4096), (2048, 4096, 16), (16, 2048, 4096), (2048, 4096, 11008), (4096, 2048, 4096),
           (2048, 128, 2048), (2048, 2048, 128), (4096, 2048, 11008)]
 
 
