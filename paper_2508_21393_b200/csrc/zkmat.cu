@@ -172,6 +172,19 @@ struct PointSlots {
   }
 };
 
+// flag = 1 if any of the n words is nonzero (benign racing stores of 1)
+__global__ void k_any_nonzero(const uint64_t* v, uint64_t n, unsigned* flag) {
+  bool nz = false;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    nz |= v[i] != 0;
+  if (__any_sync(0xffffffffu, nz) && (threadIdx.x & 31) == 0) *flag = 1u;
+}
+static bool zero_phase_enabled() {
+  static const bool on = getenv("ZKL_NO_ZERO_PHASE") == nullptr;
+  return on;
+}
+
 // 32 bytes device -> mapped host memory by a kernel (kappa for the host)
 __global__ void k_to_host32(uint4* dst, const uint4* src) {
   if (threadIdx.x < 2) dst[threadIdx.x] = src[threadIdx.x];
@@ -344,6 +357,24 @@ struct MatmulJob {
     }
     return kOk;
   }
+  // is the device vector v[0..n) all zero?  (waits for the stream)
+  int all_zero(const T* v, uint64_t n, bool* zero) {
+    static thread_local unsigned* flag_host = nullptr;
+    static thread_local unsigned* flag_dev = nullptr;
+    if (!flag_host) {
+      ZKL_CUDA(cudaHostAlloc((void**)&flag_host, 64, cudaHostAllocMapped));
+      ZKL_CUDA(cudaHostGetDevicePointer((void**)&flag_dev, flag_host, 0));
+    }
+    *flag_host = 0;
+    const uint64_t words = n * sizeof(T) / 8;
+    unsigned blocks = (unsigned)((words + 255) / 256);
+    if (blocks > 2 * kSMs) blocks = 2 * kSMs;
+    k_any_nonzero<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint64_t*>(v), words, flag_dev);
+    ZKL_LAUNCH_CHECK();
+    ZKL_CUDA(cudaStreamSynchronize(s));
+    *zero = *reinterpret_cast<volatile unsigned*>(flag_host) == 0;
+    return kOk;
+  }
   static T*& kap_host() {
     static thread_local T* p = nullptr;
     return p;
@@ -456,12 +487,37 @@ struct MatmulJob {
     void* tabs_w[2] = {buf(AV), buf(BV)};
     void* tabs_v[3] = {buf(EV), buf(BW), buf(CU)};
     if (d0) {
-      pu.tables = tabs_u;
-      pu.k = 2;
-      pu.num_vars = d0;
-      pu.tm = prod2_terms<F>(H::one());
-      pu.post_mul = H::one();
-      if ((rc = run_phase<F>(pu, *tr, rounds, point, nullptr, s))) return rc;
+      bool zero = false;
+      if (zero_phase_enabled() && (rc = all_zero(buf(HV), D0, &zero))) return rc;
+      if (zero) {
+        // A true claim (C = A B) has h = A (B E_v) - C E_v = 0 identically, so
+        // every U-phase round polynomial E_u h is the zero polynomial: the
+        // rounds are the transcript's alone (4 zero evaluations, then the
+        // challenge), and the folded finals are E_u(rho) = eq(r_u, rho) and
+        // h(rho) = 0.  Same bytes as the device rounds (a false claim keeps
+        // them, tests/test_gpu_parity.py::test_matmul_factored_vs_oracle).
+        memset(rounds, 0, (size_t)d0 * 4 * nb);
+        const uint8_t zb = 0;
+        T eq = H::one();
+        for (int j = 0; j < d0; j++) {
+          for (int x = 0; x < 4; x++) tr->append_elem("sumcheck/eval", &zb, 1);
+          challenge_canon<F>(*tr, "sumcheck/round", point + (size_t)j * nb);
+          const T r = host::from_canon<F>(ru.data() + (size_t)j * nb);
+          const T rho = host::from_canon<F>(point + (size_t)j * nb);
+          // eq(r, rho) = r rho + (1 - r)(1 - rho)
+          const T t = H::add(H::mul(r, rho), H::mul(H::sub(H::one(), r), H::sub(H::one(), rho)));
+          eq = H::mul(eq, t);
+        }
+        e_hat = eq;
+        have_e_hat = true;
+      } else {
+        pu.tables = tabs_u;
+        pu.k = 2;
+        pu.num_vars = d0;
+        pu.tm = prod2_terms<F>(H::one());
+        pu.post_mul = H::one();
+        if ((rc = run_phase<F>(pu, *tr, rounds, point, nullptr, s))) return rc;
+      }
     }
     mark(2);
     gmark(3);

@@ -327,6 +327,23 @@ def _run_isolated(code, **env):
                           cwd=ROOT_DIR, env=dict(os.environ, **env))
 
 
+def test_zero_u_phase_shortcut_off_matches_golden():
+    """A true claim's U phase is proven on the host (h = A B E_v - C E_v is
+    identically zero, so every round polynomial is zero); with the shortcut
+    off (ZKL_NO_ZERO_PHASE=1) the device rounds give the same bytes: both
+    are checked against the reference's goldens and the batch test."""
+    code = (
+        "import sys; sys.path[:0] = ['.', 'tests', 'tests/golden']\n"
+        "import test_gpu_parity as T\n"
+        "for mode in ('i16', 'i64', 'field'):\n"
+        "    T.test_matmul_sumcheck_golden(mode, 'native')\n"
+        "T.test_matmul_batch_matches_per_claim('big')\n"
+        "T.test_matmul_batch_matches_per_claim('test')\n"
+        "print('ok')\n")
+    r = _run_isolated(code, ZKL_NO_ZERO_PHASE="1")
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
+
+
 def test_stepwise_mode_matches_oracle():
     """ZKL_NO_PERSISTENT=1 (what profilers get automatically): one launch per
     round through the same drivers, still bit-exact."""
