@@ -357,22 +357,39 @@ struct MatmulJob {
     }
     return kOk;
   }
-  // is the device vector v[0..n) all zero?  (waits for the stream)
-  int all_zero(const T* v, uint64_t n, bool* zero) {
-    static thread_local unsigned* flag_host = nullptr;
-    static thread_local unsigned* flag_dev = nullptr;
-    if (!flag_host) {
-      ZKL_CUDA(cudaHostAlloc((void**)&flag_host, 64, cudaHostAllocMapped));
-      ZKL_CUDA(cudaHostGetDevicePointer((void**)&flag_dev, flag_host, 0));
+  // is the device vector v[0..n) all zero?  The check is queued now and
+  // waited for (an event right behind it) only by check_zero_wait
+  static unsigned*& zflag_host() {
+    static thread_local unsigned* p = nullptr;
+    return p;
+  }
+  static unsigned*& zflag_dev() {
+    static thread_local unsigned* p = nullptr;
+    return p;
+  }
+  static cudaEvent_t& zero_ev() {
+    static thread_local cudaEvent_t e = nullptr;
+    return e;
+  }
+  int check_zero_async(const T* v, uint64_t n) {
+    if (!zflag_host()) {
+      ZKL_CUDA(cudaHostAlloc((void**)&zflag_host(), 64, cudaHostAllocMapped));
+      ZKL_CUDA(cudaHostGetDevicePointer((void**)&zflag_dev(), zflag_host(), 0));
+      ZKL_CUDA(cudaEventCreateWithFlags(&zero_ev(), cudaEventDisableTiming));
     }
-    *flag_host = 0;
+    *reinterpret_cast<volatile unsigned*>(zflag_host()) = 0;
     const uint64_t words = n * sizeof(T) / 8;
     unsigned blocks = (unsigned)((words + 255) / 256);
     if (blocks > 2 * kSMs) blocks = 2 * kSMs;
-    k_any_nonzero<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint64_t*>(v), words, flag_dev);
+    k_any_nonzero<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint64_t*>(v), words,
+                                         zflag_dev());
     ZKL_LAUNCH_CHECK();
-    ZKL_CUDA(cudaStreamSynchronize(s));
-    *zero = *reinterpret_cast<volatile unsigned*>(flag_host) == 0;
+    ZKL_CUDA(cudaEventRecord(zero_ev(), s));
+    return kOk;
+  }
+  int check_zero_wait(bool* zero) {
+    ZKL_CUDA(cudaEventSynchronize(zero_ev()));
+    *zero = *reinterpret_cast<volatile unsigned*>(zflag_host()) == 0;
     return kOk;
   }
   static T*& kap_host() {
@@ -486,16 +503,57 @@ struct MatmulJob {
     void* tabs_u[2] = {buf(EU), buf(HV)};
     void* tabs_w[2] = {buf(AV), buf(BV)};
     void* tabs_v[3] = {buf(EV), buf(BW), buf(CU)};
+    if (!kap_host()) {
+      ZKL_CUDA(cudaHostAlloc((void**)&kap_host(), 64, cudaHostAllocMapped));
+      ZKL_CUDA(cudaHostGetDevicePointer((void**)&kap_dev(), kap_host(), 0));
+      ZKL_CUDA(cudaEventCreateWithFlags(&kap_ev(), cudaEventDisableTiming));
+    }
+    // ---- W phase inputs: E(rho_u), a = E^T A, cu = E^T C, kappa = <cu, E_v>
+    auto launch_w = [&](const uint8_t* rho_u) -> int {
+      auto w_inputs = [&]() -> int {
+        int r;
+        if (graphed) {
+          if ((r = eq_dev_on(s, buf(ERU), 2, d0))) return r;
+        } else if ((r = eq(buf(ERU), load_point(rho_u, d0), d0))) {
+          return r;
+        }
+        if ((r = fork())) return r;
+        if ((r = mv_on(side_stream(), tc, C, D0, D2, 1, buf(ERU), buf(CU)))) return r;  // cu
+        if ((r = mv(ta, A, D0, D1, 1, buf(ERU), buf(AV)))) return r;
+        if ((r = join())) return r;
+        if ((r = op_dot<F>(buf(KAP), buf(CU), buf(EV), D2, s))) return r;
+        k_to_host32<<<1, 32, 0, s>>>(reinterpret_cast<uint4*>(kap_dev()),
+                                     reinterpret_cast<const uint4*>(buf(KAP)));
+        ZKL_LAUNCH_CHECK();
+        return kOk;
+      };
+      int r;
+      if (graphed) {
+        fill_point(2, rho_u, d0);
+        if ((r = run_graphed(key_for(1), s, w_inputs, [this](cudaStream_t st) { s = st; })))
+          return r;
+      } else if ((r = w_inputs())) {
+        return r;
+      }
+      ZKL_CUDA(cudaEventRecord(kap_ev(), s));
+      return kOk;
+    };
+    bool w_launched = false;
     if (d0) {
       bool zero = false;
-      if (zero_phase_enabled() && (rc = all_zero(buf(HV), D0, &zero))) return rc;
-      if (zero) {
+      if (zero_phase_enabled()) {
         // A true claim (C = A B) has h = A (B E_v) - C E_v = 0 identically, so
         // every U-phase round polynomial E_u h is the zero polynomial: the
         // rounds are the transcript's alone (4 zero evaluations, then the
         // challenge), and the folded finals are E_u(rho) = eq(r_u, rho) and
-        // h(rho) = 0.  Same bytes as the device rounds (a false claim keeps
-        // them, tests/test_gpu_parity.py::test_matmul_factored_vs_oracle).
+        // h(rho) = 0.  Same bytes as the device rounds.  The host rounds run
+        // speculatively while the device still computes h, and the W inputs
+        // for the resulting rho_u are queued right behind the zero check; a
+        // false claim (h != 0) restores the transcript, runs the device
+        // rounds and recomputes the W inputs
+        // (tests/test_gpu_parity.py::test_matmul_factored_vs_oracle).
+        uint8_t saved[64];
+        memcpy(saved, tr->state, 64);
         memset(rounds, 0, (size_t)d0 * 4 * nb);
         const uint8_t zb = 0;
         T eq = H::one();
@@ -508,9 +566,19 @@ struct MatmulJob {
           const T t = H::add(H::mul(r, rho), H::mul(H::sub(H::one(), r), H::sub(H::one(), rho)));
           eq = H::mul(eq, t);
         }
-        e_hat = eq;
-        have_e_hat = true;
-      } else {
+        if ((rc = check_zero_async(buf(HV), D0))) return rc;
+        if ((rc = launch_w(point))) return rc;
+        w_launched = true;
+        if ((rc = check_zero_wait(&zero))) return rc;
+        if (zero) {
+          e_hat = eq;
+          have_e_hat = true;
+        } else {
+          memcpy(tr->state, saved, 64);
+          w_launched = false;
+        }
+      }
+      if (!zero) {
         pu.tables = tabs_u;
         pu.k = 2;
         pu.num_vars = d0;
@@ -521,39 +589,9 @@ struct MatmulJob {
     }
     mark(2);
     gmark(3);
-    // ---- W phase inputs: E(rho_u), a = E^T A, cu = E^T C, kappa = <cu, E_v>
-    if (!kap_host()) {
-      ZKL_CUDA(cudaHostAlloc((void**)&kap_host(), 64, cudaHostAllocMapped));
-      ZKL_CUDA(cudaHostGetDevicePointer((void**)&kap_dev(), kap_host(), 0));
-      ZKL_CUDA(cudaEventCreateWithFlags(&kap_ev(), cudaEventDisableTiming));
-    }
-    const uint8_t* rho_u = point;
-    auto w_inputs = [&]() -> int {
-      int r;
-      if (graphed) {
-        if ((r = eq_dev_on(s, buf(ERU), 2, d0))) return r;
-      } else if ((r = eq(buf(ERU), load_point(rho_u, d0), d0))) {
-        return r;
-      }
-      if ((r = fork())) return r;
-      if ((r = mv_on(side_stream(), tc, C, D0, D2, 1, buf(ERU), buf(CU)))) return r;  // cu
-      if ((r = mv(ta, A, D0, D1, 1, buf(ERU), buf(AV)))) return r;
-      if ((r = join())) return r;
-      if ((r = op_dot<F>(buf(KAP), buf(CU), buf(EV), D2, s))) return r;
-      k_to_host32<<<1, 32, 0, s>>>(reinterpret_cast<uint4*>(kap_dev()),
-                                   reinterpret_cast<const uint4*>(buf(KAP)));
-      ZKL_LAUNCH_CHECK();
-      return kOk;
-    };
-    if (graphed) {
-      fill_point(2, rho_u, d0);
-      if ((rc = run_graphed(key_for(1), s, w_inputs, [this](cudaStream_t st) { s = st; }))) return rc;
-    } else if ((rc = w_inputs())) {
-      return rc;
-    }
+    if (!w_launched && (rc = launch_w(point))) return rc;
     rounds += (size_t)d0 * 4 * nb;
     point += (size_t)d0 * nb;
-    ZKL_CUDA(cudaEventRecord(kap_ev(), s));
     mark(3);
     gmark(4);
     if (d1) {
