@@ -141,6 +141,17 @@ int zkl_sumcheck_prove(int field, void* const* tables, int k, int num_vars, int 
  * Python triple loop).  Any shape; K unbounded (int64 accumulation). */
 int zkl_igemm_i16(const int16_t* A, const int16_t* B, int64_t* C, int M, int K, int N,
                   void* stream);
+/* The same product through a library int8 GEMM (the tcgen05 tensor cores via
+ * cuBLASLt): zkl_split_i16 writes each int16 entry's planes hi = a >> 8 and
+ * lo = (a & 255) - 128 (so a = 256 hi + lo + 128); with HH = Ah Bh,
+ * HL = Ah Bl, LH = Al Bh, LL = Al Bl (int32, M x N) and the row sums of A /
+ * column sums of B, zkl_igemm_combine writes
+ *   C = 65536 HH + 256 (HL + LH) + LL + 128 (rowA_i + colB_j) - 16384 K,
+ * exact for K <= 2^16 (every int32 plane product below 2^30). */
+int zkl_split_i16(const int16_t* src, uint64_t n, int8_t* hi, int8_t* lo, void* stream);
+int zkl_igemm_combine(const int32_t* hh, const int32_t* hl, const int32_t* lh, const int32_t* ll,
+                      const int64_t* rowA, const int64_t* colB, int64_t K, int64_t* C, int M,
+                      int N, void* stream);
 
 int zkl_shard_open(const char* name, int rank, int world);
 int zkl_shard_close(void);

@@ -29,7 +29,8 @@ EXPORTS = (
     "zkl_multiplicities_index", "zkl_gather", "zkl_pair_multiplicities",
     "zkl_range_multiplicities", "zkl_rescale_witness", "zkl_transcript_append_ints", "zkl_transcript_challenge_vector",
     "zkl_sumcheck_prove_sharded", "zkl_shard_open", "zkl_shard_close", "zkl_shard_world",
-    "zkl_shard_exchange", "zkl_igemm_i16", "zkl_matmul_prove_batch",
+    "zkl_shard_exchange", "zkl_igemm_i16", "zkl_matmul_prove_batch", "zkl_split_i16",
+    "zkl_igemm_combine",
 )
 
 
@@ -79,6 +80,9 @@ _SIGS = {
     "zkl_shard_world": ([], ctypes.c_int),
     "zkl_shard_exchange": ([_vp, _u64, _vp], ctypes.c_int),
     "zkl_igemm_i16": ([_vp, _vp, _vp, _i32, _i32, _i32, _vp], ctypes.c_int),
+    "zkl_split_i16": ([_vp, _u64, _vp, _vp, _vp], ctypes.c_int),
+    "zkl_igemm_combine": ([_vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp, _i32, _i32, _vp],
+                          ctypes.c_int),
     "zkl_transcript_append": ([_vp, _u8p, _u64, _u8p, _u64], ctypes.c_int),
     "zkl_transcript_challenge": ([_i32, _vp, _u8p, _u64, _vp], ctypes.c_int),
     "zkl_batch_inverse": ([_i32, _vp, _vp, _u64, _u8p, _i64p, _vp], ctypes.c_int),

@@ -260,6 +260,14 @@ int zkl_igemm_i16(const int16_t* A, const int16_t* B, int64_t* C, int M, int K, 
                   void* stream) {
   return op_igemm16(A, B, C, M, K, N, (cudaStream_t)stream);
 }
+int zkl_split_i16(const int16_t* src, uint64_t n, int8_t* hi, int8_t* lo, void* stream) {
+  return op_split16(src, n, hi, lo, (cudaStream_t)stream);
+}
+int zkl_igemm_combine(const int32_t* hh, const int32_t* hl, const int32_t* lh, const int32_t* ll,
+                      const int64_t* rowA, const int64_t* colB, int64_t K, int64_t* C, int M,
+                      int N, void* stream) {
+  return op_igemm_combine(hh, hl, lh, ll, rowA, colB, K, C, M, N, (cudaStream_t)stream);
+}
 int zkl_shake256(const uint8_t* in, uint64_t len, uint8_t* out, uint64_t outlen) {
   shake256(in, (size_t)len, out, (size_t)outlen);
   return kOk;

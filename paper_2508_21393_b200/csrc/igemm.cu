@@ -231,7 +231,66 @@ __global__ void __launch_bounds__(256)
       }
 }
 
+// int16 -> int8 planes for a library int8 GEMM: hi = a >> 8 (signed), lo =
+// (a & 255) - 128 (signed), so a = 256 hi + lo + 128; 8 entries per thread
+__global__ void k_split16(const int16_t* __restrict__ src, uint64_t n, int8_t* __restrict__ hi,
+                          int8_t* __restrict__ lo) {
+  const uint64_t i8 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * 8;
+  if (i8 + 8 <= n && (((uintptr_t)src | (uintptr_t)hi | (uintptr_t)lo) & 15) == 0) {
+    const uint4 v = *reinterpret_cast<const uint4*>(src + i8);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t h[2], l[2];
+#pragma unroll
+    for (int q = 0; q < 2; q++) {
+      h[q] = __byte_perm(w[2 * q], w[2 * q + 1], 0x7531);
+      l[q] = __byte_perm(w[2 * q], w[2 * q + 1], 0x6420) ^ 0x80808080u;  // - 128
+    }
+    *reinterpret_cast<uint2*>(hi + i8) = make_uint2(h[0], h[1]);
+    *reinterpret_cast<uint2*>(lo + i8) = make_uint2(l[0], l[1]);
+  } else {
+    for (uint64_t i = i8; i < n && i < i8 + 8; i++) {
+      const int v = src[i];
+      hi[i] = (int8_t)(v >> 8);
+      lo[i] = (int8_t)((v & 255) - 128);
+    }
+  }
+}
+
+// C = 65536 HH + 256 (HL + LH) + LL + 128 (rowA_i + colB_j) - 16384 K: the
+// exact int64 product from the four int8 plane products (int32) and the
+// operands' row / column sums
+__global__ void k_igemm_combine(const int32_t* __restrict__ hh, const int32_t* __restrict__ hl,
+                                const int32_t* __restrict__ lh, const int32_t* __restrict__ ll,
+                                const int64_t* __restrict__ rowA, const int64_t* __restrict__ colB,
+                                int64_t K, int64_t* __restrict__ C, int M, int N) {
+  const uint64_t n = (uint64_t)M * N;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = i / N, c = i % N;
+    C[i] = 65536ll * hh[i] + 256ll * ((int64_t)hl[i] + lh[i]) + ll[i] + 128 * (rowA[r] + colB[c]) -
+           16384 * K;
+  }
+}
+
 }  // namespace
+
+int op_split16(const int16_t* src, uint64_t n, int8_t* hi, int8_t* lo, cudaStream_t s) {
+  if (!n) return kOk;
+  const uint64_t threads = (n + 7) / 8;
+  k_split16<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(src, n, hi, lo);
+  ZKL_LAUNCH_CHECK();
+  return kOk;
+}
+
+int op_igemm_combine(const int32_t* hh, const int32_t* hl, const int32_t* lh, const int32_t* ll,
+                     const int64_t* rowA, const int64_t* colB, int64_t K, int64_t* C, int M,
+                     int N, cudaStream_t s) {
+  if (M <= 0 || N <= 0) return kOk;
+  k_igemm_combine<<<grid_for((uint64_t)M * N, 256, 8), 256, 0, s>>>(hh, hl, lh, ll, rowA, colB,
+                                                                     K, C, M, N);
+  ZKL_LAUNCH_CHECK();
+  return kOk;
+}
 
 int op_igemm16(const int16_t* A, const int16_t* B, int64_t* C, int M, int K, int N,
                cudaStream_t s) {

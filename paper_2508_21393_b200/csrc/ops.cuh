@@ -87,6 +87,10 @@ int op_sumcheck_prove_sharded(void* const* tables, int k, int num_vars, const Te
                       uint8_t* finals_out, cudaStream_t s);
 int op_igemm16(const int16_t* A, const int16_t* B, int64_t* C, int M, int K, int N,
                cudaStream_t s);
+int op_split16(const int16_t* src, uint64_t n, int8_t* hi, int8_t* lo, cudaStream_t s);
+int op_igemm_combine(const int32_t* hh, const int32_t* hl, const int32_t* lh, const int32_t* ll,
+                     const int64_t* rowA, const int64_t* colB, int64_t K, int64_t* C, int M,
+                     int N, cudaStream_t s);
 int shard_world();
 int shard_rank();
 int shard_exchange(const void* mine, size_t nbytes, uint8_t* out);

@@ -226,10 +226,48 @@ def as_list(values):
 _INT_TYPES = {torch.int16: N.MT_I16, torch.int32: N.MT_I32, torch.int64: N.MT_I64}
 
 
+IGEMM_LIB = True  # large products through the library int8 GEMM (tests flip it)
+
+
+def _lib_gemm_shape(M, K, N):
+    # torch._int_mm (cuBLASLt int8, tcgen05 on B200) wants K, N multiples of 8
+    # and M > 16; the int32 plane products stay exact for K <= 2^16 (|sum| <=
+    # 2^14 K).  The planes, four GEMMs and the int64 recombination cost ~0.1 ms
+    # of fixed work, so only products of >= 2^32 MACs take this path (the
+    # per-head attention products stay on the kernel: 28 us vs 134 us)
+    return (M >= 128 and N >= 128 and K % 8 == 0 and N % 8 == 0 and 16 <= K <= (1 << 16)
+            and M * K * N >= (1 << 32))
+
+
+def _igemm16_lib(a, b, c):
+    """a @ b from four int8 plane products: hi = a >> 8, lo = (a & 255) - 128,
+    so a = 256 hi + lo + 128 and the int64 product is recombined exactly
+    (zkl_split_i16 / zkl_igemm_combine around torch._int_mm)."""
+    M, K = a.shape
+    Nn = b.shape[1]
+    ah = torch.empty((M, K), dtype=torch.int8, device=a.device)
+    al = torch.empty_like(ah)
+    bh = torch.empty((K, Nn), dtype=torch.int8, device=a.device)
+    bl = torch.empty_like(bh)
+    lib, st = N.lib(), stream()
+    N.check(lib.zkl_split_i16(ptr(a), M * K, ptr(ah), ptr(al), st))
+    N.check(lib.zkl_split_i16(ptr(b), K * Nn, ptr(bh), ptr(bl), st))
+    hh = torch._int_mm(ah, bh)
+    hl = torch._int_mm(ah, bl)
+    lh = torch._int_mm(al, bh)
+    ll = torch._int_mm(al, bl)
+    row = a.sum(1, dtype=torch.int64)
+    col = b.sum(0, dtype=torch.int64)
+    N.check(lib.zkl_igemm_combine(ptr(hh), ptr(hl), ptr(lh), ptr(ll), ptr(row), ptr(col), K,
+                                  ptr(c), M, Nn, st))
+    return c
+
+
 def igemm16(a, b, out=None):
-    """Exact int64 a @ b for int16 CUDA matrices (zkl_igemm_i16: byte-sliced
-    tensor-core GEMM, int64 accumulation); `out` an optional preallocated
-    contiguous int64 result."""
+    """Exact int64 a @ b for int16 CUDA matrices; `out` an optional
+    preallocated contiguous int64 result.  Large products go through the
+    library int8 GEMM on byte planes (_igemm16_lib), the rest through the
+    repo's byte-sliced mma.sync kernel (zkl_igemm_i16, split-K when skinny)."""
     a, b = a.contiguous(), b.contiguous()
     if a.dtype != torch.int16 or b.dtype != torch.int16 or a.dim() != 2 or b.dim() != 2:
         raise TypeError("igemm16 takes two int16 matrices")
@@ -244,6 +282,8 @@ def igemm16(a, b, out=None):
             raise ValueError("igemm16: out must be a contiguous %dx%d int64 tensor" % (M, Nn))
         c = out
     if M and Nn:
+        if IGEMM_LIB and _lib_gemm_shape(M, K, Nn):
+            return _igemm16_lib(a, b, c)
         N.check(N.lib().zkl_igemm_i16(ptr(a), ptr(b), ptr(c), M, K, Nn, stream()))
     return c
 

@@ -51,3 +51,21 @@ def test_igemm16_split_k_skinny(M, K, N):
     b[0, :] = -32768
     got = D.igemm16(a.to(torch.int16).cuda(), b.to(torch.int16).cuda()).cpu()
     assert torch.equal(got, a @ b)
+
+
+@pytest.mark.parametrize("lib", [True, False])
+@pytest.mark.parametrize("M,K,N", [(2048, 4096, 1024), (1032, 8200, 520)])
+def test_igemm16_library_and_kernel_paths(lib, M, K, N, monkeypatch):
+    """Both product paths on the same shapes: the library int8 GEMM on byte
+    planes (zkl_split_i16 + torch._int_mm + zkl_igemm_combine) and the repo's
+    mma.sync kernel, each exact against int64 products."""
+    monkeypatch.setattr(D, "IGEMM_LIB", lib)
+    g = torch.Generator().manual_seed(M * 3 + K + N)
+    a = torch.randint(-2 ** 15, 2 ** 15, (M, K), generator=g, dtype=torch.int64)
+    b = torch.randint(-2 ** 15, 2 ** 15, (K, N), generator=g, dtype=torch.int64)
+    a[0, :] = -32768
+    a[1, :] = 32767
+    b[:, 0] = -32768
+    b[:, 1] = 32767
+    got = D.igemm16(a.to(torch.int16).cuda(), b.to(torch.int16).cuda()).cpu()
+    assert torch.equal(got, a @ b)
