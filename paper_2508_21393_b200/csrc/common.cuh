@@ -56,6 +56,13 @@ ZKL_D fr_t shfl_idx(const fr_t& x, int src) {
   return y;
 }
 ZKL_D uint64_t shfl_idx(uint64_t x, int src) { return __shfl_sync(kFull, x, src); }
+ZKL_D fr_t shfl_xor(const fr_t& x, int mask) {
+  fr_t y;
+#pragma unroll
+  for (int i = 0; i < 8; i++) y.v[i] = __shfl_xor_sync(kFull, x.v[i], mask);
+  return y;
+}
+ZKL_D uint64_t shfl_xor(uint64_t x, int mask) { return __shfl_xor_sync(kFull, x, mask); }
 
 template <class F>
 ZKL_D typename F::T warp_sum(typename F::T x) {

@@ -596,6 +596,11 @@ __global__ void k_eq_outer(typename F::T* dst, const typename F::T* hi, const ty
 // pair = one product each; level 2 (per output): product of the <= 8 pair
 // values as a balanced tree.  ~4 dependent Montgomery products for m = 12
 // instead of m/2 in the two-chain direct form.
+#ifndef ZKL_EQ_ONE_LANE
+constexpr bool kEqLanes4 = true;
+#else
+constexpr bool kEqLanes4 = false;
+#endif
 template <class F>
 ZKL_D void eq_tree_body(typename F::T* dst, const PointArg<F>& pt, int off, int m) {
   using T = typename F::T;
@@ -615,6 +620,32 @@ ZKL_D void eq_tree_body(typename F::T* dst, const PointArg<F>& pt, int off, int 
   }
   __syncthreads();
   const uint64_t n = 1ull << m;
+#ifndef ZKL_EQ_ONE_LANE
+  if (G >= 3 && m >= 3) {
+    // four lanes per output: lane q multiplies the pair values of groups
+    // 2q and 2q + 1 (one product), then two shuffle-and-multiply steps: 3
+    // single dependent products after the pair stage, instead of the
+    // interleaved mul4 / mul2 / mul tree (the kernel is latency-bound)
+    const uint64_t lanes = 4 * n;  // a multiple of 32 for m >= 3
+    for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + t; l < lanes;
+         l += (uint64_t)gridDim.x * blockDim.x) {
+      const uint64_t i = l >> 2;
+      const int q = (int)(l & 3);
+      auto val = [&](int g) -> T {
+        if (g >= G) return F::one();
+        const int j0 = 2 * g;
+        const int b0 = (int)((i >> (m - 1 - j0)) & 1);
+        const int b1 = j0 + 1 < m ? (int)((i >> (m - 2 - j0)) & 1) : 0;
+        return grp[g][(b0 << 1) | b1];
+      };
+      T x = 2 * q + 1 < G ? F::mul(val(2 * q), val(2 * q + 1)) : val(2 * q);
+      x = F::mul(x, shfl_xor(x, 1));
+      if (G > 4) x = F::mul(x, shfl_xor(x, 2));
+      if (q == 0) dst[i] = x;
+    }
+    return;
+  }
+#endif
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + t; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     T v[8];
@@ -667,10 +698,35 @@ __global__ void __launch_bounds__(256) k_eq_tree_dev(typename F::T* dst, const P
   __syncthreads();
   eq_tree_body<F>(dst, sp, 0, m);
 }
+// r[0..m) and omr[0..m) of a point in mapped host memory -> device memory, by
+// one block of 16-byte loads (a PCIe read per 16 bytes, once per table, not
+// once per block of the table kernel)
 template <class F>
-int op_eq_table_dev(void* dst, const PointArg<F>* pt_dev, int m, cudaStream_t s) {
+__global__ void k_point_to_dev(const PointArg<F>* src, PointArg<F>* dst, int m) {
+  constexpr int kV = sizeof(typename F::T) / 16 > 0 ? sizeof(typename F::T) / 16 : 1;
+  const int per = (int)(m * sizeof(typename F::T) + 15) / 16;  // uint4 per array
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  constexpr int kArr = (int)(kMaxPoint * sizeof(typename F::T) / 16);  // omr offset (uint4)
+  (void)kV;
+  for (int i = threadIdx.x; i < 2 * per; i += blockDim.x) {
+    const int w = i < per ? i : kArr + (i - per);
+    d[w] = s[w];
+  }
+}
+template <class F>
+int op_eq_table_dev(void* dst, const PointArg<F>* pt_dev, int m, int slot_id, cudaStream_t s) {
   if (m < 1 || m > 16) { set_error("eq_table_dev: m=%d unsupported", m); return kErrArg; }
-  k_eq_tree_dev<F><<<grid_for(1ull << m, 256), 256, 0, s>>>((typename F::T*)dst, pt_dev, m);
+  if (slot_id < 0 || slot_id >= 8) { set_error("eq_table_dev: slot %d", slot_id); return kErrArg; }
+  // device copies of the points, one per caller slot (tables built
+  // concurrently on two streams use different slots)
+  static PointArg<F>* staged = nullptr;
+  if (!staged) ZKL_CUDA(cudaMalloc((void**)&staged, 8 * sizeof(PointArg<F>)));
+  PointArg<F>* slot = staged + slot_id;
+  k_point_to_dev<F><<<1, 64, 0, s>>>(pt_dev, slot, m);
+  ZKL_LAUNCH_CHECK();
+  k_eq_tree_dev<F><<<grid_for((kEqLanes4 && m >= 5 ? 4ull : 1ull) << m, 256), 256, 0, s>>>(
+      (typename F::T*)dst, slot, m);
   ZKL_LAUNCH_CHECK();
   return kOk;
 }
@@ -691,7 +747,8 @@ int op_eq_table(void* dst, const typename F::T* point, int m, cudaStream_t s) {
     return kOk;
   }
   if (m <= 16) {
-    k_eq_tree<F><<<grid_for(1ull << m, 256), 256, 0, s>>>(out, pt, 0, m);
+    k_eq_tree<F><<<grid_for((kEqLanes4 && m >= 5 ? 4ull : 1ull) << m, 256), 256, 0, s>>>(out, pt, 0,
+                                                                                      m);
     ZKL_LAUNCH_CHECK();
     return kOk;
   }
@@ -702,9 +759,9 @@ int op_eq_table(void* dst, const typename F::T* point, int m, cudaStream_t s) {
   if (rc) return rc;
   T* hi = (T*)ws;
   T* lo = hi + (1ull << mh);
-  k_eq_tree<F><<<grid_for(1ull << mh, 256), 256, 0, s>>>(hi, pt, 0, mh);
+  k_eq_tree<F><<<grid_for((kEqLanes4 ? 4ull : 1ull) << mh, 256), 256, 0, s>>>(hi, pt, 0, mh);
   ZKL_LAUNCH_CHECK();
-  k_eq_tree<F><<<grid_for(1ull << ml, 256), 256, 0, s>>>(lo, pt, mh, ml);
+  k_eq_tree<F><<<grid_for((kEqLanes4 ? 4ull : 1ull) << ml, 256), 256, 0, s>>>(lo, pt, mh, ml);
   ZKL_LAUNCH_CHECK();
   k_eq_outer<F><<<grid_for(1ull << m, 256), 256, 0, s>>>(out, hi, lo, ml, 1ull << m);
   ZKL_LAUNCH_CHECK();
@@ -1007,7 +1064,7 @@ int op_rescale_witness(const void* wide, int wide_type, uint64_t n, int64_t divi
   template int op_mul<F>(void*, const void*, const void*, uint64_t, cudaStream_t);          \
   template int op_read<F>(uint8_t*, const void*, uint64_t, cudaStream_t);                 \
   template int op_dot<F>(F::T*, const void*, const void*, uint64_t, cudaStream_t);          \
-  template int op_eq_table_dev<F>(void*, const PointArg<F>*, int, cudaStream_t);             \
+  template int op_eq_table_dev<F>(void*, const PointArg<F>*, int, int, cudaStream_t);        \
   template int op_expand<F>(void*, uint64_t, const void*, uint64_t, int, F::T, F::T,        \
                             cudaStream_t);                                                  \
   template int op_lift_u32<F>(void*, const uint32_t*, uint64_t, cudaStream_t);                \

@@ -25,9 +25,10 @@ struct PointArg {
   typename F::T r[kMaxPoint];
   typename F::T omr[kMaxPoint];
 };
-// eq table from a device-resident point (m <= 16)
+// eq table from a point in mapped host memory (m <= 16), staged through
+// device slot slot_id (0..7; concurrent tables take different slots)
 template <class F>
-int op_eq_table_dev(void* dst, const PointArg<F>* pt_dev, int m, cudaStream_t s);
+int op_eq_table_dev(void* dst, const PointArg<F>* pt_dev, int m, int slot_id, cudaStream_t s);
 template <class F>
 int op_fold(void* dst, const void* src, uint64_t half, typename F::T r, cudaStream_t s);
 // y = a + k * b

@@ -252,7 +252,7 @@ struct MatmulJob {
     }
   }
   int eq_dev_on(cudaStream_t st, T* dst, int p, int m) {
-    return op_eq_table_dev<F>(dst, dev_pt(p), m, st);
+    return op_eq_table_dev<F>(dst, dev_pt(p), m, slot * 4 + p, st);
   }
 
   // ZKL_TRACE: host and GPU timestamps at the phase boundaries (stderr)
