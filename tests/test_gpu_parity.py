@@ -327,6 +327,34 @@ def _run_isolated(code, **env):
                           cwd=ROOT_DIR, env=dict(os.environ, **env))
 
 
+def test_graph_cache_survives_arena_growth():
+    """The zkMat phase inputs replay from a CUDA-graph cache keyed by the
+    operand and workspace pointers and the arenas' generation: prove a claim
+    until its graphs are captured and replayed, grow the work arena underneath
+    (a claim with much longer vectors), and prove again -- every proof equals
+    the oracle's."""
+    p = P_BIG
+    dims = (7, 8, 6)
+    g = inputs.rng(77)
+    a = g.integers(-32768, 32768, size=(1 << dims[0], 1 << dims[1]))
+    b = g.integers(-32768, 32768, size=(1 << dims[1], 1 << dims[2]))
+    cm = a @ b
+    A, B, C = _dev(a, torch.int16), _dev(b, torch.int16), _dev(cm, torch.int64)
+    t2 = fs.FS(b"gc", p, b"x")
+    want = zkmat.prove_factored(a.reshape(-1), b.reshape(-1), cm.reshape(-1), dims, t2)
+    for it in range(5):
+        if it == 3:  # grow the work arena: a claim with 2^14-entry vectors
+            bd = (14, 4, 6)
+            ba = g.integers(-9, 9, size=(1 << bd[0], 1 << bd[1]))
+            bb = g.integers(-9, 9, size=(1 << bd[1], 1 << bd[2]))
+            zb.matmul_sumcheck(_dev(ba, torch.int16), _dev(bb, torch.int16),
+                               _dev(ba @ bb, torch.int64), bd, Transcript(b"big", p, b"y"))
+        t1 = Transcript(b"gc", p, b"x")
+        rounds, point, finals = zb.matmul_sumcheck(A, B, C, dims, t1)
+        assert rounds == want[0] and tuple(finals) == want[1] and point == want[2], it
+        assert t1.state == t2.state
+
+
 def test_zero_u_phase_shortcut_off_matches_golden():
     """A true claim's U phase is proven on the host (h = A B E_v - C E_v is
     identically zero, so every round polynomial is zero); with the shortcut
