@@ -153,6 +153,26 @@ int zkl_igemm_combine(const int32_t* hh, const int32_t* hl, const int32_t* lh, c
                       const int64_t* rowA, const int64_t* colB, int64_t K, int64_t* C, int M,
                       int N, void* stream);
 
+/* Hyrax row commitments (replaces commit.py:87-115 `commit`, the Pedersen
+ * multi-exponentiation of each row, in the Schnorr groups of group.py:64-70):
+ * group 0 = q = 96 p + 1 (33-byte elements; exponents BLS12-381 Fr, 8 words),
+ * group 1 = q = 52 (2^61 - 1) + 1 (9-byte elements; test-field exponents, 2
+ * words).  zkl_commit_tables fills a device buffer of
+ * zkl_commit_table_bytes(group, ngen) bytes with fixed-base window tables for
+ * ngen generators (canonical LE, element-size bytes each; the key's column
+ * generators, then its blinding generator).  zkl_commit_rows: `values`
+ * (device) holds rows x cols canonical exponents (little-endian 32-bit words)
+ * of the table laid out row-major as split_shape(n) (commit.py:25-29);
+ * `blinding` (device, rows exponents) may be NULL (binding-only mode), and
+ * blind_gen is the index of the blinding generator's table; rows_out
+ * (host) receives the rows' group elements, canonical LE.  Bit-identical to
+ * the reference's row commitments. */
+uint64_t zkl_commit_table_bytes(int group, int ngen);
+int zkl_commit_tables(int group, const uint8_t* gens_canon, int ngen, void* tables, void* stream);
+int zkl_commit_rows(int group, const void* tables, int cols, const void* values,
+                    const void* blinding, int blind_gen, int rows, uint8_t* rows_out,
+                    void* stream);
+
 int zkl_shard_open(const char* name, int rank, int world);
 int zkl_shard_close(void);
 int zkl_shard_world(void);

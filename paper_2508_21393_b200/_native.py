@@ -30,7 +30,7 @@ EXPORTS = (
     "zkl_range_multiplicities", "zkl_rescale_witness", "zkl_transcript_append_ints", "zkl_transcript_challenge_vector",
     "zkl_sumcheck_prove_sharded", "zkl_shard_open", "zkl_shard_close", "zkl_shard_world",
     "zkl_shard_exchange", "zkl_igemm_i16", "zkl_matmul_prove_batch", "zkl_split_i16",
-    "zkl_igemm_combine",
+    "zkl_igemm_combine", "zkl_commit_table_bytes", "zkl_commit_tables", "zkl_commit_rows",
 )
 
 
@@ -81,6 +81,9 @@ _SIGS = {
     "zkl_shard_exchange": ([_vp, _u64, _vp], ctypes.c_int),
     "zkl_igemm_i16": ([_vp, _vp, _vp, _i32, _i32, _i32, _vp], ctypes.c_int),
     "zkl_split_i16": ([_vp, _u64, _vp, _vp, _vp], ctypes.c_int),
+    "zkl_commit_table_bytes": ([_i32, _i32], ctypes.c_uint64),
+    "zkl_commit_tables": ([_i32, _vp, _i32, _vp, _vp], ctypes.c_int),
+    "zkl_commit_rows": ([_i32, _vp, _i32, _vp, _vp, _i32, _i32, _vp, _vp], ctypes.c_int),
     "zkl_igemm_combine": ([_vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp, _i32, _i32, _vp],
                           ctypes.c_int),
     "zkl_transcript_append": ([_vp, _u8p, _u64, _u8p, _u64], ctypes.c_int),

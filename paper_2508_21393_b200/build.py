@@ -19,7 +19,7 @@ OUT = os.path.join(HERE, "libzkl_b200.so")
 BUILD = os.path.join(ROOT, "build", "zkl")
 
 SOURCES = ["elem.cu", "sumcheck.cu", "persistent.cu", "inverse.cu", "lookup.cu", "matvec.cu", "transcript.cu",
-           "zkmat.cu", "shard.cu", "igemm.cu", "capi.cu"]
+           "zkmat.cu", "shard.cu", "igemm.cu", "commit.cu", "capi.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

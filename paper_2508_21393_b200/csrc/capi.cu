@@ -268,6 +268,16 @@ int zkl_igemm_combine(const int32_t* hh, const int32_t* hl, const int32_t* lh, c
                       int N, void* stream) {
   return op_igemm_combine(hh, hl, lh, ll, rowA, colB, K, C, M, N, (cudaStream_t)stream);
 }
+uint64_t zkl_commit_table_bytes(int group, int ngen) { return commit_table_bytes(group, ngen); }
+int zkl_commit_tables(int group, const uint8_t* gens_canon, int ngen, void* tables, void* stream) {
+  return op_commit_tables(group, gens_canon, ngen, tables, (cudaStream_t)stream);
+}
+int zkl_commit_rows(int group, const void* tables, int cols, const void* values,
+                    const void* blinding, int blind_gen, int rows, uint8_t* rows_out,
+                    void* stream) {
+  return op_commit_rows(group, tables, cols, values, blinding, blind_gen, rows, rows_out,
+                        (cudaStream_t)stream);
+}
 int zkl_shake256(const uint8_t* in, uint64_t len, uint8_t* out, uint64_t outlen) {
   shake256(in, (size_t)len, out, (size_t)outlen);
   return kOk;

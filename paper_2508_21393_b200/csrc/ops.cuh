@@ -89,6 +89,12 @@ int op_sumcheck_prove_sharded(void* const* tables, int k, int num_vars, const Te
 int op_igemm16(const int16_t* A, const int16_t* B, int64_t* C, int M, int K, int N,
                cudaStream_t s);
 int op_split16(const int16_t* src, uint64_t n, int8_t* hi, int8_t* lo, cudaStream_t s);
+// Hyrax row commitments (commit.cu): group 0 = q 96 p + 1, 1 = q 52 (2^61-1) + 1
+size_t commit_table_bytes(int group, int ngen);
+int op_commit_tables(int group, const uint8_t* gens_canon, int ngen, void* tables,
+                     cudaStream_t s);
+int op_commit_rows(int group, const void* tables, int cols, const void* vals, const void* blind,
+                   int blind_gen, int rows, uint8_t* out_canon, cudaStream_t s);
 int op_igemm_combine(const int32_t* hh, const int32_t* hl, const int32_t* lh, const int32_t* ll,
                      const int64_t* rowA, const int64_t* colB, int64_t K, int64_t* C, int M,
                      int N, cudaStream_t s);

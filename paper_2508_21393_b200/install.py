@@ -13,6 +13,8 @@ Module-attribute swap at every by-name import site:
   batch_inverse          -> zklora.field, zklora.lookup
   eq_table               -> zklora.mle, zklora.lookup, zklora.gadgets, zklora.commit
   fold_table             -> zklora.mle, zklora.sumcheck
+  commit (gpu_commit=True only)
+                         -> zklora.commit, zklora.gadgets, zklora.lookup
 and the result classes are pointed at the reference's own dataclasses, so
 proofs serialize with the reference wire format (serialize.py:52-74).
 Returns a callable that restores the original bindings.
@@ -21,7 +23,7 @@ Returns a callable that restores the original bindings.
 import importlib
 
 
-def install(pkg=None):
+def install(pkg=None, gpu_commit=False):
     from . import field as bf, gadgets as bg, lookup as bl, mle as bm, nonlinear as bn
     from . import sumcheck as bs
 
@@ -103,6 +105,14 @@ def install(pkg=None):
         swap(m, "eq_table", bm.eq_table)
     for m in (mods["mle"], zs):
         swap(m, "fold_table", bm.fold_table)
+    if gpu_commit:
+        # Hyrax row commitments on the GPU (commit_gpu.py): off by default --
+        # the north star keeps commitments on the reference path, timed
+        # separately; the same group elements either way
+        from . import commit_gpu
+
+        for m in (mods["commit"], zg, zl):
+            swap(m, "commit", commit_gpu.commit)
 
     def uninstall():
         for mod, attr, value in reversed(saved):
