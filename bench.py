@@ -635,6 +635,52 @@ def run_strong(world, rank, n=28):
     return out
 
 
+def run_commitments(num_vars=22, width_vars=11):
+    """Hyrax row commitments on the GPU (commit_gpu.py, csrc/commit.cu) for a
+    2^num_vars table of int16-valued entries (negatives as p - |x|, the block
+    tensors' form): key window tables once, then the commit itself.  The
+    north star times commitments separately; the reference's per-entry cost
+    is cpu_baseline.commitment_reference."""
+    import random
+    from collections import namedtuple
+
+    import torch
+
+    from paper_2508_21393_b200 import commit_gpu
+    from paper_2508_21393_b200 import device as D
+
+    grp = namedtuple("Group", "q order cofactor")(96 * P_BIG + 1, P_BIG, 96)
+    rnd = random.Random(1)
+    gens = tuple(pow(rnd.randrange(2, grp.q - 1), 96, grp.q) for _ in range(1 << width_vars))
+    key = namedtuple("Key", "group generators blinding_generator seed max_vars")(
+        grp, gens, pow(7, 96, grp.q), b"bench", 2 * width_vars)
+    spec = D.spec_for(P_BIG)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    commit_gpu.key_tables(key)
+    torch.cuda.synchronize()
+    t_key = time.perf_counter() - t0
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randint(-32768, 32768, (1 << num_vars,), device="cuda", dtype=torch.int32,
+                      generator=g).to(torch.int16)
+    dv = D.DeviceVector(D.lift(x, spec), 1 << num_vars, spec)
+    commit_gpu.commit_rows(key, dv, num_vars)
+    ts = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        commit_gpu.commit_rows(key, dv, num_vars)
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    sec = statistics.median(ts)
+    return {"what": "Hyrax row commitments (commit.py:98-115) of a 2^%d int16-valued table, "
+                    "q = 96 p + 1, on the GPU (fixed-base byte windows, csrc/commit.cu); "
+                    "bit-identical with the reference's commit (tests/test_gpu_commit.py)"
+                    % num_vars,
+            "seconds": sec, "us_per_entry": sec / (1 << num_vars) * 1e6,
+            "key_tables_s": t_key, "generators": (1 << width_vars) + 1}
+
+
 def run_hbm_kernels(peak_gbs):
     """The HBM-bound passes of the path, timed live with CUDA events on the
     proving stream (10 launches each, 2^27-entry inputs > L2): achieved GB/s
@@ -965,6 +1011,7 @@ def main():
         cfg4 = run_cfg4(max(1, args.steps // 10), 1, args.cfg4_shape)
 
     hbm = run_hbm_kernels(float(peaks.get("hbm_gbs", 6650.0)))
+    commitments = run_commitments()
 
     cfg5 = None
     if not args.no_cfg5:
@@ -1081,6 +1128,7 @@ def main():
         "cfg4": cfg4,
         "cfg5": cfg5,
         "hbm_kernels": hbm,
+        "commitments_gpu": commitments,
         "strong_scaling": strong,
     }
     print(json.dumps(line), flush=True)
