@@ -65,7 +65,7 @@ from .sumcheck import (  # noqa: F401
 from .transcript import Transcript  # noqa: F401
 
 
-def install(zklora_pkg=None):
+def install(zklora_pkg=None, gpu_commit=False):
     from .install import install as _install
 
-    return _install(zklora_pkg)
+    return _install(zklora_pkg, gpu_commit=gpu_commit)

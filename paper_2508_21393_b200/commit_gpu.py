@@ -25,6 +25,14 @@ from .device import MODULUS, TEST_MODULUS
 _GROUPS = {MODULUS: (0, 33, 8), TEST_MODULUS: (1, 9, 2)}
 
 
+def supports(key):
+    """True for the Schnorr groups the GPU implements (group.py:64-67)."""
+    g = key.group
+    o = _GROUPS.get(g.order)
+    return o is not None and g.q == {MODULUS: 96 * MODULUS + 1,
+                                     TEST_MODULUS: 52 * TEST_MODULUS + 1}[g.order]
+
+
 def _split_shape(num_vars):
     row_vars = (num_vars + 1) // 2
     return 1 << row_vars, 1 << (num_vars - row_vars)
@@ -99,6 +107,87 @@ def commit_rows(key, table, num_vars, blinding=None):
     raw = bytes(out)
     q = kt.qbytes
     return tuple(int.from_bytes(raw[i * q:(i + 1) * q], "little") for i in range(rows))
+
+
+def commit_row(key, values, blinding):
+    """One Pedersen row h^blinding prod_j g_j^values[j] (commit.py:87-95
+    `_row_commit`) as a group element."""
+    kt = key_tables(key)
+    cols = len(values)
+    if cols > kt.width:
+        raise _ref("commit").KeyTooSmall("key supports %d columns, need %d" % (kt.width, cols))
+    modulus = key.group.order
+    vals = _exponents(values, cols, modulus, kt.ewords)
+    blind = _exponents([blinding], 1, modulus, kt.ewords) if blinding else None
+    out = (ctypes.c_uint8 * kt.qbytes)()
+    N.check(N.lib().zkl_commit_rows(kt.group, D.ptr(kt.buf), cols, D.ptr(vals),
+                                    D.ptr(blind) if blind is not None else None, kt.width,
+                                    1, out, D.stream()))
+    return int.from_bytes(bytes(out), "little")
+
+
+def open_batch(key, tables, blindings, point, tr, rng):
+    """Drop-in for zklora.commit.open_batch (commit.py:150-215): the same
+    values, transcript records and OpeningProof, with the table-sized work on
+    the GPU -- each table's row-combined vector left^T T is a field matvec,
+    the batch combination is linear in those vectors, and the sigma proof's
+    row commitment is one GPU multi-exponentiation.  `tables` may be lists of
+    residues or DeviceVectors."""
+    from .gadgets import DeviceMatrix, _axpy, _matvec
+
+    cm = _ref("commit")
+    modulus = tr.modulus
+    spec = D.spec_for(modulus)
+    group = key.group
+    num_vars = len(point)
+    rows, cols = _split_shape(num_vars)
+    for t in tables:
+        if len(t) != rows * cols:
+            raise cm.DimensionMismatch("table does not match point arity")
+    half = (num_vars + 1) // 2
+    left = D.eq_table(list(point[:half]), spec)
+    right = D.eq_table(list(point[half:]), spec)
+    # y_k = left^T T_k (cols), value_k = <y_k, right>
+    ys, values = [], []
+    for t in tables:
+        buf = D.field_buffer(t, spec)
+        M = DeviceMatrix(buf.view(-1)[: rows * cols * spec.words].view(rows * cols, spec.words),
+                         rows, cols, N.MT_FIELD, spec)
+        y = _matvec(M, left, True, spec)
+        ys.append(y)
+        values.append(D.dot(y, right, spec, cols))
+    for r in point:
+        tr.append(b"open/point", r)
+    for v in values:
+        tr.append(b"open/value", v)
+    batch = tr.challenge(b"open/batch") if len(tables) > 1 else 1
+    # t_vec = left^T (sum_k batch^k T_k) = sum_k batch^k y_k; the blinding alike
+    t_vec = ys[0]
+    coeff = batch
+    for y in ys[1:]:
+        t_vec = _axpy(t_vec, coeff, y, cols, spec)
+        coeff = coeff * batch % modulus
+    blind = [0] * rows
+    coeff = 1
+    for b in blindings:
+        if b is not None:
+            for i, x in enumerate(b):
+                blind[i] = (blind[i] + coeff * x) % modulus
+        coeff = coeff * batch % modulus
+    b_comb = D.dot(left, D.upload(blind, spec), spec, rows)
+    y_comb = D.dot(t_vec, right, spec, cols)
+    nonce = rng.vector(cols)
+    nonce_blind = rng.next()
+    blinded_row = commit_row(key, nonce, nonce_blind)
+    nonce_dev = D.upload(nonce, spec)
+    blinded_value = D.dot(nonce_dev, right, spec, cols)
+    tr.append(b"open/sigma", group.encode(blinded_row))
+    tr.append(b"open/sigma-value", blinded_value)
+    c = tr.challenge(b"open/challenge")
+    responses = tuple(D.download(_axpy(nonce_dev, c, t_vec, cols, spec), spec, cols))
+    blinding_response = (nonce_blind + c * b_comb) % modulus
+    return values, cm.OpeningProof(y_comb, blinded_row, blinded_value, responses,
+                                   blinding_response)
 
 
 def _ref(name):

@@ -13,7 +13,7 @@ Module-attribute swap at every by-name import site:
   batch_inverse          -> zklora.field, zklora.lookup
   eq_table               -> zklora.mle, zklora.lookup, zklora.gadgets, zklora.commit
   fold_table             -> zklora.mle, zklora.sumcheck
-  commit (gpu_commit=True only)
+  commit, open_batch (gpu_commit=True only)
                          -> zklora.commit, zklora.gadgets, zklora.lookup
 and the result classes are pointed at the reference's own dataclasses, so
 proofs serialize with the reference wire format (serialize.py:52-74).
@@ -111,8 +111,25 @@ def install(pkg=None, gpu_commit=False):
         # separately; the same group elements either way
         from . import commit_gpu
 
+        ref_commit, ref_open = mods["commit"].commit, mods["commit"].open_batch
+
+        # groups the GPU implements (q = 96 p + 1, q = 52 (2^61 - 1) + 1);
+        # any other group (the reference's 31-bit toy group for exhaustive
+        # binding checks) keeps the reference's own code
+        def commit(key, table, blinding=None):
+            if commit_gpu.supports(key):
+                return commit_gpu.commit(key, table, blinding)
+            return ref_commit(key, table, blinding)
+
+        def open_batch(key, tables, blindings, point, tr, rng):
+            if commit_gpu.supports(key):
+                return commit_gpu.open_batch(key, tables, blindings, point, tr, rng)
+            return ref_open(key, tables, blindings, point, tr, rng)
+
+        commit.__wrapped__, open_batch.__wrapped__ = commit_gpu.commit, commit_gpu.open_batch
         for m in (mods["commit"], zg, zl):
-            swap(m, "commit", commit_gpu.commit)
+            swap(m, "commit", commit)
+            swap(m, "open_batch", open_batch)
 
     def uninstall():
         for mod, attr, value in reversed(saved):

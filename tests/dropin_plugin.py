@@ -41,16 +41,21 @@ def pytest_configure(config):
 
     z = importlib.import_module("zklora")
     assert os.path.dirname(z.__file__).startswith(REF), z.__file__
-    zb.install(z)
+    gpu_commit = os.environ.get("ZKL_DROPIN_GPU_COMMIT") == "1"
+    zb.install(z, gpu_commit=gpu_commit)
     # count calls at every installed binding (install() put the backend's
     # functions there; wrap them in place)
     from paper_2508_21393_b200 import gadgets as bg, lookup as bl, nonlinear as bn
     from paper_2508_21393_b200 import sumcheck as bs
 
-    backend = {id(f) for f in (bs.prove_sumcheck, bl.prove_lookup, bl.compute_multiplicities,
-               bg.prove_matmul, bg.prove_elementprod, bn.prove_rescale, bn.prove_swiglu,
-               bn.prove_rsqrt, bn.prove_softmax_row)}
-    for m in ("sumcheck", "lookup", "gadgets", "pipeline"):
+    fns = [bs.prove_sumcheck, bl.prove_lookup, bl.compute_multiplicities, bg.prove_matmul,
+           bg.prove_elementprod, bn.prove_rescale, bn.prove_swiglu, bn.prove_rsqrt,
+           bn.prove_softmax_row]
+    if gpu_commit:
+        zc = importlib.import_module("zklora.commit")
+        fns += [zc.commit, zc.open_batch]  # install()'s dispatchers
+    backend = {id(f) for f in fns}
+    for m in ("sumcheck", "lookup", "gadgets", "pipeline", "commit"):
         mod = importlib.import_module("zklora." + m)
         for attr, val in list(vars(mod).items()):
             if callable(val) and id(val) in backend:

@@ -37,6 +37,38 @@ MODULES = {
 }
 
 
+# with install(gpu_commit=True): the reference's commit / open_batch calls go to
+# the GPU Hyrax implementation (commit_gpu.py) as well
+GPU_COMMIT_MODULES = {
+    "test_commit.py": ["commit", "open_batch"],
+    "test_lookup.py": ["prove_lookup", "commit", "open_batch"],
+    "test_gadgets.py": ["prove_matmul", "commit", "open_batch"],
+    "test_pipeline.py": ["prove_matmul", "commit", "open_batch"],
+}
+
+
+def _run_module(module, tmp_path, gpu_commit):
+    calls = tmp_path / "calls.json"
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join(
+        [os.path.join(ROOT, "tests"), os.path.join(ROOT, "baseline", "_ref"), ROOT]),
+        ZKL_DROPIN_CALLS=str(calls), ZKL_DROPIN_GPU_COMMIT="1" if gpu_commit else "0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "dropin_plugin",
+                        "-p", "no:cacheprovider", "--hypothesis-seed=0", "--rootdir", REF_TESTS,
+                        os.path.join(REF_TESTS, module)],
+                       cwd=REF_TESTS, env=env, capture_output=True, text=True, timeout=3000)
+    return r, calls
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_TESTS), reason="baseline/_ref not installed")
+@pytest.mark.parametrize("module", sorted(GPU_COMMIT_MODULES))
+def test_reference_module_passes_with_gpu_commitments(module, tmp_path):
+    r, calls = _run_module(module, tmp_path, True)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    counts = json.loads(calls.read_text())
+    for name in GPU_COMMIT_MODULES[module]:
+        assert counts.get(name, 0) > 0, (name, counts)
+
+
 @pytest.mark.skipif(not os.path.isdir(REF_TESTS), reason="baseline/_ref not installed")
 @pytest.mark.parametrize("module", sorted(MODULES))
 def test_reference_module_passes_on_backend(module, tmp_path):

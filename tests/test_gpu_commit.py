@@ -132,7 +132,7 @@ def test_install_gpu_commit_proves_and_verifies_a_lookup():
 
     uninstall = install(zklora, gpu_commit=True)
     try:
-        assert ref_lookup.commit is commit_gpu.commit
+        assert ref_lookup.commit.__wrapped__ is commit_gpu.commit
         p = P_BIG
         key = ref_commit.keygen(8, b"gpu-commit-lookup", ref_group.BIG_GROUP)
         rng = ref_commit.BlindingStream(b"blind", p)
@@ -145,3 +145,36 @@ def test_install_gpu_commit_proves_and_verifies_a_lookup():
                                         Transcript(b"l", p, b"s"))
     finally:
         uninstall()
+
+
+@pytest.mark.skipif(not os.path.isdir(os.path.join(REF, "zklora")),
+                    reason="baseline/_ref not installed")
+@pytest.mark.parametrize("field,num_vars,ntables", [("big", 7, 1), ("big", 10, 3), ("test", 9, 2)])
+def test_open_batch_matches_reference(field, num_vars, ntables):
+    """commit_gpu.open_batch against zklora.commit.open_batch on the same
+    tables, point, transcript and blinding stream: the same values, the same
+    OpeningProof, the same end transcript state, and verify_batch accepts."""
+    sys.path.insert(0, REF)
+    try:
+        from zklora import commit as ref_commit
+        from zklora import group as ref_group
+        from zklora.transcript import Transcript
+    finally:
+        sys.path.remove(REF)
+    grp = ref_group.BIG_GROUP if field == "big" else ref_group.TEST_GROUP
+    p = grp.order
+    key = ref_commit.keygen(num_vars, b"gpu-open-test", grp)
+    rnd = random.Random(num_vars * 10 + ntables)
+    rows, cols = ref_commit.split_shape(num_vars)
+    tables = [[rnd.randrange(p) for _ in range(rows * cols)] for _ in range(ntables)]
+    blindings = [[rnd.randrange(p) for _ in range(rows)] if k % 2 == 0 else None
+                 for k in range(ntables)]
+    point = [rnd.randrange(p) for _ in range(num_vars)]
+    t1, t2 = Transcript(b"o", p, b"s"), Transcript(b"o", p, b"s")
+    r1, r2 = ref_commit.BlindingStream(b"n", p), ref_commit.BlindingStream(b"n", p)
+    want = ref_commit.open_batch(key, tables, blindings, point, t1, r1)
+    got = commit_gpu.open_batch(key, tables, blindings, point, t2, r2)
+    assert got == want
+    assert t1.state == t2.state
+    coms = [ref_commit.commit(key, t, b) for t, b in zip(tables, blindings)]
+    assert ref_commit.verify_batch(key, coms, point, got[0], got[1], Transcript(b"o", p, b"s"))
