@@ -1078,16 +1078,14 @@ template <int CH>
 __global__ void __launch_bounds__(256)
     k_mvf_finish(const uint64_t* part, uint64_t n, const uint64_t* sumx, fr_t offr, fr_t* y) {
   using IO = AccIO<CH>;
-  __shared__ fr_t s_k;
-  if (threadIdx.x == 0) {  // K = OFF * sum(x) mod p (sumx: 8 u64 limb sums)
-    LimbAcc<1> sa;
-#pragma unroll
-    for (int l = 0; l < 8; l++) sa.e[l] = sumx[l];
-    s_k = Fr255::mul(limb_reduce<1>(sa), offr);
-  }
-  __syncthreads();
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
+  // K = OFF * sum(x) mod p (sumx: 8 u64 limb sums), by every thread: no
+  // barrier, and the chain overlaps the thread's own reduction
+  LimbAcc<1> sa;
+#pragma unroll
+  for (int l = 0; l < 8; l++) sa.e[l] = sumx[l];
+  const fr_t s_k = Fr255::mul(limb_reduce<1>(sa), offr);
   LimbAcc<CH> acc;
   acc.zero();
   IO::add(acc, part + i * IO::NW);
@@ -1346,16 +1344,14 @@ __global__ void __launch_bounds__(128)
 // y[i] = reduce(sum_L rec[i][L] 2^(32 L)) - 2^63 sum(x)
 __global__ void __launch_bounds__(256)
     k_mvt64_finish(const uint64_t* rec, uint64_t n, const uint64_t* sumx, fr_t offr, fr_t* y) {
-  __shared__ fr_t s_k;
-  if (threadIdx.x == 0) {
-    LimbAcc<1> sa;
-#pragma unroll
-    for (int l = 0; l < 8; l++) sa.e[l] = sumx[l];
-    s_k = Fr255::mul(limb_reduce<1>(sa), offr);
-  }
-  __syncthreads();
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
+  // K = 2^63 sum(x) mod p, by every thread (no barrier: this chain runs
+  // beside the thread's own reduction)
+  LimbAcc<1> sa;
+#pragma unroll
+  for (int l = 0; l < 8; l++) sa.e[l] = sumx[l];
+  const fr_t s_k = Fr255::mul(limb_reduce<1>(sa), offr);
   // u64 limbs at 32-bit spacing -> 12 words with carries
   uint32_t w[12];
   uint64_t carry = 0;
