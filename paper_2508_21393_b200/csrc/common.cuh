@@ -167,6 +167,7 @@ constexpr size_t kFixedBcast = 256;   // challenge broadcast slot (tagged words,
 constexpr int kMbMaxOut = 16;         // raw outputs per round (LOGUP shape: 16)
 constexpr int kMbEvalWords = kMbMaxOut * 9;  // x 9 words (wide Fr sums)
 constexpr int kMbFinalWords = 8 * 8;  // up to 8 tables x 8 words
+constexpr int kMbTailWords = 3 * 64 * 8;  // host-tail tables: k x 2^h entries x 8 words
 struct alignas(128) Mailbox {
   volatile uint64_t ev[kMbEvalWords];   // device -> host: round sums
   volatile uint64_t ch[8];              // host -> device: challenge (storage form)
@@ -174,6 +175,7 @@ struct alignas(128) Mailbox {
   volatile uint32_t abort;              // host -> device
   volatile uint32_t status;             // device -> host: 1 = timed out waiting
   volatile uint32_t seq;                // host-side sequence counter (not read by the device)
+  volatile uint64_t tail[kMbTailWords];  // device -> host: folded tables of a host tail
 };
 int mailbox_for_current_device(Mailbox** host, Mailbox** dev);
 

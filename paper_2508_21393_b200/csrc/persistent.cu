@@ -1111,8 +1111,9 @@ constexpr int kClusterThreads = 256;
 
 template <class F, int MAXK, class EV>
 __global__ void __launch_bounds__(kClusterThreads)
-    k_sumcheck_cluster(TablePtrs<F, MAXK> tabs, int k, int num_vars, int j0, Terms<F> tm,
-                       Mailbox* mb, unsigned* fail, uint32_t seq0, uint64_t* trace, int L) {
+    k_sumcheck_cluster(TablePtrs<F, MAXK> tabs, int k, int num_vars, int j0, int j_end,
+                       Terms<F> tm, Mailbox* mb, unsigned* fail, uint32_t seq0, uint64_t* trace,
+                       int L) {
   using T = typename F::T;
   using R = Red<F>;
   using W = typename R::W;
@@ -1154,7 +1155,7 @@ __global__ void __launch_bounds__(kClusterThreads)
     if (s_flag == 2) return;
     r = s_r;
   }
-  for (int j = j0; j < num_vars; j++) {
+  for (int j = j0; j < j_end; j++) {
     const uint32_t seq = seq0 + (uint32_t)j + 1;
     const bool fold = j > 0;
     const bool tr0 = trace && rank == 0 && threadIdx.x == 0;
@@ -1198,7 +1199,23 @@ __global__ void __launch_bounds__(kClusterThreads)
     if (s_flag == 2) return;
     r = s_r;
   }
-  if (rank == 0) publish_finals<F, MAXK>(tabs, k, r, seq0 + (uint32_t)num_vars + 1, mb);
+  if (j_end == num_vars) {
+    if (rank == 0) publish_finals<F, MAXK>(tabs, k, r, seq0 + (uint32_t)num_vars + 1, mb);
+    return;
+  }
+  // host tail: fold by the last challenge and send the k x 2^(n - j_end)
+  // survivors to the host as tagged words (it runs the remaining rounds)
+  const uint64_t th = 1ull << (num_vars - j_end);
+  const uint32_t fseq = seq0 + (uint32_t)num_vars + 1;
+  for (uint64_t idx = gtid; idx < (uint64_t)k * th; idx += nthreads) {
+    const int q = (int)(idx / th);
+    const uint64_t i = idx - (uint64_t)q * th;
+    const T* t = tabs.t[q];
+    const T a = ld_cg(t + i), b = ld_cg(t + i + th);
+    const T f = F::add(a, F::mul(r, F::sub(b, a)));
+#pragma unroll
+    for (int w = 0; w < NC; w++) mb->tail[idx * NC + w] = tag(Words<F>::word(f, w), fseq);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1220,6 +1237,7 @@ struct Plan {
   int grid, block;   // grid kernel shape
   int cgrid, cblock; // cluster kernel shape (one cluster)
   int lanes;
+  int j_end;         // cluster kernel stops after round j_end - 1 (host tail below n)
 };
 
 template <class F, int MAXK, class EV>
@@ -1268,7 +1286,7 @@ struct Persistent {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     ZKL_CUDA(cudaLaunchKernelEx(&cfg, k_sumcheck_cluster<F, MAXK, EV>, tp, k, num_vars,
-                                pl.j_switch, tm, mb, fail, seq0, trace, pl.lanes));
+                                pl.j_switch, pl.j_end, tm, mb, fail, seq0, trace, pl.lanes));
     ZKL_LAUNCH_CHECK();
     return kOk;
   }
@@ -1285,6 +1303,7 @@ struct Persistent {
     }
     Plan pl;
     pl.lanes = lanes;
+    pl.j_end = num_vars;
     const uint64_t per_pair = lanes > 0 ? (uint64_t)lanes : 1;
     // cluster: up to 16 CTAs x 256 threads; lane mode loops when a round
     // has more pairs than lane groups (at most kClusterPasses passes)
@@ -1477,6 +1496,14 @@ static void host_quad(const typename F::T& c0, const typename F::T& c1, const ty
 
 static bool g_phase_dirty = true;  // after a failure the ticket / flags need a reset
 
+int host_tail_default() {
+  static const int v = [] {
+    const char* e = getenv("ZKL_HOST_TAIL");
+    return e ? atoi(e) : 5;
+  }();
+  return v;
+}
+
 bool no_persistent() {
   // ncu marks its target with NV_NSIGHT_INJECTION_* / NV_TPS_LAUNCH_TOKEN;
   // compute-sanitizer and other injectors use CUDA_INJECTION64_PATH.
@@ -1533,7 +1560,7 @@ static int run_phase_stepwise(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* roun
 template <class F>
 int wait_phase_finals(const PhaseArgs<F>& a, typename F::T* finals_out, cudaStream_t s) {
   constexpr int NC = Words<F>::N;
-  if (a.stepwise) {
+  if (a.stepwise || a.host_done) {
     for (int q = 0; q < a.k; q++) finals_out[q] = a.fin_cache[q];
     return kOk;
   }
@@ -1555,6 +1582,79 @@ int wait_phase_finals(const PhaseArgs<F>& a, typename F::T* finals_out, cudaStre
 template <class F>
 static int run_phase_replay(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out,
                             uint8_t* point_out, typename F::T* finals_out, cudaStream_t s);
+
+// The last n - ndev rounds of a phase on the host (PhaseArgs::host_tail):
+// the cluster kernel has folded by r_{ndev-1} and sent the k x 2^(n-ndev)
+// survivors; each round evaluates
+//   evals[x] = post_mul (post_add[j] + sum_i sum_t coef_t prod_f T_f(x, i)),
+// T(x, i) = T[i] + x (T[i + half] - T[i]), exactly the device identities,
+// then appends / draws as the device loop does and folds by the challenge.
+template <class F>
+static int host_tail_rounds(PhaseArgs<F>& a, Mailbox* mb_host, uint32_t seq0, int ndev,
+                            const typename F::T* post_add, const typename F::T& pm,
+                            HostTranscript& tr, uint8_t* rounds_out, uint8_t* point_out,
+                            cudaStream_t s) {
+  using T = typename F::T;
+  using H = typename host::For<F>::H;
+  constexpr int NC = Words<F>::N, nb = F::kBytes;
+  const Terms<F>& tm = a.tm;
+  const int n = a.num_vars, k = a.k, deg = tm.degree;
+  uint64_t cur = 1ull << (n - ndev);
+  std::vector<uint32_t> words((size_t)k * cur * NC);
+  int rc = wait_words<F>(mb_host, mb_host->tail, (int)words.size(), seq0 + (uint32_t)n + 1,
+                         words.data(), s, "tail tables", ndev);
+  if (rc) return rc;
+  std::vector<T> tab((size_t)k * cur);
+  for (size_t i = 0; i < tab.size(); i++) memcpy(&tab[i], words.data() + i * NC, nb);
+  const uint64_t stride = cur;  // table q at tab[q * stride ..]
+  std::vector<T> vx((size_t)k * 4);
+  for (int j = ndev; j < n; j++) {
+    const uint64_t half = cur >> 1;
+    T acc[kMaxTerms][4];
+    for (int t = 0; t < tm.nterms; t++)
+      for (int x = 0; x < 4; x++) acc[t][x] = H::zero();
+    for (uint64_t i = 0; i < half; i++) {
+      for (int q = 0; q < k; q++) {
+        const T a0 = tab[q * stride + i];
+        const T d = H::sub(tab[q * stride + i + half], a0);
+        T v = a0;
+        for (int x = 0; x <= deg; x++) {
+          if (x) v = H::add(v, d);
+          vx[q * 4 + x] = v;
+        }
+      }
+      for (int t = 0; t < tm.nterms; t++)
+        for (int x = 0; x <= deg; x++) {
+          T p = tm.nf[t] ? vx[tm.fi[t][0] * 4 + x] : H::one();  // no factor: constant term
+          for (int f = 1; f < tm.nf[t]; f++) p = H::mul(p, vx[tm.fi[t][f] * 4 + x]);
+          acc[t][x] = H::add(acc[t][x], p);
+        }
+    }
+    uint8_t* rj = rounds_out + (size_t)j * (deg + 1) * nb;
+    for (int x = 0; x <= deg; x++) {
+      T v = post_add ? post_add[j] : H::zero();
+      for (int t = 0; t < tm.nterms; t++) v = H::add(v, H::mul(tm.coef[t], acc[t][x]));
+      host::to_canon<F>(rj + x * nb, H::mul(pm, v));
+      tr.append_elem("sumcheck/eval", rj + x * nb, nb);
+    }
+    uint8_t rawc[64];
+    tr.challenge_squeeze("sumcheck/round", 14, rawc);
+    uint8_t* rcan = point_out + (size_t)j * nb;
+    reduce512<F>(rawc, rcan);
+    tr.challenge_absorb(rawc);
+    const T r = host::from_canon<F>(rcan);
+    for (int q = 0; q < k; q++)
+      for (uint64_t i = 0; i < half; i++) {
+        const T a0 = tab[q * stride + i];
+        tab[q * stride + i] = H::add(a0, H::mul(r, H::sub(tab[q * stride + i + half], a0)));
+      }
+    cur = half;
+  }
+  a.fin_cache.resize(k);
+  for (int q = 0; q < k; q++) a.fin_cache[q] = tab[q * stride];
+  a.host_done = true;
+  return kOk;
+}
 
 static bool profile_replay() {
   static const bool v = getenv("ZKL_PROFILE_REPLAY") != nullptr;
@@ -1601,6 +1701,16 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
   int nout = 4;
   run_dispatch<F>(rq, &pl, &nout, 0);
   if (nrun < n) pl.j_switch = nrun;  // grid kernel only, stops after round nrun-1
+  // host tail: the cluster kernel runs rounds [j_switch, n - h)
+  int h = a.host_tail;
+  if (h > n - 1) h = n - 1;
+  while (h > 0 && (size_t)k * ((size_t)1 << h) * NC > (size_t)kMbTailWords) h--;
+  if (h <= 0 || nrun < n || shape == kLogupTiled || a.sharded || a.replaying ||
+      n - h <= pl.j_switch)
+    h = 0;
+  a.host_done = false;
+  if (h) pl.j_end = n - h;
+  const int ndev = n - h;  // rounds the device runs (nrun when no tail)
   void* ws;
   rc = scratch_reserve((size_t)pl.grid * kMbMaxOut * sizeof(W), &ws, s);
   if (rc) return rc;
@@ -1687,7 +1797,7 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
   uint32_t words[kMbEvalWords];
   std::vector<double> h_first;
   if (tracing) h_first.resize(n);
-  for (int j = 0; j < nrun; j++) {
+  for (int j = 0; j < (h ? ndev : nrun); j++) {
     if (tracing) {  // first tagged word of this round visible
       while ((uint32_t)(mb_host->ev[0] >> 32) != seq0 + j + 1 && !mb_host->status) {
       }
@@ -1828,12 +1938,20 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
     }
     tr.challenge_absorb(rawc);
   }
+  if (h) {
+    rc = host_tail_rounds<F>(a, mb_host, seq0, ndev, lazy_add.empty() ? a.post_add : lazy_add.data(),
+                             pm, tr, rounds_out, point_out, s);
+    if (rc) {
+      g_phase_dirty = true;
+      return rc;
+    }
+  }
   if (finals_out) {
     rc = wait_phase_finals<F>(a, finals_out, s);
     if (rc) return rc;
   }
   if (tracing) {
-    const int n = nrun;  // rounds actually run
+    const int n = h ? ndev : nrun;  // rounds the device actually ran
     std::vector<uint64_t> tv((size_t)n * 8);
     cudaMemcpyAsync(tv.data(), trace, tv.size() * 8, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
@@ -1990,6 +2108,7 @@ int op_sumcheck_prove(void* const* tables, int k, int num_vars, const Terms<F>& 
   a.tm = tm;
   a.post_add = post_add;
   a.post_mul = post_mul;
+  a.host_tail = host_tail_default();
   std::vector<T> fin(k);
   int rc = run_phase<F>(a, tr, rounds_out, point_out, fin.data(), s);
   if (rc) return rc;

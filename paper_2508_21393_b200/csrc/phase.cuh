@@ -41,6 +41,14 @@ struct PhaseArgs {
   // the LOGUP_TILED shape, whose structure holds only while the bound
   // variables are above the tiled tables' index bits.
   int rounds_limit = 0;
+  // > 0: the last `host_tail` rounds run on the host.  The cluster kernel
+  // stops after round n - host_tail - 1, folds by its challenge and sends the
+  // 2^host_tail-entry tables through the mailbox; the host finishes the
+  // rounds (same evaluations, same transcript) and the finals, which
+  // wait_phase_finals then returns.  Ignored where unsupported (grid-kernel
+  // rounds, LOGUP_TILED, sharded, replays, stepwise mode).
+  int host_tail = 0;
+  bool host_done = false;  // set by run_phase: the finals are in fin_cache
   int forced_shape = -1;
   // LOGUP_TILED host finishing: the eq point u (num_vars, storage form) and
   // the table-side constants K3 = sum_ti B T eq_lo, SMB = sum_ti M B
@@ -61,6 +69,10 @@ struct PhaseArgs {
 // CUDA_LAUNCH_BLOCKING=1, or an injected profiler / sanitizer (a replayed
 // kernel would spin on a mailbox the host never answers)
 bool no_persistent();
+
+// rounds a phase leaves to the host by default (ZKL_HOST_TAIL, default 5;
+// 0 = every round on the device)
+int host_tail_default();
 
 // Runs every round with the native transcript `tr` (appends each evaluation
 // under "sumcheck/eval", draws "sumcheck/round").  Outputs are canonical

@@ -584,6 +584,7 @@ struct MatmulJob {
         pu.num_vars = d0;
         pu.tm = prod2_terms<F>(H::one());
         pu.post_mul = H::one();
+        pu.host_tail = host_tail_default();
         if ((rc = run_phase<F>(pu, *tr, rounds, point, nullptr, s))) return rc;
       }
     }
@@ -600,6 +601,7 @@ struct MatmulJob {
       pw.num_vars = d1;
       pw.tm = prod2_terms<F>(H::one());
       pw.post_mul = H::one();
+      pw.host_tail = host_tail_default();
       pw.prepare = [this](std::vector<T>& adds) -> int {
         int r = get_e_hat();
         if (r) return r;
@@ -661,6 +663,7 @@ struct MatmulJob {
       tm.coef[1] = cneg;
       pv.tm = tm;
       pv.post_mul = H::one();
+      pv.host_tail = host_tail_default();
       pv.prepare = [this](std::vector<T>&) -> int {
         int r = get_e_hat();
         if (r) return r;

@@ -372,6 +372,26 @@ def test_zero_u_phase_shortcut_off_matches_golden():
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
 
 
+@pytest.mark.parametrize("tail", ["0", "1", "6"])
+def test_host_tail_rounds_match_golden(tail):
+    """The last ZKL_HOST_TAIL rounds of a phase run on the host (default 5;
+    the cluster kernel sends the folded survivors through the mailbox).  With
+    every round on the device (0), one host round (1) and six (6), the
+    sumcheck and zkMat proofs are the reference's goldens, constant terms,
+    repeated factors and post_add rounds included."""
+    code = (
+        "import sys; sys.path[:0] = ['.', 'tests', 'tests/golden']\n"
+        "import pytest, test_gpu_parity as T\n"
+        "mp = pytest.MonkeyPatch()\n"
+        "T.test_sumcheck_golden(True, mp)\n"
+        "for mode in ('i16', 'i64', 'field'):\n"
+        "    T.test_matmul_sumcheck_golden(mode, 'native')\n"
+        "T.test_matmul_batch_matches_per_claim('big')\n"
+        "print('ok')\n")
+    r = _run_isolated(code, ZKL_HOST_TAIL=tail)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
+
+
 def test_stepwise_mode_matches_oracle():
     """ZKL_NO_PERSISTENT=1 (what profilers get automatically): one launch per
     round through the same drivers, still bit-exact."""
