@@ -1006,7 +1006,9 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<EV>::value)
     if (tr0) trace[j * 8 + 0] = globaltimer();
     const uint64_t tb0 = trace ? globaltimer() : 0;
     const uint64_t half = 1ull << (num_vars - 1 - j);
-    const int Lr = (L > 0 && half * (uint64_t)L <= nthreads) ? L : 0;
+    // lane mode while a round needs at most L >> 8 passes of the cluster
+    const int Ll = L & 255;
+    const int Lr = (Ll > 0 && half * (uint64_t)Ll <= nthreads * (uint64_t)(L >> 8)) ? Ll : 0;
     accumulate_round<F, MAXK, EV>(tabs, k, tm, half, fold, r, Lr, gtid, nthreads, wsum);
     if (tr0) trace[j * 8 + 1] = globaltimer();
     __syncthreads();
@@ -1162,7 +1164,9 @@ __global__ void __launch_bounds__(kClusterThreads)
     if (tr0) trace[j * 8 + 0] = globaltimer();
     const uint64_t tb0 = trace ? globaltimer() : 0;
     const uint64_t half = 1ull << (num_vars - 1 - j);
-    const int Lr = (L > 0 && half * (uint64_t)L <= nthreads) ? L : 0;
+    // lane mode while a round needs at most L >> 8 passes of the cluster
+    const int Ll = L & 255;
+    const int Lr = (Ll > 0 && half * (uint64_t)Ll <= nthreads * (uint64_t)(L >> 8)) ? Ll : 0;
     accumulate_round<F, MAXK, EV>(tabs, k, tm, half, fold, r, Lr, gtid, nthreads, wsum);
     if (tr0) trace[j * 8 + 1] = globaltimer();
     __syncthreads();
@@ -1285,8 +1289,14 @@ struct Persistent {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    static const int passes = [] {  // ZKL_CLUSTER_LANE_PASSES (default 4)
+      const char* e = getenv("ZKL_CLUSTER_LANE_PASSES");
+      const int v = e ? atoi(e) : 4;
+      return v < 1 ? 1 : v > 64 ? 64 : v;
+    }();
+    const int lp = pl.lanes | (passes << 8);
     ZKL_CUDA(cudaLaunchKernelEx(&cfg, k_sumcheck_cluster<F, MAXK, EV>, tp, k, num_vars,
-                                pl.j_switch, pl.j_end, tm, mb, fail, seq0, trace, pl.lanes));
+                                pl.j_switch, pl.j_end, tm, mb, fail, seq0, trace, lp));
     ZKL_LAUNCH_CHECK();
     return kOk;
   }
@@ -1599,15 +1609,25 @@ static int host_tail_rounds(PhaseArgs<F>& a, Mailbox* mb_host, uint32_t seq0, in
   constexpr int NC = Words<F>::N, nb = F::kBytes;
   const Terms<F>& tm = a.tm;
   const int n = a.num_vars, k = a.k, deg = tm.degree;
+  static const bool tracing = getenv("ZKL_TRACE") != nullptr;
+  auto now_us = [] {
+    return std::chrono::duration<double, std::micro>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+  };
+  const double t0 = tracing ? now_us() : 0;
   uint64_t cur = 1ull << (n - ndev);
   std::vector<uint32_t> words((size_t)k * cur * NC);
   int rc = wait_words<F>(mb_host, mb_host->tail, (int)words.size(), seq0 + (uint32_t)n + 1,
                          words.data(), s, "tail tables", ndev);
   if (rc) return rc;
+  const double t1 = tracing ? now_us() : 0;
   std::vector<T> tab((size_t)k * cur);
   for (size_t i = 0; i < tab.size(); i++) memcpy(&tab[i], words.data() + i * NC, nb);
   const uint64_t stride = cur;  // table q at tab[q * stride ..]
-  std::vector<T> vx((size_t)k * 4);
+  // per term: a 2-factor product needs 3 sums (f0 g0, f1 g1, fd gd; x = 2, 3
+  // follow from the quadratic), a linear term 2, a 3-factor product 4
+  std::vector<T> lo((size_t)k), hi((size_t)k), df((size_t)k);
   for (int j = ndev; j < n; j++) {
     const uint64_t half = cur >> 1;
     T acc[kMaxTerms][4];
@@ -1615,20 +1635,55 @@ static int host_tail_rounds(PhaseArgs<F>& a, Mailbox* mb_host, uint32_t seq0, in
       for (int x = 0; x < 4; x++) acc[t][x] = H::zero();
     for (uint64_t i = 0; i < half; i++) {
       for (int q = 0; q < k; q++) {
-        const T a0 = tab[q * stride + i];
-        const T d = H::sub(tab[q * stride + i + half], a0);
-        T v = a0;
-        for (int x = 0; x <= deg; x++) {
-          if (x) v = H::add(v, d);
-          vx[q * 4 + x] = v;
+        lo[q] = tab[q * stride + i];
+        hi[q] = tab[q * stride + i + half];
+        df[q] = H::sub(hi[q], lo[q]);
+      }
+      for (int t = 0; t < tm.nterms; t++) {
+        const int* fi = tm.fi[t];
+        switch (tm.nf[t]) {
+          case 0:
+            acc[t][0] = H::add(acc[t][0], H::one());
+            break;
+          case 1:
+            acc[t][0] = H::add(acc[t][0], lo[fi[0]]);
+            acc[t][1] = H::add(acc[t][1], hi[fi[0]]);
+            break;
+          case 2:
+            acc[t][0] = H::add(acc[t][0], H::mul(lo[fi[0]], lo[fi[1]]));
+            acc[t][1] = H::add(acc[t][1], H::mul(hi[fi[0]], hi[fi[1]]));
+            acc[t][2] = H::add(acc[t][2], H::mul(df[fi[0]], df[fi[1]]));
+            break;
+          default: {
+            T v0 = lo[fi[0]], v1 = lo[fi[1]], v2 = lo[fi[2]];
+            for (int x = 0; x <= deg; x++) {
+              if (x) {
+                v0 = H::add(v0, df[fi[0]]);
+                v1 = H::add(v1, df[fi[1]]);
+                v2 = H::add(v2, df[fi[2]]);
+              }
+              acc[t][x] = H::add(acc[t][x], H::mul(H::mul(v0, v1), v2));
+            }
+          }
         }
       }
-      for (int t = 0; t < tm.nterms; t++)
-        for (int x = 0; x <= deg; x++) {
-          T p = tm.nf[t] ? vx[tm.fi[t][0] * 4 + x] : H::one();  // no factor: constant term
-          for (int f = 1; f < tm.nf[t]; f++) p = H::mul(p, vx[tm.fi[t][f] * 4 + x]);
-          acc[t][x] = H::add(acc[t][x], p);
-        }
+    }
+    for (int t = 0; t < tm.nterms; t++) {
+      T e[4];
+      if (tm.nf[t] == 0) {  // half copies of 1 at every x
+        e[0] = e[1] = e[2] = e[3] = acc[t][0];
+      } else if (tm.nf[t] == 1) {
+        const T d = H::sub(acc[t][1], acc[t][0]);
+        e[0] = acc[t][0];
+        e[1] = acc[t][1];
+        e[2] = H::add(e[1], d);
+        e[3] = H::add(e[2], d);
+      } else if (tm.nf[t] == 2) {
+        host_quad<F>(acc[t][0], acc[t][1], acc[t][2], e);
+      } else {
+        continue;
+      }
+      for (int x = 0; x < 4; x++) acc[t][x] = e[x];
     }
     uint8_t* rj = rounds_out + (size_t)j * (deg + 1) * nb;
     for (int x = 0; x <= deg; x++) {
@@ -1653,6 +1708,9 @@ static int host_tail_rounds(PhaseArgs<F>& a, Mailbox* mb_host, uint32_t seq0, in
   a.fin_cache.resize(k);
   for (int q = 0; q < k; q++) a.fin_cache[q] = tab[q * stride];
   a.host_done = true;
+  if (tracing)
+    fprintf(stderr, "[zkl trace] host tail n=%d k=%d rounds %d: wait tables %.2f us, rounds %.2f us\n",
+            n, k, n - ndev, t1 - t0, now_us() - t1);
   return kOk;
 }
 
