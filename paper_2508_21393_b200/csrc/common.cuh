@@ -164,13 +164,14 @@ constexpr size_t kFixedBcast = 256;   // challenge broadcast slot (tagged words,
 // 32), written and read with single 8-byte accesses, so a reader knows a
 // message is complete when every word carries the expected sequence number:
 // no flag word and no system-scope fence on either side.
-constexpr int kMbMaxOut = 16;         // raw outputs per round (LOGUP shape: 16)
+constexpr int kMbMaxOut = 18;         // raw outputs per round (paired SUM2PROD2: 18)
 constexpr int kMbEvalWords = kMbMaxOut * 9;  // x 9 words (wide Fr sums)
 constexpr int kMbFinalWords = 8 * 8;  // up to 8 tables x 8 words
 constexpr int kMbTailWords = 3 * 64 * 8;  // host-tail tables: k x 2^h entries x 8 words
 struct alignas(128) Mailbox {
   volatile uint64_t ev[kMbEvalWords];   // device -> host: round sums
   volatile uint64_t ch[8];              // host -> device: challenge (storage form)
+  volatile uint64_t ch2[8];             // host -> device: a pair's second challenge
   volatile uint64_t fin[kMbFinalWords]; // device -> host: final values (storage form)
   volatile uint32_t abort;              // host -> device
   volatile uint32_t status;             // device -> host: 1 = timed out waiting

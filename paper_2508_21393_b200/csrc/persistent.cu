@@ -1006,9 +1006,10 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<EV>::value)
     if (tr0) trace[j * 8 + 0] = globaltimer();
     const uint64_t tb0 = trace ? globaltimer() : 0;
     const uint64_t half = 1ull << (num_vars - 1 - j);
-    // lane mode while a round needs at most L >> 8 passes of the cluster
+    // lane mode while a round needs at most (L >> 8) & 255 passes of the cluster
     const int Ll = L & 255;
-    const int Lr = (Ll > 0 && half * (uint64_t)Ll <= nthreads * (uint64_t)(L >> 8)) ? Ll : 0;
+    const int Lr =
+        (Ll > 0 && half * (uint64_t)Ll <= nthreads * (uint64_t)((L >> 8) & 255)) ? Ll : 0;
     accumulate_round<F, MAXK, EV>(tabs, k, tm, half, fold, r, Lr, gtid, nthreads, wsum);
     if (tr0) trace[j * 8 + 1] = globaltimer();
     __syncthreads();
@@ -1111,6 +1112,51 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<EV>::value)
 constexpr int kClusterMax = 16;
 constexpr int kClusterThreads = 256;
 
+
+// ---------------------------------------------------------------------------
+// Lookahead rounds (cluster kernel, PROD2 / SUM2PROD2 over Fr).  Round j+1's
+// raw sums are quadratics in the challenge r_j: with T the tables folded by
+// r_0 .. r_{j-1}, h = half of round j, h' = h / 2 and the round-(j+1) pair i
+// built from the quadruple a = T[i], b = T[i + h'], c = T[i + h], d =
+// T[i + h + h'], its lo / hi / difference entries are p + r (q - p) for
+// (p, q) = (a, c), (b, d), (b - a, d - c), and each product sum is
+//   sum (p_F + r dF)(p_X + r dX) = S_pp + r (S_qq - S_pp - S_dd) + r^2 S_dd
+// with S_pp = sum p_F p_X, S_qq = sum q_F q_X, S_dd = sum (q - p)_F (q - p)_X.
+// So while the host answers round j the cluster folds T by r_{j-1} and forms
+// those 3 sums per raw output; once r_j arrives CTA 0 only evaluates the
+// quadratics (two products) and publishes round j+1.  The per-pair work
+// (folds, products, cluster reduction) leaves the round trip's critical path.
+// The raw sums are the same field values the direct evaluators publish.
+template <class F, class EV>
+struct La {
+  static constexpr bool kOn = false;
+  static constexpr int NR = 1, NT = 1, L = 32;
+};
+template <int MAXK>
+struct La<Fr255, EvProd2<Fr255, MAXK>> {
+  static constexpr bool kOn = true;
+  static constexpr int NR = 3, NT = 2, L = 16;  // 8 fold lanes, 9 product lanes
+};
+template <int MAXK>
+struct La<Fr255, EvSum2Prod2<Fr255, MAXK>> {
+  static constexpr bool kOn = true;
+  static constexpr int NR = 6, NT = 3, L = 32;  // 12 fold lanes, 18 product lanes
+};
+
+// a wide sum of storage-form values -> its residue (storage form)
+ZKL_D fr_t wide_to_field(const Red<Fr255>::W& w) {
+  fr_t lo;
+#pragma unroll
+  for (int i = 0; i < 8; i++) lo.v[i] = w.w[i];
+  lo = Fr255::reduce_once(Fr255::reduce_once(lo));  // lo < 2^256 < 3p
+  if (w.w[8]) {
+    fr_t h = Fr255::zero();
+    h.v[0] = w.w[8];
+    lo = Fr255::add(lo, Fr255::mul(h, Fr255::r2()));  // w8 2^256 mod p
+  }
+  return lo;
+}
+
 template <class F, int MAXK, class EV>
 __global__ void __launch_bounds__(kClusterThreads)
     k_sumcheck_cluster(TablePtrs<F, MAXK> tabs, int k, int num_vars, int j0, int j_end,
@@ -1157,16 +1203,18 @@ __global__ void __launch_bounds__(kClusterThreads)
     if (s_flag == 2) return;
     r = s_r;
   }
-  for (int j = j0; j < j_end; j++) {
+  // one round evaluated directly: fold by r, evaluate, reduce, publish
+  auto direct_round = [&](int j) {
     const uint32_t seq = seq0 + (uint32_t)j + 1;
     const bool fold = j > 0;
     const bool tr0 = trace && rank == 0 && threadIdx.x == 0;
     if (tr0) trace[j * 8 + 0] = globaltimer();
     const uint64_t tb0 = trace ? globaltimer() : 0;
     const uint64_t half = 1ull << (num_vars - 1 - j);
-    // lane mode while a round needs at most L >> 8 passes of the cluster
+    // lane mode while a round needs at most (L >> 8) & 255 passes of the cluster
     const int Ll = L & 255;
-    const int Lr = (Ll > 0 && half * (uint64_t)Ll <= nthreads * (uint64_t)(L >> 8)) ? Ll : 0;
+    const int Lr =
+        (Ll > 0 && half * (uint64_t)Ll <= nthreads * (uint64_t)((L >> 8) & 255)) ? Ll : 0;
     accumulate_round<F, MAXK, EV>(tabs, k, tm, half, fold, r, Lr, gtid, nthreads, wsum);
     if (tr0) trace[j * 8 + 1] = globaltimer();
     __syncthreads();
@@ -1198,6 +1246,188 @@ __global__ void __launch_bounds__(kClusterThreads)
       publish_sums<F, EV::NOUT>(tot, seq, mb, s_words);
       if (trace && lane == 0) trace[j * 8 + 3] = globaltimer();
     }
+  };
+  int jl = j0;  // first round of the direct loop
+  if constexpr (La<F, EV>::kOn) {
+    // paired rounds (host flag; j_end < num_vars: a host tail follows)
+    if (((L >> 16) & 1) && j0 == 0 && j_end >= 2 && j_end < num_vars) {
+      using LA = La<F, EV>;
+      constexpr int NP = 3 * LA::NR;  // product sums per pass
+      constexpr int Lq = LA::L;
+      __shared__ W la_wsum[kClusterThreads / 32][NP];
+      __shared__ W la_gather[kClusterMax][NP];
+      __shared__ T s_r2;  // r_{j+1} of a pair (written by CTA 0)
+      __shared__ uint32_t s_cw2[NC];
+      const int tF = tm.fi[0][0], tG = tm.fi[0][1], tH = LA::NT == 3 ? tm.fi[1][1] : 0;
+      auto tab_of = [&](int t) -> T* { return tabs.t[t == 0 ? tF : t == 1 ? tG : tH]; };
+      // one pass over round j's quadruples (round j+1's pairs): the tables are
+      // first brought from round j-2 to round j by folding with (ra, rb) when
+      // `fold`; then the 3 NR product sums, reduced over the cluster and
+      // published under round j's tag
+      auto la_pass = [&](int j, int nfold, const T& ra, const T& rb) {
+        const uint64_t h1 = 1ull << (num_vars - 2 - j);  // pairs of round j+1
+        const uint64_t hj = 2 * h1;                      // round j's half
+        const uint64_t hm1 = 2 * hj, hm2 = 4 * hj;       // rounds j-1, j-2 halves
+        const uint64_t ngroups = nthreads / Lq;
+        const int q = lane & (Lq - 1), gb = lane & ~(Lq - 1);
+        // fold lane q < 4 NT: table q / 4, entry q % 4 of the quadruple (a, b, c, d)
+        const bool fl = q < 4 * LA::NT;
+        T* tq = tab_of(fl ? q >> 2 : 0);
+        const uint64_t moff = (uint64_t)(q & 1) * h1 + (uint64_t)((q >> 1) & 1) * hj;
+        // product lane q < 3 NR: raw output o = q / 3 (F x G for o < 3, F x H
+        // above), kind 0 lo (a, c), 1 hi (b, d), 2 difference (b - a, d - c);
+        // term sk: 0 p p, 1 q q, 2 (q - p)(q - p)
+        const bool pl = q < NP;
+        const int o = pl ? q / 3 : 0, sk = q % 3, kind = o % 3;
+        const int xl = o < 3 ? 4 : 8;
+        T acc = F::zero();
+        const uint64_t passes = (h1 + ngroups - 1) / ngroups;
+        uint64_t i = gtid / Lq;
+        for (uint64_t ps = 0; ps < passes; ps++, i += ngroups) {
+          const bool active = i < h1;
+          T v = F::zero();
+          if (active && fl) {
+            const uint64_t m = i + moff;
+            if (nfold == 2) {  // T_j[m] from T_{j-2}: two folds by ra, then one by rb
+              const T x0 = ld_cg(tq + m), x1 = ld_cg(tq + m + hm2);
+              const T y0 = ld_cg(tq + m + hm1), y1 = ld_cg(tq + m + hm1 + hm2);
+              const T u0 = F::add(x0, F::mul(ra, F::sub(x1, x0)));
+              const T u1 = F::add(y0, F::mul(ra, F::sub(y1, y0)));
+              v = F::add(u0, F::mul(rb, F::sub(u1, u0)));
+              tq[m] = v;
+            } else if (nfold == 1) {  // T_j[m] from T_{j-1} by ra
+              const T x0 = ld_cg(tq + m), x1 = ld_cg(tq + m + hm1);
+              v = F::add(x0, F::mul(ra, F::sub(x1, x0)));
+              tq[m] = v;
+            } else {
+              v = ld_cg(tq + m);
+            }
+          }
+          const T fa = shfl_elem<F>(v, gb), fb = shfl_elem<F>(v, gb + 1);
+          const T fc = shfl_elem<F>(v, gb + 2), fd = shfl_elem<F>(v, gb + 3);
+          const T xa = shfl_elem<F>(v, gb + xl), xb = shfl_elem<F>(v, gb + xl + 1);
+          const T xc = shfl_elem<F>(v, gb + xl + 2), xd = shfl_elem<F>(v, gb + xl + 3);
+          T pF, qF, pX, qX;
+          if (kind == 0) {
+            pF = fa; qF = fc; pX = xa; qX = xc;
+          } else if (kind == 1) {
+            pF = fb; qF = fd; pX = xb; qX = xd;
+          } else {
+            pF = F::sub(fb, fa); qF = F::sub(fd, fc); pX = F::sub(xb, xa); qX = F::sub(xd, xc);
+          }
+          const T u = sk == 0 ? pF : sk == 1 ? qF : F::sub(qF, pF);
+          const T w = sk == 0 ? pX : sk == 1 ? qX : F::sub(qX, pX);
+          const T prod = F::mul(u, w);
+          if (active && pl) acc = F::add(acc, prod);
+        }
+        W wv = R::from(acc);
+#pragma unroll
+        for (int off = 16; off >= Lq; off >>= 1) wv = R::add(wv, R::shfl_down(wv, off));
+        if (lane < NP) la_wsum[warp][lane] = wv;
+        __syncthreads();
+        if (warp == 0 && lane < NP) {
+          W t = la_wsum[0][lane];
+          for (int w2 = 1; w2 < nwarps; w2++) t = R::add(t, la_wsum[w2][lane]);
+          *cluster.map_shared_rank(&la_gather[rank][lane], 0) = t;
+        }
+        cluster.sync();
+        if (rank == 0 && warp == 0) {  // lane p: product p over the cluster, tagged words
+          const uint32_t seq = seq0 + (uint32_t)j + 1;
+          if (lane < NP) {
+            W t = la_gather[0][lane];
+            for (unsigned c2 = 1; c2 < C; c2++) t = R::add(t, la_gather[c2][lane]);
+#pragma unroll
+            for (int w = 0; w < R::NW; w++) s_words[lane * R::NW + w] = tag(R::word(t, w), seq);
+          }
+          __syncwarp();
+          constexpr int NWORDS = NP * R::NW;
+          for (int idx = 2 * lane; idx < NWORDS; idx += 64) {
+            if (idx + 1 < NWORDS)
+              st_tagged2(mb->ev + idx, s_words[idx], s_words[idx + 1]);
+            else
+              mb->ev[idx] = s_words[idx];
+          }
+        }
+      };
+      // the second challenge of a pair (ch2), read by CTA 0 and broadcast
+      auto fetch_second = [&](uint32_t seq) {
+        if (rank == 0 && warp == 0) {
+          const bool ok = warp_poll<NC>(mb->ch2, seq, s_cw2, &mb->abort);
+          if (lane == 0) {
+            if (!ok) {
+              *fail = 1;
+              mb->status = 1;
+            }
+            s_r2 = Words<F>::load(s_cw2);
+            s_flag = ok ? 0 : 2;
+          }
+          __syncwarp();
+          if (lane < (int)C) {
+            *cluster.map_shared_rank(&s_r2, lane) = s_r2;
+            *cluster.map_shared_rank(&s_flag, lane) = s_flag;
+          }
+        }
+        cluster.sync();
+      };
+      // rounds before jp (more quadruples than (L >> 17) cluster passes) run
+      // directly; the host derives the same jp
+      const uint64_t pp = (uint64_t)((L >> 17) & 127);
+      int j = 0;
+      while (j < j_end && (1ull << (num_vars - 2 - j)) * (uint64_t)Lq > nthreads * pp) j++;
+      if ((j_end - j) & 1) j++;  // whole pairs only: an odd one out runs directly
+      for (int jd = 0; jd < j; jd++) {
+        direct_round(jd);
+        fetch_challenge(seq0 + (uint32_t)jd + 1);
+        if (s_flag == 2) return;
+        r = s_r;
+      }
+      T ra = r, rb = F::zero();
+      int nfold = j > 0 ? 1 : 0;  // folds the tables lag behind (by ra, rb)
+      bool pending = false;       // after the loop: the last pair's folds
+      while (j < j_end) {
+        const bool tr0 = trace && rank == 0 && threadIdx.x == 0;
+        if (tr0) trace[j * 8 + 0] = globaltimer();
+        const bool paired = j + 1 < j_end;
+        la_pass(j, nfold, ra, rb);
+        if (tr0) trace[j * 8 + 3] = globaltimer();
+        fetch_challenge(seq0 + (uint32_t)j + 1);
+        if (s_flag == 2) return;
+        if (paired) {
+          fetch_second(seq0 + (uint32_t)j + 2);
+          if (s_flag == 2) return;
+          ra = s_r;
+          rb = s_r2;
+          nfold = 2;
+          pending = true;
+          j += 2;
+        } else {
+          r = s_r;
+          pending = false;
+          j += 1;
+        }
+        if (tr0) trace[(j - 1) * 8 + 4] = globaltimer();
+      }
+      if (pending) {
+        // the last pair's first fold: tables of round j_end - 1; the tail
+        // below folds them by r = r_{j_end - 1}
+        const uint64_t H = 1ull << (num_vars - j_end + 1);  // round j_end - 2's half
+        for (uint64_t idx = gtid; idx < (uint64_t)LA::NT * H; idx += nthreads) {
+          const int t = (int)(idx / H);
+          const uint64_t m = idx - (uint64_t)t * H;
+          T* tp = tab_of(t);
+          const T x = ld_cg(tp + m), y = ld_cg(tp + m + H);
+          tp[m] = F::add(x, F::mul(ra, F::sub(y, x)));
+        }
+        r = rb;
+        cluster.sync();
+      }
+      jl = j_end;
+    }
+  }
+  for (int j = jl; j < j_end; j++) {
+    direct_round(j);
+    const uint32_t seq = seq0 + (uint32_t)j + 1;
+    const bool tr0 = trace && rank == 0 && threadIdx.x == 0;
     fetch_challenge(seq);
     if (tr0) trace[j * 8 + 4] = globaltimer();
     if (s_flag == 2) return;
@@ -1242,6 +1472,7 @@ struct Plan {
   int cgrid, cblock; // cluster kernel shape (one cluster)
   int lanes;
   int j_end;         // cluster kernel stops after round j_end - 1 (host tail below n)
+  int la_np;         // paired rounds: product sums per pass (0 = one round per trip)
 };
 
 template <class F, int MAXK, class EV>
@@ -1294,7 +1525,13 @@ struct Persistent {
       const int v = e ? atoi(e) : 4;
       return v < 1 ? 1 : v > 64 ? 64 : v;
     }();
-    const int lp = pl.lanes | (passes << 8);
+    static const int pair_passes = [] {  // ZKL_PAIR_PASSES (run_phase reads the same)
+      const char* e = getenv("ZKL_PAIR_PASSES");
+      const int v = e ? atoi(e) : 1;
+      return v < 1 ? 1 : v > 127 ? 127 : v;
+    }();
+    const int lp = pl.lanes | (passes << 8) |
+                   (La<F, EV>::kOn && pl.la_np ? (1 << 16) | (pair_passes << 17) : 0);
     ZKL_CUDA(cudaLaunchKernelEx(&cfg, k_sumcheck_cluster<F, MAXK, EV>, tp, k, num_vars,
                                 pl.j_switch, pl.j_end, tm, mb, fail, seq0, trace, lp));
     ZKL_LAUNCH_CHECK();
@@ -1314,6 +1551,7 @@ struct Persistent {
     Plan pl;
     pl.lanes = lanes;
     pl.j_end = num_vars;
+    pl.la_np = 0;
     const uint64_t per_pair = lanes > 0 ? (uint64_t)lanes : 1;
     // cluster: up to 16 CTAs x 256 threads; lane mode loops when a round
     // has more pairs than lane groups (at most kClusterPasses passes)
@@ -1769,6 +2007,41 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
   a.host_done = false;
   if (h) pl.j_end = n - h;
   const int ndev = n - h;  // rounds the device runs (nrun when no tail)
+  // paired rounds (cluster kernel, PROD2 / SUM2PROD2 over Fr, every table in
+  // one term factor, a host tail after them; ZKL_PAIRED=0 turns them off):
+  // one pass publishes round j's and round j+1's sums (the latter as
+  // quadratics in r_j), and one round trip carries both challenges
+  static const bool paired_env = [] {
+    const char* e = getenv("ZKL_PAIRED");
+    return !(e && atoi(e) == 0);
+  }();
+  if (F::kId == Fr255::kId && paired_env && h > 0 && ndev >= 2 && pl.j_switch == 0 &&
+      !a.sharded && !a.replaying && (size_t)pl.cgrid * pl.cblock >= 64) {
+    const int f0 = tm.fi[0][0], f1 = tm.fi[0][1];
+    if (shape == kProd2 && k == 2 && f0 != f1) pl.la_np = 9;
+    if (shape == kSum2Prod2 && k == 3) {
+      const int f2 = tm.fi[1][1];
+      if (f0 != f1 && f0 != f2 && f1 != f2) pl.la_np = 18;
+    }
+  }
+  // the first paired round: the one whose pass fits ZKL_PAIR_PASSES (default
+  // 1) cluster passes (the kernel derives the same); earlier rounds direct
+  static const int pair_passes = [] {
+    const char* e = getenv("ZKL_PAIR_PASSES");
+    const int v = e ? atoi(e) : 1;
+    return v < 1 ? 1 : v > 127 ? 127 : v;
+  }();
+  int jp = 0;
+  if (pl.la_np) {
+    const uint64_t lq = pl.la_np == 9 ? 16 : 32;
+    const uint64_t nth = (uint64_t)pl.cgrid * pl.cblock;
+    while (jp < ndev && (1ull << (n - 2 - jp)) * lq > nth * (uint64_t)pair_passes) jp++;
+    if ((ndev - jp) & 1) jp++;  // whole pairs only (the kernel derives the same)
+    if (jp >= ndev - 1) pl.la_np = 0;  // nothing to pair
+  }
+  const int la_np = pl.la_np;
+  T la_sum[kMbMaxOut];  // a pair's product sums (storage form)
+  uint32_t la_cw[NC] = {};  // a pair's first challenge, held until the second is drawn
   void* ws;
   rc = scratch_reserve((size_t)pl.grid * kMbMaxOut * sizeof(W), &ws, s);
   if (rc) return rc;
@@ -1857,14 +2130,20 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
   if (tracing) h_first.resize(n);
   for (int j = 0; j < (h ? ndev : nrun); j++) {
     if (tracing) {  // first tagged word of this round visible
-      while ((uint32_t)(mb_host->ev[0] >> 32) != seq0 + j + 1 && !mb_host->status) {
+      const uint32_t tag = la_np && j > jp && (j - jp) % 2 ? seq0 + j : seq0 + j + 1;
+      while ((uint32_t)(mb_host->ev[0] >> 32) != tag && !mb_host->status) {
       }
       h_first[j] = now_us();
     }
-    rc = wait_words<F>(mb_host, mb_host->ev, nout * NW, seq0 + j + 1, words, s, "sums", j);
-    if (rc) {
-      g_phase_dirty = true;
-      return rc;
+    const bool la_round = la_np && j >= jp;
+    const bool la_first = la_round && (j - jp) % 2 == 0;  // first of a pair (or the last alone)
+    if (!la_round || la_first) {
+      rc = wait_words<F>(mb_host, mb_host->ev, (la_first ? la_np : nout) * NW, seq0 + j + 1,
+                         words, s, "sums", j);
+      if (rc) {
+        g_phase_dirty = true;
+        return rc;
+      }
     }
     if (tracing) h_seen[j] = now_us();
     if (!prepared) {
@@ -1889,7 +2168,26 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
       }
     }
     T raw[kMbMaxOut];
-    for (int q = 0; q < nout; q++) raw[q] = HostRed<F>::reduce(words + q * NW);
+    if (la_round) {
+      // product sums S[9b + 3 kind + term] (b: factor pair F.G / F.H; kind:
+      // lo, hi, difference of round j+1's pairs; term: pp, qq, dd)
+      if (la_first) {
+        for (int q = 0; q < la_np; q++) la_sum[q] = HostRed<F>::reduce(words + q * NW);
+        for (int b = 0; b < la_np / 9; b++)  // round j: (a, c) and (b, d) pairs
+          for (int t = 0; t < 3; t++) raw[3 * b + t] = H::add(la_sum[9 * b + t], la_sum[9 * b + 3 + t]);
+      } else {  // round j = (first) + 1 at r_{j-1}: pp + r (qq - pp - dd) + r^2 dd
+        const T rp = host::from_canon<F>(point_out + (size_t)(j - 1) * nb);
+        for (int b = 0; b < la_np / 9; b++)
+          for (int kd = 0; kd < 3; kd++) {
+            const T pp = la_sum[9 * b + 3 * kd], qq = la_sum[9 * b + 3 * kd + 1];
+            const T dd = la_sum[9 * b + 3 * kd + 2];
+            const T c1 = H::sub(H::sub(qq, pp), dd);
+            raw[3 * b + kd] = H::add(pp, H::mul(rp, H::add(c1, H::mul(rp, dd))));
+          }
+      }
+    } else {
+      for (int q = 0; q < nout; q++) raw[q] = HostRed<F>::reduce(words + q * NW);
+    }
     if (a.sharded) {
       // every rank's raw sums (storage form) through the shared-memory
       // all-gather; the host finishing below is linear in them
@@ -1982,7 +2280,16 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
     uint32_t cw[NC];
     memcpy(cw, &rm, nb);
     const uint64_t tg = (uint64_t)(seq0 + j + 1) << 32;
-    for (int w = 0; w < NC; w++) mb_host->ch[w] = tg | cw[w];
+    if (la_first && j + 1 < ndev) {
+      memcpy(la_cw, cw, sizeof(cw));  // sent with the pair's second challenge
+    } else if (la_round && !la_first) {
+      // the device reads ch (r_{j-1}) first, then ch2 (r_j): write ch2 first
+      for (int w = 0; w < NC; w++) mb_host->ch2[w] = tg | cw[w];
+      const uint64_t tg1 = (uint64_t)(seq0 + j) << 32;
+      for (int w = 0; w < NC; w++) mb_host->ch[w] = tg1 | la_cw[w];
+    } else {
+      for (int w = 0; w < NC; w++) mb_host->ch[w] = tg | cw[w];
+    }
     std::atomic_thread_fence(std::memory_order_seq_cst);  // drain the store buffer now
     if (tracing) h_sent[j] = now_us();
     if (pl.j_switch > 0 && j == pl.j_switch - 1 && pl.j_switch < n && nrun == n) {
@@ -2037,6 +2344,11 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
       acc[3] += t[4] ? (t[4] - (t[3] ? t[3] : t[2])) / 1e3 : 0;  // wait for challenge
       if (j + 1 < n && t[4]) loop += (tv[(size_t)(j + 1) * 8] - t[4]) / 1e3;
       hs += h_sent[j] - h_seen[j];
+      if (getenv("ZKL_TRACE")[0] == '4')  // lookahead rounds: eval+publish, passes, reduce, r wait
+        fprintf(stderr, "[zkl trace] la round %d: publish %.2f | passes %.2f | reduce %.2f | "
+                "coef->r %.2f | host seen->sent %.2f\n", j, ((double)t[3] - (double)t[0]) / 1e3,
+                ((double)t[1] - (double)t[0]) / 1e3, ((double)t[2] - (double)t[1]) / 1e3,
+                ((double)t[4] - (double)t[2]) / 1e3, h_sent[j] - h_seen[j]);
       if (getenv("ZKL_TRACE")[0] == '2')
         fprintf(stderr, "[zkl trace] round %d: accum %.2f reduce %.2f publish %.2f wait %.2f\n", j,
                 (t[1] - t[0]) / 1e3, (t[2] - t[1]) / 1e3, t[3] ? (t[3] - t[2]) / 1e3 : 0.0,
