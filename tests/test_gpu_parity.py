@@ -372,13 +372,17 @@ def test_zero_u_phase_shortcut_off_matches_golden():
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
 
 
-@pytest.mark.parametrize("tail", ["0", "1", "6"])
-def test_host_tail_rounds_match_golden(tail):
+@pytest.mark.parametrize("tail,paired", [("0", "1"), ("1", "1"), ("6", "1"), ("5", "0"),
+                                         ("5", "64"), ("3", "64")])
+def test_host_tail_rounds_match_golden(tail, paired):
     """The last ZKL_HOST_TAIL rounds of a phase run on the host (default 5;
     the cluster kernel sends the folded survivors through the mailbox).  With
     every round on the device (0), one host round (1) and six (6), the
     sumcheck and zkMat proofs are the reference's goldens, constant terms,
-    repeated factors and post_add rounds included."""
+    repeated factors and post_add rounds included.  `paired`: the cluster
+    kernel's paired rounds (PROD2 / SUM2PROD2, one round trip per two rounds)
+    on by default ("1"), off ("0"), or from round 0 on (ZKL_PAIR_PASSES=64:
+    multi-pass pair passes, the unfolded first pass and the double folds)."""
     code = (
         "import sys; sys.path[:0] = ['.', 'tests', 'tests/golden']\n"
         "import pytest, test_gpu_parity as T\n"
@@ -388,7 +392,12 @@ def test_host_tail_rounds_match_golden(tail):
         "    T.test_matmul_sumcheck_golden(mode, 'native')\n"
         "T.test_matmul_batch_matches_per_claim('big')\n"
         "print('ok')\n")
-    r = _run_isolated(code, ZKL_HOST_TAIL=tail)
+    env = {"ZKL_HOST_TAIL": tail}
+    if paired == "0":
+        env["ZKL_PAIRED"] = "0"
+    elif paired != "1":
+        env["ZKL_PAIR_PASSES"] = paired
+    r = _run_isolated(code, **env)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
 
 
