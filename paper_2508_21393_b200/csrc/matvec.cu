@@ -754,7 +754,13 @@ __global__ void __launch_bounds__(256, (R == 2 ? 3 : 2))
 // 16-byte skew per plane (conflict-free B-fragment loads); the integer pipe
 // then only assembles fragments: the IMAD-bound MAC loop becomes a load
 // stream.
-constexpr int kTcK = 256;  // columns per chunk: 8 k-steps, all loads issued up front
+#ifndef ZKL_TCK
+#define ZKL_TCK 256
+#endif
+#ifndef ZKL_TCK_MINB
+#define ZKL_TCK_MINB 1
+#endif
+constexpr int kTcK = ZKL_TCK;  // columns per chunk: kTcK / 32 k-steps, all loads issued up front
 
 ZKL_D void mma_u8(uint32_t (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -764,7 +770,7 @@ ZKL_D void mma_u8(uint32_t (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, ZKL_TCK_MINB)
     k_mvt_rows(const int16_t* M, uint64_t rows, uint64_t cols, const fr_t* x,
                uint64_t* acc_out) {
   // plane stride: a 32-byte skew keeps the per-half-warp 8-byte B loads
