@@ -1200,7 +1200,11 @@ def main():
                          "us_per_round": per_round_us,
                          "gpu_ms_per_step": ph_ms / args.steps,
                          "share_of_step": (ph_ms / args.steps) / profiled_ms_per_step,
-                         "achieved_gbs": (ph_bytes / (ph_ms / 1000.0) / 1e9) if ph_ms else 0.0},
+                         "achieved_gbs": (ph_bytes / (ph_ms / 1000.0) / 1e9) if ph_ms else 0.0,
+                         "note": "W and V phases: the last <= 5 rounds on the host (host tail, "
+                                 "outside the phase's kernel time); the device rounds pair up, two "
+                                 "per PCIe round trip, once a pair's pass fits the cluster "
+                                 "(DESIGN.md sec. 4a); us_per_round = kernel time / all rounds"},
         "eq_tables": {"launches_per_step": eq_n // args.steps, "gpu_ms_per_step": eq_ms / args.steps},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
