@@ -1114,19 +1114,19 @@ constexpr int kClusterThreads = 256;
 
 
 // ---------------------------------------------------------------------------
-// Lookahead rounds (cluster kernel, PROD2 / SUM2PROD2 over Fr).  Round j+1's
-// raw sums are quadratics in the challenge r_j: with T the tables folded by
+// Paired rounds (cluster kernel, PROD2 / SUM2PROD2 over Fr).  Round j+1's raw
+// sums are quadratics in the challenge r_j: with T the tables folded by
 // r_0 .. r_{j-1}, h = half of round j, h' = h / 2 and the round-(j+1) pair i
 // built from the quadruple a = T[i], b = T[i + h'], c = T[i + h], d =
 // T[i + h + h'], its lo / hi / difference entries are p + r (q - p) for
 // (p, q) = (a, c), (b, d), (b - a, d - c), and each product sum is
 //   sum (p_F + r dF)(p_X + r dX) = S_pp + r (S_qq - S_pp - S_dd) + r^2 S_dd
 // with S_pp = sum p_F p_X, S_qq = sum q_F q_X, S_dd = sum (q - p)_F (q - p)_X.
-// So while the host answers round j the cluster folds T by r_{j-1} and forms
-// those 3 sums per raw output; once r_j arrives CTA 0 only evaluates the
-// quadratics (two products) and publishes round j+1.  The per-pair work
-// (folds, products, cluster reduction) leaves the round trip's critical path.
-// The raw sums are the same field values the direct evaluators publish.
+// Round j's own raw sums are S_pp + S_qq over the lo and hi kinds (its pairs
+// are (a, c) and (b, d)).  So one pass publishes the 3 sums per raw output
+// (9 or 18 wide values); the host evaluates round j, draws r_j, evaluates
+// round j+1 at r_j, draws r_{j+1} and answers both (ch, ch2); the next pass
+// first folds the tables twice.  One PCIe round trip per two rounds.
 template <class F, class EV>
 struct La {
   static constexpr bool kOn = false;
@@ -2344,7 +2344,7 @@ int run_phase(PhaseArgs<F>& a, HostTranscript& tr, uint8_t* rounds_out, uint8_t*
       acc[3] += t[4] ? (t[4] - (t[3] ? t[3] : t[2])) / 1e3 : 0;  // wait for challenge
       if (j + 1 < n && t[4]) loop += (tv[(size_t)(j + 1) * 8] - t[4]) / 1e3;
       hs += h_sent[j] - h_seen[j];
-      if (getenv("ZKL_TRACE")[0] == '4')  // lookahead rounds: eval+publish, passes, reduce, r wait
+      if (getenv("ZKL_TRACE")[0] == '4')  // raw stamps t0..t4 relative (paired-round debugging)
         fprintf(stderr, "[zkl trace] la round %d: publish %.2f | passes %.2f | reduce %.2f | "
                 "coef->r %.2f | host seen->sent %.2f\n", j, ((double)t[3] - (double)t[0]) / 1e3,
                 ((double)t[1] - (double)t[0]) / 1e3, ((double)t[2] - (double)t[1]) / 1e3,
