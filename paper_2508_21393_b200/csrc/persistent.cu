@@ -846,6 +846,36 @@ ZKL_D bool warp_poll(const volatile uint64_t* src, uint32_t seq, uint32_t* out,
   }
 }
 
+// both challenges of a paired round in one PCIe read round trip: lanes
+// [0, NW/2) poll ch (tag seq), lanes [NW/2, NW) poll ch2 (tag seq + 1)
+template <int NW>
+ZKL_D bool warp_poll2(const volatile uint64_t* ch, const volatile uint64_t* ch2, uint32_t seq,
+                      uint32_t* out, uint32_t* out2, const volatile uint32_t* abort_flag) {
+  const int lane = threadIdx.x & 31;
+  const bool first = lane < NW / 2;
+  const int l2 = first ? lane : lane - NW / 2;
+  const uint32_t want = first ? seq : seq + 1;
+  const uint64_t t0 = globaltimer();
+  for (uint32_t spin = 1;; spin++) {
+    uint64_t a = (uint64_t)want << 32, b = a;
+    if (lane < NW) ld_tagged2((first ? ch : ch2) + 2 * l2, a, b);
+    const bool mine = (uint32_t)(a >> 32) == want && (uint32_t)(b >> 32) == want;
+    if (__all_sync(kFull, mine)) {
+      if (lane < NW) {
+        uint32_t* o = first ? out : out2;
+        o[2 * l2] = (uint32_t)a;
+        o[2 * l2 + 1] = (uint32_t)b;
+      }
+      __syncwarp();
+      return true;
+    }
+    if ((spin & 63) == 0) {
+      int bad = lane == 0 && ((abort_flag && *abort_flag) || globaltimer() - t0 > kSpinTimeoutNs);
+      if (__shfl_sync(kFull, bad, 0)) return false;
+    }
+  }
+}
+
 template <class F>
 struct Words {
   static constexpr int N = F::kBytes / 4;  // 8 (Fr) or 2 (M61)
@@ -1350,19 +1380,23 @@ __global__ void __launch_bounds__(kClusterThreads)
         }
       };
       // the second challenge of a pair (ch2), read by CTA 0 and broadcast
-      auto fetch_second = [&](uint32_t seq) {
+      // a pair's two challenges (ch: r_j under tag seq, ch2: r_{j+1} under
+      // seq + 1) in one poll, broadcast to every CTA
+      auto fetch_pair = [&](uint32_t seq) {
         if (rank == 0 && warp == 0) {
-          const bool ok = warp_poll<NC>(mb->ch2, seq, s_cw2, &mb->abort);
+          const bool ok = warp_poll2<NC>(mb->ch, mb->ch2, seq, s_cw, s_cw2, &mb->abort);
           if (lane == 0) {
             if (!ok) {
               *fail = 1;
               mb->status = 1;
             }
+            s_r = Words<F>::load(s_cw);
             s_r2 = Words<F>::load(s_cw2);
             s_flag = ok ? 0 : 2;
           }
           __syncwarp();
           if (lane < (int)C) {
+            *cluster.map_shared_rank(&s_r, lane) = s_r;
             *cluster.map_shared_rank(&s_r2, lane) = s_r2;
             *cluster.map_shared_rank(&s_flag, lane) = s_flag;
           }
@@ -1390,11 +1424,12 @@ __global__ void __launch_bounds__(kClusterThreads)
         const bool paired = j + 1 < j_end;
         la_pass(j, nfold, ra, rb);
         if (tr0) trace[j * 8 + 3] = globaltimer();
-        fetch_challenge(seq0 + (uint32_t)j + 1);
+        if (paired)
+          fetch_pair(seq0 + (uint32_t)j + 1);
+        else
+          fetch_challenge(seq0 + (uint32_t)j + 1);
         if (s_flag == 2) return;
         if (paired) {
-          fetch_second(seq0 + (uint32_t)j + 2);
-          if (s_flag == 2) return;
           ra = s_r;
           rb = s_r2;
           nfold = 2;
@@ -1408,18 +1443,24 @@ __global__ void __launch_bounds__(kClusterThreads)
         if (tr0) trace[(j - 1) * 8 + 4] = globaltimer();
       }
       if (pending) {
-        // the last pair's first fold: tables of round j_end - 1; the tail
-        // below folds them by r = r_{j_end - 1}
-        const uint64_t H = 1ull << (num_vars - j_end + 1);  // round j_end - 2's half
-        for (uint64_t idx = gtid; idx < (uint64_t)LA::NT * H; idx += nthreads) {
-          const int t = (int)(idx / H);
-          const uint64_t m = idx - (uint64_t)t * H;
-          T* tp = tab_of(t);
-          const T x = ld_cg(tp + m), y = ld_cg(tp + m + H);
-          tp[m] = F::add(x, F::mul(ra, F::sub(y, x)));
+        // the last pair's two folds fused into the host tail's mail: survivor
+        // i of table q from the four entries i, i + hb, i + ha, i + ha + hb of
+        // the round-(j_end - 2) table (ha, hb: rounds j_end - 2, j_end - 1 halves)
+        const uint64_t hb = 1ull << (num_vars - j_end), ha = 2 * hb;
+        const uint32_t fseq = seq0 + (uint32_t)num_vars + 1;
+        for (uint64_t idx = gtid; idx < (uint64_t)k * hb; idx += nthreads) {
+          const int q = (int)(idx / hb);
+          const uint64_t i = idx - (uint64_t)q * hb;
+          const T* t = tabs.t[q];
+          const T x0 = ld_cg(t + i), x1 = ld_cg(t + i + ha);
+          const T y0 = ld_cg(t + i + hb), y1 = ld_cg(t + i + hb + ha);
+          const T u0 = F::add(x0, F::mul(ra, F::sub(x1, x0)));
+          const T u1 = F::add(y0, F::mul(ra, F::sub(y1, y0)));
+          const T f = F::add(u0, F::mul(rb, F::sub(u1, u0)));
+#pragma unroll
+          for (int w = 0; w < NC; w++) mb->tail[idx * NC + w] = tag(Words<F>::word(f, w), fseq);
         }
-        r = rb;
-        cluster.sync();
+        return;
       }
       jl = j_end;
     }
