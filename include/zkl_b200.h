@@ -118,7 +118,9 @@ int zkl_sumcheck_round(int field, void* const* tables, int k, uint64_t size, int
  * (degree+1) evaluations appended under b"sumcheck/eval" (minimal LE ints),
  * challenge b"sumcheck/round".  post_add_canon: num_vars scalars (one per
  * round) or NULL; post_mul_canon: NULL = 1.  Outputs (canonical LE):
- * rounds_out num_vars*(degree+1) scalars, point_out num_vars, finals_out k. */
+ * rounds_out num_vars*(degree+1) scalars, point_out num_vars, finals_out k.
+ * The tables are consumed: the last rounds of a claim may run on the host
+ * (ZKL_HOST_TAIL), so their device contents afterwards are unspecified. */
 int zkl_sumcheck_prove(int field, void* const* tables, int k, int num_vars, int degree,
                        int nterms, const int32_t* nfactors, const int32_t* factors,
                        const uint8_t* coeffs_canon, const uint8_t* post_add_canon,
